@@ -1,0 +1,30 @@
+# Top-level build: the sm_100a product library and the oracle (test infra).
+#   make            -> paper_2603_19371_b200/libwarplm_b200.so + oracle/*.so
+# nvcc cross-compiles for sm_100a without a GPU.
+NVCC    ?= nvcc
+ARCH    := -gencode arch=compute_100a,code=sm_100a
+NVFLAGS ?= -O3 -std=c++17 -lineinfo -Xcompiler -fPIC -Xptxas -warn-spills
+PKG     := paper_2603_19371_b200
+CSRC    := $(PKG)/csrc
+SRCS    := $(CSRC)/kernels.cu $(CSRC)/engine.cu $(CSRC)/ops.cu $(CSRC)/synth.cu
+HDRS    := include/wlm.h $(CSRC)/common.cuh $(CSRC)/kernels.cuh $(CSRC)/internal.cuh
+OBJS    := $(patsubst $(CSRC)/%.cu,build/%.o,$(SRCS))
+LIB     := $(PKG)/libwarplm_b200.so
+
+all: $(LIB) oracle
+
+build/%.o: $(CSRC)/%.cu $(HDRS)
+	@mkdir -p build
+	$(NVCC) $(ARCH) $(NVFLAGS) -Iinclude -c $< -o $@
+
+$(LIB): $(OBJS)
+	$(NVCC) $(ARCH) -shared -o $@ $(OBJS)
+
+oracle:
+	$(MAKE) -C oracle
+
+clean:
+	rm -rf build $(LIB)
+	$(MAKE) -C oracle clean
+
+.PHONY: all oracle clean

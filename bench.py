@@ -1,0 +1,408 @@
+"""Benchmark of the factored-LM iteration (BASELINE.json config 4).
+
+Workload: a batch of independent 192^3 synthetic pairs per GPU (config 4:
+64 pairs over 8 B200 -> 8 pairs per GPU; weak scaling: per-GPU work fixed),
+LNCC + LM, rejection off.  One step = one lm_iterate attempt for every pair
+on the GPU (K2 gradient, K3 LM step + smoothing + max, K4 compositive
+resample + smoothing, K1 warp + LNCC + device-side damping).  Inputs
+(~3.9 GB per GPU) are larger than L2, so no flush is needed.
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+
+Multi-GPU: launched by torchrun, one rank per GPU; no data-path collective
+(pairs are independent); timing = max over ranks (NCCL all-reduce of the
+per-rank CUDA-event time).  Prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = json.load(open(os.path.join(ROOT, "BASELINE.json")))["metric"]
+# Canonical algorithmic HBM bytes per voxel per kernel:
+#   K1 eval  : u 12 + F 4 + M 4 (gather) + write A,B,E 12          = 32
+#   K2 grad  : A,B,E 12 + F 4 + u 12 + M 4 + write g 12            = 44
+#   K3 step  : g 12 + write dU_s 12                                = 24
+#   K4 comp. : dU_s 12 + u 12 (gather) + write u' 12               = 36
+KERNEL_BYTES = {"K1_lncc_fwd": 32, "K2_lncc_bwd": 44, "K3_step_smooth": 24, "K4_compose_smooth": 36}
+STAGE_ID = {"K1_lncc_fwd": 0, "K2_lncc_bwd": 1, "K3_step_smooth": 2, "K4_compose_smooth": 3}
+BYTES_PER_VOXEL_ITER = sum(KERNEL_BYTES.values())  # 136
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        self.out = ""
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.out, _ = self.proc.communicate(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        rows = [r.split(",") for r in (self.out or "").strip().splitlines() if r.count(",") >= 8]
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(r[1]) for r in rows]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if "Active" in r[5 + i]})
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": float(rows[0][2]),
+                "reasons": reasons, "samples": len(rows)}
+
+
+def dist_init(n_gpus):
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return rank, world, local
+
+
+def max_over_ranks(x, world, local):
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{local}")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(world, local):
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        dist.barrier(device_ids=[local])
+
+
+# ------------------------------------------------------------------ ours ----
+def run_ours(args, rank, world, local):
+    import ctypes as C
+
+    import numpy as np
+    import torch
+
+    import paper_2603_19371_b200 as P
+    from paper_2603_19371_b200._lib import Dims, SynthSpec
+
+    torch.cuda.set_device(local)
+    n = args.size
+    shape = (n, n, n)
+    nvox = n ** 3
+    pairs = args.pairs_per_gpu
+    ctx = P.Context(local)
+    lib = P.load()
+    cfg = P.reg_config(nlevels=1, factors=[1], iters=[100])
+    eng = P.Engine(shape, pairs=pairs, cfg=cfg, ctx=ctx)
+
+    # synthetic pairs (config 4 seeds 1000..1063), generated on the GPU by the
+    # product's own synth_pair into pinned host memory (the e2e inputs)
+    F_h = torch.empty((pairs,) + shape, dtype=torch.float32, pin_memory=True)
+    M_h = torch.empty((pairs,) + shape, dtype=torch.float32, pin_memory=True)
+    for p in range(pairs):
+        seed = 1000 + rank * pairs + p
+        spec = SynthSpec(Dims(n, n, n), 12, 0.0, 6.0, 0.01, seed)
+        ctx.check(lib.wlm_synth_pair(ctx.h, C.byref(spec), F_h[p].data_ptr(), M_h[p].data_ptr(),
+                                     None, 0))
+    stream = torch.cuda.ExternalStream(ctx.stream(), device=f"cuda:{local}")
+
+    eng.load(F_h, M_h)
+    eng.set_warp(None)
+    eng.begin_level(0)
+    launches0 = ctx.launches
+    for _ in range(args.warmup):
+        eng.step()
+    ctx.synchronize()
+
+    # ---- device-resident throughput (value) ----
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    barrier(world, local)
+    torch.cuda.synchronize()
+    launches_before = ctx.launches
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            eng.step()
+        ev1.record(stream)
+        ev1.synchronize()
+    torch.cuda.synchronize()
+    barrier(world, local)
+    launches_timed = ctx.launches - launches_before
+    ms = ev0.elapsed_time(ev1)
+    ms_max = max_over_ranks(ms, world, local)
+    st = eng.state(0)
+    assert math.isfinite(st["r"]), st
+
+    # ---- per-kernel durations (same stream, CUDA events around each launch) ----
+    per_kernel = {}
+    reps = max(3, min(10, args.steps))
+    for name, sid in STAGE_ID.items():
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+               for _ in range(reps)]
+        # keep the engine state coherent: run whole attempts, time one stage
+        for a, b in evs:
+            for other in (1, 2, 3, 0):
+                if other == sid:
+                    a.record(stream)
+                    ctx.check(lib.wlm_engine_stage(eng.h, other))
+                    b.record(stream)
+                else:
+                    ctx.check(lib.wlm_engine_stage(eng.h, other))
+        torch.cuda.synchronize()
+        per_kernel[name] = statistics.median(a.elapsed_time(b) for a, b in evs)
+    hbm, peak_kind = peaks()
+    dom = max(per_kernel, key=per_kernel.get)
+    launch_vox = pairs * nvox
+    achieved = KERNEL_BYTES[dom] * launch_vox / (per_kernel[dom] * 1e-3) / 1e9
+
+    # ---- end to end through the C-ABI with host buffers (e2e) ----
+    # per step: pinned host F, M -> device (wlm_engine_load), 100 LM
+    # iterations (wlm_engine_iterate), accepted warps -> pinned host
+    # (wlm_engine_get_warp).  Metric = voxel-iterations / time.
+    e2e_iters = args.e2e_iters
+    U_h = torch.empty((pairs, 3) + shape, dtype=torch.float32, pin_memory=True)
+
+    def e2e_once():
+        eng.load(F_h, M_h)
+        eng.set_warp(None)
+        eng.begin_level(0)
+        eng.iterate(e2e_iters)
+        ctx.check(lib.wlm_engine_get_warp(eng.h, U_h.data_ptr(), 1))
+
+    e2e_once()  # warm (graph already built)
+    e2e_steps = max(1, min(3, args.steps))
+    barrier(world, local)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        e2e_once()
+    torch.cuda.synchronize()
+    e2e_s = time.perf_counter() - t0
+    e2e_s = max_over_ranks(e2e_s, world, local)
+    e2e_val = world * pairs * nvox * e2e_iters * e2e_steps / e2e_s / 1e9
+    assert np.isfinite(U_h[0, :, ::17, ::17, ::17].numpy()).all()
+
+    value = world * pairs * nvox * args.steps / (ms_max * 1e-3) / 1e9  # Gvoxel/s
+    iters_per_s = world * pairs * args.steps / (ms_max * 1e-3)
+    it_frac = BYTES_PER_VOXEL_ITER * value * 1e9 / (hbm * 1e9)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline_sample(F_h[0].numpy(), M_h[0].numpy())
+
+    line = {
+        "metric": METRIC,
+        "value": round(value, 4),
+        "unit": "Gvoxel/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(ms_max / args.steps, 5),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f32",
+        "data": "synthetic (GPU synth_pair: Gaussian blobs + smoothed random warp, noise 0.01)",
+        "config": {"workload": f"config 4: batch of independent {n}^3 pairs, LNCC r=2 + pointwise LM, "
+                               f"rejection off, {pairs} pairs per GPU",
+                   "global_batch": world * pairs, "volume": list(shape), "pairs_per_gpu": pairs,
+                   "parallelism": f"dp{world} (independent pairs, no collective)",
+                   "l2": "inputs > L2 (68 B/voxel x %d voxels per GPU)" % (pairs * nvox)},
+        "iters_per_s": round(iters_per_s, 2),
+        "iters_per_s_per_pair": round(args.steps / (ms_max * 1e-3), 2),
+        "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1),
+                     "peak": hbm, "peak_kind": peak_kind, "unit": "GB/s",
+                     "frac": round(achieved / hbm, 4), "traffic": None,
+                     "algorithmic_bytes_per_voxel": KERNEL_BYTES[dom],
+                     "per_kernel_ms": {k: round(v, 4) for k, v in per_kernel.items()},
+                     "iteration_frac": round(it_frac, 4),
+                     "iteration_bytes_per_voxel": BYTES_PER_VOXEL_ITER},
+        "e2e": {"value": round(e2e_val, 4), "unit": "Gvoxel/s",
+                "h2d_bytes_per_step": 2 * pairs * nvox * 4,
+                "d2h_bytes_per_step": 3 * pairs * nvox * 4,
+                "iters_per_step": e2e_iters,
+                "path": "wlm_engine_load(host) + wlm_engine_iterate + wlm_engine_get_warp(host)"},
+        "gpu_launches": int(launches_timed),
+        "clocks": clk.summary(),
+    }
+    if cpu:
+        line["cpu_baseline"] = cpu
+    traffic = load_traffic(dom)
+    if traffic:
+        line["roofline"]["traffic"] = traffic
+    eng.close()
+    return line
+
+
+def load_traffic(kernel):
+    """DRAM bytes per launch from the committed ncu --set full summary."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(p):
+        try:
+            return json.load(open(p)).get(kernel)
+        except Exception:
+            return None
+    return None
+
+
+def cpu_baseline_sample(F, M):
+    """Reference CPU path (reference field.cpp primitives + restated LNCC/LM),
+    single thread, one LM iteration of one 192^3 pair of the same workload."""
+    import numpy as np
+
+    import oracle as O
+    kind = "reference" if O.have_ref() else "port"
+    L = O.lib(kind)
+    L.orc_set_threads(1)
+    cfg = O.default_config(nlevels=1, factors=[1], iters=[1])
+    n = F.size
+    t0 = time.perf_counter()
+    rc, _, _, _ = O.lm_run_level(F, M, np.zeros(F.shape + (3,)), cfg, 1, kind=kind)
+    dt = time.perf_counter() - t0
+    L.orc_set_threads(min(8, os.cpu_count() or 1))
+    # lm_run_level(1) = initial residual + 1 attempt (2 residual evaluations);
+    # count it as 1 iteration (conservative for the CPU)
+    return {"value": round(n / dt / 1e9, 6), "unit": "Gvoxel/s", "cores": 1, "kind": kind,
+            "sample": f"1 LM iteration (incl. initial residual) of pair 0 at {F.shape[0]}^3, "
+                      f"{dt:.1f} s, single thread (the reference is serial)"}
+
+
+# ------------------------------------------------------------- reference ----
+def run_reference(args, rank, world):
+    """The reference CPU implementation on the box's host cores: reference
+    field.cpp primitives (oracle/_ref) + the restated spec-only modules, one
+    single-threaded registration per core, pairs in parallel."""
+    import numpy as np
+
+    import oracle as O
+    kind = "reference" if O.have_ref() else "port"
+    L = O.lib(kind)
+    L.orc_set_threads(1)
+    n = args.size
+    shape = (n, n, n)
+    nvox = n ** 3
+    cores = os.cpu_count() or 1
+    pairs = min(args.pairs_per_gpu, cores)
+    data = []
+    for p in range(pairs):
+        F, M, _ = O.synth_pair(shape, 1000 + p, num_blobs=12, warp_max=6.0)
+        data.append((F, M))
+    cfg = O.default_config(nlevels=1, factors=[1], iters=[1])
+    u0 = np.zeros(shape + (3,))
+
+    def one_step():
+        th = []
+        for F, M in data:
+            t = threading.Thread(target=O.lm_run_level, args=(F, M, u0, cfg, 1), kwargs={"kind": kind})
+            t.start()
+            th.append(t)
+        for t in th:
+            t.join()
+
+    budget = args.ref_budget_s
+    t_start = time.perf_counter()
+    for _ in range(min(args.warmup, 1)):
+        one_step()
+    done = 0
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        one_step()
+        done += 1
+        if time.perf_counter() - t_start > budget:
+            break
+    dt = time.perf_counter() - t0
+    value = pairs * nvox * done / dt / 1e9
+    return {
+        "metric": METRIC, "value": round(value, 6), "unit": "Gvoxel/s", "n_gpus": world,
+        "steps": args.steps, "steps_timed": done, "warmup": args.warmup,
+        "ms_per_step": round(dt * 1e3 / max(done, 1), 1), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "impl": "reference",
+        "data": "synthetic (oracle synth_pair, seeds 1000+)",
+        "config": {"workload": f"config 4: batch of independent {n}^3 pairs, LNCC r=2 + pointwise LM, "
+                               f"rejection off; CPU sample {pairs} pairs in parallel",
+                   "global_batch": pairs, "volume": list(shape)},
+        "cpu_baseline": {"value": round(value, 6), "unit": "Gvoxel/s", "cores": pairs, "kind": kind,
+                         "sample": f"{done} steps x 1 LM iteration (incl. initial residual) on {pairs} "
+                                   f"pairs of {n}^3, one thread per pair"},
+        "e2e": {"value": round(value, 6), "unit": "Gvoxel/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--size", type=int, default=192)
+    ap.add_argument("--pairs-per-gpu", type=int, default=8)
+    ap.add_argument("--e2e-iters", type=int, default=100)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ref-budget-s", type=float, default=200.0)
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        args.warmup = 3  # timing rule: >= 3 warm-up steps
+
+    if args.impl == "reference":
+        rank = int(os.environ.get("RANK", 0))
+        world = int(os.environ.get("WORLD_SIZE", 1))
+        if rank != 0:
+            return
+        print(json.dumps(run_reference(args, rank, world)), flush=True)
+        return
+
+    rank, world, local = dist_init(args.gpus)
+    line = run_ours(args, rank, world, local)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

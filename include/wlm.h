@@ -1,0 +1,229 @@
+/*
+ * wlm.h -- C-ABI of the B200-native factored-LM registration hot path.
+ *
+ * This is the drop-in boundary.  It replaces, for the per-iteration path of
+ * the reference `warplm` library (/root/reference, C++20, namespace warplm):
+ *
+ *   reference interface (file:line)                      replaced by
+ *   --------------------------------------------------   ------------------------------
+ *   field.hpp:82   sample_trilinear                      wlm_warp_volume (whole volume)
+ *   field.hpp:90   sample_trilinear_grad                 wlm_warp_volume (+ gradient)
+ *   field.hpp:93   sample_field                          wlm_sample_field_points
+ *   field.hpp:96   compose_warp                          wlm_compose_warp
+ *   field.hpp:99   max_abs_component                     wlm_max_abs_component
+ *   field.hpp:104  normalize_step                        wlm_normalize_step
+ *   field.hpp:108  jacobian_det_min                      wlm_jacobian_det_min
+ *   field.hpp:113  gaussian_smooth(Volume3)              wlm_gaussian_smooth_vol
+ *   field.hpp:114  gaussian_smooth(DispField3)           wlm_gaussian_smooth_field
+ *   field.hpp:116-117 all_finite                         wlm_all_finite
+ *   SPEC.md:136    residual_lncc -> ResidualReport       wlm_residual_lncc
+ *   SPEC.md:247    lm_step_pointwise                     wlm_lm_step_pointwise
+ *   SPEC.md:265    update_damping                        wlm_update_damping
+ *   SPEC.md:274    rejection_test                        wlm_rejection_test
+ *   SPEC.md:283    lm_iterate                            wlm_engine_* (device-resident)
+ *   SPEC.md:292    adam_step                             wlm_engine_* (optimizer = ADAM)
+ *   SPEC.md:188    downsample                            wlm_downsample
+ *   SPEC.md:197    upsample_warp                         wlm_upsample_warp
+ *   SPEC.md:362    register -> RegResult                 wlm_register
+ *   SPEC.md:310    state_bytes                           wlm_state_bytes
+ *
+ * Host-buffer entry points take the reference's own layout: fp64, x-fastest
+ * (field.hpp:25-30), displacement fields component-innermost AoS
+ * (field.hpp:50-58).  They upload, run on the GPU and download, like a
+ * by-value reference call.  Device entry points (wlm_dev_*) take fp32
+ * structure-of-arrays device pointers (one plane per component) and run on
+ * the context's stream with no host synchronisation.
+ *
+ * Errors never cross the ABI as exceptions: every call returns wlm_status
+ * and wlm_last_error(ctx) describes the last failure.  The reference's
+ * std::invalid_argument maps to WLM_INVALID_ARG / WLM_DIM_MISMATCH, its
+ * non-finite abort to WLM_NONFINITE.  There is no CPU
+ * fallback: a missing device is WLM_CUDA.
+ *
+ * Threading: a context owns one CUDA stream and its
+ * scratch; do not share a context between host threads without locking.
+ * Distinct contexts run concurrently.
+ */
+#ifndef WLM_H
+#define WLM_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    WLM_OK = 0,
+    WLM_INVALID_ARG = 1,
+    WLM_DIM_MISMATCH = 2,
+    WLM_NONFINITE = 3,
+    WLM_OOM = 4,
+    WLM_CUDA = 5,
+    WLM_UNSUPPORTED = 6
+} wlm_status;
+
+typedef struct { int nx, ny, nz; } wlm_dims;
+
+/* LmConfig. lambda_max <= 0 or inf: uncapped. */
+typedef struct {
+    double lambda0, mu_plus, mu_minus;
+    int tile_size;   /* 1 only (tiled LM is UNSUPPORTED) */
+    int rejection;
+    double tau, lambda_max;
+    int max_retries;
+} wlm_lm_config;
+
+/* LmState. */
+typedef struct {
+    double lambda;
+    int hist_n;
+    double L1, L2;
+} wlm_lm_state;
+
+typedef struct { double beta1, beta2, eps_hat, lr; } wlm_adam_config;
+
+enum { WLM_OPT_LM = 0, WLM_OPT_ADAM = 1, WLM_OPT_GD = 2 };
+#define WLM_MAX_LEVELS 8
+
+/* RegConfig + MetricConfig + StepScale. */
+typedef struct {
+    int lncc_radius;
+    int optimizer;
+    wlm_lm_config lm;
+    wlm_adam_config adam;
+    double gd_lr;
+    int nlevels;
+    int factors[WLM_MAX_LEVELS];
+    int iters[WLM_MAX_LEVELS];
+    double target_max_disp, step_floor;
+    double sigma_update, sigma_warp;
+    int log_jacobian;
+} wlm_reg_config;
+
+/* RegResult.loss_trace row (CSV columns SPEC.md:427). */
+typedef struct {
+    int level, iter;
+    double loss_raw, r, lambda, eps;
+    int accepted, retries;
+    double jac_det_min;
+} wlm_step_log;
+
+typedef struct wlm_ctx wlm_ctx;
+typedef struct wlm_engine wlm_engine;
+
+/* ---- context ---- */
+wlm_status wlm_ctx_create(int device, wlm_ctx** out);
+void wlm_ctx_destroy(wlm_ctx* ctx);
+const char* wlm_last_error(const wlm_ctx* ctx);
+/* The context's stream (cudaStream_t as void*); device calls run on it. */
+void* wlm_ctx_stream(wlm_ctx* ctx);
+/* Use an external stream (e.g. torch's current stream) instead. */
+wlm_status wlm_ctx_set_stream(wlm_ctx* ctx, void* stream);
+wlm_status wlm_ctx_synchronize(wlm_ctx* ctx);
+/* Number of this library's kernels launched on ctx since creation. */
+uint64_t wlm_ctx_launch_count(const wlm_ctx* ctx);
+void wlm_default_reg_config(wlm_reg_config* cfg);
+/* Library build id string (arch, version). */
+const char* wlm_version(void);
+
+/* ---- host-buffer mirror of the reference field module (fp64, AoS) ---- */
+wlm_status wlm_warp_volume(wlm_ctx* ctx, const double* M, const double* u, wlm_dims d,
+                           double* Mw, double* gradM /* nullable */);
+wlm_status wlm_sample_field_points(wlm_ctx* ctx, const double* u, wlm_dims d,
+                                   const double* pts /* 3*npts */, size_t npts,
+                                   double* out /* 3*npts */);
+wlm_status wlm_compose_warp(wlm_ctx* ctx, const double* u, wlm_dims du, const double* v,
+                            wlm_dims dv, double eps, double* out);
+wlm_status wlm_max_abs_component(wlm_ctx* ctx, const double* v, wlm_dims d, double* out);
+wlm_status wlm_normalize_step(wlm_ctx* ctx, const double* v, wlm_dims d, double target,
+                              double floor_, double* eps);
+wlm_status wlm_jacobian_det_min(wlm_ctx* ctx, const double* u, wlm_dims d, double* out);
+wlm_status wlm_gaussian_smooth_vol(wlm_ctx* ctx, const double* in, wlm_dims d, double sigma,
+                                   double* out);
+wlm_status wlm_gaussian_smooth_field(wlm_ctx* ctx, const double* in, wlm_dims d,
+                                     double sigma, double* out);
+wlm_status wlm_all_finite(wlm_ctx* ctx, const double* data, size_t count, int* out);
+
+/* ---- host-buffer mirror of similarity / lmopt / pyramid (SPEC) ---- */
+wlm_status wlm_residual_lncc(wlm_ctx* ctx, const double* F, const double* M,
+                             const double* u, wlm_dims d, int radius, double* r,
+                             double* lncc, double* g /* nullable, AoS */);
+wlm_status wlm_lm_step_pointwise(wlm_ctx* ctx, double r, const double* g, wlm_dims d,
+                                 double lambda, double* out);
+void wlm_update_damping(wlm_lm_state* s, double loss_new, const wlm_lm_config* c);
+int wlm_rejection_test(double loss_new, double loss_prev, double loss_prev2, double tau);
+wlm_status wlm_downsample(wlm_ctx* ctx, const double* vol, wlm_dims d, int factor,
+                          double* out, wlm_dims* out_dims);
+wlm_status wlm_upsample_warp(wlm_ctx* ctx, const double* u, wlm_dims d, wlm_dims nd,
+                             double scale, double* out);
+/* state_bytes: persistent optimizer state, elem_bytes 4. */
+size_t wlm_state_bytes(int optimizer, wlm_dims d, int elem_bytes);
+
+/* ---- register: whole pyramid on the device ---- */
+/* F, M host fp32 (the VOL3 payload type), warp_out host fp64 AoS. */
+wlm_status wlm_register(wlm_ctx* ctx, const float* F, const float* M, wlm_dims d,
+                        const wlm_reg_config* cfg, double* warp_out,
+                        wlm_step_log* trace, size_t cap, size_t* len, double* jac_final);
+/* Peak device bytes held by the last wlm_register / engine on ctx. */
+size_t wlm_ctx_peak_bytes(const wlm_ctx* ctx);
+
+/* ---- device-resident batched LM engine (the hot loop) ----
+ * A batch of `pairs` independent registrations of identical dims; each pair
+ * has its own lambda, loss history, accept/reject state and trace.
+ * Device volumes are fp32 planes [pair][nz][ny][nx]; warps fp32
+ * [pair][3][nz][ny][nx].                                                    */
+wlm_status wlm_engine_create(wlm_ctx* ctx, wlm_dims d, int pairs, const wlm_reg_config* cfg,
+                             wlm_engine** out);
+void wlm_engine_destroy(wlm_engine* e);
+/* Copy volumes in (device or host pointers; is_host selects). */
+wlm_status wlm_engine_load(wlm_engine* e, const float* F, const float* M, int is_host);
+/* Set the current warps (fp32 SoA, device or host); NULL -> zero warps. */
+wlm_status wlm_engine_set_warp(wlm_engine* e, const float* u, int is_host);
+wlm_status wlm_engine_get_warp(wlm_engine* e, float* u, int is_host);
+/* Start a level: reset loss history, evaluate r(u) (lambda kept). */
+wlm_status wlm_engine_begin_level(wlm_engine* e, int level);
+/* Launch `iters` lm_iterate steps for every active pair (asynchronous; with
+ * rejection enabled the retries run inside a device-side WHILE graph). */
+wlm_status wlm_engine_iterate(wlm_engine* e, int iters);
+/* Launch exactly one attempt (K2..K4 + evaluation) per pair; the unit the
+ * benchmark times (rejection must be disabled). */
+wlm_status wlm_engine_step(wlm_engine* e);
+/* Copy out per-pair state / trace rows written since begin_level (syncs). */
+wlm_status wlm_engine_state(wlm_engine* e, int pair, wlm_lm_state* st, double* r,
+                            double* lncc, int* iters_done);
+wlm_status wlm_engine_trace(wlm_engine* e, int pair, wlm_step_log* rows, size_t cap,
+                            size_t* len);
+/* Device pointers of the engine's buffers (for tests / zero-copy callers). */
+wlm_status wlm_engine_buffers(wlm_engine* e, const float** F, const float** M,
+                              float** u_cur, float** g, float** vs);
+/* Scripted-residual harness: when n > 0, the evaluation
+ * kernels take attempt losses from `losses` (per pair: losses[pair*n + k])
+ * instead of the LNCC sum; n == 0 restores the real residual. */
+wlm_status wlm_engine_script_losses(wlm_engine* e, const double* losses, int n);
+
+/* Launch one stage of the attempt on every active pair (profiling hook):
+ * 0 = K1 evaluation of the attempt (warp + LNCC + state machine),
+ * 1 = K2 LNCC gradient, 2 = K3 LM step + smoothing + max,
+ * 3 = K4 compose + smoothing, 4 = K1 evaluation of the accepted warp. */
+wlm_status wlm_engine_stage(wlm_engine* e, int stage);
+
+/* ---- harness: synthetic pair on the GPU ----
+ * u_true is SoA fp32 [3][nz][ny][nx] (nullable); on_device selects whether
+ * F, M, u_true are device (1) or host (0) pointers. */
+typedef struct {
+    wlm_dims dims;
+    int num_blobs;
+    double warp_sigma; /* <= 0 -> min(dims)/16 */
+    double warp_max;
+    double noise_sigma;
+    uint64_t seed;
+} wlm_synth_spec;
+wlm_status wlm_synth_pair(wlm_ctx* ctx, const wlm_synth_spec* spec, float* F, float* M,
+                          float* u_true, int on_device);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

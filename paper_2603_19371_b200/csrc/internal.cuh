@@ -1,0 +1,227 @@
+// internal.cuh -- host-side plumbing shared by engine.cu and ops.cu:
+// context, error mapping, tracked device allocations.
+#pragma once
+
+#include <algorithm>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "kernels.cuh"
+#include "wlm.h"
+
+struct wlm_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;   // launches
+    cudaStream_t capture = nullptr;  // private stream for graph capture
+    bool own_stream = true;
+    std::string err;
+    uint64_t launches = 0;
+    size_t cur_bytes = 0, peak_bytes = 0;
+};
+
+namespace wlm {
+
+struct Fail {
+    wlm_status st;
+};
+
+inline void set_err(wlm_ctx* c, const std::string& m) {
+    if (c) c->err = m;
+}
+
+#define CK(call)                                                                          \
+    do {                                                                                  \
+        cudaError_t e_ = (call);                                                          \
+        if (e_ != cudaSuccess) {                                                          \
+            set_err(ctx, std::string(#call) + ": " + cudaGetErrorString(e_));             \
+            throw Fail{e_ == cudaErrorMemoryAllocation ? WLM_OOM : WLM_CUDA};             \
+        }                                                                                 \
+    } while (0)
+
+template <class T>
+struct DevBuf {
+    wlm_ctx* ctx = nullptr;
+    T* p = nullptr;
+    size_t count = 0;
+    DevBuf() = default;
+    DevBuf(wlm_ctx* c, size_t n) : ctx(c), count(n) {
+        if (n == 0) return;
+        cudaError_t e = cudaMalloc(&p, sizeof(T) * n);
+        if (e != cudaSuccess) {
+            p = nullptr;
+            set_err(c, std::string("cudaMalloc: ") + cudaGetErrorString(e));
+            throw Fail{WLM_OOM};
+        }
+        c->cur_bytes += sizeof(T) * n;
+        c->peak_bytes = std::max(c->peak_bytes, c->cur_bytes);
+    }
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    DevBuf(DevBuf&& o) noexcept { *this = std::move(o); }
+    DevBuf& operator=(DevBuf&& o) noexcept {
+        release();
+        ctx = o.ctx; p = o.p; count = o.count;
+        o.p = nullptr; o.count = 0;
+        return *this;
+    }
+    ~DevBuf() { release(); }
+    void release() {
+        if (p) {
+            cudaFree(p);
+            ctx->cur_bytes -= sizeof(T) * count;
+            p = nullptr;
+            count = 0;
+        }
+    }
+};
+
+inline bool valid_dims(wlm_dims d) { return d.nx > 0 && d.ny > 0 && d.nz > 0; }
+inline bool same_dims(wlm_dims a, wlm_dims b) { return a.nx == b.nx && a.ny == b.ny && a.nz == b.nz; }
+inline size_t nvox(wlm_dims d) { return (size_t)d.nx * d.ny * d.nz; }
+
+inline int smooth_radius(double sigma) {
+    if (!(sigma > 0.0)) return 0;
+    return std::max(1, (int)std::ceil(3.0 * sigma));
+}
+
+inline void fill_half_kernel(double sigma, int R, float* w, float* full) {
+    if (R == 0) { w[0] = 1.f; *full = 1.f; return; }
+    double s = 0.0;
+    for (int d = 0; d <= R; ++d) {
+        const double v = std::exp(-0.5 * (double)(d * d) / (sigma * sigma));
+        w[d] = (float)v;
+        s += d == 0 ? v : 2.0 * v;
+    }
+    *full = (float)s;
+}
+
+inline wlm_status guard(wlm_ctx* ctx) {
+    if (!ctx) return WLM_INVALID_ARG;
+    cudaError_t e = cudaSetDevice(ctx->device);
+    if (e != cudaSuccess) {
+        set_err(ctx, std::string("cudaSetDevice: ") + cudaGetErrorString(e));
+        return WLM_CUDA;
+    }
+    return WLM_OK;
+}
+
+// Runs fn with CUDA errors mapped to wlm_status.  Kernel launches are
+// credited to the outermost call only (entry points may nest).
+inline int& run_depth() {
+    static thread_local int d = 0;
+    return d;
+}
+
+template <class Fn>
+wlm_status run(wlm_ctx* ctx, Fn fn) {
+    wlm_status s = guard(ctx);
+    if (s != WLM_OK) return s;
+    const uint64_t before = g_kernel_launches;
+    ++run_depth();
+    try {
+        fn();
+    } catch (const Fail& f) {
+        if (--run_depth() == 0) ctx->launches += g_kernel_launches - before;
+        return f.st;
+    }
+    if (--run_depth() == 0) ctx->launches += g_kernel_launches - before;
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+        set_err(ctx, std::string("kernel launch: ") + cudaGetErrorString(e));
+        return WLM_CUDA;
+    }
+    return WLM_OK;
+}
+
+}  // namespace wlm
+
+
+// ===========================================================================
+// Engine
+using namespace wlm;
+struct wlm_engine {
+    wlm_ctx* ctx = nullptr;
+    Geo g{};
+    wlm_dims dims{};
+    int pairs = 0;
+    wlm_reg_config cfg{};
+    LmParams P{};
+    DevBuf<float> F, M, U, ABE, G, VS, AM, AV;
+    DevBuf<PairState> st;
+    DevBuf<double> partials, script;
+    DevBuf<wlm_step_log> trace;
+    Batch B{};
+    cudaGraphExec_t step_exec = nullptr, loop_exec = nullptr;
+    cudaGraph_t step_graph = nullptr, loop_graph = nullptr;
+    int body_kernels = 0;
+
+    ~wlm_engine() {
+        if (step_exec) cudaGraphExecDestroy(step_exec);
+        if (loop_exec) cudaGraphExecDestroy(loop_exec);
+        if (step_graph) cudaGraphDestroy(step_graph);
+        if (loop_graph) cudaGraphDestroy(loop_graph);
+    }
+
+    void body(cudaStream_t s) {
+        launch_lncc_bwd(B, P, s);
+        if (P.optimizer == WLM_OPT_ADAM) launch_adam(B, P, s);
+        launch_step_smooth(B, P, s);
+        launch_compose_smooth(B, P, s);
+        if (P.log_jacobian) launch_jacobian_diag(B, P, s);
+        launch_lncc_fwd(B, P, 1, s);
+    }
+
+    void invalidate_graphs() {
+        if (step_exec) { cudaGraphExecDestroy(step_exec); step_exec = nullptr; }
+        if (loop_exec) { cudaGraphExecDestroy(loop_exec); loop_exec = nullptr; }
+        if (step_graph) { cudaGraphDestroy(step_graph); step_graph = nullptr; }
+        if (loop_graph) { cudaGraphDestroy(loop_graph); loop_graph = nullptr; }
+    }
+
+    void build_step_graph() {
+        if (step_exec) return;
+        const uint64_t saved = g_kernel_launches;
+        CK(cudaStreamBeginCapture(ctx->capture, cudaStreamCaptureModeThreadLocal));
+        body(ctx->capture);
+        CK(cudaStreamEndCapture(ctx->capture, &step_graph));
+        body_kernels = (int)(g_kernel_launches - saved);
+        g_kernel_launches = saved;
+        CK(cudaGraphInstantiate(&step_exec, step_graph, 0));
+    }
+
+    // WHILE(any pair not done) { body; cond } -- rejection retries and the
+    // iteration count live entirely on the device.
+    void build_loop_graph() {
+        if (loop_exec) return;
+        CK(cudaGraphCreate(&loop_graph, 0));
+        cudaGraphConditionalHandle h;
+        CK(cudaGraphConditionalHandleCreate(&h, loop_graph, 1, cudaGraphCondAssignDefault));
+        alignas(cudaGraphNodeParams) unsigned char raw[sizeof(cudaGraphNodeParams)] = {};
+        cudaGraphNodeParams& cp = *reinterpret_cast<cudaGraphNodeParams*>(raw);
+        cp.type = cudaGraphNodeTypeConditional;
+        cp.conditional.handle = h;
+        cp.conditional.type = cudaGraphCondTypeWhile;
+        cp.conditional.size = 1;
+        cudaGraphNode_t node;
+        CK(cudaGraphAddNode(&node, loop_graph, nullptr, 0, &cp));
+        cudaGraph_t bodyg = cp.conditional.phGraph_out[0];
+        const uint64_t saved = g_kernel_launches;
+        CK(cudaStreamBeginCaptureToGraph(ctx->capture, bodyg, nullptr, nullptr, 0,
+                                         cudaStreamCaptureModeThreadLocal));
+        body(ctx->capture);
+        launch_loop_cond(B, h, ctx->capture);
+        cudaGraph_t out = nullptr;
+        CK(cudaStreamEndCapture(ctx->capture, &out));
+        g_kernel_launches = saved;
+        CK(cudaGraphInstantiate(&loop_exec, loop_graph, 0));
+    }
+};
+
+
+namespace wlm {
+wlm_status engine_init(wlm_engine* e, wlm_ctx* ctx, wlm_dims d, int pairs, const wlm_reg_config* c);
+void engine_alloc(wlm_engine* e);
+std::vector<PairState> read_states(wlm_engine* e);
+void copy_warps_in(wlm_engine* e, const float* u, int is_host);
+}  // namespace wlm

@@ -1,0 +1,1006 @@
+// kernels.cu -- sm_100a kernels of the factored-LM iteration (SURVEY §2.2
+// K1-K5) and the standalone field operations.
+//
+// All hot-path kernels share one z-marching separable-stencil schedule: a
+// CTA owns a 32 x TY column of output voxels and a chunk of z planes; each
+// input plane (with an R-voxel x/y halo) is produced once into shared memory,
+// filtered along x then y from shared memory, and the filtered column enters a
+// register ring of 2R+1 planes that is filtered along z.  Every global
+// read/write is a unit-stride row of one SoA plane (coalesced), the halo
+// overlap between neighbouring CTAs is served by L2, and there are no float
+// atomics: sums are per-CTA fp64 partials reduced in a fixed order by the
+// last CTA of each pair (deterministic), maxima use exact
+// ordered-integer atomics.
+#include <algorithm>
+#include <cfloat>
+#include <climits>
+#include <cmath>
+
+#include "kernels.cuh"
+
+namespace wlm {
+
+uint64_t g_kernel_launches = 0;
+
+namespace {
+constexpr int TX = 32;
+constexpr int TY = 8;
+constexpr int NT = TX * TY;
+constexpr int kNumSMs = 148;
+
+__host__ __device__ inline int cdiv(int a, int b) { return (a + b - 1) / b; }
+}  // namespace
+
+dim3 LaunchShape::grid() const { return dim3(tiles_x * tiles_y, chunks, 1); }
+
+LaunchShape shape_for(const Geo& g, int pairs, int ty) {
+    LaunchShape s;
+    s.tiles_x = cdiv(g.nx, TX);
+    s.tiles_y = cdiv(g.ny, ty);
+    const long long tiles = (long long)s.tiles_x * s.tiles_y * pairs;
+    // aim for >= 8 resident CTAs per SM worth of work; keep >= 8 planes a chunk
+    const long long want = (long long)kNumSMs * 8;
+    int chunks = (int)std::max<long long>(1, std::min<long long>(g.nz, (want + tiles - 1) / tiles));
+    int len = cdiv(g.nz, chunks);
+    len = std::max(len, std::min(g.nz, 8));
+    s.chunk_len = len;
+    s.chunks = cdiv(g.nz, len);
+    return s;
+}
+
+// ---------------------------------------------------------------------------
+// Loss / damping / rejection state machine, run by one
+// thread of the last CTA of the evaluation kernel.  Identical fp64
+// arithmetic to the oracle (oracle.cpp orc_update_damping /
+// attempt_rejected), so the lambda trajectory is bit-identical whenever the
+// accept/reject decisions agree.
+__device__ void update_damping_dev(PairState* st, const LmParams& p, double r) {
+    const bool bad = st->hist_n == 0 || r > st->L1;
+    double lam = bad ? p.mu_plus * st->lambda : p.mu_minus * st->lambda;
+    if (p.lambda_max > 0.0 && isfinite(p.lambda_max)) lam = fmin(lam, p.lambda_max);
+    st->lambda = fmax(lam, 1e-12);
+    st->L2 = st->L1;
+    st->L1 = r;
+    st->hist_n = min(st->hist_n + 1, 2);
+}
+
+__device__ bool rejection_fires(const PairState* st, const LmParams& p, double r) {
+    return p.rejection && st->hist_n >= 2 && (r - st->L1) > p.tau * fabs(st->L1 - st->L2);
+}
+
+__device__ void finalize_pair(PairState* st, const LmParams& p, int mode, double lncc, long long N,
+                              int pair) {
+    double r = 1.0 - lncc;
+    if (mode == 0) {
+        st->r_cur = r;
+        st->lncc_cur = lncc;
+        if (!isfinite(r)) { st->status = WLM_NONFINITE; st->done = 1; }
+        st->max_bits = 0u;
+        st->jac_bits = 0x7f800000;  // +inf
+        return;
+    }
+    if (p.script && p.script_n > 0) {
+        r = p.script[(long long)pair * p.script_n + min(st->attempt, p.script_n - 1)];
+        lncc = 1.0 - r;
+    }
+    st->attempt += 1;
+    st->r_try = r;
+    st->lncc_try = lncc;
+    const double maxv = (double)__uint_as_float(st->max_bits);
+    const double eps = p.target / fmax(maxv, p.step_floor);
+    if (!isfinite(r)) {  // abort
+        st->status = WLM_NONFINITE;
+        st->done = 1;
+        return;
+    }
+    bool rej = false;
+    if (p.optimizer == WLM_OPT_LM && st->retries < p.max_retries && rejection_fires(st, p, r)) {
+        double lam = p.mu_plus * st->lambda;
+        if (p.lambda_max > 0.0 && isfinite(p.lambda_max)) lam = fmin(lam, p.lambda_max);
+        st->lambda = lam;
+        st->retries += 1;
+        rej = true;
+    }
+    if (rej) {
+        st->last_rejected = 1;
+    } else {
+        const bool forced = p.optimizer == WLM_OPT_LM && st->retries >= p.max_retries &&
+                            rejection_fires(st, p, r);
+        if (p.optimizer == WLM_OPT_LM) update_damping_dev(st, p, r);
+        st->cur ^= 1;
+        st->r_cur = r;
+        st->lncc_cur = lncc;
+        st->last_rejected = 0;
+        if (p.trace && st->trace_len < p.trace_cap) {
+            wlm_step_log* row = p.trace + (long long)pair * p.trace_cap + st->trace_len;
+            row->level = st->level;
+            row->iter = st->iter;
+            row->loss_raw = lncc;
+            row->r = r;
+            row->lambda = p.optimizer == WLM_OPT_LM ? st->lambda : 0.0;
+            row->eps = eps;
+            row->accepted = forced ? 0 : 1;
+            row->retries = st->retries;
+            row->jac_det_min = p.log_jacobian ? (double)ordered_to_float(st->jac_bits)
+                                              : __longlong_as_double(0x7ff8000000000000ll);
+            st->trace_len += 1;
+        }
+        st->iter += 1;
+        st->retries = 0;
+        if (st->iter >= st->iters_target) st->done = 1;
+    }
+    st->max_bits = 0u;
+    st->jac_bits = 0x7f800000;
+}
+
+// Block-wide fixed-order double sum (result valid in thread 0).
+__device__ double block_sum(double v, double* red) {
+    v = warp_sum(v);
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    if (lane == 0) red[w] = v;
+    __syncthreads();
+    double s = 0.0;
+    if (threadIdx.x == 0)
+        for (int i = 0; i < (int)(blockDim.x >> 5); ++i) s += red[i];
+    __syncthreads();
+    return s;
+}
+
+// ---------------------------------------------------------------------------
+// K1: warp + LNCC forward.
+//   input plane (halo R): f' = F - shift_f, m' = M(x + u(x)) - shift_m
+//   window sums (box, truncated): S_f, S_m, S_ff, S_mm, S_fm   (fp32 on
+//   shifted intensities -- SURVEY §9.1 N1 / DESIGN.md "precision")
+//   rho = c / sqrt(vf vm); A = 1/(n sqrt(vf vm)); B = -rho/(n vm);
+//   E = A mu_f' + B mu_m'   -> written as three planes, sum(rho) -> partial
+template <int R>
+__global__ void __launch_bounds__(NT) k_lncc_fwd(Batch b, LmParams p, int mode, int chunk_len) {
+    constexpr int IW = TX + 2 * R, IH = TY + 2 * R, W = 2 * R + 1;
+    __shared__ float s_f[IH][IW], s_m[IH][IW];
+    __shared__ float s_x[5][IH][TX];
+    __shared__ double s_red[NT / 32];
+    __shared__ int s_last;
+
+    const int pair = blockIdx.z;
+    PairState* st = b.st + pair;
+    if (st->done) return;
+    const Geo g = b.g;
+    const long long n = g.n;
+    const int tiles_x = cdiv(g.nx, TX);
+    const int x0 = (blockIdx.x % tiles_x) * TX, y0 = (blockIdx.x / tiles_x) * TY;
+    const int zb = blockIdx.y * chunk_len, ze = min(zb + chunk_len, g.nz);
+    const int buf = mode == 0 ? st->cur : 1 - st->cur;
+    const float* __restrict__ F = b.F + (long long)pair * n;
+    const float* __restrict__ M = b.M + (long long)pair * n;
+    const float* __restrict__ U = b.U + ((long long)pair * 2 + buf) * 3 * n;
+    float* __restrict__ A = b.ABE + (long long)pair * 3 * n;
+    const float shf = st->shift_f, shm = st->shift_m;
+    const int tid = threadIdx.x, ox = tid & 31, oy = tid >> 5;
+    const int x = x0 + ox, y = y0 + oy;
+    const bool own = x < g.nx && y < g.ny;
+    const float cxy = own ? (float)(axis_count(x, g.nx, R) * axis_count(y, g.ny, R)) : 1.f;
+
+    float ring[W][5];
+#pragma unroll
+    for (int d = 0; d < W; ++d)
+#pragma unroll
+        for (int c = 0; c < 5; ++c) ring[d][c] = 0.f;
+    double rho_acc = 0.0;
+
+    for (int zi = zb - R; zi < ze + R; ++zi) {
+        const bool zin = zi >= 0 && zi < g.nz;
+        for (int idx = tid; idx < IW * IH; idx += NT) {
+            const int ix = idx % IW, iy = idx / IW;
+            const int gx = x0 - R + ix, gy = y0 - R + iy;
+            float fv = 0.f, mv = 0.f;
+            if (zin && gx >= 0 && gx < g.nx && gy >= 0 && gy < g.ny) {
+                const long long o = g.at(gx, gy, zi);
+                const Cell cell = make_cell(g, gx, gy, zi, __ldg(U + o), __ldg(U + n + o),
+                                            __ldg(U + 2 * n + o));
+                mv = cell_sample(M, cell) - shm;
+                fv = __ldg(F + o) - shf;
+            }
+            s_f[iy][ix] = fv;
+            s_m[iy][ix] = mv;
+        }
+        __syncthreads();
+        for (int idx = tid; idx < IH * TX; idx += NT) {
+            const int c = idx % TX, r = idx / TX;
+            float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f, a4 = 0.f;
+#pragma unroll
+            for (int d = 0; d < W; ++d) {
+                const float f = s_f[r][c + d], m = s_m[r][c + d];
+                a0 += f;
+                a1 += m;
+                a2 = fmaf(f, f, a2);
+                a3 = fmaf(m, m, a3);
+                a4 = fmaf(f, m, a4);
+            }
+            s_x[0][r][c] = a0; s_x[1][r][c] = a1; s_x[2][r][c] = a2;
+            s_x[3][r][c] = a3; s_x[4][r][c] = a4;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int d = 0; d < W - 1; ++d)
+#pragma unroll
+            for (int c = 0; c < 5; ++c) ring[d][c] = ring[d + 1][c];
+#pragma unroll
+        for (int c = 0; c < 5; ++c) {
+            float s = 0.f;
+#pragma unroll
+            for (int d = 0; d < W; ++d) s += s_x[c][oy + d][ox];
+            ring[W - 1][c] = s;
+        }
+        const int zo = zi - R;
+        if (zo >= zb && own) {
+            float S[5];
+#pragma unroll
+            for (int c = 0; c < 5; ++c) {
+                float s = 0.f;
+#pragma unroll
+                for (int d = 0; d < W; ++d) s += ring[d][c];
+                S[c] = s;
+            }
+            const float cnt = cxy * (float)axis_count(zo, g.nz, R);
+            const float inv = 1.f / cnt;
+            const float mf = S[0] * inv, mm = S[1] * inv;
+            const float vf = fmaf(-mf, mf, S[2] * inv);
+            const float vm = fmaf(-mm, mm, S[3] * inv);
+            const float cv = fmaf(-mf, mm, S[4] * inv);
+            const float af = mf + shf, am = mm + shm;
+            const float msf = fmaf(af, af, vf), msm = fmaf(am, am, vm);
+            float rho = 0.f, Aa = 0.f, Bb = 0.f, Ee = 0.f;
+            if (msf > 0.f && msm > 0.f && vf > 1e-9f * msf && vm > 1e-9f * msm) {
+                const float alpha = rsqrtf(vf) * rsqrtf(vm);
+                rho = cv * alpha;
+                Aa = alpha * inv;
+                Bb = -rho / vm * inv;
+                Ee = fmaf(Aa, mf, Bb * mm);
+            }
+            const long long o = g.at(x, y, zo);
+            A[o] = Aa;
+            A[n + o] = Bb;
+            A[2 * n + o] = Ee;
+            rho_acc += (double)rho;
+        }
+    }
+
+    const double tot = block_sum(rho_acc, s_red);
+    const int nblk = gridDim.x * gridDim.y;
+    const int blk = blockIdx.x + gridDim.x * blockIdx.y;
+    if (tid == 0) {
+        b.partials[(long long)pair * b.max_blocks + blk] = tot;
+        __threadfence();
+        const unsigned prev = atomicAdd(&st->counter, 1u);
+        s_last = prev == (unsigned)(nblk - 1);
+    }
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    double s = 0.0;
+    for (int i = tid; i < nblk; i += NT) s += __ldcg(b.partials + (long long)pair * b.max_blocks + i);
+    const double total = block_sum(s, s_red);
+    if (tid == 0) {
+        st->counter = 0u;
+        finalize_pair(st, p, mode, total / (double)n, n, pair);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K2: LNCC backward.  Adjoint box sums of (A, B, E) over the same windows,
+//   dr/dMw(x) = -(1/N) (f'_x S_A + m'_x S_B - S_E),  g = dr/dMw * gradM(x+u)
+template <int R>
+__global__ void __launch_bounds__(NT) k_lncc_bwd(Batch b, LmParams p, int chunk_len) {
+    constexpr int IW = TX + 2 * R, IH = TY + 2 * R, W = 2 * R + 1;
+    __shared__ float s_in[3][IH][IW];
+    __shared__ float s_x[3][IH][TX];
+
+    const int pair = blockIdx.z;
+    const PairState* st = b.st + pair;
+    if (st->done || st->last_rejected) return;
+    const Geo g = b.g;
+    const long long n = g.n;
+    const int tiles_x = cdiv(g.nx, TX);
+    const int x0 = (blockIdx.x % tiles_x) * TX, y0 = (blockIdx.x / tiles_x) * TY;
+    const int zb = blockIdx.y * chunk_len, ze = min(zb + chunk_len, g.nz);
+    const float* __restrict__ F = b.F + (long long)pair * n;
+    const float* __restrict__ M = b.M + (long long)pair * n;
+    const float* __restrict__ U = b.U + ((long long)pair * 2 + st->cur) * 3 * n;
+    const float* __restrict__ A = b.ABE + (long long)pair * 3 * n;
+    float* __restrict__ G = b.G + (long long)pair * 3 * n;
+    const float shf = st->shift_f, shm = st->shift_m;
+    const float invN = (float)(1.0 / (double)n);
+    const int tid = threadIdx.x, ox = tid & 31, oy = tid >> 5;
+    const int x = x0 + ox, y = y0 + oy;
+    const bool own = x < g.nx && y < g.ny;
+
+    float ring[W][3];
+#pragma unroll
+    for (int d = 0; d < W; ++d)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) ring[d][c] = 0.f;
+
+    for (int zi = zb - R; zi < ze + R; ++zi) {
+        const bool zin = zi >= 0 && zi < g.nz;
+        for (int idx = tid; idx < IW * IH; idx += NT) {
+            const int ix = idx % IW, iy = idx / IW;
+            const int gx = x0 - R + ix, gy = y0 - R + iy;
+            float a = 0.f, bb = 0.f, e = 0.f;
+            if (zin && gx >= 0 && gx < g.nx && gy >= 0 && gy < g.ny) {
+                const long long o = g.at(gx, gy, zi);
+                a = __ldg(A + o);
+                bb = __ldg(A + n + o);
+                e = __ldg(A + 2 * n + o);
+            }
+            s_in[0][iy][ix] = a;
+            s_in[1][iy][ix] = bb;
+            s_in[2][iy][ix] = e;
+        }
+        __syncthreads();
+        for (int idx = tid; idx < IH * TX; idx += NT) {
+            const int c = idx % TX, r = idx / TX;
+#pragma unroll
+            for (int ch = 0; ch < 3; ++ch) {
+                float s = 0.f;
+#pragma unroll
+                for (int d = 0; d < W; ++d) s += s_in[ch][r][c + d];
+                s_x[ch][r][c] = s;
+            }
+        }
+        __syncthreads();
+#pragma unroll
+        for (int d = 0; d < W - 1; ++d)
+#pragma unroll
+            for (int c = 0; c < 3; ++c) ring[d][c] = ring[d + 1][c];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            float s = 0.f;
+#pragma unroll
+            for (int d = 0; d < W; ++d) s += s_x[c][oy + d][ox];
+            ring[W - 1][c] = s;
+        }
+        const int zo = zi - R;
+        if (zo >= zb && own) {
+            float S[3];
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                float s = 0.f;
+#pragma unroll
+                for (int d = 0; d < W; ++d) s += ring[d][c];
+                S[c] = s;
+            }
+            const long long o = g.at(x, y, zo);
+            float gmx, gmy, gmz;
+            const float mw = sample_grad(M, g, x, y, zo, __ldg(U + o), __ldg(U + n + o),
+                                         __ldg(U + 2 * n + o), gmx, gmy, gmz);
+            const float f = __ldg(F + o) - shf;
+            const float dm = -invN * (fmaf(f, S[0], (mw - shm) * S[1]) - S[2]);
+            G[o] = dm * gmx;
+            G[n + o] = dm * gmy;
+            G[2 * n + o] = dm * gmz;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Gaussian z-march over 3 channels (K3, K4).  Weights w[|d|] are truncated
+// at R and renormalised per axis over in-bounds taps (field.cpp:236-244):
+// zero-filled halos + a final divide by Wx(x) Wy(y) Wz(z).
+template <int R, class Prod, class Cons>
+__device__ __forceinline__ void gauss_march3(const Geo& g, int x0, int y0, int zb, int ze,
+                                             const float* wh, float wfull, Prod& prod,
+                                             Cons& cons) {
+    constexpr int IW = TX + 2 * R, IH = TY + 2 * R, W = 2 * R + 1;
+    __shared__ float s_in[3][IH][IW];
+    __shared__ float s_x[3][IH][TX];
+    float wr[W];
+#pragma unroll
+    for (int d = 0; d < W; ++d) wr[d] = wh[d < R ? R - d : d - R];
+    const int tid = threadIdx.x, ox = tid & 31, oy = tid >> 5;
+    const int x = x0 + ox, y = y0 + oy;
+    const bool own = x < g.nx && y < g.ny;
+    const float wxy = own ? axis_wsum(x, g.nx, R, wh, wfull) * axis_wsum(y, g.ny, R, wh, wfull) : 1.f;
+    float ring[W][3];
+#pragma unroll
+    for (int d = 0; d < W; ++d)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) ring[d][c] = 0.f;
+
+    for (int zi = zb - R; zi < ze + R; ++zi) {
+        const bool zin = zi >= 0 && zi < g.nz;
+        for (int idx = tid; idx < IW * IH; idx += NT) {
+            const int ix = idx % IW, iy = idx / IW;
+            const int gx = x0 - R + ix, gy = y0 - R + iy;
+            float v[3] = {0.f, 0.f, 0.f};
+            if (zin && gx >= 0 && gx < g.nx && gy >= 0 && gy < g.ny) prod(gx, gy, zi, v);
+            s_in[0][iy][ix] = v[0];
+            s_in[1][iy][ix] = v[1];
+            s_in[2][iy][ix] = v[2];
+        }
+        __syncthreads();
+        for (int idx = tid; idx < IH * TX; idx += NT) {
+            const int c = idx % TX, r = idx / TX;
+#pragma unroll
+            for (int ch = 0; ch < 3; ++ch) {
+                float s = 0.f;
+#pragma unroll
+                for (int d = 0; d < W; ++d) s = fmaf(wr[d], s_in[ch][r][c + d], s);
+                s_x[ch][r][c] = s;
+            }
+        }
+        __syncthreads();
+#pragma unroll
+        for (int d = 0; d < W - 1; ++d)
+#pragma unroll
+            for (int c = 0; c < 3; ++c) ring[d][c] = ring[d + 1][c];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            float s = 0.f;
+#pragma unroll
+            for (int d = 0; d < W; ++d) s = fmaf(wr[d], s_x[c][oy + d][ox], s);
+            ring[W - 1][c] = s;
+        }
+        const int zo = zi - R;
+        if (zo >= zb && own) {
+            const float inv = 1.f / (wxy * axis_wsum(zo, g.nz, R, wh, wfull));
+            float o3[3];
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                float s = 0.f;
+#pragma unroll
+                for (int d = 0; d < W; ++d) s = fmaf(wr[d], ring[d][c], s);
+                o3[c] = s * inv;
+            }
+            cons(x, y, zo, o3);
+        }
+    }
+}
+
+// K3: dU = -r g / (|g|^2 + lambda) (Eq. 4) | -lr g (GD) | Adam step (precomputed),
+// smoothed with sigma_update, written to VS, max |dU_s| -> PairState.max_bits.
+template <int R>
+__global__ void __launch_bounds__(NT) k_step_smooth(Batch b, LmParams p, int chunk_len) {
+    __shared__ float s_max[NT / 32];
+    const int pair = blockIdx.z;
+    PairState* st = b.st + pair;
+    if (st->done) return;
+    const Geo g = b.g;
+    const long long n = g.n;
+    const int tiles_x = cdiv(g.nx, TX);
+    const int x0 = (blockIdx.x % tiles_x) * TX, y0 = (blockIdx.x / tiles_x) * TY;
+    const int zb = blockIdx.y * chunk_len, ze = min(zb + chunk_len, g.nz);
+    const float* __restrict__ G = b.G + (long long)pair * 3 * n;
+    float* __restrict__ V = b.VS + (long long)pair * 3 * n;
+    const float r = (float)st->r_cur, lam = (float)st->lambda;
+    const int opt = p.optimizer;
+    const float lr = (float)p.gd_lr;
+    auto prod = [&](int gx, int gy, int gz, float* v) {
+        const long long o = g.at(gx, gy, gz);
+        const float a = __ldg(G + o), bb = __ldg(G + n + o), c = __ldg(G + 2 * n + o);
+        float s;
+        if (opt == WLM_OPT_LM) s = -r / (fmaf(a, a, fmaf(bb, bb, c * c)) + lam);
+        else if (opt == WLM_OPT_GD) s = -lr;
+        else s = 1.f;  // Adam step already in G
+        v[0] = s * a; v[1] = s * bb; v[2] = s * c;
+    };
+    float mx = 0.f;
+    auto cons = [&](int x, int y, int z, const float* o3) {
+        const long long o = g.at(x, y, z);
+        V[o] = o3[0];
+        V[n + o] = o3[1];
+        V[2 * n + o] = o3[2];
+        mx = fmaxf(mx, fmaxf(fabsf(o3[0]), fmaxf(fabsf(o3[1]), fabsf(o3[2]))));
+    };
+    gauss_march3<R>(g, x0, y0, zb, ze, p.wu, p.wu_full, prod, cons);
+    mx = warp_max(mx);
+    if ((threadIdx.x & 31) == 0) s_max[threadIdx.x >> 5] = mx;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        float m = 0.f;
+        for (int i = 0; i < NT / 32; ++i) m = fmaxf(m, s_max[i]);
+        atomic_max_nonneg(&st->max_bits, m);
+    }
+}
+
+// K4: u'(x) = d(x) + u(x + d(x)), d = eps dU_s, eps = target / max(max|dU_s|,
+// floor) (Eq. 2, field.cpp:123-155), then Gaussian(sigma_warp); reads the
+// accepted buffer, writes the other one (ping-pong = free rejection restore).
+template <int R>
+__global__ void __launch_bounds__(NT) k_compose_smooth(Batch b, LmParams p, int chunk_len) {
+    const int pair = blockIdx.z;
+    const PairState* st = b.st + pair;
+    if (st->done) return;
+    const Geo g = b.g;
+    const long long n = g.n;
+    const int tiles_x = cdiv(g.nx, TX);
+    const int x0 = (blockIdx.x % tiles_x) * TX, y0 = (blockIdx.x / tiles_x) * TY;
+    const int zb = blockIdx.y * chunk_len, ze = min(zb + chunk_len, g.nz);
+    const int cur = st->cur;
+    const float* __restrict__ V = b.VS + (long long)pair * 3 * n;
+    const float* __restrict__ U = b.U + ((long long)pair * 2 + cur) * 3 * n;
+    float* __restrict__ UN = b.U + ((long long)pair * 2 + (1 - cur)) * 3 * n;
+    const float eps =
+        (float)(p.target / fmax((double)__uint_as_float(st->max_bits), p.step_floor));
+    auto prod = [&](int gx, int gy, int gz, float* v) {
+        const long long o = g.at(gx, gy, gz);
+        const float dx = eps * __ldg(V + o), dy = eps * __ldg(V + n + o),
+                    dz = eps * __ldg(V + 2 * n + o);
+        const Cell c = make_cell(g, gx, gy, gz, dx, dy, dz);
+        v[0] = dx + cell_sample(U, c);
+        v[1] = dy + cell_sample(U + n, c);
+        v[2] = dz + cell_sample(U + 2 * n, c);
+    };
+    auto cons = [&](int x, int y, int z, const float* o3) {
+        const long long o = g.at(x, y, z);
+        UN[o] = o3[0];
+        UN[n + o] = o3[1];
+        UN[2 * n + o] = o3[2];
+    };
+    gauss_march3<R>(g, x0, y0, zb, ze, p.ww, p.ww_full, prod, cons);
+}
+
+// Adam, pointwise; t = accepted iterations + 1 at this level.
+__global__ void k_adam(Batch b, LmParams p) {
+    const int pair = blockIdx.y;
+    const PairState* st = b.st + pair;
+    if (st->done) return;
+    const long long n3 = 3 * b.g.n;
+    float* G = b.G + (long long)pair * n3;
+    float* Mm = b.AM + (long long)pair * n3;
+    float* Vv = b.AV + (long long)pair * n3;
+    const int t = st->iter + 1;
+    const float b1 = (float)p.adam_b1, b2 = (float)p.adam_b2;
+    const float bc1 = (float)(1.0 - pow(p.adam_b1, t)), bc2 = (float)(1.0 - pow(p.adam_b2, t));
+    const float lr = (float)p.adam_lr, ep = (float)p.adam_eps;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n3;
+         i += (long long)gridDim.x * blockDim.x) {
+        const float gi = G[i];
+        const float m = fmaf(b1, Mm[i], (1.f - b1) * gi);
+        const float v = fmaf(b2, Vv[i], (1.f - b2) * gi * gi);
+        Mm[i] = m;
+        Vv[i] = v;
+        G[i] = -lr * (m / bc1) / (sqrtf(v / bc2) + ep);
+    }
+}
+
+// det(I + grad d) at (x,y,z) of an SoA field scaled by `scale`, central
+// differences, one-sided only on 2-voxel axes (field.cpp:157-201).
+__device__ float det_at(const float* U, const Geo& g, int x, int y, int z, float scale) {
+    const int p[3] = {x, y, z};
+    const int nn[3] = {g.nx, g.ny, g.nz};
+    float J[3][3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        int q1[3] = {x, y, z}, q0[3] = {x, y, z};
+        float k = 0.5f;
+        if (p[a] >= 1 && p[a] + 1 <= nn[a] - 1) { q1[a] = p[a] + 1; q0[a] = p[a] - 1; }
+        else if (p[a] == 0) { q1[a] = 1; q0[a] = 0; k = 1.f; }
+        else { q1[a] = p[a]; q0[a] = p[a] - 1; k = 1.f; }
+        const long long i1 = g.at(q1[0], q1[1], q1[2]), i0 = g.at(q0[0], q0[1], q0[2]);
+#pragma unroll
+        for (int c = 0; c < 3; ++c) J[c][a] = k * scale * (__ldg(U + c * g.n + i1) - __ldg(U + c * g.n + i0));
+    }
+    J[0][0] += 1.f; J[1][1] += 1.f; J[2][2] += 1.f;
+    return J[0][0] * (J[1][1] * J[2][2] - J[1][2] * J[2][1]) -
+           J[0][1] * (J[1][0] * J[2][2] - J[1][2] * J[2][0]) +
+           J[0][2] * (J[1][0] * J[2][1] - J[1][1] * J[2][0]);
+}
+
+__device__ __forceinline__ void interior(int n, int& lo, int& hi) {
+    lo = n >= 3 ? 1 : 0;
+    hi = n >= 3 ? n - 2 : n - 1;
+}
+
+__global__ void k_jacobian_diag(Batch b, LmParams p) {
+    __shared__ float s_min[32];
+    const int pair = blockIdx.y;
+    PairState* st = b.st + pair;
+    if (st->done) return;
+    const Geo g = b.g;
+    const float* V = b.VS + (long long)pair * 3 * g.n;
+    const float eps = (float)(p.target / fmax((double)__uint_as_float(st->max_bits), p.step_floor));
+    int xl, xh, yl, yh, zl, zh;
+    interior(g.nx, xl, xh); interior(g.ny, yl, yh); interior(g.nz, zl, zh);
+    const long long cx = xh - xl + 1, cy = yh - yl + 1, cz = zh - zl + 1;
+    const long long tot = cx * cy * cz;
+    float mn = FLT_MAX;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < tot;
+         i += (long long)gridDim.x * blockDim.x) {
+        const int x = xl + (int)(i % cx), y = yl + (int)((i / cx) % cy), z = zl + (int)(i / (cx * cy));
+        mn = fminf(mn, det_at(V, g, x, y, z, eps));
+    }
+    for (int o = 16; o > 0; o >>= 1) mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+    if ((threadIdx.x & 31) == 0) s_min[threadIdx.x >> 5] = mn;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        float m = FLT_MAX;
+        for (int i = 0; i < (int)(blockDim.x >> 5); ++i) m = fminf(m, s_min[i]);
+        atomicMin(&st->jac_bits, float_to_ordered(m));
+    }
+}
+
+__global__ void k_loop_cond(const PairState* st, int pairs, cudaGraphConditionalHandle h) {
+    int any = 0;
+    for (int i = 0; i < pairs; ++i) any |= !st[i].done;
+    cudaGraphSetConditional(h, any ? 1u : 0u);
+}
+
+__global__ void k_begin_level(PairState* st, int pairs, int level, int reset_lambda, double lambda0) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= pairs) return;
+    PairState& s = st[i];
+    if (reset_lambda) s.lambda = lambda0;
+    s.hist_n = 0; s.L1 = 0.0; s.L2 = 0.0;
+    s.iter = 0; s.retries = 0; s.done = 0; s.status = 0; s.trace_len = 0; s.attempt = 0;
+    s.last_rejected = 0; s.iters_target = INT_MAX; s.level = level;
+    s.max_bits = 0u; s.counter = 0u; s.jac_bits = 0x7f800000;
+}
+
+__global__ void k_set_targets(PairState* st, int pairs, int iters) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= pairs) return;
+    if (st[i].status != 0) return;
+    st[i].iters_target = st[i].iter + iters;
+    st[i].done = iters <= 0;
+}
+
+// Deterministic per-pair means (fixed-order partials inside one CTA).
+__global__ void k_shifts(Batch b) {
+    __shared__ double red[32];
+    const int pair = blockIdx.x;
+    const long long n = b.g.n;
+    for (int which = 0; which < 2; ++which) {
+        const float* v = (which == 0 ? b.F : b.M) + (long long)pair * n;
+        double s = 0.0;
+        for (long long i = threadIdx.x; i < n; i += blockDim.x) s += (double)v[i];
+        const double t = block_sum(s, red);
+        if (threadIdx.x == 0) {
+            const float mean = (float)(t / (double)n);
+            if (which == 0) b.st[pair].shift_f = mean;
+            else b.st[pair].shift_m = mean;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// launch wrappers
+#define WLM_DISPATCH_R(R_, CALL)                      \
+    switch (R_) {                                     \
+        case 0: { constexpr int RR = 0; CALL; } break; \
+        case 1: { constexpr int RR = 1; CALL; } break; \
+        case 2: { constexpr int RR = 2; CALL; } break; \
+        case 3: { constexpr int RR = 3; CALL; } break; \
+        default: break;                               \
+    }
+
+void launch_lncc_fwd(const Batch& b, const LmParams& p, int mode, cudaStream_t s) {
+    const LaunchShape sh = shape_for(b.g, b.pairs, TY);
+    dim3 grid = sh.grid();
+    grid.z = b.pairs;
+    k_lncc_fwd<2><<<grid, NT, 0, s>>>(b, p, mode, sh.chunk_len);
+    ++g_kernel_launches;
+}
+
+void launch_lncc_bwd(const Batch& b, const LmParams& p, cudaStream_t s) {
+    const LaunchShape sh = shape_for(b.g, b.pairs, TY);
+    dim3 grid = sh.grid();
+    grid.z = b.pairs;
+    k_lncc_bwd<2><<<grid, NT, 0, s>>>(b, p, sh.chunk_len);
+    ++g_kernel_launches;
+}
+
+void launch_adam(const Batch& b, const LmParams& p, cudaStream_t s) {
+    dim3 grid(kNumSMs * 4, b.pairs);
+    k_adam<<<grid, 256, 0, s>>>(b, p);
+    ++g_kernel_launches;
+}
+
+void launch_step_smooth(const Batch& b, const LmParams& p, cudaStream_t s) {
+    const LaunchShape sh = shape_for(b.g, b.pairs, TY);
+    dim3 grid = sh.grid();
+    grid.z = b.pairs;
+    WLM_DISPATCH_R(p.Ru, (k_step_smooth<RR><<<grid, NT, 0, s>>>(b, p, sh.chunk_len)));
+    ++g_kernel_launches;
+}
+
+void launch_compose_smooth(const Batch& b, const LmParams& p, cudaStream_t s) {
+    const LaunchShape sh = shape_for(b.g, b.pairs, TY);
+    dim3 grid = sh.grid();
+    grid.z = b.pairs;
+    WLM_DISPATCH_R(p.Rw, (k_compose_smooth<RR><<<grid, NT, 0, s>>>(b, p, sh.chunk_len)));
+    ++g_kernel_launches;
+}
+
+void launch_jacobian_diag(const Batch& b, const LmParams& p, cudaStream_t s) {
+    dim3 grid(kNumSMs * 2, b.pairs);
+    k_jacobian_diag<<<grid, 256, 0, s>>>(b, p);
+    ++g_kernel_launches;
+}
+
+void launch_loop_cond(const Batch& b, cudaGraphConditionalHandle h, cudaStream_t s) {
+    k_loop_cond<<<1, 1, 0, s>>>(b.st, b.pairs, h);
+    ++g_kernel_launches;
+}
+
+void launch_begin_level(const Batch& b, const LmParams&, int level, int reset_lambda, double lambda0,
+                        cudaStream_t s) {
+    k_begin_level<<<cdiv(b.pairs, 128), 128, 0, s>>>(b.st, b.pairs, level, reset_lambda, lambda0);
+    ++g_kernel_launches;
+}
+
+void launch_set_targets(const Batch& b, int iters, cudaStream_t s) {
+    k_set_targets<<<cdiv(b.pairs, 128), 128, 0, s>>>(b.st, b.pairs, iters);
+    ++g_kernel_launches;
+}
+
+void launch_shifts(const Batch& b, cudaStream_t s) {
+    k_shifts<<<b.pairs, 1024, 0, s>>>(b);
+    ++g_kernel_launches;
+}
+
+// ===========================================================================
+// Standalone field operations (reference field.hpp mirror).
+
+namespace {
+__device__ __forceinline__ AxisTap axis_tap_d(double p, int n) {
+    const double fl = floor(p);
+    const int i = (int)fmax(fmin(fl, 2147483000.0), -2147483000.0);
+    AxisTap a;
+    if (n == 1) { a.i0 = a.i1 = 0; a.t = 0.f; a.outside = true; return a; }
+    const float t = (float)(p - fl);
+    if (i < 0) { a.i0 = 0; a.i1 = 1; a.t = 0.f; a.outside = true; return a; }
+    if (i > n - 1 || (i == n - 1 && t > 0.f)) { a.i0 = n - 2; a.i1 = n - 1; a.t = 1.f; a.outside = true; return a; }
+    if (i == n - 1) { a.i0 = n - 2; a.i1 = n - 1; a.t = 1.f; a.outside = false; return a; }
+    a.i0 = i; a.i1 = i + 1; a.t = t; a.outside = false;
+    return a;
+}
+
+__device__ Cell cell_at_point(const Geo& g, double px, double py, double pz) {
+    Cell c;
+    c.finite = isfinite(px) && isfinite(py) && isfinite(pz);
+    const AxisTap X = axis_tap_d(c.finite ? px : 0.0, g.nx), Y = axis_tap_d(c.finite ? py : 0.0, g.ny),
+                  Z = axis_tap_d(c.finite ? pz : 0.0, g.nz);
+    const long long r00 = (long long)g.nx * ((long long)Y.i0 + (long long)g.ny * Z.i0);
+    const long long r10 = (long long)g.nx * ((long long)Y.i1 + (long long)g.ny * Z.i0);
+    const long long r01 = (long long)g.nx * ((long long)Y.i0 + (long long)g.ny * Z.i1);
+    const long long r11 = (long long)g.nx * ((long long)Y.i1 + (long long)g.ny * Z.i1);
+    c.o000 = r00 + X.i0; c.o100 = r00 + X.i1; c.o010 = r10 + X.i0; c.o110 = r10 + X.i1;
+    c.o001 = r01 + X.i0; c.o101 = r01 + X.i1; c.o011 = r11 + X.i0; c.o111 = r11 + X.i1;
+    c.tx = X.t; c.ty = Y.t; c.tz = Z.t;
+    return c;
+}
+
+inline int grid_for(long long n, int threads) {
+    long long b = (n + threads - 1) / threads;
+    return (int)std::min<long long>(std::max<long long>(b, 1), kNumSMs * 32);
+}
+}  // namespace
+
+__global__ void k_compose(const float* __restrict__ u, const float* __restrict__ v, float eps,
+                          float* __restrict__ out, Geo g) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < g.n;
+         i += (long long)gridDim.x * blockDim.x) {
+        const int x = (int)(i % g.nx), y = (int)((i / g.nx) % g.ny), z = (int)(i / ((long long)g.nx * g.ny));
+        const float dx = eps * v[i], dy = eps * v[g.n + i], dz = eps * v[2 * g.n + i];
+        const Cell c = make_cell(g, x, y, z, dx, dy, dz);
+        out[i] = dx + cell_sample(u, c);
+        out[g.n + i] = dy + cell_sample(u + g.n, c);
+        out[2 * g.n + i] = dz + cell_sample(u + 2 * g.n, c);
+    }
+}
+
+void launch_compose(const float* u, const float* v, float eps, float* out, const Geo& g, cudaStream_t s) {
+    k_compose<<<grid_for(g.n, 256), 256, 0, s>>>(u, v, eps, out, g);
+    ++g_kernel_launches;
+}
+
+// One separable Gaussian pass along `axis` for all channels (generic radius,
+// truncated at max(1, ceil(3 sigma)) and renormalised, field.cpp:205-269).
+struct Taps {
+    int R;
+    float w[2 * 64 + 1];
+};
+
+__global__ void k_smooth_axis(const float* __restrict__ in, float* __restrict__ out, int nchan,
+                              Geo g, int axis, Taps t) {
+    const long long tot = g.n * nchan;
+    const int n = axis == 0 ? g.nx : axis == 1 ? g.ny : g.nz;
+    const long long stride = axis == 0 ? 1 : axis == 1 ? g.nx : (long long)g.nx * g.ny;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < tot;
+         i += (long long)gridDim.x * blockDim.x) {
+        const long long v = i % g.n;
+        const int p = axis == 0 ? (int)(v % g.nx) : axis == 1 ? (int)((v / g.nx) % g.ny)
+                                                              : (int)(v / ((long long)g.nx * g.ny));
+        if (n == 1) { out[i] = in[i]; continue; }
+        const int q0 = max(0, p - t.R), q1 = min(n - 1, p + t.R);
+        float num = 0.f, den = 0.f;
+        for (int q = q0; q <= q1; ++q) {
+            const float wq = t.w[q - p + t.R];
+            num = fmaf(wq, in[i + (q - p) * stride], num);
+            den += wq;
+        }
+        out[i] = num / den;
+    }
+}
+
+void launch_smooth_generic(const float* in, float* out, float* tmp, int nchan, const Geo& g,
+                           double sigma, cudaStream_t s) {
+    if (!(sigma > 0.0)) {
+        cudaMemcpyAsync(out, in, sizeof(float) * nchan * g.n, cudaMemcpyDeviceToDevice, s);
+        return;
+    }
+    Taps t;
+    t.R = std::max(1, (int)std::ceil(3.0 * sigma));
+    if (t.R > 64) t.R = 64;  // callers reject sigma > 21 (WLM_UNSUPPORTED)
+    for (int i = -t.R; i <= t.R; ++i) t.w[i + t.R] = (float)std::exp(-0.5 * (double)(i * i) / (sigma * sigma));
+    const int blocks = grid_for(g.n * nchan, 256);
+    // x: in -> out, y: out -> tmp, z: tmp -> out
+    k_smooth_axis<<<blocks, 256, 0, s>>>(in, out, nchan, g, 0, t);
+    k_smooth_axis<<<blocks, 256, 0, s>>>(out, tmp, nchan, g, 1, t);
+    k_smooth_axis<<<blocks, 256, 0, s>>>(tmp, out, nchan, g, 2, t);
+    g_kernel_launches += 3;
+}
+
+__global__ void k_warp(const float* __restrict__ M, const float* __restrict__ u, float* Mw, float* gM, Geo g) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < g.n;
+         i += (long long)gridDim.x * blockDim.x) {
+        const int x = (int)(i % g.nx), y = (int)((i / g.nx) % g.ny), z = (int)(i / ((long long)g.nx * g.ny));
+        float a, b, c;
+        Mw[i] = sample_grad(M, g, x, y, z, u[i], u[g.n + i], u[2 * g.n + i], a, b, c);
+        if (gM) { gM[i] = a; gM[g.n + i] = b; gM[2 * g.n + i] = c; }
+    }
+}
+
+void launch_warp(const float* M, const float* u, float* Mw, float* gM, const Geo& g, cudaStream_t s) {
+    k_warp<<<grid_for(g.n, 256), 256, 0, s>>>(M, u, Mw, gM, g);
+    ++g_kernel_launches;
+}
+
+__global__ void k_max_abs(const float* __restrict__ v, long long count, unsigned* out) {
+    __shared__ float sm[32];
+    float m = 0.f;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < count;
+         i += (long long)gridDim.x * blockDim.x)
+        m = fmaxf(m, fabsf(v[i]));
+    m = warp_max(m);
+    if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = m;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        float t = 0.f;
+        for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t = fmaxf(t, sm[i]);
+        atomic_max_nonneg(out, t);
+    }
+}
+
+void launch_max_abs(const float* v, long long count, unsigned* out_bits, cudaStream_t s) {
+    k_max_abs<<<grid_for(count, 256), 256, 0, s>>>(v, count, out_bits);
+    ++g_kernel_launches;
+}
+
+__global__ void k_jacdet(const float* __restrict__ u, Geo g, int* out) {
+    __shared__ float s_min[32];
+    int xl, xh, yl, yh, zl, zh;
+    interior(g.nx, xl, xh); interior(g.ny, yl, yh); interior(g.nz, zl, zh);
+    const long long cx = xh - xl + 1, cy = yh - yl + 1, cz = zh - zl + 1;
+    float mn = FLT_MAX;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < cx * cy * cz;
+         i += (long long)gridDim.x * blockDim.x) {
+        const int x = xl + (int)(i % cx), y = yl + (int)((i / cx) % cy), z = zl + (int)(i / (cx * cy));
+        mn = fminf(mn, det_at(u, g, x, y, z, 1.f));
+    }
+    for (int o = 16; o > 0; o >>= 1) mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+    if ((threadIdx.x & 31) == 0) s_min[threadIdx.x >> 5] = mn;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        float m = FLT_MAX;
+        for (int i = 0; i < (int)(blockDim.x >> 5); ++i) m = fminf(m, s_min[i]);
+        atomicMin(out, float_to_ordered(m));
+    }
+}
+
+void launch_jacdet(const float* u, const Geo& g, int* out_ordered, cudaStream_t s) {
+    k_jacdet<<<grid_for(g.n, 256), 256, 0, s>>>(u, g, out_ordered);
+    ++g_kernel_launches;
+}
+
+__global__ void k_lm_pointwise(float r, const float* __restrict__ g, float lam, float* out, long long n) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        const float a = g[i], b = g[n + i], c = g[2 * n + i];
+        const float s = -r / (fmaf(a, a, fmaf(b, b, c * c)) + lam);
+        out[i] = s * a; out[n + i] = s * b; out[2 * n + i] = s * c;
+    }
+}
+
+void launch_lm_pointwise(double r, const float* g, double lambda, float* out, long long n, cudaStream_t s) {
+    k_lm_pointwise<<<grid_for(n, 256), 256, 0, s>>>((float)r, g, (float)lambda, out, n);
+    ++g_kernel_launches;
+}
+
+__global__ void k_nonfinite(const float* __restrict__ v, long long count, int* flag) {
+    int bad = 0;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < count;
+         i += (long long)gridDim.x * blockDim.x)
+        bad |= !isfinite(v[i]);
+    bad = __syncthreads_or(bad);
+    if (threadIdx.x == 0 && bad) atomicOr(flag, 1);
+}
+
+void launch_nonfinite(const float* v, long long count, int* flag, cudaStream_t s) {
+    k_nonfinite<<<grid_for(count, 256), 256, 0, s>>>(v, count, flag);
+    ++g_kernel_launches;
+}
+
+__global__ void k_downsample(const float* __restrict__ sm, Geo g, int f, float* out, Geo gd) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < gd.n;
+         i += (long long)gridDim.x * blockDim.x) {
+        const int x = (int)(i % gd.nx), y = (int)((i / gd.nx) % gd.ny), z = (int)(i / ((long long)gd.nx * gd.ny));
+        out[i] = sm[g.at(x * f, y * f, z * f)];
+    }
+}
+
+void launch_downsample(const float* smoothed, const Geo& g, int f, float* out, const Geo& gd, cudaStream_t s) {
+    k_downsample<<<grid_for(gd.n, 256), 256, 0, s>>>(smoothed, g, f, out, gd);
+    ++g_kernel_launches;
+}
+
+__global__ void k_upsample(const float* __restrict__ u, Geo g, Geo gd, double scale, float* out) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < gd.n;
+         i += (long long)gridDim.x * blockDim.x) {
+        const int x = (int)(i % gd.nx), y = (int)((i / gd.nx) % gd.ny), z = (int)(i / ((long long)gd.nx * gd.ny));
+        const Cell c = cell_at_point(g, x / scale, y / scale, z / scale);
+        const float sc = (float)scale;
+        out[i] = sc * cell_sample(u, c);
+        out[gd.n + i] = sc * cell_sample(u + g.n, c);
+        out[2 * gd.n + i] = sc * cell_sample(u + 2 * g.n, c);
+    }
+}
+
+void launch_upsample(const float* u, const Geo& g, const Geo& gd, float scale, float* out, cudaStream_t s) {
+    k_upsample<<<grid_for(gd.n, 256), 256, 0, s>>>(u, g, gd, (double)scale, out);
+    ++g_kernel_launches;
+}
+
+__global__ void k_sample_points(const float* __restrict__ u, Geo g, const double* pts, long long npts, double* out) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < npts;
+         i += (long long)gridDim.x * blockDim.x) {
+        const Cell c = cell_at_point(g, pts[3 * i], pts[3 * i + 1], pts[3 * i + 2]);
+        for (int ch = 0; ch < 3; ++ch) out[3 * i + ch] = (double)cell_sample(u + ch * g.n, c);
+    }
+}
+
+void launch_sample_points(const float* u, const Geo& g, const double* pts, long long npts, double* out,
+                          cudaStream_t s) {
+    k_sample_points<<<grid_for(npts, 256), 256, 0, s>>>(u, g, pts, npts, out);
+    ++g_kernel_launches;
+}
+
+__global__ void k_aos_to_soa(const double* __restrict__ in, float* __restrict__ out, long long n, int nchan) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n * nchan;
+         i += (long long)gridDim.x * blockDim.x) {
+        const long long v = i / nchan;
+        const int c = (int)(i % nchan);
+        out[(long long)c * n + v] = (float)in[i];
+    }
+}
+
+__global__ void k_soa_to_aos(const float* __restrict__ in, double* __restrict__ out, long long n, int nchan) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n * nchan;
+         i += (long long)gridDim.x * blockDim.x) {
+        const long long v = i / nchan;
+        const int c = (int)(i % nchan);
+        out[i] = (double)in[(long long)c * n + v];
+    }
+}
+
+void launch_aos_to_soa(const double* in, float* out, long long n, int nchan, cudaStream_t s) {
+    k_aos_to_soa<<<grid_for(n * nchan, 256), 256, 0, s>>>(in, out, n, nchan);
+    ++g_kernel_launches;
+}
+
+void launch_soa_to_aos(const float* in, double* out, long long n, int nchan, cudaStream_t s) {
+    k_soa_to_aos<<<grid_for(n * nchan, 256), 256, 0, s>>>(in, out, n, nchan);
+    ++g_kernel_launches;
+}
+
+}  // namespace wlm

@@ -1,0 +1,122 @@
+// kernels.cuh -- device state and launch wrappers of the LM hot path.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "common.cuh"
+#include "wlm.h"
+
+namespace wlm {
+
+// Per-pair device-resident optimizer state.  Mutated only by the evaluation
+// kernel's last block (one writer), read by the other kernels, so an
+// iteration needs no host round trip.
+struct PairState {
+    double lambda, L1, L2;   // LmState
+    double r_cur, lncc_cur;  // residual at the accepted warp
+    double r_try, lncc_try;  // residual at the latest attempt
+    int hist_n;              // accepted losses held (0..2)
+    int cur;                 // which warp buffer holds the accepted warp
+    int last_rejected;       // latest attempt rejected -> gradient kept
+    int iter;                // accepted iterations at this level
+    int retries;             // rejections in the current iteration
+    int done;                // reached iters_target (or aborted)
+    int status;              // wlm_status of the pair
+    int trace_len;
+    int attempt;             // attempts at this level (scripted-loss index)
+    int iters_target;
+    int level;
+    unsigned max_bits;       // max |dU_s| as ordered bits (K3 -> K4)
+    unsigned counter;        // last-block election counter (K1)
+    int jac_bits;            // min det(I + grad eps dU_s), ordered int
+    float shift_f, shift_m;  // per-pair intensity shift for the fp32 moments
+};
+
+// Launch-invariant parameters of one engine (passed by value).
+struct LmParams {
+    double mu_plus, mu_minus, lambda_max, tau;
+    double target, step_floor;
+    double adam_b1, adam_b2, adam_eps, adam_lr, gd_lr;
+    int rejection, max_retries, optimizer, log_jacobian;
+    int trace_cap;
+    int script_n;
+    wlm_step_log* trace;   // [pair][trace_cap]
+    const double* script;  // [pair][script_n] or null
+    int Ru, Rw;            // smoothing radii (update, warp); 0 = identity
+    float wu[8], ww[8];    // half-kernels w[|d|]
+    float wu_full, ww_full;
+    int radius;            // LNCC window radius (template-dispatched: 2 only in v1)
+};
+
+// Buffers of a batch of `pairs` registrations of identical geometry.
+struct Batch {
+    Geo g;
+    int pairs;
+    const float* F;   // [pair][n]
+    const float* M;   // [pair][n]
+    float* U;         // [pair][2][3][n] ping-pong warps
+    float* ABE;       // [pair][3][n]  LNCC window coefficients A, B, E
+    float* G;         // [pair][3][n]  gradient g, Adam step in place
+    float* VS;        // [pair][3][n]  smoothed step dU_s
+    float* AM;        // [pair][3][n]  Adam first moment (or null)
+    float* AV;        // [pair][3][n]  Adam second moment (or null)
+    PairState* st;    // [pair]
+    double* partials; // [pair][max_blocks]
+    int max_blocks;
+};
+
+struct LaunchShape {
+    int tiles_x, tiles_y, chunks, chunk_len;
+    dim3 grid() const;
+};
+LaunchShape shape_for(const Geo& g, int pairs, int ty);
+
+// K1: warp + LNCC window moments + coefficients + sum(rho); last block runs
+// the loss/damping/rejection state machine.  mode 0 evaluates the accepted
+// warp (level start), mode 1 the attempt in the other buffer.
+void launch_lncc_fwd(const Batch& b, const LmParams& p, int mode, cudaStream_t s);
+// K2: adjoint window sums -> dr/dMw -> g = dr/dMw * gradM(x + u).
+void launch_lncc_bwd(const Batch& b, const LmParams& p, cudaStream_t s);
+// Adam moment update (pointwise), writes the Adam step into G.
+void launch_adam(const Batch& b, const LmParams& p, cudaStream_t s);
+// K3: LM step (or GD / pass-through) + Gaussian(sigma_update) + max|.|.
+void launch_step_smooth(const Batch& b, const LmParams& p, cudaStream_t s);
+// K4: compositive resample with eps from the max + Gaussian(sigma_warp).
+void launch_compose_smooth(const Batch& b, const LmParams& p, cudaStream_t s);
+// Optional diagnostic: min det(I + grad(eps dU_s)) over the interior.
+void launch_jacobian_diag(const Batch& b, const LmParams& p, cudaStream_t s);
+// WHILE-loop condition: any pair not done.
+void launch_loop_cond(const Batch& b, cudaGraphConditionalHandle h, cudaStream_t s);
+// Per-pair state reset at level start.
+void launch_begin_level(const Batch& b, const LmParams& p, int level, int reset_lambda,
+                        double lambda0, cudaStream_t s);
+void launch_set_targets(const Batch& b, int iters, cudaStream_t s);
+// Intensity shifts (means of F and M per pair), deterministic.
+void launch_shifts(const Batch& b, cudaStream_t s);
+
+// ---- standalone field ops (fp32 SoA device buffers) ----
+void launch_compose(const float* u, const float* v, float eps, float* out, const Geo& g,
+                    cudaStream_t s);
+void launch_smooth_generic(const float* in, float* out, float* tmp, int nchan, const Geo& g,
+                           double sigma, cudaStream_t s);
+void launch_warp(const float* M, const float* u, float* Mw, float* gM, const Geo& g,
+                 cudaStream_t s);
+void launch_max_abs(const float* v, long long count, unsigned* out_bits, cudaStream_t s);
+void launch_jacdet(const float* u, const Geo& g, int* out_ordered, cudaStream_t s);
+void launch_lm_pointwise(double r, const float* g, double lambda, float* out, long long n,
+                         cudaStream_t s);
+void launch_nonfinite(const float* v, long long count, int* flag, cudaStream_t s);
+void launch_downsample(const float* smoothed, const Geo& g, int f, float* out, const Geo& gd,
+                       cudaStream_t s);
+void launch_upsample(const float* u, const Geo& g, const Geo& gd, float scale, float* out,
+                     cudaStream_t s);
+void launch_sample_points(const float* u, const Geo& g, const double* pts, long long npts,
+                          double* out, cudaStream_t s);
+// AoS fp64 <-> SoA fp32 conversions.
+void launch_aos_to_soa(const double* in, float* out, long long n, int nchan, cudaStream_t s);
+void launch_soa_to_aos(const float* in, double* out, long long n, int nchan, cudaStream_t s);
+
+extern uint64_t g_kernel_launches;  // per-process count (ctx keeps its own)
+
+}  // namespace wlm

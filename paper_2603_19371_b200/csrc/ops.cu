@@ -1,0 +1,381 @@
+// ops.cu -- host-buffer mirror of the reference API (fp64 AoS in/out, like a
+// by-value warplm:: call) and the register() pyramid driver.  Each entry
+// point uploads, converts to the device layout (fp32 SoA), runs sm_100a
+// kernels, and converts back.  No CPU compute path exists.
+#include <cmath>
+#include <limits>
+#include <vector>
+
+#include "internal.cuh"
+
+using namespace wlm;
+
+namespace {
+
+// fp64 AoS host -> fp32 SoA device.
+DevBuf<float> upload_soa(wlm_ctx* ctx, const double* host, size_t n, int nchan) {
+    DevBuf<double> tmp(ctx, n * nchan);
+    CK(cudaMemcpyAsync(tmp.p, host, sizeof(double) * n * nchan, cudaMemcpyHostToDevice, ctx->stream));
+    DevBuf<float> out(ctx, n * nchan);
+    launch_aos_to_soa(tmp.p, out.p, (long long)n, nchan, ctx->stream);
+    CK(cudaStreamSynchronize(ctx->stream));
+    return out;
+}
+
+void download_aos(wlm_ctx* ctx, const float* dev, size_t n, int nchan, double* host) {
+    DevBuf<double> tmp(ctx, n * nchan);
+    launch_soa_to_aos(dev, tmp.p, (long long)n, nchan, ctx->stream);
+    CK(cudaMemcpyAsync(host, tmp.p, sizeof(double) * n * nchan, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+}
+
+float read_max(wlm_ctx* ctx, const float* v, long long count) {
+    DevBuf<unsigned> bits(ctx, 1);
+    CK(cudaMemsetAsync(bits.p, 0, sizeof(unsigned), ctx->stream));
+    launch_max_abs(v, count, bits.p, ctx->stream);
+    unsigned h = 0;
+    CK(cudaMemcpyAsync(&h, bits.p, sizeof(unsigned), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    float f;
+    std::memcpy(&f, &h, 4);
+    return f;
+}
+
+double read_jacdet(wlm_ctx* ctx, const float* u, const Geo& g) {
+    DevBuf<int> o(ctx, 1);
+    const int inf_bits = 0x7f800000;
+    CK(cudaMemcpyAsync(o.p, &inf_bits, sizeof(int), cudaMemcpyHostToDevice, ctx->stream));
+    launch_jacdet(u, g, o.p, ctx->stream);
+    int h = 0;
+    CK(cudaMemcpyAsync(&h, o.p, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    return (double)ordered_to_float(h);
+}
+
+wlm_status bad(wlm_ctx* ctx, wlm_status s, const char* msg) {
+    set_err(ctx, msg);
+    return s;
+}
+
+}  // namespace
+
+extern "C" {
+
+wlm_status wlm_warp_volume(wlm_ctx* ctx, const double* M, const double* u, wlm_dims d, double* Mw,
+                           double* gradM) {
+    if (!M || !u || !Mw || !valid_dims(d)) return bad(ctx, WLM_INVALID_ARG, "warp_volume: bad args");
+    return run(ctx, [&] {
+        const size_t n = nvox(d);
+        const Geo g = make_geo(d);
+        DevBuf<float> dM = upload_soa(ctx, M, n, 1), du = upload_soa(ctx, u, n, 3);
+        DevBuf<float> dw(ctx, n), dg(ctx, gradM ? 3 * n : 0);
+        launch_warp(dM.p, du.p, dw.p, gradM ? dg.p : nullptr, g, ctx->stream);
+        download_aos(ctx, dw.p, n, 1, Mw);
+        if (gradM) download_aos(ctx, dg.p, n, 3, gradM);
+    });
+}
+
+wlm_status wlm_sample_field_points(wlm_ctx* ctx, const double* u, wlm_dims d, const double* pts,
+                                   size_t npts, double* out) {
+    if (!u || !pts || !out || !valid_dims(d)) return bad(ctx, WLM_INVALID_ARG, "sample_field: bad args");
+    return run(ctx, [&] {
+        const size_t n = nvox(d);
+        DevBuf<float> du = upload_soa(ctx, u, n, 3);
+        DevBuf<double> dp(ctx, 3 * npts), dout(ctx, 3 * npts);
+        CK(cudaMemcpyAsync(dp.p, pts, sizeof(double) * 3 * npts, cudaMemcpyHostToDevice, ctx->stream));
+        launch_sample_points(du.p, make_geo(d), dp.p, (long long)npts, dout.p, ctx->stream);
+        CK(cudaMemcpyAsync(out, dout.p, sizeof(double) * 3 * npts, cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+// compose_warp (field.cpp:123-142): dimension mismatch -> WLM_DIM_MISMATCH
+// (the reference throws std::invalid_argument, field.cpp:124-126).
+wlm_status wlm_compose_warp(wlm_ctx* ctx, const double* u, wlm_dims du, const double* v, wlm_dims dv,
+                            double eps, double* out) {
+    if (!u || !v || !out || !valid_dims(du) || !valid_dims(dv))
+        return bad(ctx, WLM_INVALID_ARG, "compose_warp: bad args");
+    if (!same_dims(du, dv)) return bad(ctx, WLM_DIM_MISMATCH, "compose_warp: dimension mismatch");
+    return run(ctx, [&] {
+        const size_t n = nvox(du);
+        DevBuf<float> a = upload_soa(ctx, u, n, 3), b = upload_soa(ctx, v, n, 3), o(ctx, 3 * n);
+        launch_compose(a.p, b.p, (float)eps, o.p, make_geo(du), ctx->stream);
+        download_aos(ctx, o.p, n, 3, out);
+    });
+}
+
+wlm_status wlm_max_abs_component(wlm_ctx* ctx, const double* v, wlm_dims d, double* out) {
+    if (!v || !out || !valid_dims(d)) return bad(ctx, WLM_INVALID_ARG, "max_abs_component: bad args");
+    return run(ctx, [&] {
+        const size_t n = nvox(d);
+        DevBuf<float> a = upload_soa(ctx, v, n, 3);
+        *out = (double)read_max(ctx, a.p, (long long)(3 * n));
+    });
+}
+
+// normalize_step (field.cpp:150-155): target outside (0, 0.5) -> INVALID_ARG.
+wlm_status wlm_normalize_step(wlm_ctx* ctx, const double* v, wlm_dims d, double target, double floor_,
+                              double* eps) {
+    if (!(target > 0.0 && target < 0.5))
+        return bad(ctx, WLM_INVALID_ARG, "normalize_step: target_max_disp must lie in (0, 0.5)");
+    double m = 0.0;
+    wlm_status s = wlm_max_abs_component(ctx, v, d, &m);
+    if (s != WLM_OK) return s;
+    *eps = target / std::max(m, floor_);
+    return WLM_OK;
+}
+
+wlm_status wlm_jacobian_det_min(wlm_ctx* ctx, const double* u, wlm_dims d, double* out) {
+    if (!u || !out || !valid_dims(d)) return bad(ctx, WLM_INVALID_ARG, "jacobian_det_min: bad args");
+    if (d.nx < 2 || d.ny < 2 || d.nz < 2)
+        return bad(ctx, WLM_INVALID_ARG, "jacobian_det_min: dims must be >= 2 per axis");
+    return run(ctx, [&] {
+        DevBuf<float> a = upload_soa(ctx, u, nvox(d), 3);
+        *out = read_jacdet(ctx, a.p, make_geo(d));
+    });
+}
+
+static wlm_status smooth_common(wlm_ctx* ctx, const double* in, wlm_dims d, double sigma, double* out,
+                                int nchan) {
+    if (!in || !out || !valid_dims(d)) return bad(ctx, WLM_INVALID_ARG, "gaussian_smooth: bad args");
+    if (sigma > 21.0) return bad(ctx, WLM_UNSUPPORTED, "gaussian_smooth: sigma > 21 (radius > 64)");
+    return run(ctx, [&] {
+        const size_t n = nvox(d);
+        DevBuf<float> a = upload_soa(ctx, in, n, nchan), o(ctx, nchan * n), t(ctx, nchan * n);
+        launch_smooth_generic(a.p, o.p, t.p, nchan, make_geo(d), sigma, ctx->stream);
+        download_aos(ctx, o.p, n, nchan, out);
+    });
+}
+
+wlm_status wlm_gaussian_smooth_vol(wlm_ctx* ctx, const double* in, wlm_dims d, double sigma, double* out) {
+    return smooth_common(ctx, in, d, sigma, out, 1);
+}
+wlm_status wlm_gaussian_smooth_field(wlm_ctx* ctx, const double* in, wlm_dims d, double sigma, double* out) {
+    return smooth_common(ctx, in, d, sigma, out, 3);
+}
+
+namespace {
+__global__ void k_nonfinite_d(const double* v, long long n, int* flag) {
+    int bad_ = 0;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x)
+        bad_ |= !isfinite(v[i]);
+    bad_ = __syncthreads_or(bad_);
+    if (threadIdx.x == 0 && bad_) atomicOr(flag, 1);
+}
+}  // namespace
+
+wlm_status wlm_all_finite(wlm_ctx* ctx, const double* data, size_t count, int* out) {
+    if (!data || !out) return bad(ctx, WLM_INVALID_ARG, "all_finite: bad args");
+    return run(ctx, [&] {
+        DevBuf<double> a(ctx, count);
+        DevBuf<int> f(ctx, 1);
+        CK(cudaMemcpyAsync(a.p, data, sizeof(double) * count, cudaMemcpyHostToDevice, ctx->stream));
+        CK(cudaMemsetAsync(f.p, 0, sizeof(int), ctx->stream));
+        const long long blocks = std::min<long long>(148 * 16, std::max<long long>(1, ((long long)count + 255) / 256));
+        k_nonfinite_d<<<(int)blocks, 256, 0, ctx->stream>>>(a.p, (long long)count, f.p);
+        ++g_kernel_launches;
+        int h = 0;
+        CK(cudaMemcpyAsync(&h, f.p, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+        *out = h ? 0 : 1;
+    });
+}
+
+// residual_lncc: the engine's own K1/K2 kernels on a one-pair
+// batch, so this entry point exercises exactly the hot-path code.
+wlm_status wlm_residual_lncc(wlm_ctx* ctx, const double* F, const double* M, const double* u, wlm_dims d,
+                             int radius, double* r, double* lncc, double* g) {
+    if (!F || !M || !u || !valid_dims(d)) return bad(ctx, WLM_INVALID_ARG, "residual_lncc: bad args");
+    wlm_reg_config cfg;
+    wlm_default_reg_config(&cfg);
+    cfg.lncc_radius = radius;
+    cfg.nlevels = 1; cfg.factors[0] = 1; cfg.iters[0] = 0;
+    wlm_engine* e = nullptr;
+    wlm_status s = wlm_engine_create(ctx, d, 1, &cfg, &e);
+    if (s != WLM_OK) return s;
+    s = run(ctx, [&] {
+        const size_t n = nvox(d);
+        std::vector<float> hf(n), hm(n);
+        for (size_t i = 0; i < n; ++i) { hf[i] = (float)F[i]; hm[i] = (float)M[i]; }
+        CK(cudaMemcpyAsync(e->F.p, hf.data(), sizeof(float) * n, cudaMemcpyHostToDevice, ctx->stream));
+        CK(cudaMemcpyAsync(e->M.p, hm.data(), sizeof(float) * n, cudaMemcpyHostToDevice, ctx->stream));
+        launch_shifts(e->B, ctx->stream);
+        DevBuf<float> du = upload_soa(ctx, u, n, 3);
+        copy_warps_in(e, du.p, 0);
+        launch_begin_level(e->B, e->P, 0, 1, cfg.lm.lambda0, ctx->stream);
+        launch_lncc_fwd(e->B, e->P, 0, ctx->stream);
+        if (g) {
+            launch_lncc_bwd(e->B, e->P, ctx->stream);
+            download_aos(ctx, e->G.p, n, 3, g);
+        }
+        const std::vector<PairState> st = read_states(e);
+        if (r) *r = st[0].r_cur;
+        if (lncc) *lncc = st[0].lncc_cur;
+        if (st[0].status) throw Fail{(wlm_status)st[0].status};
+    });
+    wlm_engine_destroy(e);
+    return s;
+}
+
+wlm_status wlm_lm_step_pointwise(wlm_ctx* ctx, double r, const double* g, wlm_dims d, double lambda,
+                                 double* out) {
+    if (!g || !out || !valid_dims(d) || !(lambda > 0.0))
+        return bad(ctx, WLM_INVALID_ARG, "lm_step_pointwise: bad args (lambda > 0)");
+    return run(ctx, [&] {
+        const size_t n = nvox(d);
+        DevBuf<float> a = upload_soa(ctx, g, n, 3), o(ctx, 3 * n);
+        launch_lm_pointwise(r, a.p, lambda, o.p, (long long)n, ctx->stream);
+        download_aos(ctx, o.p, n, 3, out);
+    });
+}
+
+// Scalar state updates: the same fp64 arithmetic the
+// device state machine runs inside the evaluation kernel.
+void wlm_update_damping(wlm_lm_state* s, double loss_new, const wlm_lm_config* c) {
+    const bool badstep = s->hist_n == 0 || loss_new > s->L1;
+    double lam = badstep ? c->mu_plus * s->lambda : c->mu_minus * s->lambda;
+    if (c->lambda_max > 0.0 && std::isfinite(c->lambda_max)) lam = std::min(lam, c->lambda_max);
+    s->lambda = std::max(lam, 1e-12);
+    s->L2 = s->L1;
+    s->L1 = loss_new;
+    s->hist_n = std::min(s->hist_n + 1, 2);
+}
+
+int wlm_rejection_test(double loss_new, double L1, double L2, double tau) {
+    return (loss_new - L1) > tau * std::fabs(L1 - L2) ? 1 : 0;
+}
+
+static wlm_dims level_dims(wlm_dims d, int f) {
+    return wlm_dims{(d.nx + f - 1) / f, (d.ny + f - 1) / f, (d.nz + f - 1) / f};
+}
+
+// downsample: Gaussian sigma = 0.5 f, then stride f.
+wlm_status wlm_downsample(wlm_ctx* ctx, const double* vol, wlm_dims d, int factor, double* out,
+                          wlm_dims* out_dims) {
+    if (!vol || !out || !valid_dims(d)) return bad(ctx, WLM_INVALID_ARG, "downsample: bad args");
+    if (factor < 1) return bad(ctx, WLM_INVALID_ARG, "downsample: factor < 1");
+    const wlm_dims nd = level_dims(d, factor);
+    if (out_dims) *out_dims = nd;
+    return run(ctx, [&] {
+        const size_t n = nvox(d);
+        DevBuf<float> a = upload_soa(ctx, vol, n, 1);
+        if (factor == 1) { download_aos(ctx, a.p, n, 1, out); return; }
+        DevBuf<float> sm(ctx, n), t(ctx, n), o(ctx, nvox(nd));
+        launch_smooth_generic(a.p, sm.p, t.p, 1, make_geo(d), 0.5 * factor, ctx->stream);
+        launch_downsample(sm.p, make_geo(d), factor, o.p, make_geo(nd), ctx->stream);
+        download_aos(ctx, o.p, nvox(nd), 1, out);
+    });
+}
+
+// upsample_warp: trilinear at x / scale, values * scale.
+wlm_status wlm_upsample_warp(wlm_ctx* ctx, const double* u, wlm_dims d, wlm_dims nd, double scale,
+                             double* out) {
+    if (!u || !out || !valid_dims(d) || !valid_dims(nd) || !(scale > 0.0))
+        return bad(ctx, WLM_INVALID_ARG, "upsample_warp: invalid dims");
+    return run(ctx, [&] {
+        DevBuf<float> a = upload_soa(ctx, u, nvox(d), 3), o(ctx, 3 * nvox(nd));
+        launch_upsample(a.p, make_geo(d), make_geo(nd), (float)scale, o.p, ctx->stream);
+        download_aos(ctx, o.p, nvox(nd), 3, out);
+    });
+}
+
+size_t wlm_state_bytes(int optimizer, wlm_dims d, int elem_bytes) {
+    if (optimizer == WLM_OPT_ADAM) return 2 * 3 * nvox(d) * (size_t)elem_bytes;  // m, v fields
+    if (optimizer == WLM_OPT_LM) return sizeof(wlm_lm_state) + sizeof(wlm_lm_config);
+    return 0;
+}
+
+// register: coarse -> fine on the device.  Level
+// images are Gaussian-downsampled from the full-resolution device copies, the
+// warp is inherited with upsample_warp, lambda carries over, the loss history
+// resets.  Within a level the iterations run as CUDA graphs with no host
+// synchronisation; the trace is read back once per level.
+wlm_status wlm_register(wlm_ctx* ctx, const float* F, const float* M, wlm_dims d, const wlm_reg_config* cfg,
+                        double* warp_out, wlm_step_log* trace, size_t cap, size_t* len, double* jac_final) {
+    if (!F || !M || !cfg || !warp_out || !valid_dims(d)) return bad(ctx, WLM_INVALID_ARG, "register: bad args");
+    if (cfg->nlevels < 1 || cfg->nlevels > WLM_MAX_LEVELS || cfg->factors[cfg->nlevels - 1] != 1)
+        return bad(ctx, WLM_INVALID_ARG, "register: schedule must end at factor 1");
+    for (int l = 0; l < cfg->nlevels; ++l) {
+        if (cfg->factors[l] < 1 || cfg->iters[l] < 0 || (l > 0 && cfg->factors[l] >= cfg->factors[l - 1]))
+            return bad(ctx, WLM_INVALID_ARG, "register: factors must strictly decrease to 1");
+        if (cfg->factors[l] > 42) return bad(ctx, WLM_UNSUPPORTED, "register: factor > 42");
+    }
+    if (len) *len = 0;
+    ctx->peak_bytes = ctx->cur_bytes;
+    size_t used = 0;
+    wlm_status result = WLM_OK;
+    wlm_status s = run(ctx, [&] {
+        const size_t n = nvox(d);
+        const Geo g0 = make_geo(d);
+        DevBuf<float> F0(ctx, n), M0(ctx, n);
+        CK(cudaMemcpyAsync(F0.p, F, sizeof(float) * n, cudaMemcpyHostToDevice, ctx->stream));
+        CK(cudaMemcpyAsync(M0.p, M, sizeof(float) * n, cudaMemcpyHostToDevice, ctx->stream));
+        wlm_engine* prev = nullptr;
+        for (int l = 0; l < cfg->nlevels; ++l) {
+            const int f = cfg->factors[l];
+            const wlm_dims ld = level_dims(d, f);
+            wlm_engine* e = nullptr;
+            wlm_status es = wlm_engine_create(ctx, ld, 1, cfg, &e);
+            if (es != WLM_OK) { if (prev) wlm_engine_destroy(prev); throw Fail{es}; }
+            if (f == 1) {
+                CK(cudaMemcpyAsync(e->F.p, F0.p, sizeof(float) * n, cudaMemcpyDeviceToDevice, ctx->stream));
+                CK(cudaMemcpyAsync(e->M.p, M0.p, sizeof(float) * n, cudaMemcpyDeviceToDevice, ctx->stream));
+            } else {
+                DevBuf<float> sm(ctx, n), t(ctx, n);
+                launch_smooth_generic(F0.p, sm.p, t.p, 1, g0, 0.5 * f, ctx->stream);
+                launch_downsample(sm.p, g0, f, e->F.p, e->g, ctx->stream);
+                launch_smooth_generic(M0.p, sm.p, t.p, 1, g0, 0.5 * f, ctx->stream);
+                launch_downsample(sm.p, g0, f, e->M.p, e->g, ctx->stream);
+                CK(cudaStreamSynchronize(ctx->stream));
+            }
+            launch_shifts(e->B, ctx->stream);
+            if (prev) {
+                const std::vector<PairState> ps = read_states(prev);
+                const float* up = prev->U.p + (size_t)ps[0].cur * 3 * (size_t)prev->g.n;
+                launch_upsample(up, prev->g, e->g, (float)cfg->factors[l - 1] / (float)f, e->U.p, ctx->stream);
+                // carry lambda: copy the whole state, then reset history
+                CK(cudaMemcpyAsync(e->st.p, prev->st.p, sizeof(PairState), cudaMemcpyDeviceToDevice, ctx->stream));
+                CK(cudaStreamSynchronize(ctx->stream));
+                wlm_engine_destroy(prev);
+                prev = nullptr;
+                // the upsampled warp is in buffer 0
+                PairState hs = ps[0];
+                hs.cur = 0;
+                CK(cudaMemcpyAsync(e->st.p, &hs, sizeof(PairState), cudaMemcpyHostToDevice, ctx->stream));
+                launch_shifts(e->B, ctx->stream);
+                launch_begin_level(e->B, e->P, l, 0, cfg->lm.lambda0, ctx->stream);
+            } else {
+                launch_begin_level(e->B, e->P, l, 1, cfg->lm.lambda0, ctx->stream);
+            }
+            launch_lncc_fwd(e->B, e->P, 0, ctx->stream);
+            const uint64_t before = g_kernel_launches;
+            es = wlm_engine_iterate(e, cfg->iters[l]);
+            (void)before;
+            if (es != WLM_OK) { wlm_engine_destroy(e); throw Fail{es}; }
+            const std::vector<PairState> ps = read_states(e);
+            const size_t rows = std::min((size_t)ps[0].trace_len, cap > used ? cap - used : 0);
+            if (rows && trace)
+                CK(cudaMemcpy(trace + used, e->trace.p, sizeof(wlm_step_log) * rows, cudaMemcpyDeviceToHost));
+            used += rows;
+            if (len) *len = used;
+            if (ps[0].status != 0) {
+                result = (wlm_status)ps[0].status;
+                set_err(ctx, "register: non-finite loss, aborted with partial trace (SPEC.md:366)");
+                wlm_engine_destroy(e);
+                return;
+            }
+            prev = e;
+        }
+        const std::vector<PairState> ps = read_states(prev);
+        const float* uf = prev->U.p + (size_t)ps[0].cur * 3 * n;
+        download_aos(ctx, uf, n, 3, warp_out);
+        if (jac_final) *jac_final = d.nx >= 2 && d.ny >= 2 && d.nz >= 2 ? read_jacdet(ctx, uf, g0)
+                                                                        : std::numeric_limits<double>::quiet_NaN();
+        wlm_engine_destroy(prev);
+    });
+    if (s != WLM_OK) return s;
+    return result;
+}
+
+}  // extern "C"

@@ -1,0 +1,125 @@
+"""Device-resident batched LM engine (wlm_engine_* in include/wlm.h).
+
+A batch of independent registrations of identical dims stays in HBM; one
+``step()`` is one lm_iterate attempt for every pair (K2 gradient, K3 LM step
++ smoothing + max, K4 compositive resample + smoothing, K1 warp + LNCC +
+device-side damping/rejection), captured as a CUDA graph.  Inputs may be
+host numpy arrays or device pointers (e.g. ``torch.Tensor.data_ptr()``).
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from ._lib import Dims, LmState, RegConfig, StepLog, load
+from .warplm import Context, default_context, reg_config, trace_rows
+
+
+class Engine:
+    def __init__(self, shape, pairs=1, cfg: RegConfig | None = None, ctx: Context | None = None):
+        self.ctx = ctx or default_context()
+        self.lib = load()
+        self.shape = tuple(int(s) for s in shape)  # (nz, ny, nx)
+        self.pairs = int(pairs)
+        self.cfg = cfg or reg_config()
+        nz, ny, nx = self.shape
+        h = C.c_void_p()
+        self.ctx.check(self.lib.wlm_engine_create(self.ctx.h, Dims(nx, ny, nz), self.pairs,
+                                                  C.byref(self.cfg), C.byref(h)))
+        self.h = h
+
+    @property
+    def nvox(self):
+        nz, ny, nx = self.shape
+        return nx * ny * nz
+
+    def _chk(self, st):
+        self.ctx.check(st)
+
+    @staticmethod
+    def _ptr(a):
+        """(pointer, is_host) for a numpy array or a CUDA tensor / int pointer."""
+        if isinstance(a, np.ndarray):
+            return a.ctypes.data, 1
+        if hasattr(a, "data_ptr"):
+            return a.data_ptr(), 0 if a.is_cuda else 1
+        return int(a), 0
+
+    def load(self, F, M):
+        """F, M: (pairs, nz, ny, nx) float32 (host numpy or device tensor)."""
+        if isinstance(F, np.ndarray):
+            F = np.ascontiguousarray(F, dtype=np.float32)
+            M = np.ascontiguousarray(M, dtype=np.float32)
+        pf, hf = self._ptr(F)
+        pm, _ = self._ptr(M)
+        self._keep = (F, M)
+        self._chk(self.lib.wlm_engine_load(self.h, pf, pm, hf))
+
+    def set_warp(self, u=None):
+        """u: (pairs, 3, nz, ny, nx) float32 SoA or None for the identity."""
+        if u is None:
+            self._chk(self.lib.wlm_engine_set_warp(self.h, None, 1))
+            return
+        if isinstance(u, np.ndarray):
+            u = np.ascontiguousarray(u, dtype=np.float32)
+        p, host = self._ptr(u)
+        self._chk(self.lib.wlm_engine_set_warp(self.h, p, host))
+        self.ctx.synchronize()
+
+    def get_warp(self):
+        out = np.empty((self.pairs, 3) + self.shape, np.float32)
+        self._chk(self.lib.wlm_engine_get_warp(self.h, out.ctypes.data, 1))
+        return out
+
+    def get_warp_device(self, tensor):
+        self._chk(self.lib.wlm_engine_get_warp(self.h, tensor.data_ptr(), 0))
+
+    def begin_level(self, level=0):
+        self._chk(self.lib.wlm_engine_begin_level(self.h, int(level)))
+
+    def iterate(self, iters):
+        self._chk(self.lib.wlm_engine_iterate(self.h, int(iters)))
+
+    def step(self):
+        self._chk(self.lib.wlm_engine_step(self.h))
+
+    def state(self, pair=0):
+        st = LmState()
+        r, ln = C.c_double(), C.c_double()
+        it = C.c_int()
+        self._chk(self.lib.wlm_engine_state(self.h, pair, C.byref(st), C.byref(r), C.byref(ln),
+                                            C.byref(it)))
+        return dict(lam=st.lam, hist_n=st.hist_n, L1=st.L1, L2=st.L2, r=r.value, lncc=ln.value,
+                    iters=it.value)
+
+    def trace(self, pair=0, cap=100000):
+        rows = (StepLog * cap)()
+        n = C.c_size_t()
+        self._chk(self.lib.wlm_engine_trace(self.h, pair, rows, cap, C.byref(n)))
+        return trace_rows(rows[i] for i in range(n.value))
+
+    def buffers(self):
+        ptrs = [C.c_void_p() for _ in range(5)]
+        self._chk(self.lib.wlm_engine_buffers(self.h, *[C.byref(p) for p in ptrs]))
+        return dict(zip(("F", "M", "u", "g", "vs"), (p.value for p in ptrs)))
+
+    def script_losses(self, losses):
+        """losses: (pairs, n) float64 -- scripted-residual harness."""
+        if losses is None:
+            self._chk(self.lib.wlm_engine_script_losses(self.h, None, 0))
+            return
+        a = np.ascontiguousarray(losses, dtype=np.float64).reshape(self.pairs, -1)
+        self._chk(self.lib.wlm_engine_script_losses(self.h, a.ctypes.data_as(C.POINTER(C.c_double)),
+                                                    a.shape[1]))
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.wlm_engine_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

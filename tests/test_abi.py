@@ -1,0 +1,80 @@
+"""CPU tests of the drop-in boundary: the C-ABI library loads, exports every
+symbol include/wlm.h declares, and the host-only pieces (scalar damping /
+rejection state machine, config defaults, state_bytes) behave like the
+reference.  No GPU compute is attempted here."""
+import ctypes as C
+import os
+import re
+
+import numpy as np
+import pytest
+
+from conftest import ROOT
+
+HEADER = os.path.join(ROOT, "include", "wlm.h")
+
+
+def declared_symbols():
+    txt = open(HEADER).read()
+    txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
+    return sorted(set(re.findall(r"\b(wlm_[a-z0-9_]+)\s*\(", txt)))
+
+
+def test_header_symbols_exported():
+    from paper_2603_19371_b200 import _lib
+    lib = C.CDLL(_lib.LIB_PATH)
+    syms = declared_symbols()
+    assert len(syms) >= 35
+    missing = [s for s in syms if not hasattr(lib, s)]
+    assert not missing, missing
+    # the Python binding declares a signature for every exported entry point
+    assert set(syms) == set(_lib.SIGNATURES), set(syms) ^ set(_lib.SIGNATURES)
+
+
+def test_library_is_sm100a():
+    from paper_2603_19371_b200 import _lib
+    out = os.popen(f"cuobjdump --list-elf {_lib.LIB_PATH} 2>&1").read()
+    assert "sm_100a" in out, out
+
+
+def test_no_gpu_means_loud_failure():
+    import paper_2603_19371_b200 as P
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    with pytest.raises(P.WlmError):
+        P.Context(0)
+
+
+def test_defaults_match_spec():
+    import paper_2603_19371_b200 as P
+    c = P.reg_config()
+    assert (c.lm.lambda0, c.lm.mu_plus, c.lm.mu_minus) == (0.006, 1.5, 0.975)
+    assert (c.lm.tile_size, c.lm.rejection, c.lm.tau, c.lm.lambda_max, c.lm.max_retries) == (1, 0, 1.0, 1.0, 10)
+    assert (c.sigma_update, c.sigma_warp) == (1.0, 0.5)
+    assert list(c.factors)[:3] == [4, 2, 1] and list(c.iters)[:3] == [100, 75, 50]
+    assert (c.target_max_disp, c.step_floor) == (0.4, 1e-12)  # field.hpp:75-78
+    assert c.lncc_radius == 2
+
+
+def test_scalar_state_machine_matches_oracle():
+    import oracle as O
+    import paper_2603_19371_b200 as P
+    rng = np.random.default_rng(0)
+    cfgP = P.lm_config()
+    cfgO = O.lm_config()
+    sP = P.LmState(0.006, 0, 0.0, 0.0)
+    sO = O.LmState(0.006, 0, 0.0, 0.0)
+    for L in rng.uniform(0.2, 0.4, size=200):
+        sP = P.update_damping(sP, L, cfgP)
+        sO = O.update_damping(sO, L, cfgO)
+        assert (sP.lam, sP.hist_n, sP.L1, sP.L2) == (sO.lam, sO.hist_n, sO.L1, sO.L2)
+    for a, b, c_ in rng.uniform(0, 1, size=(200, 3)):
+        assert P.rejection_test(a, b, c_, 1.0) == O.rejection_test(a, b, c_, 1.0)
+
+
+def test_state_bytes():
+    import paper_2603_19371_b200 as P
+    assert P.state_bytes(P.OPT_ADAM, (64, 64, 64), 4) == 6291456
+    assert P.state_bytes(P.OPT_LM, (512, 512, 512), 4) < 1024
+    assert P.state_bytes(P.OPT_ADAM, (8, 9, 10), 4) == 2 * 3 * 720 * 4

@@ -1,0 +1,294 @@
+"""GPU parity tests: the sm_100a path (through the C-ABI) against the fp64
+oracle on identical seeded inputs.
+
+Tolerances (stated once):
+  * field ops in fp32 vs the fp64 reference: max abs error <= 1e-5 * scale
+    (inputs O(1)), exact where the SPEC says exact;
+  * LNCC residual r: rel <= 1e-5 (north star); gradient rel-L2 <= 1e-4;
+  * LM runs: per-iteration loss rel <= 1e-5, identical accept/reject
+    sequence, final warp rel-L2 <= 1e-4, lambda bit-identical.
+"""
+import math
+
+import numpy as np
+import pytest
+
+import oracle as O
+from conftest import rel, smooth_field
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def P():
+    import paper_2603_19371_b200 as P
+    return P
+
+
+def soa(u):
+    """(nz,ny,nx,3) AoS -> (3,nz,ny,nx) SoA float32."""
+    return np.ascontiguousarray(np.moveaxis(u, -1, 0), dtype=np.float32)
+
+
+def aos(u):
+    return np.moveaxis(np.asarray(u, np.float64), 0, -1)
+
+
+# ------------------------------------------------------------ field ops ----
+def test_compose_vs_reference(P, ctx, golden):
+    for name in ("c6", "c876"):
+        u, v, eps = golden[f"{name}_u"], golden[f"{name}_v"], float(golden[f"{name}_eps"])
+        out = P.compose_warp(u, v, eps, ctx=ctx)
+        # inputs are rounded to fp32 on the device: compare with the oracle on
+        # the same rounded inputs (cell choice identical), and with the fp64 ref
+        ur, vr = u.astype(np.float32).astype(np.float64), v.astype(np.float32).astype(np.float64)
+        assert np.abs(out - O.compose_warp(ur, vr, eps)).max() < 2e-5 * np.abs(u).max()
+        assert np.abs(out - golden[f"{name}_out"]).max() < 1e-4 * np.abs(u).max()
+    v = np.random.default_rng(0).normal(size=(6, 6, 6, 3)).astype(np.float32).astype(np.float64)
+    assert np.array_equal(P.compose_warp(np.zeros_like(v), v, 0.5, ctx=ctx),
+                          (0.5 * v.astype(np.float32)).astype(np.float64))
+    with pytest.raises(P.DimensionMismatch):
+        P.compose_warp(np.zeros((4, 4, 4, 3)), np.zeros((4, 4, 5, 3)), 0.1, ctx=ctx)
+
+
+@pytest.mark.parametrize("key", ["1p0", "0p5", "2p3"])
+def test_smooth_vs_reference(P, ctx, golden, key):
+    sig = float(key.replace("p", "."))
+    for kind in ("field", "vol"):
+        out = P.gaussian_smooth(golden[f"sm{key}_{kind}_in"], sig, ctx=ctx)
+        assert np.abs(out - golden[f"sm{key}_{kind}_out"]).max() < 2e-6
+    c = np.full((7, 8, 9), 2.5)
+    assert np.abs(P.gaussian_smooth(c, 1.0, ctx=ctx) - 2.5).max() < 1e-6  # constants preserved
+
+
+def test_max_normalize_jacobian(P, ctx, golden):
+    u = golden["jac_u"]
+    assert P.max_abs_component(u, ctx=ctx) == pytest.approx(float(golden["max_out"]), rel=1e-7)
+    assert P.normalize_step(u, ctx=ctx) == pytest.approx(float(golden["norm_out"]), rel=1e-7)
+    assert P.jacobian_det_min(u, ctx=ctx) == pytest.approx(float(golden["jac_out"]), abs=1e-6)
+    assert P.jacobian_det_min(golden["jac2_u"], ctx=ctx) == pytest.approx(float(golden["jac2_out"]), abs=1e-6)
+    with pytest.raises(P.InvalidArgument):
+        P.normalize_step(u, P.StepScale(0.6), ctx=ctx)  # field.cpp:151-153
+    with pytest.raises(P.InvalidArgument):
+        P.jacobian_det_min(np.zeros((1, 4, 4, 3)), ctx=ctx)  # field.cpp:174-176
+    z = np.zeros((5, 5, 5, 3))
+    assert P.jacobian_det_min(z, ctx=ctx) == 1.0
+    r = z.copy(); r[..., 0] = 0.1 * np.arange(5)
+    assert P.jacobian_det_min(r, ctx=ctx) == pytest.approx(1.1, rel=1e-6)
+
+
+def test_warp_volume_vs_reference(P, ctx, golden):
+    rng = np.random.default_rng(5)
+    M = rng.normal(size=(11, 12, 13)).astype(np.float32).astype(np.float64)
+    u = smooth_field((11, 12, 13), 1, amp=3.0).astype(np.float32).astype(np.float64)
+    u[0, 0, 0] = (0.0, 0.0, 0.0)  # exact knot
+    u[1, 1, 1] = (-1e-9, 0, 0)    # just below a knot: backward difference
+    Mw, gM = P.warp_volume(M, u, ctx=ctx)
+    Mo, go = O.warp_volume(M, u)
+    assert np.abs(Mw - Mo).max() < 1e-5
+    assert np.abs(gM - go).max() < 1e-5
+    assert np.array_equal(np.sign(gM[1, 1, 1]), np.sign(go[1, 1, 1]))
+
+
+def test_sample_field_and_pyramid(P, ctx):
+    u = smooth_field((8, 9, 10), 2, amp=1.0).astype(np.float32).astype(np.float64)
+    pts = np.random.default_rng(3).uniform(-2, 11, size=(500, 3))
+    got = P.sample_field(u, pts, ctx=ctx)
+    ref = np.array([O.lib().orc_sample_field and _sample3(u, p) for p in pts])
+    assert np.abs(got - ref).max() < 1e-5
+    vol = np.random.default_rng(4).uniform(size=(20, 18, 17))
+    for f in (2, 3, 4):
+        d = P.downsample(vol, f, ctx=ctx)
+        assert d.shape == O.level_dims(vol.shape, f)
+        assert np.abs(d - O.downsample(vol, f)).max() < 2e-6
+    up = P.upsample_warp(u, (16, 18, 20), 2.0, ctx=ctx)
+    assert np.abs(up - O.upsample_warp(u, (16, 18, 20), 2.0)).max() < 2e-5
+
+
+def _sample3(u, p):
+    out = np.empty(3)
+    import ctypes as C
+    uu = np.ascontiguousarray(u)
+    O.lib().orc_sample_field(O._p(uu), O.dims_of(uu), float(p[0]), float(p[1]), float(p[2]), O._p(out))
+    return out
+
+
+def test_all_finite(P, ctx):
+    a = np.zeros((4, 4, 4, 3))
+    assert P.all_finite(a, ctx=ctx)
+    a[1, 2, 3, 1] = np.nan
+    assert not P.all_finite(a, ctx=ctx)
+    b = np.zeros((4, 4, 4)); b[0, 0, 0] = np.inf
+    assert not P.all_finite(b, ctx=ctx)
+
+
+# --------------------------------------------------------------- LNCC ----
+def _pair(shape, seed, warp_max=2.0, noise=0.01):
+    F, M, _ = O.synth_pair(shape, seed, num_blobs=8, warp_max=warp_max, noise_sigma=noise)
+    return F.astype(np.float64), M.astype(np.float64)
+
+
+@pytest.mark.parametrize("shape,offset", [((24, 20, 28), 0.0), ((33, 17, 21), 0.0), ((24, 24, 24), 10.0)])
+def test_residual_lncc_vs_oracle(P, ctx, shape, offset):
+    F, M = _pair(shape, 11)
+    F, M = F + offset, M + offset
+    F = F.astype(np.float32).astype(np.float64)
+    M = M.astype(np.float32).astype(np.float64)
+    u = smooth_field(shape, 6, amp=1.5).astype(np.float32).astype(np.float64)
+    rep = P.residual_lncc(F, M, u, ctx=ctx)
+    r, g, ln = O.residual_lncc(F, M, u)
+    assert abs(rep.r - r) / r < 1e-5
+    assert abs(rep.loss_raw - ln) < 1e-5
+    assert rel(rep.g, g) < 1e-4, rel(rep.g, g)
+
+
+def test_lncc_kats_gpu(P, ctx):
+    F, _ = _pair((16, 16, 16), 5, warp_max=0.0, noise=0.05)
+    F32 = F.astype(np.float32).astype(np.float64)
+    z = np.zeros(F.shape + (3,))
+    rep = P.residual_lncc(F32, (2 * F32 + 3).astype(np.float32).astype(np.float64), z, ctx=ctx)
+    assert abs(rep.loss_raw - 1.0) < 1e-5 and abs(rep.r) < 1e-5
+    rep = P.residual_lncc(np.full((10, 10, 10), 0.7), F32[:10, :10, :10], z[:10, :10, :10], ctx=ctx)
+    assert rep.loss_raw == 0.0 and rep.r == 1.0 and not rep.g.any()
+    with pytest.raises(P.InvalidArgument):
+        P.residual_lncc(F32[:4], F32[:4], z[:4], ctx=ctx)
+
+
+def test_lm_step_pointwise_gpu(P, ctx):
+    g = np.zeros((2, 2, 2, 3)); g[0, 0, 0] = (1, 0, 0)
+    out = P.lm_step_pointwise(2.0, g, 1.0, ctx=ctx)
+    assert np.array_equal(out[0, 0, 0], [-1.0, 0.0, 0.0]) and not out[1:].any()
+    gg = np.random.default_rng(2).normal(size=(5, 6, 7, 3))
+    assert rel(P.lm_step_pointwise(0.3, gg, 0.01, ctx=ctx), O.lm_step_pointwise(0.3, gg, 0.01)) < 1e-6
+
+
+# ------------------------------------------------------------ LM engine ----
+def run_engine(P, ctx, F, M, cfg, iters, u0=None, pairs=1):
+    eng = P.Engine(F.shape[-3:], pairs=pairs, cfg=cfg, ctx=ctx)
+    Fb = np.broadcast_to(F, (pairs,) + F.shape[-3:]) if F.ndim == 3 else F
+    Mb = np.broadcast_to(M, (pairs,) + M.shape[-3:]) if M.ndim == 3 else M
+    eng.load(np.ascontiguousarray(Fb, np.float32), np.ascontiguousarray(Mb, np.float32))
+    eng.set_warp(u0)
+    eng.begin_level(0)
+    eng.iterate(iters)
+    warp = eng.get_warp()
+    traces = [eng.trace(p) for p in range(pairs)]
+    states = [eng.state(p) for p in range(pairs)]
+    eng.close()
+    return warp, traces, states
+
+
+def compare_runs(tr_gpu, tr_orc, warp_gpu, warp_orc, loss_tol=1e-5, warp_tol=1e-4):
+    assert len(tr_gpu) == len(tr_orc)
+    for a, b in zip(tr_gpu, tr_orc):
+        assert abs(a["r"] - b.r) <= loss_tol * abs(b.r), (a["iter"], a["r"], b.r)
+        assert a["accepted"] == b.accepted and a["retries"] == b.retries, a["iter"]
+        assert a["lam"] == b.lam, (a["iter"], a["lam"], b.lam)
+    assert rel(warp_gpu, warp_orc) <= warp_tol, rel(warp_gpu, warp_orc)
+
+
+def test_config1_64cubed_100_iterations(P, ctx):
+    """Config 1 (BASELINE.json): 64^3, one level, LNCC, 100 LM iterations."""
+    F, M, _ = O.synth_pair((64, 64, 64), 0, num_blobs=12, warp_max=3.0)
+    cfg_p = P.reg_config(nlevels=1, factors=[1], iters=[100])
+    cfg_o = O.default_config(nlevels=1, factors=[1], iters=[100])
+    warp, (tr,), _ = run_engine(P, ctx, F, M, cfg_p, 100)
+    rc, u_o, st, tr_o = O.lm_run_level(F, M, np.zeros((64, 64, 64, 3)), cfg_o, 100)
+    assert rc == 0
+    compare_runs(tr, tr_o, aos(warp[0]), u_o)
+
+
+def test_rejection_sequence_matches(P, ctx):
+    """LM + capped rejection: identical accept/reject sequence (north star)."""
+    F, M, _ = O.synth_pair((32, 36, 40), 3, num_blobs=10, warp_max=3.0)
+    kw = dict(nlevels=1, factors=[1], iters=[40])
+    cfg_p = P.reg_config(**kw, **{"lm.rejection": 1, "lm.tau": 0.2})
+    cfg_o = O.default_config(**kw, **{"lm.rejection": 1, "lm.tau": 0.2})
+    warp, (tr,), _ = run_engine(P, ctx, F, M, cfg_p, 40)
+    rc, u_o, st, tr_o = O.lm_run_level(F, M, np.zeros((32, 36, 40, 3)), cfg_o, 40)
+    assert rc == 0
+    assert sum(t.retries for t in tr_o) > 0, "test should exercise rejections"
+    compare_runs(tr, tr_o, aos(warp[0]), u_o)
+
+
+def test_scripted_losses_lambda_trajectory(P, ctx):
+    """SPEC.md:290 scripted-residual harness on the device state machine."""
+    F, M, _ = O.synth_pair((16, 16, 16), 1, warp_max=1.0)
+    losses = np.r_[1.0, 0.9, np.full(11, 5.0), 0.8, 0.7, 0.75, 0.6]
+    cfg_p = P.reg_config(nlevels=1, factors=[1], iters=[6], **{"lm.rejection": 1})
+    eng = P.Engine((16, 16, 16), 1, cfg_p, ctx=ctx)
+    eng.load(F[None], M[None])
+    eng.set_warp(None)
+    eng.script_losses(losses[None])
+    eng.begin_level(0)
+    eng.iterate(6)
+    tr = eng.trace(0)
+    lam, dec, st = O.lm_replay(losses, 6, O.lm_config(rejection=1))
+    acc_lams = [l for l, d in zip(lam, dec) if d == 0]
+    assert [t["lam"] for t in tr] == acc_lams
+    assert [t["retries"] for t in tr] == [0, 0, 10, 0, 0, 0]
+    assert tr[2]["accepted"] == 0  # forced after 10 retries
+    assert eng.state(0)["lam"] == st.lam
+    eng.close()
+
+
+def test_batch_pairs_are_independent_and_deterministic(P, ctx):
+    shape = (24, 28, 32)
+    Fs, Ms = [], []
+    for s in range(3):
+        F, M, _ = O.synth_pair(shape, 100 + s, num_blobs=6, warp_max=2.0)
+        Fs.append(F); Ms.append(M)
+    cfg = P.reg_config(nlevels=1, factors=[1], iters=[15])
+    wb, trb, _ = run_engine(P, ctx, np.stack(Fs), np.stack(Ms), cfg, 15, pairs=3)
+    wb2, trb2, _ = run_engine(P, ctx, np.stack(Fs), np.stack(Ms), cfg, 15, pairs=3)
+    assert np.array_equal(wb, wb2) and trb == trb2  # bit-identical reruns
+    for s in range(3):
+        w1, (t1,), _ = run_engine(P, ctx, Fs[s], Ms[s], cfg, 15)
+        assert np.array_equal(w1[0], wb[s]) and t1 == trb[s]
+
+
+def test_adam_and_gd_paths(P, ctx):
+    F, M, _ = O.synth_pair((24, 24, 24), 8, num_blobs=6, warp_max=2.0)
+    for opt, extra in ((P.OPT_ADAM, {}), (P.OPT_GD, {"gd_lr": 2.0})):
+        cfg_p = P.reg_config(nlevels=1, factors=[1], iters=[20], optimizer=opt, **extra)
+        cfg_o = O.default_config(nlevels=1, factors=[1], iters=[20], optimizer=opt, **extra)
+        warp, (tr,), _ = run_engine(P, ctx, F, M, cfg_p, 20)
+        rc, u_o, _, tr_o = O.lm_run_level(F, M, np.zeros((24, 24, 24, 3)), cfg_o, 20)
+        for a, b in zip(tr, tr_o):
+            assert abs(a["r"] - b.r) <= 1e-5 * b.r
+        assert rel(aos(warp[0]), u_o) < 1e-4
+
+
+def test_jacobian_logged_positive(P, ctx):
+    F, M, _ = O.synth_pair((20, 20, 20), 4, warp_max=2.0)
+    cfg = P.reg_config(nlevels=1, factors=[1], iters=[10], log_jacobian=1)
+    _, (tr,), _ = run_engine(P, ctx, F, M, cfg, 10)
+    cfg_o = O.default_config(nlevels=1, factors=[1], iters=[10], log_jacobian=1)
+    _, _, _, tr_o = O.lm_run_level(F, M, np.zeros((20, 20, 20, 3)), cfg_o, 10)
+    for a, b in zip(tr, tr_o):
+        assert a["jac_det_min"] > 0
+        assert abs(a["jac_det_min"] - b.jac_det_min) < 1e-4
+
+
+def test_register_pyramid_vs_oracle(P, ctx):
+    """Config-2-shaped pyramid (scaled down): levels, warp inheritance,
+    lambda carry, rejection on."""
+    F, M, _ = O.synth_pair((40, 48, 56), 1, num_blobs=10, warp_max=4.0)
+    kw = dict(nlevels=3, factors=[4, 2, 1], iters=[30, 20, 10])
+    res = P.register(F, M, P.reg_config(**kw, **{"lm.rejection": 1}), ctx=ctx)
+    rc, w_o, tr_o, jac_o = O.register(F, M, O.default_config(**kw, **{"lm.rejection": 1}))
+    assert rc == 0 and len(res.loss_trace) == len(tr_o) == 60
+    for a, b in zip(res.loss_trace, tr_o):
+        assert (a.level, a.iter, a.accepted, a.retries) == (b.level, b.iter, b.accepted, b.retries)
+        assert abs(a.r - b.r) <= 1e-5 * b.r
+        assert a.lam == b.lam
+    assert rel(res.final_warp, w_o) < 1e-4
+    assert res.jac_det_min_final == pytest.approx(jac_o, abs=1e-4)
+    assert res.peak_device_bytes > 0
+
+
+def test_nonfinite_input_aborts(P, ctx):
+    F, M, _ = O.synth_pair((16, 16, 16), 1, warp_max=1.0)
+    M = M.copy(); M[3, 3, 3] = np.nan
+    with pytest.raises(P.NonFiniteLoss):
+        P.register(F, M, P.reg_config(nlevels=1, factors=[1], iters=[3]), ctx=ctx)
