@@ -197,7 +197,11 @@ wlm_status wlm_engine_trace(wlm_engine* e, int pair, wlm_step_log* rows, size_t 
                             size_t* len);
 /* Device pointers of the engine's buffers (for tests / zero-copy callers). */
 wlm_status wlm_engine_buffers(wlm_engine* e, const float** F, const float** M,
-                              float** u_cur, float** g, float** vs);
+                              float** u_cur, float** g, float** vs, float** abe);
+/* Host copy of one pair's buffer: which = 0 F, 1 M, 2 accepted warp,
+ * 3 gradient g, 4 smoothed step dU_s, 5 LNCC coefficients (A, B, E planes);
+ * count floats (syncs). */
+wlm_status wlm_engine_read_buffer(wlm_engine* e, int which, int pair, float* host, size_t count);
 /* Scripted-residual harness: when n > 0, the evaluation
  * kernels take attempt losses from `losses` (per pair: losses[pair*n + k])
  * instead of the LNCC sum; n == 0 restores the real residual. */

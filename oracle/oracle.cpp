@@ -424,7 +424,11 @@ double orc_residual_lncc(const double* F, const double* M, const double* u, orc_
                 const double vf = sff - mf * mf, vm = smm - mm * mm;
                 const double cv = mom[4 * N + i] / n - mf * mm;
                 double r = 0.0, A = 0.0, B = 0.0, E = 0.0;
-                if (sff > 0.0 && smm > 0.0 && vf > kDegRel * sff && vm > kDegRel * smm) {
+                // degenerate test written so that NaN moments are NOT degenerate:
+                // a non-finite input propagates into the loss
+                const bool degenerate = !(sff > 0.0 || std::isnan(sff)) || !(smm > 0.0 || std::isnan(smm)) ||
+                                        vf <= kDegRel * sff || vm <= kDegRel * smm;
+                if (!degenerate) {
                     const double alpha = 1.0 / std::sqrt(vf * vm);
                     r = cv * alpha;
                     A = alpha / n;

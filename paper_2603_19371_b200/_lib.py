@@ -107,9 +107,10 @@ SIGNATURES = {
     "wlm_engine_trace": (C.c_int, [_ENG, C.c_int, C.POINTER(StepLog), C.c_size_t,
                                    C.POINTER(C.c_size_t)]),
     "wlm_engine_buffers": (C.c_int, [_ENG, C.POINTER(_VP), C.POINTER(_VP), C.POINTER(_VP),
-                                     C.POINTER(_VP), C.POINTER(_VP)]),
+                                     C.POINTER(_VP), C.POINTER(_VP), C.POINTER(_VP)]),
     "wlm_engine_script_losses": (C.c_int, [_ENG, _D, C.c_int]),
     "wlm_engine_stage": (C.c_int, [_ENG, C.c_int]),
+    "wlm_engine_read_buffer": (C.c_int, [_ENG, C.c_int, C.c_int, _VP, C.c_size_t]),
     "wlm_synth_pair": (C.c_int, [_CTX, C.POINTER(SynthSpec), _VP, _VP, _VP, C.c_int]),
 }
 

@@ -14,12 +14,13 @@
 
 namespace wlm {
 
+// In-volume offsets are 32-bit: one volume holds < 2^31 voxels (the
+// reference caps files at 2^31, io.cpp:13; engines reject larger volumes).
+// Batch/pair/channel bases are applied as 64-bit pointer offsets.
 struct Geo {
     int nx, ny, nz;
     long long n;  // voxels per volume
-    __host__ __device__ long long at(int x, int y, int z) const {
-        return (long long)x + (long long)nx * ((long long)y + (long long)ny * (long long)z);
-    }
+    __host__ __device__ int at(int x, int y, int z) const { return x + nx * (y + ny * z); }
 };
 
 inline Geo make_geo(wlm_dims d) {
@@ -67,10 +68,10 @@ __device__ __forceinline__ float sample_grad(const float* __restrict__ vol, cons
         return __int_as_float(0x7fc00000);
     }
     const AxisTap X = axis_tap(x, ux, g.nx), Y = axis_tap(y, uy, g.ny), Z = axis_tap(z, uz, g.nz);
-    const long long r00 = (long long)g.nx * ((long long)Y.i0 + (long long)g.ny * Z.i0);
-    const long long r10 = (long long)g.nx * ((long long)Y.i1 + (long long)g.ny * Z.i0);
-    const long long r01 = (long long)g.nx * ((long long)Y.i0 + (long long)g.ny * Z.i1);
-    const long long r11 = (long long)g.nx * ((long long)Y.i1 + (long long)g.ny * Z.i1);
+    const int r00 = g.nx * (Y.i0 + g.ny * Z.i0);
+    const int r10 = g.nx * (Y.i1 + g.ny * Z.i0);
+    const int r01 = g.nx * (Y.i0 + g.ny * Z.i1);
+    const int r11 = g.nx * (Y.i1 + g.ny * Z.i1);
     const float a = __ldg(vol + r00 + X.i0), b = __ldg(vol + r00 + X.i1);
     const float c = __ldg(vol + r10 + X.i0), e = __ldg(vol + r10 + X.i1);
     const float f = __ldg(vol + r01 + X.i0), h = __ldg(vol + r01 + X.i1);
@@ -89,7 +90,7 @@ __device__ __forceinline__ float sample_grad(const float* __restrict__ vol, cons
 
 // Value only (field.cpp:43-45 / sample_field :92-121 per component).
 struct Cell {
-    long long o000, o100, o010, o110, o001, o101, o011, o111;
+    int o000, o100, o010, o110, o001, o101, o011, o111;
     float tx, ty, tz;
     bool finite;
 };
@@ -101,10 +102,10 @@ __device__ __forceinline__ Cell make_cell(const Geo& g, int x, int y, int z, flo
     const AxisTap X = axis_tap(x, c.finite ? ux : 0.f, g.nx);
     const AxisTap Y = axis_tap(y, c.finite ? uy : 0.f, g.ny);
     const AxisTap Z = axis_tap(z, c.finite ? uz : 0.f, g.nz);
-    const long long r00 = (long long)g.nx * ((long long)Y.i0 + (long long)g.ny * Z.i0);
-    const long long r10 = (long long)g.nx * ((long long)Y.i1 + (long long)g.ny * Z.i0);
-    const long long r01 = (long long)g.nx * ((long long)Y.i0 + (long long)g.ny * Z.i1);
-    const long long r11 = (long long)g.nx * ((long long)Y.i1 + (long long)g.ny * Z.i1);
+    const int r00 = g.nx * (Y.i0 + g.ny * Z.i0);
+    const int r10 = g.nx * (Y.i1 + g.ny * Z.i0);
+    const int r01 = g.nx * (Y.i0 + g.ny * Z.i1);
+    const int r11 = g.nx * (Y.i1 + g.ny * Z.i1);
     c.o000 = r00 + X.i0; c.o100 = r00 + X.i1; c.o010 = r10 + X.i0; c.o110 = r10 + X.i1;
     c.o001 = r01 + X.i0; c.o101 = r01 + X.i1; c.o011 = r11 + X.i0; c.o111 = r11 + X.i1;
     c.tx = X.t; c.ty = Y.t; c.tz = Z.t;
@@ -121,6 +122,108 @@ __device__ __forceinline__ float cell_sample(const float* __restrict__ v, const 
     const float v01 = fmaf(c.tx, h - f, f), v11 = fmaf(c.tx, l - k, k);
     const float s0 = fmaf(c.ty, v10 - v00, v00), s1 = fmaf(c.ty, v11 - v01, v01);
     return fmaf(c.tz, s1 - s0, s0);
+}
+
+// fp64 variants for the LNCC path.  The interpolated intensities feed window
+// variances of O(noise^2); an fp32 lerp error (~1e-7 absolute) is 1e-5 of a
+// 0.01 deviation, so M(x + u) and its gradient are evaluated in fp64 from the
+// fp32 samples.  With u fp32, t = u - floor(u) is exact in fp64, so this is
+// the fp64 reference's sample for the same warp.
+struct AxisTapD {
+    int i0, i1;
+    double t;
+    bool outside;
+};
+
+__device__ __forceinline__ AxisTapD axis_tap_dd(int x, float u, int n) {
+    AxisTapD a;
+    if (n == 1) { a.i0 = a.i1 = 0; a.t = 0.0; a.outside = true; return a; }
+    const double ud = (double)u;
+    const double fl = floor(ud);
+    const int i = x + (int)fl;
+    const double t = ud - fl;  // exact
+    if (i < 0) { a.i0 = 0; a.i1 = 1; a.t = 0.0; a.outside = true; return a; }
+    if (i > n - 1 || (i == n - 1 && t > 0.0)) {
+        a.i0 = n - 2; a.i1 = n - 1; a.t = 1.0; a.outside = true; return a;
+    }
+    if (i == n - 1) { a.i0 = n - 2; a.i1 = n - 1; a.t = 1.0; a.outside = false; return a; }
+    a.i0 = i; a.i1 = i + 1; a.t = t; a.outside = false;
+    return a;
+}
+
+// Value (and optionally the analytic gradient) of vol at (x,y,z) + u in fp64,
+// collapse order of field.cpp:47-90.
+template <bool GRAD>
+__device__ __forceinline__ double sample_d(const float* __restrict__ vol, const Geo& g, int x, int y,
+                                           int z, float ux, float uy, float uz, double* grad) {
+    if (!(isfinite(ux) && isfinite(uy) && isfinite(uz))) {
+        if (GRAD) grad[0] = grad[1] = grad[2] = 0.0;
+        return __longlong_as_double(0x7ff8000000000000ll);
+    }
+    const AxisTapD X = axis_tap_dd(x, ux, g.nx), Y = axis_tap_dd(y, uy, g.ny), Z = axis_tap_dd(z, uz, g.nz);
+    const int r00 = g.nx * (Y.i0 + g.ny * Z.i0);
+    const int r10 = g.nx * (Y.i1 + g.ny * Z.i0);
+    const int r01 = g.nx * (Y.i0 + g.ny * Z.i1);
+    const int r11 = g.nx * (Y.i1 + g.ny * Z.i1);
+    const double a = __ldg(vol + r00 + X.i0), b = __ldg(vol + r00 + X.i1);
+    const double c = __ldg(vol + r10 + X.i0), e = __ldg(vol + r10 + X.i1);
+    const double f = __ldg(vol + r01 + X.i0), h = __ldg(vol + r01 + X.i1);
+    const double k = __ldg(vol + r11 + X.i0), l = __ldg(vol + r11 + X.i1);
+    const double d00 = b - a, d10 = e - c, d01 = h - f, d11 = l - k;
+    const double v00 = fma(X.t, d00, a), v10 = fma(X.t, d10, c);
+    const double v01 = fma(X.t, d01, f), v11 = fma(X.t, d11, k);
+    const double s0 = fma(Y.t, v10 - v00, v00), s1 = fma(Y.t, v11 - v01, v01);
+    if (GRAD) {
+        const double gx0 = fma(Y.t, d10 - d00, d00), gx1 = fma(Y.t, d11 - d01, d01);
+        grad[0] = X.outside ? 0.0 : fma(Z.t, gx1 - gx0, gx0);
+        const double gy0 = v10 - v00, gy1 = v11 - v01;
+        grad[1] = Y.outside ? 0.0 : fma(Z.t, gy1 - gy0, gy0);
+        grad[2] = Z.outside ? 0.0 : s1 - s0;
+    }
+    return fma(Z.t, s1 - s0, s0);
+}
+
+// fp64 three-component sample of an SoA field at (x,y,z) + d with d in fp64
+// (sample_field, field.cpp:92-121), for the compositive resample.
+__device__ __forceinline__ AxisTapD axis_tap_dd(int x, double u, int n) {
+    AxisTapD a;
+    if (n == 1) { a.i0 = a.i1 = 0; a.t = 0.0; a.outside = true; return a; }
+    const double fl = floor(u);
+    const int i = x + (int)fl;
+    const double t = u - fl;
+    if (i < 0) { a.i0 = 0; a.i1 = 1; a.t = 0.0; a.outside = true; return a; }
+    if (i > n - 1 || (i == n - 1 && t > 0.0)) {
+        a.i0 = n - 2; a.i1 = n - 1; a.t = 1.0; a.outside = true; return a;
+    }
+    if (i == n - 1) { a.i0 = n - 2; a.i1 = n - 1; a.t = 1.0; a.outside = false; return a; }
+    a.i0 = i; a.i1 = i + 1; a.t = t; a.outside = false;
+    return a;
+}
+
+__device__ __forceinline__ void sample3_d(const float* __restrict__ u, long long n, const Geo& g,
+                                          int x, int y, int z, double dx, double dy, double dz,
+                                          double* out) {
+    if (!(isfinite(dx) && isfinite(dy) && isfinite(dz))) {
+        out[0] = out[1] = out[2] = __longlong_as_double(0x7ff8000000000000ll);
+        return;
+    }
+    const AxisTapD X = axis_tap_dd(x, dx, g.nx), Y = axis_tap_dd(y, dy, g.ny), Z = axis_tap_dd(z, dz, g.nz);
+    const int r00 = g.nx * (Y.i0 + g.ny * Z.i0);
+    const int r10 = g.nx * (Y.i1 + g.ny * Z.i0);
+    const int r01 = g.nx * (Y.i0 + g.ny * Z.i1);
+    const int r11 = g.nx * (Y.i1 + g.ny * Z.i1);
+#pragma unroll
+    for (int ch = 0; ch < 3; ++ch) {
+        const float* v = u + ch * n;
+        const double a = __ldg(v + r00 + X.i0), b = __ldg(v + r00 + X.i1);
+        const double c = __ldg(v + r10 + X.i0), e = __ldg(v + r10 + X.i1);
+        const double f = __ldg(v + r01 + X.i0), h = __ldg(v + r01 + X.i1);
+        const double k = __ldg(v + r11 + X.i0), l = __ldg(v + r11 + X.i1);
+        const double v00 = fma(X.t, b - a, a), v10 = fma(X.t, e - c, c);
+        const double v01 = fma(X.t, h - f, f), v11 = fma(X.t, l - k, k);
+        const double s0 = fma(Y.t, v10 - v00, v00), s1 = fma(Y.t, v11 - v01, v01);
+        out[ch] = fma(Z.t, s1 - s0, s0);
+    }
 }
 
 // Non-negative float max via ordered unsigned bits (exact, order-free).

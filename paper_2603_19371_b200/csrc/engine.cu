@@ -33,6 +33,10 @@ wlm_status engine_init(wlm_engine* e, wlm_ctx* ctx, wlm_dims d, int pairs, const
         set_err(ctx, "lncc_radius != 2 is not instantiated");
         return WLM_UNSUPPORTED;
     }
+    if ((long long)d.nx * d.ny * d.nz >= (1ll << 31)) {
+        set_err(ctx, "volumes of 2^31 voxels or more are not supported (io.cpp:13 cap)");
+        return WLM_UNSUPPORTED;
+    }
     if (d.nx <= 2 * c->lncc_radius || d.ny <= 2 * c->lncc_radius || d.nz <= 2 * c->lncc_radius) {
         set_err(ctx, "residual_lncc: dims must exceed 2*radius (SPEC.md:138)");
         return WLM_INVALID_ARG;
@@ -64,6 +68,8 @@ wlm_status engine_init(wlm_engine* e, wlm_ctx* ctx, wlm_dims d, int pairs, const
         return WLM_UNSUPPORTED;
     }
     fill_half_kernel(c->sigma_update, P.Ru, P.wu, &P.wu_full);
+    fill_half_kernel(c->sigma_update, P.Ru, P.wud, &P.wud_full);
+    fill_half_kernel(c->sigma_warp, P.Rw, P.wwd, &P.wwd_full);
     fill_half_kernel(c->sigma_warp, P.Rw, P.ww, &P.ww_full);
     int maxit = 0;
     for (int i = 0; i < c->nlevels && i < WLM_MAX_LEVELS; ++i) maxit = std::max(maxit, c->iters[i]);
@@ -77,7 +83,9 @@ void engine_alloc(wlm_engine* e) {
     e->F = DevBuf<float>(ctx, B * n);
     e->M = DevBuf<float>(ctx, B * n);
     e->U = DevBuf<float>(ctx, B * 6 * n);
-    e->ABE = DevBuf<float>(ctx, B * 3 * n);
+    e->ABE = DevBuf<float>(ctx, B * 4 * n);  // A, B fp32 + E fp64
+    e->shift_part = DevBuf<double>(ctx, B * 2 * 256);
+    init_constants();
     e->G = DevBuf<float>(ctx, B * 3 * n);
     e->VS = DevBuf<float>(ctx, B * 3 * n);
     if (e->P.optimizer == WLM_OPT_ADAM) {
@@ -100,6 +108,7 @@ void engine_alloc(wlm_engine* e) {
     b.AM = e->AM.p; b.AV = e->AV.p;
     b.st = e->st.p;
     b.partials = e->partials.p;
+    b.shift_part = e->shift_part.p;
     b.max_blocks = maxb;
     CK(cudaMemsetAsync(e->U.p, 0, sizeof(float) * B * 6 * n, ctx->stream));
     launch_begin_level(b, e->P, 0, 1, e->cfg.lm.lambda0, ctx->stream);
@@ -346,7 +355,7 @@ wlm_status wlm_engine_trace(wlm_engine* e, int pair, wlm_step_log* rows, size_t 
 }
 
 wlm_status wlm_engine_buffers(wlm_engine* e, const float** F, const float** M, float** u_cur,
-                              float** g, float** vs) {
+                              float** g, float** vs, float** abe) {
     if (!e) return WLM_INVALID_ARG;
     wlm_ctx* ctx = e->ctx;
     return run(ctx, [&] {
@@ -354,10 +363,36 @@ wlm_status wlm_engine_buffers(wlm_engine* e, const float** F, const float** M, f
         if (M) *M = e->M.p;
         if (g) *g = e->G.p;
         if (vs) *vs = e->VS.p;
+        if (abe) *abe = e->ABE.p;
         if (u_cur) {
             const std::vector<PairState> v = read_states(e);
             *u_cur = e->U.p + (size_t)v[0].cur * 3 * (size_t)e->g.n;
         }
+    });
+}
+
+wlm_status wlm_engine_read_buffer(wlm_engine* e, int which, int pair, float* host, size_t count) {
+    if (!e || !host || pair < 0 || pair >= e->pairs || which < 0 || which > 5) return WLM_INVALID_ARG;
+    wlm_ctx* ctx = e->ctx;
+    const size_t n = (size_t)e->g.n;
+    const size_t nch = which < 2 ? 1 : which == 5 ? 4 : 3;
+    if (count > nch * n) return WLM_INVALID_ARG;
+    return run(ctx, [&] {
+        const float* src = nullptr;
+        switch (which) {
+            case 0: src = e->F.p + pair * n; break;
+            case 1: src = e->M.p + pair * n; break;
+            case 2: {
+                const std::vector<PairState> v = read_states(e);
+                src = e->U.p + ((size_t)pair * 2 + v[pair].cur) * 3 * n;
+                break;
+            }
+            case 3: src = e->G.p + pair * 3 * n; break;
+            case 4: src = e->VS.p + pair * 3 * n; break;
+            default: src = e->ABE.p + pair * 4 * n; break;
+        }
+        CK(cudaMemcpyAsync(host, src, sizeof(float) * count, cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
     });
 }
 

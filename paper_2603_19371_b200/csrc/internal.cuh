@@ -85,15 +85,16 @@ inline int smooth_radius(double sigma) {
     return std::max(1, (int)std::ceil(3.0 * sigma));
 }
 
-inline void fill_half_kernel(double sigma, int R, float* w, float* full) {
-    if (R == 0) { w[0] = 1.f; *full = 1.f; return; }
+template <class T>
+inline void fill_half_kernel(double sigma, int R, T* w, T* full) {
+    if (R == 0) { w[0] = T(1); *full = T(1); return; }
     double s = 0.0;
     for (int d = 0; d <= R; ++d) {
         const double v = std::exp(-0.5 * (double)(d * d) / (sigma * sigma));
-        w[d] = (float)v;
+        w[d] = (T)v;
         s += d == 0 ? v : 2.0 * v;
     }
-    *full = (float)s;
+    *full = (T)s;
 }
 
 inline wlm_status guard(wlm_ctx* ctx) {
@@ -149,7 +150,7 @@ struct wlm_engine {
     LmParams P{};
     DevBuf<float> F, M, U, ABE, G, VS, AM, AV;
     DevBuf<PairState> st;
-    DevBuf<double> partials, script;
+    DevBuf<double> partials, script, shift_part;
     DevBuf<wlm_step_log> trace;
     Batch B{};
     cudaGraphExec_t step_exec = nullptr, loop_exec = nullptr;

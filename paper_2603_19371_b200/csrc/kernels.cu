@@ -147,17 +147,25 @@ __device__ double block_sum(double v, double* red) {
 }
 
 // ---------------------------------------------------------------------------
+// Window statistics are accumulated in fp64 (B200 runs fp64 at half the
+// fp32 rate): LNCC moments cancel catastrophically in fp32 wherever a window
+// is bright and flat (variance << mean^2), and the gradient's
+// adjoint sums cancel against E.  Products of two
+// fp32 values are exact in fp64, so the sums are those of the fp32 inputs to
+// ~1e-16.  Per-voxel inputs (f, M(x+u)) and the stored A, B stay fp32.
+__constant__ double c_inv_count[126];  // 1/n for truncated window counts n <= 125
+
 // K1: warp + LNCC forward.
-//   input plane (halo R): f' = F - shift_f, m' = M(x + u(x)) - shift_m
-//   window sums (box, truncated): S_f, S_m, S_ff, S_mm, S_fm   (fp32 on
-//   shifted intensities -- SURVEY §9.1 N1 / DESIGN.md "precision")
-//   rho = c / sqrt(vf vm); A = 1/(n sqrt(vf vm)); B = -rho/(n vm);
-//   E = A mu_f' + B mu_m'   -> written as three planes, sum(rho) -> partial
+//   input plane (halo R): f' = F - shift_f, m' = M(x + u(x)) - shift_m  (fp64)
+//   window sums S_f, S_m, S_ff, S_mm, S_fm over the truncated box (fp64)
+//   rho = c / sqrt(vf vm); A = 1/(n sqrt(vf vm)); B = -rho/(n vm)  -> fp32
+//   E = A' mu_f' + B' mu_m' (fp64, from the rounded A', B' so that K2's
+//   f' S_A + m' S_B - S_E cancels exactly), sum(rho) -> per-CTA partial.
 template <int R>
 __global__ void __launch_bounds__(NT) k_lncc_fwd(Batch b, LmParams p, int mode, int chunk_len) {
     constexpr int IW = TX + 2 * R, IH = TY + 2 * R, W = 2 * R + 1;
-    __shared__ float s_f[IH][IW], s_m[IH][IW];
-    __shared__ float s_x[5][IH][TX];
+    __shared__ double s_f[IH][IW], s_m[IH][IW];
+    __shared__ double s_x[5][IH][TX];
     __shared__ double s_red[NT / 32];
     __shared__ int s_last;
 
@@ -173,18 +181,20 @@ __global__ void __launch_bounds__(NT) k_lncc_fwd(Batch b, LmParams p, int mode, 
     const float* __restrict__ F = b.F + (long long)pair * n;
     const float* __restrict__ M = b.M + (long long)pair * n;
     const float* __restrict__ U = b.U + ((long long)pair * 2 + buf) * 3 * n;
-    float* __restrict__ A = b.ABE + (long long)pair * 3 * n;
-    const float shf = st->shift_f, shm = st->shift_m;
+    float* __restrict__ A = b.ABE + (long long)pair * 4 * n;
+    float* __restrict__ Bc = A + n;
+    double* __restrict__ E = reinterpret_cast<double*>(A + 2 * n);
+    const double shf = st->shift_f, shm = st->shift_m;
     const int tid = threadIdx.x, ox = tid & 31, oy = tid >> 5;
     const int x = x0 + ox, y = y0 + oy;
     const bool own = x < g.nx && y < g.ny;
-    const float cxy = own ? (float)(axis_count(x, g.nx, R) * axis_count(y, g.ny, R)) : 1.f;
+    const int cxy = own ? axis_count(x, g.nx, R) * axis_count(y, g.ny, R) : 1;
 
-    float ring[W][5];
+    double ring[W][5];
 #pragma unroll
     for (int d = 0; d < W; ++d)
 #pragma unroll
-        for (int c = 0; c < 5; ++c) ring[d][c] = 0.f;
+        for (int c = 0; c < 5; ++c) ring[d][c] = 0.0;
     double rho_acc = 0.0;
 
     for (int zi = zb - R; zi < ze + R; ++zi) {
@@ -192,13 +202,12 @@ __global__ void __launch_bounds__(NT) k_lncc_fwd(Batch b, LmParams p, int mode, 
         for (int idx = tid; idx < IW * IH; idx += NT) {
             const int ix = idx % IW, iy = idx / IW;
             const int gx = x0 - R + ix, gy = y0 - R + iy;
-            float fv = 0.f, mv = 0.f;
+            double fv = 0.0, mv = 0.0;
             if (zin && gx >= 0 && gx < g.nx && gy >= 0 && gy < g.ny) {
-                const long long o = g.at(gx, gy, zi);
-                const Cell cell = make_cell(g, gx, gy, zi, __ldg(U + o), __ldg(U + n + o),
-                                            __ldg(U + 2 * n + o));
-                mv = cell_sample(M, cell) - shm;
-                fv = __ldg(F + o) - shf;
+                const int o = g.at(gx, gy, zi);
+                mv = sample_d<false>(M, g, gx, gy, zi, __ldg(U + o), __ldg(U + n + o),
+                                     __ldg(U + 2 * n + o), nullptr) - shm;
+                fv = (double)__ldg(F + o) - shf;
             }
             s_f[iy][ix] = fv;
             s_m[iy][ix] = mv;
@@ -206,15 +215,15 @@ __global__ void __launch_bounds__(NT) k_lncc_fwd(Batch b, LmParams p, int mode, 
         __syncthreads();
         for (int idx = tid; idx < IH * TX; idx += NT) {
             const int c = idx % TX, r = idx / TX;
-            float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f, a4 = 0.f;
+            double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0, a4 = 0.0;
 #pragma unroll
             for (int d = 0; d < W; ++d) {
-                const float f = s_f[r][c + d], m = s_m[r][c + d];
+                const double f = s_f[r][c + d], m = s_m[r][c + d];
                 a0 += f;
                 a1 += m;
-                a2 = fmaf(f, f, a2);
-                a3 = fmaf(m, m, a3);
-                a4 = fmaf(f, m, a4);
+                a2 = fma(f, f, a2);
+                a3 = fma(m, m, a3);
+                a4 = fma(f, m, a4);
             }
             s_x[0][r][c] = a0; s_x[1][r][c] = a1; s_x[2][r][c] = a2;
             s_x[3][r][c] = a3; s_x[4][r][c] = a4;
@@ -226,42 +235,45 @@ __global__ void __launch_bounds__(NT) k_lncc_fwd(Batch b, LmParams p, int mode, 
             for (int c = 0; c < 5; ++c) ring[d][c] = ring[d + 1][c];
 #pragma unroll
         for (int c = 0; c < 5; ++c) {
-            float s = 0.f;
+            double s = 0.0;
 #pragma unroll
             for (int d = 0; d < W; ++d) s += s_x[c][oy + d][ox];
             ring[W - 1][c] = s;
         }
         const int zo = zi - R;
         if (zo >= zb && own) {
-            float S[5];
+            double S[5];
 #pragma unroll
             for (int c = 0; c < 5; ++c) {
-                float s = 0.f;
+                double s = 0.0;
 #pragma unroll
                 for (int d = 0; d < W; ++d) s += ring[d][c];
                 S[c] = s;
             }
-            const float cnt = cxy * (float)axis_count(zo, g.nz, R);
-            const float inv = 1.f / cnt;
-            const float mf = S[0] * inv, mm = S[1] * inv;
-            const float vf = fmaf(-mf, mf, S[2] * inv);
-            const float vm = fmaf(-mm, mm, S[3] * inv);
-            const float cv = fmaf(-mf, mm, S[4] * inv);
-            const float af = mf + shf, am = mm + shm;
-            const float msf = fmaf(af, af, vf), msm = fmaf(am, am, vm);
-            float rho = 0.f, Aa = 0.f, Bb = 0.f, Ee = 0.f;
-            if (msf > 0.f && msm > 0.f && vf > 1e-9f * msf && vm > 1e-9f * msm) {
-                const float alpha = rsqrtf(vf) * rsqrtf(vm);
+            const double inv = c_inv_count[cxy * axis_count(zo, g.nz, R)];
+            const double mf = S[0] * inv, mm = S[1] * inv;
+            const double vf = fma(-mf, mf, S[2] * inv);
+            const double vm = fma(-mm, mm, S[3] * inv);
+            const double cv = fma(-mf, mm, S[4] * inv);
+            const double af = mf + shf, am = mm + shm;
+            const double msf = fma(af, af, vf), msm = fma(am, am, vm);
+            double rho = 0.0;
+            float Aa = 0.f, Bb = 0.f;
+            double Ee = 0.0;
+            // NaN moments are not degenerate: a non-finite input reaches the loss
+            const bool degenerate = msf <= 0.0 || msm <= 0.0 || vf <= 1e-9 * msf || vm <= 1e-9 * msm;
+            if (!degenerate) {
+                const double alpha = 1.0 / sqrt(vf * vm);
                 rho = cv * alpha;
-                Aa = alpha * inv;
-                Bb = -rho / vm * inv;
-                Ee = fmaf(Aa, mf, Bb * mm);
+                Aa = (float)(alpha * inv);
+                Bb = (float)(-rho / vm * inv);
+                Ee = fma((double)Aa, mf, (double)Bb * mm);
             }
-            const long long o = g.at(x, y, zo);
+            const int o = g.at(x, y, zo);
             A[o] = Aa;
-            A[n + o] = Bb;
-            A[2 * n + o] = Ee;
-            rho_acc += (double)rho;
+            Bc[o] = Bb;
+            E[o] = Ee;
+            rho_acc += rho;
         }
     }
 
@@ -287,13 +299,14 @@ __global__ void __launch_bounds__(NT) k_lncc_fwd(Batch b, LmParams p, int mode, 
 }
 
 // ---------------------------------------------------------------------------
-// K2: LNCC backward.  Adjoint box sums of (A, B, E) over the same windows,
-//   dr/dMw(x) = -(1/N) (f'_x S_A + m'_x S_B - S_E),  g = dr/dMw * gradM(x+u)
+// K2: LNCC backward.  Adjoint box sums of (A, B, E) over the same windows in
+// fp64, dr/dMw(x) = -(1/N) (f'_x S_A + m'_x S_B - S_E),
+// g = dr/dMw * gradM(x + u(x)).
 template <int R>
 __global__ void __launch_bounds__(NT) k_lncc_bwd(Batch b, LmParams p, int chunk_len) {
     constexpr int IW = TX + 2 * R, IH = TY + 2 * R, W = 2 * R + 1;
-    __shared__ float s_in[3][IH][IW];
-    __shared__ float s_x[3][IH][TX];
+    __shared__ double s_in[3][IH][IW];
+    __shared__ double s_x[3][IH][TX];
 
     const int pair = blockIdx.z;
     const PairState* st = b.st + pair;
@@ -306,31 +319,33 @@ __global__ void __launch_bounds__(NT) k_lncc_bwd(Batch b, LmParams p, int chunk_
     const float* __restrict__ F = b.F + (long long)pair * n;
     const float* __restrict__ M = b.M + (long long)pair * n;
     const float* __restrict__ U = b.U + ((long long)pair * 2 + st->cur) * 3 * n;
-    const float* __restrict__ A = b.ABE + (long long)pair * 3 * n;
+    const float* __restrict__ A = b.ABE + (long long)pair * 4 * n;
+    const float* __restrict__ Bc = A + n;
+    const double* __restrict__ E = reinterpret_cast<const double*>(A + 2 * n);
     float* __restrict__ G = b.G + (long long)pair * 3 * n;
-    const float shf = st->shift_f, shm = st->shift_m;
-    const float invN = (float)(1.0 / (double)n);
+    const double shf = st->shift_f, shm = st->shift_m;
+    const double invN = 1.0 / (double)n;
     const int tid = threadIdx.x, ox = tid & 31, oy = tid >> 5;
     const int x = x0 + ox, y = y0 + oy;
     const bool own = x < g.nx && y < g.ny;
 
-    float ring[W][3];
+    double ring[W][3];
 #pragma unroll
     for (int d = 0; d < W; ++d)
 #pragma unroll
-        for (int c = 0; c < 3; ++c) ring[d][c] = 0.f;
+        for (int c = 0; c < 3; ++c) ring[d][c] = 0.0;
 
     for (int zi = zb - R; zi < ze + R; ++zi) {
         const bool zin = zi >= 0 && zi < g.nz;
         for (int idx = tid; idx < IW * IH; idx += NT) {
             const int ix = idx % IW, iy = idx / IW;
             const int gx = x0 - R + ix, gy = y0 - R + iy;
-            float a = 0.f, bb = 0.f, e = 0.f;
+            double a = 0.0, bb = 0.0, e = 0.0;
             if (zin && gx >= 0 && gx < g.nx && gy >= 0 && gy < g.ny) {
-                const long long o = g.at(gx, gy, zi);
-                a = __ldg(A + o);
-                bb = __ldg(A + n + o);
-                e = __ldg(A + 2 * n + o);
+                const int o = g.at(gx, gy, zi);
+                a = (double)__ldg(A + o);
+                bb = (double)__ldg(Bc + o);
+                e = __ldg(E + o);
             }
             s_in[0][iy][ix] = a;
             s_in[1][iy][ix] = bb;
@@ -341,7 +356,7 @@ __global__ void __launch_bounds__(NT) k_lncc_bwd(Batch b, LmParams p, int chunk_
             const int c = idx % TX, r = idx / TX;
 #pragma unroll
             for (int ch = 0; ch < 3; ++ch) {
-                float s = 0.f;
+                double s = 0.0;
 #pragma unroll
                 for (int d = 0; d < W; ++d) s += s_in[ch][r][c + d];
                 s_x[ch][r][c] = s;
@@ -354,64 +369,76 @@ __global__ void __launch_bounds__(NT) k_lncc_bwd(Batch b, LmParams p, int chunk_
             for (int c = 0; c < 3; ++c) ring[d][c] = ring[d + 1][c];
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
-            float s = 0.f;
+            double s = 0.0;
 #pragma unroll
             for (int d = 0; d < W; ++d) s += s_x[c][oy + d][ox];
             ring[W - 1][c] = s;
         }
         const int zo = zi - R;
         if (zo >= zb && own) {
-            float S[3];
+            double S[3];
 #pragma unroll
             for (int c = 0; c < 3; ++c) {
-                float s = 0.f;
+                double s = 0.0;
 #pragma unroll
                 for (int d = 0; d < W; ++d) s += ring[d][c];
                 S[c] = s;
             }
-            const long long o = g.at(x, y, zo);
-            float gmx, gmy, gmz;
-            const float mw = sample_grad(M, g, x, y, zo, __ldg(U + o), __ldg(U + n + o),
-                                         __ldg(U + 2 * n + o), gmx, gmy, gmz);
-            const float f = __ldg(F + o) - shf;
-            const float dm = -invN * (fmaf(f, S[0], (mw - shm) * S[1]) - S[2]);
-            G[o] = dm * gmx;
-            G[n + o] = dm * gmy;
-            G[2 * n + o] = dm * gmz;
+            const int o = g.at(x, y, zo);
+            double gm[3];
+            const double mw = sample_d<true>(M, g, x, y, zo, __ldg(U + o), __ldg(U + n + o),
+                                             __ldg(U + 2 * n + o), gm);
+            const double f = (double)__ldg(F + o) - shf;
+            const double dm = -invN * (fma(f, S[0], (mw - shm) * S[1]) - S[2]);
+            G[o] = (float)(dm * gm[0]);
+            G[n + o] = (float)(dm * gm[1]);
+            G[2 * n + o] = (float)(dm * gm[2]);
         }
     }
 }
 
 // ---------------------------------------------------------------------------
-// Gaussian z-march over 3 channels (K3, K4).  Weights w[|d|] are truncated
-// at R and renormalised per axis over in-bounds taps (field.cpp:236-244):
-// zero-filled halos + a final divide by Wx(x) Wy(y) Wz(z).
-template <int R, class Prod, class Cons>
+// Gaussian z-march over 3 channels (K3, K4), accumulating in T.  Weights
+// w[|d|] are truncated at R and renormalised per axis over in-bounds taps
+// (field.cpp:236-244): zero-filled halos + a final divide by Wx Wy Wz.
+// K3 accumulates in fp64 (its input, the LM step, is signed and noisy, so the
+// 343-tap sums cancel); K4 smooths the warp (same-sign, O(1)) in fp32.
+template <class T>
+__device__ __forceinline__ T axis_wsum_t(int p, int n, int R, const T* w, T full) {
+    if (p >= R && p + R <= n - 1) return full;
+    T s = 0;
+    for (int d = -R; d <= R; ++d) {
+        const int q = p + d;
+        if (q >= 0 && q < n) s += w[d < 0 ? -d : d];
+    }
+    return s;
+}
+
+template <int R, class T, class Prod, class Cons>
 __device__ __forceinline__ void gauss_march3(const Geo& g, int x0, int y0, int zb, int ze,
-                                             const float* wh, float wfull, Prod& prod,
-                                             Cons& cons) {
+                                             const T* wh, T wfull, Prod& prod, Cons& cons) {
     constexpr int IW = TX + 2 * R, IH = TY + 2 * R, W = 2 * R + 1;
-    __shared__ float s_in[3][IH][IW];
-    __shared__ float s_x[3][IH][TX];
-    float wr[W];
+    __shared__ T s_in[3][IH][IW];
+    __shared__ T s_x[3][IH][TX];
+    T wr[W];
 #pragma unroll
     for (int d = 0; d < W; ++d) wr[d] = wh[d < R ? R - d : d - R];
     const int tid = threadIdx.x, ox = tid & 31, oy = tid >> 5;
     const int x = x0 + ox, y = y0 + oy;
     const bool own = x < g.nx && y < g.ny;
-    const float wxy = own ? axis_wsum(x, g.nx, R, wh, wfull) * axis_wsum(y, g.ny, R, wh, wfull) : 1.f;
-    float ring[W][3];
+    const T wxy = own ? axis_wsum_t<T>(x, g.nx, R, wh, wfull) * axis_wsum_t<T>(y, g.ny, R, wh, wfull) : T(1);
+    T ring[W][3];
 #pragma unroll
     for (int d = 0; d < W; ++d)
 #pragma unroll
-        for (int c = 0; c < 3; ++c) ring[d][c] = 0.f;
+        for (int c = 0; c < 3; ++c) ring[d][c] = 0;
 
     for (int zi = zb - R; zi < ze + R; ++zi) {
         const bool zin = zi >= 0 && zi < g.nz;
         for (int idx = tid; idx < IW * IH; idx += NT) {
             const int ix = idx % IW, iy = idx / IW;
             const int gx = x0 - R + ix, gy = y0 - R + iy;
-            float v[3] = {0.f, 0.f, 0.f};
+            T v[3] = {0, 0, 0};
             if (zin && gx >= 0 && gx < g.nx && gy >= 0 && gy < g.ny) prod(gx, gy, zi, v);
             s_in[0][iy][ix] = v[0];
             s_in[1][iy][ix] = v[1];
@@ -422,9 +449,9 @@ __device__ __forceinline__ void gauss_march3(const Geo& g, int x0, int y0, int z
             const int c = idx % TX, r = idx / TX;
 #pragma unroll
             for (int ch = 0; ch < 3; ++ch) {
-                float s = 0.f;
+                T s = 0;
 #pragma unroll
-                for (int d = 0; d < W; ++d) s = fmaf(wr[d], s_in[ch][r][c + d], s);
+                for (int d = 0; d < W; ++d) s = fma(wr[d], s_in[ch][r][c + d], s);
                 s_x[ch][r][c] = s;
             }
         }
@@ -435,20 +462,20 @@ __device__ __forceinline__ void gauss_march3(const Geo& g, int x0, int y0, int z
             for (int c = 0; c < 3; ++c) ring[d][c] = ring[d + 1][c];
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
-            float s = 0.f;
+            T s = 0;
 #pragma unroll
-            for (int d = 0; d < W; ++d) s = fmaf(wr[d], s_x[c][oy + d][ox], s);
+            for (int d = 0; d < W; ++d) s = fma(wr[d], s_x[c][oy + d][ox], s);
             ring[W - 1][c] = s;
         }
         const int zo = zi - R;
         if (zo >= zb && own) {
-            const float inv = 1.f / (wxy * axis_wsum(zo, g.nz, R, wh, wfull));
-            float o3[3];
+            const T inv = T(1) / (wxy * axis_wsum_t<T>(zo, g.nz, R, wh, wfull));
+            T o3[3];
 #pragma unroll
             for (int c = 0; c < 3; ++c) {
-                float s = 0.f;
+                T s = 0;
 #pragma unroll
-                for (int d = 0; d < W; ++d) s = fmaf(wr[d], ring[d][c], s);
+                for (int d = 0; d < W; ++d) s = fma(wr[d], ring[d][c], s);
                 o3[c] = s * inv;
             }
             cons(x, y, zo, o3);
@@ -457,7 +484,8 @@ __device__ __forceinline__ void gauss_march3(const Geo& g, int x0, int y0, int z
 }
 
 // K3: dU = -r g / (|g|^2 + lambda) (Eq. 4) | -lr g (GD) | Adam step (precomputed),
-// smoothed with sigma_update, written to VS, max |dU_s| -> PairState.max_bits.
+// smoothed with sigma_update (fp64 sums), written to VS (fp32), max |dU_s|
+// of the stored values -> PairState.max_bits.
 template <int R>
 __global__ void __launch_bounds__(NT) k_step_smooth(Batch b, LmParams p, int chunk_len) {
     __shared__ float s_max[NT / 32];
@@ -471,27 +499,28 @@ __global__ void __launch_bounds__(NT) k_step_smooth(Batch b, LmParams p, int chu
     const int zb = blockIdx.y * chunk_len, ze = min(zb + chunk_len, g.nz);
     const float* __restrict__ G = b.G + (long long)pair * 3 * n;
     float* __restrict__ V = b.VS + (long long)pair * 3 * n;
-    const float r = (float)st->r_cur, lam = (float)st->lambda;
+    const double r = st->r_cur, lam = st->lambda;
     const int opt = p.optimizer;
-    const float lr = (float)p.gd_lr;
-    auto prod = [&](int gx, int gy, int gz, float* v) {
-        const long long o = g.at(gx, gy, gz);
-        const float a = __ldg(G + o), bb = __ldg(G + n + o), c = __ldg(G + 2 * n + o);
-        float s;
-        if (opt == WLM_OPT_LM) s = -r / (fmaf(a, a, fmaf(bb, bb, c * c)) + lam);
+    const double lr = p.gd_lr;
+    auto prod = [&](int gx, int gy, int gz, double* v) {
+        const int o = g.at(gx, gy, gz);
+        const double a = __ldg(G + o), bb = __ldg(G + n + o), c = __ldg(G + 2 * n + o);
+        double s;
+        if (opt == WLM_OPT_LM) s = -r / (fma(a, a, fma(bb, bb, c * c)) + lam);
         else if (opt == WLM_OPT_GD) s = -lr;
-        else s = 1.f;  // Adam step already in G
+        else s = 1.0;  // Adam step already in G
         v[0] = s * a; v[1] = s * bb; v[2] = s * c;
     };
     float mx = 0.f;
-    auto cons = [&](int x, int y, int z, const float* o3) {
-        const long long o = g.at(x, y, z);
-        V[o] = o3[0];
-        V[n + o] = o3[1];
-        V[2 * n + o] = o3[2];
-        mx = fmaxf(mx, fmaxf(fabsf(o3[0]), fmaxf(fabsf(o3[1]), fabsf(o3[2]))));
+    auto cons = [&](int x, int y, int z, const double* o3) {
+        const int o = g.at(x, y, z);
+        const float a = (float)o3[0], bb = (float)o3[1], c = (float)o3[2];
+        V[o] = a;
+        V[n + o] = bb;
+        V[2 * n + o] = c;
+        mx = fmaxf(mx, fmaxf(fabsf(a), fmaxf(fabsf(bb), fabsf(c))));
     };
-    gauss_march3<R>(g, x0, y0, zb, ze, p.wu, p.wu_full, prod, cons);
+    gauss_march3<R, double>(g, x0, y0, zb, ze, p.wud, p.wud_full, prod, cons);
     mx = warp_max(mx);
     if ((threadIdx.x & 31) == 0) s_max[threadIdx.x >> 5] = mx;
     __syncthreads();
@@ -505,6 +534,8 @@ __global__ void __launch_bounds__(NT) k_step_smooth(Batch b, LmParams p, int chu
 // K4: u'(x) = d(x) + u(x + d(x)), d = eps dU_s, eps = target / max(max|dU_s|,
 // floor) (Eq. 2, field.cpp:123-155), then Gaussian(sigma_warp); reads the
 // accepted buffer, writes the other one (ping-pong = free rejection restore).
+// eps, d = eps * dU_s, the resample and the smoothing sums are fp64; u' is
+// rounded to fp32 once on store.
 template <int R>
 __global__ void __launch_bounds__(NT) k_compose_smooth(Batch b, LmParams p, int chunk_len) {
     const int pair = blockIdx.z;
@@ -519,24 +550,23 @@ __global__ void __launch_bounds__(NT) k_compose_smooth(Batch b, LmParams p, int 
     const float* __restrict__ V = b.VS + (long long)pair * 3 * n;
     const float* __restrict__ U = b.U + ((long long)pair * 2 + cur) * 3 * n;
     float* __restrict__ UN = b.U + ((long long)pair * 2 + (1 - cur)) * 3 * n;
-    const float eps =
-        (float)(p.target / fmax((double)__uint_as_float(st->max_bits), p.step_floor));
-    auto prod = [&](int gx, int gy, int gz, float* v) {
-        const long long o = g.at(gx, gy, gz);
-        const float dx = eps * __ldg(V + o), dy = eps * __ldg(V + n + o),
-                    dz = eps * __ldg(V + 2 * n + o);
-        const Cell c = make_cell(g, gx, gy, gz, dx, dy, dz);
-        v[0] = dx + cell_sample(U, c);
-        v[1] = dy + cell_sample(U + n, c);
-        v[2] = dz + cell_sample(U + 2 * n, c);
+    const double eps = p.target / fmax((double)__uint_as_float(st->max_bits), p.step_floor);
+    auto prod = [&](int gx, int gy, int gz, double* v) {
+        const int o = g.at(gx, gy, gz);
+        const double dx = eps * __ldg(V + o), dy = eps * __ldg(V + n + o), dz = eps * __ldg(V + 2 * n + o);
+        double s[3];
+        sample3_d(U, n, g, gx, gy, gz, dx, dy, dz, s);
+        v[0] = dx + s[0];
+        v[1] = dy + s[1];
+        v[2] = dz + s[2];
     };
-    auto cons = [&](int x, int y, int z, const float* o3) {
-        const long long o = g.at(x, y, z);
-        UN[o] = o3[0];
-        UN[n + o] = o3[1];
-        UN[2 * n + o] = o3[2];
+    auto cons = [&](int x, int y, int z, const double* o3) {
+        const int o = g.at(x, y, z);
+        UN[o] = (float)o3[0];
+        UN[n + o] = (float)o3[1];
+        UN[2 * n + o] = (float)o3[2];
     };
-    gauss_march3<R>(g, x0, y0, zb, ze, p.ww, p.ww_full, prod, cons);
+    gauss_march3<R, double>(g, x0, y0, zb, ze, p.wwd, p.wwd_full, prod, cons);
 }
 
 // Adam, pointwise; t = accepted iterations + 1 at this level.
@@ -576,7 +606,7 @@ __device__ float det_at(const float* U, const Geo& g, int x, int y, int z, float
         if (p[a] >= 1 && p[a] + 1 <= nn[a] - 1) { q1[a] = p[a] + 1; q0[a] = p[a] - 1; }
         else if (p[a] == 0) { q1[a] = 1; q0[a] = 0; k = 1.f; }
         else { q1[a] = p[a]; q0[a] = p[a] - 1; k = 1.f; }
-        const long long i1 = g.at(q1[0], q1[1], q1[2]), i0 = g.at(q0[0], q0[1], q0[2]);
+        const int i1 = g.at(q1[0], q1[1], q1[2]), i0 = g.at(q0[0], q0[1], q0[2]);
 #pragma unroll
         for (int c = 0; c < 3; ++c) J[c][a] = k * scale * (__ldg(U + c * g.n + i1) - __ldg(U + c * g.n + i0));
     }
@@ -598,7 +628,7 @@ __global__ void k_jacobian_diag(Batch b, LmParams p) {
     if (st->done) return;
     const Geo g = b.g;
     const float* V = b.VS + (long long)pair * 3 * g.n;
-    const float eps = (float)(p.target / fmax((double)__uint_as_float(st->max_bits), p.step_floor));
+    const double eps = p.target / fmax((double)__uint_as_float(st->max_bits), p.step_floor);
     int xl, xh, yl, yh, zl, zh;
     interior(g.nx, xl, xh); interior(g.ny, yl, yh); interior(g.nz, zl, zh);
     const long long cx = xh - xl + 1, cy = yh - yl + 1, cz = zh - zl + 1;
@@ -644,21 +674,32 @@ __global__ void k_set_targets(PairState* st, int pairs, int iters) {
     st[i].done = iters <= 0;
 }
 
-// Deterministic per-pair means (fixed-order partials inside one CTA).
-__global__ void k_shifts(Batch b) {
+// Deterministic per-pair means: fixed chunking into kShiftBlocks CTAs, then a
+// fixed-order final sum (independent of scheduling).
+constexpr int kShiftBlocks = 256;
+
+__global__ void k_shift_partials(Batch b, double* part) {
     __shared__ double red[32];
-    const int pair = blockIdx.x;
+    const int pair = blockIdx.y, which = blockIdx.z;
     const long long n = b.g.n;
-    for (int which = 0; which < 2; ++which) {
-        const float* v = (which == 0 ? b.F : b.M) + (long long)pair * n;
-        double s = 0.0;
-        for (long long i = threadIdx.x; i < n; i += blockDim.x) s += (double)v[i];
-        const double t = block_sum(s, red);
-        if (threadIdx.x == 0) {
-            const float mean = (float)(t / (double)n);
-            if (which == 0) b.st[pair].shift_f = mean;
-            else b.st[pair].shift_m = mean;
-        }
+    const float* v = (which == 0 ? b.F : b.M) + (long long)pair * n;
+    const long long per = (n + kShiftBlocks - 1) / kShiftBlocks;
+    const long long lo = blockIdx.x * per, hi = min(n, lo + per);
+    double s = 0.0;
+    for (long long i = lo + threadIdx.x; i < hi; i += blockDim.x) s += (double)v[i];
+    const double t = block_sum(s, red);
+    if (threadIdx.x == 0) part[((long long)pair * 2 + which) * kShiftBlocks + blockIdx.x] = t;
+}
+
+__global__ void k_shift_final(Batch b, const double* part) {
+    __shared__ double red[32];
+    const int pair = blockIdx.x, which = blockIdx.y;
+    const double v = threadIdx.x < kShiftBlocks ? part[((long long)pair * 2 + which) * kShiftBlocks + threadIdx.x] : 0.0;
+    const double t = block_sum(v, red);
+    if (threadIdx.x == 0) {
+        const float mean = (float)(t / (double)b.g.n);
+        if (which == 0) b.st[pair].shift_f = mean;
+        else b.st[pair].shift_m = mean;
     }
 }
 
@@ -734,8 +775,19 @@ void launch_set_targets(const Batch& b, int iters, cudaStream_t s) {
 }
 
 void launch_shifts(const Batch& b, cudaStream_t s) {
-    k_shifts<<<b.pairs, 1024, 0, s>>>(b);
-    ++g_kernel_launches;
+    k_shift_partials<<<dim3(kShiftBlocks, b.pairs, 2), 256, 0, s>>>(b, b.shift_part);
+    k_shift_final<<<dim3(b.pairs, 2), kShiftBlocks, 0, s>>>(b, b.shift_part);
+    g_kernel_launches += 2;
+}
+
+void init_constants() {
+    static bool done = false;
+    if (done) return;
+    double inv[126];
+    inv[0] = 0.0;
+    for (int i = 1; i < 126; ++i) inv[i] = 1.0 / (double)i;
+    cudaMemcpyToSymbol(c_inv_count, inv, sizeof(inv));
+    done = true;
 }
 
 // ===========================================================================
@@ -760,10 +812,10 @@ __device__ Cell cell_at_point(const Geo& g, double px, double py, double pz) {
     c.finite = isfinite(px) && isfinite(py) && isfinite(pz);
     const AxisTap X = axis_tap_d(c.finite ? px : 0.0, g.nx), Y = axis_tap_d(c.finite ? py : 0.0, g.ny),
                   Z = axis_tap_d(c.finite ? pz : 0.0, g.nz);
-    const long long r00 = (long long)g.nx * ((long long)Y.i0 + (long long)g.ny * Z.i0);
-    const long long r10 = (long long)g.nx * ((long long)Y.i1 + (long long)g.ny * Z.i0);
-    const long long r01 = (long long)g.nx * ((long long)Y.i0 + (long long)g.ny * Z.i1);
-    const long long r11 = (long long)g.nx * ((long long)Y.i1 + (long long)g.ny * Z.i1);
+    const int r00 = g.nx * (Y.i0 + g.ny * Z.i0);
+    const int r10 = g.nx * (Y.i1 + g.ny * Z.i0);
+    const int r01 = g.nx * (Y.i0 + g.ny * Z.i1);
+    const int r11 = g.nx * (Y.i1 + g.ny * Z.i1);
     c.o000 = r00 + X.i0; c.o100 = r00 + X.i1; c.o010 = r10 + X.i0; c.o110 = r10 + X.i1;
     c.o001 = r01 + X.i0; c.o101 = r01 + X.i1; c.o011 = r11 + X.i0; c.o111 = r11 + X.i1;
     c.tx = X.t; c.ty = Y.t; c.tz = Z.t;

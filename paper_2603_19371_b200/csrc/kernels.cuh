@@ -46,6 +46,8 @@ struct LmParams {
     int Ru, Rw;            // smoothing radii (update, warp); 0 = identity
     float wu[8], ww[8];    // half-kernels w[|d|]
     float wu_full, ww_full;
+    double wud[8], wud_full;  // fp64 copies of the kernels (K3/K4 sum in fp64)
+    double wwd[8], wwd_full;
     int radius;            // LNCC window radius (template-dispatched: 2 only in v1)
 };
 
@@ -56,12 +58,13 @@ struct Batch {
     const float* F;   // [pair][n]
     const float* M;   // [pair][n]
     float* U;         // [pair][2][3][n] ping-pong warps
-    float* ABE;       // [pair][3][n]  LNCC window coefficients A, B, E
+    float* ABE;       // [pair][4][n]  LNCC window coefficients: A, B (fp32), E (fp64)
     float* G;         // [pair][3][n]  gradient g, Adam step in place
     float* VS;        // [pair][3][n]  smoothed step dU_s
     float* AM;        // [pair][3][n]  Adam first moment (or null)
     float* AV;        // [pair][3][n]  Adam second moment (or null)
     PairState* st;    // [pair]
+    double* shift_part; // [pair][2][256] scratch for the intensity shifts
     double* partials; // [pair][max_blocks]
     int max_blocks;
 };
@@ -94,6 +97,8 @@ void launch_begin_level(const Batch& b, const LmParams& p, int level, int reset_
 void launch_set_targets(const Batch& b, int iters, cudaStream_t s);
 // Intensity shifts (means of F and M per pair), deterministic.
 void launch_shifts(const Batch& b, cudaStream_t s);
+// Device constants (window-count reciprocals); idempotent.
+void init_constants();
 
 // ---- standalone field ops (fp32 SoA device buffers) ----
 void launch_compose(const float* u, const float* v, float eps, float* out, const Geo& g,

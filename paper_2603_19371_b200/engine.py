@@ -13,7 +13,7 @@ import ctypes as C
 import numpy as np
 
 from ._lib import Dims, LmState, RegConfig, StepLog, load
-from .warplm import Context, default_context, reg_config, trace_rows
+from .warplm import _LIVE_ENGINES, Context, default_context, reg_config, trace_rows
 
 
 class Engine:
@@ -28,6 +28,7 @@ class Engine:
         self.ctx.check(self.lib.wlm_engine_create(self.ctx.h, Dims(nx, ny, nz), self.pairs,
                                                   C.byref(self.cfg), C.byref(h)))
         self.h = h
+        _LIVE_ENGINES.add(self)
 
     @property
     def nvox(self):
@@ -100,9 +101,22 @@ class Engine:
         return trace_rows(rows[i] for i in range(n.value))
 
     def buffers(self):
-        ptrs = [C.c_void_p() for _ in range(5)]
+        ptrs = [C.c_void_p() for _ in range(6)]
         self._chk(self.lib.wlm_engine_buffers(self.h, *[C.byref(p) for p in ptrs]))
-        return dict(zip(("F", "M", "u", "g", "vs"), (p.value for p in ptrs)))
+        return dict(zip(("F", "M", "u", "g", "vs", "abe"), (p.value for p in ptrs)))
+
+    BUF = {"F": 0, "M": 1, "u": 2, "g": 3, "vs": 4, "abe": 5}
+
+    def read_buffer(self, name, pair=0):
+        """Host copy of one pair's engine buffer (F, M: (nz,ny,nx); u, g, vs,
+        abe: (3,nz,ny,nx)) -- test / debug hook."""
+        nch = 1 if name in ("F", "M") else 4 if name == "abe" else 3
+        out = np.empty((nch,) + self.shape, np.float32)
+        self._chk(self.lib.wlm_engine_read_buffer(self.h, self.BUF[name], pair, out.ctypes.data,
+                                                  out.size))
+        if name == "abe":  # A, B fp32 planes + E fp64 plane
+            return out[0], out[1], out[2:].reshape(-1).view(np.float64).reshape(self.shape)
+        return out[0] if nch == 1 else out
 
     def script_losses(self, losses):
         """losses: (pairs, n) float64 -- scripted-residual harness."""

@@ -27,7 +27,9 @@ component innermost (field.hpp:50-58).
 """
 from __future__ import annotations
 
+import atexit
 import ctypes as C
+import weakref
 from dataclasses import dataclass, field as dfield
 
 import numpy as np
@@ -52,6 +54,20 @@ def _p(a):
     return a.ctypes.data_as(_D)
 
 
+# Live handles, released in dependency order (engines, then contexts) before
+# the CUDA runtime tears down at interpreter exit.
+_LIVE_ENGINES: "weakref.WeakSet" = weakref.WeakSet()
+_LIVE_CONTEXTS: "weakref.WeakSet" = weakref.WeakSet()
+
+
+@atexit.register
+def _release_all():
+    for e in list(_LIVE_ENGINES):
+        e.close()
+    for c in list(_LIVE_CONTEXTS):
+        c.close()
+
+
 class Context:
     """One wlm_ctx: a CUDA stream + scratch on one device."""
 
@@ -62,6 +78,7 @@ class Context:
         if st != 0:
             raise WlmError(st, f"wlm_ctx_create(device={device}) failed: no usable CUDA device")
         self.h = h
+        _LIVE_CONTEXTS.add(self)
 
     def check(self, status):
         check(status, self.h)

@@ -232,6 +232,14 @@ def test_scripted_losses_lambda_trajectory(P, ctx):
     eng.close()
 
 
+def same_trace(a, b):
+    """Row-wise equality with NaN == NaN (jac_det_min is NaN when not logged)."""
+    if isinstance(a, list) and a and isinstance(a[0], list):
+        return len(a) == len(b) and all(same_trace(x, y) for x, y in zip(a, b))
+    return len(a) == len(b) and all(
+        all((x[k] == y[k]) or (x[k] != x[k] and y[k] != y[k]) for k in x) for x, y in zip(a, b))
+
+
 def test_batch_pairs_are_independent_and_deterministic(P, ctx):
     shape = (24, 28, 32)
     Fs, Ms = [], []
@@ -241,10 +249,10 @@ def test_batch_pairs_are_independent_and_deterministic(P, ctx):
     cfg = P.reg_config(nlevels=1, factors=[1], iters=[15])
     wb, trb, _ = run_engine(P, ctx, np.stack(Fs), np.stack(Ms), cfg, 15, pairs=3)
     wb2, trb2, _ = run_engine(P, ctx, np.stack(Fs), np.stack(Ms), cfg, 15, pairs=3)
-    assert np.array_equal(wb, wb2) and trb == trb2  # bit-identical reruns
+    assert np.array_equal(wb, wb2) and same_trace(trb, trb2)  # bit-identical reruns
     for s in range(3):
         w1, (t1,), _ = run_engine(P, ctx, Fs[s], Ms[s], cfg, 15)
-        assert np.array_equal(w1[0], wb[s]) and t1 == trb[s]
+        assert np.array_equal(w1[0], wb[s]) and same_trace(t1, trb[s])
 
 
 def test_adam_and_gd_paths(P, ctx):
