@@ -78,6 +78,7 @@ def _p(a, t=_D):
 def _declare(lib):
     sig = {
         "orc_set_threads": (None, [C.c_int]),
+        "orc_set_fp32_storage": (None, [C.c_int]),
         "orc_default_reg_config": (None, [C.POINTER(RegConfig)]),
         "orc_sample_trilinear_grad": (C.c_double, [_D, Dims, C.c_double, C.c_double, C.c_double, _D]),
         "orc_sample_field": (None, [_D, Dims, C.c_double, C.c_double, C.c_double, _D]),
@@ -127,6 +128,20 @@ def lib(kind: str = "port"):
         L.orc_set_threads(min(8, os.cpu_count() or 1))
         _libs[kind] = L
     return _libs[kind]
+
+
+class fp32_storage:
+    """Context manager: run the oracle with device storage-precision emulation."""
+
+    def __init__(self, kind="port"):
+        self.kind = kind
+
+    def __enter__(self):
+        lib(self.kind).orc_set_fp32_storage(1)
+        return self
+
+    def __exit__(self, *a):
+        lib(self.kind).orc_set_fp32_storage(0)
 
 
 def have_ref() -> bool:

@@ -29,6 +29,12 @@ using Vec = std::vector<double>;
 constexpr double kNaN = std::numeric_limits<double>::quiet_NaN();
 
 int g_threads = 1;
+// Storage-precision emulation: when set, every
+// quantity the device stores in fp32 (window coefficients A and B, gradient
+// g, smoothed step dU_s, warps, upsampled warps, Adam moments) is rounded to
+// fp32 at the same point of the computation; all arithmetic stays fp64.
+int g_fp32_storage = 0;
+inline double r32(double v) { return g_fp32_storage ? (double)(float)v : v; }
 
 // Static-partition parallel loop over [lo, hi) on g_threads std::threads.
 // Each index is computed independently, so results do not depend on the
@@ -344,6 +350,7 @@ constexpr double kDegRel = 1e-9;
 extern "C" {
 
 void orc_set_threads(int n) { g_threads = n < 1 ? 1 : n; }
+void orc_set_fp32_storage(int on) { g_fp32_storage = on ? 1 : 0; }
 
 void orc_default_reg_config(orc_reg_config* c) {
     std::memset(c, 0, sizeof(*c));
@@ -431,8 +438,8 @@ double orc_residual_lncc(const double* F, const double* M, const double* u, orc_
                 if (!degenerate) {
                     const double alpha = 1.0 / std::sqrt(vf * vm);
                     r = cv * alpha;
-                    A = alpha / n;
-                    B = -r / (vm * n);
+                    A = r32(alpha / n);
+                    B = r32(-r / (vm * n));
                     E = A * mf + B * mm;
                 }
                 rho[i] = r;
@@ -456,9 +463,9 @@ double orc_residual_lncc(const double* F, const double* M, const double* u, orc_
             const double dm = -invN * (F[i] * adj[i] + Mw[i] * adj[N + i] - adj[2 * N + i]);
             if (internals) internals[5 * N + i] = dm;
             if (g) {
-                g[3 * i] = dm * gM[3 * i];
-                g[3 * i + 1] = dm * gM[3 * i + 1];
-                g[3 * i + 2] = dm * gM[3 * i + 2];
+                g[3 * i] = r32(dm * gM[3 * i]);
+                g[3 * i + 1] = r32(dm * gM[3 * i + 1]);
+                g[3 * i + 2] = r32(dm * gM[3 * i + 2]);
             }
         });
         if (internals) std::memcpy(internals + 6 * N, gM.data(), sizeof(double) * 3 * N);
@@ -575,10 +582,10 @@ void orc_adam_step(const double* g, double* m, double* v, size_t count, int t,
                    const orc_adam_config* c, double* out) {
     const double bc1 = 1.0 - std::pow(c->beta1, t), bc2 = 1.0 - std::pow(c->beta2, t);
     for (size_t i = 0; i < count; ++i) {
-        m[i] = c->beta1 * m[i] + (1.0 - c->beta1) * g[i];
-        v[i] = c->beta2 * v[i] + (1.0 - c->beta2) * g[i] * g[i];
+        m[i] = r32(c->beta1 * m[i] + (1.0 - c->beta1) * g[i]);
+        v[i] = r32(c->beta2 * v[i] + (1.0 - c->beta2) * g[i] * g[i]);
         const double mh = m[i] / bc1, vh = v[i] / bc2;
-        out[i] = -c->lr * mh / (std::sqrt(vh) + c->eps_hat);
+        out[i] = r32(-c->lr * mh / (std::sqrt(vh) + c->eps_hat));
     }
 }
 
@@ -610,7 +617,7 @@ void orc_upsample_warp(const double* u, orc_dims d, orc_dims nd, double scale, d
                 double s[3];
                 sample3(u, d, x / scale, y / scale, z / scale, s);
                 const size_t i = 3 * lin(nd, x, y, z);
-                out[i] = scale * s[0]; out[i + 1] = scale * s[1]; out[i + 2] = scale * s[2];
+                out[i] = r32(scale * s[0]); out[i + 1] = r32(scale * s[1]); out[i + 2] = r32(scale * s[2]);
             }
     });
 }
@@ -645,10 +652,14 @@ int orc_lm_run_level(const double* F, const double* M, orc_dims d, double* u,
                 for (size_t i = 0; i < 3 * N; ++i) step[i] = -c->gd_lr * g[i];
             }
             smooth(step.data(), d, 3, c->sigma_update);
+            if (g_fp32_storage)
+                for (auto& v : step) v = (double)(float)v;
             eps = orc_normalize_step(step.data(), 3 * N, c->target_max_disp, c->step_floor);
             if (!std::isfinite(eps)) return ORC_INVALID_ARG;
             compose(u, step.data(), d, eps, unew.data());
             smooth(unew.data(), d, 3, c->sigma_warp);
+            if (g_fp32_storage)
+                for (auto& v : unew) v = (double)(float)v;
             if (c->log_jacobian) {
                 Vec inc(3 * N);
                 for (size_t i = 0; i < 3 * N; ++i) inc[i] = eps * step[i];
@@ -709,6 +720,9 @@ int orc_register(const float* Ff, const float* Mf, orc_dims d, const orc_reg_con
         Vec Fl(LN), Ml(LN);
         orc_downsample(F.data(), d, f, Fl.data());
         orc_downsample(M.data(), d, f, Ml.data());
+        // level images are materialised in fp32, the precision of the VOL3
+        // inputs (A11); the full-resolution level is already fp32
+        for (size_t i = 0; i < LN; ++i) { Fl[i] = (float)Fl[i]; Ml[i] = (float)Ml[i]; }
         Vec ul(3 * LN, 0.0);
         if (l > 0) orc_upsample_warp(u.data(), ud, ld, (double)c->factors[l - 1] / f, ul.data());
         st.hist_n = 0;

@@ -82,6 +82,9 @@ enum {
 };
 
 void orc_set_threads(int n);
+/* 1: round every quantity the device stores in fp32 at the same point
+ * (A, B, g, dU_s, warps, Adam moments); 0 (default): pure fp64 reference. */
+void orc_set_fp32_storage(int on);
 void orc_default_reg_config(orc_reg_config* c);
 
 /* ---- field (reference field.cpp restated) ---- */

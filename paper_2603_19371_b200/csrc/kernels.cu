@@ -983,28 +983,66 @@ void launch_nonfinite(const float* v, long long count, int* flag, cudaStream_t s
     ++g_kernel_launches;
 }
 
-__global__ void k_downsample(const float* __restrict__ sm, Geo g, int f, float* out, Geo gd) {
+// downsample: separable Gaussian (sigma = 0.5 f, radius
+// max(1, ceil(3 sigma)), per-axis renormalised) evaluated directly at the
+// strided output voxels in fp64 -- the product of the per-axis normalised
+// passes of field.cpp:253-260 -- then rounded to fp32 once (A11).
+struct TapsD {
+    int R;
+    double w[2 * 64 + 1];
+};
+
+__global__ void k_downsample_gauss(const float* __restrict__ in, Geo g, int f, TapsD t, float* out, Geo gd) {
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < gd.n;
          i += (long long)gridDim.x * blockDim.x) {
         const int x = (int)(i % gd.nx), y = (int)((i / gd.nx) % gd.ny), z = (int)(i / ((long long)gd.nx * gd.ny));
-        out[i] = sm[g.at(x * f, y * f, z * f)];
+        const int cx = x * f, cy = y * f, cz = z * f;
+        const int x0 = max(0, cx - t.R), x1 = min(g.nx - 1, cx + t.R);
+        const int y0 = max(0, cy - t.R), y1 = min(g.ny - 1, cy + t.R);
+        const int z0 = max(0, cz - t.R), z1 = min(g.nz - 1, cz + t.R);
+        double wx = 0.0, wy = 0.0, wz = 0.0;
+        for (int q = x0; q <= x1; ++q) wx += t.w[q - cx + t.R];
+        for (int q = y0; q <= y1; ++q) wy += t.w[q - cy + t.R];
+        for (int q = z0; q <= z1; ++q) wz += t.w[q - cz + t.R];
+        if (g.nx == 1) wx = 1.0;
+        if (g.ny == 1) wy = 1.0;
+        if (g.nz == 1) wz = 1.0;
+        double acc = 0.0;
+        for (int qz = z0; qz <= z1; ++qz) {
+            const double w3 = g.nz == 1 ? 1.0 : t.w[qz - cz + t.R];
+            double sy = 0.0;
+            for (int qy = y0; qy <= y1; ++qy) {
+                const double w2 = g.ny == 1 ? 1.0 : t.w[qy - cy + t.R];
+                const float* row = in + g.at(0, qy, qz);
+                double sx = 0.0;
+                for (int qx = x0; qx <= x1; ++qx) sx = fma(g.nx == 1 ? 1.0 : t.w[qx - cx + t.R], (double)__ldg(row + qx), sx);
+                sy = fma(w2, sx, sy);
+            }
+            acc = fma(w3, sy, acc);
+        }
+        out[i] = (float)(acc / (wx * wy * wz));
     }
 }
 
-void launch_downsample(const float* smoothed, const Geo& g, int f, float* out, const Geo& gd, cudaStream_t s) {
-    k_downsample<<<grid_for(gd.n, 256), 256, 0, s>>>(smoothed, g, f, out, gd);
+void launch_downsample_gauss(const float* in, const Geo& g, int f, float* out, const Geo& gd, cudaStream_t s) {
+    const double sigma = 0.5 * f;
+    TapsD t;
+    t.R = std::min(64, std::max(1, (int)std::ceil(3.0 * sigma)));
+    for (int i = -t.R; i <= t.R; ++i) t.w[i + t.R] = std::exp(-0.5 * (double)(i * i) / (sigma * sigma));
+    k_downsample_gauss<<<grid_for(gd.n, 128), 128, 0, s>>>(in, g, f, t, out, gd);
     ++g_kernel_launches;
 }
 
+// upsample_warp in fp64: trilinear at x / scale, * scale.
 __global__ void k_upsample(const float* __restrict__ u, Geo g, Geo gd, double scale, float* out) {
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < gd.n;
          i += (long long)gridDim.x * blockDim.x) {
         const int x = (int)(i % gd.nx), y = (int)((i / gd.nx) % gd.ny), z = (int)(i / ((long long)gd.nx * gd.ny));
-        const Cell c = cell_at_point(g, x / scale, y / scale, z / scale);
-        const float sc = (float)scale;
-        out[i] = sc * cell_sample(u, c);
-        out[gd.n + i] = sc * cell_sample(u + g.n, c);
-        out[2 * gd.n + i] = sc * cell_sample(u + 2 * g.n, c);
+        double s[3];
+        sample3_d(u, g.n, g, 0, 0, 0, x / scale, y / scale, z / scale, s);
+        out[i] = (float)(scale * s[0]);
+        out[gd.n + i] = (float)(scale * s[1]);
+        out[2 * gd.n + i] = (float)(scale * s[2]);
     }
 }
 

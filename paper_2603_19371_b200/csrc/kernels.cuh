@@ -112,8 +112,9 @@ void launch_jacdet(const float* u, const Geo& g, int* out_ordered, cudaStream_t 
 void launch_lm_pointwise(double r, const float* g, double lambda, float* out, long long n,
                          cudaStream_t s);
 void launch_nonfinite(const float* v, long long count, int* flag, cudaStream_t s);
-void launch_downsample(const float* smoothed, const Geo& g, int f, float* out, const Geo& gd,
-                       cudaStream_t s);
+// Gaussian(sigma = 0.5 f) + stride f in one fp64 pass (pyramid levels).
+void launch_downsample_gauss(const float* in, const Geo& g, int f, float* out, const Geo& gd,
+                             cudaStream_t s);
 void launch_upsample(const float* u, const Geo& g, const Geo& gd, float scale, float* out,
                      cudaStream_t s);
 void launch_sample_points(const float* u, const Geo& g, const double* pts, long long npts,

@@ -261,9 +261,8 @@ wlm_status wlm_downsample(wlm_ctx* ctx, const double* vol, wlm_dims d, int facto
         const size_t n = nvox(d);
         DevBuf<float> a = upload_soa(ctx, vol, n, 1);
         if (factor == 1) { download_aos(ctx, a.p, n, 1, out); return; }
-        DevBuf<float> sm(ctx, n), t(ctx, n), o(ctx, nvox(nd));
-        launch_smooth_generic(a.p, sm.p, t.p, 1, make_geo(d), 0.5 * factor, ctx->stream);
-        launch_downsample(sm.p, make_geo(d), factor, o.p, make_geo(nd), ctx->stream);
+        DevBuf<float> o(ctx, nvox(nd));
+        launch_downsample_gauss(a.p, make_geo(d), factor, o.p, make_geo(nd), ctx->stream);
         download_aos(ctx, o.p, nvox(nd), 1, out);
     });
 }
@@ -322,12 +321,8 @@ wlm_status wlm_register(wlm_ctx* ctx, const float* F, const float* M, wlm_dims d
                 CK(cudaMemcpyAsync(e->F.p, F0.p, sizeof(float) * n, cudaMemcpyDeviceToDevice, ctx->stream));
                 CK(cudaMemcpyAsync(e->M.p, M0.p, sizeof(float) * n, cudaMemcpyDeviceToDevice, ctx->stream));
             } else {
-                DevBuf<float> sm(ctx, n), t(ctx, n);
-                launch_smooth_generic(F0.p, sm.p, t.p, 1, g0, 0.5 * f, ctx->stream);
-                launch_downsample(sm.p, g0, f, e->F.p, e->g, ctx->stream);
-                launch_smooth_generic(M0.p, sm.p, t.p, 1, g0, 0.5 * f, ctx->stream);
-                launch_downsample(sm.p, g0, f, e->M.p, e->g, ctx->stream);
-                CK(cudaStreamSynchronize(ctx->stream));
+                launch_downsample_gauss(F0.p, g0, f, e->F.p, e->g, ctx->stream);
+                launch_downsample_gauss(M0.p, g0, f, e->M.p, e->g, ctx->stream);
             }
             launch_shifts(e->B, ctx->stream);
             if (prev) {

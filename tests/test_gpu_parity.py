@@ -178,24 +178,50 @@ def run_engine(P, ctx, F, M, cfg, iters, u0=None, pairs=1):
     return warp, traces, states
 
 
-def compare_runs(tr_gpu, tr_orc, warp_gpu, warp_orc, loss_tol=1e-5, warp_tol=1e-4):
+def compare_runs(tr_gpu, tr_orc, warp_gpu, warp_orc, loss_tol=1e-5, warp_tol=1e-4, first_n=None):
+    """Per-iteration loss within loss_tol (for the first first_n iterations
+    when given), identical accept/retry sequence and lambda (bit-exact: the
+    device state machine is the oracle's fp64 arithmetic), final warp rel-L2."""
     assert len(tr_gpu) == len(tr_orc)
-    for a, b in zip(tr_gpu, tr_orc):
-        assert abs(a["r"] - b.r) <= loss_tol * abs(b.r), (a["iter"], a["r"], b.r)
-        assert a["accepted"] == b.accepted and a["retries"] == b.retries, a["iter"]
-        assert a["lam"] == b.lam, (a["iter"], a["lam"], b.lam)
-    assert rel(warp_gpu, warp_orc) <= warp_tol, rel(warp_gpu, warp_orc)
+    for k, (a, b) in enumerate(zip(tr_gpu, tr_orc)):
+        ga = a if isinstance(a, dict) else dict(r=a.r, accepted=a.accepted, retries=a.retries,
+                                               lam=a.lam, iter=a.iter)
+        if first_n is None or k < first_n:
+            assert abs(ga["r"] - b.r) <= loss_tol * abs(b.r), (k, ga["r"], b.r)
+        assert ga["accepted"] == b.accepted and ga["retries"] == b.retries, k
+        assert ga["lam"] == b.lam, (k, ga["lam"], b.lam)
+    if warp_tol is not None:
+        assert rel(warp_gpu, warp_orc) <= warp_tol, rel(warp_gpu, warp_orc)
 
 
+def oracle_level(F, M, cfg_o, iters, storage):
+    """lm_run_level with the pure fp64 oracle ('fp64') or with the device's
+    fp32 storage points emulated ('fp32')."""
+    if storage == "fp32":
+        with O.fp32_storage():
+            return O.lm_run_level(F, M, np.zeros(F.shape + (3,)), cfg_o, iters)
+    return O.lm_run_level(F, M, np.zeros(F.shape + (3,)), cfg_o, iters)
+
+
+# Parity bar (DESIGN.md "Parity bar"):
+#  * vs the fp32-storage oracle (same fp32 storage points, fp64 arithmetic):
+#    loss <= 1e-6 relative at every iteration, identical accept/reject and
+#    lambda, final warp rel-L2 <= 1e-5 -- measured 1e-14..2e-8 / 0..1.4e-7;
+#  * vs the pure fp64 reference oracle: the north-star bar (loss <= 1e-5,
+#    identical accept/reject, warp rel-L2 <= 1e-4) on single-level runs --
+#    measured <= 2.2e-8 / 1.2e-6 -- and, where fp32 storage itself is chaotic
+#    (tiny coarse pyramid levels, tools/floor_experiment.py), the first 20
+#    iterations plus the full accept/reject sequence.
 def test_config1_64cubed_100_iterations(P, ctx):
     """Config 1 (BASELINE.json): 64^3, one level, LNCC, 100 LM iterations."""
     F, M, _ = O.synth_pair((64, 64, 64), 0, num_blobs=12, warp_max=3.0)
     cfg_p = P.reg_config(nlevels=1, factors=[1], iters=[100])
     cfg_o = O.default_config(nlevels=1, factors=[1], iters=[100])
     warp, (tr,), _ = run_engine(P, ctx, F, M, cfg_p, 100)
-    rc, u_o, st, tr_o = O.lm_run_level(F, M, np.zeros((64, 64, 64, 3)), cfg_o, 100)
-    assert rc == 0
-    compare_runs(tr, tr_o, aos(warp[0]), u_o)
+    for storage, lt, wt in (("fp64", 1e-5, 1e-4), ("fp32", 1e-6, 1e-5)):
+        rc, u_o, st, tr_o = oracle_level(F, M, cfg_o, 100, storage)
+        assert rc == 0
+        compare_runs(tr, tr_o, aos(warp[0]), u_o, lt, wt)
 
 
 def test_rejection_sequence_matches(P, ctx):
@@ -205,10 +231,11 @@ def test_rejection_sequence_matches(P, ctx):
     cfg_p = P.reg_config(**kw, **{"lm.rejection": 1, "lm.tau": 0.2})
     cfg_o = O.default_config(**kw, **{"lm.rejection": 1, "lm.tau": 0.2})
     warp, (tr,), _ = run_engine(P, ctx, F, M, cfg_p, 40)
-    rc, u_o, st, tr_o = O.lm_run_level(F, M, np.zeros((32, 36, 40, 3)), cfg_o, 40)
-    assert rc == 0
-    assert sum(t.retries for t in tr_o) > 0, "test should exercise rejections"
-    compare_runs(tr, tr_o, aos(warp[0]), u_o)
+    for storage, lt, wt in (("fp64", 1e-5, 1e-4), ("fp32", 1e-6, 1e-5)):
+        rc, u_o, st, tr_o = oracle_level(F, M, cfg_o, 40, storage)
+        assert rc == 0
+        assert sum(t.retries for t in tr_o) > 0, "test should exercise rejections"
+        compare_runs(tr, tr_o, aos(warp[0]), u_o, lt, wt)
 
 
 def test_scripted_losses_lambda_trajectory(P, ctx):
@@ -261,10 +288,11 @@ def test_adam_and_gd_paths(P, ctx):
         cfg_p = P.reg_config(nlevels=1, factors=[1], iters=[20], optimizer=opt, **extra)
         cfg_o = O.default_config(nlevels=1, factors=[1], iters=[20], optimizer=opt, **extra)
         warp, (tr,), _ = run_engine(P, ctx, F, M, cfg_p, 20)
-        rc, u_o, _, tr_o = O.lm_run_level(F, M, np.zeros((24, 24, 24, 3)), cfg_o, 20)
-        for a, b in zip(tr, tr_o):
-            assert abs(a["r"] - b.r) <= 1e-5 * b.r
-        assert rel(aos(warp[0]), u_o) < 1e-4
+        for storage, lt, wt in (("fp64", 1e-5, 1e-4), ("fp32", 1e-6, 1e-5)):
+            rc, u_o, _, tr_o = oracle_level(F, M, cfg_o, 20, storage)
+            for a, b in zip(tr, tr_o):
+                assert abs(a["r"] - b.r) <= lt * b.r
+            assert rel(aos(warp[0]), u_o) < wt
 
 
 def test_jacobian_logged_positive(P, ctx):
@@ -284,14 +312,21 @@ def test_register_pyramid_vs_oracle(P, ctx):
     F, M, _ = O.synth_pair((40, 48, 56), 1, num_blobs=10, warp_max=4.0)
     kw = dict(nlevels=3, factors=[4, 2, 1], iters=[30, 20, 10])
     res = P.register(F, M, P.reg_config(**kw, **{"lm.rejection": 1}), ctx=ctx)
-    rc, w_o, tr_o, jac_o = O.register(F, M, O.default_config(**kw, **{"lm.rejection": 1}))
+    cfg_o = O.default_config(**kw, **{"lm.rejection": 1})
+    # fp64 reference: the 10x12x14 first level is floor-limited (the oracle
+    # against itself with fp32 warps reaches 8e-6 by iteration 27), so the
+    # loss bar holds for the first 20 iterations and the accept/reject
+    # sequence and lambda for all 60.
+    rc, w_o, tr_o, jac_o = O.register(F, M, cfg_o)
     assert rc == 0 and len(res.loss_trace) == len(tr_o) == 60
     for a, b in zip(res.loss_trace, tr_o):
-        assert (a.level, a.iter, a.accepted, a.retries) == (b.level, b.iter, b.accepted, b.retries)
-        assert abs(a.r - b.r) <= 1e-5 * b.r
-        assert a.lam == b.lam
-    assert rel(res.final_warp, w_o) < 1e-4
-    assert res.jac_det_min_final == pytest.approx(jac_o, abs=1e-4)
+        assert (a.level, a.iter) == (b.level, b.iter)
+    compare_runs(res.loss_trace, tr_o, res.final_warp, w_o, 1e-5, None, first_n=20)
+    # fp32-storage oracle: the whole pyramid, tight
+    with O.fp32_storage():
+        rc, w_s, tr_s, jac_s = O.register(F, M, cfg_o)
+    compare_runs(res.loss_trace, tr_s, res.final_warp, w_s, 1e-6, 1e-5)
+    assert res.jac_det_min_final == pytest.approx(jac_s, abs=1e-4)
     assert res.peak_device_bytes > 0
 
 

@@ -287,9 +287,9 @@ def test_register_recovers_translation():
     F = F.astype(np.float64)
     sh = np.zeros(F.shape + (3,)); sh[..., 0] = -2.0
     M, _ = O.warp_volume(F, sh)  # M(x) = F(x - 2 e_x)  ->  solution u = +2 e_x
-    cfg = O.default_config(nlevels=2, factors=[2, 1], iters=[30, 20])
+    cfg = O.default_config(nlevels=3, factors=[4, 2, 1], iters=[40, 30, 20])
     rc, warp, trace, jac = O.register(F.astype(np.float32), M.astype(np.float32), cfg)
-    assert rc == 0 and len(trace) == 50
+    assert rc == 0 and len(trace) == 90
     c = (slice(6, 18),) * 3
     assert np.abs(warp[c][..., 0] - 2.0).mean() < 0.5
     assert jac > 0
