@@ -1,0 +1,971 @@
+// hot_kernels.cu -- the four kernels of one LM attempt
+// and the device-side loss / damping / rejection state machine (K5).
+//
+// Schedule (hot.cuh): a CTA owns a 32 x 8 column of output voxels and a chunk
+// of z planes.  Per input plane it
+//   * produces an fp64 halo tile in shared memory from inputs that were
+//     prefetched into registers two planes ahead (dense rows) and one plane
+//     ahead (data-dependent gathers),
+//   * filters it along x (shared memory) and y (shared memory -> registers),
+//   * and along z through a statically indexed register ring (the z loop is
+//     unrolled by the ring length, so the ring never moves).
+// Every global access is a unit-stride row of one SoA plane.  Sums are fp64
+// (DESIGN.md "Precision"); reductions are fixed-order.
+#include <cfloat>
+#include <climits>
+
+#include "hot.cuh"
+#include "kernels.cuh"
+
+namespace wlm {
+
+using hot::NT;
+using hot::TX;
+using hot::TY;
+
+namespace {
+__host__ __device__ inline int cdiv(int a, int b) { return (a + b - 1) / b; }
+}  // namespace
+
+__constant__ double c_inv_count[126];  // 1/n for truncated window counts n <= 125
+
+void init_constants() {
+    static bool done = false;
+    if (done) return;
+    double inv[126];
+    inv[0] = 0.0;
+    for (int i = 1; i < 126; ++i) inv[i] = 1.0 / (double)i;
+    cudaMemcpyToSymbol(c_inv_count, inv, sizeof(inv));
+    done = true;
+}
+
+// ---------------------------------------------------------------------------
+// Loss / damping / rejection state machine, run by one
+// thread of the last CTA of the evaluation kernel.  Identical fp64
+// arithmetic to the oracle (oracle.cpp orc_update_damping /
+// attempt_rejected), so the lambda trajectory is bit-identical whenever the
+// accept/reject decisions agree.
+__device__ void update_damping_dev(PairState* st, const LmParams& p, double r) {
+    const bool bad = st->hist_n == 0 || r > st->L1;
+    double lam = bad ? p.mu_plus * st->lambda : p.mu_minus * st->lambda;
+    if (p.lambda_max > 0.0 && isfinite(p.lambda_max)) lam = fmin(lam, p.lambda_max);
+    st->lambda = fmax(lam, 1e-12);
+    st->L2 = st->L1;
+    st->L1 = r;
+    st->hist_n = min(st->hist_n + 1, 2);
+}
+
+__device__ bool rejection_fires(const PairState* st, const LmParams& p, double r) {
+    return p.rejection && st->hist_n >= 2 && (r - st->L1) > p.tau * fabs(st->L1 - st->L2);
+}
+
+__device__ void finalize_pair(PairState* st, const LmParams& p, int mode, double lncc, int pair) {
+    double r = 1.0 - lncc;
+    if (mode == 0) {
+        st->r_cur = r;
+        st->lncc_cur = lncc;
+        if (!isfinite(r)) { st->status = WLM_NONFINITE; st->done = 1; }
+        st->max_bits = 0u;
+        st->jac_bits = 0x7f800000;  // +inf
+        return;
+    }
+    if (p.script && p.script_n > 0) {
+        r = p.script[(long long)pair * p.script_n + min(st->attempt, p.script_n - 1)];
+        lncc = 1.0 - r;
+    }
+    st->attempt += 1;
+    st->r_try = r;
+    st->lncc_try = lncc;
+    const double maxv = (double)__uint_as_float(st->max_bits);
+    const double eps = p.target / fmax(maxv, p.step_floor);
+    if (!isfinite(r)) {  // abort
+        st->status = WLM_NONFINITE;
+        st->done = 1;
+        return;
+    }
+    bool rej = false;
+    if (p.optimizer == WLM_OPT_LM && st->retries < p.max_retries && rejection_fires(st, p, r)) {
+        double lam = p.mu_plus * st->lambda;
+        if (p.lambda_max > 0.0 && isfinite(p.lambda_max)) lam = fmin(lam, p.lambda_max);
+        st->lambda = lam;
+        st->retries += 1;
+        rej = true;
+    }
+    if (rej) {
+        st->last_rejected = 1;
+    } else {
+        const bool forced = p.optimizer == WLM_OPT_LM && st->retries >= p.max_retries &&
+                            rejection_fires(st, p, r);
+        if (p.optimizer == WLM_OPT_LM) update_damping_dev(st, p, r);
+        st->cur ^= 1;
+        st->r_cur = r;
+        st->lncc_cur = lncc;
+        st->last_rejected = 0;
+        if (p.trace && st->trace_len < p.trace_cap) {
+            wlm_step_log* row = p.trace + (long long)pair * p.trace_cap + st->trace_len;
+            row->level = st->level;
+            row->iter = st->iter;
+            row->loss_raw = lncc;
+            row->r = r;
+            row->lambda = p.optimizer == WLM_OPT_LM ? st->lambda : 0.0;
+            row->eps = eps;
+            row->accepted = forced ? 0 : 1;
+            row->retries = st->retries;
+            row->jac_det_min = p.log_jacobian ? (double)ordered_to_float(st->jac_bits)
+                                              : __longlong_as_double(0x7ff8000000000000ll);
+            st->trace_len += 1;
+        }
+        st->iter += 1;
+        st->retries = 0;
+        if (st->iter >= st->iters_target) st->done = 1;
+    }
+    st->max_bits = 0u;
+    st->jac_bits = 0x7f800000;
+}
+
+// Block-wide fixed-order double sum (result valid in thread 0).
+static __device__ double block_sum(double v, double* red) {
+    v = warp_sum(v);
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    if (lane == 0) red[w] = v;
+    __syncthreads();
+    double s = 0.0;
+    if (threadIdx.x == 0)
+        for (int i = 0; i < (int)(blockDim.x >> 5); ++i) s += red[i];
+    __syncthreads();
+    return s;
+}
+
+// Geometry shared by the hot kernels.
+struct Tile {
+    int x0, y0, zb, ze;
+    int ox, oy, x, y;
+    bool own;
+    int nxy;
+    __device__ __forceinline__ void init(const Geo& g, int chunk_len) {
+        const int tiles_x = cdiv(g.nx, TX);
+        x0 = (blockIdx.x % tiles_x) * TX;
+        y0 = (blockIdx.x / tiles_x) * TY;
+        zb = blockIdx.y * chunk_len;
+        ze = min(zb + chunk_len, g.nz);
+        ox = threadIdx.x & 31;
+        oy = threadIdx.x >> 5;
+        x = x0 + ox;
+        y = y0 + oy;
+        own = x < g.nx && y < g.ny;
+        nxy = g.nx * g.ny;
+    }
+};
+
+// Trilinear cell of a sample at integer voxel (x,y,z) displaced by float u,
+// fp64 weights, 32-bit corner offsets (field.cpp:19-39 in split form).
+struct CellD {
+    int o[8];
+    double tx, ty, tz;
+    bool ox_, oy_, oz_;  // axis outside (gradient 0)
+    bool finite;
+};
+
+__device__ __forceinline__ void make_cell_d(CellD& c, const Geo& g, int x, int y, int z, float ux, float uy,
+                                            float uz) {
+    c.finite = isfinite(ux) && isfinite(uy) && isfinite(uz);
+    const AxisTapD X = axis_tap_dd(x, c.finite ? ux : 0.f, g.nx);
+    const AxisTapD Y = axis_tap_dd(y, c.finite ? uy : 0.f, g.ny);
+    const AxisTapD Z = axis_tap_dd(z, c.finite ? uz : 0.f, g.nz);
+    const int r00 = g.nx * (Y.i0 + g.ny * Z.i0), r10 = g.nx * (Y.i1 + g.ny * Z.i0);
+    const int r01 = g.nx * (Y.i0 + g.ny * Z.i1), r11 = g.nx * (Y.i1 + g.ny * Z.i1);
+    c.o[0] = r00 + X.i0; c.o[1] = r00 + X.i1; c.o[2] = r10 + X.i0; c.o[3] = r10 + X.i1;
+    c.o[4] = r01 + X.i0; c.o[5] = r01 + X.i1; c.o[6] = r11 + X.i0; c.o[7] = r11 + X.i1;
+    c.tx = X.t; c.ty = Y.t; c.tz = Z.t;
+    c.ox_ = X.outside; c.oy_ = Y.outside; c.oz_ = Z.outside;
+}
+
+// Value (+ gradient) of the trilinear interpolant from 8 fp32 corners, fp64,
+// collapse order of field.cpp:47-90.
+template <bool GRAD>
+__device__ __forceinline__ double lerp_cell(const CellD& c, const float* v, double* grad) {
+    const double a = v[0], b = v[1], cc = v[2], e = v[3], f = v[4], h = v[5], k = v[6], l = v[7];
+    const double d00 = b - a, d10 = e - cc, d01 = h - f, d11 = l - k;
+    const double v00 = fma(c.tx, d00, a), v10 = fma(c.tx, d10, cc);
+    const double v01 = fma(c.tx, d01, f), v11 = fma(c.tx, d11, k);
+    const double s0 = fma(c.ty, v10 - v00, v00), s1 = fma(c.ty, v11 - v01, v01);
+    if (GRAD) {
+        const double gx0 = fma(c.ty, d10 - d00, d00), gx1 = fma(c.ty, d11 - d01, d01);
+        grad[0] = c.ox_ ? 0.0 : fma(c.tz, gx1 - gx0, gx0);
+        const double gy0 = v10 - v00, gy1 = v11 - v01;
+        grad[1] = c.oy_ ? 0.0 : fma(c.tz, gy1 - gy0, gy0);
+        grad[2] = c.oz_ ? 0.0 : s1 - s0;
+    }
+    return fma(c.tz, s1 - s0, s0);
+}
+
+constexpr double kNaN64 = __builtin_nan("");
+
+// ---------------------------------------------------------------------------
+// K1: warp + LNCC forward.
+//   halo tile (H = R): f' = F - shift_f, m' = M(x + u(x)) - shift_m   (fp64)
+//   box sums S_f, S_m, S_ff, S_mm, S_fm over the truncated window      (fp64)
+//   rho = c / sqrt(vf vm); A = 1/(n sqrt(vf vm)); B = -rho/(n vm)  -> fp32
+//   E = A' mu_f' + B' mu_m'  (fp64, from the rounded A', B', so K2's
+//   f' S_A + m' S_B - S_E cancels exactly);  sum(rho) -> per-CTA partial.
+template <int R>
+__global__ void __launch_bounds__(NT, 2) k_lncc_fwd(Batch b, LmParams p, int mode, int chunk_len) {
+    using It = hot::Items<R>;
+    constexpr int IW = It::IW, IH = It::IH, NI = It::NI, SL = It::SLOTS, W = 2 * R + 1;
+    constexpr int XS = (IH * TX + NT - 1) / NT;  // x-pass items per thread
+    __shared__ double s_f[2][NI], s_m[2][NI];
+    __shared__ double s_x[5][IH][TX];
+    __shared__ double s_red[NT / 32];
+    __shared__ int s_last;
+
+    const int pair = blockIdx.z;
+    PairState* st = b.st + pair;
+    if (st->done) return;
+    const Geo g = b.g;
+    const long long n = g.n;
+    Tile t;
+    t.init(g, chunk_len);
+    const int buf = mode == 0 ? st->cur : 1 - st->cur;
+    const float* __restrict__ F = b.F + (long long)pair * n;
+    const float* __restrict__ M = b.M + (long long)pair * n;
+    const float* __restrict__ U = b.U + ((long long)pair * 2 + buf) * 3 * n;
+    float* __restrict__ Aout = b.ABE + (long long)pair * 4 * n;
+    float* __restrict__ Bout = Aout + n;
+    double* __restrict__ Eout = reinterpret_cast<double*>(Aout + 2 * n);
+    const double shf = st->shift_f, shm = st->shift_m;
+    It it;
+    it.init(t.x0, t.y0, g.nx, g.ny);
+    const int cxy = t.own ? axis_count(t.x, g.nx, R) * axis_count(t.y, g.ny, R) : 1;
+    const int ooff = t.x + g.nx * t.y;
+
+    // pipeline registers: dense rows of plane z+1 (d1) and z+2 (d2); the 8
+    // gathered M corners of plane z+1 (gc).  The cell geometry is recomputed
+    // from d1 when the gather completes (fewer live registers).
+    float d1u[SL][3], d1f[SL], d2u[SL][3], d2f[SL];
+    float gc[SL][8];
+
+    auto load_dense = [&](int z, float (&du)[SL][3], float (&df)[SL]) {
+        const bool zin = z >= 0 && z < g.nz;
+        const int po = z * t.nxy;
+#pragma unroll
+        for (int s = 0; s < SL; ++s) {
+            if (zin && it.goff[s] >= 0) {
+                const int o = po + it.goff[s];
+                du[s][0] = __ldg(U + o);
+                du[s][1] = __ldg(U + n + o);
+                du[s][2] = __ldg(U + 2 * n + o);
+                df[s] = __ldg(F + o);
+            } else {
+                du[s][0] = du[s][1] = du[s][2] = 0.f;
+                df[s] = 0.f;
+            }
+        }
+    };
+    auto issue_gather = [&](int z) {
+        const bool zin = z >= 0 && z < g.nz;
+#pragma unroll
+        for (int s = 0; s < SL; ++s) {
+            if (zin && it.goff[s] >= 0) {
+                CellD c;
+                make_cell_d(c, g, it.gx[s], it.gy[s], z, d1u[s][0], d1u[s][1], d1u[s][2]);
+#pragma unroll
+                for (int k = 0; k < 8; ++k) gc[s][k] = __ldg(M + c.o[k]);
+            }
+        }
+    };
+    auto complete = [&](int z, int sb) {
+        const bool zin = z >= 0 && z < g.nz;
+#pragma unroll
+        for (int s = 0; s < SL; ++s) {
+            if (it.sidx[s] < 0) continue;
+            double fv = 0.0, mv = 0.0;
+            if (zin && it.goff[s] >= 0) {
+                CellD c;
+                make_cell_d(c, g, it.gx[s], it.gy[s], z, d1u[s][0], d1u[s][1], d1u[s][2]);
+                mv = c.finite ? lerp_cell<false>(c, gc[s], nullptr) - shm : kNaN64;
+                fv = (double)d1f[s] - shf;
+            }
+            s_f[sb][it.sidx[s]] = fv;
+            s_m[sb][it.sidx[s]] = mv;
+        }
+    };
+
+    double ring[W][5];
+    double S[5];
+#pragma unroll
+    for (int d = 0; d < W; ++d)
+#pragma unroll
+        for (int c = 0; c < 5; ++c) ring[d][c] = 0.0;
+#pragma unroll
+    for (int c = 0; c < 5; ++c) S[c] = 0.0;
+    double rho_acc = 0.0;
+
+    const int z0 = t.zb - R, z1 = t.ze + R;  // input planes [z0, z1)
+    load_dense(z0, d1u, d1f);
+    issue_gather(z0);
+    complete(z0, 0);
+    load_dense(z0 + 1, d1u, d1f);
+    __syncthreads();
+
+    for (int zbase = z0; zbase < z1; zbase += W) {
+#pragma unroll
+        for (int ph = 0; ph < W; ++ph) {
+            const int zi = zbase + ph;
+            if (zi < z1) {
+                const int sb = (zi - z0) & 1;
+                load_dense(zi + 2, d2u, d2f);
+                issue_gather(zi + 1);
+                // x pass: 5-tap box of (f, m, ff, mm, fm)
+#pragma unroll
+                for (int q = 0; q < XS; ++q) {
+                    const int idx = threadIdx.x + q * NT;
+                    if (idx < IH * TX) {
+                        const int c = idx % TX, r = idx / TX;
+                        const double* fr = &s_f[sb][r * IW + c];
+                        const double* mr = &s_m[sb][r * IW + c];
+                        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0, a4 = 0.0;
+#pragma unroll
+                        for (int d = 0; d < W; ++d) {
+                            const double f = fr[d], m = mr[d];
+                            a0 += f;
+                            a1 += m;
+                            a2 = fma(f, f, a2);
+                            a3 = fma(m, m, a3);
+                            a4 = fma(f, m, a4);
+                        }
+                        s_x[0][r][c] = a0; s_x[1][r][c] = a1; s_x[2][r][c] = a2;
+                        s_x[3][r][c] = a3; s_x[4][r][c] = a4;
+                    }
+                }
+                __syncthreads();
+                // y pass + running z sum over the static ring
+                double P[5];
+#pragma unroll
+                for (int c = 0; c < 5; ++c) {
+                    double s = 0.0;
+#pragma unroll
+                    for (int d = 0; d < W; ++d) s += s_x[c][t.oy + d][t.ox];
+                    P[c] = s;
+                    S[c] += s - ring[ph][c];
+                    ring[ph][c] = s;
+                }
+                const int zo = zi - R;
+                if (zo >= t.zb && t.own) {
+                    const double inv = c_inv_count[cxy * axis_count(zo, g.nz, R)];
+                    const double mf = S[0] * inv, mm = S[1] * inv;
+                    const double vf = fma(-mf, mf, S[2] * inv);
+                    const double vm = fma(-mm, mm, S[3] * inv);
+                    const double cv = fma(-mf, mm, S[4] * inv);
+                    const double af = mf + shf, am = mm + shm;
+                    const double msf = fma(af, af, vf), msm = fma(am, am, vm);
+                    double rho = 0.0, Ee = 0.0;
+                    float Aa = 0.f, Bb = 0.f;
+                    // NaN moments are not degenerate: non-finite inputs reach the loss
+                    const bool degenerate = msf <= 0.0 || msm <= 0.0 || vf <= 1e-9 * msf || vm <= 1e-9 * msm;
+                    if (!degenerate) {
+                        const double alpha = hot::rsqrt_d(vf * vm);
+                        rho = cv * alpha;
+                        Aa = (float)(alpha * inv);
+                        Bb = (float)(-rho * alpha * alpha * vf * inv);  // -rho / (n vm)
+                        Ee = fma((double)Aa, mf, (double)Bb * mm);
+                    }
+                    const int o = zo * t.nxy + ooff;
+                    Aout[o] = Aa;
+                    Bout[o] = Bb;
+                    Eout[o] = Ee;
+                    rho_acc += rho;
+                }
+                (void)P;
+                complete(zi + 1, sb ^ 1);
+#pragma unroll
+                for (int s = 0; s < SL; ++s) {
+                    d1u[s][0] = d2u[s][0]; d1u[s][1] = d2u[s][1]; d1u[s][2] = d2u[s][2];
+                    d1f[s] = d2f[s];
+                }
+                __syncthreads();
+            }
+        }
+    }
+
+    const double tot = block_sum(rho_acc, s_red);
+    const int nblk = gridDim.x * gridDim.y;
+    const int blk = blockIdx.x + gridDim.x * blockIdx.y;
+    if (threadIdx.x == 0) {
+        b.partials[(long long)pair * b.max_blocks + blk] = tot;
+        __threadfence();
+        const unsigned prev = atomicAdd(&st->counter, 1u);
+        s_last = prev == (unsigned)(nblk - 1);
+    }
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    double s = 0.0;
+    for (int i = threadIdx.x; i < nblk; i += NT) s += __ldcg(b.partials + (long long)pair * b.max_blocks + i);
+    const double total = block_sum(s, s_red);
+    if (threadIdx.x == 0) {
+        st->counter = 0u;
+        finalize_pair(st, p, mode, total / (double)n, pair);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K2: LNCC backward.  Adjoint box sums of (A, B, E) over the same windows in
+// fp64; dr/dMw(x) = -(1/N)(f'_x S_A + m'_x S_B - S_E); g = dr/dMw grad M(x+u).
+// Halo rows are prefetched one plane ahead; the output voxel's u and F two
+// planes ahead and its M gathers one plane ahead of their use.
+template <int R>
+__global__ void __launch_bounds__(NT, 2) k_lncc_bwd(Batch b, LmParams p, int chunk_len) {
+    using It = hot::Items<R>;
+    constexpr int IW = It::IW, IH = It::IH, NI = It::NI, SL = It::SLOTS, W = 2 * R + 1;
+    constexpr int XS = (IH * TX + NT - 1) / NT;
+    __shared__ double s_in[2][3][NI];
+    __shared__ double s_x[3][IH][TX];
+
+    const int pair = blockIdx.z;
+    const PairState* st = b.st + pair;
+    if (st->done || st->last_rejected) return;
+    const Geo g = b.g;
+    const long long n = g.n;
+    Tile t;
+    t.init(g, chunk_len);
+    const float* __restrict__ F = b.F + (long long)pair * n;
+    const float* __restrict__ M = b.M + (long long)pair * n;
+    const float* __restrict__ U = b.U + ((long long)pair * 2 + st->cur) * 3 * n;
+    const float* __restrict__ A = b.ABE + (long long)pair * 4 * n;
+    const float* __restrict__ Bc = A + n;
+    const double* __restrict__ E = reinterpret_cast<const double*>(A + 2 * n);
+    float* __restrict__ G = b.G + (long long)pair * 3 * n;
+    const double shf = st->shift_f, shm = st->shift_m;
+    const double invN = 1.0 / (double)n;
+    It it;
+    it.init(t.x0, t.y0, g.nx, g.ny);
+    const int ooff = t.x + g.nx * t.y;
+
+    // halo rows of plane z+1
+    float ha[SL], hb[SL];
+    double he[SL];
+    auto load_halo = [&](int z) {
+        const bool zin = z >= 0 && z < g.nz;
+        const int po = z * t.nxy;
+#pragma unroll
+        for (int s = 0; s < SL; ++s) {
+            if (zin && it.goff[s] >= 0) {
+                const int o = po + it.goff[s];
+                ha[s] = __ldg(A + o);
+                hb[s] = __ldg(Bc + o);
+                he[s] = __ldg(E + o);
+            } else {
+                ha[s] = hb[s] = 0.f;
+                he[s] = 0.0;
+            }
+        }
+    };
+    auto store_halo = [&](int sb) {
+#pragma unroll
+        for (int s = 0; s < SL; ++s) {
+            if (it.sidx[s] < 0) continue;
+            s_in[sb][0][it.sidx[s]] = (double)ha[s];
+            s_in[sb][1][it.sidx[s]] = (double)hb[s];
+            s_in[sb][2][it.sidx[s]] = he[s];
+        }
+    };
+    // output-voxel pipeline: dense (u, F) of output plane zo+2, gathers of zo+1
+    float ou2[3], of2, ou1[3], of1;
+    CellD ocell_next, ocell_cur;
+    float oc_next[8], oc_cur[8];
+    float of_next = 0.f, of_cur = 0.f;
+    auto load_own = [&](int zo, float (&u)[3], float& f) {
+        if (t.own && zo >= t.zb && zo < t.ze) {
+            const int o = zo * t.nxy + ooff;
+            u[0] = __ldg(U + o); u[1] = __ldg(U + n + o); u[2] = __ldg(U + 2 * n + o);
+            f = __ldg(F + o);
+        } else {
+            u[0] = u[1] = u[2] = 0.f;
+            f = 0.f;
+        }
+    };
+    auto gather_own = [&](int zo, const float (&u)[3], float f) {
+        of_next = f;
+        if (t.own && zo >= t.zb && zo < t.ze) {
+            make_cell_d(ocell_next, g, t.x, t.y, zo, u[0], u[1], u[2]);
+#pragma unroll
+            for (int k = 0; k < 8; ++k) oc_next[k] = __ldg(M + ocell_next.o[k]);
+        }
+    };
+
+    double ring[W][3], S[3];
+#pragma unroll
+    for (int d = 0; d < W; ++d)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) ring[d][c] = 0.0;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) S[c] = 0.0;
+
+    const int z0 = t.zb - R, z1 = t.ze + R;
+    load_halo(z0);
+    store_halo(0);
+    load_halo(z0 + 1);
+    // outputs start at zo = zb (reached at zi = zb + R)
+    load_own(t.zb, ou1, of1);
+    gather_own(t.zb, ou1, of1);
+    ocell_cur = ocell_next;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) oc_cur[k] = oc_next[k];
+    of_cur = of_next;
+    load_own(t.zb + 1, ou1, of1);
+    __syncthreads();
+
+    for (int zbase = z0; zbase < z1; zbase += W) {
+#pragma unroll
+        for (int ph = 0; ph < W; ++ph) {
+            const int zi = zbase + ph;
+            if (zi < z1) {
+                const int sb = (zi - z0) & 1;
+                const int zo = zi - R;
+                const bool emit = zo >= t.zb;
+                if (emit) {
+                    load_own(zo + 2, ou2, of2);
+                    gather_own(zo + 1, ou1, of1);
+                }
+#pragma unroll
+                for (int q = 0; q < XS; ++q) {
+                    const int idx = threadIdx.x + q * NT;
+                    if (idx < IH * TX) {
+                        const int c = idx % TX, r = idx / TX;
+#pragma unroll
+                        for (int ch = 0; ch < 3; ++ch) {
+                            const double* row = &s_in[sb][ch][r * IW + c];
+                            double s = 0.0;
+#pragma unroll
+                            for (int d = 0; d < W; ++d) s += row[d];
+                            s_x[ch][r][c] = s;
+                        }
+                    }
+                }
+                __syncthreads();
+#pragma unroll
+                for (int c = 0; c < 3; ++c) {
+                    double s = 0.0;
+#pragma unroll
+                    for (int d = 0; d < W; ++d) s += s_x[c][t.oy + d][t.ox];
+                    S[c] += s - ring[ph][c];
+                    ring[ph][c] = s;
+                }
+                if (emit && t.own) {
+                    double gm[3];
+                    const double mw = ocell_cur.finite ? lerp_cell<true>(ocell_cur, oc_cur, gm) : kNaN64;
+                    if (!ocell_cur.finite) gm[0] = gm[1] = gm[2] = 0.0;
+                    const double f = (double)of_cur - shf;
+                    const double dm = -invN * (fma(f, S[0], (mw - shm) * S[1]) - S[2]);
+                    const int o = zo * t.nxy + ooff;
+                    G[o] = (float)(dm * gm[0]);
+                    G[n + o] = (float)(dm * gm[1]);
+                    G[2 * n + o] = (float)(dm * gm[2]);
+                }
+                if (emit) {
+                    ocell_cur = ocell_next;
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) oc_cur[k] = oc_next[k];
+                    of_cur = of_next;
+                    ou1[0] = ou2[0]; ou1[1] = ou2[1]; ou1[2] = ou2[2];
+                    of1 = of2;
+                }
+                store_halo(sb ^ 1);
+                load_halo(zi + 2);
+                __syncthreads();
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Gaussian 3-channel z-march in fp64 with a statically indexed ring.  The
+// producer fills s_in[3][NI] (fp64) for input plane zi; `emit` gets the
+// smoothed value at (x, y, zo).  Weights w[|d|] are truncated at R and
+// renormalised per axis over in-bounds taps (field.cpp:236-244): zero-filled
+// halos and a final divide by Wx(x) Wy(y) Wz(z).
+template <class T>
+__device__ __forceinline__ T axis_wsum_t(int p, int n, int R, const T* w, T full) {
+    if (p >= R && p + R <= n - 1) return full;
+    T s = 0;
+    for (int d = -R; d <= R; ++d) {
+        const int q = p + d;
+        if (q >= 0 && q < n) s += w[d < 0 ? -d : d];
+    }
+    return s;
+}
+
+// K3: dU = -r g / (|g|^2 + lambda) (Eq. 4) | -lr g (GD) | Adam step (in G);
+// Gaussian(sigma_update) in fp64; dU_s stored fp32; max |dU_s| (of the
+// stored values) -> PairState.max_bits.
+template <int R>
+__global__ void __launch_bounds__(NT, 2) k_step_smooth(Batch b, LmParams p, int chunk_len) {
+    using It = hot::Items<R>;
+    constexpr int IW = It::IW, IH = It::IH, NI = It::NI, SL = It::SLOTS, W = 2 * R + 1;
+    constexpr int XS = (IH * TX + NT - 1) / NT;
+    __shared__ double s_in[2][3][NI];
+    __shared__ double s_x[3][IH][TX];
+    __shared__ float s_max[NT / 32];
+
+    const int pair = blockIdx.z;
+    PairState* st = b.st + pair;
+    if (st->done) return;
+    const Geo g = b.g;
+    const long long n = g.n;
+    Tile t;
+    t.init(g, chunk_len);
+    const float* __restrict__ Gin = b.G + (long long)pair * 3 * n;
+    float* __restrict__ V = b.VS + (long long)pair * 3 * n;
+    const double r = st->r_cur, lam = st->lambda, lr = p.gd_lr;
+    const int opt = p.optimizer;
+    It it;
+    it.init(t.x0, t.y0, g.nx, g.ny);
+    const int ooff = t.x + g.nx * t.y;
+    double w[W];
+#pragma unroll
+    for (int d = 0; d < W; ++d) w[d] = p.wud[d < R ? R - d : d - R];
+    const double wxy = t.own ? axis_wsum_t<double>(t.x, g.nx, R, p.wud, p.wud_full) *
+                                   axis_wsum_t<double>(t.y, g.ny, R, p.wud, p.wud_full)
+                             : 1.0;
+
+    float hg[SL][3];
+    auto load_halo = [&](int z) {
+        const bool zin = z >= 0 && z < g.nz;
+        const int po = z * t.nxy;
+#pragma unroll
+        for (int s = 0; s < SL; ++s) {
+            if (zin && it.goff[s] >= 0) {
+                const int o = po + it.goff[s];
+                hg[s][0] = __ldg(Gin + o); hg[s][1] = __ldg(Gin + n + o); hg[s][2] = __ldg(Gin + 2 * n + o);
+            } else {
+                hg[s][0] = hg[s][1] = hg[s][2] = 0.f;
+            }
+        }
+    };
+    auto store_halo = [&](int sb) {
+#pragma unroll
+        for (int s = 0; s < SL; ++s) {
+            if (it.sidx[s] < 0) continue;
+            const double a = hg[s][0], bb = hg[s][1], c = hg[s][2];
+            double k;
+            if (opt == WLM_OPT_LM) k = -r / (fma(a, a, fma(bb, bb, c * c)) + lam);
+            else if (opt == WLM_OPT_GD) k = -lr;
+            else k = 1.0;  // Adam step already in G
+            s_in[sb][0][it.sidx[s]] = k * a;
+            s_in[sb][1][it.sidx[s]] = k * bb;
+            s_in[sb][2][it.sidx[s]] = k * c;
+        }
+    };
+
+    double ring[W][3];
+#pragma unroll
+    for (int d = 0; d < W; ++d)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) ring[d][c] = 0.0;
+    float mx = 0.f;
+
+    const int z0 = t.zb - R, z1 = t.ze + R;
+    load_halo(z0);
+    store_halo(0);
+    load_halo(z0 + 1);
+    __syncthreads();
+    for (int zbase = z0; zbase < z1; zbase += W) {
+#pragma unroll
+        for (int ph = 0; ph < W; ++ph) {
+            const int zi = zbase + ph;
+            if (zi < z1) {
+                const int sb = (zi - z0) & 1;
+#pragma unroll
+                for (int q = 0; q < XS; ++q) {
+                    const int idx = threadIdx.x + q * NT;
+                    if (idx < IH * TX) {
+                        const int c = idx % TX, rr = idx / TX;
+#pragma unroll
+                        for (int ch = 0; ch < 3; ++ch) {
+                            const double* row = &s_in[sb][ch][rr * IW + c];
+                            double s = 0.0;
+#pragma unroll
+                            for (int d = 0; d < W; ++d) s = fma(w[d], row[d], s);
+                            s_x[ch][rr][c] = s;
+                        }
+                    }
+                }
+                __syncthreads();
+#pragma unroll
+                for (int c = 0; c < 3; ++c) {
+                    double s = 0.0;
+#pragma unroll
+                    for (int d = 0; d < W; ++d) s = fma(w[d], s_x[c][t.oy + d][t.ox], s);
+                    ring[ph][c] = s;
+                }
+                const int zo = zi - R;
+                if (zo >= t.zb && t.own) {
+                    const double inv = 1.0 / (wxy * axis_wsum_t<double>(zo, g.nz, R, p.wud, p.wud_full));
+                    const int o = zo * t.nxy + ooff;
+#pragma unroll
+                    for (int c = 0; c < 3; ++c) {
+                        double s = 0.0;
+#pragma unroll
+                        for (int d = 0; d < W; ++d) s = fma(w[d], ring[(ph + 1 + d) % W][c], s);
+                        const float v = (float)(s * inv);
+                        V[c * n + o] = v;
+                        mx = fmaxf(mx, fabsf(v));
+                    }
+                }
+                store_halo(sb ^ 1);
+                load_halo(zi + 2);
+                __syncthreads();
+            }
+        }
+    }
+    mx = warp_max(mx);
+    if ((threadIdx.x & 31) == 0) s_max[threadIdx.x >> 5] = mx;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        float m = 0.f;
+        for (int i = 0; i < NT / 32; ++i) m = fmaxf(m, s_max[i]);
+        atomic_max_nonneg(&st->max_bits, m);
+    }
+}
+
+// K4: u'(x) = d(x) + u(x + d(x)), d = eps dU_s, eps = target / max(max|dU_s|,
+// floor) (Eq. 2, field.cpp:123-155), then Gaussian(sigma_warp), fp64.  The
+// normalised step bounds |d| <= target < 0.5 voxel, so every resample corner
+// lies in the 3x3x3 neighbourhood of its voxel: the accepted warp is staged
+// in a 3-plane shared-memory ring (halo R+1) and the compose "gathers" are
+// shared-memory reads.  Reads the accepted buffer, writes the other one.
+template <int R>
+__global__ void __launch_bounds__(NT, 2) k_compose_smooth(Batch b, LmParams p, int chunk_len) {
+    using It = hot::Items<R>;          // producer tile (halo R)
+    using Iu = hot::Items<R + 1>;      // warp tile (halo R + 1)
+    constexpr int IW = It::IW, IH = It::IH, NI = It::NI, SL = It::SLOTS, W = 2 * R + 1;
+    constexpr int UW = Iu::IW, UN = Iu::NI, USL = Iu::SLOTS;
+    constexpr int XS = (IH * TX + NT - 1) / NT;
+    __shared__ float s_u[3][3][UN];     // [ring slot][channel][tile]
+    __shared__ double s_in[3][NI];
+    __shared__ double s_x[3][IH][TX];
+
+    const int pair = blockIdx.z;
+    const PairState* st = b.st + pair;
+    if (st->done) return;
+    const Geo g = b.g;
+    const long long n = g.n;
+    Tile t;
+    t.init(g, chunk_len);
+    const int cur = st->cur;
+    const float* __restrict__ Vin = b.VS + (long long)pair * 3 * n;
+    const float* __restrict__ U = b.U + ((long long)pair * 2 + cur) * 3 * n;
+    float* __restrict__ UN_ = b.U + ((long long)pair * 2 + (1 - cur)) * 3 * n;
+    const double eps = p.target / fmax((double)__uint_as_float(st->max_bits), p.step_floor);
+    It it;
+    it.init(t.x0, t.y0, g.nx, g.ny);
+    Iu iu;
+    iu.init(t.x0, t.y0, g.nx, g.ny);
+    const int ooff = t.x + g.nx * t.y;
+    double w[W];
+#pragma unroll
+    for (int d = 0; d < W; ++d) w[d] = p.wwd[d < R ? R - d : d - R];
+    const double wxy = t.own ? axis_wsum_t<double>(t.x, g.nx, R, p.wwd, p.wwd_full) *
+                                   axis_wsum_t<double>(t.y, g.ny, R, p.wwd, p.wwd_full)
+                             : 1.0;
+
+    float pu[USL][3];  // warp rows of plane z + 2
+    // step rows: the thread that loads item s also produces it, so the step
+    // tile never goes through shared memory (plane z, z + 1, z + 2)
+    float v0[SL][3], v1[SL][3], v2[SL][3];
+    auto load_u = [&](int z) {
+        const bool zin = z >= 0 && z < g.nz;
+        const int po = z * t.nxy;
+#pragma unroll
+        for (int s = 0; s < USL; ++s) {
+            if (zin && iu.goff[s] >= 0) {
+                const int o = po + iu.goff[s];
+                pu[s][0] = __ldg(U + o); pu[s][1] = __ldg(U + n + o); pu[s][2] = __ldg(U + 2 * n + o);
+            } else {
+                pu[s][0] = pu[s][1] = pu[s][2] = 0.f;
+            }
+        }
+    };
+    auto store_u = [&](int z) {
+        const int slot = ((z % 3) + 3) % 3;
+#pragma unroll
+        for (int s = 0; s < USL; ++s) {
+            if (iu.sidx[s] < 0) continue;
+            s_u[slot][0][iu.sidx[s]] = pu[s][0];
+            s_u[slot][1][iu.sidx[s]] = pu[s][1];
+            s_u[slot][2][iu.sidx[s]] = pu[s][2];
+        }
+    };
+    auto load_v = [&](int z, float (&pv)[SL][3]) {
+        const bool zin = z >= 0 && z < g.nz;
+        const int po = z * t.nxy;
+#pragma unroll
+        for (int s = 0; s < SL; ++s) {
+            if (zin && it.goff[s] >= 0) {
+                const int o = po + it.goff[s];
+                pv[s][0] = __ldg(Vin + o); pv[s][1] = __ldg(Vin + n + o); pv[s][2] = __ldg(Vin + 2 * n + o);
+            } else {
+                pv[s][0] = pv[s][1] = pv[s][2] = 0.f;
+            }
+        }
+    };
+    // composed value at producer item s of plane z (fp64); warp from the ring
+    auto produce = [&](int z, const float (&pv)[SL][3]) {
+        const bool zin = z >= 0 && z < g.nz;
+#pragma unroll
+        for (int s = 0; s < SL; ++s) {
+            if (it.sidx[s] < 0) continue;
+            double o3[3] = {0.0, 0.0, 0.0};
+            if (zin && it.goff[s] >= 0) {
+                const double dx = eps * pv[s][0], dy = eps * pv[s][1], dz = eps * pv[s][2];
+                if (isfinite(dx) && isfinite(dy) && isfinite(dz)) {
+                    const AxisTapD X = axis_tap_dd(it.gx[s], dx, g.nx);
+                    const AxisTapD Y = axis_tap_dd(it.gy[s], dy, g.ny);
+                    const AxisTapD Z = axis_tap_dd(z, dz, g.nz);
+                    // tile coordinates of the corners (clamped defensively)
+                    const int ux0 = min(max(X.i0 - (t.x0 - R - 1), 0), UW - 2);
+                    const int uy0 = min(max(Y.i0 - (t.y0 - R - 1), 0), Iu::IH - 2);
+                    const int sz0 = ((Z.i0 % 3) + 3) % 3, sz1 = ((Z.i1 % 3) + 3) % 3;
+                    const int a = uy0 * UW + ux0;
+#pragma unroll
+                    for (int ch = 0; ch < 3; ++ch) {
+                        const float* p0 = &s_u[sz0][ch][a];
+                        const float* p1 = &s_u[sz1][ch][a];
+                        const double c000 = p0[0], c100 = p0[1], c010 = p0[UW], c110 = p0[UW + 1];
+                        const double c001 = p1[0], c101 = p1[1], c011 = p1[UW], c111 = p1[UW + 1];
+                        const double v00 = fma(X.t, c100 - c000, c000), v10 = fma(X.t, c110 - c010, c010);
+                        const double v01 = fma(X.t, c101 - c001, c001), v11 = fma(X.t, c111 - c011, c011);
+                        const double s0 = fma(Y.t, v10 - v00, v00), s1 = fma(Y.t, v11 - v01, v01);
+                        o3[ch] = fma(Z.t, s1 - s0, s0);
+                    }
+                    o3[0] += dx;
+                    o3[1] += dy;
+                    o3[2] += dz;
+                } else {
+                    o3[0] = o3[1] = o3[2] = kNaN64;
+                }
+            }
+            s_in[0][it.sidx[s]] = o3[0];
+            s_in[1][it.sidx[s]] = o3[1];
+            s_in[2][it.sidx[s]] = o3[2];
+        }
+    };
+
+    double ring[W][3];
+#pragma unroll
+    for (int d = 0; d < W; ++d)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) ring[d][c] = 0.0;
+
+    const int z0 = t.zb - R, z1 = t.ze + R;
+    // prologue: warp planes z0-1 .. z0+1 staged, z0+2 in registers; steps of
+    // z0 staged, z0+1 in registers
+    load_u(z0 - 1); store_u(z0 - 1);
+    load_u(z0);     store_u(z0);
+    load_u(z0 + 1); store_u(z0 + 1);
+    load_u(z0 + 2);
+    load_v(z0, v0);
+    load_v(z0 + 1, v1);
+    __syncthreads();
+
+    for (int zbase = z0; zbase < z1; zbase += W) {
+#pragma unroll
+        for (int ph = 0; ph < W; ++ph) {
+            const int zi = zbase + ph;
+            if (zi < z1) {
+                load_v(zi + 2, v2);
+                produce(zi, v0);
+                __syncthreads();
+                // the ring slot of plane zi-1 is free now
+                store_u(zi + 2);
+                load_u(zi + 3);
+#pragma unroll
+                for (int s = 0; s < SL; ++s)
+#pragma unroll
+                    for (int c = 0; c < 3; ++c) {
+                        v0[s][c] = v1[s][c];
+                        v1[s][c] = v2[s][c];
+                    }
+#pragma unroll
+                for (int q = 0; q < XS; ++q) {
+                    const int idx = threadIdx.x + q * NT;
+                    if (idx < IH * TX) {
+                        const int c = idx % TX, rr = idx / TX;
+#pragma unroll
+                        for (int ch = 0; ch < 3; ++ch) {
+                            const double* row = &s_in[ch][rr * IW + c];
+                            double s = 0.0;
+#pragma unroll
+                            for (int d = 0; d < W; ++d) s = fma(w[d], row[d], s);
+                            s_x[ch][rr][c] = s;
+                        }
+                    }
+                }
+                __syncthreads();
+#pragma unroll
+                for (int c = 0; c < 3; ++c) {
+                    double s = 0.0;
+#pragma unroll
+                    for (int d = 0; d < W; ++d) s = fma(w[d], s_x[c][t.oy + d][t.ox], s);
+                    ring[ph][c] = s;
+                }
+                const int zo = zi - R;
+                if (zo >= t.zb && t.own) {
+                    const double inv = 1.0 / (wxy * axis_wsum_t<double>(zo, g.nz, R, p.wwd, p.wwd_full));
+                    const int o = zo * t.nxy + ooff;
+#pragma unroll
+                    for (int c = 0; c < 3; ++c) {
+                        double s = 0.0;
+#pragma unroll
+                        for (int d = 0; d < W; ++d) s = fma(w[d], ring[(ph + 1 + d) % W][c], s);
+                        UN_[c * n + o] = (float)(s * inv);
+                    }
+                }
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+#define WLM_DISPATCH_R(R_, CALL)                       \
+    switch (R_) {                                      \
+        case 0: { constexpr int RR = 0; CALL; } break; \
+        case 1: { constexpr int RR = 1; CALL; } break; \
+        case 2: { constexpr int RR = 2; CALL; } break; \
+        case 3: { constexpr int RR = 3; CALL; } break; \
+        default: break;                                \
+    }
+
+void launch_lncc_fwd(const Batch& b, const LmParams& p, int mode, cudaStream_t s) {
+    const LaunchShape sh = shape_for(b.g, b.pairs, TY);
+    dim3 grid = sh.grid();
+    grid.z = b.pairs;
+    k_lncc_fwd<2><<<grid, NT, 0, s>>>(b, p, mode, sh.chunk_len);
+    ++g_kernel_launches;
+}
+
+void launch_lncc_bwd(const Batch& b, const LmParams& p, cudaStream_t s) {
+    const LaunchShape sh = shape_for(b.g, b.pairs, TY);
+    dim3 grid = sh.grid();
+    grid.z = b.pairs;
+    k_lncc_bwd<2><<<grid, NT, 0, s>>>(b, p, sh.chunk_len);
+    ++g_kernel_launches;
+}
+
+void launch_step_smooth(const Batch& b, const LmParams& p, cudaStream_t s) {
+    const LaunchShape sh = shape_for(b.g, b.pairs, TY);
+    dim3 grid = sh.grid();
+    grid.z = b.pairs;
+    WLM_DISPATCH_R(p.Ru, (k_step_smooth<RR><<<grid, NT, 0, s>>>(b, p, sh.chunk_len)));
+    ++g_kernel_launches;
+}
+
+void launch_compose_smooth(const Batch& b, const LmParams& p, cudaStream_t s) {
+    const LaunchShape sh = shape_for(b.g, b.pairs, TY);
+    dim3 grid = sh.grid();
+    grid.z = b.pairs;
+    WLM_DISPATCH_R(p.Rw, (k_compose_smooth<RR><<<grid, NT, 0, s>>>(b, p, sh.chunk_len)));
+    ++g_kernel_launches;
+}
+
+}  // namespace wlm

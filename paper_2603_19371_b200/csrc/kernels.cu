@@ -48,91 +48,6 @@ LaunchShape shape_for(const Geo& g, int pairs, int ty) {
     return s;
 }
 
-// ---------------------------------------------------------------------------
-// Loss / damping / rejection state machine, run by one
-// thread of the last CTA of the evaluation kernel.  Identical fp64
-// arithmetic to the oracle (oracle.cpp orc_update_damping /
-// attempt_rejected), so the lambda trajectory is bit-identical whenever the
-// accept/reject decisions agree.
-__device__ void update_damping_dev(PairState* st, const LmParams& p, double r) {
-    const bool bad = st->hist_n == 0 || r > st->L1;
-    double lam = bad ? p.mu_plus * st->lambda : p.mu_minus * st->lambda;
-    if (p.lambda_max > 0.0 && isfinite(p.lambda_max)) lam = fmin(lam, p.lambda_max);
-    st->lambda = fmax(lam, 1e-12);
-    st->L2 = st->L1;
-    st->L1 = r;
-    st->hist_n = min(st->hist_n + 1, 2);
-}
-
-__device__ bool rejection_fires(const PairState* st, const LmParams& p, double r) {
-    return p.rejection && st->hist_n >= 2 && (r - st->L1) > p.tau * fabs(st->L1 - st->L2);
-}
-
-__device__ void finalize_pair(PairState* st, const LmParams& p, int mode, double lncc, long long N,
-                              int pair) {
-    double r = 1.0 - lncc;
-    if (mode == 0) {
-        st->r_cur = r;
-        st->lncc_cur = lncc;
-        if (!isfinite(r)) { st->status = WLM_NONFINITE; st->done = 1; }
-        st->max_bits = 0u;
-        st->jac_bits = 0x7f800000;  // +inf
-        return;
-    }
-    if (p.script && p.script_n > 0) {
-        r = p.script[(long long)pair * p.script_n + min(st->attempt, p.script_n - 1)];
-        lncc = 1.0 - r;
-    }
-    st->attempt += 1;
-    st->r_try = r;
-    st->lncc_try = lncc;
-    const double maxv = (double)__uint_as_float(st->max_bits);
-    const double eps = p.target / fmax(maxv, p.step_floor);
-    if (!isfinite(r)) {  // abort
-        st->status = WLM_NONFINITE;
-        st->done = 1;
-        return;
-    }
-    bool rej = false;
-    if (p.optimizer == WLM_OPT_LM && st->retries < p.max_retries && rejection_fires(st, p, r)) {
-        double lam = p.mu_plus * st->lambda;
-        if (p.lambda_max > 0.0 && isfinite(p.lambda_max)) lam = fmin(lam, p.lambda_max);
-        st->lambda = lam;
-        st->retries += 1;
-        rej = true;
-    }
-    if (rej) {
-        st->last_rejected = 1;
-    } else {
-        const bool forced = p.optimizer == WLM_OPT_LM && st->retries >= p.max_retries &&
-                            rejection_fires(st, p, r);
-        if (p.optimizer == WLM_OPT_LM) update_damping_dev(st, p, r);
-        st->cur ^= 1;
-        st->r_cur = r;
-        st->lncc_cur = lncc;
-        st->last_rejected = 0;
-        if (p.trace && st->trace_len < p.trace_cap) {
-            wlm_step_log* row = p.trace + (long long)pair * p.trace_cap + st->trace_len;
-            row->level = st->level;
-            row->iter = st->iter;
-            row->loss_raw = lncc;
-            row->r = r;
-            row->lambda = p.optimizer == WLM_OPT_LM ? st->lambda : 0.0;
-            row->eps = eps;
-            row->accepted = forced ? 0 : 1;
-            row->retries = st->retries;
-            row->jac_det_min = p.log_jacobian ? (double)ordered_to_float(st->jac_bits)
-                                              : __longlong_as_double(0x7ff8000000000000ll);
-            st->trace_len += 1;
-        }
-        st->iter += 1;
-        st->retries = 0;
-        if (st->iter >= st->iters_target) st->done = 1;
-    }
-    st->max_bits = 0u;
-    st->jac_bits = 0x7f800000;
-}
-
 // Block-wide fixed-order double sum (result valid in thread 0).
 __device__ double block_sum(double v, double* red) {
     v = warp_sum(v);
@@ -144,429 +59,6 @@ __device__ double block_sum(double v, double* red) {
         for (int i = 0; i < (int)(blockDim.x >> 5); ++i) s += red[i];
     __syncthreads();
     return s;
-}
-
-// ---------------------------------------------------------------------------
-// Window statistics are accumulated in fp64 (B200 runs fp64 at half the
-// fp32 rate): LNCC moments cancel catastrophically in fp32 wherever a window
-// is bright and flat (variance << mean^2), and the gradient's
-// adjoint sums cancel against E.  Products of two
-// fp32 values are exact in fp64, so the sums are those of the fp32 inputs to
-// ~1e-16.  Per-voxel inputs (f, M(x+u)) and the stored A, B stay fp32.
-__constant__ double c_inv_count[126];  // 1/n for truncated window counts n <= 125
-
-// K1: warp + LNCC forward.
-//   input plane (halo R): f' = F - shift_f, m' = M(x + u(x)) - shift_m  (fp64)
-//   window sums S_f, S_m, S_ff, S_mm, S_fm over the truncated box (fp64)
-//   rho = c / sqrt(vf vm); A = 1/(n sqrt(vf vm)); B = -rho/(n vm)  -> fp32
-//   E = A' mu_f' + B' mu_m' (fp64, from the rounded A', B' so that K2's
-//   f' S_A + m' S_B - S_E cancels exactly), sum(rho) -> per-CTA partial.
-template <int R>
-__global__ void __launch_bounds__(NT) k_lncc_fwd(Batch b, LmParams p, int mode, int chunk_len) {
-    constexpr int IW = TX + 2 * R, IH = TY + 2 * R, W = 2 * R + 1;
-    __shared__ double s_f[IH][IW], s_m[IH][IW];
-    __shared__ double s_x[5][IH][TX];
-    __shared__ double s_red[NT / 32];
-    __shared__ int s_last;
-
-    const int pair = blockIdx.z;
-    PairState* st = b.st + pair;
-    if (st->done) return;
-    const Geo g = b.g;
-    const long long n = g.n;
-    const int tiles_x = cdiv(g.nx, TX);
-    const int x0 = (blockIdx.x % tiles_x) * TX, y0 = (blockIdx.x / tiles_x) * TY;
-    const int zb = blockIdx.y * chunk_len, ze = min(zb + chunk_len, g.nz);
-    const int buf = mode == 0 ? st->cur : 1 - st->cur;
-    const float* __restrict__ F = b.F + (long long)pair * n;
-    const float* __restrict__ M = b.M + (long long)pair * n;
-    const float* __restrict__ U = b.U + ((long long)pair * 2 + buf) * 3 * n;
-    float* __restrict__ A = b.ABE + (long long)pair * 4 * n;
-    float* __restrict__ Bc = A + n;
-    double* __restrict__ E = reinterpret_cast<double*>(A + 2 * n);
-    const double shf = st->shift_f, shm = st->shift_m;
-    const int tid = threadIdx.x, ox = tid & 31, oy = tid >> 5;
-    const int x = x0 + ox, y = y0 + oy;
-    const bool own = x < g.nx && y < g.ny;
-    const int cxy = own ? axis_count(x, g.nx, R) * axis_count(y, g.ny, R) : 1;
-
-    double ring[W][5];
-#pragma unroll
-    for (int d = 0; d < W; ++d)
-#pragma unroll
-        for (int c = 0; c < 5; ++c) ring[d][c] = 0.0;
-    double rho_acc = 0.0;
-
-    for (int zi = zb - R; zi < ze + R; ++zi) {
-        const bool zin = zi >= 0 && zi < g.nz;
-        for (int idx = tid; idx < IW * IH; idx += NT) {
-            const int ix = idx % IW, iy = idx / IW;
-            const int gx = x0 - R + ix, gy = y0 - R + iy;
-            double fv = 0.0, mv = 0.0;
-            if (zin && gx >= 0 && gx < g.nx && gy >= 0 && gy < g.ny) {
-                const int o = g.at(gx, gy, zi);
-                mv = sample_d<false>(M, g, gx, gy, zi, __ldg(U + o), __ldg(U + n + o),
-                                     __ldg(U + 2 * n + o), nullptr) - shm;
-                fv = (double)__ldg(F + o) - shf;
-            }
-            s_f[iy][ix] = fv;
-            s_m[iy][ix] = mv;
-        }
-        __syncthreads();
-        for (int idx = tid; idx < IH * TX; idx += NT) {
-            const int c = idx % TX, r = idx / TX;
-            double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0, a4 = 0.0;
-#pragma unroll
-            for (int d = 0; d < W; ++d) {
-                const double f = s_f[r][c + d], m = s_m[r][c + d];
-                a0 += f;
-                a1 += m;
-                a2 = fma(f, f, a2);
-                a3 = fma(m, m, a3);
-                a4 = fma(f, m, a4);
-            }
-            s_x[0][r][c] = a0; s_x[1][r][c] = a1; s_x[2][r][c] = a2;
-            s_x[3][r][c] = a3; s_x[4][r][c] = a4;
-        }
-        __syncthreads();
-#pragma unroll
-        for (int d = 0; d < W - 1; ++d)
-#pragma unroll
-            for (int c = 0; c < 5; ++c) ring[d][c] = ring[d + 1][c];
-#pragma unroll
-        for (int c = 0; c < 5; ++c) {
-            double s = 0.0;
-#pragma unroll
-            for (int d = 0; d < W; ++d) s += s_x[c][oy + d][ox];
-            ring[W - 1][c] = s;
-        }
-        const int zo = zi - R;
-        if (zo >= zb && own) {
-            double S[5];
-#pragma unroll
-            for (int c = 0; c < 5; ++c) {
-                double s = 0.0;
-#pragma unroll
-                for (int d = 0; d < W; ++d) s += ring[d][c];
-                S[c] = s;
-            }
-            const double inv = c_inv_count[cxy * axis_count(zo, g.nz, R)];
-            const double mf = S[0] * inv, mm = S[1] * inv;
-            const double vf = fma(-mf, mf, S[2] * inv);
-            const double vm = fma(-mm, mm, S[3] * inv);
-            const double cv = fma(-mf, mm, S[4] * inv);
-            const double af = mf + shf, am = mm + shm;
-            const double msf = fma(af, af, vf), msm = fma(am, am, vm);
-            double rho = 0.0;
-            float Aa = 0.f, Bb = 0.f;
-            double Ee = 0.0;
-            // NaN moments are not degenerate: a non-finite input reaches the loss
-            const bool degenerate = msf <= 0.0 || msm <= 0.0 || vf <= 1e-9 * msf || vm <= 1e-9 * msm;
-            if (!degenerate) {
-                const double alpha = 1.0 / sqrt(vf * vm);
-                rho = cv * alpha;
-                Aa = (float)(alpha * inv);
-                Bb = (float)(-rho / vm * inv);
-                Ee = fma((double)Aa, mf, (double)Bb * mm);
-            }
-            const int o = g.at(x, y, zo);
-            A[o] = Aa;
-            Bc[o] = Bb;
-            E[o] = Ee;
-            rho_acc += rho;
-        }
-    }
-
-    const double tot = block_sum(rho_acc, s_red);
-    const int nblk = gridDim.x * gridDim.y;
-    const int blk = blockIdx.x + gridDim.x * blockIdx.y;
-    if (tid == 0) {
-        b.partials[(long long)pair * b.max_blocks + blk] = tot;
-        __threadfence();
-        const unsigned prev = atomicAdd(&st->counter, 1u);
-        s_last = prev == (unsigned)(nblk - 1);
-    }
-    __syncthreads();
-    if (!s_last) return;
-    __threadfence();
-    double s = 0.0;
-    for (int i = tid; i < nblk; i += NT) s += __ldcg(b.partials + (long long)pair * b.max_blocks + i);
-    const double total = block_sum(s, s_red);
-    if (tid == 0) {
-        st->counter = 0u;
-        finalize_pair(st, p, mode, total / (double)n, n, pair);
-    }
-}
-
-// ---------------------------------------------------------------------------
-// K2: LNCC backward.  Adjoint box sums of (A, B, E) over the same windows in
-// fp64, dr/dMw(x) = -(1/N) (f'_x S_A + m'_x S_B - S_E),
-// g = dr/dMw * gradM(x + u(x)).
-template <int R>
-__global__ void __launch_bounds__(NT) k_lncc_bwd(Batch b, LmParams p, int chunk_len) {
-    constexpr int IW = TX + 2 * R, IH = TY + 2 * R, W = 2 * R + 1;
-    __shared__ double s_in[3][IH][IW];
-    __shared__ double s_x[3][IH][TX];
-
-    const int pair = blockIdx.z;
-    const PairState* st = b.st + pair;
-    if (st->done || st->last_rejected) return;
-    const Geo g = b.g;
-    const long long n = g.n;
-    const int tiles_x = cdiv(g.nx, TX);
-    const int x0 = (blockIdx.x % tiles_x) * TX, y0 = (blockIdx.x / tiles_x) * TY;
-    const int zb = blockIdx.y * chunk_len, ze = min(zb + chunk_len, g.nz);
-    const float* __restrict__ F = b.F + (long long)pair * n;
-    const float* __restrict__ M = b.M + (long long)pair * n;
-    const float* __restrict__ U = b.U + ((long long)pair * 2 + st->cur) * 3 * n;
-    const float* __restrict__ A = b.ABE + (long long)pair * 4 * n;
-    const float* __restrict__ Bc = A + n;
-    const double* __restrict__ E = reinterpret_cast<const double*>(A + 2 * n);
-    float* __restrict__ G = b.G + (long long)pair * 3 * n;
-    const double shf = st->shift_f, shm = st->shift_m;
-    const double invN = 1.0 / (double)n;
-    const int tid = threadIdx.x, ox = tid & 31, oy = tid >> 5;
-    const int x = x0 + ox, y = y0 + oy;
-    const bool own = x < g.nx && y < g.ny;
-
-    double ring[W][3];
-#pragma unroll
-    for (int d = 0; d < W; ++d)
-#pragma unroll
-        for (int c = 0; c < 3; ++c) ring[d][c] = 0.0;
-
-    for (int zi = zb - R; zi < ze + R; ++zi) {
-        const bool zin = zi >= 0 && zi < g.nz;
-        for (int idx = tid; idx < IW * IH; idx += NT) {
-            const int ix = idx % IW, iy = idx / IW;
-            const int gx = x0 - R + ix, gy = y0 - R + iy;
-            double a = 0.0, bb = 0.0, e = 0.0;
-            if (zin && gx >= 0 && gx < g.nx && gy >= 0 && gy < g.ny) {
-                const int o = g.at(gx, gy, zi);
-                a = (double)__ldg(A + o);
-                bb = (double)__ldg(Bc + o);
-                e = __ldg(E + o);
-            }
-            s_in[0][iy][ix] = a;
-            s_in[1][iy][ix] = bb;
-            s_in[2][iy][ix] = e;
-        }
-        __syncthreads();
-        for (int idx = tid; idx < IH * TX; idx += NT) {
-            const int c = idx % TX, r = idx / TX;
-#pragma unroll
-            for (int ch = 0; ch < 3; ++ch) {
-                double s = 0.0;
-#pragma unroll
-                for (int d = 0; d < W; ++d) s += s_in[ch][r][c + d];
-                s_x[ch][r][c] = s;
-            }
-        }
-        __syncthreads();
-#pragma unroll
-        for (int d = 0; d < W - 1; ++d)
-#pragma unroll
-            for (int c = 0; c < 3; ++c) ring[d][c] = ring[d + 1][c];
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-            double s = 0.0;
-#pragma unroll
-            for (int d = 0; d < W; ++d) s += s_x[c][oy + d][ox];
-            ring[W - 1][c] = s;
-        }
-        const int zo = zi - R;
-        if (zo >= zb && own) {
-            double S[3];
-#pragma unroll
-            for (int c = 0; c < 3; ++c) {
-                double s = 0.0;
-#pragma unroll
-                for (int d = 0; d < W; ++d) s += ring[d][c];
-                S[c] = s;
-            }
-            const int o = g.at(x, y, zo);
-            double gm[3];
-            const double mw = sample_d<true>(M, g, x, y, zo, __ldg(U + o), __ldg(U + n + o),
-                                             __ldg(U + 2 * n + o), gm);
-            const double f = (double)__ldg(F + o) - shf;
-            const double dm = -invN * (fma(f, S[0], (mw - shm) * S[1]) - S[2]);
-            G[o] = (float)(dm * gm[0]);
-            G[n + o] = (float)(dm * gm[1]);
-            G[2 * n + o] = (float)(dm * gm[2]);
-        }
-    }
-}
-
-// ---------------------------------------------------------------------------
-// Gaussian z-march over 3 channels (K3, K4), accumulating in T.  Weights
-// w[|d|] are truncated at R and renormalised per axis over in-bounds taps
-// (field.cpp:236-244): zero-filled halos + a final divide by Wx Wy Wz.
-// K3 accumulates in fp64 (its input, the LM step, is signed and noisy, so the
-// 343-tap sums cancel); K4 smooths the warp (same-sign, O(1)) in fp32.
-template <class T>
-__device__ __forceinline__ T axis_wsum_t(int p, int n, int R, const T* w, T full) {
-    if (p >= R && p + R <= n - 1) return full;
-    T s = 0;
-    for (int d = -R; d <= R; ++d) {
-        const int q = p + d;
-        if (q >= 0 && q < n) s += w[d < 0 ? -d : d];
-    }
-    return s;
-}
-
-template <int R, class T, class Prod, class Cons>
-__device__ __forceinline__ void gauss_march3(const Geo& g, int x0, int y0, int zb, int ze,
-                                             const T* wh, T wfull, Prod& prod, Cons& cons) {
-    constexpr int IW = TX + 2 * R, IH = TY + 2 * R, W = 2 * R + 1;
-    __shared__ T s_in[3][IH][IW];
-    __shared__ T s_x[3][IH][TX];
-    T wr[W];
-#pragma unroll
-    for (int d = 0; d < W; ++d) wr[d] = wh[d < R ? R - d : d - R];
-    const int tid = threadIdx.x, ox = tid & 31, oy = tid >> 5;
-    const int x = x0 + ox, y = y0 + oy;
-    const bool own = x < g.nx && y < g.ny;
-    const T wxy = own ? axis_wsum_t<T>(x, g.nx, R, wh, wfull) * axis_wsum_t<T>(y, g.ny, R, wh, wfull) : T(1);
-    T ring[W][3];
-#pragma unroll
-    for (int d = 0; d < W; ++d)
-#pragma unroll
-        for (int c = 0; c < 3; ++c) ring[d][c] = 0;
-
-    for (int zi = zb - R; zi < ze + R; ++zi) {
-        const bool zin = zi >= 0 && zi < g.nz;
-        for (int idx = tid; idx < IW * IH; idx += NT) {
-            const int ix = idx % IW, iy = idx / IW;
-            const int gx = x0 - R + ix, gy = y0 - R + iy;
-            T v[3] = {0, 0, 0};
-            if (zin && gx >= 0 && gx < g.nx && gy >= 0 && gy < g.ny) prod(gx, gy, zi, v);
-            s_in[0][iy][ix] = v[0];
-            s_in[1][iy][ix] = v[1];
-            s_in[2][iy][ix] = v[2];
-        }
-        __syncthreads();
-        for (int idx = tid; idx < IH * TX; idx += NT) {
-            const int c = idx % TX, r = idx / TX;
-#pragma unroll
-            for (int ch = 0; ch < 3; ++ch) {
-                T s = 0;
-#pragma unroll
-                for (int d = 0; d < W; ++d) s = fma(wr[d], s_in[ch][r][c + d], s);
-                s_x[ch][r][c] = s;
-            }
-        }
-        __syncthreads();
-#pragma unroll
-        for (int d = 0; d < W - 1; ++d)
-#pragma unroll
-            for (int c = 0; c < 3; ++c) ring[d][c] = ring[d + 1][c];
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-            T s = 0;
-#pragma unroll
-            for (int d = 0; d < W; ++d) s = fma(wr[d], s_x[c][oy + d][ox], s);
-            ring[W - 1][c] = s;
-        }
-        const int zo = zi - R;
-        if (zo >= zb && own) {
-            const T inv = T(1) / (wxy * axis_wsum_t<T>(zo, g.nz, R, wh, wfull));
-            T o3[3];
-#pragma unroll
-            for (int c = 0; c < 3; ++c) {
-                T s = 0;
-#pragma unroll
-                for (int d = 0; d < W; ++d) s = fma(wr[d], ring[d][c], s);
-                o3[c] = s * inv;
-            }
-            cons(x, y, zo, o3);
-        }
-    }
-}
-
-// K3: dU = -r g / (|g|^2 + lambda) (Eq. 4) | -lr g (GD) | Adam step (precomputed),
-// smoothed with sigma_update (fp64 sums), written to VS (fp32), max |dU_s|
-// of the stored values -> PairState.max_bits.
-template <int R>
-__global__ void __launch_bounds__(NT) k_step_smooth(Batch b, LmParams p, int chunk_len) {
-    __shared__ float s_max[NT / 32];
-    const int pair = blockIdx.z;
-    PairState* st = b.st + pair;
-    if (st->done) return;
-    const Geo g = b.g;
-    const long long n = g.n;
-    const int tiles_x = cdiv(g.nx, TX);
-    const int x0 = (blockIdx.x % tiles_x) * TX, y0 = (blockIdx.x / tiles_x) * TY;
-    const int zb = blockIdx.y * chunk_len, ze = min(zb + chunk_len, g.nz);
-    const float* __restrict__ G = b.G + (long long)pair * 3 * n;
-    float* __restrict__ V = b.VS + (long long)pair * 3 * n;
-    const double r = st->r_cur, lam = st->lambda;
-    const int opt = p.optimizer;
-    const double lr = p.gd_lr;
-    auto prod = [&](int gx, int gy, int gz, double* v) {
-        const int o = g.at(gx, gy, gz);
-        const double a = __ldg(G + o), bb = __ldg(G + n + o), c = __ldg(G + 2 * n + o);
-        double s;
-        if (opt == WLM_OPT_LM) s = -r / (fma(a, a, fma(bb, bb, c * c)) + lam);
-        else if (opt == WLM_OPT_GD) s = -lr;
-        else s = 1.0;  // Adam step already in G
-        v[0] = s * a; v[1] = s * bb; v[2] = s * c;
-    };
-    float mx = 0.f;
-    auto cons = [&](int x, int y, int z, const double* o3) {
-        const int o = g.at(x, y, z);
-        const float a = (float)o3[0], bb = (float)o3[1], c = (float)o3[2];
-        V[o] = a;
-        V[n + o] = bb;
-        V[2 * n + o] = c;
-        mx = fmaxf(mx, fmaxf(fabsf(a), fmaxf(fabsf(bb), fabsf(c))));
-    };
-    gauss_march3<R, double>(g, x0, y0, zb, ze, p.wud, p.wud_full, prod, cons);
-    mx = warp_max(mx);
-    if ((threadIdx.x & 31) == 0) s_max[threadIdx.x >> 5] = mx;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        float m = 0.f;
-        for (int i = 0; i < NT / 32; ++i) m = fmaxf(m, s_max[i]);
-        atomic_max_nonneg(&st->max_bits, m);
-    }
-}
-
-// K4: u'(x) = d(x) + u(x + d(x)), d = eps dU_s, eps = target / max(max|dU_s|,
-// floor) (Eq. 2, field.cpp:123-155), then Gaussian(sigma_warp); reads the
-// accepted buffer, writes the other one (ping-pong = free rejection restore).
-// eps, d = eps * dU_s, the resample and the smoothing sums are fp64; u' is
-// rounded to fp32 once on store.
-template <int R>
-__global__ void __launch_bounds__(NT) k_compose_smooth(Batch b, LmParams p, int chunk_len) {
-    const int pair = blockIdx.z;
-    const PairState* st = b.st + pair;
-    if (st->done) return;
-    const Geo g = b.g;
-    const long long n = g.n;
-    const int tiles_x = cdiv(g.nx, TX);
-    const int x0 = (blockIdx.x % tiles_x) * TX, y0 = (blockIdx.x / tiles_x) * TY;
-    const int zb = blockIdx.y * chunk_len, ze = min(zb + chunk_len, g.nz);
-    const int cur = st->cur;
-    const float* __restrict__ V = b.VS + (long long)pair * 3 * n;
-    const float* __restrict__ U = b.U + ((long long)pair * 2 + cur) * 3 * n;
-    float* __restrict__ UN = b.U + ((long long)pair * 2 + (1 - cur)) * 3 * n;
-    const double eps = p.target / fmax((double)__uint_as_float(st->max_bits), p.step_floor);
-    auto prod = [&](int gx, int gy, int gz, double* v) {
-        const int o = g.at(gx, gy, gz);
-        const double dx = eps * __ldg(V + o), dy = eps * __ldg(V + n + o), dz = eps * __ldg(V + 2 * n + o);
-        double s[3];
-        sample3_d(U, n, g, gx, gy, gz, dx, dy, dz, s);
-        v[0] = dx + s[0];
-        v[1] = dy + s[1];
-        v[2] = dz + s[2];
-    };
-    auto cons = [&](int x, int y, int z, const double* o3) {
-        const int o = g.at(x, y, z);
-        UN[o] = (float)o3[0];
-        UN[n + o] = (float)o3[1];
-        UN[2 * n + o] = (float)o3[2];
-    };
-    gauss_march3<R, double>(g, x0, y0, zb, ze, p.wwd, p.wwd_full, prod, cons);
 }
 
 // Adam, pointwise; t = accepted iterations + 1 at this level.
@@ -705,50 +197,9 @@ __global__ void k_shift_final(Batch b, const double* part) {
 
 // ---------------------------------------------------------------------------
 // launch wrappers
-#define WLM_DISPATCH_R(R_, CALL)                      \
-    switch (R_) {                                     \
-        case 0: { constexpr int RR = 0; CALL; } break; \
-        case 1: { constexpr int RR = 1; CALL; } break; \
-        case 2: { constexpr int RR = 2; CALL; } break; \
-        case 3: { constexpr int RR = 3; CALL; } break; \
-        default: break;                               \
-    }
-
-void launch_lncc_fwd(const Batch& b, const LmParams& p, int mode, cudaStream_t s) {
-    const LaunchShape sh = shape_for(b.g, b.pairs, TY);
-    dim3 grid = sh.grid();
-    grid.z = b.pairs;
-    k_lncc_fwd<2><<<grid, NT, 0, s>>>(b, p, mode, sh.chunk_len);
-    ++g_kernel_launches;
-}
-
-void launch_lncc_bwd(const Batch& b, const LmParams& p, cudaStream_t s) {
-    const LaunchShape sh = shape_for(b.g, b.pairs, TY);
-    dim3 grid = sh.grid();
-    grid.z = b.pairs;
-    k_lncc_bwd<2><<<grid, NT, 0, s>>>(b, p, sh.chunk_len);
-    ++g_kernel_launches;
-}
-
 void launch_adam(const Batch& b, const LmParams& p, cudaStream_t s) {
     dim3 grid(kNumSMs * 4, b.pairs);
     k_adam<<<grid, 256, 0, s>>>(b, p);
-    ++g_kernel_launches;
-}
-
-void launch_step_smooth(const Batch& b, const LmParams& p, cudaStream_t s) {
-    const LaunchShape sh = shape_for(b.g, b.pairs, TY);
-    dim3 grid = sh.grid();
-    grid.z = b.pairs;
-    WLM_DISPATCH_R(p.Ru, (k_step_smooth<RR><<<grid, NT, 0, s>>>(b, p, sh.chunk_len)));
-    ++g_kernel_launches;
-}
-
-void launch_compose_smooth(const Batch& b, const LmParams& p, cudaStream_t s) {
-    const LaunchShape sh = shape_for(b.g, b.pairs, TY);
-    dim3 grid = sh.grid();
-    grid.z = b.pairs;
-    WLM_DISPATCH_R(p.Rw, (k_compose_smooth<RR><<<grid, NT, 0, s>>>(b, p, sh.chunk_len)));
     ++g_kernel_launches;
 }
 
@@ -778,16 +229,6 @@ void launch_shifts(const Batch& b, cudaStream_t s) {
     k_shift_partials<<<dim3(kShiftBlocks, b.pairs, 2), 256, 0, s>>>(b, b.shift_part);
     k_shift_final<<<dim3(b.pairs, 2), kShiftBlocks, 0, s>>>(b, b.shift_part);
     g_kernel_launches += 2;
-}
-
-void init_constants() {
-    static bool done = false;
-    if (done) return;
-    double inv[126];
-    inv[0] = 0.0;
-    for (int i = 1; i < 126; ++i) inv[i] = 1.0 / (double)i;
-    cudaMemcpyToSymbol(c_inv_count, inv, sizeof(inv));
-    done = true;
 }
 
 // ===========================================================================
