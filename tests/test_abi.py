@@ -73,6 +73,37 @@ def test_scalar_state_machine_matches_oracle():
         assert P.rejection_test(a, b, c_, 1.0) == O.rejection_test(a, b, c_, 1.0)
 
 
+def build_adapter_demo(tmp_path):
+    import subprocess
+    exe = tmp_path / "adapter_demo"
+    lib_dir = os.path.join(ROOT, "paper_2603_19371_b200")
+    subprocess.run(["g++", "-std=c++17", "-O1", "-I", os.path.join(ROOT, "include"),
+                    os.path.join(ROOT, "tests", "cpp", "adapter_demo.cpp"), "-L", lib_dir,
+                    "-lwarplm_b200", f"-Wl,-rpath,{lib_dir}", "-o", str(exe)], check=True)
+    return exe
+
+
+def test_cpp_adapter_builds(tmp_path):
+    """The reference-signature C++ adapter compiles and links against the ABI."""
+    assert build_adapter_demo(tmp_path).exists()
+
+
+@pytest.mark.skipif(not os.path.exists("/root/reference/proj/include/warplm/field.hpp"),
+                    reason="reference headers not present")
+def test_cpp_adapter_accepts_reference_types(tmp_path):
+    """Drop-in: the adapter takes warplm::Volume3 / DispField3 themselves."""
+    import subprocess
+    src = tmp_path / "drop_in.cpp"
+    src.write_text('#include "warplm/field.hpp"\n#include "wlm_warplm.hpp"\n'
+                   "double f(const warplm::DispField3& u, const warplm::DispField3& v) {\n"
+                   "  warplm::DispField3 w = wlm_warplm::compose_warp(u, v, 0.3);\n"
+                   "  warplm::Volume3 s = wlm_warplm::gaussian_smooth(warplm::Volume3(u.dims), 1.0);\n"
+                   "  return wlm_warplm::normalize_step(w, warplm::StepScale{}) + s.data[0]\n"
+                   "       + wlm_warplm::jacobian_det_min(w);\n}\n")
+    subprocess.run(["g++", "-std=c++20", "-fsyntax-only", "-I", "/root/reference/proj/include",
+                    "-I", os.path.join(ROOT, "include"), str(src)], check=True)
+
+
 def test_state_bytes():
     import paper_2603_19371_b200 as P
     assert P.state_bytes(P.OPT_ADAM, (64, 64, 64), 4) == 6291456  # SPEC.md:316

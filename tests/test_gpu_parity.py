@@ -335,3 +335,13 @@ def test_nonfinite_input_aborts(P, ctx):
     M = M.copy(); M[3, 3, 3] = np.nan
     with pytest.raises(P.NonFiniteLoss):
         P.register(F, M, P.reg_config(nlevels=1, factors=[1], iters=[3]), ctx=ctx)
+
+
+def test_cpp_adapter_runs_on_gpu(tmp_path):
+    """A reference-style C++ caller (tests/cpp/adapter_demo.cpp) through the
+    ABI: compose_warp KAT, normalize_step, dim-mismatch exception."""
+    import subprocess
+    from test_abi import build_adapter_demo
+    exe = build_adapter_demo(tmp_path)
+    out = subprocess.run([str(exe)], capture_output=True, text=True)
+    assert out.returncode == 0, out.stdout + out.stderr
