@@ -30,11 +30,14 @@ sys.path.insert(0, ROOT)
 
 METRIC = json.load(open(os.path.join(ROOT, "BASELINE.json")))["metric"]
 # Canonical algorithmic HBM bytes per voxel per kernel:
-#   K1 eval  : u 12 + F 4 + M 4 (gather) + write A,B,E 12          = 32
-#   K2 grad  : A,B,E 12 + F 4 + u 12 + M 4 + write g 12            = 44
-#   K3 step  : g 12 + write dU_s 12                                = 24
-#   K4 comp. : dU_s 12 + u 12 (gather) + write u' 12               = 36
-KERNEL_BYTES = {"K1_lncc_fwd": 32, "K2_lncc_bwd": 44, "K3_step_smooth": 24, "K4_compose_smooth": 36}
+#   K1 eval  : u 12 + F 4 + M 4 (gather) + write A,B 8 + E 8 (fp64)  = 36
+#   K2 grad  : A,B 8 + E 8 + F 4 + u 12 + M 4 + write g 12          = 48
+#   K3 step  : g 12 + write dU_s 12                                 = 24
+#   K4 comp. : dU_s 12 + u 12 (gather) + write u' 12                = 36
+# (SURVEY 8(d)'s canonical 136 B stores E in fp32; E is fp64 here for the
+#  exact adjoint cancellation.)  K1 is timed as its two
+#  launches (K1a warp of M, K1b window pass) against the 36 B it must move.
+KERNEL_BYTES = {"K1_lncc_fwd": 36, "K2_lncc_bwd": 48, "K3_step_smooth": 24, "K4_compose_smooth": 36}
 STAGE_ID = {"K1_lncc_fwd": 0, "K2_lncc_bwd": 1, "K3_step_smooth": 2, "K4_compose_smooth": 3}
 BYTES_PER_VOXEL_ITER = sum(KERNEL_BYTES.values())  # 136
 

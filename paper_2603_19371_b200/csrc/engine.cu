@@ -84,6 +84,7 @@ void engine_alloc(wlm_engine* e) {
     e->M = DevBuf<float>(ctx, B * n);
     e->U = DevBuf<float>(ctx, B * 6 * n);
     e->ABE = DevBuf<float>(ctx, B * 4 * n);  // A, B fp32 + E fp64
+    e->MW = DevBuf<double>(ctx, B * n);
     e->shift_part = DevBuf<double>(ctx, B * 2 * 256);
     init_constants();
     e->G = DevBuf<float>(ctx, B * 3 * n);
@@ -106,6 +107,7 @@ void engine_alloc(wlm_engine* e) {
     b.pairs = e->pairs;
     b.F = e->F.p; b.M = e->M.p; b.U = e->U.p; b.ABE = e->ABE.p; b.G = e->G.p; b.VS = e->VS.p;
     b.AM = e->AM.p; b.AV = e->AV.p;
+    b.MW = e->MW.p;
     b.st = e->st.p;
     b.partials = e->partials.p;
     b.shift_part = e->shift_part.p;

@@ -202,8 +202,47 @@ __device__ __forceinline__ double lerp_cell(const CellD& c, const float* v, doub
 constexpr double kNaN64 = __builtin_nan("");
 
 // ---------------------------------------------------------------------------
-// K1: warp + LNCC forward.
-//   halo tile (H = R): f' = F - shift_f, m' = M(x + u(x)) - shift_m   (fp64)
+// K1a: warp of the moving image, Mw(x) = M(x + u(x)) in fp64 (fp32 samples,
+// exact fp64 weights -- field.cpp:47-90), one voxel per thread-iteration with
+// four independent gathers in flight per thread.  Written once per voxel, so
+// the LNCC window pass never re-gathers its halo.
+__global__ void __launch_bounds__(256) k_warp_moving(Batch b, int mode) {
+    const int pair = blockIdx.y;
+    const PairState* st = b.st + pair;
+    if (st->done) return;
+    const Geo g = b.g;
+    const long long n = g.n;
+    const int buf = mode == 0 ? st->cur : 1 - st->cur;
+    const float* __restrict__ M = b.M + (long long)pair * n;
+    const float* __restrict__ U = b.U + ((long long)pair * 2 + buf) * 3 * n;
+    double* __restrict__ MW = b.MW + (long long)pair * n;
+    const int nxy = g.nx * g.ny;
+    constexpr int V = 4;
+    const long long stride = (long long)gridDim.x * blockDim.x * V;
+    for (long long base = ((long long)blockIdx.x * blockDim.x) * V + threadIdx.x; base < n; base += stride) {
+        CellD c[V];
+        float v[V][8];
+        int idx[V];
+#pragma unroll
+        for (int k = 0; k < V; ++k) {
+            const long long i = base + (long long)k * blockDim.x;
+            idx[k] = i < n ? (int)i : -1;
+            if (idx[k] >= 0) {
+                const int o = idx[k];
+                const int z = o / nxy, rem = o - z * nxy, y = rem / g.nx, x = rem - y * g.nx;
+                make_cell_d(c[k], g, x, y, z, __ldg(U + o), __ldg(U + n + o), __ldg(U + 2 * n + o));
+#pragma unroll
+                for (int j = 0; j < 8; ++j) v[k][j] = __ldg(M + c[k].o[j]);
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < V; ++k)
+            if (idx[k] >= 0) MW[idx[k]] = c[k].finite ? lerp_cell<false>(c[k], v[k], nullptr) : kNaN64;
+    }
+}
+
+// K1b: LNCC forward window pass.
+//   halo tile (H = R): f' = F - shift_f, m' = Mw - shift_m              (fp64)
 //   box sums S_f, S_m, S_ff, S_mm, S_fm over the truncated window      (fp64)
 //   rho = c / sqrt(vf vm); A = 1/(n sqrt(vf vm)); B = -rho/(n vm)  -> fp32
 //   E = A' mu_f' + B' mu_m'  (fp64, from the rounded A', B', so K2's
@@ -225,10 +264,8 @@ __global__ void __launch_bounds__(NT, 2) k_lncc_fwd(Batch b, LmParams p, int mod
     const long long n = g.n;
     Tile t;
     t.init(g, chunk_len);
-    const int buf = mode == 0 ? st->cur : 1 - st->cur;
     const float* __restrict__ F = b.F + (long long)pair * n;
-    const float* __restrict__ M = b.M + (long long)pair * n;
-    const float* __restrict__ U = b.U + ((long long)pair * 2 + buf) * 3 * n;
+    const double* __restrict__ MW = b.MW + (long long)pair * n;
     float* __restrict__ Aout = b.ABE + (long long)pair * 4 * n;
     float* __restrict__ Bout = Aout + n;
     double* __restrict__ Eout = reinterpret_cast<double*>(Aout + 2 * n);
@@ -237,56 +274,37 @@ __global__ void __launch_bounds__(NT, 2) k_lncc_fwd(Batch b, LmParams p, int mod
     it.init(t.x0, t.y0, g.nx, g.ny);
     const int cxy = t.own ? axis_count(t.x, g.nx, R) * axis_count(t.y, g.ny, R) : 1;
     const int ooff = t.x + g.nx * t.y;
+    (void)mode;
 
-    // pipeline registers: dense rows of plane z+1 (d1) and z+2 (d2); the 8
-    // gathered M corners of plane z+1 (gc).  The cell geometry is recomputed
-    // from d1 when the gather completes (fewer live registers).
-    float d1u[SL][3], d1f[SL], d2u[SL][3], d2f[SL];
-    float gc[SL][8];
-
-    auto load_dense = [&](int z, float (&du)[SL][3], float (&df)[SL]) {
+    // dense rows of the next plane (d1 -> shared memory at the end of the
+    // current plane) and of the plane after (d2, loads in flight)
+    float d1f[SL], d2f[SL];
+    double d1m[SL], d2m[SL];
+    auto load_dense = [&](int z, float (&df)[SL], double (&dm)[SL]) {
         const bool zin = z >= 0 && z < g.nz;
         const int po = z * t.nxy;
 #pragma unroll
         for (int s = 0; s < SL; ++s) {
             if (zin && it.goff[s] >= 0) {
                 const int o = po + it.goff[s];
-                du[s][0] = __ldg(U + o);
-                du[s][1] = __ldg(U + n + o);
-                du[s][2] = __ldg(U + 2 * n + o);
                 df[s] = __ldg(F + o);
+                dm[s] = __ldg(MW + o);
             } else {
-                du[s][0] = du[s][1] = du[s][2] = 0.f;
                 df[s] = 0.f;
+                dm[s] = 0.0;
             }
         }
     };
-    auto issue_gather = [&](int z) {
-        const bool zin = z >= 0 && z < g.nz;
-#pragma unroll
-        for (int s = 0; s < SL; ++s) {
-            if (zin && it.goff[s] >= 0) {
-                CellD c;
-                make_cell_d(c, g, it.gx[s], it.gy[s], z, d1u[s][0], d1u[s][1], d1u[s][2]);
-#pragma unroll
-                for (int k = 0; k < 8; ++k) gc[s][k] = __ldg(M + c.o[k]);
-            }
-        }
-    };
+    // absent (out-of-volume) items contribute 0 to every sum (truncated
+    // windows, A2); present items may carry NaN, which propagates
     auto complete = [&](int z, int sb) {
         const bool zin = z >= 0 && z < g.nz;
 #pragma unroll
         for (int s = 0; s < SL; ++s) {
             if (it.sidx[s] < 0) continue;
-            double fv = 0.0, mv = 0.0;
-            if (zin && it.goff[s] >= 0) {
-                CellD c;
-                make_cell_d(c, g, it.gx[s], it.gy[s], z, d1u[s][0], d1u[s][1], d1u[s][2]);
-                mv = c.finite ? lerp_cell<false>(c, gc[s], nullptr) - shm : kNaN64;
-                fv = (double)d1f[s] - shf;
-            }
-            s_f[sb][it.sidx[s]] = fv;
-            s_m[sb][it.sidx[s]] = mv;
+            const bool present = zin && it.goff[s] >= 0;
+            s_f[sb][it.sidx[s]] = present ? (double)d1f[s] - shf : 0.0;
+            s_m[sb][it.sidx[s]] = present ? d1m[s] - shm : 0.0;
         }
     };
 
@@ -301,10 +319,9 @@ __global__ void __launch_bounds__(NT, 2) k_lncc_fwd(Batch b, LmParams p, int mod
     double rho_acc = 0.0;
 
     const int z0 = t.zb - R, z1 = t.ze + R;  // input planes [z0, z1)
-    load_dense(z0, d1u, d1f);
-    issue_gather(z0);
+    load_dense(z0, d1f, d1m);
     complete(z0, 0);
-    load_dense(z0 + 1, d1u, d1f);
+    load_dense(z0 + 1, d1f, d1m);
     __syncthreads();
 
     for (int zbase = z0; zbase < z1; zbase += W) {
@@ -313,8 +330,7 @@ __global__ void __launch_bounds__(NT, 2) k_lncc_fwd(Batch b, LmParams p, int mod
             const int zi = zbase + ph;
             if (zi < z1) {
                 const int sb = (zi - z0) & 1;
-                load_dense(zi + 2, d2u, d2f);
-                issue_gather(zi + 1);
+                load_dense(zi + 2, d2f, d2m);
                 // x pass: 5-tap box of (f, m, ff, mm, fm)
 #pragma unroll
                 for (int q = 0; q < XS; ++q) {
@@ -379,7 +395,7 @@ __global__ void __launch_bounds__(NT, 2) k_lncc_fwd(Batch b, LmParams p, int mod
                 complete(zi + 1, sb ^ 1);
 #pragma unroll
                 for (int s = 0; s < SL; ++s) {
-                    d1u[s][0] = d2u[s][0]; d1u[s][1] = d2u[s][1]; d1u[s][2] = d2u[s][2];
+                    d1m[s] = d2m[s];
                     d1f[s] = d2f[s];
                 }
                 __syncthreads();
@@ -937,11 +953,14 @@ __global__ void __launch_bounds__(NT, 2) k_compose_smooth(Batch b, LmParams p, i
     }
 
 void launch_lncc_fwd(const Batch& b, const LmParams& p, int mode, cudaStream_t s) {
+    const long long per = (b.g.n + 1023) / 1024;  // 256 threads x 4 voxels per CTA-iteration
+    const int wb = (int)std::min<long long>(std::max<long long>(per, 1), 148LL * 16 / std::max(1, b.pairs) + 1);
+    k_warp_moving<<<dim3(wb, b.pairs), 256, 0, s>>>(b, mode);
     const LaunchShape sh = shape_for(b.g, b.pairs, TY);
     dim3 grid = sh.grid();
     grid.z = b.pairs;
     k_lncc_fwd<2><<<grid, NT, 0, s>>>(b, p, mode, sh.chunk_len);
-    ++g_kernel_launches;
+    g_kernel_launches += 2;
 }
 
 void launch_lncc_bwd(const Batch& b, const LmParams& p, cudaStream_t s) {

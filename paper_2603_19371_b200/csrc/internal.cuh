@@ -149,6 +149,7 @@ struct wlm_engine {
     wlm_reg_config cfg{};
     LmParams P{};
     DevBuf<float> F, M, U, ABE, G, VS, AM, AV;
+    DevBuf<double> MW;
     DevBuf<PairState> st;
     DevBuf<double> partials, script, shift_part;
     DevBuf<wlm_step_log> trace;
