@@ -206,39 +206,59 @@ constexpr double kNaN64 = __builtin_nan("");
 // exact fp64 weights -- field.cpp:47-90), one voxel per thread-iteration with
 // four independent gathers in flight per thread.  Written once per voxel, so
 // the LNCC window pass never re-gathers its halo.
+// One axis of the split-form cell: integer corner index and exact fp64
+// weight.  Interior samples (the common case) take the first branch; the
+// clamp rules of field.cpp:19-39 only run near the volume faces.
+__device__ __forceinline__ void axis_fast(int x, float u, int n, int& i0, int& step, double& t) {
+    const float fl = floorf(u);
+    const int i = x + (int)fl;
+    const double tt = (double)u - (double)fl;  // exact
+    if (i >= 0 && i <= n - 2) { i0 = i; step = 1; t = tt; return; }
+    if (n == 1) { i0 = 0; step = 0; t = 0.0; return; }
+    if (i < 0) { i0 = 0; step = 1; t = 0.0; return; }
+    i0 = n - 2; step = 1; t = 1.0;  // i >= n-1: at or beyond the last voxel
+}
+
+// Launch: block (32 x 8) = a 32 x 8 (x, y) tile of one plane; grid
+// (tiles, nz, pairs).  One voxel per thread, no index division, few
+// registers (high occupancy hides the gather latency).
 __global__ void __launch_bounds__(256) k_warp_moving(Batch b, int mode) {
-    const int pair = blockIdx.y;
+    const int pair = blockIdx.z;
     const PairState* st = b.st + pair;
     if (st->done) return;
     const Geo g = b.g;
     const long long n = g.n;
+    const int tiles_x = cdiv(g.nx, 32);
+    const int x = (blockIdx.x % tiles_x) * 32 + (threadIdx.x & 31);
+    const int y = (blockIdx.x / tiles_x) * 8 + (threadIdx.x >> 5);
+    if (x >= g.nx || y >= g.ny) return;
+    const int z = blockIdx.y;
     const int buf = mode == 0 ? st->cur : 1 - st->cur;
     const float* __restrict__ M = b.M + (long long)pair * n;
     const float* __restrict__ U = b.U + ((long long)pair * 2 + buf) * 3 * n;
-    double* __restrict__ MW = b.MW + (long long)pair * n;
-    const int nxy = g.nx * g.ny;
-    constexpr int V = 4;
-    const long long stride = (long long)gridDim.x * blockDim.x * V;
-    for (long long base = ((long long)blockIdx.x * blockDim.x) * V + threadIdx.x; base < n; base += stride) {
-        CellD c[V];
-        float v[V][8];
-        int idx[V];
-#pragma unroll
-        for (int k = 0; k < V; ++k) {
-            const long long i = base + (long long)k * blockDim.x;
-            idx[k] = i < n ? (int)i : -1;
-            if (idx[k] >= 0) {
-                const int o = idx[k];
-                const int z = o / nxy, rem = o - z * nxy, y = rem / g.nx, x = rem - y * g.nx;
-                make_cell_d(c[k], g, x, y, z, __ldg(U + o), __ldg(U + n + o), __ldg(U + 2 * n + o));
-#pragma unroll
-                for (int j = 0; j < 8; ++j) v[k][j] = __ldg(M + c[k].o[j]);
-            }
-        }
-#pragma unroll
-        for (int k = 0; k < V; ++k)
-            if (idx[k] >= 0) MW[idx[k]] = c[k].finite ? lerp_cell<false>(c[k], v[k], nullptr) : kNaN64;
+    const int o = x + g.nx * (y + g.ny * z);
+    const float ux = __ldg(U + o), uy = __ldg(U + n + o), uz = __ldg(U + 2 * n + o);
+    double mw;
+    if (isfinite(ux) && isfinite(uy) && isfinite(uz)) {
+        int ix, sx, iy, sy, iz, sz;
+        double tx, ty, tz;
+        axis_fast(x, ux, g.nx, ix, sx, tx);
+        axis_fast(y, uy, g.ny, iy, sy, ty);
+        axis_fast(z, uz, g.nz, iz, sz, tz);
+        const float* p = M + ix + g.nx * (iy + g.ny * iz);
+        const int dy = sy * g.nx, dz = sz * g.nx * g.ny;
+        const double a = __ldg(p), bb = __ldg(p + sx);
+        const double c = __ldg(p + dy), e = __ldg(p + dy + sx);
+        const double f = __ldg(p + dz), h = __ldg(p + dz + sx);
+        const double k = __ldg(p + dz + dy), l = __ldg(p + dz + dy + sx);
+        const double v00 = fma(tx, bb - a, a), v10 = fma(tx, e - c, c);
+        const double v01 = fma(tx, h - f, f), v11 = fma(tx, l - k, k);
+        const double s0 = fma(ty, v10 - v00, v00), s1 = fma(ty, v11 - v01, v01);
+        mw = fma(tz, s1 - s0, s0);
+    } else {
+        mw = kNaN64;
     }
+    b.MW[(long long)pair * n + o] = mw;
 }
 
 // K1b: LNCC forward window pass.
@@ -643,6 +663,7 @@ __global__ void __launch_bounds__(NT, 2) k_step_smooth(Batch b, LmParams p, int 
     const double wxy = t.own ? axis_wsum_t<double>(t.x, g.nx, R, p.wud, p.wud_full) *
                                    axis_wsum_t<double>(t.y, g.ny, R, p.wud, p.wud_full)
                              : 1.0;
+    const double inv_xy = 1.0 / wxy, inv_full = inv_xy / p.wud_full;
 
     float hg[SL][3];
     auto load_halo = [&](int z) {
@@ -716,7 +737,7 @@ __global__ void __launch_bounds__(NT, 2) k_step_smooth(Batch b, LmParams p, int 
                 }
                 const int zo = zi - R;
                 if (zo >= t.zb && t.own) {
-                    const double inv = 1.0 / (wxy * axis_wsum_t<double>(zo, g.nz, R, p.wud, p.wud_full));
+                    const double inv = (zo >= R && zo + R <= g.nz - 1) ? inv_full : inv_xy / axis_wsum_t<double>(zo, g.nz, R, p.wud, p.wud_full);
                     const int o = zo * t.nxy + ooff;
 #pragma unroll
                     for (int c = 0; c < 3; ++c) {
@@ -784,6 +805,7 @@ __global__ void __launch_bounds__(NT, 2) k_compose_smooth(Batch b, LmParams p, i
     const double wxy = t.own ? axis_wsum_t<double>(t.x, g.nx, R, p.wwd, p.wwd_full) *
                                    axis_wsum_t<double>(t.y, g.ny, R, p.wwd, p.wwd_full)
                              : 1.0;
+    const double inv_xy = 1.0 / wxy, inv_full = inv_xy / p.wwd_full;
 
     float pu[USL][3];  // warp rows of plane z + 2
     // step rows: the thread that loads item s also produces it, so the step
@@ -927,7 +949,7 @@ __global__ void __launch_bounds__(NT, 2) k_compose_smooth(Batch b, LmParams p, i
                 }
                 const int zo = zi - R;
                 if (zo >= t.zb && t.own) {
-                    const double inv = 1.0 / (wxy * axis_wsum_t<double>(zo, g.nz, R, p.wwd, p.wwd_full));
+                    const double inv = (zo >= R && zo + R <= g.nz - 1) ? inv_full : inv_xy / axis_wsum_t<double>(zo, g.nz, R, p.wwd, p.wwd_full);
                     const int o = zo * t.nxy + ooff;
 #pragma unroll
                     for (int c = 0; c < 3; ++c) {
@@ -953,9 +975,8 @@ __global__ void __launch_bounds__(NT, 2) k_compose_smooth(Batch b, LmParams p, i
     }
 
 void launch_lncc_fwd(const Batch& b, const LmParams& p, int mode, cudaStream_t s) {
-    const long long per = (b.g.n + 1023) / 1024;  // 256 threads x 4 voxels per CTA-iteration
-    const int wb = (int)std::min<long long>(std::max<long long>(per, 1), 148LL * 16 / std::max(1, b.pairs) + 1);
-    k_warp_moving<<<dim3(wb, b.pairs), 256, 0, s>>>(b, mode);
+    const dim3 wgrid(cdiv(b.g.nx, 32) * cdiv(b.g.ny, 8), b.g.nz, b.pairs);
+    k_warp_moving<<<wgrid, 256, 0, s>>>(b, mode);
     const LaunchShape sh = shape_for(b.g, b.pairs, TY);
     dim3 grid = sh.grid();
     grid.z = b.pairs;
