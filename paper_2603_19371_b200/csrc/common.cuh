@@ -17,16 +17,39 @@ namespace wlm {
 // In-volume offsets are 32-bit: one volume holds < 2^31 voxels (the
 // reference caps files at 2^31, io.cpp:13; engines reject larger volumes).
 // Batch/pair/channel bases are applied as 64-bit pointer offsets.
+//
+// z-slab decomposition (config 5): a rank owns planes
+// [zs, ze) of the global volume; its per-voxel buffers (warps, coefficients,
+// gradient, step) hold planes [zlo, zlo + nzl) = owned planes plus halo
+// planes filled by the exchange.  F and M are replicated whole (nfull).
+// Volume faces are always the global ones (z = 0, nz - 1).
 struct Geo {
-    int nx, ny, nz;
-    long long n;  // voxels per volume
+    int nx, ny, nz;   // global volume
+    long long n;      // voxels of one local buffer plane-stack (nx * ny * nzl)
+    int zs, ze;       // owned planes (global z)
+    int zlo, nzl;     // local buffer planes [zlo, zlo + nzl)
+    long long nfull;  // voxels of the whole volume (F, M)
     __host__ __device__ int at(int x, int y, int z) const { return x + nx * (y + ny * z); }
+    __host__ __device__ int lat(int x, int y, int z) const { return x + nx * (y + ny * (z - zlo)); }
 };
 
 inline Geo make_geo(wlm_dims d) {
     Geo g;
     g.nx = d.nx; g.ny = d.ny; g.nz = d.nz;
     g.n = (long long)d.nx * d.ny * d.nz;
+    g.zs = 0; g.ze = d.nz; g.zlo = 0; g.nzl = d.nz;
+    g.nfull = g.n;
+    return g;
+}
+
+// Slab geometry: owned [zs, ze), halo h planes each side (clipped to the volume).
+inline Geo make_slab_geo(wlm_dims d, int zs, int ze, int h) {
+    Geo g = make_geo(d);
+    g.zs = zs; g.ze = ze;
+    g.zlo = zs - h < 0 ? 0 : zs - h;
+    const int zhi = ze + h > d.nz ? d.nz : ze + h;
+    g.nzl = zhi - g.zlo;
+    g.n = (long long)d.nx * d.ny * g.nzl;
     return g;
 }
 

@@ -80,8 +80,10 @@ wlm_status engine_init(wlm_engine* e, wlm_ctx* ctx, wlm_dims d, int pairs, const
 void engine_alloc(wlm_engine* e) {
     wlm_ctx* ctx = e->ctx;
     const size_t n = (size_t)e->g.n, B = (size_t)e->pairs;
-    e->F = DevBuf<float>(ctx, B * n);
-    e->M = DevBuf<float>(ctx, B * n);
+    if (!e->shared_fm) {  // slab groups share one whole-volume F, M
+        e->F = DevBuf<float>(ctx, B * (size_t)e->g.nfull);
+        e->M = DevBuf<float>(ctx, B * (size_t)e->g.nfull);
+    }
     e->U = DevBuf<float>(ctx, B * 6 * n);
     e->ABE = DevBuf<float>(ctx, B * 4 * n);  // A, B fp32 + E fp64
     e->MW = DevBuf<double>(ctx, B * n);
@@ -97,21 +99,24 @@ void engine_alloc(wlm_engine* e) {
     }
     e->st = DevBuf<PairState>(ctx, B);
     CK(cudaMemsetAsync(e->st.p, 0, sizeof(PairState) * B, ctx->stream));
-    const LaunchShape sh = shape_for(e->g, e->pairs, 8);
-    const int maxb = sh.tiles_x * sh.tiles_y * sh.chunks;
-    e->partials = DevBuf<double>(ctx, B * (size_t)maxb);
+    const int tiles = plane_tiles(e->g);
+    e->partials = DevBuf<double>(ctx, B * (size_t)e->g.nz * tiles * 8);
+    if (!e->shared_plane_sum) e->plane_sum = DevBuf<double>(ctx, B * (size_t)e->g.nz);
     e->trace = DevBuf<wlm_step_log>(ctx, B * (size_t)e->P.trace_cap);
     e->P.trace = e->trace.p;
     Batch& b = e->B;
     b.g = e->g;
     b.pairs = e->pairs;
-    b.F = e->F.p; b.M = e->M.p; b.U = e->U.p; b.ABE = e->ABE.p; b.G = e->G.p; b.VS = e->VS.p;
+    if (!e->shared_fm) { b.F = e->F.p; b.M = e->M.p; }
+    b.U = e->U.p; b.ABE = e->ABE.p; b.G = e->G.p; b.VS = e->VS.p;
     b.AM = e->AM.p; b.AV = e->AV.p;
     b.MW = e->MW.p;
     b.st = e->st.p;
     b.partials = e->partials.p;
+    if (!e->shared_plane_sum) b.plane_sum = e->plane_sum.p;
+    b.zero_foreign_planes = 0;
     b.shift_part = e->shift_part.p;
-    b.max_blocks = maxb;
+    b.max_blocks = tiles;
     CK(cudaMemsetAsync(e->U.p, 0, sizeof(float) * B * 6 * n, ctx->stream));
     launch_begin_level(b, e->P, 0, 1, e->cfg.lm.lambda0, ctx->stream);
 }
@@ -243,7 +248,7 @@ wlm_status wlm_engine_load(wlm_engine* e, const float* F, const float* M, int is
     if (!e || !F || !M) return WLM_INVALID_ARG;
     wlm_ctx* ctx = e->ctx;
     return run(ctx, [&] {
-        const size_t bytes = sizeof(float) * (size_t)e->g.n * e->pairs;
+        const size_t bytes = sizeof(float) * (size_t)e->g.nfull * e->pairs;
         const cudaMemcpyKind k = is_host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
         CK(cudaMemcpyAsync(e->F.p, F, bytes, k, ctx->stream));
         CK(cudaMemcpyAsync(e->M.p, M, bytes, k, ctx->stream));
@@ -277,7 +282,8 @@ wlm_status wlm_engine_begin_level(wlm_engine* e, int level) {
     wlm_ctx* ctx = e->ctx;
     return run(ctx, [&] {
         launch_begin_level(e->B, e->P, level, 0, e->cfg.lm.lambda0, ctx->stream);
-        launch_lncc_fwd(e->B, e->P, 0, ctx->stream);
+        e->stage_eval(0, ctx->stream);
+        e->stage_finalize(0, ctx->stream);
     });
 }
 
@@ -315,11 +321,11 @@ wlm_status wlm_engine_stage(wlm_engine* e, int stage) {
     wlm_ctx* ctx = e->ctx;
     return run(ctx, [&] {
         switch (stage) {
-            case 0: launch_lncc_fwd(e->B, e->P, 1, ctx->stream); break;
+            case 0: e->stage_eval(1, ctx->stream); e->stage_finalize(1, ctx->stream); break;
             case 1: launch_lncc_bwd(e->B, e->P, ctx->stream); break;
             case 2: launch_step_smooth(e->B, e->P, ctx->stream); break;
             case 3: launch_compose_smooth(e->B, e->P, ctx->stream); break;
-            default: launch_lncc_fwd(e->B, e->P, 0, ctx->stream); break;
+            default: e->stage_eval(0, ctx->stream); e->stage_finalize(0, ctx->stream); break;
         }
     });
 }

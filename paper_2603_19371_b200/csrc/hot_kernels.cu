@@ -1,16 +1,28 @@
-// hot_kernels.cu -- the four kernels of one LM attempt
-// and the device-side loss / damping / rejection state machine (K5).
+// hot_kernels.cu -- the kernels of one LM attempt.
 //
-// Schedule (hot.cuh): a CTA owns a 32 x 8 column of output voxels and a chunk
-// of z planes.  Per input plane it
-//   * produces an fp64 halo tile in shared memory from inputs that were
-//     prefetched into registers two planes ahead (dense rows) and one plane
-//     ahead (data-dependent gathers),
-//   * filters it along x (shared memory) and y (shared memory -> registers),
-//   * and along z through a statically indexed register ring (the z loop is
-//     unrolled by the ring length, so the ring never moves).
+//   K1a k_warp_moving    Mw = M(x + u) in fp64 (flat gather kernel)
+//   K1b k_lncc_fwd       LNCC window moments -> rho, A, B, E; per-plane sum(rho)
+//   K5  k_finalize       sum(rho) in z order -> r; loss/damping/rejection state
+//   K2  k_lncc_bwd       adjoint window sums -> g
+//   K3  k_step_smooth    LM step + Gaussian(sigma_update) + max|.|
+//   K4  k_compose_smooth compositive resample + Gaussian(sigma_warp)
+//
+// Schedule of the stencil kernels (hot.cuh): a CTA owns a 32 x 8 column of
+// output voxels and a chunk of the rank's owned z planes.  Per input plane it
+//   * produces an fp64 halo tile in shared memory from inputs prefetched into
+//     registers one or two planes ahead,
+//   * filters it along x (shared memory), y (shared memory -> registers) and
+//     z through a statically indexed register ring (the z loop is unrolled by
+//     the ring length; z sums are taken directly over the ring, so every
+//     voxel's arithmetic is independent of chunking and of the slab split).
 // Every global access is a unit-stride row of one SoA plane.  Sums are fp64
-// (DESIGN.md "Precision"); reductions are fixed-order.
+// (DESIGN.md "Precision"); sum(rho) is reduced per plane in a fixed order and
+// then over planes in z order, so results are bit-identical for any batch
+// size, chunking or number of z slabs.
+//
+// Slabs (Geo in common.cuh): per-voxel buffers are local ([zlo, zlo+nzl),
+// indexed with Geo::lat), F and M are whole-volume (Geo::at), faces are the
+// global ones.
 #include <cfloat>
 #include <climits>
 
@@ -40,8 +52,7 @@ void init_constants() {
 }
 
 // ---------------------------------------------------------------------------
-// Loss / damping / rejection state machine, run by one
-// thread of the last CTA of the evaluation kernel.  Identical fp64
+// Loss / damping / rejection state machine.  Identical fp64
 // arithmetic to the oracle (oracle.cpp orc_update_damping /
 // attempt_rejected), so the lambda trajectory is bit-identical whenever the
 // accept/reject decisions agree.
@@ -136,7 +147,8 @@ static __device__ double block_sum(double v, double* red) {
     return s;
 }
 
-// Geometry shared by the hot kernels.
+// Geometry shared by the stencil kernels: this CTA's 32 x 8 column and its
+// chunk of owned planes.
 struct Tile {
     int x0, y0, zb, ze;
     int ox, oy, x, y;
@@ -146,8 +158,8 @@ struct Tile {
         const int tiles_x = cdiv(g.nx, TX);
         x0 = (blockIdx.x % tiles_x) * TX;
         y0 = (blockIdx.x / tiles_x) * TY;
-        zb = blockIdx.y * chunk_len;
-        ze = min(zb + chunk_len, g.nz);
+        zb = g.zs + blockIdx.y * chunk_len;
+        ze = min(zb + chunk_len, g.ze);
         ox = threadIdx.x & 31;
         oy = threadIdx.x >> 5;
         x = x0 + ox;
@@ -155,110 +167,87 @@ struct Tile {
         own = x < g.nx && y < g.ny;
         nxy = g.nx * g.ny;
     }
+    // offset of plane z in a local (slab) buffer / in a whole-volume buffer
+    __device__ __forceinline__ int lp(const Geo& g, int z) const { return (z - g.zlo) * nxy; }
+    __device__ __forceinline__ int gp(int z) const { return z * nxy; }
 };
 
-// Trilinear cell of a sample at integer voxel (x,y,z) displaced by float u,
-// fp64 weights, 32-bit corner offsets (field.cpp:19-39 in split form).
-struct CellD {
-    int o[8];
-    double tx, ty, tz;
-    bool ox_, oy_, oz_;  // axis outside (gradient 0)
-    bool finite;
+// One axis of the split-form cell (field.cpp:19-39): integer corner index,
+// exact fp64 weight, "outside" flag (gradient 0).  Interior samples take the
+// first branch; the clamp rules only run near the volume faces.
+struct Tap {
+    int i0, step;
+    double t;
+    bool outside;
 };
 
-__device__ __forceinline__ void make_cell_d(CellD& c, const Geo& g, int x, int y, int z, float ux, float uy,
-                                            float uz) {
-    c.finite = isfinite(ux) && isfinite(uy) && isfinite(uz);
-    const AxisTapD X = axis_tap_dd(x, c.finite ? ux : 0.f, g.nx);
-    const AxisTapD Y = axis_tap_dd(y, c.finite ? uy : 0.f, g.ny);
-    const AxisTapD Z = axis_tap_dd(z, c.finite ? uz : 0.f, g.nz);
-    const int r00 = g.nx * (Y.i0 + g.ny * Z.i0), r10 = g.nx * (Y.i1 + g.ny * Z.i0);
-    const int r01 = g.nx * (Y.i0 + g.ny * Z.i1), r11 = g.nx * (Y.i1 + g.ny * Z.i1);
-    c.o[0] = r00 + X.i0; c.o[1] = r00 + X.i1; c.o[2] = r10 + X.i0; c.o[3] = r10 + X.i1;
-    c.o[4] = r01 + X.i0; c.o[5] = r01 + X.i1; c.o[6] = r11 + X.i0; c.o[7] = r11 + X.i1;
-    c.tx = X.t; c.ty = Y.t; c.tz = Z.t;
-    c.ox_ = X.outside; c.oy_ = Y.outside; c.oz_ = Z.outside;
+__device__ __forceinline__ Tap axis_split(int x, float u, int n) {
+    Tap a;
+    const float fl = floorf(u);
+    const int i = x + (int)fl;
+    const double tt = (double)u - (double)fl;  // exact, in [0, 1)
+    if (i >= 0 && i <= n - 2) { a.i0 = i; a.step = 1; a.t = tt; a.outside = false; return a; }
+    if (n == 1) { a.i0 = 0; a.step = 0; a.t = 0.0; a.outside = true; return a; }
+    if (i < 0) { a.i0 = 0; a.step = 1; a.t = 0.0; a.outside = true; return a; }
+    a.i0 = n - 2; a.step = 1; a.t = 1.0;
+    a.outside = i > n - 1 || tt > 0.0;  // exactly on the last voxel: not outside
+    return a;
 }
 
-// Value (+ gradient) of the trilinear interpolant from 8 fp32 corners, fp64,
-// collapse order of field.cpp:47-90.
+// Sample (and analytic gradient) of a whole-volume fp32 image at voxel
+// (x,y,z) + u, fp64, collapse order of field.cpp:47-90.  Non-finite u ->
+// NaN value, zero gradient (field.cpp:49-52).
 template <bool GRAD>
-__device__ __forceinline__ double lerp_cell(const CellD& c, const float* v, double* grad) {
-    const double a = v[0], b = v[1], cc = v[2], e = v[3], f = v[4], h = v[5], k = v[6], l = v[7];
-    const double d00 = b - a, d10 = e - cc, d01 = h - f, d11 = l - k;
-    const double v00 = fma(c.tx, d00, a), v10 = fma(c.tx, d10, cc);
-    const double v01 = fma(c.tx, d01, f), v11 = fma(c.tx, d11, k);
-    const double s0 = fma(c.ty, v10 - v00, v00), s1 = fma(c.ty, v11 - v01, v01);
-    if (GRAD) {
-        const double gx0 = fma(c.ty, d10 - d00, d00), gx1 = fma(c.ty, d11 - d01, d01);
-        grad[0] = c.ox_ ? 0.0 : fma(c.tz, gx1 - gx0, gx0);
-        const double gy0 = v10 - v00, gy1 = v11 - v01;
-        grad[1] = c.oy_ ? 0.0 : fma(c.tz, gy1 - gy0, gy0);
-        grad[2] = c.oz_ ? 0.0 : s1 - s0;
+__device__ __forceinline__ double sample_vol(const float* __restrict__ M, const Geo& g, int x, int y, int z,
+                                             float ux, float uy, float uz, double* grad) {
+    if (!(isfinite(ux) && isfinite(uy) && isfinite(uz))) {
+        if (GRAD) grad[0] = grad[1] = grad[2] = 0.0;
+        return __longlong_as_double(0x7ff8000000000000ll);
     }
-    return fma(c.tz, s1 - s0, s0);
+    const Tap X = axis_split(x, ux, g.nx), Y = axis_split(y, uy, g.ny), Z = axis_split(z, uz, g.nz);
+    const float* p = M + X.i0 + g.nx * (Y.i0 + g.ny * Z.i0);
+    const int sx = X.step, dy = Y.step * g.nx, dz = Z.step * g.nx * g.ny;
+    const double a = __ldg(p), b = __ldg(p + sx);
+    const double c = __ldg(p + dy), e = __ldg(p + dy + sx);
+    const double f = __ldg(p + dz), h = __ldg(p + dz + sx);
+    const double k = __ldg(p + dz + dy), l = __ldg(p + dz + dy + sx);
+    const double d00 = b - a, d10 = e - c, d01 = h - f, d11 = l - k;
+    const double v00 = fma(X.t, d00, a), v10 = fma(X.t, d10, c);
+    const double v01 = fma(X.t, d01, f), v11 = fma(X.t, d11, k);
+    const double s0 = fma(Y.t, v10 - v00, v00), s1 = fma(Y.t, v11 - v01, v01);
+    if (GRAD) {
+        const double gx0 = fma(Y.t, d10 - d00, d00), gx1 = fma(Y.t, d11 - d01, d01);
+        grad[0] = X.outside ? 0.0 : fma(Z.t, gx1 - gx0, gx0);
+        const double gy0 = v10 - v00, gy1 = v11 - v01;
+        grad[1] = Y.outside ? 0.0 : fma(Z.t, gy1 - gy0, gy0);
+        grad[2] = Z.outside ? 0.0 : s1 - s0;
+    }
+    return fma(Z.t, s1 - s0, s0);
 }
 
 constexpr double kNaN64 = __builtin_nan("");
 
 // ---------------------------------------------------------------------------
-// K1a: warp of the moving image, Mw(x) = M(x + u(x)) in fp64 (fp32 samples,
-// exact fp64 weights -- field.cpp:47-90), one voxel per thread-iteration with
-// four independent gathers in flight per thread.  Written once per voxel, so
-// the LNCC window pass never re-gathers its halo.
-// One axis of the split-form cell: integer corner index and exact fp64
-// weight.  Interior samples (the common case) take the first branch; the
-// clamp rules of field.cpp:19-39 only run near the volume faces.
-__device__ __forceinline__ void axis_fast(int x, float u, int n, int& i0, int& step, double& t) {
-    const float fl = floorf(u);
-    const int i = x + (int)fl;
-    const double tt = (double)u - (double)fl;  // exact
-    if (i >= 0 && i <= n - 2) { i0 = i; step = 1; t = tt; return; }
-    if (n == 1) { i0 = 0; step = 0; t = 0.0; return; }
-    if (i < 0) { i0 = 0; step = 1; t = 0.0; return; }
-    i0 = n - 2; step = 1; t = 1.0;  // i >= n-1: at or beyond the last voxel
-}
-
-// Launch: block (32 x 8) = a 32 x 8 (x, y) tile of one plane; grid
-// (tiles, nz, pairs).  One voxel per thread, no index division, few
-// registers (high occupancy hides the gather latency).
-__global__ void __launch_bounds__(256) k_warp_moving(Batch b, int mode) {
+// K1a: warp of the moving image, Mw(x) = M(x + u(x)) in fp64, for the owned
+// planes plus the 2 halo planes the window pass reads.  Block (32 x 8) = a
+// 32 x 8 (x, y) tile of one plane; one voxel per thread, few registers (high
+// occupancy hides the gather latency).
+__global__ void __launch_bounds__(256) k_warp_moving(Batch b, int mode, int z_first) {
     const int pair = blockIdx.z;
     const PairState* st = b.st + pair;
     if (st->done) return;
     const Geo g = b.g;
-    const long long n = g.n;
     const int tiles_x = cdiv(g.nx, 32);
     const int x = (blockIdx.x % tiles_x) * 32 + (threadIdx.x & 31);
     const int y = (blockIdx.x / tiles_x) * 8 + (threadIdx.x >> 5);
     if (x >= g.nx || y >= g.ny) return;
-    const int z = blockIdx.y;
+    const int z = z_first + blockIdx.y;
     const int buf = mode == 0 ? st->cur : 1 - st->cur;
-    const float* __restrict__ M = b.M + (long long)pair * n;
-    const float* __restrict__ U = b.U + ((long long)pair * 2 + buf) * 3 * n;
-    const int o = x + g.nx * (y + g.ny * z);
-    const float ux = __ldg(U + o), uy = __ldg(U + n + o), uz = __ldg(U + 2 * n + o);
-    double mw;
-    if (isfinite(ux) && isfinite(uy) && isfinite(uz)) {
-        int ix, sx, iy, sy, iz, sz;
-        double tx, ty, tz;
-        axis_fast(x, ux, g.nx, ix, sx, tx);
-        axis_fast(y, uy, g.ny, iy, sy, ty);
-        axis_fast(z, uz, g.nz, iz, sz, tz);
-        const float* p = M + ix + g.nx * (iy + g.ny * iz);
-        const int dy = sy * g.nx, dz = sz * g.nx * g.ny;
-        const double a = __ldg(p), bb = __ldg(p + sx);
-        const double c = __ldg(p + dy), e = __ldg(p + dy + sx);
-        const double f = __ldg(p + dz), h = __ldg(p + dz + sx);
-        const double k = __ldg(p + dz + dy), l = __ldg(p + dz + dy + sx);
-        const double v00 = fma(tx, bb - a, a), v10 = fma(tx, e - c, c);
-        const double v01 = fma(tx, h - f, f), v11 = fma(tx, l - k, k);
-        const double s0 = fma(ty, v10 - v00, v00), s1 = fma(ty, v11 - v01, v01);
-        mw = fma(tz, s1 - s0, s0);
-    } else {
-        mw = kNaN64;
-    }
-    b.MW[(long long)pair * n + o] = mw;
+    const float* __restrict__ M = b.M + (long long)pair * g.nfull;
+    const float* __restrict__ U = b.U + ((long long)pair * 2 + buf) * 3 * g.n;
+    const int o = g.lat(x, y, z);
+    b.MW[(long long)pair * g.n + o] =
+        sample_vol<false>(M, g, x, y, z, __ldg(U + o), __ldg(U + g.n + o), __ldg(U + 2 * g.n + o), nullptr);
 }
 
 // K1b: LNCC forward window pass.
@@ -266,35 +255,36 @@ __global__ void __launch_bounds__(256) k_warp_moving(Batch b, int mode) {
 //   box sums S_f, S_m, S_ff, S_mm, S_fm over the truncated window      (fp64)
 //   rho = c / sqrt(vf vm); A = 1/(n sqrt(vf vm)); B = -rho/(n vm)  -> fp32
 //   E = A' mu_f' + B' mu_m'  (fp64, from the rounded A', B', so K2's
-//   f' S_A + m' S_B - S_E cancels exactly);  sum(rho) -> per-CTA partial.
+//   f' S_A + m' S_B - S_E cancels exactly).
+//   sum(rho): one partial per (plane, tile, warp); the last CTA of the pair
+//   reduces them per owned plane in a fixed order into plane_sum[z].
 template <int R>
-__global__ void __launch_bounds__(NT, 2) k_lncc_fwd(Batch b, LmParams p, int mode, int chunk_len) {
+__global__ void __launch_bounds__(NT, 2) k_lncc_fwd(Batch b, int chunk_len) {
     using It = hot::Items<R>;
     constexpr int IW = It::IW, IH = It::IH, NI = It::NI, SL = It::SLOTS, W = 2 * R + 1;
     constexpr int XS = (IH * TX + NT - 1) / NT;  // x-pass items per thread
     __shared__ double s_f[2][NI], s_m[2][NI];
     __shared__ double s_x[5][IH][TX];
-    __shared__ double s_red[NT / 32];
     __shared__ int s_last;
 
     const int pair = blockIdx.z;
     PairState* st = b.st + pair;
     if (st->done) return;
     const Geo g = b.g;
-    const long long n = g.n;
     Tile t;
     t.init(g, chunk_len);
-    const float* __restrict__ F = b.F + (long long)pair * n;
-    const double* __restrict__ MW = b.MW + (long long)pair * n;
-    float* __restrict__ Aout = b.ABE + (long long)pair * 4 * n;
-    float* __restrict__ Bout = Aout + n;
-    double* __restrict__ Eout = reinterpret_cast<double*>(Aout + 2 * n);
+    const float* __restrict__ F = b.F + (long long)pair * g.nfull;
+    const double* __restrict__ MW = b.MW + (long long)pair * g.n;
+    float* __restrict__ Aout = b.ABE + (long long)pair * 4 * g.n;
+    float* __restrict__ Bout = Aout + g.n;
+    double* __restrict__ Eout = reinterpret_cast<double*>(Aout + 2 * g.n);
     const double shf = st->shift_f, shm = st->shift_m;
+    const int tiles = cdiv(g.nx, TX) * cdiv(g.ny, TY);
+    double* __restrict__ part = b.partials + (long long)pair * g.nz * tiles * (NT / 32);
     It it;
     it.init(t.x0, t.y0, g.nx, g.ny);
     const int cxy = t.own ? axis_count(t.x, g.nx, R) * axis_count(t.y, g.ny, R) : 1;
     const int ooff = t.x + g.nx * t.y;
-    (void)mode;
 
     // dense rows of the next plane (d1 -> shared memory at the end of the
     // current plane) and of the plane after (d2, loads in flight)
@@ -302,13 +292,11 @@ __global__ void __launch_bounds__(NT, 2) k_lncc_fwd(Batch b, LmParams p, int mod
     double d1m[SL], d2m[SL];
     auto load_dense = [&](int z, float (&df)[SL], double (&dm)[SL]) {
         const bool zin = z >= 0 && z < g.nz;
-        const int po = z * t.nxy;
 #pragma unroll
         for (int s = 0; s < SL; ++s) {
             if (zin && it.goff[s] >= 0) {
-                const int o = po + it.goff[s];
-                df[s] = __ldg(F + o);
-                dm[s] = __ldg(MW + o);
+                df[s] = __ldg(F + t.gp(z) + it.goff[s]);
+                dm[s] = __ldg(MW + t.lp(g, z) + it.goff[s]);
             } else {
                 df[s] = 0.f;
                 dm[s] = 0.0;
@@ -329,14 +317,10 @@ __global__ void __launch_bounds__(NT, 2) k_lncc_fwd(Batch b, LmParams p, int mod
     };
 
     double ring[W][5];
-    double S[5];
 #pragma unroll
     for (int d = 0; d < W; ++d)
 #pragma unroll
         for (int c = 0; c < 5; ++c) ring[d][c] = 0.0;
-#pragma unroll
-    for (int c = 0; c < 5; ++c) S[c] = 0.0;
-    double rho_acc = 0.0;
 
     const int z0 = t.zb - R, z1 = t.ze + R;  // input planes [z0, z1)
     load_dense(z0, d1f, d1m);
@@ -374,44 +358,52 @@ __global__ void __launch_bounds__(NT, 2) k_lncc_fwd(Batch b, LmParams p, int mod
                     }
                 }
                 __syncthreads();
-                // y pass + running z sum over the static ring
-                double P[5];
+                // y pass into the static ring; z sum taken directly over the ring
 #pragma unroll
                 for (int c = 0; c < 5; ++c) {
                     double s = 0.0;
 #pragma unroll
                     for (int d = 0; d < W; ++d) s += s_x[c][t.oy + d][t.ox];
-                    P[c] = s;
-                    S[c] += s - ring[ph][c];
                     ring[ph][c] = s;
                 }
                 const int zo = zi - R;
-                if (zo >= t.zb && t.own) {
-                    const double inv = c_inv_count[cxy * axis_count(zo, g.nz, R)];
-                    const double mf = S[0] * inv, mm = S[1] * inv;
-                    const double vf = fma(-mf, mf, S[2] * inv);
-                    const double vm = fma(-mm, mm, S[3] * inv);
-                    const double cv = fma(-mf, mm, S[4] * inv);
-                    const double af = mf + shf, am = mm + shm;
-                    const double msf = fma(af, af, vf), msm = fma(am, am, vm);
-                    double rho = 0.0, Ee = 0.0;
-                    float Aa = 0.f, Bb = 0.f;
-                    // NaN moments are not degenerate: non-finite inputs reach the loss
-                    const bool degenerate = msf <= 0.0 || msm <= 0.0 || vf <= 1e-9 * msf || vm <= 1e-9 * msm;
-                    if (!degenerate) {
-                        const double alpha = hot::rsqrt_d(vf * vm);
-                        rho = cv * alpha;
-                        Aa = (float)(alpha * inv);
-                        Bb = (float)(-rho * alpha * alpha * vf * inv);  // -rho / (n vm)
-                        Ee = fma((double)Aa, mf, (double)Bb * mm);
+                if (zo >= t.zb) {
+                    double rho = 0.0;
+                    if (t.own) {
+                        double S[5];
+#pragma unroll
+                        for (int c = 0; c < 5; ++c) {
+                            double s = 0.0;
+#pragma unroll
+                            for (int d = 0; d < W; ++d) s += ring[(ph + 1 + d) % W][c];
+                            S[c] = s;
+                        }
+                        const double inv = c_inv_count[cxy * axis_count(zo, g.nz, R)];
+                        const double mf = S[0] * inv, mm = S[1] * inv;
+                        const double vf = fma(-mf, mf, S[2] * inv);
+                        const double vm = fma(-mm, mm, S[3] * inv);
+                        const double cv = fma(-mf, mm, S[4] * inv);
+                        const double af = mf + shf, am = mm + shm;
+                        const double msf = fma(af, af, vf), msm = fma(am, am, vm);
+                        double Ee = 0.0;
+                        float Aa = 0.f, Bb = 0.f;
+                        // NaN moments are not degenerate: non-finite inputs reach the loss
+                        const bool degenerate = msf <= 0.0 || msm <= 0.0 || vf <= 1e-9 * msf || vm <= 1e-9 * msm;
+                        if (!degenerate) {
+                            const double alpha = hot::rsqrt_d(vf * vm);
+                            rho = cv * alpha;
+                            Aa = (float)(alpha * inv);
+                            Bb = (float)(-rho * alpha * alpha * vf * inv);  // -rho / (n vm)
+                            Ee = fma((double)Aa, mf, (double)Bb * mm);
+                        }
+                        const int o = t.lp(g, zo) + ooff;
+                        Aout[o] = Aa;
+                        Bout[o] = Bb;
+                        Eout[o] = Ee;
                     }
-                    const int o = zo * t.nxy + ooff;
-                    Aout[o] = Aa;
-                    Bout[o] = Bb;
-                    Eout[o] = Ee;
-                    rho_acc += rho;
+                    rho = warp_sum(rho);
+                    if (t.ox == 0) part[((long long)zo * tiles + blockIdx.x) * (NT / 32) + t.oy] = rho;
                 }
-                (void)P;
                 complete(zi + 1, sb ^ 1);
 #pragma unroll
                 for (int s = 0; s < SL; ++s) {
@@ -423,11 +415,9 @@ __global__ void __launch_bounds__(NT, 2) k_lncc_fwd(Batch b, LmParams p, int mod
         }
     }
 
-    const double tot = block_sum(rho_acc, s_red);
+    // the pair's last CTA reduces the owned planes' partials, fixed order
     const int nblk = gridDim.x * gridDim.y;
-    const int blk = blockIdx.x + gridDim.x * blockIdx.y;
     if (threadIdx.x == 0) {
-        b.partials[(long long)pair * b.max_blocks + blk] = tot;
         __threadfence();
         const unsigned prev = atomicAdd(&st->counter, 1u);
         s_last = prev == (unsigned)(nblk - 1);
@@ -435,13 +425,32 @@ __global__ void __launch_bounds__(NT, 2) k_lncc_fwd(Batch b, LmParams p, int mod
     __syncthreads();
     if (!s_last) return;
     __threadfence();
-    double s = 0.0;
-    for (int i = threadIdx.x; i < nblk; i += NT) s += __ldcg(b.partials + (long long)pair * b.max_blocks + i);
-    const double total = block_sum(s, s_red);
-    if (threadIdx.x == 0) {
-        st->counter = 0u;
-        finalize_pair(st, p, mode, total / (double)n, pair);
+    double* __restrict__ psum = b.plane_sum + (long long)pair * g.nz;
+    for (int z = threadIdx.x; z < g.nz; z += NT) {
+        double s = 0.0;
+        if (z >= g.zs && z < g.ze) {
+            const double* pz = part + (long long)z * tiles * (NT / 32);
+            for (int i = 0; i < tiles * (NT / 32); ++i) s += __ldcg(pz + i);
+        }
+        if (z >= g.zs && z < g.ze) psum[z] = s;
+        else if (b.zero_foreign_planes) psum[z] = 0.0;
     }
+    if (threadIdx.x == 0) st->counter = 0u;
+}
+
+// K5: r from the per-plane sums in z order (identical on every rank for any
+// slab split), then the loss / damping / rejection state machine.
+__global__ void k_finalize(Batch b, LmParams p, int mode) {
+    __shared__ double red[32];
+    const int pair = blockIdx.x;
+    PairState* st = b.st + pair;
+    if (st->done) return;
+    const double* psum = b.plane_sum + (long long)pair * b.g.nz;
+    double s = 0.0;
+    // fixed partition of z (thread t: z = t, t+NT, ...), then a fixed tree
+    for (int z = threadIdx.x; z < b.g.nz; z += blockDim.x) s += psum[z];
+    const double tot = block_sum(s, red);
+    if (threadIdx.x == 0) finalize_pair(st, p, mode, tot / (double)b.g.nfull, pair);
 }
 
 // ---------------------------------------------------------------------------
@@ -464,29 +473,29 @@ __global__ void __launch_bounds__(NT, 2) k_lncc_bwd(Batch b, LmParams p, int chu
     const long long n = g.n;
     Tile t;
     t.init(g, chunk_len);
-    const float* __restrict__ F = b.F + (long long)pair * n;
-    const float* __restrict__ M = b.M + (long long)pair * n;
+    const float* __restrict__ F = b.F + (long long)pair * g.nfull;
+    const float* __restrict__ M = b.M + (long long)pair * g.nfull;
     const float* __restrict__ U = b.U + ((long long)pair * 2 + st->cur) * 3 * n;
     const float* __restrict__ A = b.ABE + (long long)pair * 4 * n;
     const float* __restrict__ Bc = A + n;
     const double* __restrict__ E = reinterpret_cast<const double*>(A + 2 * n);
     float* __restrict__ G = b.G + (long long)pair * 3 * n;
     const double shf = st->shift_f, shm = st->shift_m;
-    const double invN = 1.0 / (double)n;
+    const double invN = 1.0 / (double)g.nfull;
     It it;
     it.init(t.x0, t.y0, g.nx, g.ny);
     const int ooff = t.x + g.nx * t.y;
+    (void)p;
 
     // halo rows of plane z+1
     float ha[SL], hb[SL];
     double he[SL];
     auto load_halo = [&](int z) {
         const bool zin = z >= 0 && z < g.nz;
-        const int po = z * t.nxy;
 #pragma unroll
         for (int s = 0; s < SL; ++s) {
             if (zin && it.goff[s] >= 0) {
-                const int o = po + it.goff[s];
+                const int o = t.lp(g, z) + it.goff[s];
                 ha[s] = __ldg(A + o);
                 hb[s] = __ldg(Bc + o);
                 he[s] = __ldg(E + o);
@@ -505,49 +514,44 @@ __global__ void __launch_bounds__(NT, 2) k_lncc_bwd(Batch b, LmParams p, int chu
             s_in[sb][2][it.sidx[s]] = he[s];
         }
     };
-    // output-voxel pipeline: dense (u, F) of output plane zo+2, gathers of zo+1
-    float ou2[3], of2, ou1[3], of1;
-    CellD ocell_next, ocell_cur;
-    float oc_next[8], oc_cur[8];
-    float of_next = 0.f, of_cur = 0.f;
+    // output-voxel pipeline: u and F of output plane zo+2 (dense), the 8 M
+    // corners of zo+1 (gathers in flight), those of zo (consumed now)
+    float ou2[3], of2 = 0.f, ou1[3], of1 = 0.f, ou0[3], of0 = 0.f;
+    float oc1[8], oc0[8];
     auto load_own = [&](int zo, float (&u)[3], float& f) {
         if (t.own && zo >= t.zb && zo < t.ze) {
-            const int o = zo * t.nxy + ooff;
+            const int o = t.lp(g, zo) + ooff;
             u[0] = __ldg(U + o); u[1] = __ldg(U + n + o); u[2] = __ldg(U + 2 * n + o);
-            f = __ldg(F + o);
+            f = __ldg(F + t.gp(zo) + ooff);
         } else {
             u[0] = u[1] = u[2] = 0.f;
             f = 0.f;
         }
     };
-    auto gather_own = [&](int zo, const float (&u)[3], float f) {
-        of_next = f;
-        if (t.own && zo >= t.zb && zo < t.ze) {
-            make_cell_d(ocell_next, g, t.x, t.y, zo, u[0], u[1], u[2]);
-#pragma unroll
-            for (int k = 0; k < 8; ++k) oc_next[k] = __ldg(M + ocell_next.o[k]);
+    auto gather_own = [&](int zo, const float (&u)[3], float (&c)[8]) {
+        if (t.own && zo >= t.zb && zo < t.ze && isfinite(u[0]) && isfinite(u[1]) && isfinite(u[2])) {
+            const Tap X = axis_split(t.x, u[0], g.nx), Y = axis_split(t.y, u[1], g.ny),
+                      Z = axis_split(zo, u[2], g.nz);
+            const float* q = M + X.i0 + g.nx * (Y.i0 + g.ny * Z.i0);
+            const int sx = X.step, dy = Y.step * g.nx, dz = Z.step * t.nxy;
+            c[0] = __ldg(q); c[1] = __ldg(q + sx); c[2] = __ldg(q + dy); c[3] = __ldg(q + dy + sx);
+            c[4] = __ldg(q + dz); c[5] = __ldg(q + dz + sx); c[6] = __ldg(q + dz + dy);
+            c[7] = __ldg(q + dz + dy + sx);
         }
     };
 
-    double ring[W][3], S[3];
+    double ring[W][3];
 #pragma unroll
     for (int d = 0; d < W; ++d)
 #pragma unroll
         for (int c = 0; c < 3; ++c) ring[d][c] = 0.0;
-#pragma unroll
-    for (int c = 0; c < 3; ++c) S[c] = 0.0;
 
     const int z0 = t.zb - R, z1 = t.ze + R;
     load_halo(z0);
     store_halo(0);
     load_halo(z0 + 1);
-    // outputs start at zo = zb (reached at zi = zb + R)
-    load_own(t.zb, ou1, of1);
-    gather_own(t.zb, ou1, of1);
-    ocell_cur = ocell_next;
-#pragma unroll
-    for (int k = 0; k < 8; ++k) oc_cur[k] = oc_next[k];
-    of_cur = of_next;
+    load_own(t.zb, ou0, of0);
+    gather_own(t.zb, ou0, oc0);
     load_own(t.zb + 1, ou1, of1);
     __syncthreads();
 
@@ -561,7 +565,7 @@ __global__ void __launch_bounds__(NT, 2) k_lncc_bwd(Batch b, LmParams p, int chu
                 const bool emit = zo >= t.zb;
                 if (emit) {
                     load_own(zo + 2, ou2, of2);
-                    gather_own(zo + 1, ou1, of1);
+                    gather_own(zo + 1, ou1, oc1);
                 }
 #pragma unroll
                 for (int q = 0; q < XS; ++q) {
@@ -584,27 +588,46 @@ __global__ void __launch_bounds__(NT, 2) k_lncc_bwd(Batch b, LmParams p, int chu
                     double s = 0.0;
 #pragma unroll
                     for (int d = 0; d < W; ++d) s += s_x[c][t.oy + d][t.ox];
-                    S[c] += s - ring[ph][c];
                     ring[ph][c] = s;
                 }
                 if (emit && t.own) {
-                    double gm[3];
-                    const double mw = ocell_cur.finite ? lerp_cell<true>(ocell_cur, oc_cur, gm) : kNaN64;
-                    if (!ocell_cur.finite) gm[0] = gm[1] = gm[2] = 0.0;
-                    const double f = (double)of_cur - shf;
+                    double S[3];
+#pragma unroll
+                    for (int c = 0; c < 3; ++c) {
+                        double s = 0.0;
+#pragma unroll
+                        for (int d = 0; d < W; ++d) s += ring[(ph + 1 + d) % W][c];
+                        S[c] = s;
+                    }
+                    double gm[3] = {0.0, 0.0, 0.0};
+                    double mw = kNaN64;
+                    if (isfinite(ou0[0]) && isfinite(ou0[1]) && isfinite(ou0[2])) {
+                        const Tap X = axis_split(t.x, ou0[0], g.nx), Y = axis_split(t.y, ou0[1], g.ny),
+                                  Z = axis_split(zo, ou0[2], g.nz);
+                        const double a = oc0[0], bb = oc0[1], c = oc0[2], e = oc0[3];
+                        const double f = oc0[4], h = oc0[5], k = oc0[6], l = oc0[7];
+                        const double d00 = bb - a, d10 = e - c, d01 = h - f, d11 = l - k;
+                        const double v00 = fma(X.t, d00, a), v10 = fma(X.t, d10, c);
+                        const double v01 = fma(X.t, d01, f), v11 = fma(X.t, d11, k);
+                        const double s0 = fma(Y.t, v10 - v00, v00), s1 = fma(Y.t, v11 - v01, v01);
+                        const double gx0 = fma(Y.t, d10 - d00, d00), gx1 = fma(Y.t, d11 - d01, d01);
+                        gm[0] = X.outside ? 0.0 : fma(Z.t, gx1 - gx0, gx0);
+                        gm[1] = Y.outside ? 0.0 : fma(Z.t, (v11 - v01) - (v10 - v00), v10 - v00);
+                        gm[2] = Z.outside ? 0.0 : s1 - s0;
+                        mw = fma(Z.t, s1 - s0, s0);
+                    }
+                    const double f = (double)of0 - shf;
                     const double dm = -invN * (fma(f, S[0], (mw - shm) * S[1]) - S[2]);
-                    const int o = zo * t.nxy + ooff;
+                    const int o = t.lp(g, zo) + ooff;
                     G[o] = (float)(dm * gm[0]);
                     G[n + o] = (float)(dm * gm[1]);
                     G[2 * n + o] = (float)(dm * gm[2]);
                 }
                 if (emit) {
-                    ocell_cur = ocell_next;
 #pragma unroll
-                    for (int k = 0; k < 8; ++k) oc_cur[k] = oc_next[k];
-                    of_cur = of_next;
-                    ou1[0] = ou2[0]; ou1[1] = ou2[1]; ou1[2] = ou2[2];
-                    of1 = of2;
+                    for (int k = 0; k < 8; ++k) oc0[k] = oc1[k];
+                    ou0[0] = ou1[0]; ou0[1] = ou1[1]; ou0[2] = ou1[2]; of0 = of1;
+                    ou1[0] = ou2[0]; ou1[1] = ou2[1]; ou1[2] = ou2[2]; of1 = of2;
                 }
                 store_halo(sb ^ 1);
                 load_halo(zi + 2);
@@ -615,11 +638,9 @@ __global__ void __launch_bounds__(NT, 2) k_lncc_bwd(Batch b, LmParams p, int chu
 }
 
 // ---------------------------------------------------------------------------
-// Gaussian 3-channel z-march in fp64 with a statically indexed ring.  The
-// producer fills s_in[3][NI] (fp64) for input plane zi; `emit` gets the
-// smoothed value at (x, y, zo).  Weights w[|d|] are truncated at R and
-// renormalised per axis over in-bounds taps (field.cpp:236-244): zero-filled
-// halos and a final divide by Wx(x) Wy(y) Wz(z).
+// Gaussian weights w[|d|] are truncated at R and renormalised per axis over
+// in-bounds taps (field.cpp:236-244): zero-filled halos and a final divide by
+// Wx(x) Wy(y) Wz(z).
 template <class T>
 __device__ __forceinline__ T axis_wsum_t(int p, int n, int R, const T* w, T full) {
     if (p >= R && p + R <= n - 1) return full;
@@ -668,11 +689,10 @@ __global__ void __launch_bounds__(NT, 2) k_step_smooth(Batch b, LmParams p, int 
     float hg[SL][3];
     auto load_halo = [&](int z) {
         const bool zin = z >= 0 && z < g.nz;
-        const int po = z * t.nxy;
 #pragma unroll
         for (int s = 0; s < SL; ++s) {
             if (zin && it.goff[s] >= 0) {
-                const int o = po + it.goff[s];
+                const int o = t.lp(g, z) + it.goff[s];
                 hg[s][0] = __ldg(Gin + o); hg[s][1] = __ldg(Gin + n + o); hg[s][2] = __ldg(Gin + 2 * n + o);
             } else {
                 hg[s][0] = hg[s][1] = hg[s][2] = 0.f;
@@ -737,8 +757,10 @@ __global__ void __launch_bounds__(NT, 2) k_step_smooth(Batch b, LmParams p, int 
                 }
                 const int zo = zi - R;
                 if (zo >= t.zb && t.own) {
-                    const double inv = (zo >= R && zo + R <= g.nz - 1) ? inv_full : inv_xy / axis_wsum_t<double>(zo, g.nz, R, p.wud, p.wud_full);
-                    const int o = zo * t.nxy + ooff;
+                    const double inv = (zo >= R && zo + R <= g.nz - 1)
+                                           ? inv_full
+                                           : inv_xy / axis_wsum_t<double>(zo, g.nz, R, p.wud, p.wud_full);
+                    const int o = t.lp(g, zo) + ooff;
 #pragma unroll
                     for (int c = 0; c < 3; ++c) {
                         double s = 0.0;
@@ -776,9 +798,9 @@ __global__ void __launch_bounds__(NT, 2) k_compose_smooth(Batch b, LmParams p, i
     using It = hot::Items<R>;          // producer tile (halo R)
     using Iu = hot::Items<R + 1>;      // warp tile (halo R + 1)
     constexpr int IW = It::IW, IH = It::IH, NI = It::NI, SL = It::SLOTS, W = 2 * R + 1;
-    constexpr int UW = Iu::IW, UN = Iu::NI, USL = Iu::SLOTS;
+    constexpr int UW = Iu::IW, UNI = Iu::NI, USL = Iu::SLOTS;
     constexpr int XS = (IH * TX + NT - 1) / NT;
-    __shared__ float s_u[3][3][UN];     // [ring slot][channel][tile]
+    __shared__ float s_u[3][3][UNI];    // [ring slot][channel][tile]
     __shared__ double s_in[3][NI];
     __shared__ double s_x[3][IH][TX];
 
@@ -807,17 +829,16 @@ __global__ void __launch_bounds__(NT, 2) k_compose_smooth(Batch b, LmParams p, i
                              : 1.0;
     const double inv_xy = 1.0 / wxy, inv_full = inv_xy / p.wwd_full;
 
-    float pu[USL][3];  // warp rows of plane z + 2
+    float pu[USL][3];  // warp rows of plane z + 3 (loads in flight)
     // step rows: the thread that loads item s also produces it, so the step
     // tile never goes through shared memory (plane z, z + 1, z + 2)
     float v0[SL][3], v1[SL][3], v2[SL][3];
     auto load_u = [&](int z) {
         const bool zin = z >= 0 && z < g.nz;
-        const int po = z * t.nxy;
 #pragma unroll
         for (int s = 0; s < USL; ++s) {
             if (zin && iu.goff[s] >= 0) {
-                const int o = po + iu.goff[s];
+                const int o = t.lp(g, z) + iu.goff[s];
                 pu[s][0] = __ldg(U + o); pu[s][1] = __ldg(U + n + o); pu[s][2] = __ldg(U + 2 * n + o);
             } else {
                 pu[s][0] = pu[s][1] = pu[s][2] = 0.f;
@@ -836,11 +857,10 @@ __global__ void __launch_bounds__(NT, 2) k_compose_smooth(Batch b, LmParams p, i
     };
     auto load_v = [&](int z, float (&pv)[SL][3]) {
         const bool zin = z >= 0 && z < g.nz;
-        const int po = z * t.nxy;
 #pragma unroll
         for (int s = 0; s < SL; ++s) {
             if (zin && it.goff[s] >= 0) {
-                const int o = po + it.goff[s];
+                const int o = t.lp(g, z) + it.goff[s];
                 pv[s][0] = __ldg(Vin + o); pv[s][1] = __ldg(Vin + n + o); pv[s][2] = __ldg(Vin + 2 * n + o);
             } else {
                 pv[s][0] = pv[s][1] = pv[s][2] = 0.f;
@@ -897,7 +917,7 @@ __global__ void __launch_bounds__(NT, 2) k_compose_smooth(Batch b, LmParams p, i
 
     const int z0 = t.zb - R, z1 = t.ze + R;
     // prologue: warp planes z0-1 .. z0+1 staged, z0+2 in registers; steps of
-    // z0 staged, z0+1 in registers
+    // z0 and z0+1 in registers
     load_u(z0 - 1); store_u(z0 - 1);
     load_u(z0);     store_u(z0);
     load_u(z0 + 1); store_u(z0 + 1);
@@ -949,8 +969,10 @@ __global__ void __launch_bounds__(NT, 2) k_compose_smooth(Batch b, LmParams p, i
                 }
                 const int zo = zi - R;
                 if (zo >= t.zb && t.own) {
-                    const double inv = (zo >= R && zo + R <= g.nz - 1) ? inv_full : inv_xy / axis_wsum_t<double>(zo, g.nz, R, p.wwd, p.wwd_full);
-                    const int o = zo * t.nxy + ooff;
+                    const double inv = (zo >= R && zo + R <= g.nz - 1)
+                                           ? inv_full
+                                           : inv_xy / axis_wsum_t<double>(zo, g.nz, R, p.wwd, p.wwd_full);
+                    const int o = t.lp(g, zo) + ooff;
 #pragma unroll
                     for (int c = 0; c < 3; ++c) {
                         double s = 0.0;
@@ -974,14 +996,24 @@ __global__ void __launch_bounds__(NT, 2) k_compose_smooth(Batch b, LmParams p, i
         default: break;                                \
     }
 
+int plane_tiles(const Geo& g) { return cdiv(g.nx, TX) * cdiv(g.ny, TY); }
+
 void launch_lncc_fwd(const Batch& b, const LmParams& p, int mode, cudaStream_t s) {
-    const dim3 wgrid(cdiv(b.g.nx, 32) * cdiv(b.g.ny, 8), b.g.nz, b.pairs);
-    k_warp_moving<<<wgrid, 256, 0, s>>>(b, mode);
+    (void)p;
+    // Mw for the owned planes plus the window pass's 2-plane halo
+    const int zf = std::max(0, b.g.zs - 2), zl = std::min(b.g.nz, b.g.ze + 2);
+    const dim3 wgrid(cdiv(b.g.nx, 32) * cdiv(b.g.ny, 8), zl - zf, b.pairs);
+    k_warp_moving<<<wgrid, 256, 0, s>>>(b, mode, zf);
     const LaunchShape sh = shape_for(b.g, b.pairs, TY);
     dim3 grid = sh.grid();
     grid.z = b.pairs;
-    k_lncc_fwd<2><<<grid, NT, 0, s>>>(b, p, mode, sh.chunk_len);
+    k_lncc_fwd<2><<<grid, NT, 0, s>>>(b, sh.chunk_len);
     g_kernel_launches += 2;
+}
+
+void launch_finalize(const Batch& b, const LmParams& p, int mode, cudaStream_t s) {
+    k_finalize<<<b.pairs, 256, 0, s>>>(b, p, mode);
+    ++g_kernel_launches;
 }
 
 void launch_lncc_bwd(const Batch& b, const LmParams& p, cudaStream_t s) {

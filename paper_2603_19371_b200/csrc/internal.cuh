@@ -151,12 +151,14 @@ struct wlm_engine {
     DevBuf<float> F, M, U, ABE, G, VS, AM, AV;
     DevBuf<double> MW;
     DevBuf<PairState> st;
-    DevBuf<double> partials, script, shift_part;
+    DevBuf<double> partials, script, shift_part, plane_sum;
     DevBuf<wlm_step_log> trace;
     Batch B{};
     cudaGraphExec_t step_exec = nullptr, loop_exec = nullptr;
     cudaGraph_t step_graph = nullptr, loop_graph = nullptr;
     int body_kernels = 0;
+    bool shared_fm = false;         // F, M owned by a slab group (Batch set by the group)
+    bool shared_plane_sum = false;  // per-plane sum(rho) owned by a slab group
 
     ~wlm_engine() {
         if (step_exec) cudaGraphExecDestroy(step_exec);
@@ -165,13 +167,25 @@ struct wlm_engine {
         if (loop_graph) cudaGraphDestroy(loop_graph);
     }
 
-    void body(cudaStream_t s) {
+    // Stages of one attempt (a slab group interleaves them with exchanges).
+    void stage_grad(cudaStream_t s) {
         launch_lncc_bwd(B, P, s);
         if (P.optimizer == WLM_OPT_ADAM) launch_adam(B, P, s);
-        launch_step_smooth(B, P, s);
+    }
+    void stage_step(cudaStream_t s) { launch_step_smooth(B, P, s); }
+    void stage_compose(cudaStream_t s) {
         launch_compose_smooth(B, P, s);
         if (P.log_jacobian) launch_jacobian_diag(B, P, s);
-        launch_lncc_fwd(B, P, 1, s);
+    }
+    void stage_eval(int mode, cudaStream_t s) { launch_lncc_fwd(B, P, mode, s); }
+    void stage_finalize(int mode, cudaStream_t s) { launch_finalize(B, P, mode, s); }
+
+    void body(cudaStream_t s) {
+        stage_grad(s);
+        stage_step(s);
+        stage_compose(s);
+        stage_eval(1, s);
+        stage_finalize(1, s);
     }
 
     void invalidate_graphs() {

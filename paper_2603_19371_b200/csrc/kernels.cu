@@ -38,13 +38,15 @@ LaunchShape shape_for(const Geo& g, int pairs, int ty) {
     s.tiles_x = cdiv(g.nx, TX);
     s.tiles_y = cdiv(g.ny, ty);
     const long long tiles = (long long)s.tiles_x * s.tiles_y * pairs;
-    // aim for >= 8 resident CTAs per SM worth of work; keep >= 8 planes a chunk
+    // chunks of the owned planes: aim for >= 8 resident CTAs per SM worth of
+    // work; keep >= 8 planes a chunk
+    const int nzo = g.ze - g.zs;
     const long long want = (long long)kNumSMs * 8;
-    int chunks = (int)std::max<long long>(1, std::min<long long>(g.nz, (want + tiles - 1) / tiles));
-    int len = cdiv(g.nz, chunks);
-    len = std::max(len, std::min(g.nz, 8));
+    int chunks = (int)std::max<long long>(1, std::min<long long>(nzo, (want + tiles - 1) / tiles));
+    int len = cdiv(nzo, chunks);
+    len = std::max(len, std::min(nzo, 8));
     s.chunk_len = len;
-    s.chunks = cdiv(g.nz, len);
+    s.chunks = cdiv(nzo, len);
     return s;
 }
 
@@ -66,7 +68,7 @@ __global__ void k_adam(Batch b, LmParams p) {
     const int pair = blockIdx.y;
     const PairState* st = b.st + pair;
     if (st->done) return;
-    const long long n3 = 3 * b.g.n;
+    const long long n = b.g.n, n3 = 3 * n;
     float* G = b.G + (long long)pair * n3;
     float* Mm = b.AM + (long long)pair * n3;
     float* Vv = b.AV + (long long)pair * n3;
@@ -74,8 +76,12 @@ __global__ void k_adam(Batch b, LmParams p) {
     const float b1 = (float)p.adam_b1, b2 = (float)p.adam_b2;
     const float bc1 = (float)(1.0 - pow(p.adam_b1, t)), bc2 = (float)(1.0 - pow(p.adam_b2, t));
     const float lr = (float)p.adam_lr, ep = (float)p.adam_eps;
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n3;
-         i += (long long)gridDim.x * blockDim.x) {
+    // owned planes of each component (slab halos are refreshed by exchange)
+    const long long nxy = (long long)b.g.nx * b.g.ny;
+    const long long lo = (b.g.zs - b.g.zlo) * nxy, cnt = (b.g.ze - b.g.zs) * nxy;
+    for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < 3 * cnt;
+         j += (long long)gridDim.x * blockDim.x) {
+        const long long i = (j / cnt) * n + lo + j % cnt;
         const float gi = G[i];
         const float m = fmaf(b1, Mm[i], (1.f - b1) * gi);
         const float v = fmaf(b2, Vv[i], (1.f - b2) * gi * gi);
@@ -98,7 +104,7 @@ __device__ float det_at(const float* U, const Geo& g, int x, int y, int z, float
         if (p[a] >= 1 && p[a] + 1 <= nn[a] - 1) { q1[a] = p[a] + 1; q0[a] = p[a] - 1; }
         else if (p[a] == 0) { q1[a] = 1; q0[a] = 0; k = 1.f; }
         else { q1[a] = p[a]; q0[a] = p[a] - 1; k = 1.f; }
-        const int i1 = g.at(q1[0], q1[1], q1[2]), i0 = g.at(q0[0], q0[1], q0[2]);
+        const int i1 = g.lat(q1[0], q1[1], q1[2]), i0 = g.lat(q0[0], q0[1], q0[2]);
 #pragma unroll
         for (int c = 0; c < 3; ++c) J[c][a] = k * scale * (__ldg(U + c * g.n + i1) - __ldg(U + c * g.n + i0));
     }
@@ -123,7 +129,9 @@ __global__ void k_jacobian_diag(Batch b, LmParams p) {
     const double eps = p.target / fmax((double)__uint_as_float(st->max_bits), p.step_floor);
     int xl, xh, yl, yh, zl, zh;
     interior(g.nx, xl, xh); interior(g.ny, yl, yh); interior(g.nz, zl, zh);
-    const long long cx = xh - xl + 1, cy = yh - yl + 1, cz = zh - zl + 1;
+    zl = max(zl, g.zs);       // owned planes only (slabs)
+    zh = min(zh, g.ze - 1);
+    const long long cx = xh - xl + 1, cy = yh - yl + 1, cz = max(zh - zl + 1, 0);
     const long long tot = cx * cy * cz;
     float mn = FLT_MAX;
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < tot;
@@ -173,7 +181,7 @@ constexpr int kShiftBlocks = 256;
 __global__ void k_shift_partials(Batch b, double* part) {
     __shared__ double red[32];
     const int pair = blockIdx.y, which = blockIdx.z;
-    const long long n = b.g.n;
+    const long long n = b.g.nfull;  // F, M are whole-volume (replicated across slabs)
     const float* v = (which == 0 ? b.F : b.M) + (long long)pair * n;
     const long long per = (n + kShiftBlocks - 1) / kShiftBlocks;
     const long long lo = blockIdx.x * per, hi = min(n, lo + per);
@@ -189,7 +197,7 @@ __global__ void k_shift_final(Batch b, const double* part) {
     const double v = threadIdx.x < kShiftBlocks ? part[((long long)pair * 2 + which) * kShiftBlocks + threadIdx.x] : 0.0;
     const double t = block_sum(v, red);
     if (threadIdx.x == 0) {
-        const float mean = (float)(t / (double)b.g.n);
+        const float mean = (float)(t / (double)b.g.nfull);
         if (which == 0) b.st[pair].shift_f = mean;
         else b.st[pair].shift_m = mean;
     }

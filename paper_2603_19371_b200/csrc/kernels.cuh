@@ -66,7 +66,9 @@ struct Batch {
     float* AV;        // [pair][3][n]  Adam second moment (or null)
     PairState* st;    // [pair]
     double* shift_part; // [pair][2][256] scratch for the intensity shifts
-    double* partials; // [pair][max_blocks]
+    double* partials; // [pair][nz][tiles][8] per-(plane, tile, warp) sum(rho)
+    double* plane_sum;  // [pair][nz] per-plane sum(rho) (global z; shared by slabs)
+    int zero_foreign_planes;  // NCCL slabs: zero non-owned planes before the all-reduce
     int max_blocks;
 };
 
@@ -80,6 +82,11 @@ LaunchShape shape_for(const Geo& g, int pairs, int ty);
 // the loss/damping/rejection state machine.  mode 0 evaluates the accepted
 // warp (level start), mode 1 the attempt in the other buffer.
 void launch_lncc_fwd(const Batch& b, const LmParams& p, int mode, cudaStream_t s);
+// K5: r = 1 - mean(rho) from the per-plane sums (z order), then the state
+// machine.  Runs after the plane sums of every slab are in place.
+void launch_finalize(const Batch& b, const LmParams& p, int mode, cudaStream_t s);
+// 32 x 8 tiles per plane (size of the per-plane partial arrays).
+int plane_tiles(const Geo& g);
 // K2: adjoint window sums -> dr/dMw -> g = dr/dMw * gradM(x + u).
 void launch_lncc_bwd(const Batch& b, const LmParams& p, cudaStream_t s);
 // Adam moment update (pointwise), writes the Adam step into G.

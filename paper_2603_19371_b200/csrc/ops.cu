@@ -204,7 +204,8 @@ wlm_status wlm_residual_lncc(wlm_ctx* ctx, const double* F, const double* M, con
         DevBuf<float> du = upload_soa(ctx, u, n, 3);
         copy_warps_in(e, du.p, 0);
         launch_begin_level(e->B, e->P, 0, 1, cfg.lm.lambda0, ctx->stream);
-        launch_lncc_fwd(e->B, e->P, 0, ctx->stream);
+        e->stage_eval(0, ctx->stream);
+        e->stage_finalize(0, ctx->stream);
         if (g) {
             launch_lncc_bwd(e->B, e->P, ctx->stream);
             download_aos(ctx, e->G.p, n, 3, g);
@@ -343,7 +344,8 @@ wlm_status wlm_register(wlm_ctx* ctx, const float* F, const float* M, wlm_dims d
             } else {
                 launch_begin_level(e->B, e->P, l, 1, cfg->lm.lambda0, ctx->stream);
             }
-            launch_lncc_fwd(e->B, e->P, 0, ctx->stream);
+            e->stage_eval(0, ctx->stream);
+            e->stage_finalize(0, ctx->stream);
             const uint64_t before = g_kernel_launches;
             es = wlm_engine_iterate(e, cfg->iters[l]);
             (void)before;
