@@ -213,6 +213,28 @@ wlm_status wlm_engine_script_losses(wlm_engine* e, const double* losses, int n);
  * 3 = K4 compose + smoothing, 4 = K1 evaluation of the accepted warp. */
 wlm_status wlm_engine_stage(wlm_engine* e, int stage);
 
+/* ---- z-slab group: one registration split along z ----
+ * nslabs slabs of >= 4 planes each; each slab computes its owned planes and
+ * exchanges halo planes after every producer stage; sum(rho) is reduced per
+ * plane in z order, so losses, decisions and warps are bit-identical for
+ * every nslabs (and to wlm_engine with pairs = 1).  Warps are whole-volume
+ * fp32 SoA [3][nz][ny][nx].  This in-process form runs every slab on the
+ * context's device; DESIGN.md §6 maps the same exchange schedule to one
+ * process per GPU.                                                          */
+typedef struct wlm_slab_group wlm_slab_group;
+wlm_status wlm_slab_group_create(wlm_ctx* ctx, wlm_dims d, int nslabs,
+                                 const wlm_reg_config* cfg, wlm_slab_group** out);
+void wlm_slab_group_destroy(wlm_slab_group* g);
+wlm_status wlm_slab_group_load(wlm_slab_group* g, const float* F, const float* M, int is_host);
+wlm_status wlm_slab_group_set_warp(wlm_slab_group* g, const float* u, int is_host);
+wlm_status wlm_slab_group_get_warp(wlm_slab_group* g, float* u, int is_host);
+wlm_status wlm_slab_group_begin_level(wlm_slab_group* g, int level);
+wlm_status wlm_slab_group_iterate(wlm_slab_group* g, int iters);
+/* Trace of the registration; fails if the slabs' state machines disagree. */
+wlm_status wlm_slab_group_trace(wlm_slab_group* g, wlm_step_log* rows, size_t cap, size_t* len);
+wlm_status wlm_slab_group_state(wlm_slab_group* g, wlm_lm_state* st, double* r, double* lncc,
+                                int* iters_done);
+
 /* ---- harness: synthetic pair on the GPU ----
  * u_true is SoA fp32 [3][nz][ny][nx] (nullable); on_device selects whether
  * F, M, u_true are device (1) or host (0) pointers. */

@@ -111,6 +111,15 @@ SIGNATURES = {
     "wlm_engine_script_losses": (C.c_int, [_ENG, _D, C.c_int]),
     "wlm_engine_stage": (C.c_int, [_ENG, C.c_int]),
     "wlm_engine_read_buffer": (C.c_int, [_ENG, C.c_int, C.c_int, _VP, C.c_size_t]),
+    "wlm_slab_group_create": (C.c_int, [_CTX, Dims, C.c_int, C.POINTER(RegConfig), C.POINTER(_ENG)]),
+    "wlm_slab_group_destroy": (None, [_ENG]),
+    "wlm_slab_group_load": (C.c_int, [_ENG, _VP, _VP, C.c_int]),
+    "wlm_slab_group_set_warp": (C.c_int, [_ENG, _VP, C.c_int]),
+    "wlm_slab_group_get_warp": (C.c_int, [_ENG, _VP, C.c_int]),
+    "wlm_slab_group_begin_level": (C.c_int, [_ENG, C.c_int]),
+    "wlm_slab_group_iterate": (C.c_int, [_ENG, C.c_int]),
+    "wlm_slab_group_trace": (C.c_int, [_ENG, C.POINTER(StepLog), C.c_size_t, C.POINTER(C.c_size_t)]),
+    "wlm_slab_group_state": (C.c_int, [_ENG, C.POINTER(LmState), _D, _D, C.POINTER(C.c_int)]),
     "wlm_synth_pair": (C.c_int, [_CTX, C.POINTER(SynthSpec), _VP, _VP, _VP, C.c_int]),
 }
 

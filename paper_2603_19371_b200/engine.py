@@ -137,3 +137,75 @@ class Engine:
             self.close()
         except Exception:
             pass
+
+
+class SlabGroup:
+    """One registration split into ``nslabs`` z-slabs (wlm_slab_group_* in
+    include/wlm.h, config 5).  Same calls as :class:`Engine` with pairs = 1;
+    results are bit-identical for every ``nslabs``."""
+
+    def __init__(self, shape, nslabs, cfg: RegConfig | None = None, ctx: Context | None = None):
+        self.ctx = ctx or default_context()
+        self.lib = load()
+        self.shape = tuple(int(s) for s in shape)
+        self.nslabs = int(nslabs)
+        self.cfg = cfg or reg_config()
+        nz, ny, nx = self.shape
+        h = C.c_void_p()
+        self.ctx.check(self.lib.wlm_slab_group_create(self.ctx.h, Dims(nx, ny, nz), self.nslabs,
+                                                      C.byref(self.cfg), C.byref(h)))
+        self.h = h
+        _LIVE_ENGINES.add(self)
+
+    def _chk(self, st):
+        self.ctx.check(st)
+
+    def load(self, F, M):
+        F = np.ascontiguousarray(F, dtype=np.float32)
+        M = np.ascontiguousarray(M, dtype=np.float32)
+        self._chk(self.lib.wlm_slab_group_load(self.h, F.ctypes.data, M.ctypes.data, 1))
+        self.ctx.synchronize()
+
+    def set_warp(self, u=None):
+        if u is None:
+            self._chk(self.lib.wlm_slab_group_set_warp(self.h, None, 1))
+            return
+        u = np.ascontiguousarray(u, dtype=np.float32)
+        self._chk(self.lib.wlm_slab_group_set_warp(self.h, u.ctypes.data, 1))
+
+    def get_warp(self):
+        out = np.empty((3,) + self.shape, np.float32)
+        self._chk(self.lib.wlm_slab_group_get_warp(self.h, out.ctypes.data, 1))
+        return out
+
+    def begin_level(self, level=0):
+        self._chk(self.lib.wlm_slab_group_begin_level(self.h, int(level)))
+
+    def iterate(self, iters):
+        self._chk(self.lib.wlm_slab_group_iterate(self.h, int(iters)))
+
+    def state(self):
+        st = LmState()
+        r, ln = C.c_double(), C.c_double()
+        it = C.c_int()
+        self._chk(self.lib.wlm_slab_group_state(self.h, C.byref(st), C.byref(r), C.byref(ln),
+                                                C.byref(it)))
+        return dict(lam=st.lam, hist_n=st.hist_n, L1=st.L1, L2=st.L2, r=r.value, lncc=ln.value,
+                    iters=it.value)
+
+    def trace(self, cap=100000):
+        rows = (StepLog * cap)()
+        n = C.c_size_t()
+        self._chk(self.lib.wlm_slab_group_trace(self.h, rows, cap, C.byref(n)))
+        return trace_rows(rows[i] for i in range(n.value))
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.wlm_slab_group_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -345,3 +345,36 @@ def test_cpp_adapter_runs_on_gpu(tmp_path):
     exe = build_adapter_demo(tmp_path)
     out = subprocess.run([str(exe)], capture_output=True, text=True)
     assert out.returncode == 0, out.stdout + out.stderr
+
+
+# ------------------------------------------------------- z-slab groups ----
+def run_slabs(P, ctx, F, M, cfg, iters, nslabs):
+    grp = P.SlabGroup(F.shape, nslabs, cfg=cfg, ctx=ctx)
+    grp.load(F, M)
+    grp.set_warp(None)
+    grp.begin_level(0)
+    grp.iterate(iters)
+    out = grp.get_warp(), grp.trace(), grp.state()
+    grp.close()
+    return out
+
+
+@pytest.mark.parametrize("extra", [{}, {"lm.rejection": 1, "lm.tau": 0.2, "log_jacobian": 1},
+                                   {"optimizer": 1}])
+def test_slab_group_is_bit_identical_to_single_domain(P, ctx, extra):
+    """Config 5 decomposition: 1, 2, 3 and 5 z-slabs (uneven splits) give the
+    single-domain engine's losses, decisions, lambda and warp bit for bit."""
+    F, M, _ = O.synth_pair((20, 24, 28), 21, num_blobs=8, warp_max=2.5)
+    cfg = P.reg_config(nlevels=1, factors=[1], iters=[12], **extra)
+    w1, (t1,), (s1,) = run_engine(P, ctx, F, M, cfg, 12)
+    for ns in (1, 2, 3, 5):
+        w, t, s = run_slabs(P, ctx, F, M, cfg, 12, ns)
+        assert same_trace(t, t1), ns
+        assert np.array_equal(w, w1[0]), (ns, float(np.abs(w - w1[0]).max()))
+        assert s["lam"] == s1["lam"] and s["r"] == s1["r"]
+
+
+def test_slab_group_rejects_thin_slabs(P, ctx):
+    cfg = P.reg_config(nlevels=1, factors=[1], iters=[1])
+    with pytest.raises(P.InvalidArgument):
+        P.SlabGroup((12, 16, 16), 4, cfg=cfg, ctx=ctx)
