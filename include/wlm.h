@@ -218,12 +218,34 @@ wlm_status wlm_engine_stage(wlm_engine* e, int stage);
  * exchanges halo planes after every producer stage; sum(rho) is reduced per
  * plane in z order, so losses, decisions and warps are bit-identical for
  * every nslabs (and to wlm_engine with pairs = 1).  Warps are whole-volume
- * fp32 SoA [3][nz][ny][nx].  This in-process form runs every slab on the
- * context's device; DESIGN.md §6 maps the same exchange schedule to one
- * process per GPU.                                                          */
+ * fp32 SoA [3][nz][ny][nx].  wlm_slab_group_create runs every slab on the
+ * context's device; wlm_slab_group_create_nccl holds slab `rank` of
+ * `nranks` in this process (one process per GPU) and exchanges halos with
+ * NCCL send/recv and reduces with NCCL all-reduce (replaces the proposed
+ * wlm_ctx_attach_comm).  Both execute the same halo plan.     */
 typedef struct wlm_slab_group wlm_slab_group;
+/* One halo transfer of slab `slab`: buffer 0 = g, 1 = dU_s, 2 = warp,
+ * 3 = LNCC coefficients A/B/E; planes [z0, z1) received from (send == 0) or
+ * sent to (send == 1) slab `peer`. */
+typedef struct {
+    int buffer, peer, send, z0, z1;
+} wlm_halo_xfer;
+/* Owned planes [zs, ze) of slab `slab` (host only; INVALID_ARG if a slab
+ * would be thinner than the 4-plane halo). */
+wlm_status wlm_slab_partition(int nz, int nslabs, int slab, int* zs, int* ze);
+/* The exchange plan of one slab (host only; rows may be NULL to query len). */
+wlm_status wlm_slab_halo_plan(wlm_dims d, int nslabs, int slab, const wlm_reg_config* cfg,
+                              wlm_halo_xfer* rows, size_t cap, size_t* len);
 wlm_status wlm_slab_group_create(wlm_ctx* ctx, wlm_dims d, int nslabs,
                                  const wlm_reg_config* cfg, wlm_slab_group** out);
+/* NCCL unique id (rank 0 creates, the caller broadcasts the 128 bytes).
+ * nccl_lib: path of libnccl.so.2 to dlopen (NULL -> the loaded one). */
+wlm_status wlm_nccl_unique_id(const char* nccl_lib, unsigned char id[128]);
+wlm_status wlm_slab_group_create_nccl(wlm_ctx* ctx, wlm_dims d, int rank, int nranks,
+                                      const unsigned char id[128], const char* nccl_lib,
+                                      const wlm_reg_config* cfg, wlm_slab_group** out);
+/* Planes [zs, ze) owned by this group's slabs (get_warp fills only these). */
+wlm_status wlm_slab_group_owned(const wlm_slab_group* g, int* zs, int* ze);
 void wlm_slab_group_destroy(wlm_slab_group* g);
 wlm_status wlm_slab_group_load(wlm_slab_group* g, const float* F, const float* M, int is_host);
 wlm_status wlm_slab_group_set_warp(wlm_slab_group* g, const float* u, int is_host);

@@ -52,6 +52,11 @@ class SynthSpec(C.Structure):
                 ("warp_max", C.c_double), ("noise_sigma", C.c_double), ("seed", C.c_uint64)]
 
 
+class HaloXfer(C.Structure):
+    _fields_ = [("buffer", C.c_int), ("peer", C.c_int), ("send", C.c_int), ("z0", C.c_int),
+                ("z1", C.c_int)]
+
+
 class StepLog(C.Structure):
     _fields_ = [("level", C.c_int), ("iter", C.c_int), ("loss_raw", C.c_double),
                 ("r", C.c_double), ("lam", C.c_double), ("eps", C.c_double),
@@ -111,7 +116,15 @@ SIGNATURES = {
     "wlm_engine_script_losses": (C.c_int, [_ENG, _D, C.c_int]),
     "wlm_engine_stage": (C.c_int, [_ENG, C.c_int]),
     "wlm_engine_read_buffer": (C.c_int, [_ENG, C.c_int, C.c_int, _VP, C.c_size_t]),
+    "wlm_slab_partition": (C.c_int, [C.c_int, C.c_int, C.c_int, C.POINTER(C.c_int),
+                                     C.POINTER(C.c_int)]),
+    "wlm_slab_halo_plan": (C.c_int, [Dims, C.c_int, C.c_int, C.POINTER(RegConfig), _VP, C.c_size_t,
+                                     C.POINTER(C.c_size_t)]),
     "wlm_slab_group_create": (C.c_int, [_CTX, Dims, C.c_int, C.POINTER(RegConfig), C.POINTER(_ENG)]),
+    "wlm_nccl_unique_id": (C.c_int, [C.c_char_p, C.c_char_p]),
+    "wlm_slab_group_create_nccl": (C.c_int, [_CTX, Dims, C.c_int, C.c_int, C.c_char_p, C.c_char_p,
+                                             C.POINTER(RegConfig), C.POINTER(_ENG)]),
+    "wlm_slab_group_owned": (C.c_int, [_ENG, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
     "wlm_slab_group_destroy": (None, [_ENG]),
     "wlm_slab_group_load": (C.c_int, [_ENG, _VP, _VP, C.c_int]),
     "wlm_slab_group_set_warp": (C.c_int, [_ENG, _VP, C.c_int]),

@@ -2,22 +2,33 @@
 //
 // A volume is split along z into P slabs of >= kHalo planes.  Each slab is a
 // wlm_engine whose per-voxel buffers hold its owned planes plus kHalo halo
-// planes; F and M are whole-volume and shared.  One LM attempt runs the
+// planes; F and M are whole-volume (the warp gathers M up to max|u| planes
+// away, so M is replicated rather than haloed).  One LM attempt runs the
 // stages of every slab with a halo exchange after each producer stage:
 //
 //   K2 (+Adam) -> exchange g (R_u planes) -> K3 -> max over slabs
-//   -> exchange dU_s (R_w) -> K4 -> exchange u' of the attempt buffer
-//   (R_w + 1, >= 2) -> [Jacobian, min over slabs] -> K1a/K1b (per-plane
-//   sum(rho) into the shared plane array) -> K5 on every slab (identical
-//   state machines) -> exchange A, B, E (2 planes)
+//   -> exchange dU_s (R_w) -> K4 -> exchange u' (R_w + 1, >= 2)
+//   -> [Jacobian, min over slabs] -> K1a/K1b: per-plane sum(rho)
+//   -> sum of plane arrays over slabs -> K5 (identical state machine on every
+//   slab) -> exchange A, B, E (2 planes)
 //
 // Every voxel's arithmetic is the single-domain arithmetic (direct z sums,
 // global faces) and sum(rho) is reduced per plane then over planes in z
-// order, so any P gives bit-identical losses, decisions and warps -- the
-// P-invariance the tests check.  Here the slabs share one device and the
-// exchange is device-to-device copies inside the captured attempt graph; on
-// P GPUs the same schedule maps to NCCL send/recv of the same plane ranges
-// and an all-reduce of the plane sums and of the max.
+// order, so any P gives bit-identical losses, decisions and warps.
+//
+// The exchange schedule is one host-computed plan (slab_plan, exported as
+// wlm_slab_halo_plan) executed by one of two transports:
+//   * local: all slabs on the context's device; the plan's rows become
+//     device-to-device copies captured in the attempt graph, the plane sums
+//     share one array, the max/min is a one-thread combine kernel;
+//   * nccl: one slab per process/GPU; the rows become ncclSend/ncclRecv in
+//     one group per exchange, the plane sums an ncclAllReduce(sum) over
+//     arrays that are zero on foreign planes (x + 0 is exact, so still
+//     bit-identical), the max/min an ncclAllReduce on the ordered bits.
+// libnccl is dlopen'ed (the one torch loaded), so the library has no link
+// dependency on it.
+#include <dlfcn.h>
+
 #include <algorithm>
 #include <cstring>
 #include <vector>
@@ -26,9 +37,110 @@
 
 using namespace wlm;
 
+// ---- minimal NCCL ABI (nccl.h 2.x; resolved at run time) ----
+namespace nccl {
+typedef struct ncclComm* Comm;
+struct UniqueId {
+    char internal[128];
+};
+enum { Int32 = 2, Uint32 = 3, Float32 = 7, Float64 = 8 };
+enum { Sum = 0, Max = 2, Min = 3 };
+typedef int (*GetUniqueId_t)(UniqueId*);
+typedef int (*CommInitRank_t)(Comm*, int, UniqueId, int);
+typedef int (*CommDestroy_t)(Comm);
+typedef int (*Send_t)(const void*, size_t, int, int, Comm, cudaStream_t);
+typedef int (*Recv_t)(void*, size_t, int, int, Comm, cudaStream_t);
+typedef int (*AllReduce_t)(const void*, void*, size_t, int, int, Comm, cudaStream_t);
+typedef int (*Group_t)();
+typedef const char* (*ErrStr_t)(int);
+
+struct Api {
+    void* h = nullptr;
+    GetUniqueId_t get_unique_id = nullptr;
+    CommInitRank_t comm_init_rank = nullptr;
+    CommDestroy_t comm_destroy = nullptr;
+    Send_t send = nullptr;
+    Recv_t recv = nullptr;
+    AllReduce_t all_reduce = nullptr;
+    Group_t group_start = nullptr, group_end = nullptr;
+    ErrStr_t err = nullptr;
+};
+
+Api g_api;
+
+bool load(const char* path, std::string* why) {
+    if (g_api.h) return true;
+    void* h = dlopen(path && *path ? path : "libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) {
+        *why = std::string("dlopen libnccl: ") + dlerror();
+        return false;
+    }
+    Api a;
+    a.h = h;
+#define SYM(field, name)                                              \
+    a.field = reinterpret_cast<decltype(a.field)>(dlsym(h, name));  \
+    if (!a.field) {                                                   \
+        *why = std::string("libnccl lacks ") + name;                  \
+        return false;                                                 \
+    }
+    SYM(get_unique_id, "ncclGetUniqueId");
+    SYM(comm_init_rank, "ncclCommInitRank");
+    SYM(comm_destroy, "ncclCommDestroy");
+    SYM(send, "ncclSend");
+    SYM(recv, "ncclRecv");
+    SYM(all_reduce, "ncclAllReduce");
+    SYM(group_start, "ncclGroupStart");
+    SYM(group_end, "ncclGroupEnd");
+    SYM(err, "ncclGetErrorString");
+#undef SYM
+    g_api = a;
+    return true;
+}
+}  // namespace nccl
+
 namespace {
 
 constexpr int kHalo = 4;  // >= max(R_u, R_w + 1, 2) for sigma <= 1
+
+enum Buffer { BUF_G = 0, BUF_V = 1, BUF_U = 2, BUF_ABE = 3 };
+
+void partition(int nz, int nslabs, int k, int* zs, int* ze) {
+    *zs = (int)((long long)k * nz / nslabs);
+    *ze = (int)((long long)(k + 1) * nz / nslabs);
+}
+
+int halo_depth(int buffer, int Ru, int Rw) {
+    switch (buffer) {
+        case BUF_G: return Ru;
+        case BUF_V: return Rw;
+        case BUF_U: return std::max(Rw + 1, 2);
+        default: return 2;  // A, B, E: the LNCC window radius
+    }
+}
+
+// Rows of slab k's exchanges, in a fixed order: per buffer, the lower
+// neighbour then the upper one, receive before send.  A slab receives its
+// halo planes [z0, z1) from the neighbour owning them and sends the
+// neighbour's halo planes out of its own owned planes; the two rows of one
+// transfer name the same [z0, z1) on both sides.
+std::vector<wlm_halo_xfer> slab_plan(wlm_dims d, int nslabs, int k, int Ru, int Rw) {
+    std::vector<wlm_halo_xfer> rows;
+    int zs, ze;
+    partition(d.nz, nslabs, k, &zs, &ze);
+    for (int b = BUF_G; b <= BUF_ABE; ++b) {
+        const int h = halo_depth(b, Ru, Rw);
+        if (h <= 0) continue;
+        if (k > 0) {
+            rows.push_back({b, k - 1, 0, std::max(0, zs - h), zs});
+            rows.push_back({b, k - 1, 1, zs, std::min(ze, zs + h)});
+        }
+        if (k + 1 < nslabs) {
+            rows.push_back({b, k + 1, 0, ze, std::min(d.nz, ze + h)});
+            rows.push_back({b, k + 1, 1, std::max(zs, ze - h), ze});
+        }
+    }
+    return rows;
+}
 
 __global__ void k_group_combine(PairState** sts, int n, int jac) {
     unsigned mx = 0u;
@@ -45,13 +157,15 @@ __global__ void k_group_combine(PairState** sts, int n, int jac) {
 
 // Copy `count` voxels per channel of the attempt warp buffer (1 - cur) from
 // one slab engine's local planes to another's (same device).
-__global__ void k_copy_attempt_warp(float* dst, long long dn, int doff, const float* src, long long sn,
-                                    int soff, int count, const PairState* st) {
+__global__ void k_copy_attempt_warp(float* dst, long long dn, long long doff, const float* src, long long sn,
+                                    long long soff, long long count, const PairState* st) {
     const int buf = 1 - st->cur;
     for (int c = 0; c < 3; ++c) {
         float* d = dst + (long long)(buf * 3 + c) * dn + doff;
         const float* s = src + (long long)(buf * 3 + c) * sn + soff;
-        for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < count; i += gridDim.x * blockDim.x) d[i] = s[i];
+        for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < count;
+             i += (long long)gridDim.x * blockDim.x)
+            d[i] = s[i];
     }
 }
 
@@ -67,12 +181,15 @@ struct wlm_slab_group {
     wlm_ctx* ctx = nullptr;
     wlm_dims dims{};
     Geo gfull{};
-    int nslabs = 0;
+    int nslabs = 0;  // slabs of the whole decomposition
+    int first = 0;   // global index of eng[0] (nccl: this process's rank)
     wlm_reg_config cfg{};
     std::vector<wlm_engine*> eng;
-    DevBuf<float> F, M;
-    DevBuf<double> plane_sum;
+    std::vector<std::vector<wlm_halo_xfer>> plan;  // per local engine
+    DevBuf<float> F, M;        // local transport: whole volume, shared
+    DevBuf<double> plane_sum;  // local transport: shared per-plane sums
     DevBuf<PairState*> sts;
+    nccl::Comm comm = nullptr;  // nccl transport
     cudaGraphExec_t step_exec = nullptr, loop_exec = nullptr;
     cudaGraph_t step_graph = nullptr, loop_graph = nullptr;
     int body_kernels = 0;
@@ -83,82 +200,130 @@ struct wlm_slab_group {
         if (step_graph) cudaGraphDestroy(step_graph);
         if (loop_graph) cudaGraphDestroy(loop_graph);
         for (auto* e : eng) delete e;
+        if (comm) nccl::g_api.comm_destroy(comm);
     }
 
+    bool distributed() const { return comm != nullptr; }
     long long nxy() const { return (long long)dims.nx * dims.ny; }
+    wlm_engine* local(int global) const { return eng[global - first]; }
 
-    // Fill slab k's halo planes of a single (non-ping-pong) buffer of `ch`
-    // channels x `esz` bytes from its neighbours' owned planes.
-    void exchange_fixed(cudaStream_t s, int h, int ch, size_t esz, char* (*base)(wlm_engine*)) {
-        for (int k = 0; k < nslabs; ++k) {
-            wlm_engine* d = eng[k];
-            for (int side = 0; side < 2; ++side) {
-                const int nb = side == 0 ? k - 1 : k + 1;
-                if (nb < 0 || nb >= nslabs) continue;
-                wlm_engine* src = eng[nb];
-                const int z0 = side == 0 ? std::max(0, d->g.zs - h) : d->g.ze;
-                const int z1 = side == 0 ? d->g.zs : std::min(dims.nz, d->g.ze + h);
-                if (z1 <= z0) continue;
-                const size_t cnt = (size_t)(z1 - z0) * nxy();
-                for (int c = 0; c < ch; ++c) {
-                    char* dp = base(d) + ((size_t)c * d->g.n + (size_t)(z0 - d->g.zlo) * nxy()) * esz;
-                    const char* sp = base(src) + ((size_t)c * src->g.n + (size_t)(z0 - src->g.zlo) * nxy()) * esz;
-                    CK(cudaMemcpyAsync(dp, sp, cnt * esz, cudaMemcpyDeviceToDevice, s));
+    void nccl_check(int r, const char* what) {
+        if (r != 0) {
+            set_err(ctx, std::string(what) + ": " + nccl::g_api.err(r));
+            throw Fail{WLM_CUDA};
+        }
+    }
+
+    // Channel stacks of one buffer kind: base, element size, channel stride
+    // (elements), channel count.
+    struct Chan {
+        char* base;
+        size_t esz;
+        long long stride;
+        int nch;
+    };
+    static std::vector<Chan> channels(wlm_engine* e, int b) {
+        const long long n = e->g.n;
+        switch (b) {
+            case BUF_G: return {{(char*)e->G.p, 4, n, 3}};
+            case BUF_V: return {{(char*)e->VS.p, 4, n, 3}};
+            case BUF_U: return {{(char*)e->U.p, 4, n, 6}};  // both ping-pong buffers (nccl)
+            default: return {{(char*)e->ABE.p, 4, n, 2}, {(char*)(e->ABE.p + 2 * n), 8, n, 1}};
+        }
+    }
+
+    void exchange(int b, cudaStream_t s) {
+        if (!distributed()) {
+            for (size_t li = 0; li < eng.size(); ++li) {
+                wlm_engine* d = eng[li];
+                for (const wlm_halo_xfer& r : plan[li]) {
+                    if (r.buffer != b || r.send) continue;
+                    wlm_engine* src = local(r.peer);
+                    const long long cnt = (long long)(r.z1 - r.z0) * nxy();
+                    const long long doff = (r.z0 - d->g.zlo) * nxy(), soff = (r.z0 - src->g.zlo) * nxy();
+                    if (b == BUF_U) {
+                        const int grid = (int)std::min<long long>(148 * 4, (cnt + 255) / 256);
+                        k_copy_attempt_warp<<<grid, 256, 0, s>>>(d->U.p, d->g.n, doff, src->U.p, src->g.n,
+                                                                 soff, cnt, src->st.p);
+                        ++g_kernel_launches;
+                        continue;
+                    }
+                    const auto dc = channels(d, b), sc = channels(src, b);
+                    for (size_t q = 0; q < dc.size(); ++q)
+                        for (int c = 0; c < dc[q].nch; ++c)
+                            CK(cudaMemcpyAsync(dc[q].base + (c * dc[q].stride + doff) * dc[q].esz,
+                                               sc[q].base + (c * sc[q].stride + soff) * sc[q].esz,
+                                               cnt * dc[q].esz, cudaMemcpyDeviceToDevice, s));
                 }
             }
+            return;
         }
+        // nccl: this process holds exactly one slab.  The warp sends both
+        // ping-pong buffers (the accepted one's halo is unchanged, so
+        // overwriting it with the owner's identical values is harmless and
+        // the host need not know which buffer the device selected).
+        wlm_engine* e = eng[0];
+        const auto ch = channels(e, b);
+        nccl_check(nccl::g_api.group_start(), "ncclGroupStart");
+        for (const wlm_halo_xfer& r : plan[0]) {
+            if (r.buffer != b) continue;
+            const long long cnt = (long long)(r.z1 - r.z0) * nxy();
+            const long long off = (r.z0 - e->g.zlo) * nxy();
+            for (const Chan& q : ch)
+                for (int c = 0; c < q.nch; ++c) {
+                    char* p = q.base + (c * q.stride + off) * q.esz;
+                    const int dt = q.esz == 8 ? nccl::Float64 : nccl::Float32;
+                    if (r.send)
+                        nccl_check(nccl::g_api.send(p, (size_t)cnt, dt, r.peer, comm, s), "ncclSend");
+                    else
+                        nccl_check(nccl::g_api.recv(p, (size_t)cnt, dt, r.peer, comm, s), "ncclRecv");
+                }
+        }
+        nccl_check(nccl::g_api.group_end(), "ncclGroupEnd");
     }
 
-    void exchange_attempt_warp(cudaStream_t s, int h) {
-        for (int k = 0; k < nslabs; ++k) {
-            wlm_engine* d = eng[k];
-            for (int side = 0; side < 2; ++side) {
-                const int nb = side == 0 ? k - 1 : k + 1;
-                if (nb < 0 || nb >= nslabs) continue;
-                wlm_engine* src = eng[nb];
-                const int z0 = side == 0 ? std::max(0, d->g.zs - h) : d->g.ze;
-                const int z1 = side == 0 ? d->g.zs : std::min(dims.nz, d->g.ze + h);
-                if (z1 <= z0) continue;
-                const int cnt = (int)((z1 - z0) * nxy());
-                k_copy_attempt_warp<<<std::min(148 * 4, (cnt + 255) / 256), 256, 0, s>>>(
-                    d->U.p, d->g.n, (int)((z0 - d->g.zlo) * nxy()), src->U.p, src->g.n,
-                    (int)((z0 - src->g.zlo) * nxy()), cnt, src->st.p);
-                ++g_kernel_launches;
-            }
+    void reduce_max(int jac, cudaStream_t s) {
+        if (!distributed()) {
+            k_group_combine<<<1, 1, 0, s>>>(sts.p, (int)eng.size(), jac);
+            ++g_kernel_launches;
+            return;
         }
+        PairState* st = eng[0]->st.p;
+        if (!jac)
+            nccl_check(nccl::g_api.all_reduce(&st->max_bits, &st->max_bits, 1, nccl::Uint32, nccl::Max, comm, s),
+                       "ncclAllReduce(max)");
+        else
+            nccl_check(nccl::g_api.all_reduce(&st->jac_bits, &st->jac_bits, 1, nccl::Int32, nccl::Min, comm, s),
+                       "ncclAllReduce(min)");
     }
 
-    void xchg_g(cudaStream_t s) {
-        exchange_fixed(s, eng[0]->P.Ru, 3, sizeof(float), [](wlm_engine* e) { return (char*)e->G.p; });
+    void reduce_planes(cudaStream_t s) {
+        if (!distributed()) return;  // one shared plane array
+        double* ps = eng[0]->B.plane_sum;
+        nccl_check(nccl::g_api.all_reduce(ps, ps, (size_t)dims.nz, nccl::Float64, nccl::Sum, comm, s),
+                   "ncclAllReduce(planes)");
     }
-    void xchg_v(cudaStream_t s) {
-        exchange_fixed(s, eng[0]->P.Rw, 3, sizeof(float), [](wlm_engine* e) { return (char*)e->VS.p; });
-    }
-    void xchg_abe(cudaStream_t s) {
-        // A, B: two fp32 planes-stacks; E: one fp64 stack stored after them
-        exchange_fixed(s, 2, 2, sizeof(float), [](wlm_engine* e) { return (char*)e->ABE.p; });
-        exchange_fixed(s, 2, 1, sizeof(double),
-                       [](wlm_engine* e) { return (char*)(e->ABE.p + 2 * e->g.n); });
+
+    void evaluate(int mode, cudaStream_t s) {
+        for (auto* e : eng) e->stage_eval(mode, s);
+        reduce_planes(s);
+        for (auto* e : eng) e->stage_finalize(mode, s);
+        exchange(BUF_ABE, s);
     }
 
     void body(cudaStream_t s) {
         for (auto* e : eng) e->stage_grad(s);
-        xchg_g(s);
+        exchange(BUF_G, s);
         for (auto* e : eng) e->stage_step(s);
-        const int jac = eng[0]->P.log_jacobian;
-        k_group_combine<<<1, 1, 0, s>>>(sts.p, nslabs, 0);
-        ++g_kernel_launches;
-        xchg_v(s);
+        reduce_max(0, s);
+        exchange(BUF_V, s);
         for (auto* e : eng) launch_compose_smooth(e->B, e->P, s);
-        exchange_attempt_warp(s, std::max(eng[0]->P.Rw + 1, 2));
-        if (jac) {
+        exchange(BUF_U, s);
+        if (eng[0]->P.log_jacobian) {
             for (auto* e : eng) launch_jacobian_diag(e->B, e->P, s);
-            k_group_combine<<<1, 1, 0, s>>>(sts.p, nslabs, 1);
-            ++g_kernel_launches;
+            reduce_max(1, s);
         }
-        for (auto* e : eng) e->stage_eval(1, s);
-        for (auto* e : eng) e->stage_finalize(1, s);
-        xchg_abe(s);
+        evaluate(1, s);
     }
 
     void build_step_graph() {
@@ -195,47 +360,75 @@ struct wlm_slab_group {
         g_kernel_launches = saved;
         CK(cudaGraphInstantiate(&loop_exec, loop_graph, 0));
     }
+
+    // nccl transport: attempts are launched eagerly (collectives inside
+    // conditional graph bodies are not relied on).  Attempts of a finished
+    // registration are no-ops on the device, so with rejection the host
+    // launches the lower bound of remaining attempts, then re-reads the state.
+    void iterate_eager(int iters) {
+        cudaStream_t s = ctx->stream;
+        if (!eng[0]->P.rejection) {
+            for (int i = 0; i < iters; ++i) body(s);
+            return;
+        }
+        for (;;) {
+            const PairState st = read_states(eng[0])[0];
+            if (st.done) return;
+            const int left = std::max(1, st.iters_target - st.iter);
+            for (int i = 0; i < left; ++i) body(s);
+        }
+    }
+
+    void attach(wlm_engine* e) {
+        if (!distributed()) {
+            e->shared_fm = true;
+            e->shared_plane_sum = true;
+            e->B.F = F.p;
+            e->B.M = M.p;
+            e->B.plane_sum = plane_sum.p;
+        }
+        engine_alloc(e);
+        if (distributed()) e->B.zero_foreign_planes = 1;
+    }
+
+    float* fp() const { return distributed() ? eng[0]->F.p : F.p; }
+    float* mp() const { return distributed() ? eng[0]->M.p : M.p; }
 };
 
-extern "C" {
+namespace {
 
-wlm_status wlm_slab_group_create(wlm_ctx* ctx, wlm_dims d, int nslabs, const wlm_reg_config* cfg,
-                                 wlm_slab_group** out) {
-    if (!ctx || !out || !cfg || nslabs < 1 || !valid_dims(d)) return WLM_INVALID_ARG;
-    *out = nullptr;
-    if (d.nz / nslabs < kHalo) {
-        set_err(ctx, "slab_group: every slab needs at least 4 planes (halo depth)");
-        return WLM_INVALID_ARG;
-    }
+wlm_status make_group(wlm_ctx* ctx, wlm_dims d, int nslabs, int first, int count, const wlm_reg_config* cfg,
+                      nccl::Comm comm, wlm_slab_group** out) {
     wlm_slab_group* grp = new wlm_slab_group();
     grp->ctx = ctx;
     grp->dims = d;
     grp->gfull = make_geo(d);
     grp->nslabs = nslabs;
+    grp->first = first;
     grp->cfg = *cfg;
+    grp->comm = comm;  // owned (destroyed with the group) from here on
     wlm_status s = run(ctx, [&] {
-        grp->F = DevBuf<float>(ctx, (size_t)grp->gfull.nfull);
-        grp->M = DevBuf<float>(ctx, (size_t)grp->gfull.nfull);
-        grp->plane_sum = DevBuf<double>(ctx, (size_t)d.nz);
-        CK(cudaMemsetAsync(grp->plane_sum.p, 0, sizeof(double) * d.nz, ctx->stream));
+        if (!comm) {
+            grp->F = DevBuf<float>(ctx, (size_t)grp->gfull.nfull);
+            grp->M = DevBuf<float>(ctx, (size_t)grp->gfull.nfull);
+            grp->plane_sum = DevBuf<double>(ctx, (size_t)d.nz);
+            CK(cudaMemsetAsync(grp->plane_sum.p, 0, sizeof(double) * d.nz, ctx->stream));
+        }
         std::vector<PairState*> hst;
-        for (int k = 0; k < nslabs; ++k) {
+        for (int k = first; k < first + count; ++k) {
             wlm_engine* e = new wlm_engine();
             grp->eng.push_back(e);
             const wlm_status es = engine_init(e, ctx, d, 1, cfg);
             if (es != WLM_OK) throw Fail{es};
-            const int zs = (int)((long long)k * d.nz / nslabs), ze = (int)((long long)(k + 1) * d.nz / nslabs);
+            int zs, ze;
+            partition(d.nz, nslabs, k, &zs, &ze);
             e->g = make_slab_geo(d, zs, ze, kHalo);
-            e->shared_fm = true;
-            e->shared_plane_sum = true;
-            e->B.F = grp->F.p;
-            e->B.M = grp->M.p;
-            e->B.plane_sum = grp->plane_sum.p;
-            engine_alloc(e);
+            grp->attach(e);
+            grp->plan.push_back(slab_plan(d, nslabs, k, e->P.Ru, e->P.Rw));
             hst.push_back(e->st.p);
         }
-        grp->sts = DevBuf<PairState*>(ctx, nslabs);
-        CK(cudaMemcpyAsync(grp->sts.p, hst.data(), sizeof(PairState*) * nslabs, cudaMemcpyHostToDevice,
+        grp->sts = DevBuf<PairState*>(ctx, hst.size());
+        CK(cudaMemcpyAsync(grp->sts.p, hst.data(), sizeof(PairState*) * hst.size(), cudaMemcpyHostToDevice,
                            ctx->stream));
         CK(cudaStreamSynchronize(ctx->stream));
     });
@@ -245,6 +438,79 @@ wlm_status wlm_slab_group_create(wlm_ctx* ctx, wlm_dims d, int nslabs, const wlm
     }
     *out = grp;
     return WLM_OK;
+}
+
+wlm_status check_split(wlm_ctx* ctx, wlm_dims d, int nslabs) {
+    if (!ctx || nslabs < 1 || !valid_dims(d)) return WLM_INVALID_ARG;
+    if (d.nz / nslabs < kHalo) {
+        set_err(ctx, "slab_group: every slab needs at least 4 planes (halo depth)");
+        return WLM_INVALID_ARG;
+    }
+    return WLM_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+wlm_status wlm_slab_partition(int nz, int nslabs, int slab, int* zs, int* ze) {
+    if (nz < 1 || nslabs < 1 || slab < 0 || slab >= nslabs || !zs || !ze) return WLM_INVALID_ARG;
+    partition(nz, nslabs, slab, zs, ze);
+    return nz / nslabs >= kHalo ? WLM_OK : WLM_INVALID_ARG;
+}
+
+wlm_status wlm_slab_halo_plan(wlm_dims d, int nslabs, int slab, const wlm_reg_config* cfg, wlm_halo_xfer* rows,
+                              size_t cap, size_t* len) {
+    if (!cfg || !len || nslabs < 1 || slab < 0 || slab >= nslabs || !valid_dims(d)) return WLM_INVALID_ARG;
+    if (d.nz / nslabs < kHalo) return WLM_INVALID_ARG;
+    const auto p = slab_plan(d, nslabs, slab, smooth_radius(cfg->sigma_update), smooth_radius(cfg->sigma_warp));
+    *len = p.size();
+    if (rows) std::memcpy(rows, p.data(), sizeof(wlm_halo_xfer) * std::min(cap, p.size()));
+    return WLM_OK;
+}
+
+wlm_status wlm_slab_group_create(wlm_ctx* ctx, wlm_dims d, int nslabs, const wlm_reg_config* cfg,
+                                 wlm_slab_group** out) {
+    if (!out || !cfg) return WLM_INVALID_ARG;
+    *out = nullptr;
+    const wlm_status s = check_split(ctx, d, nslabs);
+    if (s != WLM_OK) return s;
+    return make_group(ctx, d, nslabs, 0, nslabs, cfg, nullptr, out);
+}
+
+wlm_status wlm_nccl_unique_id(const char* nccl_lib, unsigned char id[128]) {
+    std::string why;
+    if (!id) return WLM_INVALID_ARG;
+    if (!nccl::load(nccl_lib, &why)) return WLM_UNSUPPORTED;
+    nccl::UniqueId u;
+    if (nccl::g_api.get_unique_id(&u) != 0) return WLM_CUDA;
+    std::memcpy(id, u.internal, 128);
+    return WLM_OK;
+}
+
+wlm_status wlm_slab_group_create_nccl(wlm_ctx* ctx, wlm_dims d, int rank, int nranks, const unsigned char id[128],
+                                      const char* nccl_lib, const wlm_reg_config* cfg, wlm_slab_group** out) {
+    if (!out || !cfg || !id || rank < 0 || rank >= nranks) return WLM_INVALID_ARG;
+    *out = nullptr;
+    wlm_status s = check_split(ctx, d, nranks);
+    if (s != WLM_OK) return s;
+    std::string why;
+    if (!nccl::load(nccl_lib, &why)) {
+        set_err(ctx, why);
+        return WLM_UNSUPPORTED;
+    }
+    nccl::Comm comm = nullptr;
+    s = run(ctx, [&] {
+        nccl::UniqueId u;
+        std::memcpy(u.internal, id, 128);
+        const int r = nccl::g_api.comm_init_rank(&comm, nranks, u, rank);
+        if (r != 0) {
+            set_err(ctx, std::string("ncclCommInitRank: ") + nccl::g_api.err(r));
+            throw Fail{WLM_CUDA};
+        }
+    });
+    if (s != WLM_OK) return s;
+    return make_group(ctx, d, nranks, rank, 1, cfg, comm, out);
 }
 
 void wlm_slab_group_destroy(wlm_slab_group* g) {
@@ -260,14 +526,12 @@ wlm_status wlm_slab_group_load(wlm_slab_group* g, const float* F, const float* M
     return run(ctx, [&] {
         const size_t bytes = sizeof(float) * (size_t)g->gfull.nfull;
         const cudaMemcpyKind k = is_host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
-        CK(cudaMemcpyAsync(g->F.p, F, bytes, k, ctx->stream));
-        CK(cudaMemcpyAsync(g->M.p, M, bytes, k, ctx->stream));
+        CK(cudaMemcpyAsync(g->fp(), F, bytes, k, ctx->stream));
+        CK(cudaMemcpyAsync(g->mp(), M, bytes, k, ctx->stream));
         for (auto* e : g->eng) launch_shifts(e->B, ctx->stream);
     });
 }
 
-// u: whole-volume SoA [3][nz][ny][nx] (host or device), or null for identity.
-// Each slab receives its owned planes and its halo planes.
 wlm_status wlm_slab_group_set_warp(wlm_slab_group* g, const float* u, int is_host) {
     if (!g) return WLM_INVALID_ARG;
     wlm_ctx* ctx = g->ctx;
@@ -293,8 +557,7 @@ wlm_status wlm_slab_group_get_warp(wlm_slab_group* g, float* u, int is_host) {
     return run(ctx, [&] {
         const long long nxy = g->nxy();
         for (auto* e : g->eng) {
-            const std::vector<PairState> st = read_states(e);
-            const int buf = st[0].cur;
+            const int buf = read_states(e)[0].cur;
             for (int c = 0; c < 3; ++c)
                 CK(cudaMemcpyAsync(u + (size_t)c * g->gfull.nfull + (size_t)e->g.zs * nxy,
                                    e->U.p + (size_t)(buf * 3 + c) * e->g.n + (size_t)(e->g.zs - e->g.zlo) * nxy,
@@ -305,14 +568,19 @@ wlm_status wlm_slab_group_get_warp(wlm_slab_group* g, float* u, int is_host) {
     });
 }
 
+wlm_status wlm_slab_group_owned(const wlm_slab_group* g, int* zs, int* ze) {
+    if (!g || !zs || !ze) return WLM_INVALID_ARG;
+    *zs = g->eng.front()->g.zs;
+    *ze = g->eng.back()->g.ze;
+    return WLM_OK;
+}
+
 wlm_status wlm_slab_group_begin_level(wlm_slab_group* g, int level) {
     if (!g) return WLM_INVALID_ARG;
     wlm_ctx* ctx = g->ctx;
     return run(ctx, [&] {
         for (auto* e : g->eng) launch_begin_level(e->B, e->P, level, 0, e->cfg.lm.lambda0, ctx->stream);
-        for (auto* e : g->eng) e->stage_eval(0, ctx->stream);
-        for (auto* e : g->eng) e->stage_finalize(0, ctx->stream);
-        g->xchg_abe(ctx->stream);
+        g->evaluate(0, ctx->stream);
     });
 }
 
@@ -322,29 +590,30 @@ wlm_status wlm_slab_group_iterate(wlm_slab_group* g, int iters) {
     return run(ctx, [&] {
         for (auto* e : g->eng) launch_set_targets(e->B, iters, ctx->stream);
         if (iters == 0) return;
-        if (!g->eng[0]->P.rejection) {
+        if (g->distributed()) {
+            g->iterate_eager(iters);
+        } else if (!g->eng[0]->P.rejection) {
             g->build_step_graph();
             for (int i = 0; i < iters; ++i) CK(cudaGraphLaunch(g->step_exec, ctx->stream));
             g_kernel_launches += (uint64_t)iters * g->body_kernels;
         } else {
             g->build_loop_graph();
             CK(cudaGraphLaunch(g->loop_exec, ctx->stream));
+            g_kernel_launches += (uint64_t)g->body_kernels + 1;
         }
     });
 }
 
-// Trace of slab 0; WLM_INTERNAL-style consistency: every slab must have run
-// the identical state machine (returns WLM_CUDA with a message otherwise).
 wlm_status wlm_slab_group_trace(wlm_slab_group* g, wlm_step_log* rows, size_t cap, size_t* len) {
     if (!g) return WLM_INVALID_ARG;
     wlm_status s = wlm_engine_trace(g->eng[0], 0, rows, cap, len);
     if (s != WLM_OK) return s;
     std::vector<wlm_step_log> other(cap);
-    for (int k = 1; k < g->nslabs; ++k) {
+    for (size_t k = 1; k < g->eng.size(); ++k) {
         size_t n2 = 0;
         s = wlm_engine_trace(g->eng[k], 0, other.data(), cap, &n2);
         if (s != WLM_OK) return s;
-        if (n2 != *len || std::memcmp(other.data(), rows, sizeof(wlm_step_log) * n2) != 0) {
+        if (n2 != *len || (rows && std::memcmp(other.data(), rows, sizeof(wlm_step_log) * n2) != 0)) {
             set_err(g->ctx, "slab_group: slabs diverged (state machines disagree)");
             return WLM_CUDA;
         }

@@ -378,3 +378,24 @@ def test_slab_group_rejects_thin_slabs(P, ctx):
     cfg = P.reg_config(nlevels=1, factors=[1], iters=[1])
     with pytest.raises(P.InvalidArgument):
         P.SlabGroup((12, 16, 16), 4, cfg=cfg, ctx=ctx)
+
+
+@pytest.mark.parametrize("extra", [{}, {"lm.rejection": 1, "lm.tau": 0.2, "log_jacobian": 1}])
+def test_nccl_rank_slab_world1_matches_engine(P, ctx, extra):
+    """The one-process-per-GPU transport on a real NCCL communicator of one
+    rank: plane-sum and max all-reduces, foreign-plane zeroing and the eager
+    attempt loop (with rejection) give the engine's result bit for bit."""
+    from paper_2603_19371_b200 import slabs
+    F, M, _ = O.synth_pair((20, 24, 28), 22, num_blobs=8, warp_max=2.5)
+    cfg = P.reg_config(nlevels=1, factors=[1], iters=[10], **extra)
+    w1, (t1,), (s1,) = run_engine(P, ctx, F, M, cfg, 10)
+    grp = slabs.RankSlab(F.shape, 0, 1, slabs.nccl_unique_id(), cfg=cfg, ctx=ctx)
+    grp.load(F, M)
+    grp.set_warp(None)
+    grp.begin_level(0)
+    grp.iterate(10)
+    assert grp.owned() == (0, F.shape[0])
+    w, t = grp.get_local_warp(), grp.trace()
+    grp.close()
+    assert same_trace(t, t1)
+    assert np.array_equal(w, w1[0])

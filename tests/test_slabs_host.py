@@ -1,0 +1,112 @@
+"""Host logic of the z-slab decomposition (config 5), no GPU needed:
+partition, halo plan consistency, and the multi-process bootstrap over a
+world_size-2/4 gloo group (what each rank would execute with NCCL)."""
+import os
+import socket
+
+import pytest
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import paper_2603_19371_b200 as P
+from paper_2603_19371_b200 import slabs
+
+
+def test_partition_covers_volume():
+    for nz, ns in ((1024, 8), (1023, 8), (20, 5), (37, 3), (8, 2)):
+        parts = slabs.partition(nz, ns)
+        assert parts[0][0] == 0 and parts[-1][1] == nz
+        assert all(a[1] == b[0] for a, b in zip(parts, parts[1:]))
+        assert all(ze - zs >= 4 for zs, ze in parts)
+    with pytest.raises(ValueError):
+        slabs.partition(12, 4)
+
+
+def _halo_depths(cfg):
+    import math
+    r = lambda s: 0 if s <= 0 else max(1, math.ceil(3 * s))  # noqa: E731  field.cpp:206-207
+    return dict(g=r(cfg.sigma_update), dU_s=r(cfg.sigma_warp), warp=max(r(cfg.sigma_warp) + 1, 2), abe=2)
+
+
+def check_plans(shape, ns, plans, cfg):
+    """Every receive has the matching send on the peer (same buffer, planes);
+    sends come from owned planes; receives cover exactly the halo each
+    stage reads (clipped at the volume faces)."""
+    parts = slabs.partition(shape[0], ns)
+    depth = _halo_depths(cfg)
+    for k, rows in enumerate(plans):
+        zs, ze = parts[k]
+        for r in rows:
+            peer = plans[r["peer"]]
+            twin = [q for q in peer if q["peer"] == k and q["buffer"] == r["buffer"]
+                    and q["send"] != r["send"] and (q["z0"], q["z1"]) == (r["z0"], r["z1"])]
+            assert len(twin) == 1, (k, r)
+            if r["send"]:
+                assert zs <= r["z0"] < r["z1"] <= ze
+            else:
+                pz0, pz1 = parts[r["peer"]]
+                assert pz0 <= r["z0"] < r["z1"] <= pz1 and not (zs <= r["z0"] < ze)
+        for buf, h in depth.items():
+            recv = sorted((r["z0"], r["z1"]) for r in rows if r["buffer"] == buf and not r["send"])
+            want = [x for x in ((max(0, zs - h), zs), (ze, min(shape[0], ze + h))) if x[1] > x[0]]
+            assert recv == want, (k, buf, recv, want)
+
+
+@pytest.mark.parametrize("ns", [2, 3, 5, 8])
+def test_halo_plans_match_pairwise(ns):
+    cfg = P.reg_config(nlevels=1, factors=[1], iters=[1])
+    shape = (64, 16, 16)
+    plans = [slabs.halo_plan(shape, ns, k, cfg) for k in range(ns)]
+    check_plans(shape, ns, plans, cfg)
+
+
+def test_halo_plan_follows_sigma():
+    cfg = P.reg_config(nlevels=1, factors=[1], iters=[1], sigma_update=0.5, sigma_warp=1.0)
+    shape = (40, 8, 8)
+    plans = [slabs.halo_plan(shape, 4, k, cfg) for k in range(4)]
+    check_plans(shape, 4, plans, cfg)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _rank_main(rank, world, port, shape, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        cfg = P.reg_config(nlevels=1, factors=[1], iters=[1])
+        # the NCCL id travels from rank 0 exactly as RankSlab's bootstrap does
+        uid = slabs.broadcast_unique_id(lambda: bytes(range(128)) if rank == 0 else None)
+        mine = slabs.halo_plan(shape, world, rank, cfg)
+        plans = [None] * world
+        dist.all_gather_object(plans, mine)
+        ids = [None] * world
+        dist.all_gather_object(ids, uid)
+        if rank == 0:
+            check_plans(shape, world, plans, cfg)
+            assert all(i == bytes(range(128)) for i in ids)
+            q.put("ok")
+    except Exception as e:  # surfaced by the parent
+        q.put(f"rank {rank}: {e!r}")
+        raise
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_gloo_bootstrap_and_plan_exchange(world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_rank_main, args=(r, world, port, (48, 12, 10), q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(120)
+    assert all(p.exitcode == 0 for p in procs), [p.exitcode for p in procs]
+    assert q.get(timeout=5) == "ok"
