@@ -292,6 +292,108 @@ def run_ours(args, rank, world, local):
     return line
 
 
+def run_slabs(args, rank, world, local):
+    """Config 5: one large volume (default 1024^3) split into `world` z-slabs,
+    one per GPU (NCCL halo exchange + plane-sum/max all-reduce); at N=1 the
+    same group with one slab.  Strong scaling (the volume is fixed)."""
+    import ctypes as C
+
+    import torch
+
+    import paper_2603_19371_b200 as P
+    from paper_2603_19371_b200 import slabs
+    from paper_2603_19371_b200._lib import Dims, SynthSpec
+
+    torch.cuda.set_device(local)
+    n = args.size
+    shape = (n, n, n)
+    nvox = n ** 3
+    ctx = P.Context(local)
+    lib = P.load()
+    cfg = P.reg_config(nlevels=1, factors=[1], iters=[args.steps])
+    # identical synthetic pair on every rank (seed 7, warp_max 16; SURVEY 8(d))
+    F_d = torch.empty(shape, dtype=torch.float32, device=f"cuda:{local}")
+    M_d = torch.empty(shape, dtype=torch.float32, device=f"cuda:{local}")
+    spec = SynthSpec(Dims(n, n, n), 96, 0.0, 16.0, 0.01, 7)
+    ctx.check(lib.wlm_synth_pair(ctx.h, C.byref(spec), F_d.data_ptr(), M_d.data_ptr(), None, 1))
+    if world > 1:
+        import torch.distributed as dist
+        uid = slabs.broadcast_unique_id(slabs.nccl_unique_id)
+        grp = slabs.RankSlab(shape, rank, world, uid, cfg=cfg, ctx=ctx)
+    else:
+        grp = P.SlabGroup(shape, 1, cfg=cfg, ctx=ctx)
+    grp.load(F_d, M_d)
+    F_h = F_d.cpu().pin_memory() if args.e2e_iters > 0 else None
+    M_h = M_d.cpu().pin_memory() if args.e2e_iters > 0 else None
+    del F_d, M_d
+    torch.cuda.empty_cache()
+    stream = torch.cuda.ExternalStream(ctx.stream(), device=f"cuda:{local}")
+    grp.set_warp(None)
+    grp.begin_level(0)
+    grp.iterate(args.warmup)
+    ctx.synchronize()
+
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    barrier(world, local)
+    torch.cuda.synchronize()
+    launches_before = ctx.launches
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        grp.iterate(args.steps)
+        ev1.record(stream)
+        ev1.synchronize()
+    torch.cuda.synchronize()
+    barrier(world, local)
+    launches_timed = ctx.launches - launches_before
+    ms_max = max_over_ranks(ev0.elapsed_time(ev1), world, local)
+    st = grp.state()
+    assert math.isfinite(st["r"]), st
+
+    e2e = None
+    if args.e2e_iters > 0:
+        U_h = torch.empty((3,) + shape, dtype=torch.float32, pin_memory=True)
+        barrier(world, local)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        grp.load(F_h, M_h)
+        grp.set_warp(None)
+        grp.begin_level(0)
+        grp.iterate(args.e2e_iters)
+        grp.get_warp(U_h)
+        torch.cuda.synchronize()
+        e2e_s = max_over_ranks(time.perf_counter() - t0, world, local)
+        e2e = {"value": round(nvox * args.e2e_iters / e2e_s / 1e9, 4), "unit": "Gvoxel/s",
+               "h2d_bytes_per_step": 2 * nvox * 4, "d2h_bytes_per_step": 3 * nvox * 4 // world,
+               "iters_per_step": args.e2e_iters,
+               "path": "wlm_slab_group_load(host) + begin_level + iterate + get_warp(host, owned planes)"}
+
+    hbm, peak_kind = peaks()
+    value = nvox * args.steps / (ms_max * 1e-3) / 1e9
+    it_frac = BYTES_PER_VOXEL_ITER * value / hbm / max(world, 1)
+    line = {
+        "metric": METRIC, "value": round(value, 4), "unit": "Gvoxel/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_max / args.steps, 4),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (GPU synth_pair, 96 blobs, smoothed random warp, max 16 voxels, seed 7)",
+        "config": {"workload": f"config 5: one {n}^3 pair, z-slab sharded over {world} GPU(s), LNCC r=2 + "
+                               f"pointwise LM, rejection off",
+                   "volume": list(shape), "parallelism": f"z-slab x{world} (halo exchange + NCCL all-reduce)"
+                   if world > 1 else "single slab", "l2": "inputs > L2"},
+        "iters_per_s": round(args.steps / (ms_max * 1e-3), 3),
+        "roofline": {"bound": "hbm", "kernel": "iteration (K1..K4 + exchanges)",
+                     "achieved": round(value * BYTES_PER_VOXEL_ITER / max(world, 1), 1), "peak": hbm,
+                     "peak_kind": peak_kind, "unit": "GB/s", "frac": round(it_frac, 4), "traffic": None,
+                     "iteration_bytes_per_voxel": BYTES_PER_VOXEL_ITER},
+        "gpu_launches": int(launches_timed),
+        "clocks": clk.summary(),
+    }
+    if e2e:
+        line["e2e"] = e2e
+    grp.close()
+    return line
+
+
 def load_traffic(kernel):
     """DRAM bytes per launch from the committed ncu --set full summary."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
@@ -398,7 +500,11 @@ def main():
     ap.add_argument("--e2e-iters", type=int, default=100)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-budget-s", type=float, default=200.0)
+    ap.add_argument("--config", type=int, default=4, choices=[4, 5],
+                    help="4: batch of 192^3 pairs (default, weak scaling); 5: one 1024^3 volume in z-slabs")
     args = ap.parse_args()
+    if args.config == 5 and args.size == 192:
+        args.size = 1024
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3  # timing rule: >= 3 warm-up steps
 
@@ -411,7 +517,7 @@ def main():
         return
 
     rank, world, local = dist_init(args.gpus)
-    line = run_ours(args, rank, world, local)
+    line = (run_slabs if args.config == 5 else run_ours)(args, rank, world, local)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -161,21 +161,31 @@ class SlabGroup:
         self.ctx.check(st)
 
     def load(self, F, M):
-        F = np.ascontiguousarray(F, dtype=np.float32)
-        M = np.ascontiguousarray(M, dtype=np.float32)
-        self._chk(self.lib.wlm_slab_group_load(self.h, F.ctypes.data, M.ctypes.data, 1))
+        """F, M: whole (nz, ny, nx) float32 volumes (numpy or CUDA tensor)."""
+        if isinstance(F, np.ndarray):
+            F = np.ascontiguousarray(F, dtype=np.float32)
+            M = np.ascontiguousarray(M, dtype=np.float32)
+        pf, hf = Engine._ptr(F)
+        pm, _ = Engine._ptr(M)
+        self._chk(self.lib.wlm_slab_group_load(self.h, pf, pm, hf))
         self.ctx.synchronize()
 
     def set_warp(self, u=None):
         if u is None:
             self._chk(self.lib.wlm_slab_group_set_warp(self.h, None, 1))
             return
-        u = np.ascontiguousarray(u, dtype=np.float32)
-        self._chk(self.lib.wlm_slab_group_set_warp(self.h, u.ctypes.data, 1))
+        if isinstance(u, np.ndarray):
+            u = np.ascontiguousarray(u, dtype=np.float32)
+        p, host = Engine._ptr(u)
+        self._chk(self.lib.wlm_slab_group_set_warp(self.h, p, host))
 
-    def get_warp(self):
-        out = np.empty((3,) + self.shape, np.float32)
-        self._chk(self.lib.wlm_slab_group_get_warp(self.h, out.ctypes.data, 1))
+    def get_warp(self, out=None):
+        """Whole-volume (3, nz, ny, nx) warp (planes owned elsewhere are left
+        untouched); out may be a numpy array or a pinned/CUDA tensor."""
+        if out is None:
+            out = np.zeros((3,) + self.shape, np.float32)
+        p, host = Engine._ptr(out)
+        self._chk(self.lib.wlm_slab_group_get_warp(self.h, p, host))
         return out
 
     def begin_level(self, level=0):
