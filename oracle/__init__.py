@@ -79,6 +79,8 @@ def _declare(lib):
     sig = {
         "orc_set_threads": (None, [C.c_int]),
         "orc_set_fp32_storage": (None, [C.c_int]),
+        "orc_set_dev_flags": (None, [C.c_int]),
+        "orc_dev_smooth32": (None, [_D, Dims, C.c_double, C.c_int]),
         "orc_default_reg_config": (None, [C.POINTER(RegConfig)]),
         "orc_sample_trilinear_grad": (C.c_double, [_D, Dims, C.c_double, C.c_double, C.c_double, _D]),
         "orc_sample_field": (None, [_D, Dims, C.c_double, C.c_double, C.c_double, _D]),
@@ -133,11 +135,11 @@ def lib(kind: str = "port"):
 class fp32_storage:
     """Context manager: run the oracle with device storage-precision emulation."""
 
-    def __init__(self, kind="port"):
-        self.kind = kind
+    def __init__(self, kind="port", mode=1):
+        self.kind, self.mode = kind, mode
 
     def __enter__(self):
-        lib(self.kind).orc_set_fp32_storage(1)
+        lib(self.kind).orc_set_fp32_storage(self.mode)
         return self
 
     def __exit__(self, *a):

@@ -33,7 +33,9 @@ int g_threads = 1;
 // quantity the device stores in fp32 (window coefficients A and B, gradient
 // g, smoothed step dU_s, warps, upsampled warps, Adam moments) is rounded to
 // fp32 at the same point of the computation; all arithmetic stays fp64.
-int g_fp32_storage = 0;
+int g_fp32_storage = 0;  // 0 fp64, 1 fp32 storage points, 2 + device fp32 arithmetic
+int g_dev_k3norm64 = 0;
+int g_dev_flags = 3;  // mode 2: bit0 K3 step+smooth fp32, bit1 K4 smooth fp32, bit2 compose fp32
 inline double r32(double v) { return g_fp32_storage ? (double)(float)v : v; }
 
 // Static-partition parallel loop over [lo, hi) on g_threads std::threads.
@@ -279,6 +281,154 @@ void smooth(double* data, orc_dims d, int nchan, double sigma) {
 #endif
 }
 
+// ---- device-arithmetic emulation (fp32-storage mode 2) ----
+// The engine's K3/K4 step and Gaussian passes run in fp32 (DESIGN.md
+// "Precision"); mode 2 reproduces their exact operation order so the
+// fp32-storage bar stays a tight check of the device algorithm:
+//   weights w[|d|] = (float)exp(-d^2 / 2 sigma^2), full = (float)(fp64 sum);
+//   each pass s = fmaf(w[d], in[p - R + d], s) for d = 0..2R over a
+//   zero-filled halo; out = s_z * ((1 / (Wx Wy)) * (1 / Wz)), W* the fp32
+//   in-bounds weight sums (hot_kernels.cu k_step_smooth / k_compose_smooth).
+struct DevKernel {
+    int R = 0;
+    float w[8] = {0};
+    float wlo[8] = {0};  // w64 - w (exact-shape experiment)
+    double w64[8] = {0};
+    float full = 1.f;
+};
+int g_dev_hilo = 0;
+DevKernel dev_kernel(double sigma) {
+    DevKernel k;
+    if (!(sigma > 0.0)) { k.w[0] = 1.f; return k; }
+    k.R = std::max(1, (int)std::ceil(3.0 * sigma));
+    double s = 0.0;
+    for (int d = 0; d <= k.R; ++d) {
+        const double v = std::exp(-0.5 * (double)(d * d) / (sigma * sigma));
+        k.w[d] = (float)v;
+        k.wlo[d] = (float)(v - (double)k.w[d]);
+        k.w64[d] = v;
+        s += d == 0 ? v : 2.0 * v;
+    }
+    k.full = (float)s;
+    return k;
+}
+float dev_wsum(int p, int n, const DevKernel& k) {
+    if (p >= k.R && p + k.R <= n - 1) return k.full;
+    float s = 0.f;
+    for (int d = -k.R; d <= k.R; ++d) {
+        const int q = p + d;
+        if (q >= 0 && q < n) s += k.w[d < 0 ? -d : d];
+    }
+    return s;
+}
+// Exact fp64 sum of the fp32 weights over the in-bounds taps.
+double dev_wsum64(int p, int n, const DevKernel& k) {
+    double s = 0.0;
+    for (int d = -k.R; d <= k.R; ++d) {
+        const int q = p + d;
+        if (q >= 0 && q < n) s += g_dev_hilo ? k.w64[d < 0 ? -d : d] : (double)k.w[d < 0 ? -d : d];
+    }
+    return s;
+}
+// data: AoS 3-channel field (values already fp32), smoothed in place.
+// norm64: normalise in fp64 by the exact weight sums (K4, where a scale bias
+// would accumulate in the warp) instead of the fp32 reciprocal (K3, whose
+// output is max-normalised anyway).
+void dev_smooth32(double* data, orc_dims d, double sigma, bool norm64) {
+    const DevKernel k = dev_kernel(sigma);
+    const bool hilo = norm64 && g_dev_hilo;
+    if (k.R == 0) return;
+    const int R = k.R;
+    const size_t N = nvox(d);
+    std::vector<float> a(3 * N), b(3 * N);
+    for (size_t i = 0; i < 3 * N; ++i) a[i] = (float)data[i];
+    const int n3[3] = {d.nx, d.ny, d.nz};
+    auto pass = [&](const std::vector<float>& in, std::vector<float>& out, int axis) {
+        const long long stride = axis == 0 ? 1 : axis == 1 ? d.nx : (long long)d.nx * d.ny;
+        const int n = n3[axis];
+        par_for(0, d.nz, [&](long long zz) {
+            const int z = (int)zz;
+            for (int y = 0; y < d.ny; ++y)
+                for (int x = 0; x < d.nx; ++x) {
+                    const int pcoord = axis == 0 ? x : axis == 1 ? y : z;
+                    const size_t i = lin(d, x, y, z);
+                    for (int c = 0; c < 3; ++c) {
+                        float s = 0.f;
+                        for (int t = 0; t <= 2 * R; ++t) {
+                            const int q = pcoord - R + t;
+                            const float v = (q >= 0 && q < n) ? in[3 * (i + (long long)(q - pcoord) * stride) + c] : 0.f;
+                            const int dd = t < R ? R - t : t - R;
+                            s = std::fmaf(k.w[dd], v, s);
+                            if (hilo) s = std::fmaf(k.wlo[dd], v, s);
+                        }
+                        out[3 * i + c] = s;
+                    }
+                }
+        });
+    };
+    pass(a, b, 0);
+    pass(b, a, 1);
+    pass(a, b, 2);
+    par_for(0, d.nz, [&](long long zz) {
+        const int z = (int)zz;
+        const float iz = 1.f / dev_wsum(z, d.nz, k);
+        const double wz64 = dev_wsum64(z, d.nz, k);
+        for (int y = 0; y < d.ny; ++y)
+            for (int x = 0; x < d.nx; ++x) {
+                const size_t i = lin(d, x, y, z);
+                if (norm64) {
+                    // exact sums of the fp32 weights, fp64 normalisation: no scale bias
+                    const double inv = 1.0 / (dev_wsum64(x, d.nx, k) * dev_wsum64(y, d.ny, k) * wz64);
+                    for (int c = 0; c < 3; ++c) data[3 * i + c] = (double)(float)((double)b[3 * i + c] * inv);
+                } else {
+                    const float ixy = 1.f / (dev_wsum(x, d.nx, k) * dev_wsum(y, d.ny, k));
+                    const float inv = ixy * iz;
+                    for (int c = 0; c < 3; ++c) data[3 * i + c] = (double)(b[3 * i + c] * inv);
+                }
+            }
+    });
+}
+// Experimental fp32 compose (mode 2 with orc_set_dev_compose32): d rounded
+// to fp32, split-form taps (exact), fp32 fused lerps, u' = d + u(x + d).
+void dev_compose32(const double* u, const double* v, orc_dims d, double eps, double* out) {
+    par_for(0, d.nz, [&](long long zz) {
+        const int z = (int)zz;
+        for (int y = 0; y < d.ny; ++y)
+            for (int x = 0; x < d.nx; ++x) {
+                const size_t i = 3 * lin(d, x, y, z);
+                const float sx = (float)(eps * v[i]), sy = (float)(eps * v[i + 1]), sz = (float)(eps * v[i + 2]);
+                const Tap X = resolve((double)x + sx, d.nx), Y = resolve((double)y + sy, d.ny),
+                          Z = resolve((double)z + sz, d.nz);
+                const float wx = (float)X.w, wy = (float)Y.w, wz = (float)Z.w;
+                const float dd[3] = {sx, sy, sz};
+                for (int ch = 0; ch < 3; ++ch) {
+                    auto at = [&](int xx, int yy, int zq) { return (float)u[3 * lin(d, xx, yy, zq) + ch]; };
+                    const float a = at(X.lo, Y.lo, Z.lo), b = at(X.hi, Y.lo, Z.lo);
+                    const float c = at(X.lo, Y.hi, Z.lo), e = at(X.hi, Y.hi, Z.lo);
+                    const float f = at(X.lo, Y.lo, Z.hi), h = at(X.hi, Y.lo, Z.hi);
+                    const float k = at(X.lo, Y.hi, Z.hi), l = at(X.hi, Y.hi, Z.hi);
+                    const float r00 = std::fmaf(wx, b - a, a), r10 = std::fmaf(wx, e - c, c);
+                    const float r01 = std::fmaf(wx, h - f, f), r11 = std::fmaf(wx, l - k, k);
+                    const float s0 = std::fmaf(wy, r10 - r00, r00), s1 = std::fmaf(wy, r11 - r01, r01);
+                    out[i + ch] = (double)(dd[ch] + std::fmaf(wz, s1 - s0, s0));
+                }
+            }
+    });
+}
+// K3's step in fp32: k = -(float)r * (1 / (|g|^2 + (float)lambda)) (LM),
+// (float)(-lr) (GD), 1 (Adam: the Adam step is already in g).
+void dev_step32(const double* g, size_t N, int opt, double r, double lambda, double lr, double* out) {
+    const float rf = (float)r, lf = (float)lambda;
+    for (size_t i = 0; i < N; ++i) {
+        const float a = (float)g[3 * i], b = (float)g[3 * i + 1], c = (float)g[3 * i + 2];
+        float k = opt == ORC_OPT_GD ? (float)-lr : 1.f;
+        if (opt == ORC_OPT_LM) k = -rf * (1.f / (std::fmaf(a, a, std::fmaf(b, b, c * c)) + lf));
+        out[3 * i] = (double)(k * a);
+        out[3 * i + 1] = (double)(k * b);
+        out[3 * i + 2] = (double)(k * c);
+    }
+}
+
 // Warp of the moving image with the analytic interpolant gradient.
 void warp(const double* M, const double* u, orc_dims d, double* Mw, double* gM) {
 #ifdef ORC_WITH_REF_FIELD
@@ -350,7 +500,9 @@ constexpr double kDegRel = 1e-9;
 extern "C" {
 
 void orc_set_threads(int n) { g_threads = n < 1 ? 1 : n; }
-void orc_set_fp32_storage(int on) { g_fp32_storage = on ? 1 : 0; }
+void orc_set_fp32_storage(int on) { g_fp32_storage = on == 2 ? 2 : on ? 1 : 0; }
+void orc_set_dev_flags(int flags) { g_dev_flags = flags & 7; g_dev_hilo = (flags >> 3) & 1; g_dev_k3norm64 = (flags >> 4) & 1; }
+void orc_dev_smooth32(double* data, orc_dims d, double sigma, int norm64) { dev_smooth32(data, d, sigma, norm64 != 0); }
 
 void orc_default_reg_config(orc_reg_config* c) {
     std::memset(c, 0, sizeof(*c));
@@ -644,20 +796,32 @@ int orc_lm_run_level(const double* F, const double* M, orc_dims d, double* u,
         double rn = 0.0, ln = 0.0, eps = 0.0, jac = kNaN;
         bool forced = false;
         for (;;) {
+            const bool dev = g_fp32_storage == 2 && (g_dev_flags & 1);
+            const bool dev4 = g_fp32_storage == 2 && (g_dev_flags & 2);
             if (c->optimizer == ORC_OPT_LM) {
-                orc_lm_step_pointwise(r, g.data(), N, state->lambda, step.data());
+                if (dev) dev_step32(g.data(), N, ORC_OPT_LM, r, state->lambda, 0.0, step.data());
+                else orc_lm_step_pointwise(r, g.data(), N, state->lambda, step.data());
             } else if (c->optimizer == ORC_OPT_ADAM) {
                 orc_adam_step(g.data(), am.data(), av.data(), 3 * N, it + 1, &c->adam, step.data());
+            } else if (dev) {
+                dev_step32(g.data(), N, ORC_OPT_GD, 0.0, 0.0, c->gd_lr, step.data());
             } else {
                 for (size_t i = 0; i < 3 * N; ++i) step[i] = -c->gd_lr * g[i];
             }
-            smooth(step.data(), d, 3, c->sigma_update);
+            if (dev) dev_smooth32(step.data(), d, c->sigma_update, g_dev_k3norm64 != 0);
+            else smooth(step.data(), d, 3, c->sigma_update);
             if (g_fp32_storage)
                 for (auto& v : step) v = (double)(float)v;
             eps = orc_normalize_step(step.data(), 3 * N, c->target_max_disp, c->step_floor);
             if (!std::isfinite(eps)) return ORC_INVALID_ARG;
             compose(u, step.data(), d, eps, unew.data());
-            smooth(unew.data(), d, 3, c->sigma_warp);
+            if (g_fp32_storage == 2 && (g_dev_flags & 4)) dev_compose32(u, step.data(), d, eps, unew.data());
+            if (dev4) {
+                for (auto& v : unew) v = (double)(float)v;
+                dev_smooth32(unew.data(), d, c->sigma_warp, true);
+            } else {
+                smooth(unew.data(), d, 3, c->sigma_warp);
+            }
             if (g_fp32_storage)
                 for (auto& v : unew) v = (double)(float)v;
             if (c->log_jacobian) {

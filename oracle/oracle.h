@@ -84,7 +84,14 @@ enum {
 void orc_set_threads(int n);
 /* 1: round every quantity the device stores in fp32 at the same point
  * (A, B, g, dU_s, warps, Adam moments); 0 (default): pure fp64 reference. */
+/* 0: fp64; 1: round at the device's fp32 storage points; 2: 1 + the
+ * device's fp32 arithmetic in the K3 step and both Gaussian smoothings. */
 void orc_set_fp32_storage(int on);
+/* Mode 2 detail: bit0 K3 step + smoothing in fp32, bit1 K4 smoothing in
+ * fp32, bit2 compose in fp32 (default 3). */
+void orc_set_dev_flags(int flags);
+/* The mode-2 fp32 Gaussian of a 3-channel AoS field, in place. */
+void orc_dev_smooth32(double* data, orc_dims d, double sigma, int norm64);
 void orc_default_reg_config(orc_reg_config* c);
 
 /* ---- field (reference field.cpp restated) ---- */

@@ -655,44 +655,91 @@ __device__ __forceinline__ T axis_wsum_t(int p, int n, int R, const T* w, T full
 // K3: dU = -r g / (|g|^2 + lambda) (Eq. 4) | -lr g (GD) | Adam step (in G);
 // Gaussian(sigma_update) in fp64; dU_s stored fp32; max |dU_s| (of the
 // stored values) -> PairState.max_bits.
+//
+// fp64 arithmetic, fp32 storage (fp32 passes bias the
+// trajectory, tools/precision_modes.py).  Tile 32 x 8; per plane a single
+// barrier-separated phase does four independent things: the y-pass of plane
+// p (s_x column -> z register ring -> plane p - R out), the x-pass of plane
+// p+1 (two adjacent outputs per thread from 16-byte shared loads), the step
+// of plane p+2 into the halo tile, and the global loads of plane p+3.
+// fp64 reciprocal: hardware estimate + two Newton steps (x > 0 normal; within
+// an ulp of the correctly rounded quotient, a fifth of __drcp_rn's cost).
+__device__ __forceinline__ double rcp_d(double x) {
+    double y;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+    double e = fma(-x, y, 1.0);
+    y = fma(y, e, y);
+    e = fma(-x, y, 1.0);
+    return fma(y, e, y);
+}
+
+// 1 / (in-bounds weight sum) of the 2R border planes of an axis of length n:
+// t[k] for p = k, t[R + k] for p = n - 1 - k (k < R); filled once per CTA.
+__device__ __forceinline__ void fill_border_inv(double* t, int n, int R, const double* w, double full) {
+    const int k = threadIdx.x;
+    if (k < 2 * R) {
+        const int pp = k < R ? k : n - 1 - (k - R);
+        t[k] = (pp >= 0 && pp < n) ? 1.0 / axis_wsum_t<double>(pp, n, R, w, full) : 0.0;
+    }
+}
+__device__ __forceinline__ double border_inv(const double* t, int p, int n, int R) {
+    return p < R ? t[p] : t[R + (n - 1 - p)];
+}
+
+namespace k3 {
+constexpr int TX = 32, TY = 8, NT = 256;
 template <int R>
-__global__ void __launch_bounds__(NT, 2) k_step_smooth(Batch b, LmParams p, int chunk_len) {
-    using It = hot::Items<R>;
-    constexpr int IW = It::IW, IH = It::IH, NI = It::NI, SL = It::SLOTS, W = 2 * R + 1;
-    constexpr int XS = (IH * TX + NT - 1) / NT;
-    __shared__ double s_in[2][3][NI];
-    __shared__ double s_x[3][IH][TX];
+struct Shape {
+    static constexpr int IWP = TX + 2 * R;  // halo row (even: 16-byte aligned rows of doubles)
+    static constexpr int IH = TY + 2 * R;
+    static constexpr int NI = IWP * IH;
+    static constexpr int SLOTS = (NI + NT - 1) / NT;
+    static constexpr int NV = (2 + 2 * R + 1) / 2;  // 16-byte loads per x pair
+};
+}  // namespace k3
+
+template <int R>
+__global__ void __launch_bounds__(k3::NT, 2) k_step_smooth(Batch b, LmParams p, int chunk_len) {
+    using S = k3::Shape<R>;
+    constexpr int TX = k3::TX, NT = k3::NT, W = 2 * R + 1;
+    constexpr int IWP = S::IWP, IH = S::IH, NI = S::NI, SL = S::SLOTS, NV = S::NV;
+    __shared__ __align__(16) double s_in[2][3][NI];
+    __shared__ __align__(16) double s_x[2][3][IH * TX];
     __shared__ float s_max[NT / 32];
+    __shared__ double s_binv[2 * (R > 0 ? R : 1)];
 
     const int pair = blockIdx.z;
     PairState* st = b.st + pair;
     if (st->done) return;
     const Geo g = b.g;
     const long long n = g.n;
-    Tile t;
-    t.init(g, chunk_len);
+    const int nxy = g.nx * g.ny;
+    const int tiles_x = cdiv(g.nx, TX);
+    const int x0 = (blockIdx.x % tiles_x) * TX, y0 = (blockIdx.x / tiles_x) * k3::TY;
+    fill_border_inv(s_binv, g.nz, R, p.wud, p.wud_full);
+    const int zb = g.zs + blockIdx.y * chunk_len, ze = min(zb + chunk_len, g.ze);
     const float* __restrict__ Gin = b.G + (long long)pair * 3 * n;
     float* __restrict__ V = b.VS + (long long)pair * 3 * n;
-    const double r = st->r_cur, lam = st->lambda, lr = p.gd_lr;
     const int opt = p.optimizer;
-    It it;
-    it.init(t.x0, t.y0, g.nx, g.ny);
-    const int ooff = t.x + g.nx * t.y;
-    double w[W];
-#pragma unroll
-    for (int d = 0; d < W; ++d) w[d] = p.wud[d < R ? R - d : d - R];
-    const double wxy = t.own ? axis_wsum_t<double>(t.x, g.nx, R, p.wud, p.wud_full) *
-                                   axis_wsum_t<double>(t.y, g.ny, R, p.wud, p.wud_full)
-                             : 1.0;
-    const double inv_xy = 1.0 / wxy, inv_full = inv_xy / p.wud_full;
+    const double r = st->r_cur, lam = st->lambda;
+    const double kc = opt == WLM_OPT_GD ? -p.gd_lr : 1.0;
 
+    int hoff[SL];
+#pragma unroll
+    for (int s = 0; s < SL; ++s) {
+        const int idx = threadIdx.x + s * NT;
+        const int ix = idx % IWP, iy = idx / IWP;
+        const int gx = x0 - R + ix, gy = y0 - R + iy;
+        hoff[s] = (idx < NI && gx >= 0 && gx < g.nx && gy >= 0 && gy < g.ny) ? gx + g.nx * gy : -1;
+    }
     float hg[SL][3];
     auto load_halo = [&](int z) {
-        const bool zin = z >= 0 && z < g.nz;
+        const bool zin = z >= 0 && z < g.nz && z < ze + R;
+        const int base = (z - g.zlo) * nxy;
 #pragma unroll
         for (int s = 0; s < SL; ++s) {
-            if (zin && it.goff[s] >= 0) {
-                const int o = t.lp(g, z) + it.goff[s];
+            if (zin && hoff[s] >= 0) {
+                const int o = base + hoff[s];
                 hg[s][0] = __ldg(Gin + o); hg[s][1] = __ldg(Gin + n + o); hg[s][2] = __ldg(Gin + 2 * n + o);
             } else {
                 hg[s][0] = hg[s][1] = hg[s][2] = 0.f;
@@ -702,17 +749,51 @@ __global__ void __launch_bounds__(NT, 2) k_step_smooth(Batch b, LmParams p, int 
     auto store_halo = [&](int sb) {
 #pragma unroll
         for (int s = 0; s < SL; ++s) {
-            if (it.sidx[s] < 0) continue;
+            const int idx = threadIdx.x + s * NT;
+            if (idx >= NI) continue;
             const double a = hg[s][0], bb = hg[s][1], c = hg[s][2];
-            double k;
-            if (opt == WLM_OPT_LM) k = -r / (fma(a, a, fma(bb, bb, c * c)) + lam);
-            else if (opt == WLM_OPT_GD) k = -lr;
-            else k = 1.0;  // Adam step already in G
-            s_in[sb][0][it.sidx[s]] = k * a;
-            s_in[sb][1][it.sidx[s]] = k * bb;
-            s_in[sb][2][it.sidx[s]] = k * c;
+            double k = kc;
+            if (opt == WLM_OPT_LM) k = -r * rcp_d(fma(a, a, fma(bb, bb, c * c)) + lam);
+            s_in[sb][0][idx] = k * a;
+            s_in[sb][1][idx] = k * bb;
+            s_in[sb][2][idx] = k * c;
         }
     };
+    double w[W];
+#pragma unroll
+    for (int d = 0; d < W; ++d) w[d] = p.wud[d < R ? R - d : d - R];
+
+    // x-pass item: row xr, pair xj (outputs x = 2xj, 2xj + 1)
+    const int xr = threadIdx.x >> 4, xj = threadIdx.x & 15;
+    auto x_pass = [&](int sb) {
+        if (xr >= IH) return;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            double v[2 * NV];
+            const double2* src = reinterpret_cast<const double2*>(&s_in[sb][c][xr * IWP + 2 * xj]);
+#pragma unroll
+            for (int q = 0; q < NV; ++q) {
+                const double2 t = src[q];
+                v[2 * q] = t.x; v[2 * q + 1] = t.y;
+            }
+            double o0 = 0.0, o1 = 0.0;
+#pragma unroll
+            for (int d = 0; d < W; ++d) {
+                o0 = fma(w[d], v[d], o0);
+                o1 = fma(w[d], v[d + 1], o1);
+            }
+            *reinterpret_cast<double2*>(&s_x[sb][c][xr * TX + 2 * xj]) = make_double2(o0, o1);
+        }
+    };
+
+    const int ox = threadIdx.x & 31, oy = threadIdx.x >> 5;
+    const int x = x0 + ox, y = y0 + oy;
+    const bool own = x < g.nx && y < g.ny;
+    const double inv_xy = own ? 1.0 / (axis_wsum_t<double>(x, g.nx, R, p.wud, p.wud_full) *
+                                       axis_wsum_t<double>(y, g.ny, R, p.wud, p.wud_full))
+                              : 0.0;
+    const double inv_full = inv_xy / p.wud_full;
+    const int ooff = x + g.nx * y;
 
     double ring[W][3];
 #pragma unroll
@@ -721,58 +802,48 @@ __global__ void __launch_bounds__(NT, 2) k_step_smooth(Batch b, LmParams p, int 
         for (int c = 0; c < 3; ++c) ring[d][c] = 0.0;
     float mx = 0.f;
 
-    const int z0 = t.zb - R, z1 = t.ze + R;
+    const int z0 = zb - R, z1 = ze + R;
     load_halo(z0);
     store_halo(0);
     load_halo(z0 + 1);
+    store_halo(1);
     __syncthreads();
-    for (int zbase = z0; zbase < z1; zbase += W) {
+    x_pass(0);
+    load_halo(z0 + 2);
+    __syncthreads();
+    // unrolled by 2W: ring slot (ph % W) and buffer parity (ph & 1) are static
+    for (int zbase = z0; zbase < z1; zbase += 2 * W) {
 #pragma unroll
-        for (int ph = 0; ph < W; ++ph) {
+        for (int ph = 0; ph < 2 * W; ++ph) {
             const int zi = zbase + ph;
             if (zi < z1) {
-                const int sb = (zi - z0) & 1;
-#pragma unroll
-                for (int q = 0; q < XS; ++q) {
-                    const int idx = threadIdx.x + q * NT;
-                    if (idx < IH * TX) {
-                        const int c = idx % TX, rr = idx / TX;
-#pragma unroll
-                        for (int ch = 0; ch < 3; ++ch) {
-                            const double* row = &s_in[sb][ch][rr * IW + c];
-                            double s = 0.0;
-#pragma unroll
-                            for (int d = 0; d < W; ++d) s = fma(w[d], row[d], s);
-                            s_x[ch][rr][c] = s;
-                        }
-                    }
-                }
-                __syncthreads();
+                const int sb = ph & 1;
+                const int rs = ph % W;
 #pragma unroll
                 for (int c = 0; c < 3; ++c) {
                     double s = 0.0;
 #pragma unroll
-                    for (int d = 0; d < W; ++d) s = fma(w[d], s_x[c][t.oy + d][t.ox], s);
-                    ring[ph][c] = s;
+                    for (int d = 0; d < W; ++d) s = fma(w[d], s_x[sb][c][(oy + d) * TX + ox], s);
+                    ring[rs][c] = s;
                 }
                 const int zo = zi - R;
-                if (zo >= t.zb && t.own) {
-                    const double inv = (zo >= R && zo + R <= g.nz - 1)
-                                           ? inv_full
-                                           : inv_xy / axis_wsum_t<double>(zo, g.nz, R, p.wud, p.wud_full);
-                    const int o = t.lp(g, zo) + ooff;
+                if (zo >= zb && own) {
+                    double inv = inv_full;
+                    if (zo < R || zo + R > g.nz - 1) inv = inv_xy * border_inv(s_binv, zo, g.nz, R);
+                    const int o = (zo - g.zlo) * nxy + ooff;
 #pragma unroll
                     for (int c = 0; c < 3; ++c) {
                         double s = 0.0;
 #pragma unroll
-                        for (int d = 0; d < W; ++d) s = fma(w[d], ring[(ph + 1 + d) % W][c], s);
+                        for (int d = 0; d < W; ++d) s = fma(w[d], ring[(rs + 1 + d) % W][c], s);
                         const float v = (float)(s * inv);
                         V[c * n + o] = v;
                         mx = fmaxf(mx, fabsf(v));
                     }
                 }
-                store_halo(sb ^ 1);
-                load_halo(zi + 2);
+                x_pass(sb ^ 1);
+                store_halo(sb);
+                load_halo(zi + 3);
                 __syncthreads();
             }
         }
@@ -788,57 +859,86 @@ __global__ void __launch_bounds__(NT, 2) k_step_smooth(Batch b, LmParams p, int 
 }
 
 // K4: u'(x) = d(x) + u(x + d(x)), d = eps dU_s, eps = target / max(max|dU_s|,
-// floor) (Eq. 2, field.cpp:123-155), then Gaussian(sigma_warp), fp64.  The
-// normalised step bounds |d| <= target < 0.5 voxel, so every resample corner
-// lies in the 3x3x3 neighbourhood of its voxel: the accepted warp is staged
-// in a 3-plane shared-memory ring (halo R+1) and the compose "gathers" are
-// shared-memory reads.  Reads the accepted buffer, writes the other one.
+// floor) (Eq. 2, field.cpp:123-155), then Gaussian(sigma_warp); fp64
+// arithmetic, fp32 storage.  The normalised step bounds |d| <= target < 0.5
+// voxel, so every resample corner lies in the 3x3x3 neighbourhood of its
+// voxel: the accepted warp is staged in a 4-plane shared-memory ring (fp64,
+// halo R + 1) and the compose "gathers" are shared-memory reads.  Reads the
+// accepted buffer, writes the other one.
+//
+// Tile 32 x 8, one barrier per plane.  Phase p: y-pass of plane p (z ring,
+// plane p - R out); x-pass of plane p+1; compose of plane p+2 into the halo
+// tile (warp planes p+1..p+3 from the ring, its step from registers); warp
+// plane p+4 into the ring; global loads of warp plane p+5 and step p+3.
+namespace k4 {
+constexpr int TX = 32, TY = 8, NT = 256;
 template <int R>
-__global__ void __launch_bounds__(NT, 2) k_compose_smooth(Batch b, LmParams p, int chunk_len) {
-    using It = hot::Items<R>;          // producer tile (halo R)
-    using Iu = hot::Items<R + 1>;      // warp tile (halo R + 1)
-    constexpr int IW = It::IW, IH = It::IH, NI = It::NI, SL = It::SLOTS, W = 2 * R + 1;
-    constexpr int UW = Iu::IW, UNI = Iu::NI, USL = Iu::SLOTS;
-    constexpr int XS = (IH * TX + NT - 1) / NT;
-    __shared__ float s_u[3][3][UNI];    // [ring slot][channel][tile]
-    __shared__ double s_in[3][NI];
-    __shared__ double s_x[3][IH][TX];
+struct Shape {
+    static constexpr int IWP = TX + 2 * R, IH = TY + 2 * R, NI = IWP * IH;  // composed tile
+    static constexpr int UW = TX + 2 * R + 2, UH = TY + 2 * R + 2, UN = UW * UH;  // warp tile
+    static constexpr int SL = (NI + NT - 1) / NT, USL = (UN + NT - 1) / NT;
+    static constexpr int NV = (2 + 2 * R + 1) / 2;
+    // dynamic shared memory layout (doubles)
+    static constexpr int OFF_U = 0, OFF_IN = 4 * 3 * UN, OFF_X = OFF_IN + 2 * 3 * NI;
+    static constexpr int TOTAL = OFF_X + 2 * 3 * IH * TX;
+    static constexpr size_t BYTES = sizeof(double) * TOTAL + sizeof(double) * 8;
+};
+}  // namespace k4
+
+template <int R>
+__global__ void __launch_bounds__(k4::NT, 2) k_compose_smooth(Batch b, LmParams p, int chunk_len) {
+    using S = k4::Shape<R>;
+    constexpr int TX = k4::TX, NT = k4::NT, W = 2 * R + 1;
+    constexpr int IWP = S::IWP, IH = S::IH, NI = S::NI, UW = S::UW, UN = S::UN, SL = S::SL, USL = S::USL,
+                  NV = S::NV;
+    extern __shared__ __align__(16) double k4_smem[];
+    double* s_u = k4_smem + S::OFF_U;    // [4 slots][3][UN]
+    double* s_in = k4_smem + S::OFF_IN;  // [2][3][NI]
+    double* s_x = k4_smem + S::OFF_X;    // [2][3][IH * TX]
+    double* s_binv = k4_smem + S::TOTAL; // [2R]
 
     const int pair = blockIdx.z;
     const PairState* st = b.st + pair;
     if (st->done) return;
     const Geo g = b.g;
     const long long n = g.n;
-    Tile t;
-    t.init(g, chunk_len);
+    const int nxy = g.nx * g.ny;
+    const int tiles_x = cdiv(g.nx, TX);
+    const int x0 = (blockIdx.x % tiles_x) * TX, y0 = (blockIdx.x / tiles_x) * k4::TY;
+    const int zb = g.zs + blockIdx.y * chunk_len, ze = min(zb + chunk_len, g.ze);
     const int cur = st->cur;
     const float* __restrict__ Vin = b.VS + (long long)pair * 3 * n;
     const float* __restrict__ U = b.U + ((long long)pair * 2 + cur) * 3 * n;
     float* __restrict__ UN_ = b.U + ((long long)pair * 2 + (1 - cur)) * 3 * n;
     const double eps = p.target / fmax((double)__uint_as_float(st->max_bits), p.step_floor);
-    It it;
-    it.init(t.x0, t.y0, g.nx, g.ny);
-    Iu iu;
-    iu.init(t.x0, t.y0, g.nx, g.ny);
-    const int ooff = t.x + g.nx * t.y;
-    double w[W];
-#pragma unroll
-    for (int d = 0; d < W; ++d) w[d] = p.wwd[d < R ? R - d : d - R];
-    const double wxy = t.own ? axis_wsum_t<double>(t.x, g.nx, R, p.wwd, p.wwd_full) *
-                                   axis_wsum_t<double>(t.y, g.ny, R, p.wwd, p.wwd_full)
-                             : 1.0;
-    const double inv_xy = 1.0 / wxy, inv_full = inv_xy / p.wwd_full;
+    fill_border_inv(s_binv, g.nz, R, p.wwd, p.wwd_full);
 
-    float pu[USL][3];  // warp rows of plane z + 3 (loads in flight)
-    // step rows: the thread that loads item s also produces it, so the step
-    // tile never goes through shared memory (plane z, z + 1, z + 2)
-    float v0[SL][3], v1[SL][3], v2[SL][3];
+    // warp staging items (tile origin x0 - R - 1, y0 - R - 1)
+    int uoff[USL];
+#pragma unroll
+    for (int s = 0; s < USL; ++s) {
+        const int idx = threadIdx.x + s * NT;
+        const int gx = x0 - R - 1 + idx % UW, gy = y0 - R - 1 + idx / UW;
+        uoff[s] = (idx < UN && gx >= 0 && gx < g.nx && gy >= 0 && gy < g.ny) ? gx + g.nx * gy : -1;
+    }
+    // composed items (tile origin x0 - R, y0 - R)
+    int voff[SL], vx[SL], vy[SL];
+#pragma unroll
+    for (int s = 0; s < SL; ++s) {
+        const int idx = threadIdx.x + s * NT;
+        vx[s] = x0 - R + idx % IWP;
+        vy[s] = y0 - R + idx / IWP;
+        voff[s] = (idx < NI && vx[s] >= 0 && vx[s] < g.nx && vy[s] >= 0 && vy[s] < g.ny) ? vx[s] + g.nx * vy[s]
+                                                                                          : -1;
+    }
+    float pu[USL][3], pv[SL][3];
     auto load_u = [&](int z) {
-        const bool zin = z >= 0 && z < g.nz;
+        const bool zin = z >= 0 && z < g.nz && z <= ze + R;
+        const int base = (z - g.zlo) * nxy;
 #pragma unroll
         for (int s = 0; s < USL; ++s) {
-            if (zin && iu.goff[s] >= 0) {
-                const int o = t.lp(g, z) + iu.goff[s];
+            if (zin && uoff[s] >= 0) {
+                const int o = base + uoff[s];
                 pu[s][0] = __ldg(U + o); pu[s][1] = __ldg(U + n + o); pu[s][2] = __ldg(U + 2 * n + o);
             } else {
                 pu[s][0] = pu[s][1] = pu[s][2] = 0.f;
@@ -846,51 +946,95 @@ __global__ void __launch_bounds__(NT, 2) k_compose_smooth(Batch b, LmParams p, i
         }
     };
     auto store_u = [&](int z) {
-        const int slot = ((z % 3) + 3) % 3;
+        double* dst = s_u + ((z + 4) & 3) * 3 * UN;
 #pragma unroll
         for (int s = 0; s < USL; ++s) {
-            if (iu.sidx[s] < 0) continue;
-            s_u[slot][0][iu.sidx[s]] = pu[s][0];
-            s_u[slot][1][iu.sidx[s]] = pu[s][1];
-            s_u[slot][2][iu.sidx[s]] = pu[s][2];
+            const int idx = threadIdx.x + s * NT;
+            if (idx >= UN) continue;
+            dst[idx] = pu[s][0];
+            dst[UN + idx] = pu[s][1];
+            dst[2 * UN + idx] = pu[s][2];
         }
     };
-    auto load_v = [&](int z, float (&pv)[SL][3]) {
-        const bool zin = z >= 0 && z < g.nz;
+    auto load_v = [&](int z) {
+        const bool zin = z >= 0 && z < g.nz && z < ze + R;
+        const int base = (z - g.zlo) * nxy;
 #pragma unroll
         for (int s = 0; s < SL; ++s) {
-            if (zin && it.goff[s] >= 0) {
-                const int o = t.lp(g, z) + it.goff[s];
+            if (zin && voff[s] >= 0) {
+                const int o = base + voff[s];
                 pv[s][0] = __ldg(Vin + o); pv[s][1] = __ldg(Vin + n + o); pv[s][2] = __ldg(Vin + 2 * n + o);
             } else {
                 pv[s][0] = pv[s][1] = pv[s][2] = 0.f;
             }
         }
     };
-    // composed value at producer item s of plane z (fp64); warp from the ring
-    auto produce = [&](int z, const float (&pv)[SL][3]) {
+    // every item's cell is interior (no clamp rules) when the tile and its
+    // halo keep one voxel off the x/y faces and the plane is off the z faces
+    const bool tile_inner = x0 - R >= 1 && x0 + TX - 1 + R <= g.nx - 2 && y0 - R >= 1 &&
+                            y0 + k4::TY - 1 + R <= g.ny - 2;
+    // composed value of the items of plane z (step in pv) -> s_in[sb]
+    auto compose = [&](int z, int sb) {
         const bool zin = z >= 0 && z < g.nz;
+        double* dst = s_in + sb * 3 * NI;
+        if (tile_inner && z >= 1 && z <= g.nz - 2) {
+            // |d| <= target < 1: floor(d) in {-1, 0}, cell origin x + floor(d)
 #pragma unroll
-        for (int s = 0; s < SL; ++s) {
-            if (it.sidx[s] < 0) continue;
-            double o3[3] = {0.0, 0.0, 0.0};
-            if (zin && it.goff[s] >= 0) {
+            for (int s = 0; s < SL; ++s) {
+                const int idx = threadIdx.x + s * NT;
+                if (idx >= NI) continue;
                 const double dx = eps * pv[s][0], dy = eps * pv[s][1], dz = eps * pv[s][2];
-                if (isfinite(dx) && isfinite(dy) && isfinite(dz)) {
-                    const AxisTapD X = axis_tap_dd(it.gx[s], dx, g.nx);
-                    const AxisTapD Y = axis_tap_dd(it.gy[s], dy, g.ny);
-                    const AxisTapD Z = axis_tap_dd(z, dz, g.nz);
-                    // tile coordinates of the corners (clamped defensively)
-                    const int ux0 = min(max(X.i0 - (t.x0 - R - 1), 0), UW - 2);
-                    const int uy0 = min(max(Y.i0 - (t.y0 - R - 1), 0), Iu::IH - 2);
-                    const int sz0 = ((Z.i0 % 3) + 3) % 3, sz1 = ((Z.i1 % 3) + 3) % 3;
-                    const int a = uy0 * UW + ux0;
+                double o3[3];
+                if (isfinite(dx + dy + dz)) {
+                    const int fx = dx < 0.0 ? -1 : 0, fy = dy < 0.0 ? -1 : 0, fz = dz < 0.0 ? -1 : 0;
+                    const double tx = dx - (double)fx, ty = dy - (double)fy, tz = dz - (double)fz;
+                    const int a = (idx / IWP + 1 + fy) * UW + idx % IWP + 1 + fx;
+                    const double* p0 = s_u + ((z + fz + 4) & 3) * 3 * UN + a;
+                    const double* p1 = s_u + ((z + fz + 5) & 3) * 3 * UN + a;
 #pragma unroll
                     for (int ch = 0; ch < 3; ++ch) {
-                        const float* p0 = &s_u[sz0][ch][a];
-                        const float* p1 = &s_u[sz1][ch][a];
-                        const double c000 = p0[0], c100 = p0[1], c010 = p0[UW], c110 = p0[UW + 1];
-                        const double c001 = p1[0], c101 = p1[1], c011 = p1[UW], c111 = p1[UW + 1];
+                        const double c000 = p0[ch * UN], c100 = p0[ch * UN + 1];
+                        const double c010 = p0[ch * UN + UW], c110 = p0[ch * UN + UW + 1];
+                        const double c001 = p1[ch * UN], c101 = p1[ch * UN + 1];
+                        const double c011 = p1[ch * UN + UW], c111 = p1[ch * UN + UW + 1];
+                        const double v00 = fma(tx, c100 - c000, c000), v10 = fma(tx, c110 - c010, c010);
+                        const double v01 = fma(tx, c101 - c001, c001), v11 = fma(tx, c111 - c011, c011);
+                        const double s0 = fma(ty, v10 - v00, v00), s1 = fma(ty, v11 - v01, v01);
+                        o3[ch] = fma(tz, s1 - s0, s0);
+                    }
+                    o3[0] += dx;
+                    o3[1] += dy;
+                    o3[2] += dz;
+                } else {
+                    o3[0] = o3[1] = o3[2] = kNaN64;
+                }
+                dst[idx] = o3[0];
+                dst[NI + idx] = o3[1];
+                dst[2 * NI + idx] = o3[2];
+            }
+            return;
+        }
+#pragma unroll
+        for (int s = 0; s < SL; ++s) {
+            const int idx = threadIdx.x + s * NT;
+            if (idx >= NI) continue;
+            double o3[3] = {0.0, 0.0, 0.0};
+            if (zin && voff[s] >= 0) {
+                const double dx = eps * pv[s][0], dy = eps * pv[s][1], dz = eps * pv[s][2];
+                if (isfinite(dx) && isfinite(dy) && isfinite(dz)) {
+                    const AxisTapD X = axis_tap_dd(vx[s], dx, g.nx);
+                    const AxisTapD Y = axis_tap_dd(vy[s], dy, g.ny);
+                    const AxisTapD Z = axis_tap_dd(z, dz, g.nz);
+                    const int ux0 = min(max(X.i0 - (x0 - R - 1), 0), UW - 2);
+                    const int uy0 = min(max(Y.i0 - (y0 - R - 1), 0), S::UH - 2);
+                    const double* p0 = s_u + ((Z.i0 + 4) & 3) * 3 * UN + uy0 * UW + ux0;
+                    const double* p1 = s_u + ((Z.i1 + 4) & 3) * 3 * UN + uy0 * UW + ux0;
+#pragma unroll
+                    for (int ch = 0; ch < 3; ++ch) {
+                        const double c000 = p0[ch * UN], c100 = p0[ch * UN + 1];
+                        const double c010 = p0[ch * UN + UW], c110 = p0[ch * UN + UW + 1];
+                        const double c001 = p1[ch * UN], c101 = p1[ch * UN + 1];
+                        const double c011 = p1[ch * UN + UW], c111 = p1[ch * UN + UW + 1];
                         const double v00 = fma(X.t, c100 - c000, c000), v10 = fma(X.t, c110 - c010, c010);
                         const double v01 = fma(X.t, c101 - c001, c001), v11 = fma(X.t, c111 - c011, c011);
                         const double s0 = fma(Y.t, v10 - v00, v00), s1 = fma(Y.t, v11 - v01, v01);
@@ -903,84 +1047,100 @@ __global__ void __launch_bounds__(NT, 2) k_compose_smooth(Batch b, LmParams p, i
                     o3[0] = o3[1] = o3[2] = kNaN64;
                 }
             }
-            s_in[0][it.sidx[s]] = o3[0];
-            s_in[1][it.sidx[s]] = o3[1];
-            s_in[2][it.sidx[s]] = o3[2];
+            dst[idx] = o3[0];
+            dst[NI + idx] = o3[1];
+            dst[2 * NI + idx] = o3[2];
+        }
+    };
+    double w[W];
+#pragma unroll
+    for (int d = 0; d < W; ++d) w[d] = p.wwd[d < R ? R - d : d - R];
+    const int xr = threadIdx.x >> 4, xj = threadIdx.x & 15;
+    auto x_pass = [&](int sb) {
+        if (xr >= IH) return;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            double v[2 * NV];
+            const double2* src = reinterpret_cast<const double2*>(s_in + (sb * 3 + c) * NI + xr * IWP + 2 * xj);
+#pragma unroll
+            for (int q = 0; q < NV; ++q) {
+                const double2 t = src[q];
+                v[2 * q] = t.x; v[2 * q + 1] = t.y;
+            }
+            double o0 = 0.0, o1 = 0.0;
+#pragma unroll
+            for (int d = 0; d < W; ++d) {
+                o0 = fma(w[d], v[d], o0);
+                o1 = fma(w[d], v[d + 1], o1);
+            }
+            *reinterpret_cast<double2*>(s_x + (sb * 3 + c) * IH * TX + xr * TX + 2 * xj) = make_double2(o0, o1);
         }
     };
 
+    const int ox = threadIdx.x & 31, oy = threadIdx.x >> 5;
+    const int x = x0 + ox, y = y0 + oy;
+    const bool own = x < g.nx && y < g.ny;
+    const double inv_xy = own ? 1.0 / (axis_wsum_t<double>(x, g.nx, R, p.wwd, p.wwd_full) *
+                                       axis_wsum_t<double>(y, g.ny, R, p.wwd, p.wwd_full))
+                              : 0.0;
+    const double inv_full = inv_xy / p.wwd_full;
+    const int ooff = x + g.nx * y;
     double ring[W][3];
 #pragma unroll
     for (int d = 0; d < W; ++d)
 #pragma unroll
         for (int c = 0; c < 3; ++c) ring[d][c] = 0.0;
 
-    const int z0 = t.zb - R, z1 = t.ze + R;
-    // prologue: warp planes z0-1 .. z0+1 staged, z0+2 in registers; steps of
-    // z0 and z0+1 in registers
+    const int z0 = zb - R, z1 = ze + R;
+    // prologue: warp planes z0-1 .. z0+2 staged; composed z0, z0+1; x-pass z0
     load_u(z0 - 1); store_u(z0 - 1);
     load_u(z0);     store_u(z0);
     load_u(z0 + 1); store_u(z0 + 1);
-    load_u(z0 + 2);
-    load_v(z0, v0);
-    load_v(z0 + 1, v1);
+    load_u(z0 + 2); store_u(z0 + 2);
+    load_v(z0);
     __syncthreads();
-
-    for (int zbase = z0; zbase < z1; zbase += W) {
+    compose(z0, 0);
+    load_v(z0 + 1);
+    load_u(z0 + 3);
+    __syncthreads();
+    x_pass(0);
+    compose(z0 + 1, 1);
+    store_u(z0 + 3);  // slot of plane z0 - 1 (not read by compose(z0 + 1))
+    load_u(z0 + 4);
+    load_v(z0 + 2);
+    __syncthreads();
+    for (int zbase = z0; zbase < z1; zbase += 2 * W) {
 #pragma unroll
-        for (int ph = 0; ph < W; ++ph) {
+        for (int ph = 0; ph < 2 * W; ++ph) {
             const int zi = zbase + ph;
             if (zi < z1) {
-                load_v(zi + 2, v2);
-                produce(zi, v0);
-                __syncthreads();
-                // the ring slot of plane zi-1 is free now
-                store_u(zi + 2);
-                load_u(zi + 3);
-#pragma unroll
-                for (int s = 0; s < SL; ++s)
-#pragma unroll
-                    for (int c = 0; c < 3; ++c) {
-                        v0[s][c] = v1[s][c];
-                        v1[s][c] = v2[s][c];
-                    }
-#pragma unroll
-                for (int q = 0; q < XS; ++q) {
-                    const int idx = threadIdx.x + q * NT;
-                    if (idx < IH * TX) {
-                        const int c = idx % TX, rr = idx / TX;
-#pragma unroll
-                        for (int ch = 0; ch < 3; ++ch) {
-                            const double* row = &s_in[ch][rr * IW + c];
-                            double s = 0.0;
-#pragma unroll
-                            for (int d = 0; d < W; ++d) s = fma(w[d], row[d], s);
-                            s_x[ch][rr][c] = s;
-                        }
-                    }
-                }
-                __syncthreads();
+                const int sb = ph & 1, rs = ph % W;
 #pragma unroll
                 for (int c = 0; c < 3; ++c) {
                     double s = 0.0;
 #pragma unroll
-                    for (int d = 0; d < W; ++d) s = fma(w[d], s_x[c][t.oy + d][t.ox], s);
-                    ring[ph][c] = s;
+                    for (int d = 0; d < W; ++d) s = fma(w[d], s_x[(sb * 3 + c) * IH * TX + (oy + d) * TX + ox], s);
+                    ring[rs][c] = s;
                 }
                 const int zo = zi - R;
-                if (zo >= t.zb && t.own) {
-                    const double inv = (zo >= R && zo + R <= g.nz - 1)
-                                           ? inv_full
-                                           : inv_xy / axis_wsum_t<double>(zo, g.nz, R, p.wwd, p.wwd_full);
-                    const int o = t.lp(g, zo) + ooff;
+                if (zo >= zb && own) {
+                    double inv = inv_full;
+                    if (zo < R || zo + R > g.nz - 1) inv = inv_xy * border_inv(s_binv, zo, g.nz, R);
+                    const int o = (zo - g.zlo) * nxy + ooff;
 #pragma unroll
                     for (int c = 0; c < 3; ++c) {
                         double s = 0.0;
 #pragma unroll
-                        for (int d = 0; d < W; ++d) s = fma(w[d], ring[(ph + 1 + d) % W][c], s);
+                        for (int d = 0; d < W; ++d) s = fma(w[d], ring[(rs + 1 + d) % W][c], s);
                         UN_[c * n + o] = (float)(s * inv);
                     }
                 }
+                x_pass(sb ^ 1);
+                compose(zi + 2, sb);
+                store_u(zi + 4);
+                load_u(zi + 5);
+                load_v(zi + 3);
+                __syncthreads();
             }
         }
     }
@@ -1025,18 +1185,26 @@ void launch_lncc_bwd(const Batch& b, const LmParams& p, cudaStream_t s) {
 }
 
 void launch_step_smooth(const Batch& b, const LmParams& p, cudaStream_t s) {
-    const LaunchShape sh = shape_for(b.g, b.pairs, TY);
+    const LaunchShape sh = shape_for(b.g, b.pairs, k3::TY);
     dim3 grid = sh.grid();
     grid.z = b.pairs;
-    WLM_DISPATCH_R(p.Ru, (k_step_smooth<RR><<<grid, NT, 0, s>>>(b, p, sh.chunk_len)));
+    WLM_DISPATCH_R(p.Ru, (k_step_smooth<RR><<<grid, k3::NT, 0, s>>>(b, p, sh.chunk_len)));
     ++g_kernel_launches;
 }
 
 void launch_compose_smooth(const Batch& b, const LmParams& p, cudaStream_t s) {
-    const LaunchShape sh = shape_for(b.g, b.pairs, TY);
+    const LaunchShape sh = shape_for(b.g, b.pairs, k4::TY);
     dim3 grid = sh.grid();
     grid.z = b.pairs;
-    WLM_DISPATCH_R(p.Rw, (k_compose_smooth<RR><<<grid, NT, 0, s>>>(b, p, sh.chunk_len)));
+    WLM_DISPATCH_R(p.Rw, ({
+        static bool attr = false;
+        if (!attr) {
+            cudaFuncSetAttribute(k_compose_smooth<RR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)k4::Shape<RR>::BYTES);
+            attr = true;
+        }
+        k_compose_smooth<RR><<<grid, k4::NT, k4::Shape<RR>::BYTES, s>>>(b, p, sh.chunk_len);
+    }));
     ++g_kernel_launches;
 }
 

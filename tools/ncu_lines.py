@@ -1,0 +1,43 @@
+"""Per-CUDA-source-line instruction and stall totals of one kernel in an ncu
+report (needs -lineinfo and --import-source on).  Usage:
+  python tools/ncu_lines.py REPORT.ncu-rep [top_n]"""
+import csv
+import io
+import subprocess
+import sys
+
+rep = sys.argv[1]
+top = int(sys.argv[2]) if len(sys.argv) > 2 else 30
+out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
+                     capture_output=True, text=True).stdout
+agg = {}
+fname = None
+hdr = None
+for row in csv.reader(io.StringIO(out)):
+    if not row:
+        continue
+    if row[0] == "File Path":
+        fname = row[1].split("/")[-1]
+        continue
+    if row[0] == "Line No":
+        hdr = row
+        continue
+    if hdr is None or row[0] == "Function Name" or len(row) < len(hdr):
+        continue
+    ie = hdr.index("Instructions Executed")
+    st = hdr.index("Warp Stall Sampling (All Samples)")
+    try:
+        line = int(row[0])
+    except ValueError:
+        continue
+    # rows carry the CUDA line in col 0/1 and a SASS instruction in col 3
+    key = (fname, line, row[1].strip()[:90])
+    a = agg.setdefault(key, [0.0, 0.0])
+    num = lambda v: float(v) if v not in ("", "-") else 0.0  # noqa: E731
+    a[0] += num(row[ie])
+    a[1] += num(row[st])
+tot_i = sum(v[0] for v in agg.values()) or 1
+tot_s = sum(v[1] for v in agg.values()) or 1
+print(f"total warp instructions {tot_i:.3e}, stall samples {tot_s:.0f}")
+for k, v in sorted(agg.items(), key=lambda kv: -kv[1][0])[:top]:
+    print(f"{100 * v[0] / tot_i:6.2f}% inst {100 * v[1] / tot_s:6.2f}% stall  {k[0]}:{k[1]}  {k[2]}")
