@@ -746,7 +746,7 @@ __global__ void __launch_bounds__(k3::NT, 2) k_step_smooth(Batch b, LmParams p, 
             }
         }
     };
-    auto store_halo = [&](int sb) {
+    auto store_halo = [&](double* dst) {
 #pragma unroll
         for (int s = 0; s < SL; ++s) {
             const int idx = threadIdx.x + s * NT;
@@ -754,9 +754,9 @@ __global__ void __launch_bounds__(k3::NT, 2) k_step_smooth(Batch b, LmParams p, 
             const double a = hg[s][0], bb = hg[s][1], c = hg[s][2];
             double k = kc;
             if (opt == WLM_OPT_LM) k = -r * rcp_d(fma(a, a, fma(bb, bb, c * c)) + lam);
-            s_in[sb][0][idx] = k * a;
-            s_in[sb][1][idx] = k * bb;
-            s_in[sb][2][idx] = k * c;
+            dst[idx] = k * a;
+            dst[NI + idx] = k * bb;
+            dst[2 * NI + idx] = k * c;
         }
     };
     double w[W];
@@ -765,12 +765,12 @@ __global__ void __launch_bounds__(k3::NT, 2) k_step_smooth(Batch b, LmParams p, 
 
     // x-pass item: row xr, pair xj (outputs x = 2xj, 2xj + 1)
     const int xr = threadIdx.x >> 4, xj = threadIdx.x & 15;
-    auto x_pass = [&](int sb) {
+    auto x_pass = [&](const double* in, double* out) {
         if (xr >= IH) return;
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
             double v[2 * NV];
-            const double2* src = reinterpret_cast<const double2*>(&s_in[sb][c][xr * IWP + 2 * xj]);
+            const double2* src = reinterpret_cast<const double2*>(in + c * NI + xr * IWP + 2 * xj);
 #pragma unroll
             for (int q = 0; q < NV; ++q) {
                 const double2 t = src[q];
@@ -782,7 +782,7 @@ __global__ void __launch_bounds__(k3::NT, 2) k_step_smooth(Batch b, LmParams p, 
                 o0 = fma(w[d], v[d], o0);
                 o1 = fma(w[d], v[d + 1], o1);
             }
-            *reinterpret_cast<double2*>(&s_x[sb][c][xr * TX + 2 * xj]) = make_double2(o0, o1);
+            *reinterpret_cast<double2*>(out + c * IH * TX + xr * TX + 2 * xj) = make_double2(o0, o1);
         }
     };
 
@@ -803,27 +803,28 @@ __global__ void __launch_bounds__(k3::NT, 2) k_step_smooth(Batch b, LmParams p, 
     float mx = 0.f;
 
     const int z0 = zb - R, z1 = ze + R;
+    double* in_a = &s_in[0][0][0];  // halo tile of plane p + 2 (written)
+    double* in_b = &s_in[1][0][0];  // halo tile of plane p + 1 (x-passed)
+    double* x_a = &s_x[0][0][0];    // x-passed plane p (y-passed)
+    double* x_b = &s_x[1][0][0];
     load_halo(z0);
-    store_halo(0);
+    store_halo(in_a);
     load_halo(z0 + 1);
-    store_halo(1);
+    store_halo(in_b);
     __syncthreads();
-    x_pass(0);
+    x_pass(in_a, x_a);
     load_halo(z0 + 2);
     __syncthreads();
-    // unrolled by 2W: ring slot (ph % W) and buffer parity (ph & 1) are static
-    for (int zbase = z0; zbase < z1; zbase += 2 * W) {
+    for (int zbase = z0; zbase < z1; zbase += W) {
 #pragma unroll
-        for (int ph = 0; ph < 2 * W; ++ph) {
-            const int zi = zbase + ph;
+        for (int rs = 0; rs < W; ++rs) {
+            const int zi = zbase + rs;
             if (zi < z1) {
-                const int sb = ph & 1;
-                const int rs = ph % W;
 #pragma unroll
                 for (int c = 0; c < 3; ++c) {
                     double s = 0.0;
 #pragma unroll
-                    for (int d = 0; d < W; ++d) s = fma(w[d], s_x[sb][c][(oy + d) * TX + ox], s);
+                    for (int d = 0; d < W; ++d) s = fma(w[d], x_a[c * IH * TX + (oy + d) * TX + ox], s);
                     ring[rs][c] = s;
                 }
                 const int zo = zi - R;
@@ -841,9 +842,11 @@ __global__ void __launch_bounds__(k3::NT, 2) k_step_smooth(Batch b, LmParams p, 
                         mx = fmaxf(mx, fabsf(v));
                     }
                 }
-                x_pass(sb ^ 1);
-                store_halo(sb);
+                x_pass(in_b, x_b);
+                store_halo(in_a);
                 load_halo(zi + 3);
+                double* t = in_a; in_a = in_b; in_b = t;
+                t = x_a; x_a = x_b; x_b = t;
                 __syncthreads();
             }
         }
@@ -862,9 +865,11 @@ __global__ void __launch_bounds__(k3::NT, 2) k_step_smooth(Batch b, LmParams p, 
 // floor) (Eq. 2, field.cpp:123-155), then Gaussian(sigma_warp); fp64
 // arithmetic, fp32 storage.  The normalised step bounds |d| <= target < 0.5
 // voxel, so every resample corner lies in the 3x3x3 neighbourhood of its
-// voxel: the accepted warp is staged in a 4-plane shared-memory ring (fp64,
-// halo R + 1) and the compose "gathers" are shared-memory reads.  Reads the
-// accepted buffer, writes the other one.
+// voxel: the accepted warp (fp32 in HBM) is staged exactly in a 4-plane
+// fp32 shared-memory ring (halo R + 1) and the compose "gathers" are
+// shared-memory reads widened to fp64 (F2F runs on its own pipe; fp64 staging
+// would double the shared-memory traffic of the gathers, the limiter).
+// Reads the accepted buffer, writes the other one.
 //
 // Tile 32 x 8, one barrier per plane.  Phase p: y-pass of plane p (z ring,
 // plane p - R out); x-pass of plane p+1; compose of plane p+2 into the halo
@@ -874,12 +879,15 @@ namespace k4 {
 constexpr int TX = 32, TY = 8, NT = 256;
 template <int R>
 struct Shape {
-    static constexpr int IWP = TX + 2 * R, IH = TY + 2 * R, NI = IWP * IH;  // composed tile
+    // composed tile: IW = TX + 2R items a row, stored with the warp tile's row
+    // stride so a warp's corner reads are consecutive (bank-conflict free)
+    static constexpr int IW = TX + 2 * R, IH = TY + 2 * R;
     static constexpr int UW = TX + 2 * R + 2, UH = TY + 2 * R + 2, UN = UW * UH;  // warp tile
+    static constexpr int IWP = UW, NI = IWP * IH;
     static constexpr int SL = (NI + NT - 1) / NT, USL = (UN + NT - 1) / NT;
     static constexpr int NV = (2 + 2 * R + 1) / 2;
     // dynamic shared memory layout (doubles)
-    static constexpr int OFF_U = 0, OFF_IN = 4 * 3 * UN, OFF_X = OFF_IN + 2 * 3 * NI;
+    static constexpr int OFF_U = 0, OFF_IN = (4 * 3 * UN + 1) / 2, OFF_X = OFF_IN + 2 * 3 * NI;  // s_u fp32
     static constexpr int TOTAL = OFF_X + 2 * 3 * IH * TX;
     static constexpr size_t BYTES = sizeof(double) * TOTAL + sizeof(double) * 8;
 };
@@ -892,7 +900,7 @@ __global__ void __launch_bounds__(k4::NT, 2) k_compose_smooth(Batch b, LmParams 
     constexpr int IWP = S::IWP, IH = S::IH, NI = S::NI, UW = S::UW, UN = S::UN, SL = S::SL, USL = S::USL,
                   NV = S::NV;
     extern __shared__ __align__(16) double k4_smem[];
-    double* s_u = k4_smem + S::OFF_U;    // [4 slots][3][UN]
+    float* s_u = reinterpret_cast<float*>(k4_smem + S::OFF_U);  // [4 slots][3][UN] fp32
     double* s_in = k4_smem + S::OFF_IN;  // [2][3][NI]
     double* s_x = k4_smem + S::OFF_X;    // [2][3][IH * TX]
     double* s_binv = k4_smem + S::TOTAL; // [2R]
@@ -928,8 +936,9 @@ __global__ void __launch_bounds__(k4::NT, 2) k_compose_smooth(Batch b, LmParams 
         const int idx = threadIdx.x + s * NT;
         vx[s] = x0 - R + idx % IWP;
         vy[s] = y0 - R + idx / IWP;
-        voff[s] = (idx < NI && vx[s] >= 0 && vx[s] < g.nx && vy[s] >= 0 && vy[s] < g.ny) ? vx[s] + g.nx * vy[s]
-                                                                                          : -1;
+        voff[s] = (idx < NI && idx % IWP < S::IW && vx[s] >= 0 && vx[s] < g.nx && vy[s] >= 0 && vy[s] < g.ny)
+                      ? vx[s] + g.nx * vy[s]
+                      : -1;
     }
     float pu[USL][3], pv[SL][3];
     auto load_u = [&](int z) {
@@ -946,7 +955,7 @@ __global__ void __launch_bounds__(k4::NT, 2) k_compose_smooth(Batch b, LmParams 
         }
     };
     auto store_u = [&](int z) {
-        double* dst = s_u + ((z + 4) & 3) * 3 * UN;
+        float* dst = s_u + ((z + 4) & 3) * 3 * UN;
 #pragma unroll
         for (int s = 0; s < USL; ++s) {
             const int idx = threadIdx.x + s * NT;
@@ -969,28 +978,29 @@ __global__ void __launch_bounds__(k4::NT, 2) k_compose_smooth(Batch b, LmParams 
             }
         }
     };
-    // every item's cell is interior (no clamp rules) when the tile and its
-    // halo keep one voxel off the x/y faces and the plane is off the z faces
-    const bool tile_inner = x0 - R >= 1 && x0 + TX - 1 + R <= g.nx - 2 && y0 - R >= 1 &&
-                            y0 + k4::TY - 1 + R <= g.ny - 2;
-    // composed value of the items of plane z (step in pv) -> s_in[sb]
-    auto compose = [&](int z, int sb) {
+    // an item's cell needs no clamp rules when it is one voxel off the faces
+    bool inner[SL];
+#pragma unroll
+    for (int s = 0; s < SL; ++s)
+        inner[s] = voff[s] >= 0 && vx[s] >= 1 && vx[s] <= g.nx - 2 && vy[s] >= 1 && vy[s] <= g.ny - 2;
+    // composed value of the items of plane z (step in pv) -> dst
+    auto compose = [&](int z, double* dst) {
         const bool zin = z >= 0 && z < g.nz;
-        double* dst = s_in + sb * 3 * NI;
-        if (tile_inner && z >= 1 && z <= g.nz - 2) {
+        const bool zinner = z >= 1 && z <= g.nz - 2;
+        {
             // |d| <= target < 1: floor(d) in {-1, 0}, cell origin x + floor(d)
 #pragma unroll
             for (int s = 0; s < SL; ++s) {
                 const int idx = threadIdx.x + s * NT;
-                if (idx >= NI) continue;
+                if (idx >= NI || !(zinner && inner[s])) continue;
                 const double dx = eps * pv[s][0], dy = eps * pv[s][1], dz = eps * pv[s][2];
                 double o3[3];
                 if (isfinite(dx + dy + dz)) {
                     const int fx = dx < 0.0 ? -1 : 0, fy = dy < 0.0 ? -1 : 0, fz = dz < 0.0 ? -1 : 0;
                     const double tx = dx - (double)fx, ty = dy - (double)fy, tz = dz - (double)fz;
                     const int a = (idx / IWP + 1 + fy) * UW + idx % IWP + 1 + fx;
-                    const double* p0 = s_u + ((z + fz + 4) & 3) * 3 * UN + a;
-                    const double* p1 = s_u + ((z + fz + 5) & 3) * 3 * UN + a;
+                    const float* p0 = s_u + ((z + fz + 4) & 3) * 3 * UN + a;
+                    const float* p1 = s_u + ((z + fz + 5) & 3) * 3 * UN + a;
 #pragma unroll
                     for (int ch = 0; ch < 3; ++ch) {
                         const double c000 = p0[ch * UN], c100 = p0[ch * UN + 1];
@@ -1012,12 +1022,11 @@ __global__ void __launch_bounds__(k4::NT, 2) k_compose_smooth(Batch b, LmParams 
                 dst[NI + idx] = o3[1];
                 dst[2 * NI + idx] = o3[2];
             }
-            return;
         }
 #pragma unroll
         for (int s = 0; s < SL; ++s) {
             const int idx = threadIdx.x + s * NT;
-            if (idx >= NI) continue;
+            if (idx >= NI || idx % IWP >= S::IW || (zinner && inner[s])) continue;
             double o3[3] = {0.0, 0.0, 0.0};
             if (zin && voff[s] >= 0) {
                 const double dx = eps * pv[s][0], dy = eps * pv[s][1], dz = eps * pv[s][2];
@@ -1027,8 +1036,8 @@ __global__ void __launch_bounds__(k4::NT, 2) k_compose_smooth(Batch b, LmParams 
                     const AxisTapD Z = axis_tap_dd(z, dz, g.nz);
                     const int ux0 = min(max(X.i0 - (x0 - R - 1), 0), UW - 2);
                     const int uy0 = min(max(Y.i0 - (y0 - R - 1), 0), S::UH - 2);
-                    const double* p0 = s_u + ((Z.i0 + 4) & 3) * 3 * UN + uy0 * UW + ux0;
-                    const double* p1 = s_u + ((Z.i1 + 4) & 3) * 3 * UN + uy0 * UW + ux0;
+                    const float* p0 = s_u + ((Z.i0 + 4) & 3) * 3 * UN + uy0 * UW + ux0;
+                    const float* p1 = s_u + ((Z.i1 + 4) & 3) * 3 * UN + uy0 * UW + ux0;
 #pragma unroll
                     for (int ch = 0; ch < 3; ++ch) {
                         const double c000 = p0[ch * UN], c100 = p0[ch * UN + 1];
@@ -1056,12 +1065,12 @@ __global__ void __launch_bounds__(k4::NT, 2) k_compose_smooth(Batch b, LmParams 
 #pragma unroll
     for (int d = 0; d < W; ++d) w[d] = p.wwd[d < R ? R - d : d - R];
     const int xr = threadIdx.x >> 4, xj = threadIdx.x & 15;
-    auto x_pass = [&](int sb) {
+    auto x_pass = [&](const double* in, double* out) {
         if (xr >= IH) return;
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
             double v[2 * NV];
-            const double2* src = reinterpret_cast<const double2*>(s_in + (sb * 3 + c) * NI + xr * IWP + 2 * xj);
+            const double2* src = reinterpret_cast<const double2*>(in + c * NI + xr * IWP + 2 * xj);
 #pragma unroll
             for (int q = 0; q < NV; ++q) {
                 const double2 t = src[q];
@@ -1073,7 +1082,7 @@ __global__ void __launch_bounds__(k4::NT, 2) k_compose_smooth(Batch b, LmParams 
                 o0 = fma(w[d], v[d], o0);
                 o1 = fma(w[d], v[d + 1], o1);
             }
-            *reinterpret_cast<double2*>(s_x + (sb * 3 + c) * IH * TX + xr * TX + 2 * xj) = make_double2(o0, o1);
+            *reinterpret_cast<double2*>(out + c * IH * TX + xr * TX + 2 * xj) = make_double2(o0, o1);
         }
     };
 
@@ -1098,28 +1107,32 @@ __global__ void __launch_bounds__(k4::NT, 2) k_compose_smooth(Batch b, LmParams 
     load_u(z0 + 1); store_u(z0 + 1);
     load_u(z0 + 2); store_u(z0 + 2);
     load_v(z0);
+    // double buffers as swapped pointers: halo tiles (composed) and x-passed
+    double* in_a = s_in;           // composed plane p + 2 is written here
+    double* in_b = s_in + 3 * NI;  // composed plane p + 1 is read here
+    double* x_a = s_x;             // x-passed plane p is read here
+    double* x_b = s_x + 3 * IH * TX;
     __syncthreads();
-    compose(z0, 0);
+    compose(z0, in_a);
     load_v(z0 + 1);
     load_u(z0 + 3);
     __syncthreads();
-    x_pass(0);
-    compose(z0 + 1, 1);
+    x_pass(in_a, x_a);
+    compose(z0 + 1, in_b);
     store_u(z0 + 3);  // slot of plane z0 - 1 (not read by compose(z0 + 1))
     load_u(z0 + 4);
     load_v(z0 + 2);
     __syncthreads();
-    for (int zbase = z0; zbase < z1; zbase += 2 * W) {
+    for (int zbase = z0; zbase < z1; zbase += W) {
 #pragma unroll
-        for (int ph = 0; ph < 2 * W; ++ph) {
-            const int zi = zbase + ph;
+        for (int rs = 0; rs < W; ++rs) {
+            const int zi = zbase + rs;
             if (zi < z1) {
-                const int sb = ph & 1, rs = ph % W;
 #pragma unroll
                 for (int c = 0; c < 3; ++c) {
                     double s = 0.0;
 #pragma unroll
-                    for (int d = 0; d < W; ++d) s = fma(w[d], s_x[(sb * 3 + c) * IH * TX + (oy + d) * TX + ox], s);
+                    for (int d = 0; d < W; ++d) s = fma(w[d], x_a[c * IH * TX + (oy + d) * TX + ox], s);
                     ring[rs][c] = s;
                 }
                 const int zo = zi - R;
@@ -1135,11 +1148,13 @@ __global__ void __launch_bounds__(k4::NT, 2) k_compose_smooth(Batch b, LmParams 
                         UN_[c * n + o] = (float)(s * inv);
                     }
                 }
-                x_pass(sb ^ 1);
-                compose(zi + 2, sb);
+                x_pass(in_b, x_b);
+                compose(zi + 2, in_a);
                 store_u(zi + 4);
                 load_u(zi + 5);
                 load_v(zi + 3);
+                double* t = in_a; in_a = in_b; in_b = t;
+                t = x_a; x_a = x_b; x_b = t;
                 __syncthreads();
             }
         }
