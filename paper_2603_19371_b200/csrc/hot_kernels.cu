@@ -258,45 +258,62 @@ __global__ void __launch_bounds__(256) k_warp_moving(Batch b, int mode, int z_fi
 //   f' S_A + m' S_B - S_E cancels exactly).
 //   sum(rho): one partial per (plane, tile, warp); the last CTA of the pair
 //   reduces them per owned plane in a fixed order into plane_sum[z].
+// Schedule (as K3): one barrier per plane; phase p runs the y-pass of plane p
+// (z ring, plane p - R out), the x-pass of plane p+1 (two outputs per thread
+// from 16-byte shared loads), the halo tile of plane p+2 and the loads of
+// plane p+3.
+namespace k1 {
+constexpr int TX = 32, TY = 8, NT = 256;
 template <int R>
-__global__ void __launch_bounds__(NT, 2) k_lncc_fwd(Batch b, int chunk_len) {
-    using It = hot::Items<R>;
-    constexpr int IW = It::IW, IH = It::IH, NI = It::NI, SL = It::SLOTS, W = 2 * R + 1;
-    constexpr int XS = (IH * TX + NT - 1) / NT;  // x-pass items per thread
-    __shared__ double s_f[2][NI], s_m[2][NI];
-    __shared__ double s_x[5][IH][TX];
+struct Shape {
+    static constexpr int IWP = TX + 2 * R, IH = TY + 2 * R, NI = IWP * IH;
+    static constexpr int SL = (NI + NT - 1) / NT;
+    static constexpr int NV = (2 + 2 * R + 1) / 2;
+};
+}  // namespace k1
+
+template <int R>
+__global__ void __launch_bounds__(k1::NT, 2) k_lncc_fwd(Batch b, int chunk_len) {
+    using S = k1::Shape<R>;
+    constexpr int TX = k1::TX, NT = k1::NT, W = 2 * R + 1;
+    constexpr int IWP = S::IWP, IH = S::IH, NI = S::NI, SL = S::SL, NV = S::NV;
+    __shared__ __align__(16) double s_in[2][2][NI];  // [buffer][f', m'][tile]
+    __shared__ __align__(16) double s_x[2][5][IH * TX];
     __shared__ int s_last;
 
     const int pair = blockIdx.z;
     PairState* st = b.st + pair;
     if (st->done) return;
     const Geo g = b.g;
-    Tile t;
-    t.init(g, chunk_len);
+    const int nxy = g.nx * g.ny;
+    const int tiles_x = cdiv(g.nx, TX);
+    const int x0 = (blockIdx.x % tiles_x) * TX, y0 = (blockIdx.x / tiles_x) * k1::TY;
+    const int zb = g.zs + blockIdx.y * chunk_len, ze = min(zb + chunk_len, g.ze);
     const float* __restrict__ F = b.F + (long long)pair * g.nfull;
     const double* __restrict__ MW = b.MW + (long long)pair * g.n;
     float* __restrict__ Aout = b.ABE + (long long)pair * 4 * g.n;
     float* __restrict__ Bout = Aout + g.n;
     double* __restrict__ Eout = reinterpret_cast<double*>(Aout + 2 * g.n);
     const double shf = st->shift_f, shm = st->shift_m;
-    const int tiles = cdiv(g.nx, TX) * cdiv(g.ny, TY);
+    const int tiles = cdiv(g.nx, TX) * cdiv(g.ny, k1::TY);
     double* __restrict__ part = b.partials + (long long)pair * g.nz * tiles * (NT / 32);
-    It it;
-    it.init(t.x0, t.y0, g.nx, g.ny);
-    const int cxy = t.own ? axis_count(t.x, g.nx, R) * axis_count(t.y, g.ny, R) : 1;
-    const int ooff = t.x + g.nx * t.y;
 
-    // dense rows of the next plane (d1 -> shared memory at the end of the
-    // current plane) and of the plane after (d2, loads in flight)
-    float d1f[SL], d2f[SL];
-    double d1m[SL], d2m[SL];
-    auto load_dense = [&](int z, float (&df)[SL], double (&dm)[SL]) {
-        const bool zin = z >= 0 && z < g.nz;
+    int hoff[SL];
+#pragma unroll
+    for (int s = 0; s < SL; ++s) {
+        const int idx = threadIdx.x + s * NT;
+        const int gx = x0 - R + idx % IWP, gy = y0 - R + idx / IWP;
+        hoff[s] = (idx < NI && gx >= 0 && gx < g.nx && gy >= 0 && gy < g.ny) ? gx + g.nx * gy : -1;
+    }
+    float df[SL];
+    double dm[SL];
+    auto load_dense = [&](int z) {
+        const bool zin = z >= 0 && z < g.nz && z < ze + R;
 #pragma unroll
         for (int s = 0; s < SL; ++s) {
-            if (zin && it.goff[s] >= 0) {
-                df[s] = __ldg(F + t.gp(z) + it.goff[s]);
-                dm[s] = __ldg(MW + t.lp(g, z) + it.goff[s]);
+            if (zin && hoff[s] >= 0) {
+                df[s] = __ldg(F + z * nxy + hoff[s]);
+                dm[s] = __ldg(MW + (z - g.zlo) * nxy + hoff[s]);
             } else {
                 df[s] = 0.f;
                 dm[s] = 0.0;
@@ -305,84 +322,101 @@ __global__ void __launch_bounds__(NT, 2) k_lncc_fwd(Batch b, int chunk_len) {
     };
     // absent (out-of-volume) items contribute 0 to every sum (truncated
     // windows, A2); present items may carry NaN, which propagates
-    auto complete = [&](int z, int sb) {
+    auto complete = [&](int z, double* dst) {
         const bool zin = z >= 0 && z < g.nz;
 #pragma unroll
         for (int s = 0; s < SL; ++s) {
-            if (it.sidx[s] < 0) continue;
-            const bool present = zin && it.goff[s] >= 0;
-            s_f[sb][it.sidx[s]] = present ? (double)d1f[s] - shf : 0.0;
-            s_m[sb][it.sidx[s]] = present ? d1m[s] - shm : 0.0;
+            const int idx = threadIdx.x + s * NT;
+            if (idx >= NI) continue;
+            const bool present = zin && hoff[s] >= 0;
+            dst[idx] = present ? (double)df[s] - shf : 0.0;
+            dst[NI + idx] = present ? dm[s] - shm : 0.0;
+        }
+    };
+    // x pass: 5-tap box of (f, m, ff, mm, fm), two adjacent outputs
+    const int xr = threadIdx.x >> 4, xj = threadIdx.x & 15;
+    auto x_pass = [&](const double* in, double* out) {
+        if (xr >= IH) return;
+        double f[2 * NV], m[2 * NV];
+        const double2* sf = reinterpret_cast<const double2*>(in + xr * IWP + 2 * xj);
+        const double2* sm = reinterpret_cast<const double2*>(in + NI + xr * IWP + 2 * xj);
+#pragma unroll
+        for (int q = 0; q < NV; ++q) {
+            const double2 a = sf[q], c = sm[q];
+            f[2 * q] = a.x; f[2 * q + 1] = a.y;
+            m[2 * q] = c.x; m[2 * q + 1] = c.y;
+        }
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+            double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0, a4 = 0.0;
+#pragma unroll
+            for (int d = 0; d < W; ++d) {
+                const double fv = f[j + d], mv = m[j + d];
+                a0 += fv;
+                a1 += mv;
+                a2 = fma(fv, fv, a2);
+                a3 = fma(mv, mv, a3);
+                a4 = fma(fv, mv, a4);
+            }
+            double* o = out + xr * TX + 2 * xj + j;
+            o[0] = a0; o[IH * TX] = a1; o[2 * IH * TX] = a2; o[3 * IH * TX] = a3; o[4 * IH * TX] = a4;
         }
     };
 
+    const int ox = threadIdx.x & 31, oy = threadIdx.x >> 5;
+    const int x = x0 + ox, y = y0 + oy;
+    const bool own = x < g.nx && y < g.ny;
+    const int cxy = own ? axis_count(x, g.nx, R) * axis_count(y, g.ny, R) : 1;
+    const int ooff = x + g.nx * y;
     double ring[W][5];
 #pragma unroll
     for (int d = 0; d < W; ++d)
 #pragma unroll
         for (int c = 0; c < 5; ++c) ring[d][c] = 0.0;
 
-    const int z0 = t.zb - R, z1 = t.ze + R;  // input planes [z0, z1)
-    load_dense(z0, d1f, d1m);
-    complete(z0, 0);
-    load_dense(z0 + 1, d1f, d1m);
+    const int z0 = zb - R, z1 = ze + R;  // input planes [z0, z1)
+    double* in_a = &s_in[0][0][0];
+    double* in_b = &s_in[1][0][0];
+    double* x_a = &s_x[0][0][0];
+    double* x_b = &s_x[1][0][0];
+    load_dense(z0);
+    complete(z0, in_a);
+    load_dense(z0 + 1);
+    complete(z0 + 1, in_b);
     __syncthreads();
-
+    x_pass(in_a, x_a);
+    load_dense(z0 + 2);
+    __syncthreads();
     for (int zbase = z0; zbase < z1; zbase += W) {
 #pragma unroll
-        for (int ph = 0; ph < W; ++ph) {
-            const int zi = zbase + ph;
+        for (int rs = 0; rs < W; ++rs) {
+            const int zi = zbase + rs;
             if (zi < z1) {
-                const int sb = (zi - z0) & 1;
-                load_dense(zi + 2, d2f, d2m);
-                // x pass: 5-tap box of (f, m, ff, mm, fm)
-#pragma unroll
-                for (int q = 0; q < XS; ++q) {
-                    const int idx = threadIdx.x + q * NT;
-                    if (idx < IH * TX) {
-                        const int c = idx % TX, r = idx / TX;
-                        const double* fr = &s_f[sb][r * IW + c];
-                        const double* mr = &s_m[sb][r * IW + c];
-                        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0, a4 = 0.0;
-#pragma unroll
-                        for (int d = 0; d < W; ++d) {
-                            const double f = fr[d], m = mr[d];
-                            a0 += f;
-                            a1 += m;
-                            a2 = fma(f, f, a2);
-                            a3 = fma(m, m, a3);
-                            a4 = fma(f, m, a4);
-                        }
-                        s_x[0][r][c] = a0; s_x[1][r][c] = a1; s_x[2][r][c] = a2;
-                        s_x[3][r][c] = a3; s_x[4][r][c] = a4;
-                    }
-                }
-                __syncthreads();
                 // y pass into the static ring; z sum taken directly over the ring
 #pragma unroll
                 for (int c = 0; c < 5; ++c) {
                     double s = 0.0;
 #pragma unroll
-                    for (int d = 0; d < W; ++d) s += s_x[c][t.oy + d][t.ox];
-                    ring[ph][c] = s;
+                    for (int d = 0; d < W; ++d) s += x_a[c * IH * TX + (oy + d) * TX + ox];
+                    ring[rs][c] = s;
                 }
                 const int zo = zi - R;
-                if (zo >= t.zb) {
+                if (zo >= zb) {
                     double rho = 0.0;
-                    if (t.own) {
-                        double S[5];
+                    if (own) {
+                        double Sm[5];
 #pragma unroll
                         for (int c = 0; c < 5; ++c) {
                             double s = 0.0;
 #pragma unroll
-                            for (int d = 0; d < W; ++d) s += ring[(ph + 1 + d) % W][c];
-                            S[c] = s;
+                            for (int d = 0; d < W; ++d) s += ring[(rs + 1 + d) % W][c];
+                            Sm[c] = s;
                         }
                         const double inv = c_inv_count[cxy * axis_count(zo, g.nz, R)];
-                        const double mf = S[0] * inv, mm = S[1] * inv;
-                        const double vf = fma(-mf, mf, S[2] * inv);
-                        const double vm = fma(-mm, mm, S[3] * inv);
-                        const double cv = fma(-mf, mm, S[4] * inv);
+                        const double mf = Sm[0] * inv, mm = Sm[1] * inv;
+                        const double vf = fma(-mf, mf, Sm[2] * inv);
+                        const double vm = fma(-mm, mm, Sm[3] * inv);
+                        const double cv = fma(-mf, mm, Sm[4] * inv);
                         const double af = mf + shf, am = mm + shm;
                         const double msf = fma(af, af, vf), msm = fma(am, am, vm);
                         double Ee = 0.0;
@@ -396,20 +430,19 @@ __global__ void __launch_bounds__(NT, 2) k_lncc_fwd(Batch b, int chunk_len) {
                             Bb = (float)(-rho * alpha * alpha * vf * inv);  // -rho / (n vm)
                             Ee = fma((double)Aa, mf, (double)Bb * mm);
                         }
-                        const int o = t.lp(g, zo) + ooff;
+                        const int o = (zo - g.zlo) * nxy + ooff;
                         Aout[o] = Aa;
                         Bout[o] = Bb;
                         Eout[o] = Ee;
                     }
                     rho = warp_sum(rho);
-                    if (t.ox == 0) part[((long long)zo * tiles + blockIdx.x) * (NT / 32) + t.oy] = rho;
+                    if (ox == 0) part[((long long)zo * tiles + blockIdx.x) * (NT / 32) + oy] = rho;
                 }
-                complete(zi + 1, sb ^ 1);
-#pragma unroll
-                for (int s = 0; s < SL; ++s) {
-                    d1m[s] = d2m[s];
-                    d1f[s] = d2f[s];
-                }
+                x_pass(in_b, x_b);
+                complete(zi + 2, in_a);
+                load_dense(zi + 3);
+                double* t = in_a; in_a = in_b; in_b = t;
+                t = x_a; x_a = x_b; x_b = t;
                 __syncthreads();
             }
         }
@@ -1179,10 +1212,10 @@ void launch_lncc_fwd(const Batch& b, const LmParams& p, int mode, cudaStream_t s
     const int zf = std::max(0, b.g.zs - 2), zl = std::min(b.g.nz, b.g.ze + 2);
     const dim3 wgrid(cdiv(b.g.nx, 32) * cdiv(b.g.ny, 8), zl - zf, b.pairs);
     k_warp_moving<<<wgrid, 256, 0, s>>>(b, mode, zf);
-    const LaunchShape sh = shape_for(b.g, b.pairs, TY);
+    const LaunchShape sh = shape_for(b.g, b.pairs, k1::TY);
     dim3 grid = sh.grid();
     grid.z = b.pairs;
-    k_lncc_fwd<2><<<grid, NT, 0, s>>>(b, sh.chunk_len);
+    k_lncc_fwd<2><<<grid, k1::NT, 0, s>>>(b, sh.chunk_len);
     g_kernel_launches += 2;
 }
 
