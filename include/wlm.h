@@ -16,6 +16,7 @@
  *   field.hpp:113  gaussian_smooth(Volume3)              wlm_gaussian_smooth_vol
  *   field.hpp:114  gaussian_smooth(DispField3)           wlm_gaussian_smooth_field
  *   field.hpp:116-117 all_finite                         wlm_all_finite
+ *   SPEC.md:127    residual_mse -> ResidualReport        wlm_residual_mse
  *   SPEC.md:136    residual_lncc -> ResidualReport       wlm_residual_lncc
  *   SPEC.md:247    lm_step_pointwise                     wlm_lm_step_pointwise
  *   SPEC.md:265    update_damping                        wlm_update_damping
@@ -85,6 +86,8 @@ typedef struct {
 typedef struct { double beta1, beta2, eps_hat, lr; } wlm_adam_config;
 
 enum { WLM_OPT_LM = 0, WLM_OPT_ADAM = 1, WLM_OPT_GD = 2 };
+/* MetricConfig.kind: mi is not built (WLM_UNSUPPORTED). */
+enum { WLM_METRIC_LNCC = 0, WLM_METRIC_MSE = 1 };
 #define WLM_MAX_LEVELS 8
 
 /* RegConfig + MetricConfig + StepScale. */
@@ -100,6 +103,7 @@ typedef struct {
     double target_max_disp, step_floor;
     double sigma_update, sigma_warp;
     int log_jacobian;
+    int metric; /* WLM_METRIC_* (SPEC.md:121), default LNCC */
 } wlm_reg_config;
 
 /* RegResult.loss_trace row (CSV columns SPEC.md:427). */
@@ -150,6 +154,10 @@ wlm_status wlm_all_finite(wlm_ctx* ctx, const double* data, size_t count, int* o
 wlm_status wlm_residual_lncc(wlm_ctx* ctx, const double* F, const double* M,
                              const double* u, wlm_dims d, int radius, double* r,
                              double* lncc, double* g /* nullable, AoS */);
+/* residual_mse: r = mean (f - m(x+u))^2, g = grad_u r with
+ * the analytic interpolant gradient; g nullable, AoS. */
+wlm_status wlm_residual_mse(wlm_ctx* ctx, const double* F, const double* M, const double* u,
+                            wlm_dims d, double* r, double* g);
 wlm_status wlm_lm_step_pointwise(wlm_ctx* ctx, double r, const double* g, wlm_dims d,
                                  double lambda, double* out);
 void wlm_update_damping(wlm_lm_state* s, double loss_new, const wlm_lm_config* c);

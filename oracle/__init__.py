@@ -52,7 +52,7 @@ class RegConfig(C.Structure):
                 ("factors", C.c_int * MAX_LEVELS), ("iters", C.c_int * MAX_LEVELS),
                 ("target_max_disp", C.c_double), ("step_floor", C.c_double),
                 ("sigma_update", C.c_double), ("sigma_warp", C.c_double),
-                ("log_jacobian", C.c_int)]
+                ("log_jacobian", C.c_int), ("metric", C.c_int)]
 
 
 class StepLog(C.Structure):

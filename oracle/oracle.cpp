@@ -630,12 +630,12 @@ double orc_residual_mse(const double* F, const double* M, const double* u, orc_d
     const size_t N = nvox(d);
     Vec Mw(N), gM(3 * N);
     warp(M, u, d, Mw.data(), gM.data());
-    double s = 0.0;
+    double s = 0.0;  // fixed serial order
     for (size_t i = 0; i < N; ++i) { const double e = F[i] - Mw[i]; s += e * e; }
     if (g)
         for (size_t i = 0; i < N; ++i) {
             const double k = -2.0 * (F[i] - Mw[i]) / (double)N;
-            for (int c = 0; c < 3; ++c) g[3 * i + c] = k * gM[3 * i + c];
+            for (int c = 0; c < 3; ++c) g[3 * i + c] = r32(k * gM[3 * i + c]);
         }
     return s / (double)N;
 }
@@ -787,8 +787,18 @@ int orc_lm_run_level(const double* F, const double* M, orc_dims d, double* u,
     const int R = c->lncc_radius;
     Vec g(3 * N), step(3 * N), unew(3 * N), gnew(3 * N), am, av;
     if (c->optimizer == ORC_OPT_ADAM) { am.assign(3 * N, 0.0); av.assign(3 * N, 0.0); }
+    // MetricConfig.kind: loss_raw is LNCC (r = 1 - LNCC) or the
+    // MSE itself (r = MSE)
+    auto residual = [&](const double* uu, double* gg, double* raw) {
+        if (c->metric == ORC_METRIC_MSE) {
+            const double m = orc_residual_mse(F, M, uu, d, gg);
+            *raw = m;
+            return m;
+        }
+        return orc_residual_lncc(F, M, uu, d, R, gg, raw, nullptr);
+    };
     double lncc = 0.0;
-    double r = orc_residual_lncc(F, M, u, d, R, g.data(), &lncc, nullptr);
+    double r = residual(u, g.data(), &lncc);
     if (!std::isfinite(r)) return ORC_NONFINITE;
     int nt = 0;
     for (int it = 0; it < iters; ++it) {
@@ -829,7 +839,7 @@ int orc_lm_run_level(const double* F, const double* M, orc_dims d, double* u,
                 for (size_t i = 0; i < 3 * N; ++i) inc[i] = eps * step[i];
                 jac = jac_min(inc.data(), d);
             }
-            rn = orc_residual_lncc(F, M, unew.data(), d, R, gnew.data(), &ln, nullptr);
+            rn = residual(unew.data(), gnew.data(), &ln);
             if (!std::isfinite(rn)) {
                 if (trace && ntrace) *ntrace = nt;
                 return ORC_NONFINITE;

@@ -49,6 +49,7 @@ typedef struct {
 typedef struct { double beta1, beta2, eps_hat, lr; } orc_adam_config;
 
 enum { ORC_OPT_LM = 0, ORC_OPT_ADAM = 1, ORC_OPT_GD = 2 };
+enum { ORC_METRIC_LNCC = 0, ORC_METRIC_MSE = 1 };
 
 #define ORC_MAX_LEVELS 8
 /* RegConfig, SPEC.md:352-355 plus MetricConfig and
@@ -65,6 +66,7 @@ typedef struct {
     double target_max_disp, step_floor;
     double sigma_update, sigma_warp;
     int log_jacobian; /* compute jacobian_det_min(eps*dU_s) per accepted step */
+    int metric;       /* ORC_METRIC_* (MetricConfig.kind) */
 } orc_reg_config;
 
 /* One RegResult.loss_trace row + CSV extras. */

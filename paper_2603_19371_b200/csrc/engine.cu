@@ -29,7 +29,11 @@ wlm_status engine_init(wlm_engine* e, wlm_ctx* ctx, wlm_dims d, int pairs, const
         set_err(ctx, "tile_size > 1 (tiled LM, SPEC.md:256) is not implemented on the device");
         return WLM_UNSUPPORTED;
     }
-    if (c->lncc_radius != 2) {
+    if (c->metric != WLM_METRIC_LNCC && c->metric != WLM_METRIC_MSE) {
+        set_err(ctx, "metric: only LNCC and MSE are built (MI is SURVEY §8(f) #3)");
+        return WLM_UNSUPPORTED;
+    }
+    if (c->metric == WLM_METRIC_LNCC && c->lncc_radius != 2) {
         set_err(ctx, "lncc_radius != 2 is not instantiated");
         return WLM_UNSUPPORTED;
     }
@@ -37,7 +41,8 @@ wlm_status engine_init(wlm_engine* e, wlm_ctx* ctx, wlm_dims d, int pairs, const
         set_err(ctx, "volumes of 2^31 voxels or more are not supported (io.cpp:13 cap)");
         return WLM_UNSUPPORTED;
     }
-    if (d.nx <= 2 * c->lncc_radius || d.ny <= 2 * c->lncc_radius || d.nz <= 2 * c->lncc_radius) {
+    if (c->metric == WLM_METRIC_LNCC &&
+        (d.nx <= 2 * c->lncc_radius || d.ny <= 2 * c->lncc_radius || d.nz <= 2 * c->lncc_radius)) {
         set_err(ctx, "residual_lncc: dims must exceed 2*radius (SPEC.md:138)");
         return WLM_INVALID_ARG;
     }
@@ -61,6 +66,7 @@ wlm_status engine_init(wlm_engine* e, wlm_ctx* ctx, wlm_dims d, int pairs, const
     P.optimizer = c->optimizer;
     P.log_jacobian = c->log_jacobian;
     P.radius = c->lncc_radius;
+    P.metric = c->metric;
     P.Ru = smooth_radius(c->sigma_update);
     P.Rw = smooth_radius(c->sigma_warp);
     if (P.Ru > 3 || P.Rw > 3) {
@@ -175,6 +181,7 @@ void wlm_default_reg_config(wlm_reg_config* c) {
     c->target_max_disp = 0.4; c->step_floor = 1e-12;
     c->sigma_update = 1.0; c->sigma_warp = 0.5;
     c->log_jacobian = 0;
+    c->metric = WLM_METRIC_LNCC;
 }
 
 wlm_status wlm_ctx_create(int device, wlm_ctx** out) {

@@ -70,8 +70,12 @@ __device__ bool rejection_fires(const PairState* st, const LmParams& p, double r
     return p.rejection && st->hist_n >= 2 && (r - st->L1) > p.tau * fabs(st->L1 - st->L2);
 }
 
-__device__ void finalize_pair(PairState* st, const LmParams& p, int mode, double lncc, int pair) {
-    double r = 1.0 - lncc;
+// val: mean rho (LNCC: loss_raw = LNCC, r = 1 - LNCC) or the MSE (loss_raw =
+// r = MSE).  PairState's lncc_* fields hold loss_raw.
+__device__ void finalize_pair(PairState* st, const LmParams& p, int mode, double val, int pair) {
+    const bool mse = p.metric == WLM_METRIC_MSE;
+    double lncc = val;
+    double r = mse ? val : 1.0 - val;
     if (mode == 0) {
         st->r_cur = r;
         st->lncc_cur = lncc;
@@ -82,7 +86,7 @@ __device__ void finalize_pair(PairState* st, const LmParams& p, int mode, double
     }
     if (p.script && p.script_n > 0) {
         r = p.script[(long long)pair * p.script_n + min(st->attempt, p.script_n - 1)];
-        lncc = 1.0 - r;
+        lncc = mse ? r : 1.0 - r;
     }
     st->attempt += 1;
     st->r_try = r;
@@ -248,6 +252,93 @@ __global__ void __launch_bounds__(256) k_warp_moving(Batch b, int mode, int z_fi
     const int o = g.lat(x, y, z);
     b.MW[(long long)pair * g.n + o] =
         sample_vol<false>(M, g, x, y, z, __ldg(U + o), __ldg(U + g.n + o), __ldg(U + 2 * g.n + o), nullptr);
+}
+
+// The pair's last CTA (of a 2D grid of 256-thread CTAs) reduces the owned
+// planes' per-(tile, warp) partials in a fixed order into plane_sum[z];
+// foreign planes are zeroed for the NCCL slab all-reduce.
+__device__ void reduce_plane_partials(const Batch& b, PairState* st, const double* part, int tiles,
+                                      int* s_last) {
+    const Geo& g = b.g;
+    const int nblk = gridDim.x * gridDim.y;
+    if (threadIdx.x == 0) {
+        __threadfence();
+        const unsigned prev = atomicAdd(&st->counter, 1u);
+        *s_last = prev == (unsigned)(nblk - 1);
+    }
+    __syncthreads();
+    if (!*s_last) return;
+    __threadfence();
+    double* __restrict__ psum = b.plane_sum + (long long)(st - b.st) * g.nz;
+    for (int z = threadIdx.x; z < g.nz; z += blockDim.x) {
+        double s = 0.0;
+        if (z >= g.zs && z < g.ze) {
+            const double* pz = part + (long long)z * tiles * 8;
+            for (int i = 0; i < tiles * 8; ++i) s += __ldcg(pz + i);
+        }
+        if (z >= g.zs && z < g.ze) psum[z] = s;
+        else if (b.zero_foreign_planes) psum[z] = 0.0;
+    }
+    if (threadIdx.x == 0) st->counter = 0u;
+}
+
+// MSE forward: one fp64 partial of sum (f - Mw)^2 per
+// (plane, tile, warp) in the K1b layout, then the same fixed-order plane
+// reduction; K5 turns it into r = loss_raw = MSE.
+__global__ void __launch_bounds__(256) k_mse_fwd(Batch b, int chunk_len) {
+    __shared__ int s_last;
+    const int pair = blockIdx.z;
+    PairState* st = b.st + pair;
+    if (st->done) return;
+    const Geo g = b.g;
+    const int nxy = g.nx * g.ny;
+    const int tiles_x = cdiv(g.nx, 32);
+    const int tiles = tiles_x * cdiv(g.ny, 8);
+    const int ox = threadIdx.x & 31, oy = threadIdx.x >> 5;
+    const int x = (blockIdx.x % tiles_x) * 32 + ox, y = (blockIdx.x / tiles_x) * 8 + oy;
+    const bool own = x < g.nx && y < g.ny;
+    const int zb = g.zs + blockIdx.y * chunk_len, ze = min(zb + chunk_len, g.ze);
+    const float* __restrict__ F = b.F + (long long)pair * g.nfull;
+    const double* __restrict__ MW = b.MW + (long long)pair * g.n;
+    double* __restrict__ part = b.partials + (long long)pair * g.nz * tiles * 8;
+    const int ooff = x + g.nx * y;
+    for (int z = zb; z < ze; ++z) {
+        double e2 = 0.0;
+        if (own) {
+            const double e = (double)__ldg(F + z * nxy + ooff) - __ldg(MW + (z - g.zlo) * nxy + ooff);
+            e2 = e * e;
+        }
+        e2 = warp_sum(e2);
+        if (ox == 0) part[((long long)z * tiles + blockIdx.x) * 8 + oy] = e2;
+    }
+    reduce_plane_partials(b, st, part, tiles, &s_last);
+}
+
+// MSE gradient: g = -2 (f - Mw) / N * grad M(x+u) at the accepted warp
+// (the oracle's orc_residual_mse arithmetic); skipped after a rejection, like
+// K2, because the gradient is unchanged.
+__global__ void __launch_bounds__(256) k_mse_grad(Batch b) {
+    const int pair = blockIdx.z;
+    const PairState* st = b.st + pair;
+    if (st->done || st->last_rejected) return;
+    const Geo g = b.g;
+    const int tiles_x = cdiv(g.nx, 32);
+    const int x = (blockIdx.x % tiles_x) * 32 + (threadIdx.x & 31);
+    const int y = (blockIdx.x / tiles_x) * 8 + (threadIdx.x >> 5);
+    if (x >= g.nx || y >= g.ny) return;
+    const int z = g.zs + blockIdx.y;
+    const long long n = g.n;
+    const float* __restrict__ M = b.M + (long long)pair * g.nfull;
+    const float* __restrict__ F = b.F + (long long)pair * g.nfull;
+    const float* __restrict__ U = b.U + ((long long)pair * 2 + st->cur) * 3 * n;
+    float* __restrict__ G = b.G + (long long)pair * 3 * n;
+    const int o = g.lat(x, y, z);
+    double grad[3];
+    const double mw = sample_vol<true>(M, g, x, y, z, __ldg(U + o), __ldg(U + n + o), __ldg(U + 2 * n + o), grad);
+    const double k = -2.0 * ((double)__ldg(F + g.at(x, y, z)) - mw) / (double)g.nfull;
+    G[o] = (float)(k * grad[0]);
+    G[n + o] = (float)(k * grad[1]);
+    G[2 * n + o] = (float)(k * grad[2]);
 }
 
 // K1b: LNCC forward window pass.
@@ -448,27 +539,7 @@ __global__ void __launch_bounds__(k1::NT, 2) k_lncc_fwd(Batch b, int chunk_len) 
         }
     }
 
-    // the pair's last CTA reduces the owned planes' partials, fixed order
-    const int nblk = gridDim.x * gridDim.y;
-    if (threadIdx.x == 0) {
-        __threadfence();
-        const unsigned prev = atomicAdd(&st->counter, 1u);
-        s_last = prev == (unsigned)(nblk - 1);
-    }
-    __syncthreads();
-    if (!s_last) return;
-    __threadfence();
-    double* __restrict__ psum = b.plane_sum + (long long)pair * g.nz;
-    for (int z = threadIdx.x; z < g.nz; z += NT) {
-        double s = 0.0;
-        if (z >= g.zs && z < g.ze) {
-            const double* pz = part + (long long)z * tiles * (NT / 32);
-            for (int i = 0; i < tiles * (NT / 32); ++i) s += __ldcg(pz + i);
-        }
-        if (z >= g.zs && z < g.ze) psum[z] = s;
-        else if (b.zero_foreign_planes) psum[z] = 0.0;
-    }
-    if (threadIdx.x == 0) st->counter = 0u;
+    reduce_plane_partials(b, st, part, tiles, &s_last);
 }
 
 // K5: r from the per-plane sums in z order (identical on every rank for any
@@ -1205,6 +1276,24 @@ __global__ void __launch_bounds__(k4::NT, 2) k_compose_smooth(Batch b, LmParams 
     }
 
 int plane_tiles(const Geo& g) { return cdiv(g.nx, TX) * cdiv(g.ny, TY); }
+
+void launch_mse_fwd(const Batch& b, const LmParams& p, int mode, cudaStream_t s) {
+    (void)p;
+    const dim3 wgrid(cdiv(b.g.nx, 32) * cdiv(b.g.ny, 8), b.g.ze - b.g.zs, b.pairs);
+    k_warp_moving<<<wgrid, 256, 0, s>>>(b, mode, b.g.zs);
+    const LaunchShape sh = shape_for(b.g, b.pairs, 8);
+    dim3 grid = sh.grid();
+    grid.z = b.pairs;
+    k_mse_fwd<<<grid, 256, 0, s>>>(b, sh.chunk_len);
+    g_kernel_launches += 2;
+}
+
+void launch_mse_grad(const Batch& b, const LmParams& p, cudaStream_t s) {
+    (void)p;
+    const dim3 grid(cdiv(b.g.nx, 32) * cdiv(b.g.ny, 8), b.g.ze - b.g.zs, b.pairs);
+    k_mse_grad<<<grid, 256, 0, s>>>(b);
+    ++g_kernel_launches;
+}
 
 void launch_lncc_fwd(const Batch& b, const LmParams& p, int mode, cudaStream_t s) {
     (void)p;

@@ -169,7 +169,8 @@ struct wlm_engine {
 
     // Stages of one attempt (a slab group interleaves them with exchanges).
     void stage_grad(cudaStream_t s) {
-        launch_lncc_bwd(B, P, s);
+        if (P.metric == WLM_METRIC_MSE) launch_mse_grad(B, P, s);
+        else launch_lncc_bwd(B, P, s);
         if (P.optimizer == WLM_OPT_ADAM) launch_adam(B, P, s);
     }
     void stage_step(cudaStream_t s) { launch_step_smooth(B, P, s); }
@@ -177,7 +178,10 @@ struct wlm_engine {
         launch_compose_smooth(B, P, s);
         if (P.log_jacobian) launch_jacobian_diag(B, P, s);
     }
-    void stage_eval(int mode, cudaStream_t s) { launch_lncc_fwd(B, P, mode, s); }
+    void stage_eval(int mode, cudaStream_t s) {
+        if (P.metric == WLM_METRIC_MSE) launch_mse_fwd(B, P, mode, s);
+        else launch_lncc_fwd(B, P, mode, s);
+    }
     void stage_finalize(int mode, cudaStream_t s) { launch_finalize(B, P, mode, s); }
 
     void body(cudaStream_t s) {

@@ -49,6 +49,7 @@ struct LmParams {
     double wud[8], wud_full;  // fp64 copies of the kernels (K3/K4 sum in fp64)
     double wwd[8], wwd_full;
     int radius;            // LNCC window radius (template-dispatched: 2 only in v1)
+    int metric;            // WLM_METRIC_LNCC | WLM_METRIC_MSE
 };
 
 // Buffers of a batch of `pairs` registrations of identical geometry.
@@ -78,6 +79,10 @@ struct LaunchShape {
 };
 LaunchShape shape_for(const Geo& g, int pairs, int ty);
 
+// MSE: K1a warp + per-plane sum (f - Mw)^2; gradient
+// g = -2 (f - Mw)/N grad M(x+u) (pointwise, analytic interpolant gradient).
+void launch_mse_fwd(const Batch& b, const LmParams& p, int mode, cudaStream_t s);
+void launch_mse_grad(const Batch& b, const LmParams& p, cudaStream_t s);
 // K1: warp + LNCC window moments + coefficients + sum(rho); last block runs
 // the loss/damping/rejection state machine.  mode 0 evaluates the accepted
 // warp (level start), mode 1 the attempt in the other buffer.

@@ -35,7 +35,7 @@ from dataclasses import dataclass, field as dfield
 import numpy as np
 
 from ._lib import (AdamConfig, Dims, DimensionMismatch, InvalidArgument, LmConfig, LmState,
-                   NonFiniteLoss, OPT_ADAM, OPT_GD, OPT_LM, RegConfig, StepLog, WlmError, check,
+                   METRIC_LNCC, METRIC_MSE, NonFiniteLoss, OPT_ADAM, OPT_GD, OPT_LM, RegConfig, StepLog, WlmError, check,
                    load)
 
 __all__ = [
@@ -44,7 +44,7 @@ __all__ = [
     "warp_volume", "residual_lncc", "lm_step_pointwise", "update_damping", "rejection_test",
     "downsample", "upsample_warp", "state_bytes", "register", "reg_config", "lm_config",
     "DimensionMismatch", "InvalidArgument", "NonFiniteLoss", "WlmError", "OPT_LM", "OPT_ADAM",
-    "OPT_GD", "LmState", "LmConfig",
+    "OPT_GD", "LmState", "LmConfig", "METRIC_LNCC", "METRIC_MSE", "residual_mse",
 ]
 
 _D = C.POINTER(C.c_double)
@@ -250,6 +250,19 @@ def residual_lncc(F, M, u, radius=2, gradient=True, ctx=None) -> ResidualReport:
     c.check(c.lib.wlm_residual_lncc(c.h, _p(F), _p(M), _p(u), _dims(F.shape), int(radius),
                                     C.byref(r), C.byref(ln), _p(g) if gradient else None))
     return ResidualReport(r.value, g, ln.value)
+
+
+def residual_mse(F, M, u, gradient=True, ctx=None) -> ResidualReport:
+    """residual_mse (SPEC.md:127-135): r = loss_raw = mean (f - m(x+u))^2."""
+    F, M, u = _vol(F), _vol(M), _fld(u)
+    if F.shape != M.shape or u.shape[:3] != F.shape:
+        raise DimensionMismatch(2, "residual_mse: dimension mismatch")
+    c = _ctx(ctx)
+    r = C.c_double()
+    g = np.empty(F.shape + (3,)) if gradient else None
+    c.check(c.lib.wlm_residual_mse(c.h, _p(F), _p(M), _p(u), _dims(F.shape), C.byref(r),
+                                   _p(g) if gradient else None))
+    return ResidualReport(r.value, g, r.value)
 
 
 def lm_step_pointwise(r, g, lam, ctx=None):

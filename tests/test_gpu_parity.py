@@ -399,3 +399,39 @@ def test_nccl_rank_slab_world1_matches_engine(P, ctx, extra):
     grp.close()
     assert same_trace(t, t1)
     assert np.array_equal(w, w1[0])
+
+
+# ------------------------------------------------------------------- MSE ----
+def test_residual_mse_vs_oracle(P, ctx):
+    F, M = _pair((20, 22, 24), 12)
+    F = F.astype(np.float32).astype(np.float64)
+    M = M.astype(np.float32).astype(np.float64)
+    u = smooth_field(F.shape, 7, amp=1.2).astype(np.float32).astype(np.float64)
+    rep = P.residual_mse(F, M, u, ctx=ctx)
+    r, g = O.residual_mse(F, M, u)
+    assert abs(rep.r - r) <= 1e-12 * r and rep.loss_raw == rep.r
+    assert rel(rep.g, g) < 1e-6, rel(rep.g, g)
+    z = np.zeros(F.shape + (3,))
+    assert P.residual_mse(F, F, z, ctx=ctx).r == 0.0
+    assert P.residual_mse(np.zeros_like(F), np.ones_like(F), z, ctx=ctx).r == 1.0
+
+
+def test_mse_engine_vs_oracle(P, ctx):
+    """MetricConfig.kind = mse through the device engine (K1a + MSE partials,
+    pointwise MSE gradient, same step / smoothing / compose kernels)."""
+    F, M, _ = O.synth_pair((32, 36, 40), 6, num_blobs=10, warp_max=3.0)
+    kw = dict(nlevels=1, factors=[1], iters=[30], metric=1)
+    warp, (tr,), _ = run_engine(P, ctx, F, M, P.reg_config(**kw), 30)
+    for storage, lt, wt in (("fp64", 1e-5, 1e-4), ("fp32", 1e-6, 1e-5)):
+        rc, u_o, st, tr_o = oracle_level(F, M, O.default_config(**kw), 30, storage)
+        assert rc == 0
+        compare_runs(tr, tr_o, aos(warp[0]), u_o, lt, wt)
+    assert all(t["r"] == t["loss_raw"] for t in tr)
+
+
+def test_mse_slab_group_bit_identical(P, ctx):
+    F, M, _ = O.synth_pair((20, 24, 28), 23, num_blobs=8, warp_max=2.5)
+    cfg = P.reg_config(nlevels=1, factors=[1], iters=[10], metric=1)
+    w1, (t1,), _ = run_engine(P, ctx, F, M, cfg, 10)
+    w, t, _ = run_slabs(P, ctx, F, M, cfg, 10, 3)
+    assert same_trace(t, t1) and np.array_equal(w, w1[0])

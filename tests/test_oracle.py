@@ -151,6 +151,32 @@ def test_mse_gradient_finite_differences():
     assert np.all(errs < 1e-4), errs
 
 
+def test_mse_kats():
+    """aligned pair -> 0; constant offset -> 1; at u = 0
+    r equals the plain mean-squared difference (independent one-liner)."""
+    rng = np.random.default_rng(4)
+    F = rng.uniform(size=(6, 7, 8))
+    z = np.zeros(F.shape + (3,))
+    r, g = O.residual_mse(F, F, z)
+    assert r == 0.0 and not g.any()
+    r, _ = O.residual_mse(np.zeros_like(F), np.ones_like(F), z)
+    assert r == 1.0
+    M = rng.uniform(size=F.shape)
+    r, _ = O.residual_mse(F, M, z)
+    assert abs(r - np.mean((F - M) ** 2)) <= 1e-12
+
+
+def test_mse_lm_iterate_decreases_loss():
+    """lm_run_level with MetricConfig.kind = mse (SPEC.md:121): r = loss_raw."""
+    F, M, _ = O.synth_pair((16, 16, 16), 2, num_blobs=6, warp_max=1.5)
+    cfg = O.default_config(nlevels=1, factors=[1], iters=[15], metric=1)
+    rc, u, st, tr = O.lm_run_level(F, M, np.zeros((16, 16, 16, 3)), cfg, 15)
+    assert rc == 0 and len(tr) == 15
+    assert all(t.r == t.loss_raw for t in tr)
+    r0, _ = O.residual_mse(F, M, np.zeros((16, 16, 16, 3)))
+    assert tr[-1].r < 0.8 * r0
+
+
 def test_lm_step_kats_and_sherman_morrison():
     g = np.zeros((2, 2, 2, 3)); g[0, 0, 0] = (1, 0, 0)
     out = O.lm_step_pointwise(2.0, g, 1.0)
