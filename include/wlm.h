@@ -19,6 +19,7 @@
  *   SPEC.md:127    residual_mse -> ResidualReport        wlm_residual_mse
  *   SPEC.md:136    residual_lncc -> ResidualReport       wlm_residual_lncc
  *   SPEC.md:247    lm_step_pointwise                     wlm_lm_step_pointwise
+ *   SPEC.md:301    demons_step_mse                       wlm_demons_step_mse
  *   SPEC.md:265    update_damping                        wlm_update_damping
  *   SPEC.md:274    rejection_test                        wlm_rejection_test
  *   SPEC.md:283    lm_iterate                            wlm_engine_* (device-resident)
@@ -85,7 +86,9 @@ typedef struct {
 
 typedef struct { double beta1, beta2, eps_hat, lr; } wlm_adam_config;
 
-enum { WLM_OPT_LM = 0, WLM_OPT_ADAM = 1, WLM_OPT_GD = 2 };
+/* DEMONS: Eq. 9 active forces from the MSE per-voxel residual;
+ * requires metric = MSE. */
+enum { WLM_OPT_LM = 0, WLM_OPT_ADAM = 1, WLM_OPT_GD = 2, WLM_OPT_DEMONS = 3 };
 /* MetricConfig.kind: mi is not built (WLM_UNSUPPORTED). */
 enum { WLM_METRIC_LNCC = 0, WLM_METRIC_MSE = 1 };
 #define WLM_MAX_LEVELS 8
@@ -104,6 +107,7 @@ typedef struct {
     double sigma_update, sigma_warp;
     int log_jacobian;
     int metric; /* WLM_METRIC_* (SPEC.md:121), default LNCC */
+    double demons_alpha; /* DemonsConfig.alpha, default 1 */
 } wlm_reg_config;
 
 /* RegResult.loss_trace row (CSV columns SPEC.md:427). */
@@ -160,6 +164,11 @@ wlm_status wlm_residual_mse(wlm_ctx* ctx, const double* F, const double* M, cons
                             wlm_dims d, double* r, double* g);
 wlm_status wlm_lm_step_pointwise(wlm_ctx* ctx, double r, const double* g, wlm_dims d,
                                  double lambda, double* out);
+/* demons_step_mse (Eq. 9): out = r_x n_x / (|n_x|^2 + alpha^2
+ * r_x^2), 0 where the denominator is 0.  r: per-voxel residual f - m(x+u)
+ * (N), n: moving-image gradient at x + u (AoS). */
+wlm_status wlm_demons_step_mse(wlm_ctx* ctx, const double* r, const double* n, wlm_dims d,
+                               double alpha, double* out);
 void wlm_update_damping(wlm_lm_state* s, double loss_new, const wlm_lm_config* c);
 int wlm_rejection_test(double loss_new, double loss_prev, double loss_prev2, double tau);
 wlm_status wlm_downsample(wlm_ctx* ctx, const double* vol, wlm_dims d, int factor,

@@ -52,7 +52,7 @@ class RegConfig(C.Structure):
                 ("factors", C.c_int * MAX_LEVELS), ("iters", C.c_int * MAX_LEVELS),
                 ("target_max_disp", C.c_double), ("step_floor", C.c_double),
                 ("sigma_update", C.c_double), ("sigma_warp", C.c_double),
-                ("log_jacobian", C.c_int), ("metric", C.c_int)]
+                ("log_jacobian", C.c_int), ("metric", C.c_int), ("demons_alpha", C.c_double)]
 
 
 class StepLog(C.Structure):
@@ -93,6 +93,7 @@ def _declare(lib):
         "orc_all_finite": (C.c_int, [_D, C.c_size_t]),
         "orc_residual_lncc": (C.c_double, [_D, _D, _D, Dims, C.c_int, _D, _D, _D]),
         "orc_residual_mse": (C.c_double, [_D, _D, _D, Dims, _D]),
+        "orc_demons_step_mse": (None, [_D, _D, C.c_size_t, C.c_double, _D]),
         "orc_lm_step_pointwise": (None, [C.c_double, _D, C.c_size_t, C.c_double, _D]),
         "orc_lm_step_dense3": (None, [C.c_double, _D, C.c_double, _D]),
         "orc_update_damping": (None, [C.POINTER(LmState), C.c_double, C.POINTER(LmConfig)]),
@@ -289,6 +290,13 @@ def residual_mse(F, M, u, kind="port"):
     g = np.empty(F.shape + (3,))
     r = lib(kind).orc_residual_mse(_p(F), _p(M), _p(u), dims_of(F), _p(g))
     return r, g
+
+
+def demons_step_mse(r, n, alpha, kind="port"):
+    r, n = _c64(r), _c64(n)
+    out = np.empty_like(n)
+    lib(kind).orc_demons_step_mse(_p(r), _p(n), r.size, float(alpha), _p(out))
+    return out
 
 
 def lm_step_pointwise(r, g, lam, kind="port"):

@@ -519,6 +519,8 @@ void orc_default_reg_config(orc_reg_config* c) {
     c->target_max_disp = 0.4; c->step_floor = 1e-12;      // field.hpp:75-78
     c->sigma_update = 1.0; c->sigma_warp = 0.5;
     c->log_jacobian = 0;
+    c->metric = ORC_METRIC_LNCC;
+    c->demons_alpha = 1.0;
 }
 
 double orc_sample_trilinear_grad(const double* vol, orc_dims d, double px, double py,
@@ -638,6 +640,17 @@ double orc_residual_mse(const double* F, const double* M, const double* u, orc_d
             for (int c = 0; c < 3; ++c) g[3 * i + c] = r32(k * gM[3 * i + c]);
         }
     return s / (double)N;
+}
+
+// Eq. (9): Demons active forces r_x n_x / (|n_x|^2 +
+// alpha^2 r_x^2); both terms zero -> 0.
+void orc_demons_step_mse(const double* r, const double* n, size_t N, double alpha, double* out) {
+    par_for(0, (long long)N, [&](long long i) {
+        const double rx = r[i], a = n[3 * i], b = n[3 * i + 1], c = n[3 * i + 2];
+        const double den = a * a + b * b + c * c + alpha * alpha * rx * rx;
+        const double s = den > 0.0 ? rx / den : 0.0;
+        out[3 * i] = s * a; out[3 * i + 1] = s * b; out[3 * i + 2] = s * c;
+    });
 }
 
 // Eq. (4): dU = -r g / (|g|^2 + lambda); zero gradient -> exactly zero.
@@ -813,6 +826,13 @@ int orc_lm_run_level(const double* F, const double* M, orc_dims d, double* u,
                 else orc_lm_step_pointwise(r, g.data(), N, state->lambda, step.data());
             } else if (c->optimizer == ORC_OPT_ADAM) {
                 orc_adam_step(g.data(), am.data(), av.data(), 3 * N, it + 1, &c->adam, step.data());
+            } else if (c->optimizer == ORC_OPT_DEMONS) {
+                // Eq. 9 from the MSE per-voxel residual at the accepted warp
+                Vec Mw(N), gM(3 * N), rx(N);
+                warp(M, u, d, Mw.data(), gM.data());
+                for (size_t i = 0; i < N; ++i) rx[i] = F[i] - Mw[i];
+                orc_demons_step_mse(rx.data(), gM.data(), N, c->demons_alpha, step.data());
+                for (auto& v : step) v = r32(v);  // stored where the device keeps g
             } else if (dev) {
                 dev_step32(g.data(), N, ORC_OPT_GD, 0.0, 0.0, c->gd_lr, step.data());
             } else {

@@ -48,7 +48,7 @@ typedef struct {
 /* AdamConfig. */
 typedef struct { double beta1, beta2, eps_hat, lr; } orc_adam_config;
 
-enum { ORC_OPT_LM = 0, ORC_OPT_ADAM = 1, ORC_OPT_GD = 2 };
+enum { ORC_OPT_LM = 0, ORC_OPT_ADAM = 1, ORC_OPT_GD = 2, ORC_OPT_DEMONS = 3 };
 enum { ORC_METRIC_LNCC = 0, ORC_METRIC_MSE = 1 };
 
 #define ORC_MAX_LEVELS 8
@@ -67,6 +67,7 @@ typedef struct {
     double sigma_update, sigma_warp;
     int log_jacobian; /* compute jacobian_det_min(eps*dU_s) per accepted step */
     int metric;       /* ORC_METRIC_* (MetricConfig.kind) */
+    double demons_alpha; /* DemonsConfig.alpha */
 } orc_reg_config;
 
 /* One RegResult.loss_trace row + CSV extras. */
@@ -121,7 +122,10 @@ int orc_all_finite(const double* data, size_t count);
  *   [6N,9N) gradM (AoS)                                                    */
 double orc_residual_lncc(const double* F, const double* M, const double* u, orc_dims d,
                          int radius, double* g, double* lncc, double* internals);
-/* MSE -- used only by the finite-difference self-check */
+/* demons_step_mse (Eq. 9); r: N per-voxel residuals
+ * f - m(x+u), n: AoS moving gradient at x + u. */
+void orc_demons_step_mse(const double* r, const double* n, size_t N, double alpha, double* out);
+/* MSE; g nullable */
 double orc_residual_mse(const double* F, const double* M, const double* u, orc_dims d,
                         double* g);
 

@@ -33,6 +33,14 @@ wlm_status engine_init(wlm_engine* e, wlm_ctx* ctx, wlm_dims d, int pairs, const
         set_err(ctx, "metric: only LNCC and MSE are built (MI is SURVEY §8(f) #3)");
         return WLM_UNSUPPORTED;
     }
+    if (c->optimizer < WLM_OPT_LM || c->optimizer > WLM_OPT_DEMONS) {
+        set_err(ctx, "optimizer: LM, ADAM, GD or DEMONS");
+        return WLM_INVALID_ARG;
+    }
+    if (c->optimizer == WLM_OPT_DEMONS && (c->metric != WLM_METRIC_MSE || !(c->demons_alpha > 0.0))) {
+        set_err(ctx, "DEMONS needs metric = MSE (per-voxel residual, SPEC.md:166) and alpha > 0 (SPEC.md:243)");
+        return WLM_INVALID_ARG;
+    }
     if (c->metric == WLM_METRIC_LNCC && c->lncc_radius != 2) {
         set_err(ctx, "lncc_radius != 2 is not instantiated");
         return WLM_UNSUPPORTED;
@@ -67,6 +75,7 @@ wlm_status engine_init(wlm_engine* e, wlm_ctx* ctx, wlm_dims d, int pairs, const
     P.log_jacobian = c->log_jacobian;
     P.radius = c->lncc_radius;
     P.metric = c->metric;
+    P.demons_alpha = c->demons_alpha;
     P.Ru = smooth_radius(c->sigma_update);
     P.Rw = smooth_radius(c->sigma_warp);
     if (P.Ru > 3 || P.Rw > 3) {
@@ -182,6 +191,7 @@ void wlm_default_reg_config(wlm_reg_config* c) {
     c->sigma_update = 1.0; c->sigma_warp = 0.5;
     c->log_jacobian = 0;
     c->metric = WLM_METRIC_LNCC;
+    c->demons_alpha = 1.0;
 }
 
 wlm_status wlm_ctx_create(int device, wlm_ctx** out) {

@@ -316,8 +316,10 @@ __global__ void __launch_bounds__(256) k_mse_fwd(Batch b, int chunk_len) {
 
 // MSE gradient: g = -2 (f - Mw) / N * grad M(x+u) at the accepted warp
 // (the oracle's orc_residual_mse arithmetic); skipped after a rejection, like
-// K2, because the gradient is unchanged.
-__global__ void __launch_bounds__(256) k_mse_grad(Batch b) {
+// K2, because the gradient is unchanged.  With the Demons optimizer the same
+// per-voxel residual r_x = f - Mw and n_x = grad M(x+u) give the Eq. 9 step
+// instead, which K3 then smooths like an Adam step.
+__global__ void __launch_bounds__(256) k_mse_grad(Batch b, int demons, double alpha) {
     const int pair = blockIdx.z;
     const PairState* st = b.st + pair;
     if (st->done || st->last_rejected) return;
@@ -335,7 +337,16 @@ __global__ void __launch_bounds__(256) k_mse_grad(Batch b) {
     const int o = g.lat(x, y, z);
     double grad[3];
     const double mw = sample_vol<true>(M, g, x, y, z, __ldg(U + o), __ldg(U + n + o), __ldg(U + 2 * n + o), grad);
-    const double k = -2.0 * ((double)__ldg(F + g.at(x, y, z)) - mw) / (double)g.nfull;
+    const double e = (double)__ldg(F + g.at(x, y, z)) - mw;
+    if (demons) {
+        double st3[3];
+        demons_step(e, grad[0], grad[1], grad[2], alpha, st3);
+        G[o] = (float)st3[0];
+        G[n + o] = (float)st3[1];
+        G[2 * n + o] = (float)st3[2];
+        return;
+    }
+    const double k = -2.0 * e / (double)g.nfull;
     G[o] = (float)(k * grad[0]);
     G[n + o] = (float)(k * grad[1]);
     G[2 * n + o] = (float)(k * grad[2]);
@@ -1289,9 +1300,8 @@ void launch_mse_fwd(const Batch& b, const LmParams& p, int mode, cudaStream_t s)
 }
 
 void launch_mse_grad(const Batch& b, const LmParams& p, cudaStream_t s) {
-    (void)p;
     const dim3 grid(cdiv(b.g.nx, 32) * cdiv(b.g.ny, 8), b.g.ze - b.g.zs, b.pairs);
-    k_mse_grad<<<grid, 256, 0, s>>>(b);
+    k_mse_grad<<<grid, 256, 0, s>>>(b, p.optimizer == WLM_OPT_DEMONS, p.demons_alpha);
     ++g_kernel_launches;
 }
 

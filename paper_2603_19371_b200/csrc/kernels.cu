@@ -418,6 +418,19 @@ void launch_lm_pointwise(double r, const float* g, double lambda, float* out, lo
     ++g_kernel_launches;
 }
 
+__global__ void k_demons_pointwise(const double* __restrict__ r, const double* __restrict__ n, long long N,
+                                   double alpha, double* __restrict__ out) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < N;
+         i += (long long)gridDim.x * blockDim.x)
+        demons_step(r[i], n[3 * i], n[3 * i + 1], n[3 * i + 2], alpha, out + 3 * i);
+}
+
+void launch_demons_pointwise(const double* r, const double* n, long long N, double alpha, double* out,
+                             cudaStream_t s) {
+    k_demons_pointwise<<<grid_for(N, 256), 256, 0, s>>>(r, n, N, alpha, out);
+    ++g_kernel_launches;
+}
+
 __global__ void k_nonfinite(const float* __restrict__ v, long long count, int* flag) {
     int bad = 0;
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < count;

@@ -50,6 +50,7 @@ struct LmParams {
     double wwd[8], wwd_full;
     int radius;            // LNCC window radius (template-dispatched: 2 only in v1)
     int metric;            // WLM_METRIC_LNCC | WLM_METRIC_MSE
+    double demons_alpha;   // DemonsConfig.alpha (optimizer DEMONS)
 };
 
 // Buffers of a batch of `pairs` registrations of identical geometry.
@@ -122,6 +123,16 @@ void launch_warp(const float* M, const float* u, float* Mw, float* gM, const Geo
                  cudaStream_t s);
 void launch_max_abs(const float* v, long long count, unsigned* out_bits, cudaStream_t s);
 void launch_jacdet(const float* u, const Geo& g, int* out_ordered, cudaStream_t s);
+// Eq. 9 in fp64 with the oracle's operation order (no contraction): bitwise
+// equal to orc_demons_step_mse.  r: [N], n, out: AoS [N][3].
+__device__ __forceinline__ void demons_step(double rx, double a, double b, double c, double alpha, double* o) {
+    const double den = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(a, a), __dmul_rn(b, b)), __dmul_rn(c, c)),
+                                 __dmul_rn(__dmul_rn(__dmul_rn(alpha, alpha), rx), rx));
+    const double s = den > 0.0 ? __ddiv_rn(rx, den) : 0.0;
+    o[0] = __dmul_rn(s, a); o[1] = __dmul_rn(s, b); o[2] = __dmul_rn(s, c);
+}
+void launch_demons_pointwise(const double* r, const double* n, long long N, double alpha, double* out,
+                             cudaStream_t s);
 void launch_lm_pointwise(double r, const float* g, double lambda, float* out, long long n,
                          cudaStream_t s);
 void launch_nonfinite(const float* v, long long count, int* flag, cudaStream_t s);

@@ -252,6 +252,21 @@ wlm_status wlm_residual_mse(wlm_ctx* ctx, const double* F, const double* M, cons
     return s;
 }
 
+wlm_status wlm_demons_step_mse(wlm_ctx* ctx, const double* r, const double* n, wlm_dims d, double alpha,
+                               double* out) {
+    if (!r || !n || !out || !valid_dims(d) || !(alpha > 0.0))
+        return bad(ctx, WLM_INVALID_ARG, "demons_step_mse: bad args (alpha > 0, SPEC.md:243)");
+    return run(ctx, [&] {
+        const size_t N = nvox(d);
+        DevBuf<double> dr(ctx, N), dn(ctx, 3 * N), dout(ctx, 3 * N);
+        CK(cudaMemcpyAsync(dr.p, r, sizeof(double) * N, cudaMemcpyHostToDevice, ctx->stream));
+        CK(cudaMemcpyAsync(dn.p, n, sizeof(double) * 3 * N, cudaMemcpyHostToDevice, ctx->stream));
+        launch_demons_pointwise(dr.p, dn.p, (long long)N, alpha, dout.p, ctx->stream);
+        CK(cudaMemcpyAsync(out, dout.p, sizeof(double) * 3 * N, cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
 wlm_status wlm_lm_step_pointwise(wlm_ctx* ctx, double r, const double* g, wlm_dims d, double lambda,
                                  double* out) {
     if (!g || !out || !valid_dims(d) || !(lambda > 0.0))

@@ -35,7 +35,7 @@ from dataclasses import dataclass, field as dfield
 import numpy as np
 
 from ._lib import (AdamConfig, Dims, DimensionMismatch, InvalidArgument, LmConfig, LmState,
-                   METRIC_LNCC, METRIC_MSE, NonFiniteLoss, OPT_ADAM, OPT_GD, OPT_LM, RegConfig, StepLog, WlmError, check,
+                   METRIC_LNCC, METRIC_MSE, NonFiniteLoss, OPT_ADAM, OPT_DEMONS, OPT_GD, OPT_LM, RegConfig, StepLog, WlmError, check,
                    load)
 
 __all__ = [
@@ -44,7 +44,8 @@ __all__ = [
     "warp_volume", "residual_lncc", "lm_step_pointwise", "update_damping", "rejection_test",
     "downsample", "upsample_warp", "state_bytes", "register", "reg_config", "lm_config",
     "DimensionMismatch", "InvalidArgument", "NonFiniteLoss", "WlmError", "OPT_LM", "OPT_ADAM",
-    "OPT_GD", "LmState", "LmConfig", "METRIC_LNCC", "METRIC_MSE", "residual_mse",
+    "OPT_GD", "OPT_DEMONS", "LmState", "LmConfig", "METRIC_LNCC", "METRIC_MSE", "residual_mse",
+    "demons_step_mse",
 ]
 
 _D = C.POINTER(C.c_double)
@@ -263,6 +264,18 @@ def residual_mse(F, M, u, gradient=True, ctx=None) -> ResidualReport:
     c.check(c.lib.wlm_residual_mse(c.h, _p(F), _p(M), _p(u), _dims(F.shape), C.byref(r),
                                    _p(g) if gradient else None))
     return ResidualReport(r.value, g, r.value)
+
+
+def demons_step_mse(r, n, alpha=1.0, ctx=None):
+    """demons_step_mse (Eq. 9): r (nz,ny,nx) per-voxel residual,
+    n (nz,ny,nx,3) moving gradient; returns the (nz,ny,nx,3) update."""
+    r, n = _vol(r), _fld(n)
+    if n.shape[:3] != r.shape:
+        raise DimensionMismatch(2, "demons_step_mse: dimension mismatch")
+    c = _ctx(ctx)
+    out = np.empty_like(n)
+    c.check(c.lib.wlm_demons_step_mse(c.h, _p(r), _p(n), _dims(r.shape), float(alpha), _p(out)))
+    return out
 
 
 def lm_step_pointwise(r, g, lam, ctx=None):

@@ -435,3 +435,27 @@ def test_mse_slab_group_bit_identical(P, ctx):
     w1, (t1,), _ = run_engine(P, ctx, F, M, cfg, 10)
     w, t, _ = run_slabs(P, ctx, F, M, cfg, 10, 3)
     assert same_trace(t, t1) and np.array_equal(w, w1[0])
+
+
+# ---------------------------------------------------------------- Demons ----
+def test_demons_step_mirror_bitwise(P, ctx):
+    rng = np.random.default_rng(5)
+    r = rng.normal(size=(6, 7, 8))
+    n = rng.normal(size=(6, 7, 8, 3))
+    r[0, 0, 0] = 0.0; n[0, 0, 0] = 0.0  # zero denominator -> 0
+    for alpha in (0.5, 1.0):
+        assert np.array_equal(P.demons_step_mse(r, n, alpha, ctx=ctx), O.demons_step_mse(r, n, alpha))
+    out = P.demons_step_mse(np.ones((1, 1, 1)), np.array([[[[2.0, 0, 0]]]]), 1.0, ctx=ctx)
+    assert np.allclose(out[0, 0, 0], [0.4, 0, 0], rtol=0, atol=1e-15)
+
+
+def test_demons_engine_vs_oracle(P, ctx):
+    F, M, _ = O.synth_pair((24, 28, 32), 9, num_blobs=8, warp_max=2.5)
+    kw = dict(nlevels=1, factors=[1], iters=[20], metric=1, optimizer=3, demons_alpha=1.0)
+    warp, (tr,), _ = run_engine(P, ctx, F, M, P.reg_config(**kw), 20)
+    for storage, lt, wt in (("fp64", 1e-5, 1e-4), ("fp32", 1e-6, 1e-5)):
+        rc, u_o, _, tr_o = oracle_level(F, M, O.default_config(**kw), 20, storage)
+        assert rc == 0
+        compare_runs(tr, tr_o, aos(warp[0]), u_o, lt, wt)
+    with pytest.raises(P.InvalidArgument):  # Demons needs the MSE per-voxel residual
+        P.Engine((8, 8, 8), 1, P.reg_config(optimizer=3), ctx=ctx)

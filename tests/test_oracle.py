@@ -177,6 +177,38 @@ def test_mse_lm_iterate_decreases_loss():
     assert tr[-1].r < 0.8 * r0
 
 
+def test_demons_kats_and_lm_equivalence():
+    """SPEC.md:305-308, :327, :484: r_x = 0 -> 0; n = (2,0,0), r = 1, alpha = 1
+    -> (0.4, 0, 0); equals per-voxel LM with r := r_x, lambda := alpha^2 r_x^2
+    (g := -n, the gradient of r_x = f - m(x+u)) to 1e-12."""
+    assert not O.demons_step_mse(np.zeros((2, 2, 2)), np.ones((2, 2, 2, 3)), 1.0).any()
+    out = O.demons_step_mse(np.ones((1, 1, 1)), np.array([[[[2.0, 0.0, 0.0]]]]), 1.0)
+    assert np.allclose(out[0, 0, 0], [0.4, 0.0, 0.0], rtol=0, atol=1e-15)
+    # zero denominator (n = 0 and r = 0) -> 0, not NaN
+    assert not O.demons_step_mse(np.zeros((1, 1, 1)), np.zeros((1, 1, 1, 3)), 1.0).any()
+    rng = np.random.default_rng(17)
+    F = O.gaussian_smooth(rng.uniform(size=(8, 9, 10)), 1.0)
+    M = O.gaussian_smooth(rng.uniform(size=(8, 9, 10)), 1.0)
+    u = smooth_field((8, 9, 10), 5, amp=0.8) + 0.2
+    Mw, gM = O.warp_volume(M, u)
+    rx = F - Mw
+    for alpha in (0.5, 1.0, 2.0):
+        d = O.demons_step_mse(rx, gM, alpha)
+        lm = np.empty_like(d)
+        for i in np.ndindex(rx.shape):
+            lm[i] = O.lm_step_pointwise(rx[i], -gM[i].reshape(1, 1, 1, 3), alpha ** 2 * rx[i] ** 2)[0, 0, 0]
+        assert np.abs(d - lm).max() < 1e-12
+
+
+def test_demons_registration_decreases_mse():
+    F, M, _ = O.synth_pair((16, 16, 16), 3, num_blobs=6, warp_max=1.5)
+    cfg = O.default_config(nlevels=1, factors=[1], iters=[15], metric=1, optimizer=3)
+    rc, u, st, tr = O.lm_run_level(F, M, np.zeros((16, 16, 16, 3)), cfg, 15)
+    assert rc == 0 and len(tr) == 15 and all(t.lam == 0.0 for t in tr)
+    r0, _ = O.residual_mse(F, M, np.zeros((16, 16, 16, 3)))
+    assert tr[-1].r < 0.8 * r0
+
+
 def test_lm_step_kats_and_sherman_morrison():
     g = np.zeros((2, 2, 2, 3)); g[0, 0, 0] = (1, 0, 0)
     out = O.lm_step_pointwise(2.0, g, 1.0)
