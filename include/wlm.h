@@ -19,6 +19,7 @@
  *   SPEC.md:127    residual_mse -> ResidualReport        wlm_residual_mse
  *   SPEC.md:136    residual_lncc -> ResidualReport       wlm_residual_lncc
  *   SPEC.md:247    lm_step_pointwise                     wlm_lm_step_pointwise
+ *   SPEC.md:256    lm_step_tiled                         wlm_lm_step_tiled
  *   SPEC.md:301    demons_step_mse                       wlm_demons_step_mse
  *   SPEC.md:265    update_damping                        wlm_update_damping
  *   SPEC.md:274    rejection_test                        wlm_rejection_test
@@ -71,7 +72,7 @@ typedef struct { int nx, ny, nz; } wlm_dims;
 /* LmConfig. lambda_max <= 0 or inf: uncapped. */
 typedef struct {
     double lambda0, mu_plus, mu_minus;
-    int tile_size;   /* 1 only (tiled LM is UNSUPPORTED) */
+    int tile_size;   /* k of Eq. 5 (1 = pointwise Eq. 4); slab groups: 1 only */
     int rejection;
     double tau, lambda_max;
     int max_retries;
@@ -164,6 +165,11 @@ wlm_status wlm_residual_mse(wlm_ctx* ctx, const double* F, const double* M, cons
                             wlm_dims d, double* r, double* g);
 wlm_status wlm_lm_step_pointwise(wlm_ctx* ctx, double r, const double* g, wlm_dims d,
                                  double lambda, double* out);
+/* lm_step_tiled (Eq. 5): non-overlapping k^3 tiles (partial
+ * at the far faces), H = sum g g^T per tile, Delta u = -r (H + lambda I)^{-1} g
+ * with the explicit 3x3 inverse; fp64, bitwise the oracle's. */
+wlm_status wlm_lm_step_tiled(wlm_ctx* ctx, double r, const double* g, wlm_dims d, double lambda,
+                             int k, double* out);
 /* demons_step_mse (Eq. 9): out = r_x n_x / (|n_x|^2 + alpha^2
  * r_x^2), 0 where the denominator is 0.  r: per-voxel residual f - m(x+u)
  * (N), n: moving-image gradient at x + u (AoS). */

@@ -96,6 +96,7 @@ def _declare(lib):
         "orc_demons_step_mse": (None, [_D, _D, C.c_size_t, C.c_double, _D]),
         "orc_lm_step_pointwise": (None, [C.c_double, _D, C.c_size_t, C.c_double, _D]),
         "orc_lm_step_dense3": (None, [C.c_double, _D, C.c_double, _D]),
+        "orc_lm_step_tiled": (None, [C.c_double, _D, Dims, C.c_double, C.c_int, _D]),
         "orc_update_damping": (None, [C.POINTER(LmState), C.c_double, C.POINTER(LmConfig)]),
         "orc_rejection_test": (C.c_int, [C.c_double, C.c_double, C.c_double, C.c_double]),
         "orc_lm_replay": (C.c_int, [_D, C.c_int, C.c_int, C.POINTER(LmConfig), _D, _I,
@@ -303,6 +304,13 @@ def lm_step_pointwise(r, g, lam, kind="port"):
     g = _c64(g)
     out = np.empty_like(g)
     lib(kind).orc_lm_step_pointwise(float(r), _p(g), g.size // 3, float(lam), _p(out))
+    return out
+
+
+def lm_step_tiled(r, g, lam, k, kind="port"):
+    g = _c64(g)
+    out = np.empty_like(g)
+    lib(kind).orc_lm_step_tiled(float(r), _p(g), dims_of(g[..., 0]), float(lam), int(k), _p(out))
     return out
 
 

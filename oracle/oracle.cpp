@@ -642,6 +642,48 @@ double orc_residual_mse(const double* F, const double* M, const double* u, orc_d
     return s / (double)N;
 }
 
+// Eq. (5): tiled LM.  Non-overlapping k^3 tiles (partial at
+// the far faces); H = sum over the tile of g g^T, accumulated in z, y, x
+// order; Delta u(x) = -r (H + lambda I)^{-1} g(x) with the explicit
+// (adjugate / determinant) inverse of the symmetric 3x3.
+void tile_step_matrix(const double H[6], double r, double lambda, double Mout[6]) {
+    // H = [a b c; b d e; c e f] + lambda I
+    const double a = H[0] + lambda, b = H[1], c = H[2], d = H[3] + lambda, e = H[4], f = H[5] + lambda;
+    const double c00 = d * f - e * e, c01 = c * e - b * f, c02 = b * e - c * d;
+    const double c11 = a * f - c * c, c12 = b * c - a * e, c22 = a * d - b * b;
+    const double det = a * c00 + b * c01 + c * c02;
+    const double s = -r / det;
+    Mout[0] = s * c00; Mout[1] = s * c01; Mout[2] = s * c02;
+    Mout[3] = s * c11; Mout[4] = s * c12; Mout[5] = s * c22;
+}
+void orc_lm_step_tiled(double r, const double* g, orc_dims d, double lambda, int k, double* out) {
+    const int tx = (d.nx + k - 1) / k, ty = (d.ny + k - 1) / k, tz = (d.nz + k - 1) / k;
+    par_for(0, (long long)tx * ty * tz, [&](long long t) {
+        const int bx = (int)(t % tx), by = (int)((t / tx) % ty), bz = (int)(t / ((long long)tx * ty));
+        const int x1 = std::min(d.nx, (bx + 1) * k), y1 = std::min(d.ny, (by + 1) * k),
+                  z1 = std::min(d.nz, (bz + 1) * k);
+        double H[6] = {0, 0, 0, 0, 0, 0};
+        for (int z = bz * k; z < z1; ++z)
+            for (int y = by * k; y < y1; ++y)
+                for (int x = bx * k; x < x1; ++x) {
+                    const double* gi = g + 3 * lin(d, x, y, z);
+                    H[0] += gi[0] * gi[0]; H[1] += gi[0] * gi[1]; H[2] += gi[0] * gi[2];
+                    H[3] += gi[1] * gi[1]; H[4] += gi[1] * gi[2]; H[5] += gi[2] * gi[2];
+                }
+        double Mt[6];
+        tile_step_matrix(H, r, lambda, Mt);
+        for (int z = bz * k; z < z1; ++z)
+            for (int y = by * k; y < y1; ++y)
+                for (int x = bx * k; x < x1; ++x) {
+                    const size_t i = 3 * lin(d, x, y, z);
+                    const double g0 = g[i], g1 = g[i + 1], g2 = g[i + 2];
+                    out[i] = Mt[0] * g0 + Mt[1] * g1 + Mt[2] * g2;
+                    out[i + 1] = Mt[1] * g0 + Mt[3] * g1 + Mt[4] * g2;
+                    out[i + 2] = Mt[2] * g0 + Mt[4] * g1 + Mt[5] * g2;
+                }
+    });
+}
+
 // Eq. (9): Demons active forces r_x n_x / (|n_x|^2 +
 // alpha^2 r_x^2); both terms zero -> 0.
 void orc_demons_step_mse(const double* r, const double* n, size_t N, double alpha, double* out) {
@@ -821,7 +863,9 @@ int orc_lm_run_level(const double* F, const double* M, orc_dims d, double* u,
         for (;;) {
             const bool dev = g_fp32_storage == 2 && (g_dev_flags & 1);
             const bool dev4 = g_fp32_storage == 2 && (g_dev_flags & 2);
-            if (c->optimizer == ORC_OPT_LM) {
+            if (c->optimizer == ORC_OPT_LM && c->lm.tile_size > 1) {
+                orc_lm_step_tiled(r, g.data(), d, state->lambda, c->lm.tile_size, step.data());
+            } else if (c->optimizer == ORC_OPT_LM) {
                 if (dev) dev_step32(g.data(), N, ORC_OPT_LM, r, state->lambda, 0.0, step.data());
                 else orc_lm_step_pointwise(r, g.data(), N, state->lambda, step.data());
             } else if (c->optimizer == ORC_OPT_ADAM) {
@@ -900,7 +944,7 @@ int orc_register(const float* Ff, const float* Mf, orc_dims d, const orc_reg_con
         if (c->factors[l] < 1 || c->iters[l] < 0) return ORC_INVALID_ARG;
         if (l > 0 && c->factors[l] >= c->factors[l - 1]) return ORC_INVALID_ARG;
     }
-    if (c->lm.tile_size != 1) return ORC_UNSUPPORTED;
+    if (c->lm.tile_size < 1) return ORC_INVALID_ARG;
     const size_t N = nvox(d);
     Vec F(Ff, Ff + N), M(Mf, Mf + N);
     orc_lm_state st{c->lm.lambda0, 0, 0.0, 0.0};

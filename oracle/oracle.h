@@ -134,6 +134,8 @@ void orc_lm_step_pointwise(double r, const double* g, size_t nvox, double lambda
                            double* out);
 /* Explicit 3x3 damped solve (g g^T + lambda I) d = -r g (Appendix A oracle). */
 void orc_lm_step_dense3(double r, const double* g3, double lambda, double* out3);
+/* lm_step_tiled (Eq. 5): k^3 tiles, explicit 3x3 inverse. */
+void orc_lm_step_tiled(double r, const double* g, orc_dims d, double lambda, int k, double* out);
 void orc_update_damping(orc_lm_state* s, double loss_new, const orc_lm_config* c);
 int orc_rejection_test(double loss_new, double loss_prev, double loss_prev2, double tau);
 /* Scripted-residual harness: replays `losses` (one per attempt)

@@ -93,6 +93,7 @@ SIGNATURES = {
     "wlm_residual_lncc": (C.c_int, [_CTX, _D, _D, _D, Dims, C.c_int, _D, _D, _D]),
     "wlm_residual_mse": (C.c_int, [_CTX, _D, _D, _D, Dims, _D, _D]),
     "wlm_demons_step_mse": (C.c_int, [_CTX, _D, _D, Dims, C.c_double, _D]),
+    "wlm_lm_step_tiled": (C.c_int, [_CTX, C.c_double, _D, Dims, C.c_double, C.c_int, _D]),
     "wlm_lm_step_pointwise": (C.c_int, [_CTX, C.c_double, _D, Dims, C.c_double, _D]),
     "wlm_update_damping": (None, [C.POINTER(LmState), C.c_double, C.POINTER(LmConfig)]),
     "wlm_rejection_test": (C.c_int, [C.c_double, C.c_double, C.c_double, C.c_double]),

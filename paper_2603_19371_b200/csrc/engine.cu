@@ -25,9 +25,9 @@ wlm_status engine_init(wlm_engine* e, wlm_ctx* ctx, wlm_dims d, int pairs, const
     e->g = make_geo(d);
     e->pairs = pairs;
     e->cfg = *c;
-    if (c->lm.tile_size != 1) {
-        set_err(ctx, "tile_size > 1 (tiled LM, SPEC.md:256) is not implemented on the device");
-        return WLM_UNSUPPORTED;
+    if (c->lm.tile_size < 1) {
+        set_err(ctx, "lm.tile_size must be >= 1 (SPEC.md:259)");
+        return WLM_INVALID_ARG;
     }
     if (c->metric != WLM_METRIC_LNCC && c->metric != WLM_METRIC_MSE) {
         set_err(ctx, "metric: only LNCC and MSE are built (MI is SURVEY §8(f) #3)");
@@ -76,6 +76,7 @@ wlm_status engine_init(wlm_engine* e, wlm_ctx* ctx, wlm_dims d, int pairs, const
     P.radius = c->lncc_radius;
     P.metric = c->metric;
     P.demons_alpha = c->demons_alpha;
+    P.tile_k = c->lm.tile_size;
     P.Ru = smooth_radius(c->sigma_update);
     P.Rw = smooth_radius(c->sigma_warp);
     if (P.Ru > 3 || P.Rw > 3) {
@@ -117,6 +118,13 @@ void engine_alloc(wlm_engine* e) {
     const int tiles = plane_tiles(e->g);
     e->partials = DevBuf<double>(ctx, B * (size_t)e->g.nz * tiles * 8);
     if (!e->shared_plane_sum) e->plane_sum = DevBuf<double>(ctx, B * (size_t)e->g.nz);
+    if (e->P.tile_k > 1) {  // tiled LM (Eq. 5): one matrix per k^3 tile
+        const int k = e->P.tile_k;
+        e->B.tkx = (e->g.nx + k - 1) / k;
+        e->B.tky = (e->g.ny + k - 1) / k;
+        e->B.tkz = (e->g.nz + k - 1) / k;
+        e->TM = DevBuf<double>(ctx, B * 6 * (size_t)e->B.tkx * e->B.tky * e->B.tkz);
+    }
     e->trace = DevBuf<wlm_step_log>(ctx, B * (size_t)e->P.trace_cap);
     e->P.trace = e->trace.p;
     Batch& b = e->B;
@@ -131,6 +139,7 @@ void engine_alloc(wlm_engine* e) {
     if (!e->shared_plane_sum) b.plane_sum = e->plane_sum.p;
     b.zero_foreign_planes = 0;
     b.shift_part = e->shift_part.p;
+    b.TM = e->TM.p;
     b.max_blocks = tiles;
     CK(cudaMemsetAsync(e->U.p, 0, sizeof(float) * B * 6 * n, ctx->stream));
     launch_begin_level(b, e->P, 0, 1, e->cfg.lm.lambda0, ctx->stream);

@@ -813,7 +813,7 @@ struct Shape {
 };
 }  // namespace k3
 
-template <int R>
+template <int R, bool TILED>
 __global__ void __launch_bounds__(k3::NT, 2) k_step_smooth(Batch b, LmParams p, int chunk_len) {
     using S = k3::Shape<R>;
     constexpr int TX = k3::TX, NT = k3::NT, W = 2 * R + 1;
@@ -861,12 +861,31 @@ __global__ void __launch_bounds__(k3::NT, 2) k_step_smooth(Batch b, LmParams p, 
             }
         }
     };
+    // tiled LM (Eq. 5): the item's k^3 tile matrix -r (H + lambda I)^{-1}
+    const int tk = p.tile_k;
+    constexpr bool tiled = TILED;  // launched only for LM with tile_size > 1
+    const double* __restrict__ TM = tiled ? b.TM + (long long)pair * 6 * b.tkx * b.tky * b.tkz : nullptr;
+    int htile[SL];  // (y tile) * tkx + x tile of each halo item
+#pragma unroll
+    for (int s = 0; s < SL; ++s) {
+        const int idx = threadIdx.x + s * NT;
+        const int gx = x0 - R + idx % IWP, gy = y0 - R + idx / IWP;
+        htile[s] = (tiled && hoff[s] >= 0) ? (gy / tk) * b.tkx + gx / tk : 0;
+    }
+    int hz = 0;  // z tile of the plane being stored
     auto store_halo = [&](double* dst) {
 #pragma unroll
         for (int s = 0; s < SL; ++s) {
             const int idx = threadIdx.x + s * NT;
             if (idx >= NI) continue;
             const double a = hg[s][0], bb = hg[s][1], c = hg[s][2];
+            if (tiled) {
+                const double* M6 = TM + ((long long)hz * b.tkx * b.tky + htile[s]) * 6;
+                dst[idx] = M6[0] * a + M6[1] * bb + M6[2] * c;
+                dst[NI + idx] = M6[1] * a + M6[3] * bb + M6[4] * c;
+                dst[2 * NI + idx] = M6[2] * a + M6[4] * bb + M6[5] * c;
+                continue;
+            }
             double k = kc;
             if (opt == WLM_OPT_LM) k = -r * rcp_d(fma(a, a, fma(bb, bb, c * c)) + lam);
             dst[idx] = k * a;
@@ -922,9 +941,12 @@ __global__ void __launch_bounds__(k3::NT, 2) k_step_smooth(Batch b, LmParams p, 
     double* in_b = &s_in[1][0][0];  // halo tile of plane p + 1 (x-passed)
     double* x_a = &s_x[0][0][0];    // x-passed plane p (y-passed)
     double* x_b = &s_x[1][0][0];
+    auto ztile = [&](int z) { return tiled && z >= 0 && z < g.nz ? z / tk : 0; };
     load_halo(z0);
+    hz = ztile(z0);
     store_halo(in_a);
     load_halo(z0 + 1);
+    hz = ztile(z0 + 1);
     store_halo(in_b);
     __syncthreads();
     x_pass(in_a, x_a);
@@ -958,6 +980,7 @@ __global__ void __launch_bounds__(k3::NT, 2) k_step_smooth(Batch b, LmParams p, 
                     }
                 }
                 x_pass(in_b, x_b);
+                hz = ztile(zi + 2);
                 store_halo(in_a);
                 load_halo(zi + 3);
                 double* t = in_a; in_a = in_b; in_b = t;
@@ -1335,7 +1358,11 @@ void launch_step_smooth(const Batch& b, const LmParams& p, cudaStream_t s) {
     const LaunchShape sh = shape_for(b.g, b.pairs, k3::TY);
     dim3 grid = sh.grid();
     grid.z = b.pairs;
-    WLM_DISPATCH_R(p.Ru, (k_step_smooth<RR><<<grid, k3::NT, 0, s>>>(b, p, sh.chunk_len)));
+    if (p.optimizer == WLM_OPT_LM && p.tile_k > 1) {
+        WLM_DISPATCH_R(p.Ru, (k_step_smooth<RR, true><<<grid, k3::NT, 0, s>>>(b, p, sh.chunk_len)));
+    } else {
+        WLM_DISPATCH_R(p.Ru, (k_step_smooth<RR, false><<<grid, k3::NT, 0, s>>>(b, p, sh.chunk_len)));
+    }
     ++g_kernel_launches;
 }
 

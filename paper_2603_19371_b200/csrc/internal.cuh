@@ -151,7 +151,7 @@ struct wlm_engine {
     DevBuf<float> F, M, U, ABE, G, VS, AM, AV;
     DevBuf<double> MW;
     DevBuf<PairState> st;
-    DevBuf<double> partials, script, shift_part, plane_sum;
+    DevBuf<double> partials, script, shift_part, plane_sum, TM;
     DevBuf<wlm_step_log> trace;
     Batch B{};
     cudaGraphExec_t step_exec = nullptr, loop_exec = nullptr;
@@ -173,7 +173,10 @@ struct wlm_engine {
         else launch_lncc_bwd(B, P, s);
         if (P.optimizer == WLM_OPT_ADAM) launch_adam(B, P, s);
     }
-    void stage_step(cudaStream_t s) { launch_step_smooth(B, P, s); }
+    void stage_step(cudaStream_t s) {
+        if (P.optimizer == WLM_OPT_LM && P.tile_k > 1) launch_tile_matrix(B, P, s);
+        launch_step_smooth(B, P, s);
+    }
     void stage_compose(cudaStream_t s) {
         launch_compose_smooth(B, P, s);
         if (P.log_jacobian) launch_jacobian_diag(B, P, s);

@@ -418,6 +418,94 @@ void launch_lm_pointwise(double r, const float* g, double lambda, float* out, lo
     ++g_kernel_launches;
 }
 
+// -r (H + lambda I)^{-1} by the adjugate, rounding steps as the oracle's
+// tile_step_matrix (no contraction).
+__device__ __forceinline__ void tile_matrix(const double H[6], double r, double lambda, double* Mo) {
+    const double a = __dadd_rn(H[0], lambda), b = H[1], c = H[2], d = __dadd_rn(H[3], lambda), e = H[4],
+                 f = __dadd_rn(H[5], lambda);
+    const double c00 = __dsub_rn(__dmul_rn(d, f), __dmul_rn(e, e));
+    const double c01 = __dsub_rn(__dmul_rn(c, e), __dmul_rn(b, f));
+    const double c02 = __dsub_rn(__dmul_rn(b, e), __dmul_rn(c, d));
+    const double c11 = __dsub_rn(__dmul_rn(a, f), __dmul_rn(c, c));
+    const double c12 = __dsub_rn(__dmul_rn(b, c), __dmul_rn(a, e));
+    const double c22 = __dsub_rn(__dmul_rn(a, d), __dmul_rn(b, b));
+    const double det = __dadd_rn(__dadd_rn(__dmul_rn(a, c00), __dmul_rn(b, c01)), __dmul_rn(c, c02));
+    const double s = __ddiv_rn(-r, det);
+    Mo[0] = __dmul_rn(s, c00); Mo[1] = __dmul_rn(s, c01); Mo[2] = __dmul_rn(s, c02);
+    Mo[3] = __dmul_rn(s, c11); Mo[4] = __dmul_rn(s, c12); Mo[5] = __dmul_rn(s, c22);
+}
+__device__ __forceinline__ void add_outer(double H[6], double g0, double g1, double g2) {
+    H[0] = __dadd_rn(H[0], __dmul_rn(g0, g0)); H[1] = __dadd_rn(H[1], __dmul_rn(g0, g1));
+    H[2] = __dadd_rn(H[2], __dmul_rn(g0, g2)); H[3] = __dadd_rn(H[3], __dmul_rn(g1, g1));
+    H[4] = __dadd_rn(H[4], __dmul_rn(g1, g2)); H[5] = __dadd_rn(H[5], __dmul_rn(g2, g2));
+}
+
+// Engine: one thread per (pair, tile); g is the stored fp32 gradient (SoA).
+__global__ void k_tile_matrix(Batch b, LmParams p) {
+    const long long ntiles = (long long)b.tkx * b.tky * b.tkz;
+    const int pair = blockIdx.y;
+    const PairState* st = b.st + pair;
+    if (st->done) return;
+    const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (t >= ntiles) return;
+    const Geo g = b.g;
+    const int k = p.tile_k;
+    const int bx = (int)(t % b.tkx), by = (int)((t / b.tkx) % b.tky), bz = (int)(t / ((long long)b.tkx * b.tky));
+    const int x1 = min(g.nx, (bx + 1) * k), y1 = min(g.ny, (by + 1) * k), z1 = min(g.nz, (bz + 1) * k);
+    const float* G = b.G + (long long)pair * 3 * g.n;
+    double H[6] = {0, 0, 0, 0, 0, 0};
+    for (int z = bz * k; z < z1; ++z)
+        for (int y = by * k; y < y1; ++y)
+            for (int x = bx * k; x < x1; ++x) {
+                const int o = g.lat(x, y, z);
+                add_outer(H, G[o], G[g.n + o], G[2 * g.n + o]);
+            }
+    tile_matrix(H, st->r_cur, st->lambda, b.TM + ((long long)pair * ntiles + t) * 6);
+}
+
+void launch_tile_matrix(const Batch& b, const LmParams& p, cudaStream_t s) {
+    const long long ntiles = (long long)b.tkx * b.tky * b.tkz;
+    k_tile_matrix<<<dim3((unsigned)((ntiles + 127) / 128), b.pairs), 128, 0, s>>>(b, p);
+    ++g_kernel_launches;
+}
+
+// Mirror op (fp64 AoS, one thread per tile): bitwise the oracle's
+// orc_lm_step_tiled.
+__global__ void k_lm_tiled_fp64(double r, const double* __restrict__ g, Geo geo, double lambda, int k, int tkx,
+                                int tky, int tkz, double* __restrict__ out) {
+    const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (t >= (long long)tkx * tky * tkz) return;
+    const int bx = (int)(t % tkx), by = (int)((t / tkx) % tky), bz = (int)(t / ((long long)tkx * tky));
+    const int x1 = min(geo.nx, (bx + 1) * k), y1 = min(geo.ny, (by + 1) * k), z1 = min(geo.nz, (bz + 1) * k);
+    double H[6] = {0, 0, 0, 0, 0, 0};
+    for (int z = bz * k; z < z1; ++z)
+        for (int y = by * k; y < y1; ++y)
+            for (int x = bx * k; x < x1; ++x) {
+                const double* gi = g + 3 * (long long)geo.at(x, y, z);
+                add_outer(H, gi[0], gi[1], gi[2]);
+            }
+    double M[6];
+    tile_matrix(H, r, lambda, M);
+    for (int z = bz * k; z < z1; ++z)
+        for (int y = by * k; y < y1; ++y)
+            for (int x = bx * k; x < x1; ++x) {
+                const long long i = 3 * (long long)geo.at(x, y, z);
+                const double g0 = g[i], g1 = g[i + 1], g2 = g[i + 2];
+                out[i] = __dadd_rn(__dadd_rn(__dmul_rn(M[0], g0), __dmul_rn(M[1], g1)), __dmul_rn(M[2], g2));
+                out[i + 1] = __dadd_rn(__dadd_rn(__dmul_rn(M[1], g0), __dmul_rn(M[3], g1)), __dmul_rn(M[4], g2));
+                out[i + 2] = __dadd_rn(__dadd_rn(__dmul_rn(M[2], g0), __dmul_rn(M[4], g1)), __dmul_rn(M[5], g2));
+            }
+}
+
+void launch_lm_tiled_fp64(double r, const double* g, const Geo& geo, double lambda, int k, double* tm,
+                          double* out, cudaStream_t s) {
+    (void)tm;
+    const int tkx = cdiv(geo.nx, k), tky = cdiv(geo.ny, k), tkz = cdiv(geo.nz, k);
+    const long long nt = (long long)tkx * tky * tkz;
+    k_lm_tiled_fp64<<<(unsigned)((nt + 127) / 128), 128, 0, s>>>(r, g, geo, lambda, k, tkx, tky, tkz, out);
+    ++g_kernel_launches;
+}
+
 __global__ void k_demons_pointwise(const double* __restrict__ r, const double* __restrict__ n, long long N,
                                    double alpha, double* __restrict__ out) {
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < N;

@@ -51,6 +51,7 @@ struct LmParams {
     int radius;            // LNCC window radius (template-dispatched: 2 only in v1)
     int metric;            // WLM_METRIC_LNCC | WLM_METRIC_MSE
     double demons_alpha;   // DemonsConfig.alpha (optimizer DEMONS)
+    int tile_k;            // LmConfig.tile_size (Eq. 5); 1 = pointwise Eq. 4
 };
 
 // Buffers of a batch of `pairs` registrations of identical geometry.
@@ -71,6 +72,8 @@ struct Batch {
     double* partials; // [pair][nz][tiles][8] per-(plane, tile, warp) sum(rho)
     double* plane_sum;  // [pair][nz] per-plane sum(rho) (global z; shared by slabs)
     int zero_foreign_planes;  // NCCL slabs: zero non-owned planes before the all-reduce
+    double* TM;       // [pair][tiles][6] tiled LM: -r (H + lambda I)^{-1} (symmetric), or null
+    int tkx, tky, tkz;  // tile counts (tile_k > 1)
     int max_blocks;
 };
 
@@ -123,6 +126,11 @@ void launch_warp(const float* M, const float* u, float* Mw, float* gM, const Geo
                  cudaStream_t s);
 void launch_max_abs(const float* v, long long count, unsigned* out_bits, cudaStream_t s);
 void launch_jacdet(const float* u, const Geo& g, int* out_ordered, cudaStream_t s);
+// Tiled LM (Eq. 5): per-tile -r (H + lambda I)^{-1}, H = sum g g^T.
+void launch_tile_matrix(const Batch& b, const LmParams& p, cudaStream_t s);
+// Mirror op: the same in fp64 on AoS buffers, operation order of the oracle.
+void launch_lm_tiled_fp64(double r, const double* g, const Geo& geo, double lambda, int k, double* tm,
+                          double* out, cudaStream_t s);
 // Eq. 9 in fp64 with the oracle's operation order (no contraction): bitwise
 // equal to orc_demons_step_mse.  r: [N], n, out: AoS [N][3].
 __device__ __forceinline__ void demons_step(double rx, double a, double b, double c, double alpha, double* o) {

@@ -252,6 +252,20 @@ wlm_status wlm_residual_mse(wlm_ctx* ctx, const double* F, const double* M, cons
     return s;
 }
 
+wlm_status wlm_lm_step_tiled(wlm_ctx* ctx, double r, const double* g, wlm_dims d, double lambda, int k,
+                             double* out) {
+    if (!g || !out || !valid_dims(d) || !(lambda > 0.0) || k < 1)
+        return bad(ctx, WLM_INVALID_ARG, "lm_step_tiled: bad args (lambda > 0, k >= 1)");
+    return run(ctx, [&] {
+        const size_t N = nvox(d);
+        DevBuf<double> dg(ctx, 3 * N), dout(ctx, 3 * N);
+        CK(cudaMemcpyAsync(dg.p, g, sizeof(double) * 3 * N, cudaMemcpyHostToDevice, ctx->stream));
+        launch_lm_tiled_fp64(r, dg.p, make_geo(d), lambda, k, nullptr, dout.p, ctx->stream);
+        CK(cudaMemcpyAsync(out, dout.p, sizeof(double) * 3 * N, cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
 wlm_status wlm_demons_step_mse(wlm_ctx* ctx, const double* r, const double* n, wlm_dims d, double alpha,
                                double* out) {
     if (!r || !n || !out || !valid_dims(d) || !(alpha > 0.0))

@@ -440,8 +440,12 @@ wlm_status make_group(wlm_ctx* ctx, wlm_dims d, int nslabs, int first, int count
     return WLM_OK;
 }
 
-wlm_status check_split(wlm_ctx* ctx, wlm_dims d, int nslabs) {
+wlm_status check_split(wlm_ctx* ctx, wlm_dims d, int nslabs, const wlm_reg_config* cfg) {
     if (!ctx || nslabs < 1 || !valid_dims(d)) return WLM_INVALID_ARG;
+    if (cfg->lm.tile_size != 1) {
+        set_err(ctx, "slab_group: tiled LM (tile_size > 1) pools g over tiles that cross slabs; not built");
+        return WLM_UNSUPPORTED;
+    }
     if (d.nz / nslabs < kHalo) {
         set_err(ctx, "slab_group: every slab needs at least 4 planes (halo depth)");
         return WLM_INVALID_ARG;
@@ -473,7 +477,7 @@ wlm_status wlm_slab_group_create(wlm_ctx* ctx, wlm_dims d, int nslabs, const wlm
                                  wlm_slab_group** out) {
     if (!out || !cfg) return WLM_INVALID_ARG;
     *out = nullptr;
-    const wlm_status s = check_split(ctx, d, nslabs);
+    const wlm_status s = check_split(ctx, d, nslabs, cfg);
     if (s != WLM_OK) return s;
     return make_group(ctx, d, nslabs, 0, nslabs, cfg, nullptr, out);
 }
@@ -492,7 +496,7 @@ wlm_status wlm_slab_group_create_nccl(wlm_ctx* ctx, wlm_dims d, int rank, int nr
                                       const char* nccl_lib, const wlm_reg_config* cfg, wlm_slab_group** out) {
     if (!out || !cfg || !id || rank < 0 || rank >= nranks) return WLM_INVALID_ARG;
     *out = nullptr;
-    wlm_status s = check_split(ctx, d, nranks);
+    wlm_status s = check_split(ctx, d, nranks, cfg);
     if (s != WLM_OK) return s;
     std::string why;
     if (!nccl::load(nccl_lib, &why)) {

@@ -45,7 +45,7 @@ __all__ = [
     "downsample", "upsample_warp", "state_bytes", "register", "reg_config", "lm_config",
     "DimensionMismatch", "InvalidArgument", "NonFiniteLoss", "WlmError", "OPT_LM", "OPT_ADAM",
     "OPT_GD", "OPT_DEMONS", "LmState", "LmConfig", "METRIC_LNCC", "METRIC_MSE", "residual_mse",
-    "demons_step_mse",
+    "demons_step_mse", "lm_step_tiled",
 ]
 
 _D = C.POINTER(C.c_double)
@@ -264,6 +264,15 @@ def residual_mse(F, M, u, gradient=True, ctx=None) -> ResidualReport:
     c.check(c.lib.wlm_residual_mse(c.h, _p(F), _p(M), _p(u), _dims(F.shape), C.byref(r),
                                    _p(g) if gradient else None))
     return ResidualReport(r.value, g, r.value)
+
+
+def lm_step_tiled(r, g, lam, k, ctx=None):
+    """lm_step_tiled (Eq. 5) on the GPU, fp64."""
+    g = _fld(g)
+    c = _ctx(ctx)
+    out = np.empty_like(g)
+    c.check(c.lib.wlm_lm_step_tiled(c.h, float(r), _p(g), _dims(g.shape), float(lam), int(k), _p(out)))
+    return out
 
 
 def demons_step_mse(r, n, alpha=1.0, ctx=None):

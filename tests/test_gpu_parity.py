@@ -459,3 +459,24 @@ def test_demons_engine_vs_oracle(P, ctx):
         compare_runs(tr, tr_o, aos(warp[0]), u_o, lt, wt)
     with pytest.raises(P.InvalidArgument):  # Demons needs the MSE per-voxel residual
         P.Engine((8, 8, 8), 1, P.reg_config(optimizer=3), ctx=ctx)
+
+
+# -------------------------------------------------------------- tiled LM ----
+def test_tiled_lm_mirror_bitwise(P, ctx):
+    rng = np.random.default_rng(9)
+    for shape, k in (((6, 6, 6), 3), ((7, 5, 9), 2), ((9, 8, 7), 4), ((5, 6, 7), 1)):
+        g = rng.normal(size=shape + (3,))
+        assert np.array_equal(P.lm_step_tiled(0.3, g, 0.2, k, ctx=ctx), O.lm_step_tiled(0.3, g, 0.2, k))
+
+
+@pytest.mark.parametrize("k", [2, 3])
+def test_tiled_lm_engine_vs_oracle(P, ctx, k):
+    F, M, _ = O.synth_pair((24, 28, 32), 14, num_blobs=8, warp_max=2.5)
+    kw = dict(nlevels=1, factors=[1], iters=[20], **{"lm.tile_size": k})
+    warp, (tr,), _ = run_engine(P, ctx, F, M, P.reg_config(**kw), 20)
+    for storage, lt, wt in (("fp64", 1e-5, 1e-4), ("fp32", 1e-6, 1e-5)):
+        rc, u_o, _, tr_o = oracle_level(F, M, O.default_config(**kw), 20, storage)
+        assert rc == 0
+        compare_runs(tr, tr_o, aos(warp[0]), u_o, lt, wt)
+    with pytest.raises(P.WlmError):  # slab groups pool only pointwise steps
+        P.SlabGroup((24, 28, 32), 2, cfg=P.reg_config(**kw), ctx=ctx)

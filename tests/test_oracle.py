@@ -177,6 +177,41 @@ def test_mse_lm_iterate_decreases_loss():
     assert tr[-1].r < 0.8 * r0
 
 
+def _dense_tiled(r, g, lam, k):
+    """Independent dense per-tile assemble-and-solve."""
+    out = np.empty_like(g)
+    nz, ny, nx, _ = g.shape
+    for z0 in range(0, nz, k):
+        for y0 in range(0, ny, k):
+            for x0 in range(0, nx, k):
+                blk = g[z0:z0 + k, y0:y0 + k, x0:x0 + k].reshape(-1, 3)
+                H = blk.T @ blk + lam * np.eye(3)
+                sol = np.linalg.solve(H, -r * blk.T).T
+                out[z0:z0 + k, y0:y0 + k, x0:x0 + k] = sol.reshape(g[z0:z0 + k, y0:y0 + k, x0:x0 + k].shape)
+    return out
+
+
+def test_tiled_lm_kats():
+    """k = 1 == pointwise to 1e-12; g = 0 -> 0; random
+    6^3 and 7^3 (partial tiles), k = 3 (and 2, 4) == dense per-tile solve."""
+    rng = np.random.default_rng(21)
+    g = rng.normal(size=(5, 6, 7, 3))
+    assert np.abs(O.lm_step_tiled(0.7, g, 0.3, 1) - O.lm_step_pointwise(0.7, g, 0.3)).max() < 1e-12
+    assert not O.lm_step_tiled(0.7, np.zeros_like(g), 0.3, 3).any()
+    for shape, k in (((6, 6, 6), 3), ((7, 7, 7), 3), ((7, 5, 9), 2), ((8, 7, 6), 4)):
+        g = rng.normal(size=shape + (3,)) * rng.uniform(0.01, 2.0)
+        lam = rng.uniform(0.01, 3.0)
+        ref = _dense_tiled(0.4, g, lam, k)
+        assert np.abs(O.lm_step_tiled(0.4, g, lam, k) - ref).max() < 1e-10
+
+
+def test_tiled_lm_iterate():
+    F, M, _ = O.synth_pair((16, 16, 16), 5, num_blobs=6, warp_max=1.5)
+    cfg = O.default_config(nlevels=1, factors=[1], iters=[10], **{"lm.tile_size": 3})
+    rc, u, st, tr = O.lm_run_level(F, M, np.zeros((16, 16, 16, 3)), cfg, 10)
+    assert rc == 0 and len(tr) == 10 and tr[-1].r < tr[0].r
+
+
 def test_demons_kats_and_lm_equivalence():
     """SPEC.md:305-308, :327, :484: r_x = 0 -> 0; n = (2,0,0), r = 1, alpha = 1
     -> (0.4, 0, 0); equals per-voxel LM with r := r_x, lambda := alpha^2 r_x^2
