@@ -17,6 +17,7 @@
  *   field.hpp:114  gaussian_smooth(DispField3)           wlm_gaussian_smooth_field
  *   field.hpp:116-117 all_finite                         wlm_all_finite
  *   SPEC.md:127    residual_mse -> ResidualReport        wlm_residual_mse
+ *   SPEC.md:145    residual_mi -> ResidualReport         wlm_residual_mi
  *   SPEC.md:136    residual_lncc -> ResidualReport       wlm_residual_lncc
  *   SPEC.md:247    lm_step_pointwise                     wlm_lm_step_pointwise
  *   SPEC.md:256    lm_step_tiled                         wlm_lm_step_tiled
@@ -90,8 +91,8 @@ typedef struct { double beta1, beta2, eps_hat, lr; } wlm_adam_config;
 /* DEMONS: Eq. 9 active forces from the MSE per-voxel residual;
  * requires metric = MSE. */
 enum { WLM_OPT_LM = 0, WLM_OPT_ADAM = 1, WLM_OPT_GD = 2, WLM_OPT_DEMONS = 3 };
-/* MetricConfig.kind: mi is not built (WLM_UNSUPPORTED). */
-enum { WLM_METRIC_LNCC = 0, WLM_METRIC_MSE = 1 };
+/* MetricConfig.kind. */
+enum { WLM_METRIC_LNCC = 0, WLM_METRIC_MSE = 1, WLM_METRIC_MI = 2 };
 #define WLM_MAX_LEVELS 8
 
 /* RegConfig + MetricConfig + StepScale. */
@@ -109,6 +110,8 @@ typedef struct {
     int log_jacobian;
     int metric; /* WLM_METRIC_* (SPEC.md:121), default LNCC */
     double demons_alpha; /* DemonsConfig.alpha, default 1 */
+    int mi_bins;         /* MetricConfig.mi_bins B, 2..64 (default 32) */
+    double mi_sigma;     /* MetricConfig.mi_parzen_sigma in bin widths, (0, 2] (default 1) */
 } wlm_reg_config;
 
 /* RegResult.loss_trace row (CSV columns SPEC.md:427). */
@@ -159,6 +162,10 @@ wlm_status wlm_all_finite(wlm_ctx* ctx, const double* data, size_t count, int* o
 wlm_status wlm_residual_lncc(wlm_ctx* ctx, const double* F, const double* M,
                              const double* u, wlm_dims d, int radius, double* r,
                              double* lncc, double* g /* nullable, AoS */);
+/* residual_mi: Parzen-window MI in bits on a B x B grid
+ * (A13-A15); r = log2 B - MI; g nullable, AoS. */
+wlm_status wlm_residual_mi(wlm_ctx* ctx, const double* F, const double* M, const double* u,
+                           wlm_dims d, int bins, double sigma, double* r, double* mi, double* g);
 /* residual_mse: r = mean (f - m(x+u))^2, g = grad_u r with
  * the analytic interpolant gradient; g nullable, AoS. */
 wlm_status wlm_residual_mse(wlm_ctx* ctx, const double* F, const double* M, const double* u,

@@ -52,7 +52,8 @@ class RegConfig(C.Structure):
                 ("factors", C.c_int * MAX_LEVELS), ("iters", C.c_int * MAX_LEVELS),
                 ("target_max_disp", C.c_double), ("step_floor", C.c_double),
                 ("sigma_update", C.c_double), ("sigma_warp", C.c_double),
-                ("log_jacobian", C.c_int), ("metric", C.c_int), ("demons_alpha", C.c_double)]
+                ("log_jacobian", C.c_int), ("metric", C.c_int), ("demons_alpha", C.c_double),
+                ("mi_bins", C.c_int), ("mi_sigma", C.c_double)]
 
 
 class StepLog(C.Structure):
@@ -93,6 +94,7 @@ def _declare(lib):
         "orc_all_finite": (C.c_int, [_D, C.c_size_t]),
         "orc_residual_lncc": (C.c_double, [_D, _D, _D, Dims, C.c_int, _D, _D, _D]),
         "orc_residual_mse": (C.c_double, [_D, _D, _D, Dims, _D]),
+        "orc_residual_mi": (C.c_double, [_D, _D, _D, Dims, C.c_int, C.c_double, _D, _D]),
         "orc_demons_step_mse": (None, [_D, _D, C.c_size_t, C.c_double, _D]),
         "orc_lm_step_pointwise": (None, [C.c_double, _D, C.c_size_t, C.c_double, _D]),
         "orc_lm_step_dense3": (None, [C.c_double, _D, C.c_double, _D]),
@@ -284,6 +286,16 @@ def residual_lncc(F, M, u, radius=2, internals=False, kind="port"):
                             it[5 * N:6 * N].reshape(s), it[6 * N:].reshape(s + (3,)))
         return r, g, ln.value, ins
     return r, g, ln.value
+
+
+def residual_mi(F, M, u, bins=32, sigma=1.0, kind="port"):
+    """(r, g, MI): r = log2(bins) - MI in bits."""
+    F, M, u = _c64(F), _c64(M), _c64(u)
+    g = np.empty(F.shape + (3,))
+    mi = C.c_double()
+    r = lib(kind).orc_residual_mi(_p(F), _p(M), _p(u), dims_of(F), int(bins), float(sigma), _p(g),
+                                  C.byref(mi))
+    return r, g, mi.value
 
 
 def residual_mse(F, M, u, kind="port"):

@@ -521,6 +521,7 @@ void orc_default_reg_config(orc_reg_config* c) {
     c->log_jacobian = 0;
     c->metric = ORC_METRIC_LNCC;
     c->demons_alpha = 1.0;
+    c->mi_bins = 32; c->mi_sigma = 1.0;
 }
 
 double orc_sample_trilinear_grad(const double* vol, orc_dims d, double px, double py,
@@ -695,6 +696,109 @@ void orc_demons_step_mse(const double* r, const double* n, size_t N, double alph
     });
 }
 
+// ---- Parzen-window mutual information ----
+// Pinned choices (A13-A15): F and M min-max normalised over the
+// whole (level) volume; Parzen coordinate t = v (B - 1), bins 0..B-1; kernel
+// exp(-s^2 / 2 sigma^2) on |s| <= 4 sigma (sigma in bin widths), normalised
+// per sample over the in-range bins, so p = (1/N) sum_x a(t_f) b(t_m)^T sums
+// to 1; logs floored at 1e-12; MI in bits, r = log2 B - MI.
+struct Parzen {
+    int lo, n;        // first bin, bin count (<= 9 for sigma = 1)
+    double w[64], dw[64];  // normalised weights and d/dt
+};
+Parzen parzen(double t, int B, double sigma) {
+    Parzen P;
+    const double reach = 4.0 * sigma;
+    int lo = (int)std::ceil(t - reach), hi = (int)std::floor(t + reach);
+    lo = std::max(lo, 0);
+    hi = std::min(hi, B - 1);
+    P.lo = lo;
+    P.n = std::max(0, std::min(hi - lo + 1, 64));
+    double S = 0.0, Sd = 0.0, raw[64], draw[64];
+    for (int k = 0; k < P.n; ++k) {
+        const double sft = t - (double)(lo + k);
+        raw[k] = std::exp(-0.5 * sft * sft / (sigma * sigma));
+        draw[k] = -sft / (sigma * sigma) * raw[k];
+        S += raw[k];
+        Sd += draw[k];
+    }
+    for (int k = 0; k < P.n; ++k) {
+        P.w[k] = raw[k] / S;
+        P.dw[k] = (draw[k] * S - raw[k] * Sd) / (S * S);
+    }
+    return P;
+}
+void minmax(const double* v, size_t N, double* lo, double* range) {
+    double a = v[0], b = v[0];
+    for (size_t i = 1; i < N; ++i) { a = std::min(a, v[i]); b = std::max(b, v[i]); }
+    *lo = a;
+    *range = b > a ? b - a : 1.0;
+}
+
+double orc_residual_mi(const double* F, const double* M, const double* u, orc_dims d, int B, double sigma,
+                       double* g, double* mi_out) {
+    if (B < 2 || !(sigma > 0.0)) return kNaN;
+    const size_t N = nvox(d);
+    Vec Mw(N), gM(3 * N);
+    warp(M, u, d, Mw.data(), gM.data());
+    double flo, frange, mlo, mrange;
+    minmax(F, N, &flo, &frange);
+    minmax(M, N, &mlo, &mrange);
+    const double sf = (double)(B - 1) / frange, sm = (double)(B - 1) / mrange;
+    std::vector<double> P((size_t)B * B, 0.0);
+    // fixed serial order
+    for (size_t i = 0; i < N; ++i) {
+        const Parzen a = parzen((F[i] - flo) * sf, B, sigma), b = parzen((Mw[i] - mlo) * sm, B, sigma);
+        for (int ii = 0; ii < a.n; ++ii)
+            for (int jj = 0; jj < b.n; ++jj) P[(size_t)(a.lo + ii) * B + b.lo + jj] += a.w[ii] * b.w[jj];
+    }
+    const double invN = 1.0 / (double)N, eps = 1e-12, il2 = 1.0 / std::log(2.0);
+    std::vector<double> pf(B, 0.0), pm(B, 0.0);
+    for (int i = 0; i < B; ++i)
+        for (int j = 0; j < B; ++j) {
+            const double p = P[(size_t)i * B + j] * invN;
+            P[(size_t)i * B + j] = p;
+            pf[i] += p;
+            pm[j] += p;
+        }
+    double mi = 0.0;
+    for (int i = 0; i < B; ++i)
+        for (int j = 0; j < B; ++j) {
+            const double p = P[(size_t)i * B + j];
+            mi += p * std::log2(std::max(p, eps));
+        }
+    for (int i = 0; i < B; ++i) mi -= pf[i] * std::log2(std::max(pf[i], eps));
+    for (int j = 0; j < B; ++j) mi -= pm[j] * std::log2(std::max(pm[j], eps));
+    if (mi_out) *mi_out = mi;
+    if (g) {
+        // dMI/dp_ij (joint minus moving-marginal part; the fixed marginal does
+        // not depend on u)
+        std::vector<double> T((size_t)B * B);
+        for (int i = 0; i < B; ++i)
+            for (int j = 0; j < B; ++j) {
+                const double p = P[(size_t)i * B + j];
+                const double lj = std::log2(std::max(p, eps)) + (p >= eps ? il2 : 0.0);
+                const double lm = std::log2(std::max(pm[j], eps)) + (pm[j] >= eps ? il2 : 0.0);
+                T[(size_t)i * B + j] = lj - lm;
+            }
+        par_for(0, (long long)N, [&](long long ix) {
+            const size_t i = (size_t)ix;
+            const Parzen a = parzen((F[i] - flo) * sf, B, sigma), b = parzen((Mw[i] - mlo) * sm, B, sigma);
+            double s = 0.0;
+            for (int ii = 0; ii < a.n; ++ii) {
+                double t = 0.0;
+                for (int jj = 0; jj < b.n; ++jj) t += b.dw[jj] * T[(size_t)(a.lo + ii) * B + b.lo + jj];
+                s += a.w[ii] * t;
+            }
+            const double dr = -invN * sm * s;  // dr/dMw = -dMI/dMw
+            g[3 * i] = r32(dr * gM[3 * i]);
+            g[3 * i + 1] = r32(dr * gM[3 * i + 1]);
+            g[3 * i + 2] = r32(dr * gM[3 * i + 2]);
+        });
+    }
+    return std::log2((double)B) - mi;
+}
+
 // Eq. (4): dU = -r g / (|g|^2 + lambda); zero gradient -> exactly zero.
 void orc_lm_step_pointwise(double r, const double* g, size_t n, double lambda, double* out) {
     par_for(0, (long long)n, [&](long long i) {
@@ -850,6 +954,7 @@ int orc_lm_run_level(const double* F, const double* M, orc_dims d, double* u,
             *raw = m;
             return m;
         }
+        if (c->metric == ORC_METRIC_MI) return orc_residual_mi(F, M, uu, d, c->mi_bins, c->mi_sigma, gg, raw);
         return orc_residual_lncc(F, M, uu, d, R, gg, raw, nullptr);
     };
     double lncc = 0.0;

@@ -49,7 +49,7 @@ typedef struct {
 typedef struct { double beta1, beta2, eps_hat, lr; } orc_adam_config;
 
 enum { ORC_OPT_LM = 0, ORC_OPT_ADAM = 1, ORC_OPT_GD = 2, ORC_OPT_DEMONS = 3 };
-enum { ORC_METRIC_LNCC = 0, ORC_METRIC_MSE = 1 };
+enum { ORC_METRIC_LNCC = 0, ORC_METRIC_MSE = 1, ORC_METRIC_MI = 2 };
 
 #define ORC_MAX_LEVELS 8
 /* RegConfig, SPEC.md:352-355 plus MetricConfig and
@@ -68,6 +68,8 @@ typedef struct {
     int log_jacobian; /* compute jacobian_det_min(eps*dU_s) per accepted step */
     int metric;       /* ORC_METRIC_* (MetricConfig.kind) */
     double demons_alpha; /* DemonsConfig.alpha */
+    int mi_bins;         /* MetricConfig.mi_bins B */
+    double mi_sigma;     /* MetricConfig.mi_parzen_sigma, bin widths */
 } orc_reg_config;
 
 /* One RegResult.loss_trace row + CSV extras. */
@@ -125,6 +127,9 @@ double orc_residual_lncc(const double* F, const double* M, const double* u, orc_
 /* demons_step_mse (Eq. 9); r: N per-voxel residuals
  * f - m(x+u), n: AoS moving gradient at x + u. */
 void orc_demons_step_mse(const double* r, const double* n, size_t N, double alpha, double* out);
+/* MI: r = log2 B - MI (bits), g nullable; *mi = MI. */
+double orc_residual_mi(const double* F, const double* M, const double* u, orc_dims d, int B, double sigma,
+                       double* g, double* mi);
 /* MSE; g nullable */
 double orc_residual_mse(const double* F, const double* M, const double* u, orc_dims d,
                         double* g);

@@ -14,7 +14,7 @@ LIB_PATH = os.path.join(HERE, "libwarplm_b200.so")
 
 MAX_LEVELS = 8
 OPT_LM, OPT_ADAM, OPT_GD, OPT_DEMONS = 0, 1, 2, 3
-METRIC_LNCC, METRIC_MSE = 0, 1
+METRIC_LNCC, METRIC_MSE, METRIC_MI = 0, 1, 2
 
 STATUS = {0: "OK", 1: "INVALID_ARG", 2: "DIM_MISMATCH", 3: "NONFINITE", 4: "OOM", 5: "CUDA",
           6: "UNSUPPORTED"}
@@ -45,7 +45,8 @@ class RegConfig(C.Structure):
                 ("factors", C.c_int * MAX_LEVELS), ("iters", C.c_int * MAX_LEVELS),
                 ("target_max_disp", C.c_double), ("step_floor", C.c_double),
                 ("sigma_update", C.c_double), ("sigma_warp", C.c_double),
-                ("log_jacobian", C.c_int), ("metric", C.c_int), ("demons_alpha", C.c_double)]
+                ("log_jacobian", C.c_int), ("metric", C.c_int), ("demons_alpha", C.c_double),
+                ("mi_bins", C.c_int), ("mi_sigma", C.c_double)]
 
 
 class SynthSpec(C.Structure):
@@ -92,6 +93,7 @@ SIGNATURES = {
     "wlm_all_finite": (C.c_int, [_CTX, _D, C.c_size_t, C.POINTER(C.c_int)]),
     "wlm_residual_lncc": (C.c_int, [_CTX, _D, _D, _D, Dims, C.c_int, _D, _D, _D]),
     "wlm_residual_mse": (C.c_int, [_CTX, _D, _D, _D, Dims, _D, _D]),
+    "wlm_residual_mi": (C.c_int, [_CTX, _D, _D, _D, Dims, C.c_int, C.c_double, _D, _D, _D]),
     "wlm_demons_step_mse": (C.c_int, [_CTX, _D, _D, Dims, C.c_double, _D]),
     "wlm_lm_step_tiled": (C.c_int, [_CTX, C.c_double, _D, Dims, C.c_double, C.c_int, _D]),
     "wlm_lm_step_pointwise": (C.c_int, [_CTX, C.c_double, _D, Dims, C.c_double, _D]),

@@ -29,9 +29,14 @@ wlm_status engine_init(wlm_engine* e, wlm_ctx* ctx, wlm_dims d, int pairs, const
         set_err(ctx, "lm.tile_size must be >= 1 (SPEC.md:259)");
         return WLM_INVALID_ARG;
     }
-    if (c->metric != WLM_METRIC_LNCC && c->metric != WLM_METRIC_MSE) {
-        set_err(ctx, "metric: only LNCC and MSE are built (MI is SURVEY §8(f) #3)");
-        return WLM_UNSUPPORTED;
+    if (c->metric != WLM_METRIC_LNCC && c->metric != WLM_METRIC_MSE && c->metric != WLM_METRIC_MI) {
+        set_err(ctx, "metric: LNCC, MSE or MI");
+        return WLM_INVALID_ARG;
+    }
+    if (c->metric == WLM_METRIC_MI && (c->mi_bins < 2 || c->mi_bins > 64 || !(c->mi_sigma > 0.0) ||
+                                       c->mi_sigma > 2.0)) {
+        set_err(ctx, "MI: mi_bins in [2, 64] (SPEC.md:124), mi_sigma in (0, 2] bin widths");
+        return WLM_INVALID_ARG;
     }
     if (c->optimizer < WLM_OPT_LM || c->optimizer > WLM_OPT_DEMONS) {
         set_err(ctx, "optimizer: LM, ADAM, GD or DEMONS");
@@ -77,6 +82,8 @@ wlm_status engine_init(wlm_engine* e, wlm_ctx* ctx, wlm_dims d, int pairs, const
     P.metric = c->metric;
     P.demons_alpha = c->demons_alpha;
     P.tile_k = c->lm.tile_size;
+    P.mi_bins = c->mi_bins;
+    P.mi_sigma = c->mi_sigma;
     P.Ru = smooth_radius(c->sigma_update);
     P.Rw = smooth_radius(c->sigma_warp);
     if (P.Ru > 3 || P.Rw > 3) {
@@ -103,7 +110,7 @@ void engine_alloc(wlm_engine* e) {
     e->U = DevBuf<float>(ctx, B * 6 * n);
     e->ABE = DevBuf<float>(ctx, B * 4 * n);  // A, B fp32 + E fp64
     e->MW = DevBuf<double>(ctx, B * n);
-    e->shift_part = DevBuf<double>(ctx, B * 2 * 256);
+    e->shift_part = DevBuf<double>(ctx, B * 2 * 256 * 3);  // sums + (min, max)
     init_constants();
     e->G = DevBuf<float>(ctx, B * 3 * n);
     e->VS = DevBuf<float>(ctx, B * 3 * n);
@@ -125,6 +132,12 @@ void engine_alloc(wlm_engine* e) {
         e->B.tkz = (e->g.nz + k - 1) / k;
         e->TM = DevBuf<double>(ctx, B * 6 * (size_t)e->B.tkx * e->B.tky * e->B.tkz);
     }
+    if (e->P.metric == WLM_METRIC_MI) {
+        const size_t bb = (size_t)e->P.mi_bins * e->P.mi_bins;
+        e->HIST = DevBuf<unsigned long long>(ctx, B * bb);
+        e->MIT = DevBuf<double>(ctx, B * bb);
+        CK(cudaMemsetAsync(e->HIST.p, 0, sizeof(unsigned long long) * B * bb, ctx->stream));
+    }
     e->trace = DevBuf<wlm_step_log>(ctx, B * (size_t)e->P.trace_cap);
     e->P.trace = e->trace.p;
     Batch& b = e->B;
@@ -140,6 +153,8 @@ void engine_alloc(wlm_engine* e) {
     b.zero_foreign_planes = 0;
     b.shift_part = e->shift_part.p;
     b.TM = e->TM.p;
+    b.HIST = e->HIST.p;
+    b.MIT = e->MIT.p;
     b.max_blocks = tiles;
     CK(cudaMemsetAsync(e->U.p, 0, sizeof(float) * B * 6 * n, ctx->stream));
     launch_begin_level(b, e->P, 0, 1, e->cfg.lm.lambda0, ctx->stream);
@@ -201,6 +216,8 @@ void wlm_default_reg_config(wlm_reg_config* c) {
     c->log_jacobian = 0;
     c->metric = WLM_METRIC_LNCC;
     c->demons_alpha = 1.0;
+    c->mi_bins = 32;
+    c->mi_sigma = 1.0;
 }
 
 wlm_status wlm_ctx_create(int device, wlm_ctx** out) {

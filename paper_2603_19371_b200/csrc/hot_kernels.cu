@@ -73,9 +73,11 @@ __device__ bool rejection_fires(const PairState* st, const LmParams& p, double r
 // val: mean rho (LNCC: loss_raw = LNCC, r = 1 - LNCC) or the MSE (loss_raw =
 // r = MSE).  PairState's lncc_* fields hold loss_raw.
 __device__ void finalize_pair(PairState* st, const LmParams& p, int mode, double val, int pair) {
+    // loss_raw -> r: LNCC 1 - LNCC, MSE itself, MI log2 B - MI
+    const double top = p.metric == WLM_METRIC_MI ? log2((double)p.mi_bins) : 1.0;
     const bool mse = p.metric == WLM_METRIC_MSE;
     double lncc = val;
-    double r = mse ? val : 1.0 - val;
+    double r = mse ? val : top - val;
     if (mode == 0) {
         st->r_cur = r;
         st->lncc_cur = lncc;
@@ -86,7 +88,7 @@ __device__ void finalize_pair(PairState* st, const LmParams& p, int mode, double
     }
     if (p.script && p.script_n > 0) {
         r = p.script[(long long)pair * p.script_n + min(st->attempt, p.script_n - 1)];
-        lncc = mse ? r : 1.0 - r;
+        lncc = mse ? r : top - r;
     }
     st->attempt += 1;
     st->r_try = r;
@@ -350,6 +352,150 @@ __global__ void __launch_bounds__(256) k_mse_grad(Batch b, int demons, double al
     G[o] = (float)(k * grad[0]);
     G[n + o] = (float)(k * grad[1]);
     G[2 * n + o] = (float)(k * grad[2]);
+}
+
+// ---- MI (A13-A15, the oracle's orc_residual_mi) ----
+constexpr int kParzenMax = 17;  // bins reached by |t - k| <= 4 sigma, sigma <= 2
+struct ParzenD {
+    int lo, n;
+    double w[kParzenMax], dw[kParzenMax];
+};
+__device__ __forceinline__ void parzen_d(double t, int B, double sigma, ParzenD& P, bool deriv) {
+    const double reach = 4.0 * sigma;
+    const int lo = max((int)ceil(t - reach), 0), hi = min((int)floor(t + reach), B - 1);
+    P.lo = lo;
+    P.n = max(0, min(hi - lo + 1, kParzenMax));
+    double S = 0.0, Sd = 0.0;
+    for (int k = 0; k < P.n; ++k) {
+        const double sft = t - (double)(lo + k);
+        const double raw = exp(-0.5 * sft * sft / (sigma * sigma));
+        P.w[k] = raw;
+        P.dw[k] = -sft / (sigma * sigma) * raw;
+        S += raw;
+        Sd += P.dw[k];
+    }
+    for (int k = 0; k < P.n; ++k) {
+        if (deriv) P.dw[k] = (P.dw[k] * S - P.w[k] * Sd) / (S * S);
+        P.w[k] = P.w[k] / S;
+    }
+}
+__device__ __forceinline__ double mi_scale(double lo, double hi, int B) {
+    return (double)(B - 1) / (hi > lo ? hi - lo : 1.0);
+}
+
+// Joint histogram of the owned voxels: per-CTA fixed-point (2^-32) shared
+// histogram, integer atomics (exact, so the sum is independent of order,
+// chunking and slab split), merged into HIST.
+__global__ void __launch_bounds__(256) k_mi_hist(Batch b, LmParams p, int chunk_len) {
+    extern __shared__ unsigned long long sh_hist[];
+    const int pair = blockIdx.z;
+    const PairState* st = b.st + pair;
+    if (st->done) return;
+    const Geo g = b.g;
+    const int B = p.mi_bins;
+    for (int i = threadIdx.x; i < B * B; i += blockDim.x) sh_hist[i] = 0ull;
+    __syncthreads();
+    const int nxy = g.nx * g.ny;
+    const int tiles_x = cdiv(g.nx, 32);
+    const int x = (blockIdx.x % tiles_x) * 32 + (threadIdx.x & 31), y = (blockIdx.x / tiles_x) * 8 + (threadIdx.x >> 5);
+    const int zb = g.zs + blockIdx.y * chunk_len, ze = min(zb + chunk_len, g.ze);
+    const double sf = mi_scale(st->lo_f, st->hi_f, B), sm = mi_scale(st->lo_m, st->hi_m, B);
+    const float* __restrict__ F = b.F + (long long)pair * g.nfull;
+    const double* __restrict__ MW = b.MW + (long long)pair * g.n;
+    if (x < g.nx && y < g.ny) {
+        for (int z = zb; z < ze; ++z) {
+            ParzenD a, c;
+            parzen_d(((double)__ldg(F + z * nxy + x + g.nx * y) - st->lo_f) * sf, B, p.mi_sigma, a, false);
+            parzen_d((__ldg(MW + (z - g.zlo) * nxy + x + g.nx * y) - st->lo_m) * sm, B, p.mi_sigma, c, false);
+            for (int i = 0; i < a.n; ++i)
+                for (int j = 0; j < c.n; ++j)
+                    atomicAdd(&sh_hist[(a.lo + i) * B + c.lo + j],
+                              (unsigned long long)llrint(a.w[i] * c.w[j] * 4294967296.0));
+        }
+    }
+    __syncthreads();
+    unsigned long long* H = b.HIST + (long long)pair * B * B;
+    for (int i = threadIdx.x; i < B * B; i += blockDim.x)
+        if (sh_hist[i]) atomicAdd(&H[i], sh_hist[i]);
+}
+
+// MI from the histogram (fixed-order reductions), the gradient table, then
+// the loss / damping / rejection state machine; clears the histogram.
+__global__ void k_mi_finalize(Batch b, LmParams p, int mode) {
+    __shared__ double red[32];
+    __shared__ double s_pm[64];
+    const int pair = blockIdx.x;
+    PairState* st = b.st + pair;
+    if (st->done) return;
+    const int B = p.mi_bins;
+    unsigned long long* H = b.HIST + (long long)pair * B * B;
+    double* T = b.MIT + (long long)pair * B * B;
+    const double invN = 1.0 / (double)b.g.nfull, unit = 1.0 / 4294967296.0, eps = 1e-12;
+    const double il2 = 1.0 / log(2.0);
+    // marginals: thread j sums column j (moving), thread B + i row i (fixed)
+    double part = 0.0;
+    if (threadIdx.x < B) {
+        double s = 0.0;
+        for (int i = 0; i < B; ++i) s += (double)H[i * B + threadIdx.x] * unit * invN;
+        s_pm[threadIdx.x] = s;
+    }
+    __syncthreads();
+    if (threadIdx.x < B) {  // - p_m log p_m
+        const double pm = s_pm[threadIdx.x];
+        part -= pm * log2(fmax(pm, eps));
+    } else if (threadIdx.x < 2 * B) {  // - p_f log p_f
+        const int i = threadIdx.x - B;
+        double pf = 0.0;
+        for (int j = 0; j < B; ++j) pf += (double)H[i * B + j] * unit * invN;
+        part -= pf * log2(fmax(pf, eps));
+    }
+    for (int k = threadIdx.x; k < B * B; k += blockDim.x) {  // + p log p, gradient table
+        const double pij = (double)H[k] * unit * invN;
+        const double pm = s_pm[k % B];
+        part += pij * log2(fmax(pij, eps));
+        T[k] = (log2(fmax(pij, eps)) + (pij >= eps ? il2 : 0.0)) - (log2(fmax(pm, eps)) + (pm >= eps ? il2 : 0.0));
+    }
+    const double mi = block_sum(part, red);
+    for (int k = threadIdx.x; k < B * B; k += blockDim.x) H[k] = 0ull;
+    if (threadIdx.x == 0) finalize_pair(st, p, mode, mi, pair);
+}
+
+// g = dr/dMw grad M(x+u), dr/dMw = -(1/N) s_m sum_i a_i(t_f) sum_j b'_j(t_m) T_ij
+// at the accepted warp; skipped after a rejection (gradient unchanged).
+__global__ void __launch_bounds__(256) k_mi_grad(Batch b, LmParams p) {
+    const int pair = blockIdx.z;
+    const PairState* st = b.st + pair;
+    if (st->done || st->last_rejected) return;
+    const Geo g = b.g;
+    const int tiles_x = cdiv(g.nx, 32);
+    const int x = (blockIdx.x % tiles_x) * 32 + (threadIdx.x & 31);
+    const int y = (blockIdx.x / tiles_x) * 8 + (threadIdx.x >> 5);
+    if (x >= g.nx || y >= g.ny) return;
+    const int z = g.zs + blockIdx.y;
+    const int B = p.mi_bins;
+    const long long n = g.n;
+    const float* __restrict__ M = b.M + (long long)pair * g.nfull;
+    const float* __restrict__ F = b.F + (long long)pair * g.nfull;
+    const float* __restrict__ U = b.U + ((long long)pair * 2 + st->cur) * 3 * n;
+    const double* __restrict__ T = b.MIT + (long long)pair * B * B;
+    float* __restrict__ G = b.G + (long long)pair * 3 * n;
+    const int o = g.lat(x, y, z);
+    double grad[3];
+    const double mw = sample_vol<true>(M, g, x, y, z, __ldg(U + o), __ldg(U + n + o), __ldg(U + 2 * n + o), grad);
+    const double sf = mi_scale(st->lo_f, st->hi_f, B), sm = mi_scale(st->lo_m, st->hi_m, B);
+    ParzenD a, c;
+    parzen_d(((double)__ldg(F + g.at(x, y, z)) - st->lo_f) * sf, B, p.mi_sigma, a, false);
+    parzen_d((mw - st->lo_m) * sm, B, p.mi_sigma, c, true);
+    double s = 0.0;
+    for (int i = 0; i < a.n; ++i) {
+        double t = 0.0;
+        for (int j = 0; j < c.n; ++j) t += c.dw[j] * __ldg(T + (a.lo + i) * B + c.lo + j);
+        s += a.w[i] * t;
+    }
+    const double dr = -(1.0 / (double)g.nfull) * sm * s;
+    G[o] = (float)(dr * grad[0]);
+    G[n + o] = (float)(dr * grad[1]);
+    G[2 * n + o] = (float)(dr * grad[2]);
 }
 
 // K1b: LNCC forward window pass.
@@ -1320,6 +1466,27 @@ void launch_mse_fwd(const Batch& b, const LmParams& p, int mode, cudaStream_t s)
     grid.z = b.pairs;
     k_mse_fwd<<<grid, 256, 0, s>>>(b, sh.chunk_len);
     g_kernel_launches += 2;
+}
+
+void launch_mi_fwd(const Batch& b, const LmParams& p, int mode, cudaStream_t s) {
+    const dim3 wgrid(cdiv(b.g.nx, 32) * cdiv(b.g.ny, 8), b.g.ze - b.g.zs, b.pairs);
+    k_warp_moving<<<wgrid, 256, 0, s>>>(b, mode, b.g.zs);
+    const LaunchShape sh = shape_for(b.g, b.pairs, 8);
+    dim3 grid = sh.grid();
+    grid.z = b.pairs;
+    k_mi_hist<<<grid, 256, sizeof(unsigned long long) * p.mi_bins * p.mi_bins, s>>>(b, p, sh.chunk_len);
+    g_kernel_launches += 2;
+}
+
+void launch_mi_finalize(const Batch& b, const LmParams& p, int mode, cudaStream_t s) {
+    k_mi_finalize<<<b.pairs, 256, 0, s>>>(b, p, mode);
+    ++g_kernel_launches;
+}
+
+void launch_mi_grad(const Batch& b, const LmParams& p, cudaStream_t s) {
+    const dim3 grid(cdiv(b.g.nx, 32) * cdiv(b.g.ny, 8), b.g.ze - b.g.zs, b.pairs);
+    k_mi_grad<<<grid, 256, 0, s>>>(b, p);
+    ++g_kernel_launches;
 }
 
 void launch_mse_grad(const Batch& b, const LmParams& p, cudaStream_t s) {

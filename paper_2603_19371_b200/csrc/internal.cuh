@@ -151,7 +151,8 @@ struct wlm_engine {
     DevBuf<float> F, M, U, ABE, G, VS, AM, AV;
     DevBuf<double> MW;
     DevBuf<PairState> st;
-    DevBuf<double> partials, script, shift_part, plane_sum, TM;
+    DevBuf<double> partials, script, shift_part, plane_sum, TM, MIT;
+    DevBuf<unsigned long long> HIST;
     DevBuf<wlm_step_log> trace;
     Batch B{};
     cudaGraphExec_t step_exec = nullptr, loop_exec = nullptr;
@@ -170,6 +171,7 @@ struct wlm_engine {
     // Stages of one attempt (a slab group interleaves them with exchanges).
     void stage_grad(cudaStream_t s) {
         if (P.metric == WLM_METRIC_MSE) launch_mse_grad(B, P, s);
+        else if (P.metric == WLM_METRIC_MI) launch_mi_grad(B, P, s);
         else launch_lncc_bwd(B, P, s);
         if (P.optimizer == WLM_OPT_ADAM) launch_adam(B, P, s);
     }
@@ -183,9 +185,13 @@ struct wlm_engine {
     }
     void stage_eval(int mode, cudaStream_t s) {
         if (P.metric == WLM_METRIC_MSE) launch_mse_fwd(B, P, mode, s);
+        else if (P.metric == WLM_METRIC_MI) launch_mi_fwd(B, P, mode, s);
         else launch_lncc_fwd(B, P, mode, s);
     }
-    void stage_finalize(int mode, cudaStream_t s) { launch_finalize(B, P, mode, s); }
+    void stage_finalize(int mode, cudaStream_t s) {
+        if (P.metric == WLM_METRIC_MI) launch_mi_finalize(B, P, mode, s);
+        else launch_finalize(B, P, mode, s);
+    }
 
     void body(cudaStream_t s) {
         stage_grad(s);

@@ -178,17 +178,38 @@ __global__ void k_set_targets(PairState* st, int pairs, int iters) {
 // fixed-order final sum (independent of scheduling).
 constexpr int kShiftBlocks = 256;
 
+// part: [pair][2][kShiftBlocks] sums, then [pair][2][kShiftBlocks][2] (min,
+// max) at offset pairs * 2 * kShiftBlocks (the MI normalisation range).
 __global__ void k_shift_partials(Batch b, double* part) {
     __shared__ double red[32];
+    __shared__ float rmin[32], rmax[32];
     const int pair = blockIdx.y, which = blockIdx.z;
     const long long n = b.g.nfull;  // F, M are whole-volume (replicated across slabs)
     const float* v = (which == 0 ? b.F : b.M) + (long long)pair * n;
     const long long per = (n + kShiftBlocks - 1) / kShiftBlocks;
     const long long lo = blockIdx.x * per, hi = min(n, lo + per);
     double s = 0.0;
-    for (long long i = lo + threadIdx.x; i < hi; i += blockDim.x) s += (double)v[i];
-    const double t = block_sum(s, red);
-    if (threadIdx.x == 0) part[((long long)pair * 2 + which) * kShiftBlocks + blockIdx.x] = t;
+    float mn = INFINITY, mx = -INFINITY;
+    for (long long i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+        const float x = v[i];
+        s += (double)x;
+        mn = fminf(mn, x);
+        mx = fmaxf(mx, x);
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    }
+    if ((threadIdx.x & 31) == 0) { rmin[threadIdx.x >> 5] = mn; rmax[threadIdx.x >> 5] = mx; }
+    const double t = block_sum(s, red);  // contains __syncthreads
+    if (threadIdx.x == 0) {
+        part[((long long)pair * 2 + which) * kShiftBlocks + blockIdx.x] = t;
+        float a = rmin[0], c = rmax[0];
+        for (int w = 1; w < (int)(blockDim.x >> 5); ++w) { a = fminf(a, rmin[w]); c = fmaxf(c, rmax[w]); }
+        double* mm = part + (long long)b.pairs * 2 * kShiftBlocks;
+        mm[(((long long)pair * 2 + which) * kShiftBlocks + blockIdx.x) * 2] = a;
+        mm[(((long long)pair * 2 + which) * kShiftBlocks + blockIdx.x) * 2 + 1] = c;
+    }
 }
 
 __global__ void k_shift_final(Batch b, const double* part) {
@@ -198,8 +219,12 @@ __global__ void k_shift_final(Batch b, const double* part) {
     const double t = block_sum(v, red);
     if (threadIdx.x == 0) {
         const float mean = (float)(t / (double)b.g.nfull);
-        if (which == 0) b.st[pair].shift_f = mean;
-        else b.st[pair].shift_m = mean;
+        const double* mm = part + (long long)b.pairs * 2 * kShiftBlocks + ((long long)pair * 2 + which) * kShiftBlocks * 2;
+        double a = mm[0], c = mm[1];
+        for (int i = 1; i < kShiftBlocks; ++i) { a = fmin(a, mm[2 * i]); c = fmax(c, mm[2 * i + 1]); }
+        PairState& st = b.st[pair];
+        if (which == 0) { st.shift_f = mean; st.lo_f = a; st.hi_f = c; }
+        else { st.shift_m = mean; st.lo_m = a; st.hi_m = c; }
     }
 }
 

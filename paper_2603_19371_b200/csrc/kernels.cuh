@@ -31,6 +31,7 @@ struct PairState {
     unsigned counter;        // last-block election counter (K1)
     int jac_bits;            // min det(I + grad eps dU_s), ordered int
     float shift_f, shift_m;  // per-pair intensity shift for the fp32 moments
+    double lo_f, hi_f, lo_m, hi_m;  // min / max of F and M (MI normalisation)
 };
 
 // Launch-invariant parameters of one engine (passed by value).
@@ -52,6 +53,8 @@ struct LmParams {
     int metric;            // WLM_METRIC_LNCC | WLM_METRIC_MSE
     double demons_alpha;   // DemonsConfig.alpha (optimizer DEMONS)
     int tile_k;            // LmConfig.tile_size (Eq. 5); 1 = pointwise Eq. 4
+    int mi_bins;           // MI: B x B Parzen grid
+    double mi_sigma;       // MI: Parzen sigma in bin widths
 };
 
 // Buffers of a batch of `pairs` registrations of identical geometry.
@@ -73,6 +76,8 @@ struct Batch {
     double* plane_sum;  // [pair][nz] per-plane sum(rho) (global z; shared by slabs)
     int zero_foreign_planes;  // NCCL slabs: zero non-owned planes before the all-reduce
     double* TM;       // [pair][tiles][6] tiled LM: -r (H + lambda I)^{-1} (symmetric), or null
+    unsigned long long* HIST;  // [pair][B*B] MI joint histogram, fixed point 2^-32 (exact sums)
+    double* MIT;      // [pair][B*B] MI gradient table dMI/dp_ij - dMI/dp_m(j)
     int tkx, tky, tkz;  // tile counts (tile_k > 1)
     int max_blocks;
 };
@@ -86,6 +91,11 @@ LaunchShape shape_for(const Geo& g, int pairs, int ty);
 // MSE: K1a warp + per-plane sum (f - Mw)^2; gradient
 // g = -2 (f - Mw)/N grad M(x+u) (pointwise, analytic interpolant gradient).
 void launch_mse_fwd(const Batch& b, const LmParams& p, int mode, cudaStream_t s);
+// MI: K1a + fixed-point Parzen joint histogram; finalize
+// (MI, gradient table, state machine); pointwise gradient.
+void launch_mi_fwd(const Batch& b, const LmParams& p, int mode, cudaStream_t s);
+void launch_mi_finalize(const Batch& b, const LmParams& p, int mode, cudaStream_t s);
+void launch_mi_grad(const Batch& b, const LmParams& p, cudaStream_t s);
 void launch_mse_grad(const Batch& b, const LmParams& p, cudaStream_t s);
 // K1: warp + LNCC window moments + coefficients + sum(rho); last block runs
 // the loss/damping/rejection state machine.  mode 0 evaluates the accepted

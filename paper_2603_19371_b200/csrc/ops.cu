@@ -219,6 +219,43 @@ wlm_status wlm_residual_lncc(wlm_ctx* ctx, const double* F, const double* M, con
     return s;
 }
 
+wlm_status wlm_residual_mi(wlm_ctx* ctx, const double* F, const double* M, const double* u, wlm_dims d, int bins,
+                           double sigma, double* r, double* mi, double* g) {
+    if (!F || !M || !u || !valid_dims(d)) return bad(ctx, WLM_INVALID_ARG, "residual_mi: bad args");
+    wlm_reg_config cfg;
+    wlm_default_reg_config(&cfg);
+    cfg.metric = WLM_METRIC_MI;
+    cfg.mi_bins = bins;
+    cfg.mi_sigma = sigma;
+    cfg.nlevels = 1; cfg.factors[0] = 1; cfg.iters[0] = 0;
+    wlm_engine* e = nullptr;
+    wlm_status s = wlm_engine_create(ctx, d, 1, &cfg, &e);
+    if (s != WLM_OK) return s;
+    s = run(ctx, [&] {
+        const size_t n = nvox(d);
+        std::vector<float> hf(n), hm(n);
+        for (size_t i = 0; i < n; ++i) { hf[i] = (float)F[i]; hm[i] = (float)M[i]; }
+        CK(cudaMemcpyAsync(e->F.p, hf.data(), sizeof(float) * n, cudaMemcpyHostToDevice, ctx->stream));
+        CK(cudaMemcpyAsync(e->M.p, hm.data(), sizeof(float) * n, cudaMemcpyHostToDevice, ctx->stream));
+        launch_shifts(e->B, ctx->stream);
+        DevBuf<float> du = upload_soa(ctx, u, n, 3);
+        copy_warps_in(e, du.p, 0);
+        launch_begin_level(e->B, e->P, 0, 1, cfg.lm.lambda0, ctx->stream);
+        e->stage_eval(0, ctx->stream);
+        e->stage_finalize(0, ctx->stream);
+        if (g) {
+            launch_mi_grad(e->B, e->P, ctx->stream);
+            download_aos(ctx, e->G.p, n, 3, g);
+        }
+        const std::vector<PairState> st = read_states(e);
+        if (r) *r = st[0].r_cur;
+        if (mi) *mi = st[0].lncc_cur;
+        if (st[0].status) throw Fail{(wlm_status)st[0].status};
+    });
+    wlm_engine_destroy(e);
+    return s;
+}
+
 wlm_status wlm_residual_mse(wlm_ctx* ctx, const double* F, const double* M, const double* u, wlm_dims d,
                             double* r, double* g) {
     if (!F || !M || !u || !valid_dims(d)) return bad(ctx, WLM_INVALID_ARG, "residual_mse: bad args");

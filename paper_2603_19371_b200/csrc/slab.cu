@@ -442,6 +442,10 @@ wlm_status make_group(wlm_ctx* ctx, wlm_dims d, int nslabs, int first, int count
 
 wlm_status check_split(wlm_ctx* ctx, wlm_dims d, int nslabs, const wlm_reg_config* cfg) {
     if (!ctx || nslabs < 1 || !valid_dims(d)) return WLM_INVALID_ARG;
+    if (cfg->metric == WLM_METRIC_MI) {
+        set_err(ctx, "slab_group: MI needs the joint histogram of the whole volume; not built");
+        return WLM_UNSUPPORTED;
+    }
     if (cfg->lm.tile_size != 1) {
         set_err(ctx, "slab_group: tiled LM (tile_size > 1) pools g over tiles that cross slabs; not built");
         return WLM_UNSUPPORTED;

@@ -35,7 +35,7 @@ from dataclasses import dataclass, field as dfield
 import numpy as np
 
 from ._lib import (AdamConfig, Dims, DimensionMismatch, InvalidArgument, LmConfig, LmState,
-                   METRIC_LNCC, METRIC_MSE, NonFiniteLoss, OPT_ADAM, OPT_DEMONS, OPT_GD, OPT_LM, RegConfig, StepLog, WlmError, check,
+                   METRIC_LNCC, METRIC_MI, METRIC_MSE, NonFiniteLoss, OPT_ADAM, OPT_DEMONS, OPT_GD, OPT_LM, RegConfig, StepLog, WlmError, check,
                    load)
 
 __all__ = [
@@ -44,7 +44,7 @@ __all__ = [
     "warp_volume", "residual_lncc", "lm_step_pointwise", "update_damping", "rejection_test",
     "downsample", "upsample_warp", "state_bytes", "register", "reg_config", "lm_config",
     "DimensionMismatch", "InvalidArgument", "NonFiniteLoss", "WlmError", "OPT_LM", "OPT_ADAM",
-    "OPT_GD", "OPT_DEMONS", "LmState", "LmConfig", "METRIC_LNCC", "METRIC_MSE", "residual_mse",
+    "OPT_GD", "OPT_DEMONS", "LmState", "LmConfig", "METRIC_LNCC", "METRIC_MSE", "METRIC_MI", "residual_mse", "residual_mi",
     "demons_step_mse", "lm_step_tiled",
 ]
 
@@ -251,6 +251,19 @@ def residual_lncc(F, M, u, radius=2, gradient=True, ctx=None) -> ResidualReport:
     c.check(c.lib.wlm_residual_lncc(c.h, _p(F), _p(M), _p(u), _dims(F.shape), int(radius),
                                     C.byref(r), C.byref(ln), _p(g) if gradient else None))
     return ResidualReport(r.value, g, ln.value)
+
+
+def residual_mi(F, M, u, bins=32, sigma=1.0, gradient=True, ctx=None) -> ResidualReport:
+    """residual_mi (SPEC.md:145-153): r = log2(bins) - MI, loss_raw = MI (bits)."""
+    F, M, u = _vol(F), _vol(M), _fld(u)
+    if F.shape != M.shape or u.shape[:3] != F.shape:
+        raise DimensionMismatch(2, "residual_mi: dimension mismatch")
+    c = _ctx(ctx)
+    r, mi = C.c_double(), C.c_double()
+    g = np.empty(F.shape + (3,)) if gradient else None
+    c.check(c.lib.wlm_residual_mi(c.h, _p(F), _p(M), _p(u), _dims(F.shape), int(bins), float(sigma),
+                                  C.byref(r), C.byref(mi), _p(g) if gradient else None))
+    return ResidualReport(r.value, g, mi.value)
 
 
 def residual_mse(F, M, u, gradient=True, ctx=None) -> ResidualReport:

@@ -480,3 +480,27 @@ def test_tiled_lm_engine_vs_oracle(P, ctx, k):
         compare_runs(tr, tr_o, aos(warp[0]), u_o, lt, wt)
     with pytest.raises(P.WlmError):  # slab groups pool only pointwise steps
         P.SlabGroup((24, 28, 32), 2, cfg=P.reg_config(**kw), ctx=ctx)
+
+
+# -------------------------------------------------------------------- MI ----
+def test_residual_mi_vs_oracle(P, ctx):
+    F, M = _pair((20, 22, 24), 13)
+    F = F.astype(np.float32).astype(np.float64)
+    M = M.astype(np.float32).astype(np.float64)
+    u = smooth_field(F.shape, 8, amp=1.2).astype(np.float32).astype(np.float64)
+    for bins, sigma in ((32, 1.0), (16, 0.5)):
+        rep = P.residual_mi(F, M, u, bins=bins, sigma=sigma, ctx=ctx)
+        r, g, mi = O.residual_mi(F, M, u, bins=bins, sigma=sigma)
+        assert abs(rep.r - r) <= 1e-9 * r and abs(rep.loss_raw - mi) <= 1e-9
+        assert rel(rep.g, g) < 1e-6, rel(rep.g, g)
+
+
+def test_mi_engine_vs_oracle(P, ctx):
+    F, M, _ = O.synth_pair((24, 28, 32), 15, num_blobs=10, warp_max=2.5)
+    kw = dict(nlevels=1, factors=[1], iters=[20], metric=2, mi_bins=24)
+    warp, (tr,), _ = run_engine(P, ctx, F, M, P.reg_config(**kw), 20)
+    for storage, lt, wt in (("fp64", 1e-5, 1e-4), ("fp32", 1e-6, 1e-5)):
+        rc, u_o, _, tr_o = oracle_level(F, M, O.default_config(**kw), 20, storage)
+        assert rc == 0
+        compare_runs(tr, tr_o, aos(warp[0]), u_o, lt, wt)
+    assert tr[-1]["loss_raw"] > tr[0]["loss_raw"]  # MI increases

@@ -177,6 +177,37 @@ def test_mse_lm_iterate_decreases_loss():
     assert tr[-1].r < 0.8 * r0
 
 
+def test_mi_kats_and_bounds():
+    """SPEC.md:150-153, :157-159.  Identical images with B levels on the bin
+    centres reach MI ~ log2 B when the Parzen kernel is narrow (sigma = 0.25
+    bin; at the default sigma = 1 the kernel blurs adjacent levels, DESIGN.md
+    A16); independent noise -> MI < 0.1 bits at 32^3; 0 <= MI <= log2 B."""
+    rng = np.random.default_rng(0)
+    B = 32
+    F = np.repeat(np.arange(B, dtype=float), 32 ** 3 // B).reshape(32, 32, 32)
+    rng.shuffle(F.reshape(-1))
+    z = np.zeros(F.shape + (3,))
+    r, g, mi = O.residual_mi(F, F, z, bins=B, sigma=0.25)
+    assert r < 0.2 and abs(r - (np.log2(B) - mi)) < 1e-12
+    r, g, mi = O.residual_mi(rng.uniform(size=(32, 32, 32)), rng.uniform(size=(32, 32, 32)), z)
+    assert mi < 0.1
+    for seed in range(20):
+        q = np.random.default_rng(100 + seed)
+        F = q.uniform(size=(6, 6, 6)) ** q.uniform(0.5, 3)
+        M = q.normal(size=(6, 6, 6))
+        r, _, mi = O.residual_mi(F, M, np.zeros((6, 6, 6, 3)), bins=int(q.integers(2, 40)))
+        assert -1e-12 <= mi and r >= -1e-12
+
+
+def test_mi_gradient_finite_differences():
+    rng = np.random.default_rng(6)
+    F = O.gaussian_smooth(rng.uniform(size=(10, 10, 10)), 1.0)
+    M = O.gaussian_smooth(rng.uniform(size=(10, 10, 10)), 1.0)
+    u = smooth_field((10, 10, 10), 3, amp=0.7) + 0.137
+    errs, _ = _fd_check(lambda a, b, c: O.residual_mi(a, b, c, bins=16)[:2], F, M, u)
+    assert np.all(errs < 1e-3), errs
+
+
 def _dense_tiled(r, g, lam, k):
     """Independent dense per-tile assemble-and-solve."""
     out = np.empty_like(g)
