@@ -15,7 +15,11 @@
 //   jacobian_det_min          field.hpp:108    jacobian_det_min             invalid_argument (dims < 2)
 //   gaussian_smooth (vol/fld) field.hpp:113-114 gaussian_smooth
 //   all_finite                field.hpp:116-117 all_finite
+//   residual_mse              SPEC.md:127      residual_mse -> ResidualReport
 //   residual_lncc             SPEC.md:136      residual_lncc -> ResidualReport
+//   residual_mi               SPEC.md:145      residual_mi -> ResidualReport
+//   lm_step_tiled             SPEC.md:256      lm_step_tiled
+//   demons_step_mse           SPEC.md:301      demons_step_mse
 //   register                  SPEC.md:362      register_pair -> RegResult   runtime_error (non-finite)
 #pragma once
 
@@ -132,6 +136,47 @@ ResidualReport<Field> residual_lncc(const Volume& F, const Volume& M, const Fiel
                             &rep.r, &rep.loss_raw, rep.g.data.data()),
           c);
     return rep;
+}
+
+template <class Volume, class Field>
+ResidualReport<Field> residual_mse(const Volume& F, const Volume& M, const Field& u,
+                                   Context& c = default_context()) {
+    ResidualReport<Field> rep;
+    rep.g = Field(u.dims);
+    check(wlm_residual_mse(c.get(), F.data.data(), M.data.data(), u.data.data(), dims_of(F.dims), &rep.r,
+                           rep.g.data.data()),
+          c);
+    rep.loss_raw = rep.r;
+    return rep;
+}
+
+// MetricConfig{kind = mi, mi_bins, mi_parzen_sigma}.
+template <class Volume, class Field>
+ResidualReport<Field> residual_mi(const Volume& F, const Volume& M, const Field& u, int bins = 32,
+                                  double sigma = 1.0, Context& c = default_context()) {
+    ResidualReport<Field> rep;
+    rep.g = Field(u.dims);
+    check(wlm_residual_mi(c.get(), F.data.data(), M.data.data(), u.data.data(), dims_of(F.dims), bins, sigma,
+                          &rep.r, &rep.loss_raw, rep.g.data.data()),
+          c);
+    return rep;
+}
+
+template <class Field>
+Field lm_step_tiled(double r, const Field& g, double lambda, int k, Context& c = default_context()) {
+    Field out(g.dims);
+    check(wlm_lm_step_tiled(c.get(), r, g.data.data(), dims_of(g.dims), lambda, k, out.data.data()), c);
+    return out;
+}
+
+template <class Volume, class Field>
+Field demons_step_mse(const Volume& per_voxel_r, const Field& moving_grad, double alpha,
+                      Context& c = default_context()) {
+    Field out(moving_grad.dims);
+    check(wlm_demons_step_mse(c.get(), per_voxel_r.data.data(), moving_grad.data.data(),
+                              dims_of(moving_grad.dims), alpha, out.data.data()),
+          c);
+    return out;
 }
 
 // RegResult.

@@ -53,7 +53,20 @@ int main() {
         threw = true;  // field.cpp:124-126
     }
     const double jac = wlm_warplm::jacobian_det_min(u);
-    std::printf("compose max err %.3g, eps %.6f, dim-mismatch throws %d, jac(0) %.1f\n", err, eps,
-                (int)threw, jac);
-    return (err < 1e-6 && threw && jac == 1.0) ? 0 : 1;
+    // SPEC.md:132-133 (MSE KATs) and :307 (Demons KAT) through the adapter
+    Volume3 F(d), M(d);
+    for (std::size_t i = 0; i < F.data.size(); ++i) M.data[i] = 1.0;
+    const auto mse = wlm_warplm::residual_mse(F, M, u);
+    Volume3 r1(Dims3{1, 1, 1});
+    r1.data[0] = 1.0;
+    DispField3 n1(Dims3{1, 1, 1});
+    n1.data[0] = 2.0;
+    const DispField3 dm = wlm_warplm::demons_step_mse(r1, n1, 1.0);
+    const DispField3 t1 = wlm_warplm::lm_step_tiled(0.5, v, 0.1, 3);
+    std::printf("compose max err %.3g, eps %.6f, dim-mismatch throws %d, jac(0) %.1f, mse %.1f, demons %.3f\n",
+                err, eps, (int)threw, jac, mse.r, dm.data[0]);
+    return (err < 1e-6 && threw && jac == 1.0 && mse.r == 1.0 && std::fabs(dm.data[0] - 0.4) < 1e-15 &&
+            t1.data.size() == v.data.size())
+               ? 0
+               : 1;
 }
