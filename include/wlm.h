@@ -30,6 +30,8 @@
  *   SPEC.md:197    upsample_warp                         wlm_upsample_warp
  *   SPEC.md:362    register -> RegResult                 wlm_register
  *   SPEC.md:310    state_bytes                           wlm_state_bytes
+ *   io.hpp:18-21   read/write_vol3, read/write_dsp3      wlm_read_vol3 ... wlm_write_dsp3
+ *   SPEC.md:427    CSV trace                             wlm_write_trace_csv
  *
  * Host-buffer entry points take the reference's own layout: fp64, x-fastest
  * (field.hpp:25-30), displacement fields component-innermost AoS
@@ -286,6 +288,21 @@ wlm_status wlm_slab_group_iterate(wlm_slab_group* g, int iters);
 wlm_status wlm_slab_group_trace(wlm_slab_group* g, wlm_step_log* rows, size_t cap, size_t* len);
 wlm_status wlm_slab_group_state(wlm_slab_group* g, wlm_lm_state* st, double* r, double* lncc,
                                 int* iters_done);
+
+/* ---- data formats either side of the path (io.hpp:15-21) ----
+ * VOL3 / DSP3 exactly as the reference reads and writes them (same checks,
+ * same messages, WLM_INVALID_ARG for every io_error).  dst / src are host
+ * (on_device = 0; no CUDA call, ctx may be NULL) or device pointers; device
+ * reads stream through double-buffered pinned staging; DSP3 is AoS on disk,
+ * SoA fp32 [3][nz][ny][nx] in memory (transposed on the device). */
+wlm_status wlm_io_dims(const char* path, int is_field, wlm_dims* d);
+wlm_status wlm_read_vol3(wlm_ctx* ctx, const char* path, float* dst, size_t cap, int on_device, wlm_dims* d);
+wlm_status wlm_read_dsp3(wlm_ctx* ctx, const char* path, float* dst_soa, size_t cap, int on_device,
+                         wlm_dims* d);
+wlm_status wlm_write_vol3(wlm_ctx* ctx, const char* path, const float* src, int on_device, wlm_dims d);
+wlm_status wlm_write_dsp3(wlm_ctx* ctx, const char* path, const float* src_soa, int on_device, wlm_dims d);
+/* RegResult.loss_trace as CSV: "# warplm-csv v1" + the SPEC.md:427 columns. */
+wlm_status wlm_write_trace_csv(const char* path, const wlm_step_log* rows, size_t n);
 
 /* ---- harness: synthetic pair on the GPU ----
  * u_true is SoA fp32 [3][nz][ny][nx] (nullable); on_device selects whether

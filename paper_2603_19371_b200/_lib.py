@@ -139,6 +139,12 @@ SIGNATURES = {
     "wlm_slab_group_iterate": (C.c_int, [_ENG, C.c_int]),
     "wlm_slab_group_trace": (C.c_int, [_ENG, C.POINTER(StepLog), C.c_size_t, C.POINTER(C.c_size_t)]),
     "wlm_slab_group_state": (C.c_int, [_ENG, C.POINTER(LmState), _D, _D, C.POINTER(C.c_int)]),
+    "wlm_io_dims": (C.c_int, [C.c_char_p, C.c_int, C.POINTER(Dims)]),
+    "wlm_read_vol3": (C.c_int, [_CTX, C.c_char_p, _VP, C.c_size_t, C.c_int, C.POINTER(Dims)]),
+    "wlm_read_dsp3": (C.c_int, [_CTX, C.c_char_p, _VP, C.c_size_t, C.c_int, C.POINTER(Dims)]),
+    "wlm_write_vol3": (C.c_int, [_CTX, C.c_char_p, _VP, C.c_int, Dims]),
+    "wlm_write_dsp3": (C.c_int, [_CTX, C.c_char_p, _VP, C.c_int, Dims]),
+    "wlm_write_trace_csv": (C.c_int, [C.c_char_p, C.POINTER(StepLog), C.c_size_t]),
     "wlm_synth_pair": (C.c_int, [_CTX, C.POINTER(SynthSpec), _VP, _VP, _VP, C.c_int]),
 }
 
