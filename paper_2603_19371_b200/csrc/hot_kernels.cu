@@ -1262,29 +1262,36 @@ __global__ void __launch_bounds__(k4::NT, 2) k_compose_smooth(Batch b, LmParams 
             }
         }
     };
-    // an item's cell needs no clamp rules when it is one voxel off the faces
-    bool inner[SL];
-#pragma unroll
-    for (int s = 0; s < SL; ++s)
-        inner[s] = voff[s] >= 0 && vx[s] >= 1 && vx[s] <= g.nx - 2 && vy[s] >= 1 && vy[s] <= g.ny - 2;
+    // Every item in one branch-free path: |d| <= target < 1, so the cell
+    // origin is x + floor(d) with floor(d) in {-1, 0}; the clamp rules of
+    // field.cpp:19-39 (origin < 0 -> 0 with t = 0; origin > n-2 -> n-2 with
+    // t = 1, which also covers a sample exactly on the last voxel) are two
+    // selects per axis; n == 1 axes sample index 0 with t = 0.
+    auto clamp_axis = [](int& i, double& t, int n) {
+        if (n == 1) { i = 0; t = 0.0; return; }
+        if (i < 0) { i = 0; t = 0.0; }
+        else if (i > n - 2) { i = n - 2; t = 1.0; }
+    };
     // composed value of the items of plane z (step in pv) -> dst
     auto compose = [&](int z, double* dst) {
         const bool zin = z >= 0 && z < g.nz;
-        const bool zinner = z >= 1 && z <= g.nz - 2;
-        {
-            // |d| <= target < 1: floor(d) in {-1, 0}, cell origin x + floor(d)
 #pragma unroll
-            for (int s = 0; s < SL; ++s) {
-                const int idx = threadIdx.x + s * NT;
-                if (idx >= NI || !(zinner && inner[s])) continue;
+        for (int s = 0; s < SL; ++s) {
+            const int idx = threadIdx.x + s * NT;
+            if (idx >= NI || idx % IWP >= S::IW) continue;
+            double o3[3] = {0.0, 0.0, 0.0};
+            if (zin && voff[s] >= 0) {
                 const double dx = eps * pv[s][0], dy = eps * pv[s][1], dz = eps * pv[s][2];
-                double o3[3];
                 if (isfinite(dx + dy + dz)) {
                     const int fx = dx < 0.0 ? -1 : 0, fy = dy < 0.0 ? -1 : 0, fz = dz < 0.0 ? -1 : 0;
-                    const double tx = dx - (double)fx, ty = dy - (double)fy, tz = dz - (double)fz;
-                    const int a = (idx / IWP + 1 + fy) * UW + idx % IWP + 1 + fx;
-                    const float* p0 = s_u + ((z + fz + 4) & 3) * 3 * UN + a;
-                    const float* p1 = s_u + ((z + fz + 5) & 3) * 3 * UN + a;
+                    double tx = dx - (double)fx, ty = dy - (double)fy, tz = dz - (double)fz;
+                    int ix = vx[s] + fx, iy = vy[s] + fy, iz = z + fz;
+                    clamp_axis(ix, tx, g.nx);
+                    clamp_axis(iy, ty, g.ny);
+                    clamp_axis(iz, tz, g.nz);
+                    const int a = (iy - (y0 - R - 1)) * UW + ix - (x0 - R - 1);
+                    const float* p0 = s_u + ((iz + 4) & 3) * 3 * UN + a;
+                    const float* p1 = s_u + ((iz + 5) & 3) * 3 * UN + a;
 #pragma unroll
                     for (int ch = 0; ch < 3; ++ch) {
                         const double c000 = p0[ch * UN], c100 = p0[ch * UN + 1];
@@ -1295,43 +1302,6 @@ __global__ void __launch_bounds__(k4::NT, 2) k_compose_smooth(Batch b, LmParams 
                         const double v01 = fma(tx, c101 - c001, c001), v11 = fma(tx, c111 - c011, c011);
                         const double s0 = fma(ty, v10 - v00, v00), s1 = fma(ty, v11 - v01, v01);
                         o3[ch] = fma(tz, s1 - s0, s0);
-                    }
-                    o3[0] += dx;
-                    o3[1] += dy;
-                    o3[2] += dz;
-                } else {
-                    o3[0] = o3[1] = o3[2] = kNaN64;
-                }
-                dst[idx] = o3[0];
-                dst[NI + idx] = o3[1];
-                dst[2 * NI + idx] = o3[2];
-            }
-        }
-#pragma unroll
-        for (int s = 0; s < SL; ++s) {
-            const int idx = threadIdx.x + s * NT;
-            if (idx >= NI || idx % IWP >= S::IW || (zinner && inner[s])) continue;
-            double o3[3] = {0.0, 0.0, 0.0};
-            if (zin && voff[s] >= 0) {
-                const double dx = eps * pv[s][0], dy = eps * pv[s][1], dz = eps * pv[s][2];
-                if (isfinite(dx) && isfinite(dy) && isfinite(dz)) {
-                    const AxisTapD X = axis_tap_dd(vx[s], dx, g.nx);
-                    const AxisTapD Y = axis_tap_dd(vy[s], dy, g.ny);
-                    const AxisTapD Z = axis_tap_dd(z, dz, g.nz);
-                    const int ux0 = min(max(X.i0 - (x0 - R - 1), 0), UW - 2);
-                    const int uy0 = min(max(Y.i0 - (y0 - R - 1), 0), S::UH - 2);
-                    const float* p0 = s_u + ((Z.i0 + 4) & 3) * 3 * UN + uy0 * UW + ux0;
-                    const float* p1 = s_u + ((Z.i1 + 4) & 3) * 3 * UN + uy0 * UW + ux0;
-#pragma unroll
-                    for (int ch = 0; ch < 3; ++ch) {
-                        const double c000 = p0[ch * UN], c100 = p0[ch * UN + 1];
-                        const double c010 = p0[ch * UN + UW], c110 = p0[ch * UN + UW + 1];
-                        const double c001 = p1[ch * UN], c101 = p1[ch * UN + 1];
-                        const double c011 = p1[ch * UN + UW], c111 = p1[ch * UN + UW + 1];
-                        const double v00 = fma(X.t, c100 - c000, c000), v10 = fma(X.t, c110 - c010, c010);
-                        const double v01 = fma(X.t, c101 - c001, c001), v11 = fma(X.t, c111 - c011, c011);
-                        const double s0 = fma(Y.t, v10 - v00, v00), s1 = fma(Y.t, v11 - v01, v01);
-                        o3[ch] = fma(Z.t, s1 - s0, s0);
                     }
                     o3[0] += dx;
                     o3[1] += dy;
