@@ -717,23 +717,44 @@ __global__ void k_finalize(Batch b, LmParams p, int mode) {
 // ---------------------------------------------------------------------------
 // K2: LNCC backward.  Adjoint box sums of (A, B, E) over the same windows in
 // fp64; dr/dMw(x) = -(1/N)(f'_x S_A + m'_x S_B - S_E); g = dr/dMw grad M(x+u).
-// Halo rows are prefetched one plane ahead; the output voxel's u and F two
-// planes ahead and its M gathers one plane ahead of their use.
+// Schedule (as K1b): one barrier per plane; phase p runs the y-pass of plane p
+// (z ring, output plane p - R), the x-pass of plane p+1 (two outputs per
+// thread from 16-byte shared loads), the halo tile of plane p+2 and the loads
+// of plane p+3.  The output voxel's u and F are loaded three planes ahead and
+// its 8 M corners gathered two planes ahead of their use.
+namespace k2 {
+constexpr int TX = 32, TY = 8, NT = 256;
 template <int R>
-__global__ void __launch_bounds__(NT, 2) k_lncc_bwd(Batch b, LmParams p, int chunk_len) {
-    using It = hot::Items<R>;
-    constexpr int IW = It::IW, IH = It::IH, NI = It::NI, SL = It::SLOTS, W = 2 * R + 1;
-    constexpr int XS = (IH * TX + NT - 1) / NT;
-    __shared__ double s_in[2][3][NI];
-    __shared__ double s_x[3][IH][TX];
+struct Shape {
+    static constexpr int IWP = TX + 2 * R, IH = TY + 2 * R, NI = IWP * IH;
+    static constexpr int SL = (NI + NT - 1) / NT;
+    static constexpr int NV = (2 + 2 * R + 1) / 2;
+};
+// one output voxel in flight: u, F, and (once gathered) its cell
+struct Own {
+    float u[3], f;
+    float c[8];
+};
+}  // namespace k2
+
+template <int R>
+__global__ void __launch_bounds__(k2::NT, 2) k_lncc_bwd(Batch b, LmParams p, int chunk_len) {
+    using S = k2::Shape<R>;
+    constexpr int TX = k2::TX, NT = k2::NT, W = 2 * R + 1;
+    constexpr int IWP = S::IWP, IH = S::IH, NI = S::NI, SL = S::SL, NV = S::NV;
+    __shared__ __align__(16) double s_in[2][3][NI];
+    __shared__ __align__(16) double s_x[2][3][IH * TX];
+    (void)p;
 
     const int pair = blockIdx.z;
     const PairState* st = b.st + pair;
     if (st->done || st->last_rejected) return;
     const Geo g = b.g;
     const long long n = g.n;
-    Tile t;
-    t.init(g, chunk_len);
+    const int nxy = g.nx * g.ny;
+    const int tiles_x = cdiv(g.nx, TX);
+    const int x0 = (blockIdx.x % tiles_x) * TX, y0 = (blockIdx.x / tiles_x) * k2::TY;
+    const int zb = g.zs + blockIdx.y * chunk_len, ze = min(zb + chunk_len, g.ze);
     const float* __restrict__ F = b.F + (long long)pair * g.nfull;
     const float* __restrict__ M = b.M + (long long)pair * g.nfull;
     const float* __restrict__ U = b.U + ((long long)pair * 2 + st->cur) * 3 * n;
@@ -743,61 +764,88 @@ __global__ void __launch_bounds__(NT, 2) k_lncc_bwd(Batch b, LmParams p, int chu
     float* __restrict__ G = b.G + (long long)pair * 3 * n;
     const double shf = st->shift_f, shm = st->shift_m;
     const double invN = 1.0 / (double)g.nfull;
-    It it;
-    it.init(t.x0, t.y0, g.nx, g.ny);
-    const int ooff = t.x + g.nx * t.y;
-    (void)p;
 
-    // halo rows of plane z+1
+    int hoff[SL];
+#pragma unroll
+    for (int s = 0; s < SL; ++s) {
+        const int idx = threadIdx.x + s * NT;
+        const int gx = x0 - R + idx % IWP, gy = y0 - R + idx / IWP;
+        hoff[s] = (idx < NI && gx >= 0 && gx < g.nx && gy >= 0 && gy < g.ny) ? gx + g.nx * gy : -1;
+    }
     float ha[SL], hb[SL];
     double he[SL];
     auto load_halo = [&](int z) {
-        const bool zin = z >= 0 && z < g.nz;
+        const bool zin = z >= 0 && z < g.nz && z < ze + R;
+        const int base = (z - g.zlo) * nxy;
 #pragma unroll
         for (int s = 0; s < SL; ++s) {
-            if (zin && it.goff[s] >= 0) {
-                const int o = t.lp(g, z) + it.goff[s];
-                ha[s] = __ldg(A + o);
-                hb[s] = __ldg(Bc + o);
-                he[s] = __ldg(E + o);
+            if (zin && hoff[s] >= 0) {
+                ha[s] = __ldg(A + base + hoff[s]);
+                hb[s] = __ldg(Bc + base + hoff[s]);
+                he[s] = __ldg(E + base + hoff[s]);
             } else {
                 ha[s] = hb[s] = 0.f;
                 he[s] = 0.0;
             }
         }
     };
-    auto store_halo = [&](int sb) {
+    auto store_halo = [&](double* dst) {
 #pragma unroll
         for (int s = 0; s < SL; ++s) {
-            if (it.sidx[s] < 0) continue;
-            s_in[sb][0][it.sidx[s]] = (double)ha[s];
-            s_in[sb][1][it.sidx[s]] = (double)hb[s];
-            s_in[sb][2][it.sidx[s]] = he[s];
+            const int idx = threadIdx.x + s * NT;
+            if (idx >= NI) continue;
+            dst[idx] = (double)ha[s];
+            dst[NI + idx] = (double)hb[s];
+            dst[2 * NI + idx] = he[s];
         }
     };
-    // output-voxel pipeline: u and F of output plane zo+2 (dense), the 8 M
-    // corners of zo+1 (gathers in flight), those of zo (consumed now)
-    float ou2[3], of2 = 0.f, ou1[3], of1 = 0.f, ou0[3], of0 = 0.f;
-    float oc1[8], oc0[8];
-    auto load_own = [&](int zo, float (&u)[3], float& f) {
-        if (t.own && zo >= t.zb && zo < t.ze) {
-            const int o = t.lp(g, zo) + ooff;
-            u[0] = __ldg(U + o); u[1] = __ldg(U + n + o); u[2] = __ldg(U + 2 * n + o);
-            f = __ldg(F + t.gp(zo) + ooff);
+    const int xr = threadIdx.x >> 4, xj = threadIdx.x & 15;
+    auto x_pass = [&](const double* in, double* out) {
+        if (xr >= IH) return;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            double v[2 * NV];
+            const double2* src = reinterpret_cast<const double2*>(in + c * NI + xr * IWP + 2 * xj);
+#pragma unroll
+            for (int q = 0; q < NV; ++q) {
+                const double2 t = src[q];
+                v[2 * q] = t.x; v[2 * q + 1] = t.y;
+            }
+            double o0 = 0.0, o1 = 0.0;
+#pragma unroll
+            for (int d = 0; d < W; ++d) {
+                o0 += v[d];
+                o1 += v[d + 1];
+            }
+            *reinterpret_cast<double2*>(out + c * IH * TX + xr * TX + 2 * xj) = make_double2(o0, o1);
+        }
+    };
+
+    const int ox = threadIdx.x & 31, oy = threadIdx.x >> 5;
+    const int x = x0 + ox, y = y0 + oy;
+    const bool own = x < g.nx && y < g.ny;
+    const int ooff = x + g.nx * y;
+    // output pipeline: planes zo (consumed), zo+1 (gathered), zo+2, zo+3 (dense loads)
+    k2::Own o0, o1, o2, o3;
+    auto load_own = [&](int zo, k2::Own& w) {
+        if (own && zo >= zb && zo < ze) {
+            const int o = (zo - g.zlo) * nxy + ooff;
+            w.u[0] = __ldg(U + o); w.u[1] = __ldg(U + n + o); w.u[2] = __ldg(U + 2 * n + o);
+            w.f = __ldg(F + zo * nxy + ooff);
         } else {
-            u[0] = u[1] = u[2] = 0.f;
-            f = 0.f;
+            w.u[0] = w.u[1] = w.u[2] = 0.f;
+            w.f = 0.f;
         }
     };
-    auto gather_own = [&](int zo, const float (&u)[3], float (&c)[8]) {
-        if (t.own && zo >= t.zb && zo < t.ze && isfinite(u[0]) && isfinite(u[1]) && isfinite(u[2])) {
-            const Tap X = axis_split(t.x, u[0], g.nx), Y = axis_split(t.y, u[1], g.ny),
-                      Z = axis_split(zo, u[2], g.nz);
+    auto gather_own = [&](int zo, k2::Own& w) {
+        if (own && zo >= zb && zo < ze && isfinite(w.u[0]) && isfinite(w.u[1]) && isfinite(w.u[2])) {
+            const Tap X = axis_split(x, w.u[0], g.nx), Y = axis_split(y, w.u[1], g.ny),
+                      Z = axis_split(zo, w.u[2], g.nz);
             const float* q = M + X.i0 + g.nx * (Y.i0 + g.ny * Z.i0);
-            const int sx = X.step, dy = Y.step * g.nx, dz = Z.step * t.nxy;
-            c[0] = __ldg(q); c[1] = __ldg(q + sx); c[2] = __ldg(q + dy); c[3] = __ldg(q + dy + sx);
-            c[4] = __ldg(q + dz); c[5] = __ldg(q + dz + sx); c[6] = __ldg(q + dz + dy);
-            c[7] = __ldg(q + dz + dy + sx);
+            const int sx = X.step, dy = Y.step * g.nx, dz = Z.step * nxy;
+            w.c[0] = __ldg(q); w.c[1] = __ldg(q + sx); w.c[2] = __ldg(q + dy); w.c[3] = __ldg(q + dy + sx);
+            w.c[4] = __ldg(q + dz); w.c[5] = __ldg(q + dz + sx); w.c[6] = __ldg(q + dz + dy);
+            w.c[7] = __ldg(q + dz + dy + sx);
         }
     };
 
@@ -807,66 +855,58 @@ __global__ void __launch_bounds__(NT, 2) k_lncc_bwd(Batch b, LmParams p, int chu
 #pragma unroll
         for (int c = 0; c < 3; ++c) ring[d][c] = 0.0;
 
-    const int z0 = t.zb - R, z1 = t.ze + R;
+    const int z0 = zb - R, z1 = ze + R;
+    double* in_a = &s_in[0][0][0];
+    double* in_b = &s_in[1][0][0];
+    double* x_a = &s_x[0][0][0];
+    double* x_b = &s_x[1][0][0];
     load_halo(z0);
-    store_halo(0);
+    store_halo(in_a);
     load_halo(z0 + 1);
-    load_own(t.zb, ou0, of0);
-    gather_own(t.zb, ou0, oc0);
-    load_own(t.zb + 1, ou1, of1);
+    store_halo(in_b);
+    load_own(zb, o0);
+    gather_own(zb, o0);
+    load_own(zb + 1, o1);
+    gather_own(zb + 1, o1);
+    load_own(zb + 2, o2);
     __syncthreads();
-
+    x_pass(in_a, x_a);
+    load_halo(z0 + 2);
+    __syncthreads();
     for (int zbase = z0; zbase < z1; zbase += W) {
 #pragma unroll
-        for (int ph = 0; ph < W; ++ph) {
-            const int zi = zbase + ph;
+        for (int rs = 0; rs < W; ++rs) {
+            const int zi = zbase + rs;
             if (zi < z1) {
-                const int sb = (zi - z0) & 1;
                 const int zo = zi - R;
-                const bool emit = zo >= t.zb;
+                const bool emit = zo >= zb;
                 if (emit) {
-                    load_own(zo + 2, ou2, of2);
-                    gather_own(zo + 1, ou1, oc1);
+                    load_own(zo + 3, o3);
+                    gather_own(zo + 2, o2);
                 }
-#pragma unroll
-                for (int q = 0; q < XS; ++q) {
-                    const int idx = threadIdx.x + q * NT;
-                    if (idx < IH * TX) {
-                        const int c = idx % TX, r = idx / TX;
-#pragma unroll
-                        for (int ch = 0; ch < 3; ++ch) {
-                            const double* row = &s_in[sb][ch][r * IW + c];
-                            double s = 0.0;
-#pragma unroll
-                            for (int d = 0; d < W; ++d) s += row[d];
-                            s_x[ch][r][c] = s;
-                        }
-                    }
-                }
-                __syncthreads();
 #pragma unroll
                 for (int c = 0; c < 3; ++c) {
                     double s = 0.0;
 #pragma unroll
-                    for (int d = 0; d < W; ++d) s += s_x[c][t.oy + d][t.ox];
-                    ring[ph][c] = s;
+                    for (int d = 0; d < W; ++d) s += x_a[c * IH * TX + (oy + d) * TX + ox];
+                    ring[rs][c] = s;
                 }
-                if (emit && t.own) {
-                    double S[3];
+                if (emit && own) {
+                    double Sm[3];
 #pragma unroll
                     for (int c = 0; c < 3; ++c) {
                         double s = 0.0;
 #pragma unroll
-                        for (int d = 0; d < W; ++d) s += ring[(ph + 1 + d) % W][c];
-                        S[c] = s;
+                        for (int d = 0; d < W; ++d) s += ring[(rs + 1 + d) % W][c];
+                        Sm[c] = s;
                     }
                     double gm[3] = {0.0, 0.0, 0.0};
                     double mw = kNaN64;
-                    if (isfinite(ou0[0]) && isfinite(ou0[1]) && isfinite(ou0[2])) {
-                        const Tap X = axis_split(t.x, ou0[0], g.nx), Y = axis_split(t.y, ou0[1], g.ny),
-                                  Z = axis_split(zo, ou0[2], g.nz);
-                        const double a = oc0[0], bb = oc0[1], c = oc0[2], e = oc0[3];
-                        const double f = oc0[4], h = oc0[5], k = oc0[6], l = oc0[7];
+                    if (isfinite(o0.u[0]) && isfinite(o0.u[1]) && isfinite(o0.u[2])) {
+                        const Tap X = axis_split(x, o0.u[0], g.nx), Y = axis_split(y, o0.u[1], g.ny),
+                                  Z = axis_split(zo, o0.u[2], g.nz);
+                        const double a = o0.c[0], bb = o0.c[1], c = o0.c[2], e = o0.c[3];
+                        const double f = o0.c[4], h = o0.c[5], k = o0.c[6], l = o0.c[7];
                         const double d00 = bb - a, d10 = e - c, d01 = h - f, d11 = l - k;
                         const double v00 = fma(X.t, d00, a), v10 = fma(X.t, d10, c);
                         const double v01 = fma(X.t, d01, f), v11 = fma(X.t, d11, k);
@@ -877,21 +917,23 @@ __global__ void __launch_bounds__(NT, 2) k_lncc_bwd(Batch b, LmParams p, int chu
                         gm[2] = Z.outside ? 0.0 : s1 - s0;
                         mw = fma(Z.t, s1 - s0, s0);
                     }
-                    const double f = (double)of0 - shf;
-                    const double dm = -invN * (fma(f, S[0], (mw - shm) * S[1]) - S[2]);
-                    const int o = t.lp(g, zo) + ooff;
+                    const double f = (double)o0.f - shf;
+                    const double dm = -invN * (fma(f, Sm[0], (mw - shm) * Sm[1]) - Sm[2]);
+                    const int o = (zo - g.zlo) * nxy + ooff;
                     G[o] = (float)(dm * gm[0]);
                     G[n + o] = (float)(dm * gm[1]);
                     G[2 * n + o] = (float)(dm * gm[2]);
                 }
                 if (emit) {
-#pragma unroll
-                    for (int k = 0; k < 8; ++k) oc0[k] = oc1[k];
-                    ou0[0] = ou1[0]; ou0[1] = ou1[1]; ou0[2] = ou1[2]; of0 = of1;
-                    ou1[0] = ou2[0]; ou1[1] = ou2[1]; ou1[2] = ou2[2]; of1 = of2;
+                    o0 = o1;
+                    o1 = o2;
+                    o2 = o3;
                 }
-                store_halo(sb ^ 1);
-                load_halo(zi + 2);
+                x_pass(in_b, x_b);
+                store_halo(in_a);
+                load_halo(zi + 3);
+                double* t = in_a; in_a = in_b; in_b = t;
+                t = x_a; x_a = x_b; x_b = t;
                 __syncthreads();
             }
         }
@@ -1484,10 +1526,10 @@ void launch_finalize(const Batch& b, const LmParams& p, int mode, cudaStream_t s
 }
 
 void launch_lncc_bwd(const Batch& b, const LmParams& p, cudaStream_t s) {
-    const LaunchShape sh = shape_for(b.g, b.pairs, TY);
+    const LaunchShape sh = shape_for(b.g, b.pairs, k2::TY);
     dim3 grid = sh.grid();
     grid.z = b.pairs;
-    k_lncc_bwd<2><<<grid, NT, 0, s>>>(b, p, sh.chunk_len);
+    k_lncc_bwd<2><<<grid, k2::NT, 0, s>>>(b, p, sh.chunk_len);
     ++g_kernel_launches;
 }
 
