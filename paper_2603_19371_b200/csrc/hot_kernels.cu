@@ -594,6 +594,7 @@ __global__ void __launch_bounds__(k1::NT, 2) k_lncc_fwd(Batch b, int chunk_len) 
             f[2 * q] = a.x; f[2 * q + 1] = a.y;
             m[2 * q] = c.x; m[2 * q + 1] = c.y;
         }
+        double a[2][5];
 #pragma unroll
         for (int j = 0; j < 2; ++j) {
             double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0, a4 = 0.0;
@@ -606,9 +607,12 @@ __global__ void __launch_bounds__(k1::NT, 2) k_lncc_fwd(Batch b, int chunk_len) 
                 a3 = fma(mv, mv, a3);
                 a4 = fma(fv, mv, a4);
             }
-            double* o = out + xr * TX + 2 * xj + j;
-            o[0] = a0; o[IH * TX] = a1; o[2 * IH * TX] = a2; o[3 * IH * TX] = a3; o[4 * IH * TX] = a4;
+            a[j][0] = a0; a[j][1] = a1; a[j][2] = a2; a[j][3] = a3; a[j][4] = a4;
         }
+        // the two outputs of a moment are adjacent: one 16-byte store each
+#pragma unroll
+        for (int c = 0; c < 5; ++c)
+            *reinterpret_cast<double2*>(out + c * IH * TX + xr * TX + 2 * xj) = make_double2(a[0][c], a[1][c]);
     };
 
     const int ox = threadIdx.x & 31, oy = threadIdx.x >> 5;
