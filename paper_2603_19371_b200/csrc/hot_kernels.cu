@@ -238,7 +238,11 @@ constexpr double kNaN64 = __builtin_nan("");
 // planes plus the 2 halo planes the window pass reads.  Block (32 x 8) = a
 // 32 x 8 (x, y) tile of one plane; one voxel per thread, few registers (high
 // occupancy hides the gather latency).
-__global__ void __launch_bounds__(256) k_warp_moving(Batch b, int mode, int z_first) {
+// Each thread warps kZP planes of one (x, y) column: all displacement loads
+// are issued first, then all 8 kZP corner gathers, so a thread keeps kZP
+// independent load chains in flight (the kernel is gather-latency bound).
+constexpr int kZP = 4;
+__global__ void __launch_bounds__(256) k_warp_moving(Batch b, int mode, int z_first, int z_last) {
     const int pair = blockIdx.z;
     const PairState* st = b.st + pair;
     if (st->done) return;
@@ -247,13 +251,23 @@ __global__ void __launch_bounds__(256) k_warp_moving(Batch b, int mode, int z_fi
     const int x = (blockIdx.x % tiles_x) * 32 + (threadIdx.x & 31);
     const int y = (blockIdx.x / tiles_x) * 8 + (threadIdx.x >> 5);
     if (x >= g.nx || y >= g.ny) return;
-    const int z = z_first + blockIdx.y;
+    const int zf = z_first + blockIdx.y * kZP;
     const int buf = mode == 0 ? st->cur : 1 - st->cur;
     const float* __restrict__ M = b.M + (long long)pair * g.nfull;
     const float* __restrict__ U = b.U + ((long long)pair * 2 + buf) * 3 * g.n;
-    const int o = g.lat(x, y, z);
-    b.MW[(long long)pair * g.n + o] =
-        sample_vol<false>(M, g, x, y, z, __ldg(U + o), __ldg(U + g.n + o), __ldg(U + 2 * g.n + o), nullptr);
+    double* __restrict__ MW = b.MW + (long long)pair * g.n;
+    float u[kZP][3];
+#pragma unroll
+    for (int k = 0; k < kZP; ++k) {
+        const int z = min(zf + k, z_last - 1);
+        const int o = g.lat(x, y, z);
+        u[k][0] = __ldg(U + o); u[k][1] = __ldg(U + g.n + o); u[k][2] = __ldg(U + 2 * g.n + o);
+    }
+#pragma unroll
+    for (int k = 0; k < kZP; ++k) {
+        const int z = zf + k;
+        if (z < z_last) MW[g.lat(x, y, z)] = sample_vol<false>(M, g, x, y, z, u[k][0], u[k][1], u[k][2], nullptr);
+    }
 }
 
 // The pair's last CTA (of a 2D grid of 256-thread CTAs) reduces the owned
@@ -1475,8 +1489,8 @@ int plane_tiles(const Geo& g) { return cdiv(g.nx, TX) * cdiv(g.ny, TY); }
 
 void launch_mse_fwd(const Batch& b, const LmParams& p, int mode, cudaStream_t s) {
     (void)p;
-    const dim3 wgrid(cdiv(b.g.nx, 32) * cdiv(b.g.ny, 8), b.g.ze - b.g.zs, b.pairs);
-    k_warp_moving<<<wgrid, 256, 0, s>>>(b, mode, b.g.zs);
+    const dim3 wgrid(cdiv(b.g.nx, 32) * cdiv(b.g.ny, 8), cdiv(b.g.ze - b.g.zs, kZP), b.pairs);
+    k_warp_moving<<<wgrid, 256, 0, s>>>(b, mode, b.g.zs, b.g.ze);
     const LaunchShape sh = shape_for(b.g, b.pairs, 8);
     dim3 grid = sh.grid();
     grid.z = b.pairs;
@@ -1485,8 +1499,8 @@ void launch_mse_fwd(const Batch& b, const LmParams& p, int mode, cudaStream_t s)
 }
 
 void launch_mi_fwd(const Batch& b, const LmParams& p, int mode, cudaStream_t s) {
-    const dim3 wgrid(cdiv(b.g.nx, 32) * cdiv(b.g.ny, 8), b.g.ze - b.g.zs, b.pairs);
-    k_warp_moving<<<wgrid, 256, 0, s>>>(b, mode, b.g.zs);
+    const dim3 wgrid(cdiv(b.g.nx, 32) * cdiv(b.g.ny, 8), cdiv(b.g.ze - b.g.zs, kZP), b.pairs);
+    k_warp_moving<<<wgrid, 256, 0, s>>>(b, mode, b.g.zs, b.g.ze);
     const LaunchShape sh = shape_for(b.g, b.pairs, 8);
     dim3 grid = sh.grid();
     grid.z = b.pairs;
@@ -1515,8 +1529,8 @@ void launch_lncc_fwd(const Batch& b, const LmParams& p, int mode, cudaStream_t s
     (void)p;
     // Mw for the owned planes plus the window pass's 2-plane halo
     const int zf = std::max(0, b.g.zs - 2), zl = std::min(b.g.nz, b.g.ze + 2);
-    const dim3 wgrid(cdiv(b.g.nx, 32) * cdiv(b.g.ny, 8), zl - zf, b.pairs);
-    k_warp_moving<<<wgrid, 256, 0, s>>>(b, mode, zf);
+    const dim3 wgrid(cdiv(b.g.nx, 32) * cdiv(b.g.ny, 8), cdiv(zl - zf, kZP), b.pairs);
+    k_warp_moving<<<wgrid, 256, 0, s>>>(b, mode, zf, zl);
     const LaunchShape sh = shape_for(b.g, b.pairs, k1::TY);
     dim3 grid = sh.grid();
     grid.z = b.pairs;
