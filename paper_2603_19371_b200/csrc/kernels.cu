@@ -38,10 +38,10 @@ LaunchShape shape_for(const Geo& g, int pairs, int ty) {
     s.tiles_x = cdiv(g.nx, TX);
     s.tiles_y = cdiv(g.ny, ty);
     const long long tiles = (long long)s.tiles_x * s.tiles_y * pairs;
-    // chunks of the owned planes: aim for >= 8 resident CTAs per SM worth of
+    // chunks of the owned planes: aim for >= 4 resident CTAs per SM worth of
     // work; keep >= 8 planes a chunk
     const int nzo = g.ze - g.zs;
-    const long long want = (long long)kNumSMs * 8;
+    const long long want = (long long)kNumSMs * 4;
     int chunks = (int)std::max<long long>(1, std::min<long long>(nzo, (want + tiles - 1) / tiles));
     int len = cdiv(nzo, chunks);
     len = std::max(len, std::min(nzo, 8));
