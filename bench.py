@@ -116,20 +116,24 @@ def dist_init(n_gpus):
 
 
 def max_over_ranks(x, world, local):
+    """Max of a per-rank scalar (NCCL: on the rank's device; gloo: host)."""
     if world == 1:
         return x
     import torch
     import torch.distributed as dist
-    t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{local}")
+    dev = f"cuda:{local}" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([x], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
 
 def barrier(world, local):
     if world > 1:
-        import torch
         import torch.distributed as dist
-        dist.barrier(device_ids=[local])
+        if dist.get_backend() == "nccl":
+            dist.barrier(device_ids=[local])
+        else:
+            dist.barrier()
 
 
 # ------------------------------------------------------------------ ours ----
