@@ -251,6 +251,10 @@ def run_ours(args, rank, world, local):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline_sample(F_h[0].numpy(), M_h[0].numpy())
+    extra = None
+    if rank == 0 and world == 1 and not args.no_extra:
+        eng.close()  # free the batch engine before the pyramid runs
+        extra = pyramid_configs(ctx, lib)
 
     line = {
         "metric": METRIC,
@@ -289,6 +293,8 @@ def run_ours(args, rank, world, local):
     }
     if cpu:
         line["cpu_baseline"] = cpu
+    if extra:
+        line["pyramid_configs"] = extra
     traffic = load_traffic(dom)
     if traffic:
         line["roofline"]["traffic"] = traffic
@@ -396,6 +402,57 @@ def run_slabs(args, rank, world, local):
         line["e2e"] = e2e
     grp.close()
     return line
+
+
+def pyramid_configs(ctx, lib):
+    """BASELINE configs 2 and 3 through the whole-pyramid API (wlm_register):
+    config 2 (brain-shaped, [4,2,1] x [100,75,50], LNCC + LM + rejection) and
+    config 3 (lung-shaped, [8,4,2,1] x [100,100,75,50]) run with LM and with
+    Adam, reporting wall time (host buffers in and out) and the arena
+    high-water mark -- the north star's "peak device memory next to an
+    Adam-state baseline"."""
+    import ctypes as C
+
+    import numpy as np
+
+    import paper_2603_19371_b200 as P
+    from paper_2603_19371_b200._lib import Dims, SynthSpec
+
+    def synth(nx, ny, nz, seed, wmax):
+        F = np.empty((nz, ny, nx), np.float32)
+        M = np.empty((nz, ny, nx), np.float32)
+        spec = SynthSpec(Dims(nx, ny, nz), 12, 0.0, wmax, 0.01, seed)
+        ctx.check(lib.wlm_synth_pair(ctx.h, C.byref(spec), F.ctypes.data, M.ctypes.data, None, 0))
+        return F, M
+
+    def run(F, M, cfg):
+        P.register(F, M, cfg, ctx=ctx)  # warm (module load, first allocations)
+        t0 = time.perf_counter()
+        res = P.register(F, M, cfg, ctx=ctx)
+        dt = time.perf_counter() - t0
+        attempts = sum(1 + t.retries for t in res.loss_trace)
+        return res, dt, attempts
+
+    out = {}
+    F, M = synth(160, 192, 224, 1, 6.0)
+    cfg = P.reg_config(nlevels=3, factors=[4, 2, 1], iters=[100, 75, 50], **{"lm.rejection": 1})
+    res, dt, att = run(F, M, cfg)
+    out["config2"] = {"dims": [160, 192, 224], "schedule": "[4,2,1] x [100,75,50]", "rejection": True,
+                      "wall_s": round(dt, 4), "attempts": att, "accepted_iters": len(res.loss_trace),
+                      "final_r": res.loss_trace[-1].r, "peak_device_bytes": res.peak_device_bytes}
+    F, M = synth(224, 192, 224, 2, 8.0)
+    kw = dict(nlevels=4, factors=[8, 4, 2, 1], iters=[100, 100, 75, 50])
+    lm, dt_lm, _ = run(F, M, P.reg_config(**kw))
+    ad, dt_ad, _ = run(F, M, P.reg_config(optimizer=P.OPT_ADAM, **kw))
+    out["config3"] = {"dims": [224, 192, 224], "schedule": "[8,4,2,1] x [100,100,75,50]",
+                      "lm": {"wall_s": round(dt_lm, 4), "peak_device_bytes": lm.peak_device_bytes,
+                             "final_r": lm.loss_trace[-1].r},
+                      "adam": {"wall_s": round(dt_ad, 4), "peak_device_bytes": ad.peak_device_bytes,
+                               "final_r": ad.loss_trace[-1].r},
+                      "lm_memory_saving": round(1 - lm.peak_device_bytes / ad.peak_device_bytes, 4),
+                      "state_bytes": {"lm": P.state_bytes(P.OPT_LM, (224, 192, 224)),
+                                      "adam": P.state_bytes(P.OPT_ADAM, (224, 192, 224))}}
+    return out
 
 
 def load_traffic(kernel):
@@ -507,6 +564,7 @@ def main():
     ap.add_argument("--pairs-per-gpu", type=int, default=8)
     ap.add_argument("--e2e-iters", type=int, default=100)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extra", action="store_true", help="skip the config 2/3 pyramid runs")
     ap.add_argument("--ref-budget-s", type=float, default=200.0)
     ap.add_argument("--config", type=int, default=4, choices=[4, 5],
                     help="4: batch of 192^3 pairs (default, weak scaling); 5: one 1024^3 volume in z-slabs")
