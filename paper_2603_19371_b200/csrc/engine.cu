@@ -110,6 +110,7 @@ void engine_alloc(wlm_engine* e) {
     e->U = DevBuf<float>(ctx, B * 6 * n);
     e->ABE = DevBuf<float>(ctx, B * 4 * n);  // A, B fp32 + E fp64
     e->MW = DevBuf<double>(ctx, B * n);
+    if (e->P.metric == WLM_METRIC_LNCC) e->GM = DevBuf<double>(ctx, B * 3 * n);  // K1a -> K2
     e->shift_part = DevBuf<double>(ctx, B * 2 * 256 * 3);  // sums + (min, max)
     init_constants();
     e->G = DevBuf<float>(ctx, B * 3 * n);
@@ -147,6 +148,7 @@ void engine_alloc(wlm_engine* e) {
     b.U = e->U.p; b.ABE = e->ABE.p; b.G = e->G.p; b.VS = e->VS.p;
     b.AM = e->AM.p; b.AV = e->AV.p;
     b.MW = e->MW.p;
+    b.GM = e->GM.p;
     b.st = e->st.p;
     b.partials = e->partials.p;
     if (!e->shared_plane_sum) b.plane_sum = e->plane_sum.p;

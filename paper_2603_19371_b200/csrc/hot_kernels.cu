@@ -241,7 +241,12 @@ constexpr double kNaN64 = __builtin_nan("");
 // Each thread warps kZP planes of one (x, y) column: all displacement loads
 // are issued first, then all 8 kZP corner gathers, so a thread keeps kZP
 // independent load chains in flight (the kernel is gather-latency bound).
+// With GRAD (LNCC) it also stores the analytic interpolant gradient: the
+// evaluated warp becomes the accepted one exactly when K2 runs next (K2 is
+// skipped after a rejection), so K2 reads Mw and grad M instead of
+// re-gathering M at the same points.
 constexpr int kZP = 4;
+template <bool GRAD>
 __global__ void __launch_bounds__(256) k_warp_moving(Batch b, int mode, int z_first, int z_last) {
     const int pair = blockIdx.z;
     const PairState* st = b.st + pair;
@@ -266,7 +271,18 @@ __global__ void __launch_bounds__(256) k_warp_moving(Batch b, int mode, int z_fi
 #pragma unroll
     for (int k = 0; k < kZP; ++k) {
         const int z = zf + k;
-        if (z < z_last) MW[g.lat(x, y, z)] = sample_vol<false>(M, g, x, y, z, u[k][0], u[k][1], u[k][2], nullptr);
+        if (z >= z_last) continue;
+        const int o = g.lat(x, y, z);
+        if (GRAD) {
+            double gr[3];
+            MW[o] = sample_vol<true>(M, g, x, y, z, u[k][0], u[k][1], u[k][2], gr);
+            double* GMp = b.GM + (long long)pair * 3 * g.n;
+            GMp[o] = gr[0];
+            GMp[g.n + o] = gr[1];
+            GMp[2 * g.n + o] = gr[2];
+        } else {
+            MW[o] = sample_vol<false>(M, g, x, y, z, u[k][0], u[k][1], u[k][2], nullptr);
+        }
     }
 }
 
@@ -738,8 +754,8 @@ __global__ void k_finalize(Batch b, LmParams p, int mode) {
 // Schedule (as K1b): one barrier per plane; phase p runs the y-pass of plane p
 // (z ring, output plane p - R), the x-pass of plane p+1 (two outputs per
 // thread from 16-byte shared loads), the halo tile of plane p+2 and the loads
-// of plane p+3.  The output voxel's u and F are loaded three planes ahead and
-// its 8 M corners gathered two planes ahead of their use.
+// of plane p+3.  Mw and grad M(x+u) come from K1a's evaluation of this warp
+// (no gathers here), loaded three planes ahead.
 namespace k2 {
 constexpr int TX = 32, TY = 8, NT = 256;
 template <int R>
@@ -748,10 +764,10 @@ struct Shape {
     static constexpr int SL = (NI + NT - 1) / NT;
     static constexpr int NV = (2 + 2 * R + 1) / 2;
 };
-// one output voxel in flight: u, F, and (once gathered) its cell
+// one output voxel in flight: F, Mw and grad M (K1a)
 struct Own {
-    float u[3], f;
-    float c[8];
+    float f;
+    double mw, gm[3];
 };
 }  // namespace k2
 
@@ -843,27 +859,20 @@ __global__ void __launch_bounds__(k2::NT, 2) k_lncc_bwd(Batch b, LmParams p, int
     const int x = x0 + ox, y = y0 + oy;
     const bool own = x < g.nx && y < g.ny;
     const int ooff = x + g.nx * y;
-    // output pipeline: planes zo (consumed), zo+1 (gathered), zo+2, zo+3 (dense loads)
+    // output pipeline (dense loads, three planes ahead): F, Mw and grad M of
+    // the accepted warp from K1a
+    const double* __restrict__ MWp = b.MW + (long long)pair * n;
+    const double* __restrict__ GMp = b.GM + (long long)pair * 3 * n;
     k2::Own o0, o1, o2, o3;
     auto load_own = [&](int zo, k2::Own& w) {
         if (own && zo >= zb && zo < ze) {
             const int o = (zo - g.zlo) * nxy + ooff;
-            w.u[0] = __ldg(U + o); w.u[1] = __ldg(U + n + o); w.u[2] = __ldg(U + 2 * n + o);
             w.f = __ldg(F + zo * nxy + ooff);
+            w.mw = __ldg(MWp + o);
+            w.gm[0] = __ldg(GMp + o); w.gm[1] = __ldg(GMp + n + o); w.gm[2] = __ldg(GMp + 2 * n + o);
         } else {
-            w.u[0] = w.u[1] = w.u[2] = 0.f;
             w.f = 0.f;
-        }
-    };
-    auto gather_own = [&](int zo, k2::Own& w) {
-        if (own && zo >= zb && zo < ze && isfinite(w.u[0]) && isfinite(w.u[1]) && isfinite(w.u[2])) {
-            const Tap X = axis_split(x, w.u[0], g.nx), Y = axis_split(y, w.u[1], g.ny),
-                      Z = axis_split(zo, w.u[2], g.nz);
-            const float* q = M + X.i0 + g.nx * (Y.i0 + g.ny * Z.i0);
-            const int sx = X.step, dy = Y.step * g.nx, dz = Z.step * nxy;
-            w.c[0] = __ldg(q); w.c[1] = __ldg(q + sx); w.c[2] = __ldg(q + dy); w.c[3] = __ldg(q + dy + sx);
-            w.c[4] = __ldg(q + dz); w.c[5] = __ldg(q + dz + sx); w.c[6] = __ldg(q + dz + dy);
-            w.c[7] = __ldg(q + dz + dy + sx);
+            w.mw = w.gm[0] = w.gm[1] = w.gm[2] = 0.0;
         }
     };
 
@@ -883,9 +892,7 @@ __global__ void __launch_bounds__(k2::NT, 2) k_lncc_bwd(Batch b, LmParams p, int
     load_halo(z0 + 1);
     store_halo(in_b);
     load_own(zb, o0);
-    gather_own(zb, o0);
     load_own(zb + 1, o1);
-    gather_own(zb + 1, o1);
     load_own(zb + 2, o2);
     __syncthreads();
     x_pass(in_a, x_a);
@@ -898,10 +905,7 @@ __global__ void __launch_bounds__(k2::NT, 2) k_lncc_bwd(Batch b, LmParams p, int
             if (zi < z1) {
                 const int zo = zi - R;
                 const bool emit = zo >= zb;
-                if (emit) {
-                    load_own(zo + 3, o3);
-                    gather_own(zo + 2, o2);
-                }
+                if (emit) load_own(zo + 3, o3);
 #pragma unroll
                 for (int c = 0; c < 3; ++c) {
                     double s = 0.0;
@@ -918,23 +922,8 @@ __global__ void __launch_bounds__(k2::NT, 2) k_lncc_bwd(Batch b, LmParams p, int
                         for (int d = 0; d < W; ++d) s += ring[(rs + 1 + d) % W][c];
                         Sm[c] = s;
                     }
-                    double gm[3] = {0.0, 0.0, 0.0};
-                    double mw = kNaN64;
-                    if (isfinite(o0.u[0]) && isfinite(o0.u[1]) && isfinite(o0.u[2])) {
-                        const Tap X = axis_split(x, o0.u[0], g.nx), Y = axis_split(y, o0.u[1], g.ny),
-                                  Z = axis_split(zo, o0.u[2], g.nz);
-                        const double a = o0.c[0], bb = o0.c[1], c = o0.c[2], e = o0.c[3];
-                        const double f = o0.c[4], h = o0.c[5], k = o0.c[6], l = o0.c[7];
-                        const double d00 = bb - a, d10 = e - c, d01 = h - f, d11 = l - k;
-                        const double v00 = fma(X.t, d00, a), v10 = fma(X.t, d10, c);
-                        const double v01 = fma(X.t, d01, f), v11 = fma(X.t, d11, k);
-                        const double s0 = fma(Y.t, v10 - v00, v00), s1 = fma(Y.t, v11 - v01, v01);
-                        const double gx0 = fma(Y.t, d10 - d00, d00), gx1 = fma(Y.t, d11 - d01, d01);
-                        gm[0] = X.outside ? 0.0 : fma(Z.t, gx1 - gx0, gx0);
-                        gm[1] = Y.outside ? 0.0 : fma(Z.t, (v11 - v01) - (v10 - v00), v10 - v00);
-                        gm[2] = Z.outside ? 0.0 : s1 - s0;
-                        mw = fma(Z.t, s1 - s0, s0);
-                    }
+                    const double mw = o0.mw;
+                    const double* gm = o0.gm;
                     const double f = (double)o0.f - shf;
                     const double dm = -invN * (fma(f, Sm[0], (mw - shm) * Sm[1]) - Sm[2]);
                     const int o = (zo - g.zlo) * nxy + ooff;
@@ -1490,7 +1479,7 @@ int plane_tiles(const Geo& g) { return cdiv(g.nx, TX) * cdiv(g.ny, TY); }
 void launch_mse_fwd(const Batch& b, const LmParams& p, int mode, cudaStream_t s) {
     (void)p;
     const dim3 wgrid(cdiv(b.g.nx, 32) * cdiv(b.g.ny, 8), cdiv(b.g.ze - b.g.zs, kZP), b.pairs);
-    k_warp_moving<<<wgrid, 256, 0, s>>>(b, mode, b.g.zs, b.g.ze);
+    k_warp_moving<false><<<wgrid, 256, 0, s>>>(b, mode, b.g.zs, b.g.ze);
     const LaunchShape sh = shape_for(b.g, b.pairs, 8);
     dim3 grid = sh.grid();
     grid.z = b.pairs;
@@ -1500,7 +1489,7 @@ void launch_mse_fwd(const Batch& b, const LmParams& p, int mode, cudaStream_t s)
 
 void launch_mi_fwd(const Batch& b, const LmParams& p, int mode, cudaStream_t s) {
     const dim3 wgrid(cdiv(b.g.nx, 32) * cdiv(b.g.ny, 8), cdiv(b.g.ze - b.g.zs, kZP), b.pairs);
-    k_warp_moving<<<wgrid, 256, 0, s>>>(b, mode, b.g.zs, b.g.ze);
+    k_warp_moving<false><<<wgrid, 256, 0, s>>>(b, mode, b.g.zs, b.g.ze);
     const LaunchShape sh = shape_for(b.g, b.pairs, 8);
     dim3 grid = sh.grid();
     grid.z = b.pairs;
@@ -1530,7 +1519,7 @@ void launch_lncc_fwd(const Batch& b, const LmParams& p, int mode, cudaStream_t s
     // Mw for the owned planes plus the window pass's 2-plane halo
     const int zf = std::max(0, b.g.zs - 2), zl = std::min(b.g.nz, b.g.ze + 2);
     const dim3 wgrid(cdiv(b.g.nx, 32) * cdiv(b.g.ny, 8), cdiv(zl - zf, kZP), b.pairs);
-    k_warp_moving<<<wgrid, 256, 0, s>>>(b, mode, zf, zl);
+    k_warp_moving<true><<<wgrid, 256, 0, s>>>(b, mode, zf, zl);
     const LaunchShape sh = shape_for(b.g, b.pairs, k1::TY);
     dim3 grid = sh.grid();
     grid.z = b.pairs;

@@ -149,7 +149,7 @@ struct wlm_engine {
     wlm_reg_config cfg{};
     LmParams P{};
     DevBuf<float> F, M, U, ABE, G, VS, AM, AV;
-    DevBuf<double> MW;
+    DevBuf<double> MW, GM;
     DevBuf<PairState> st;
     DevBuf<double> partials, script, shift_part, plane_sum, TM, MIT;
     DevBuf<unsigned long long> HIST;

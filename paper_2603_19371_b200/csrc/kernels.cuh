@@ -65,7 +65,8 @@ struct Batch {
     const float* M;   // [pair][n]
     float* U;         // [pair][2][3][n] ping-pong warps
     float* ABE;       // [pair][4][n]  LNCC window coefficients: A, B (fp32), E (fp64)
-    double* MW;       // [pair][n]     warped moving image M(x + u) (fp64, K1a -> K1b)
+    double* MW;       // [pair][n]     warped moving image M(x + u) (fp64, K1a -> K1b, K2)
+    double* GM;       // [pair][3][n]  grad M(x + u) of the evaluated warp (LNCC: K1a -> K2), or null
     float* G;         // [pair][3][n]  gradient g, Adam step in place
     float* VS;        // [pair][3][n]  smoothed step dU_s
     float* AM;        // [pair][3][n]  Adam first moment (or null)
