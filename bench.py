@@ -29,17 +29,21 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = json.load(open(os.path.join(ROOT, "BASELINE.json")))["metric"]
-# Canonical algorithmic HBM bytes per voxel per kernel:
-#   K1 eval  : u 12 + F 4 + M 4 (gather) + write A,B 8 + E 8 (fp64)  = 36
-#   K2 grad  : A,B 8 + E 8 + F 4 + u 12 + M 4 + write g 12          = 48
-#   K3 step  : g 12 + write dU_s 12                                 = 24
-#   K4 comp. : dU_s 12 + u 12 (gather) + write u' 12                = 36
-# (SURVEY 8(d)'s canonical 136 B stores E in fp32; E is fp64 here for the
-#  exact adjoint cancellation.)  K1 is timed as its two
-#  launches (K1a warp of M, K1b window pass) against the 36 B it must move.
-KERNEL_BYTES = {"K1_lncc_fwd": 36, "K2_lncc_bwd": 48, "K3_step_smooth": 24, "K4_compose_smooth": 36}
+# Algorithmic HBM bytes per voxel per kernel: SURVEY 8(d)'s canonical figures
+# (each logical array read or written once per stage, fp32), the numerator of
+# roofline.achieved:
+#   K1 eval  : u 12 + F 4 + M 4 + write A, B, E 12                   = 32
+#   K2 grad  : A, B, E 12 + F 4 + u 12 + M 4 + write g 12            = 44
+#   K3 step  : g 12 + write dU_s 12                                  = 24
+#   K4 comp. : dU_s 12 + u 12 + write u' 12                          = 36
+# This design moves more by choice: E in fp64 (+4 B in
+# K1 and K2), Mw in fp64 between K1a and K1b (+16 B), and grad M(x+u) in fp64
+# from K1a to K2 instead of a second gather (+24 B write, +24 B read, -16 B
+# u/M in K2) -- reported as design_bytes_per_voxel.
+KERNEL_BYTES = {"K1_lncc_fwd": 32, "K2_lncc_bwd": 44, "K3_step_smooth": 24, "K4_compose_smooth": 36}
+DESIGN_BYTES = {"K1_lncc_fwd": 76, "K2_lncc_bwd": 64, "K3_step_smooth": 24, "K4_compose_smooth": 36}
 STAGE_ID = {"K1_lncc_fwd": 0, "K2_lncc_bwd": 1, "K3_step_smooth": 2, "K4_compose_smooth": 3}
-BYTES_PER_VOXEL_ITER = sum(KERNEL_BYTES.values())  # 136
+BYTES_PER_VOXEL_ITER = sum(KERNEL_BYTES.values())  # 136 (SURVEY 8(d) canonical)
 
 
 def peaks():
@@ -280,6 +284,7 @@ def run_ours(args, rank, world, local):
                      "peak": hbm, "peak_kind": peak_kind, "unit": "GB/s",
                      "frac": round(achieved / hbm, 4), "traffic": None,
                      "algorithmic_bytes_per_voxel": KERNEL_BYTES[dom],
+                     "design_bytes_per_voxel": DESIGN_BYTES[dom],
                      "per_kernel_ms": {k: round(v, 4) for k, v in per_kernel.items()},
                      "iteration_frac": round(it_frac, 4),
                      "iteration_bytes_per_voxel": BYTES_PER_VOXEL_ITER},
