@@ -43,7 +43,7 @@ typedef struct ncclComm* Comm;
 struct UniqueId {
     char internal[128];
 };
-enum { Int32 = 2, Uint32 = 3, Float32 = 7, Float64 = 8 };
+enum { Int32 = 2, Uint32 = 3, Uint64 = 5, Float32 = 7, Float64 = 8 };
 enum { Sum = 0, Max = 2, Min = 3 };
 typedef int (*GetUniqueId_t)(UniqueId*);
 typedef int (*CommInitRank_t)(Comm*, int, UniqueId, int);
@@ -99,6 +99,8 @@ bool load(const char* path, std::string* why) {
 }  // namespace nccl
 
 namespace {
+
+int cdiv_host(int a, int b) { return (a + b - 1) / b; }
 
 constexpr int kHalo = 4;  // >= max(R_u, R_w + 1, 2) for sigma <= 1
 
@@ -171,6 +173,16 @@ __global__ void k_copy_attempt_warp(float* dst, long long dn, long long doff, co
 
 __global__ void k_set_cur0(PairState* st) { st->cur = 0; }
 
+// MI: sum of the slabs' fixed-point joint histograms, written back to every
+// slab (integer sums: exact and order-independent).
+__global__ void k_hist_allreduce(unsigned long long** h, int n, int bins2) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < bins2; i += gridDim.x * blockDim.x) {
+        unsigned long long t = 0ull;
+        for (int k = 0; k < n; ++k) t += h[k][i];
+        for (int k = 0; k < n; ++k) h[k][i] = t;
+    }
+}
+
 __global__ void k_group_cond(const PairState* st, cudaGraphConditionalHandle h) {
     cudaGraphSetConditional(h, st->done ? 0u : 1u);
 }
@@ -189,6 +201,7 @@ struct wlm_slab_group {
     DevBuf<float> F, M;        // local transport: whole volume, shared
     DevBuf<double> plane_sum;  // local transport: shared per-plane sums
     DevBuf<PairState*> sts;
+    DevBuf<unsigned long long*> hists;  // MI: every slab's histogram (in-process)
     nccl::Comm comm = nullptr;  // nccl transport
     cudaGraphExec_t step_exec = nullptr, loop_exec = nullptr;
     cudaGraph_t step_graph = nullptr, loop_graph = nullptr;
@@ -298,6 +311,18 @@ struct wlm_slab_group {
     }
 
     void reduce_planes(cudaStream_t s) {
+        if (eng[0]->P.metric == WLM_METRIC_MI) {  // the loss is the whole-volume histogram
+            const int bins2 = eng[0]->P.mi_bins * eng[0]->P.mi_bins;
+            if (!distributed()) {
+                k_hist_allreduce<<<cdiv_host(bins2, 256), 256, 0, s>>>(hists.p, (int)eng.size(), bins2);
+                ++g_kernel_launches;
+            } else {
+                unsigned long long* h = eng[0]->B.HIST;
+                nccl_check(nccl::g_api.all_reduce(h, h, (size_t)bins2, nccl::Uint64, nccl::Sum, comm, s),
+                           "ncclAllReduce(histogram)");
+            }
+            return;
+        }
         if (!distributed()) return;  // one shared plane array
         double* ps = eng[0]->B.plane_sum;
         nccl_check(nccl::g_api.all_reduce(ps, ps, (size_t)dims.nz, nccl::Float64, nccl::Sum, comm, s),
@@ -430,6 +455,13 @@ wlm_status make_group(wlm_ctx* ctx, wlm_dims d, int nslabs, int first, int count
         grp->sts = DevBuf<PairState*>(ctx, hst.size());
         CK(cudaMemcpyAsync(grp->sts.p, hst.data(), sizeof(PairState*) * hst.size(), cudaMemcpyHostToDevice,
                            ctx->stream));
+        if (cfg->metric == WLM_METRIC_MI) {
+            std::vector<unsigned long long*> hh;
+            for (auto* e : grp->eng) hh.push_back(e->B.HIST);
+            grp->hists = DevBuf<unsigned long long*>(ctx, hh.size());
+            CK(cudaMemcpyAsync(grp->hists.p, hh.data(), sizeof(unsigned long long*) * hh.size(),
+                               cudaMemcpyHostToDevice, ctx->stream));
+        }
         CK(cudaStreamSynchronize(ctx->stream));
     });
     if (s != WLM_OK) {
@@ -442,10 +474,6 @@ wlm_status make_group(wlm_ctx* ctx, wlm_dims d, int nslabs, int first, int count
 
 wlm_status check_split(wlm_ctx* ctx, wlm_dims d, int nslabs, const wlm_reg_config* cfg) {
     if (!ctx || nslabs < 1 || !valid_dims(d)) return WLM_INVALID_ARG;
-    if (cfg->metric == WLM_METRIC_MI) {
-        set_err(ctx, "slab_group: MI needs the joint histogram of the whole volume; not built");
-        return WLM_UNSUPPORTED;
-    }
     if (cfg->lm.tile_size != 1) {
         set_err(ctx, "slab_group: tiled LM (tile_size > 1) pools g over tiles that cross slabs; not built");
         return WLM_UNSUPPORTED;

@@ -380,7 +380,8 @@ def test_slab_group_rejects_thin_slabs(P, ctx):
         P.SlabGroup((12, 16, 16), 4, cfg=cfg, ctx=ctx)
 
 
-@pytest.mark.parametrize("extra", [{}, {"lm.rejection": 1, "lm.tau": 0.2, "log_jacobian": 1}])
+@pytest.mark.parametrize("extra", [{}, {"lm.rejection": 1, "lm.tau": 0.2, "log_jacobian": 1},
+                                   {"metric": 2, "mi_bins": 16}])
 def test_nccl_rank_slab_world1_matches_engine(P, ctx, extra):
     """The one-process-per-GPU transport on a real NCCL communicator of one
     rank: plane-sum and max all-reduces, foreign-plane zeroing and the eager
@@ -504,3 +505,14 @@ def test_mi_engine_vs_oracle(P, ctx):
         assert rc == 0
         compare_runs(tr, tr_o, aos(warp[0]), u_o, lt, wt)
     assert tr[-1]["loss_raw"] > tr[0]["loss_raw"]  # MI increases
+
+
+def test_mi_slab_group_bit_identical(P, ctx):
+    """MI over z-slabs: the slabs' fixed-point histograms are summed exactly,
+    so any split gives the single-domain trajectory bit for bit."""
+    F, M, _ = O.synth_pair((20, 24, 28), 24, num_blobs=8, warp_max=2.5)
+    cfg = P.reg_config(nlevels=1, factors=[1], iters=[8], metric=2, mi_bins=20)
+    w1, (t1,), _ = run_engine(P, ctx, F, M, cfg, 8)
+    for ns in (2, 3):
+        w, t, _ = run_slabs(P, ctx, F, M, cfg, 8, ns)
+        assert same_trace(t, t1) and np.array_equal(w, w1[0]), ns
