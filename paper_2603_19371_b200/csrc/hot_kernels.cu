@@ -23,6 +23,7 @@
 // Slabs (Geo in common.cuh): per-voxel buffers are local ([zlo, zlo+nzl),
 // indexed with Geo::lat), F and M are whole-volume (Geo::at), faces are the
 // global ones.
+#include <atomic>
 #include <cfloat>
 #include <climits>
 
@@ -41,14 +42,24 @@ __host__ __device__ inline int cdiv(int a, int b) { return (a + b - 1) / b; }
 
 __constant__ double c_inv_count[126];  // 1/n for truncated window counts n <= 125
 
+// Constant memory and function attributes are per device: one bit per
+// device ordinal (a process may drive several devices through several
+// contexts).
+static std::atomic<unsigned long long> g_const_ready{0ull};
+static unsigned long long device_bit() {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    return 1ull << (dev & 63);
+}
+
 void init_constants() {
-    static bool done = false;
-    if (done) return;
+    const unsigned long long bit = device_bit();
+    if (g_const_ready.load() & bit) return;
     double inv[126];
     inv[0] = 0.0;
     for (int i = 1; i < 126; ++i) inv[i] = 1.0 / (double)i;
     cudaMemcpyToSymbol(c_inv_count, inv, sizeof(inv));
-    done = true;
+    g_const_ready.fetch_or(bit);
 }
 
 // ---------------------------------------------------------------------------
@@ -1557,11 +1568,12 @@ void launch_compose_smooth(const Batch& b, const LmParams& p, cudaStream_t s) {
     dim3 grid = sh.grid();
     grid.z = b.pairs;
     WLM_DISPATCH_R(p.Rw, ({
-        static bool attr = false;
-        if (!attr) {
+        static std::atomic<unsigned long long> attr{0ull};  // per device
+        const unsigned long long bit = device_bit();
+        if (!(attr.load() & bit)) {
             cudaFuncSetAttribute(k_compose_smooth<RR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)k4::Shape<RR>::BYTES);
-            attr = true;
+            attr.fetch_or(bit);
         }
         k_compose_smooth<RR><<<grid, k4::NT, k4::Shape<RR>::BYTES, s>>>(b, p, sh.chunk_len);
     }));
