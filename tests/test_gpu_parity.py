@@ -516,3 +516,17 @@ def test_mi_slab_group_bit_identical(P, ctx):
     for ns in (2, 3):
         w, t, _ = run_slabs(P, ctx, F, M, cfg, 8, ns)
         assert same_trace(t, t1) and np.array_equal(w, w1[0]), ns
+
+
+@pytest.mark.parametrize("extra", [{"metric": 1}, {"metric": 1, "optimizer": 3},
+                                   {"metric": 2, "mi_bins": 24}, {"lm.tile_size": 2}])
+def test_register_pyramid_other_losses_and_steps(P, ctx, extra):
+    """The whole pyramid (levels, warp inheritance, lambda carry) with MSE,
+    Demons, MI and tiled LM against the fp32-storage oracle."""
+    F, M, _ = O.synth_pair((32, 40, 48), 3, num_blobs=10, warp_max=3.0)
+    kw = dict(nlevels=2, factors=[2, 1], iters=[12, 8], **extra)
+    res = P.register(F, M, P.reg_config(**kw), ctx=ctx)
+    with O.fp32_storage():
+        rc, w_s, tr_s, _ = O.register(F, M, O.default_config(**kw))
+    assert rc == 0 and len(res.loss_trace) == len(tr_s) == 20
+    compare_runs(res.loss_trace, tr_s, res.final_warp, w_s, 1e-6, 1e-5)
