@@ -1220,7 +1220,7 @@ __global__ void __launch_bounds__(k3::NT, 2) k_step_smooth(Batch b, LmParams p, 
 // tile (warp planes p+1..p+3 from the ring, its step from registers); warp
 // plane p+4 into the ring; global loads of warp plane p+5 and step p+3.
 namespace k4 {
-constexpr int TX = 32, TY = 8, NT = 256;
+constexpr int TX = 32, TY = 16, NT = 512;
 template <int R>
 struct Shape {
     // composed tile: IW = TX + 2R items a row, stored with the warp tile's row
@@ -1238,7 +1238,7 @@ struct Shape {
 }  // namespace k4
 
 template <int R>
-__global__ void __launch_bounds__(k4::NT, 2) k_compose_smooth(Batch b, LmParams p, int chunk_len) {
+__global__ void __launch_bounds__(k4::NT, 1) k_compose_smooth(Batch b, LmParams p, int chunk_len) {
     using S = k4::Shape<R>;
     constexpr int TX = k4::TX, NT = k4::NT, W = 2 * R + 1;
     constexpr int IWP = S::IWP, IH = S::IH, NI = S::NI, UW = S::UW, UN = S::UN, SL = S::SL, USL = S::USL,
