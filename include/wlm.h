@@ -75,7 +75,7 @@ typedef struct { int nx, ny, nz; } wlm_dims;
 /* LmConfig. lambda_max <= 0 or inf: uncapped. */
 typedef struct {
     double lambda0, mu_plus, mu_minus;
-    int tile_size;   /* k of Eq. 5 (1 = pointwise Eq. 4); slab groups: 1 only */
+    int tile_size;   /* k of Eq. 5 (1 = pointwise Eq. 4) */
     int rejection;
     double tau, lambda_max;
     int max_retries;
@@ -254,11 +254,15 @@ wlm_status wlm_engine_stage(wlm_engine* e, int stage);
  * context's device; wlm_slab_group_create_nccl holds slab `rank` of
  * `nranks` in this process (one process per GPU) and exchanges halos with
  * NCCL send/recv and reduces with NCCL all-reduce (replaces the proposed
- * wlm_ctx_attach_comm).  Both execute the same halo plan.     */
+ * wlm_ctx_attach_comm).  Both execute the same halo plan.
+ * Every loss (LNCC, MSE, MI) and step (pointwise or tiled LM, Adam, GD,
+ * Demons) runs sharded.                                                      */
 typedef struct wlm_slab_group wlm_slab_group;
 /* One halo transfer of slab `slab`: buffer 0 = g, 1 = dU_s, 2 = warp,
- * 3 = LNCC coefficients A/B/E; planes [z0, z1) received from (send == 0) or
- * sent to (send == 1) slab `peer`. */
+ * 3 = LNCC coefficients A/B/E, 4 = tiled-LM step matrices (whole k^3
+ * tile-planes); planes [z0, z1) received from (send == 0) or sent to
+ * (send == 1) slab `peer`.  With lm.tile_size = k > 1 the slab boundaries
+ * are rounded down to multiples of k. */
 typedef struct {
     int buffer, peer, send, z0, z1;
 } wlm_halo_xfer;

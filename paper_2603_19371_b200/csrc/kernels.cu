@@ -476,6 +476,7 @@ __global__ void k_tile_matrix(Batch b, LmParams p) {
     const Geo g = b.g;
     const int k = p.tile_k;
     const int bx = (int)(t % b.tkx), by = (int)((t / b.tkx) % b.tky), bz = (int)(t / ((long long)b.tkx * b.tky));
+    if (bz * k < g.zs || bz * k >= g.ze) return;  // slabs: tiles of the owned (tile-aligned) planes
     const int x1 = min(g.nx, (bx + 1) * k), y1 = min(g.ny, (by + 1) * k), z1 = min(g.nz, (bz + 1) * k);
     const float* G = b.G + (long long)pair * 3 * g.n;
     double H[6] = {0, 0, 0, 0, 0, 0};

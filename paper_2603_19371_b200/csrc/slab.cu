@@ -31,6 +31,7 @@
 
 #include <algorithm>
 #include <cstring>
+#include <string>
 #include <vector>
 
 #include "internal.cuh"
@@ -104,11 +105,18 @@ int cdiv_host(int a, int b) { return (a + b - 1) / b; }
 
 constexpr int kHalo = 4;  // >= max(R_u, R_w + 1, 2) for sigma <= 1
 
-enum Buffer { BUF_G = 0, BUF_V = 1, BUF_U = 2, BUF_ABE = 3 };
+enum Buffer { BUF_G = 0, BUF_V = 1, BUF_U = 2, BUF_ABE = 3, BUF_TM = 4 };
 
-void partition(int nz, int nslabs, int k, int* zs, int* ze) {
-    *zs = (int)((long long)k * nz / nslabs);
-    *ze = (int)((long long)(k + 1) * nz / nslabs);
+// Owned planes of slab k; with tiled LM (align = k of Eq. 5) the boundaries
+// sit on tile boundaries so no k^3 tile straddles two slabs.
+void partition(int nz, int nslabs, int k, int* zs, int* ze, int align = 1) {
+    auto bound = [&](int i) {
+        if (i >= nslabs) return nz;
+        const int z = (int)((long long)i * nz / nslabs);
+        return align > 1 ? z / align * align : z;
+    };
+    *zs = bound(k);
+    *ze = bound(k + 1);
 }
 
 int halo_depth(int buffer, int Ru, int Rw) {
@@ -125,10 +133,24 @@ int halo_depth(int buffer, int Ru, int Rw) {
 // halo planes [z0, z1) from the neighbour owning them and sends the
 // neighbour's halo planes out of its own owned planes; the two rows of one
 // transfer name the same [z0, z1) on both sides.
-std::vector<wlm_halo_xfer> slab_plan(wlm_dims d, int nslabs, int k, int Ru, int Rw) {
+// Tiled LM: the step matrices of the k^3 tiles covering the R_u halo planes
+// come from the neighbour that owns them (rows in planes, whole tile-planes).
+std::vector<wlm_halo_xfer> slab_plan(wlm_dims d, int nslabs, int k, int Ru, int Rw, int tk = 1) {
     std::vector<wlm_halo_xfer> rows;
     int zs, ze;
-    partition(d.nz, nslabs, k, &zs, &ze);
+    partition(d.nz, nslabs, k, &zs, &ze, tk);
+    auto down = [&](int z) { return std::max(0, (z >= 0 ? z : z - tk + 1) / tk * tk); };
+    auto up = [&](int z) { return std::min(d.nz, (z + tk - 1) / tk * tk); };
+    if (tk > 1) {
+        if (k > 0) {
+            rows.push_back({BUF_TM, k - 1, 0, down(zs - Ru), zs});
+            rows.push_back({BUF_TM, k - 1, 1, zs, up(zs + Ru)});
+        }
+        if (k + 1 < nslabs) {
+            rows.push_back({BUF_TM, k + 1, 0, ze, up(ze + Ru)});
+            rows.push_back({BUF_TM, k + 1, 1, down(ze - Ru), ze});
+        }
+    }
     for (int b = BUF_G; b <= BUF_ABE; ++b) {
         const int h = halo_depth(b, Ru, Rw);
         if (h <= 0) continue;
@@ -245,7 +267,42 @@ struct wlm_slab_group {
         }
     }
 
+    // Tile step matrices: global tile-plane indexing on every slab, so a row
+    // [z0, z1) (tile-aligned planes) is the same byte range on both sides.
+    void tm_range(const wlm_halo_xfer& r, size_t* off, size_t* cnt) const {
+        const LmParams& P = eng[0]->P;
+        const int k = P.tile_k;
+        const size_t plane = (size_t)eng[0]->B.tkx * eng[0]->B.tky * 6;
+        const int b0 = r.z0 / k, b1 = (r.z1 + k - 1) / k;
+        *off = (size_t)b0 * plane;
+        *cnt = (size_t)(b1 - b0) * plane;
+    }
+
     void exchange(int b, cudaStream_t s) {
+        if (b == BUF_TM) {
+            if (!distributed()) {
+                for (size_t li = 0; li < eng.size(); ++li)
+                    for (const wlm_halo_xfer& r : plan[li]) {
+                        if (r.buffer != BUF_TM || r.send) continue;
+                        size_t off, cnt;
+                        tm_range(r, &off, &cnt);
+                        CK(cudaMemcpyAsync(eng[li]->B.TM + off, local(r.peer)->B.TM + off, sizeof(double) * cnt,
+                                           cudaMemcpyDeviceToDevice, s));
+                    }
+                return;
+            }
+            nccl_check(nccl::g_api.group_start(), "ncclGroupStart");
+            for (const wlm_halo_xfer& r : plan[0]) {
+                if (r.buffer != BUF_TM) continue;
+                size_t off, cnt;
+                tm_range(r, &off, &cnt);
+                double* p = eng[0]->B.TM + off;
+                if (r.send) nccl_check(nccl::g_api.send(p, cnt, nccl::Float64, r.peer, comm, s), "ncclSend");
+                else nccl_check(nccl::g_api.recv(p, cnt, nccl::Float64, r.peer, comm, s), "ncclRecv");
+            }
+            nccl_check(nccl::g_api.group_end(), "ncclGroupEnd");
+            return;
+        }
         if (!distributed()) {
             for (size_t li = 0; li < eng.size(); ++li) {
                 wlm_engine* d = eng[li];
@@ -339,7 +396,13 @@ struct wlm_slab_group {
     void body(cudaStream_t s) {
         for (auto* e : eng) e->stage_grad(s);
         exchange(BUF_G, s);
-        for (auto* e : eng) e->stage_step(s);
+        if (eng[0]->P.optimizer == WLM_OPT_LM && eng[0]->P.tile_k > 1) {
+            for (auto* e : eng) launch_tile_matrix(e->B, e->P, s);  // owned tiles
+            exchange(BUF_TM, s);                                   // halo tiles
+            for (auto* e : eng) launch_step_smooth(e->B, e->P, s);
+        } else {
+            for (auto* e : eng) e->stage_step(s);
+        }
         reduce_max(0, s);
         exchange(BUF_V, s);
         for (auto* e : eng) launch_compose_smooth(e->B, e->P, s);
@@ -446,10 +509,11 @@ wlm_status make_group(wlm_ctx* ctx, wlm_dims d, int nslabs, int first, int count
             const wlm_status es = engine_init(e, ctx, d, 1, cfg);
             if (es != WLM_OK) throw Fail{es};
             int zs, ze;
-            partition(d.nz, nslabs, k, &zs, &ze);
+            const int tk = std::max(1, cfg->lm.tile_size);
+            partition(d.nz, nslabs, k, &zs, &ze, tk);
             e->g = make_slab_geo(d, zs, ze, kHalo);
             grp->attach(e);
-            grp->plan.push_back(slab_plan(d, nslabs, k, e->P.Ru, e->P.Rw));
+            grp->plan.push_back(slab_plan(d, nslabs, k, e->P.Ru, e->P.Rw, tk));
             hst.push_back(e->st.p);
         }
         grp->sts = DevBuf<PairState*>(ctx, hst.size());
@@ -474,13 +538,18 @@ wlm_status make_group(wlm_ctx* ctx, wlm_dims d, int nslabs, int first, int count
 
 wlm_status check_split(wlm_ctx* ctx, wlm_dims d, int nslabs, const wlm_reg_config* cfg) {
     if (!ctx || nslabs < 1 || !valid_dims(d)) return WLM_INVALID_ARG;
-    if (cfg->lm.tile_size != 1) {
-        set_err(ctx, "slab_group: tiled LM (tile_size > 1) pools g over tiles that cross slabs; not built");
-        return WLM_UNSUPPORTED;
-    }
-    if (d.nz / nslabs < kHalo) {
-        set_err(ctx, "slab_group: every slab needs at least 4 planes (halo depth)");
-        return WLM_INVALID_ARG;
+    // every slab (tile-aligned when tiled) holds at least the halo depth and,
+    // with tiles, the R_u + k planes its halo tiles can reach into
+    const int tk = std::max(1, cfg->lm.tile_size);
+    const int need = tk > 1 ? std::max(kHalo, smooth_radius(cfg->sigma_update) + tk) : kHalo;
+    for (int k = 0; k < nslabs; ++k) {
+        int zs, ze;
+        partition(d.nz, nslabs, k, &zs, &ze, tk);
+        if (ze - zs < need) {
+            set_err(ctx, "slab_group: every slab needs at least " + std::to_string(need) +
+                             " planes (halo depth" + (tk > 1 ? " + tile" : "") + ")");
+            return WLM_INVALID_ARG;
+        }
     }
     return WLM_OK;
 }
@@ -499,7 +568,8 @@ wlm_status wlm_slab_halo_plan(wlm_dims d, int nslabs, int slab, const wlm_reg_co
                               size_t cap, size_t* len) {
     if (!cfg || !len || nslabs < 1 || slab < 0 || slab >= nslabs || !valid_dims(d)) return WLM_INVALID_ARG;
     if (d.nz / nslabs < kHalo) return WLM_INVALID_ARG;
-    const auto p = slab_plan(d, nslabs, slab, smooth_radius(cfg->sigma_update), smooth_radius(cfg->sigma_warp));
+    const auto p = slab_plan(d, nslabs, slab, smooth_radius(cfg->sigma_update), smooth_radius(cfg->sigma_warp),
+                             std::max(1, cfg->lm.tile_size));
     *len = p.size();
     if (rows) std::memcpy(rows, p.data(), sizeof(wlm_halo_xfer) * std::min(cap, p.size()));
     return WLM_OK;

@@ -18,7 +18,7 @@ from ._lib import Dims, HaloXfer, RegConfig, load
 from .engine import SlabGroup
 from .warplm import Context, default_context, reg_config
 
-BUFFERS = ("g", "dU_s", "warp", "abe")
+BUFFERS = ("g", "dU_s", "warp", "abe", "tm")
 
 
 def partition(nz, nslabs):

@@ -485,8 +485,10 @@ def test_tiled_lm_engine_vs_oracle(P, ctx, k):
         rc, u_o, _, tr_o = oracle_level(F, M, O.default_config(**kw), 20, storage)
         assert rc == 0
         compare_runs(tr, tr_o, aos(warp[0]), u_o, lt, wt)
-    with pytest.raises(P.WlmError):  # slab groups pool only pointwise steps
-        P.SlabGroup((24, 28, 32), 2, cfg=P.reg_config(**kw), ctx=ctx)
+    # z-slabs: tile-aligned boundaries + step matrices of the halo tiles
+    for ns in (2, 3):
+        w, t, _ = run_slabs(P, ctx, F, M, P.reg_config(**kw), 20, ns)
+        assert same_trace(t, tr) and np.array_equal(w, warp[0]), (k, ns)
 
 
 # -------------------------------------------------------------------- MI ----

@@ -110,3 +110,20 @@ def test_gloo_bootstrap_and_plan_exchange(world):
         p.join(120)
     assert all(p.exitcode == 0 for p in procs), [p.exitcode for p in procs]
     assert q.get(timeout=5) == "ok"
+
+
+def test_tiled_plans_have_twin_sends():
+    """Tiled LM: slab boundaries on tile boundaries, the step matrices of the
+    halo tiles travel as whole tile-planes; every receive has its twin send."""
+    for k, ns in ((2, 3), (3, 2), (4, 3)):
+        cfg = P.reg_config(nlevels=1, factors=[1], iters=[1], **{"lm.tile_size": k})
+        shape = (40, 12, 10)
+        plans = [slabs.halo_plan(shape, ns, s, cfg) for s in range(ns)]
+        for s, rows in enumerate(plans):
+            tm = [r for r in rows if r["buffer"] == "tm"]
+            assert tm or ns == 1
+            for r in tm:
+                assert r["z0"] % k == 0 and (r["z1"] % k == 0 or r["z1"] == shape[0])
+                twin = [q for q in plans[r["peer"]] if q["peer"] == s and q["buffer"] == "tm"
+                        and q["send"] != r["send"] and (q["z0"], q["z1"]) == (r["z0"], r["z1"])]
+                assert len(twin) == 1, (k, ns, s, r)
