@@ -158,6 +158,7 @@ void engine_alloc(wlm_engine* e) {
     b.HIST = e->HIST.p;
     b.MIT = e->MIT.p;
     b.max_blocks = tiles;
+    make_tma_u(b, e->P.Rw);
     CK(cudaMemsetAsync(e->U.p, 0, sizeof(float) * B * 6 * n, ctx->stream));
     launch_begin_level(b, e->P, 0, 1, e->cfg.lm.lambda0, ctx->stream);
 }

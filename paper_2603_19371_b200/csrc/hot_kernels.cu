@@ -24,6 +24,7 @@
 // indexed with Geo::lat), F and M are whole-volume (Geo::at), faces are the
 // global ones.
 #include <atomic>
+#include <cstring>
 #include <cfloat>
 #include <climits>
 
@@ -801,8 +802,6 @@ __global__ void __launch_bounds__(k2::NT, 2) k_lncc_bwd(Batch b, LmParams p, int
     const int x0 = (blockIdx.x % tiles_x) * TX, y0 = (blockIdx.x / tiles_x) * k2::TY;
     const int zb = g.zs + blockIdx.y * chunk_len, ze = min(zb + chunk_len, g.ze);
     const float* __restrict__ F = b.F + (long long)pair * g.nfull;
-    const float* __restrict__ M = b.M + (long long)pair * g.nfull;
-    const float* __restrict__ U = b.U + ((long long)pair * 2 + st->cur) * 3 * n;
     const float* __restrict__ A = b.ABE + (long long)pair * 4 * n;
     const float* __restrict__ Bc = A + n;
     const double* __restrict__ E = reinterpret_cast<const double*>(A + 2 * n);
@@ -1226,28 +1225,76 @@ struct Shape {
     // composed tile: IW = TX + 2R items a row, stored with the warp tile's row
     // stride so a warp's corner reads are consecutive (bank-conflict free)
     static constexpr int IW = TX + 2 * R, IH = TY + 2 * R;
-    static constexpr int UW = TX + 2 * R + 2, UH = TY + 2 * R + 2, UN = UW * UH;  // warp tile
+    // warp tile: x origin x0 - XO (a 16-byte aligned TMA box start), rows
+    // padded to 16 bytes (the box's inner extent), covering x0 - R - 1 ..
+    // x0 + TX + R
+    static constexpr int XO = 4;
+    static constexpr int UW = (TX + R + 1 + XO + 3) / 4 * 4, UH = TY + 2 * R + 2, UN = UW * UH;
     static constexpr int IWP = UW, NI = IWP * IH;
     static constexpr int SL = (NI + NT - 1) / NT, USL = (UN + NT - 1) / NT;
     static constexpr int NV = (2 + 2 * R + 1) / 2;
+    // ring slot: [3][UH][UW] fp32 (one TMA box), 128-byte aligned
+    static constexpr int SLOT = (3 * UN + 31) / 32 * 32;
+    static constexpr uint32_t BOX_BYTES = 3u * UN * 4u;
     // dynamic shared memory layout (doubles)
-    static constexpr int OFF_U = 0, OFF_IN = (4 * 3 * UN + 1) / 2, OFF_X = OFF_IN + 2 * 3 * NI;  // s_u fp32
+    static constexpr int OFF_U = 0, OFF_IN = 4 * SLOT / 2, OFF_X = OFF_IN + 2 * 3 * NI;  // s_u fp32
     static constexpr int TOTAL = OFF_X + 2 * 3 * IH * TX;
-    static constexpr size_t BYTES = sizeof(double) * TOTAL + sizeof(double) * 8;
+    static constexpr int OFF_BAR = TOTAL + 8;  // 4 mbarriers (after s_binv)
+    static constexpr size_t BYTES = sizeof(double) * (OFF_BAR + 4) + 128;  // + base alignment slack
 };
 }  // namespace k4
 
-template <int R>
-__global__ void __launch_bounds__(k4::NT, 1) k_compose_smooth(Batch b, LmParams p, int chunk_len) {
+// ---- TMA (cp.async.bulk.tensor) + mbarrier helpers ----
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+// Bounded wait: a lost transfer traps (kernel error) instead of hanging.
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    uint32_t done = 0;
+    for (long long spins = 0; !done; ++spins) {
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+            : "=r"(done)
+            : "r"(smem_u32(bar)), "r"(parity)
+            : "memory");
+        if (spins > (1ll << 28)) __trap();
+    }
+}
+__device__ __forceinline__ void tma_load_5d(void* dst, const CUtensorMap* map, int c0, int c1, int c2, int c3,
+                                            int c4, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, "
+        "%5, %6}], [%7];" ::"r"(smem_u32(dst)),
+        "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4), "r"(smem_u32(bar))
+        : "memory");
+}
+
+// TMA: the accepted warp's plane z (all three components, the (UW x UH)
+// box at the tile origin, zero-filled outside the volume like the register
+// path) arrives in its ring slot by one bulk tensor copy issued by thread 0;
+// consumers wait on the slot's mbarrier.  Used when the U rows are 16-byte
+// multiples (nx % 4 == 0), else the register-staged path.
+template <int R, bool TMA>
+__global__ void __launch_bounds__(k4::NT, 1) k_compose_smooth(Batch b, LmParams p, int chunk_len,
+                                                              const __grid_constant__ CUtensorMap tmap_u) {
     using S = k4::Shape<R>;
     constexpr int TX = k4::TX, NT = k4::NT, W = 2 * R + 1;
     constexpr int IWP = S::IWP, IH = S::IH, NI = S::NI, UW = S::UW, UN = S::UN, SL = S::SL, USL = S::USL,
                   NV = S::NV;
-    extern __shared__ __align__(16) double k4_smem[];
+    extern __shared__ __align__(16) double k4_smem_raw[];
+    // TMA writes need 128-byte aligned destinations: align the whole layout
+    double* k4_smem = reinterpret_cast<double*>(
+        reinterpret_cast<char*>(k4_smem_raw) + ((128 - (smem_u32(k4_smem_raw) & 127)) & 127));
     float* s_u = reinterpret_cast<float*>(k4_smem + S::OFF_U);  // [4 slots][3][UN] fp32
     double* s_in = k4_smem + S::OFF_IN;  // [2][3][NI]
     double* s_x = k4_smem + S::OFF_X;    // [2][3][IH * TX]
     double* s_binv = k4_smem + S::TOTAL; // [2R]
+    uint64_t* s_bar = reinterpret_cast<uint64_t*>(k4_smem + S::OFF_BAR);  // [4] TMA ring slots
 
     const int pair = blockIdx.z;
     const PairState* st = b.st + pair;
@@ -1265,12 +1312,12 @@ __global__ void __launch_bounds__(k4::NT, 1) k_compose_smooth(Batch b, LmParams 
     const double eps = p.target / fmax((double)__uint_as_float(st->max_bits), p.step_floor);
     fill_border_inv(s_binv, g.nz, R, p.wwd, p.wwd_full);
 
-    // warp staging items (tile origin x0 - R - 1, y0 - R - 1)
+    // warp staging items (tile origin x0 - XO, y0 - R - 1)
     int uoff[USL];
 #pragma unroll
     for (int s = 0; s < USL; ++s) {
         const int idx = threadIdx.x + s * NT;
-        const int gx = x0 - R - 1 + idx % UW, gy = y0 - R - 1 + idx / UW;
+        const int gx = x0 - S::XO + idx % UW, gy = y0 - R - 1 + idx / UW;
         uoff[s] = (idx < UN && gx >= 0 && gx < g.nx && gy >= 0 && gy < g.ny) ? gx + g.nx * gy : -1;
     }
     // composed items (tile origin x0 - R, y0 - R)
@@ -1299,7 +1346,7 @@ __global__ void __launch_bounds__(k4::NT, 1) k_compose_smooth(Batch b, LmParams 
         }
     };
     auto store_u = [&](int z) {
-        float* dst = s_u + ((z + 4) & 3) * 3 * UN;
+        float* dst = s_u + ((z + 4) & 3) * S::SLOT;
 #pragma unroll
         for (int s = 0; s < USL; ++s) {
             const int idx = threadIdx.x + s * NT;
@@ -1349,9 +1396,9 @@ __global__ void __launch_bounds__(k4::NT, 1) k_compose_smooth(Batch b, LmParams 
                     clamp_axis(ix, tx, g.nx);
                     clamp_axis(iy, ty, g.ny);
                     clamp_axis(iz, tz, g.nz);
-                    const int a = (iy - (y0 - R - 1)) * UW + ix - (x0 - R - 1);
-                    const float* p0 = s_u + ((iz + 4) & 3) * 3 * UN + a;
-                    const float* p1 = s_u + ((iz + 5) & 3) * 3 * UN + a;
+                    const int a = (iy - (y0 - R - 1)) * UW + ix - (x0 - S::XO);
+                    const float* p0 = s_u + ((iz + 4) & 3) * S::SLOT + a;
+                    const float* p1 = s_u + ((iz + 5) & 3) * S::SLOT + a;
 #pragma unroll
                     for (int ch = 0; ch < 3; ++ch) {
                         const double c000 = p0[ch * UN], c100 = p0[ch * UN + 1];
@@ -1374,6 +1421,19 @@ __global__ void __launch_bounds__(k4::NT, 1) k_compose_smooth(Batch b, LmParams 
             dst[NI + idx] = o3[1];
             dst[2 * NI + idx] = o3[2];
         }
+    };
+    // TMA ring: plane q lands in slot (q + 4) & 3; its n-th use of the slot
+    // (n = (q - first) / 4 with first = z0 - 1) completes mbarrier phase n & 1
+    const int zfirst = zb - R - 1;
+    auto tma_issue = [&](int z) {
+        if (!TMA || threadIdx.x != 0) return;
+        const int slot = (z + 4) & 3;
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // prior generic reads of the slot
+        mbar_expect_tx(&s_bar[slot], S::BOX_BYTES);
+        tma_load_5d(s_u + slot * S::SLOT, &tmap_u, x0 - S::XO, y0 - R - 1, z - g.zlo, cur * 3, pair, &s_bar[slot]);
+    };
+    auto tma_wait = [&](int z) {
+        if (TMA) mbar_wait(&s_bar[(z + 4) & 3], (uint32_t)(((z - zfirst) >> 2) & 1));
     };
     double w[W];
 #pragma unroll
@@ -1416,10 +1476,22 @@ __global__ void __launch_bounds__(k4::NT, 1) k_compose_smooth(Batch b, LmParams 
 
     const int z0 = zb - R, z1 = ze + R;
     // prologue: warp planes z0-1 .. z0+2 staged; composed z0, z0+1; x-pass z0
-    load_u(z0 - 1); store_u(z0 - 1);
-    load_u(z0);     store_u(z0);
-    load_u(z0 + 1); store_u(z0 + 1);
-    load_u(z0 + 2); store_u(z0 + 2);
+    if (TMA) {
+        if (threadIdx.x == 0) {
+            for (int i = 0; i < 4; ++i) mbar_init(&s_bar[i], 1);
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        }
+        __syncthreads();
+        tma_issue(z0 - 1);
+        tma_issue(z0);
+        tma_issue(z0 + 1);
+        tma_issue(z0 + 2);
+    } else {
+        load_u(z0 - 1); store_u(z0 - 1);
+        load_u(z0);     store_u(z0);
+        load_u(z0 + 1); store_u(z0 + 1);
+        load_u(z0 + 2); store_u(z0 + 2);
+    }
     load_v(z0);
     // double buffers as swapped pointers: halo tiles (composed) and x-passed
     double* in_a = s_in;           // composed plane p + 2 is written here
@@ -1427,14 +1499,21 @@ __global__ void __launch_bounds__(k4::NT, 1) k_compose_smooth(Batch b, LmParams 
     double* x_a = s_x;             // x-passed plane p is read here
     double* x_b = s_x + 3 * IH * TX;
     __syncthreads();
+    tma_wait(z0 - 1);
+    tma_wait(z0);
+    tma_wait(z0 + 1);
     compose(z0, in_a);
     load_v(z0 + 1);
-    load_u(z0 + 3);
+    if (!TMA) load_u(z0 + 3);
     __syncthreads();
+    tma_issue(z0 + 3);  // slot of plane z0 - 1 (last read by compose(z0))
     x_pass(in_a, x_a);
+    tma_wait(z0 + 2);
     compose(z0 + 1, in_b);
-    store_u(z0 + 3);  // slot of plane z0 - 1 (not read by compose(z0 + 1))
-    load_u(z0 + 4);
+    if (!TMA) {
+        store_u(z0 + 3);  // slot of plane z0 - 1 (not read by compose(z0 + 1))
+        load_u(z0 + 4);
+    }
     load_v(z0 + 2);
     __syncthreads();
     for (int zbase = z0; zbase < z1; zbase += W) {
@@ -1462,10 +1541,15 @@ __global__ void __launch_bounds__(k4::NT, 1) k_compose_smooth(Batch b, LmParams 
                         UN_[c * n + o] = (float)(s * inv);
                     }
                 }
+                // plane zi was last read by compose(zi + 1) before the barrier
+                if (TMA && zi + 4 <= z1 + 2) tma_issue(zi + 4);
                 x_pass(in_b, x_b);
+                tma_wait(zi + 3);
                 compose(zi + 2, in_a);
-                store_u(zi + 4);
-                load_u(zi + 5);
+                if (!TMA) {
+                    store_u(zi + 4);
+                    load_u(zi + 5);
+                }
                 load_v(zi + 3);
                 double* t = in_a; in_a = in_b; in_b = t;
                 t = x_a; x_a = x_b; x_b = t;
@@ -1563,6 +1647,36 @@ void launch_step_smooth(const Batch& b, const LmParams& p, cudaStream_t s) {
     ++g_kernel_launches;
 }
 
+void make_tma_u(Batch& b, int Rw) {
+    b.tma_u_ok = 0;
+    std::memset(&b.tma_u, 0, sizeof(b.tma_u));
+    const Geo& g = b.g;
+    if (g.nx % 4 != 0 || Rw > 3) return;
+    typedef CUresult (*Encode)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                               const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                               CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+    static Encode encode = nullptr;
+    if (!encode) {
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess || !fn)
+            return;
+        encode = reinterpret_cast<Encode>(fn);
+    }
+    int uw = 0, uh = 0;
+    WLM_DISPATCH_R(Rw, (uw = k4::Shape<RR>::UW, uh = k4::Shape<RR>::UH));
+    const cuuint64_t dims[5] = {(cuuint64_t)g.nx, (cuuint64_t)g.ny, (cuuint64_t)g.nzl, 6, (cuuint64_t)b.pairs};
+    const cuuint64_t strides[4] = {(cuuint64_t)g.nx * 4, (cuuint64_t)g.nx * g.ny * 4, (cuuint64_t)g.n * 4,
+                                   (cuuint64_t)g.n * 6 * 4};
+    const cuuint32_t box[5] = {(cuuint32_t)uw, (cuuint32_t)uh, 1, 3, 1};
+    const cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+    const CUresult r = encode(&b.tma_u, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 5, b.U, dims, strides, box, estr,
+                              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                              CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    b.tma_u_ok = r == CUDA_SUCCESS ? 1 : 0;
+}
+
 void launch_compose_smooth(const Batch& b, const LmParams& p, cudaStream_t s) {
     const LaunchShape sh = shape_for(b.g, b.pairs, k4::TY);
     dim3 grid = sh.grid();
@@ -1571,11 +1685,16 @@ void launch_compose_smooth(const Batch& b, const LmParams& p, cudaStream_t s) {
         static std::atomic<unsigned long long> attr{0ull};  // per device
         const unsigned long long bit = device_bit();
         if (!(attr.load() & bit)) {
-            cudaFuncSetAttribute(k_compose_smooth<RR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+            cudaFuncSetAttribute(k_compose_smooth<RR, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)k4::Shape<RR>::BYTES);
+            cudaFuncSetAttribute(k_compose_smooth<RR, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)k4::Shape<RR>::BYTES);
             attr.fetch_or(bit);
         }
-        k_compose_smooth<RR><<<grid, k4::NT, k4::Shape<RR>::BYTES, s>>>(b, p, sh.chunk_len);
+        if (b.tma_u_ok)
+            k_compose_smooth<RR, true><<<grid, k4::NT, k4::Shape<RR>::BYTES, s>>>(b, p, sh.chunk_len, b.tma_u);
+        else
+            k_compose_smooth<RR, false><<<grid, k4::NT, k4::Shape<RR>::BYTES, s>>>(b, p, sh.chunk_len, b.tma_u);
     }));
     ++g_kernel_launches;
 }

@@ -1,6 +1,7 @@
 // kernels.cuh -- device state and launch wrappers of the LM hot path.
 #pragma once
 
+#include <cuda.h>  // CUtensorMap (types only; the encoder is fetched at run time)
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -80,6 +81,8 @@ struct Batch {
     unsigned long long* HIST;  // [pair][B*B] MI joint histogram, fixed point 2^-32 (exact sums)
     double* MIT;      // [pair][B*B] MI gradient table dMI/dp_ij - dMI/dp_m(j)
     int tkx, tky, tkz;  // tile counts (tile_k > 1)
+    int tma_u_ok;       // K4 stages the accepted warp by TMA (tma_u valid)
+    CUtensorMap tma_u;  // 5D map over U: (x, y, local z, buffer*3 + component, pair)
     int max_blocks;
 };
 
@@ -98,6 +101,9 @@ void launch_mi_fwd(const Batch& b, const LmParams& p, int mode, cudaStream_t s);
 void launch_mi_finalize(const Batch& b, const LmParams& p, int mode, cudaStream_t s);
 void launch_mi_grad(const Batch& b, const LmParams& p, cudaStream_t s);
 void launch_mse_grad(const Batch& b, const LmParams& p, cudaStream_t s);
+// K4's TMA descriptor for the engine's U buffer (box = one warp-ring slot);
+// leaves tma_u_ok = 0 when the layout does not allow it (nx % 4 != 0).
+void make_tma_u(Batch& b, int R_warp);
 // K1: warp + LNCC window moments + coefficients + sum(rho); last block runs
 // the loss/damping/rejection state machine.  mode 0 evaluates the accepted
 // warp (level start), mode 1 the attempt in the other buffer.
