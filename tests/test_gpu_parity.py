@@ -538,3 +538,26 @@ def test_register_pyramid_other_losses_and_steps(P, ctx, extra):
         rc, w_s, tr_s, _ = O.register(F, M, O.default_config(**kw))
     assert rc == 0 and len(res.loss_trace) == len(tr_s) == 20
     compare_runs(res.loss_trace, tr_s, res.final_warp, w_s, 1e-6, 1e-5)
+
+
+def test_bench_json_contract():
+    """bench.py's one-line JSON keeps the driver's contract (small config)."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--steps", "3", "--warmup", "3",
+                          "--size", "64", "--pairs-per-gpu", "2", "--no-cpu-baseline", "--no-extra",
+                          "--e2e-iters", "2"], capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = json.loads(out.stdout.strip().splitlines()[-1])
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
+              "scaling", "vs_baseline", "dtype", "data", "config", "roofline", "e2e", "gpu_launches", "clocks"):
+        assert k in line, k
+    assert line["steps"] == 3 and line["warmup"] == 3 and line["value"] > 0
+    rf = line["roofline"]
+    assert rf["bound"] == "hbm" and 0 < rf["frac"] < 1 and rf["peak"] > 0 and rf["unit"] == "GB/s"
+    e2e = line["e2e"]
+    assert e2e["h2d_bytes_per_step"] > 0 and e2e["d2h_bytes_per_step"] > 0 and e2e["value"] > 0
+    assert line["gpu_launches"] == 6 * 3  # K2, K3, K4, K1a, K1b, K5 per step
