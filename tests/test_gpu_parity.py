@@ -273,6 +273,43 @@ def same_trace(a, b):
         all((x[k] == y[k]) or (x[k] != x[k] and y[k] != y[k]) for k in x) for x, y in zip(a, b))
 
 
+@pytest.mark.parametrize("shape", [(1, 9, 10), (7, 1, 6), (5, 6, 1), (2, 3, 4), (3, 17, 33), (5, 6, 7),
+                                   (6, 13, 21), (9, 10, 37)])
+def test_degenerate_and_ragged_dims_match_oracle(P, ctx, shape):
+    """n == 1 axes (resolve_axis collapse, field.cpp:21-24; smoothing skipped,
+    :220), two-voxel axes, and widths that are not multiples of 4 (K4's
+    register-staged path instead of TMA): the ops and a rejection-on LM run
+    against the fp32-storage oracle.  LNCC needs every dim > 2 radius
+    (SPEC.md:138); thinner volumes run MSE."""
+    rng = np.random.default_rng(sum(shape))
+    F = O.gaussian_smooth(rng.normal(size=shape), 1.0).astype(np.float32)
+    M = O.gaussian_smooth(rng.normal(size=shape), 1.0).astype(np.float32)
+    F64, M64 = F.astype(np.float64), M.astype(np.float64)
+    u = smooth_field(shape, 7, sigma=1.0, amp=1.5).astype(np.float32).astype(np.float64)
+    v = smooth_field(shape, 8, sigma=1.0, amp=1.0).astype(np.float32).astype(np.float64)
+    assert np.abs(P.compose_warp(u, v, 0.3, ctx=ctx) - O.compose_warp(u, v, 0.3)).max() < 2e-5
+    for sig in (1.0, 0.5):
+        assert np.abs(P.gaussian_smooth(u, sig, ctx=ctx) - O.gaussian_smooth(u, sig)).max() < 2e-6
+    lncc = min(shape) > 4
+    if lncc:
+        rep = P.residual_lncc(F64, M64, u, ctx=ctx)
+        r_o, g_o, _ = O.residual_lncc(F64, M64, u)
+    else:
+        with pytest.raises(P.InvalidArgument):
+            P.residual_lncc(F64, M64, u, ctx=ctx)
+        rep = P.residual_mse(F64, M64, u, ctx=ctx)
+        r_o, g_o = O.residual_mse(F64, M64, u)
+    assert abs(rep.r - r_o) <= 1e-5 * abs(r_o)
+    assert rel(rep.g, g_o) < 1e-4, rel(rep.g, g_o)
+    kw = dict(nlevels=1, factors=[1], iters=[12], metric=0 if lncc else 1)
+    cfg_p = P.reg_config(**kw, **{"lm.rejection": 1, "lm.tau": 0.5})
+    cfg_o = O.default_config(**kw, **{"lm.rejection": 1, "lm.tau": 0.5})
+    warp, (tr,), _ = run_engine(P, ctx, F, M, cfg_p, 12)
+    rc, u_o, _, tr_o = oracle_level(F, M, cfg_o, 12, "fp32")
+    assert rc == 0
+    compare_runs(tr, tr_o, aos(warp[0]), u_o, 1e-6, 1e-5)
+
+
 def test_batch_pairs_are_independent_and_deterministic(P, ctx):
     shape = (24, 28, 32)
     Fs, Ms = [], []
