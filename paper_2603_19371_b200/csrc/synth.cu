@@ -89,13 +89,27 @@ __global__ void k_scale(float* u, long long n3, const unsigned* maxbits, float t
         u[i] *= s;
 }
 
+// fp64 lerps of the fp32 image, rounded once: at a knot (t = 0 or 1) the
+// sample is exactly the voxel value, so warp_max = 0 gives moving == fixed
+// even on the last index, where the cell has t = 1.
+__device__ __forceinline__ float cell_sample_exact(const float* __restrict__ v, const Cell& c) {
+    if (!c.finite) return __int_as_float(0x7fc00000);
+    const double tx = c.tx, ty = c.ty, tz = c.tz;
+    const double a = v[c.o000], b = v[c.o100], cc = v[c.o010], e = v[c.o110];
+    const double f = v[c.o001], h = v[c.o101], k = v[c.o011], l = v[c.o111];
+    const double v00 = fma(tx, b - a, a), v10 = fma(tx, e - cc, cc);
+    const double v01 = fma(tx, h - f, f), v11 = fma(tx, l - k, k);
+    const double s0 = fma(ty, v10 - v00, v00), s1 = fma(ty, v11 - v01, v01);
+    return (float)fma(tz, s1 - s0, s0);
+}
+
 __global__ void k_moving(const float* F, const float* u, float* Fo, float* Mo, Geo g, float noise,
                          uint64_t seed) {
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < g.n;
          i += (long long)gridDim.x * blockDim.x) {
         const int x = (int)(i % g.nx), y = (int)((i / g.nx) % g.ny), z = (int)(i / ((long long)g.nx * g.ny));
         const Cell c = make_cell(g, x, y, z, u[i], u[g.n + i], u[2 * g.n + i]);
-        const float m = cell_sample(F, c);
+        const float m = cell_sample_exact(F, c);
         Fo[i] = F[i] + noise * normal(seed, 101, (uint64_t)i);
         Mo[i] = m + noise * normal(seed, 102, (uint64_t)i);
     }

@@ -45,7 +45,7 @@ __all__ = [
     "downsample", "upsample_warp", "state_bytes", "register", "reg_config", "lm_config",
     "DimensionMismatch", "InvalidArgument", "NonFiniteLoss", "WlmError", "OPT_LM", "OPT_ADAM",
     "OPT_GD", "OPT_DEMONS", "LmState", "LmConfig", "METRIC_LNCC", "METRIC_MSE", "METRIC_MI", "residual_mse", "residual_mi",
-    "demons_step_mse", "lm_step_tiled",
+    "demons_step_mse", "lm_step_tiled", "synth_pair", "trace_rows",
 ]
 
 _D = C.POINTER(C.c_double)
@@ -342,6 +342,23 @@ def upsample_warp(u, new_shape, scale, ctx=None):
     c.check(c.lib.wlm_upsample_warp(c.h, _p(u), _dims(u.shape), _dims(new_shape), float(scale),
                                     _p(out)))
     return out
+
+
+def synth_pair(shape, seed, num_blobs=12, warp_max=3.0, noise_sigma=0.01, warp_sigma=0.0, ctx=None):
+    """synth_pair on the GPU: (fixed, moving, u_true) with
+    shape (nz, ny, nx), u_true (nz, ny, nx, 3) AoS; moving is fixed sampled
+    through Id + u_true.  Raises InvalidArgument when no positive-Jacobian
+    warp is found in 10 draws."""
+    from ._lib import SynthSpec
+    nz, ny, nx = (int(s) for s in shape)
+    c = _ctx(ctx)
+    spec = SynthSpec(Dims(nx, ny, nz), int(num_blobs), float(warp_sigma), float(warp_max),
+                     float(noise_sigma), int(seed))
+    F = np.empty((nz, ny, nx), np.float32)
+    M = np.empty_like(F)
+    U = np.empty((3, nz, ny, nx), np.float32)
+    c.check(c.lib.wlm_synth_pair(c.h, C.byref(spec), F.ctypes.data, M.ctypes.data, U.ctypes.data, 0))
+    return F, M, np.ascontiguousarray(np.moveaxis(U, 0, -1))
 
 
 def state_bytes(optimizer, shape, elem_bytes=4) -> int:
