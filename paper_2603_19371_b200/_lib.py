@@ -10,7 +10,8 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libwarplm_b200.so")
+# WLM_LIB_PATH selects another build of the same library (A/B kernel variants)
+LIB_PATH = os.environ.get("WLM_LIB_PATH") or os.path.join(HERE, "libwarplm_b200.so")
 
 MAX_LEVELS = 8
 OPT_LM, OPT_ADAM, OPT_GD, OPT_DEMONS = 0, 1, 2, 3

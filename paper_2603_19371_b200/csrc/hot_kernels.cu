@@ -28,6 +28,8 @@
 #include <cfloat>
 #include <climits>
 
+#include <cuda_pipeline.h>
+
 #include "hot.cuh"
 #include "kernels.cuh"
 
@@ -766,8 +768,11 @@ __global__ void k_finalize(Batch b, LmParams p, int mode) {
 // Schedule (as K1b): one barrier per plane; phase p runs the y-pass of plane p
 // (z ring, output plane p - R), the x-pass of plane p+1 (two outputs per
 // thread from 16-byte shared loads), the halo tile of plane p+2 and the loads
-// of plane p+3.  Mw and grad M(x+u) come from K1a's evaluation of this warp
-// (no gathers here), loaded three planes ahead.
+// of plane p+3.  F, Mw and grad M(x+u) of the output voxels (K1a's
+// evaluation of this warp, no gathers here) are copied one plane ahead by
+// cp.async into shared memory, which keeps them out of the register file:
+// K2 0.99 -> 0.90 ms against register staging three planes ahead.  The
+// tunables below were measured with tools/ab_bench.sh.
 namespace k2 {
 constexpr int TX = 32, TY = 8, NT = 256;
 template <int R>
@@ -776,20 +781,38 @@ struct Shape {
     static constexpr int SL = (NI + NT - 1) / NT;
     static constexpr int NV = (2 + 2 * R + 1) / 2;
 };
-// one output voxel in flight: F, Mw and grad M (K1a)
-struct Own {
-    float f;
-    double mw, gm[3];
+// per-voxel inputs of the output planes (F, Mw, grad M from K1a), staged by
+// cp.async into a ring of OWN_SLOTS planes in dynamic shared memory; each
+// thread copies and later reads only its own voxel, so no barrier guards it
+#ifndef WLM_K2_OWN_SLOTS
+#define WLM_K2_OWN_SLOTS 2
+#endif
+#ifndef WLM_K2_HALO_DEPTH
+#define WLM_K2_HALO_DEPTH 1
+#endif
+constexpr int HALO_DEPTH = WLM_K2_HALO_DEPTH;  // halo planes in flight in registers
+constexpr int OWN_SLOTS = WLM_K2_OWN_SLOTS;  // power of two
+constexpr int OWN_AHEAD = OWN_SLOTS - 1;
+struct OwnSlot {
+    double mw[NT];
+    double gm[3][NT];
+    float f[NT];
 };
+constexpr size_t OWN_BYTES = sizeof(OwnSlot) * OWN_SLOTS;
 }  // namespace k2
 
 template <int R>
-__global__ void __launch_bounds__(k2::NT, 2) k_lncc_bwd(Batch b, LmParams p, int chunk_len) {
+#ifndef WLM_K2_MIN_BLOCKS
+#define WLM_K2_MIN_BLOCKS 2
+#endif
+__global__ void __launch_bounds__(k2::NT, WLM_K2_MIN_BLOCKS) k_lncc_bwd(Batch b, LmParams p, int chunk_len) {
     using S = k2::Shape<R>;
     constexpr int TX = k2::TX, NT = k2::NT, W = 2 * R + 1;
     constexpr int IWP = S::IWP, IH = S::IH, NI = S::NI, SL = S::SL, NV = S::NV;
     __shared__ __align__(16) double s_in[2][3][NI];
     __shared__ __align__(16) double s_x[2][3][IH * TX];
+    extern __shared__ __align__(16) unsigned char k2_smem[];
+    k2::OwnSlot* const s_own = reinterpret_cast<k2::OwnSlot*>(k2_smem);
     (void)p;
 
     const int pair = blockIdx.z;
@@ -816,20 +839,23 @@ __global__ void __launch_bounds__(k2::NT, 2) k_lncc_bwd(Batch b, LmParams p, int
         const int gx = x0 - R + idx % IWP, gy = y0 - R + idx / IWP;
         hoff[s] = (idx < NI && gx >= 0 && gx < g.nx && gy >= 0 && gy < g.ny) ? gx + g.nx * gy : -1;
     }
-    float ha[SL], hb[SL];
-    double he[SL];
-    auto load_halo = [&](int z) {
+    // halo registers, HALO_DEPTH planes in flight: h[0] is stored this
+    // phase, the rest were loaded in earlier phases and move down after it
+    constexpr int HD = k2::HALO_DEPTH;
+    float ha[HD][SL], hb[HD][SL];
+    double he[HD][SL];
+    auto load_halo = [&](int z, int j) {
         const bool zin = z >= 0 && z < g.nz && z < ze + R;
         const int base = (z - g.zlo) * nxy;
 #pragma unroll
         for (int s = 0; s < SL; ++s) {
             if (zin && hoff[s] >= 0) {
-                ha[s] = __ldg(A + base + hoff[s]);
-                hb[s] = __ldg(Bc + base + hoff[s]);
-                he[s] = __ldg(E + base + hoff[s]);
+                ha[j][s] = __ldg(A + base + hoff[s]);
+                hb[j][s] = __ldg(Bc + base + hoff[s]);
+                he[j][s] = __ldg(E + base + hoff[s]);
             } else {
-                ha[s] = hb[s] = 0.f;
-                he[s] = 0.0;
+                ha[j][s] = hb[j][s] = 0.f;
+                he[j][s] = 0.0;
             }
         }
     };
@@ -838,10 +864,20 @@ __global__ void __launch_bounds__(k2::NT, 2) k_lncc_bwd(Batch b, LmParams p, int
         for (int s = 0; s < SL; ++s) {
             const int idx = threadIdx.x + s * NT;
             if (idx >= NI) continue;
-            dst[idx] = (double)ha[s];
-            dst[NI + idx] = (double)hb[s];
-            dst[2 * NI + idx] = he[s];
+            dst[idx] = (double)ha[0][s];
+            dst[NI + idx] = (double)hb[0][s];
+            dst[2 * NI + idx] = he[0][s];
         }
+    };
+    auto shift_halo = [&] {
+#pragma unroll
+        for (int j = 0; j + 1 < HD; ++j)
+#pragma unroll
+            for (int s = 0; s < SL; ++s) {
+                ha[j][s] = ha[j + 1][s];
+                hb[j][s] = hb[j + 1][s];
+                he[j][s] = he[j + 1][s];
+            }
     };
     const int xr = threadIdx.x >> 4, xj = threadIdx.x & 15;
     auto x_pass = [&](const double* in, double* out) {
@@ -869,21 +905,22 @@ __global__ void __launch_bounds__(k2::NT, 2) k_lncc_bwd(Batch b, LmParams p, int
     const int x = x0 + ox, y = y0 + oy;
     const bool own = x < g.nx && y < g.ny;
     const int ooff = x + g.nx * y;
-    // output pipeline (dense loads, three planes ahead): F, Mw and grad M of
-    // the accepted warp from K1a
+    // output pipeline: F, Mw and grad M of the accepted warp (K1a), copied
+    // asynchronously OWN_AHEAD planes ahead, one commit group per plane
     const double* __restrict__ MWp = b.MW + (long long)pair * n;
     const double* __restrict__ GMp = b.GM + (long long)pair * 3 * n;
-    k2::Own o0, o1, o2, o3;
-    auto load_own = [&](int zo, k2::Own& w) {
+    const int t = threadIdx.x;
+    auto issue_own = [&](int zo) {
         if (own && zo >= zb && zo < ze) {
+            k2::OwnSlot& sl = s_own[zo & (k2::OWN_SLOTS - 1)];
             const int o = (zo - g.zlo) * nxy + ooff;
-            w.f = __ldg(F + zo * nxy + ooff);
-            w.mw = __ldg(MWp + o);
-            w.gm[0] = __ldg(GMp + o); w.gm[1] = __ldg(GMp + n + o); w.gm[2] = __ldg(GMp + 2 * n + o);
-        } else {
-            w.f = 0.f;
-            w.mw = w.gm[0] = w.gm[1] = w.gm[2] = 0.0;
+            __pipeline_memcpy_async(&sl.f[t], F + zo * nxy + ooff, sizeof(float));
+            __pipeline_memcpy_async(&sl.mw[t], MWp + o, sizeof(double));
+            __pipeline_memcpy_async(&sl.gm[0][t], GMp + o, sizeof(double));
+            __pipeline_memcpy_async(&sl.gm[1][t], GMp + n + o, sizeof(double));
+            __pipeline_memcpy_async(&sl.gm[2][t], GMp + 2 * n + o, sizeof(double));
         }
+        __pipeline_commit();
     };
 
     double ring[W][3];
@@ -897,16 +934,15 @@ __global__ void __launch_bounds__(k2::NT, 2) k_lncc_bwd(Batch b, LmParams p, int
     double* in_b = &s_in[1][0][0];
     double* x_a = &s_x[0][0][0];
     double* x_b = &s_x[1][0][0];
-    load_halo(z0);
+    for (int q = 0; q < k2::OWN_AHEAD; ++q) issue_own(zb + q);
+    load_halo(z0, 0);
     store_halo(in_a);
-    load_halo(z0 + 1);
+    load_halo(z0 + 1, 0);
     store_halo(in_b);
-    load_own(zb, o0);
-    load_own(zb + 1, o1);
-    load_own(zb + 2, o2);
     __syncthreads();
     x_pass(in_a, x_a);
-    load_halo(z0 + 2);
+#pragma unroll
+    for (int j = 0; j < HD; ++j) load_halo(z0 + 2 + j, j);
     __syncthreads();
     for (int zbase = z0; zbase < z1; zbase += W) {
 #pragma unroll
@@ -915,7 +951,7 @@ __global__ void __launch_bounds__(k2::NT, 2) k_lncc_bwd(Batch b, LmParams p, int
             if (zi < z1) {
                 const int zo = zi - R;
                 const bool emit = zo >= zb;
-                if (emit) load_own(zo + 3, o3);
+                if (emit) issue_own(zo + k2::OWN_AHEAD);
 #pragma unroll
                 for (int c = 0; c < 3; ++c) {
                     double s = 0.0;
@@ -923,7 +959,9 @@ __global__ void __launch_bounds__(k2::NT, 2) k_lncc_bwd(Batch b, LmParams p, int
                     for (int d = 0; d < W; ++d) s += x_a[c * IH * TX + (oy + d) * TX + ox];
                     ring[rs][c] = s;
                 }
+                if (emit) __pipeline_wait_prior(k2::OWN_AHEAD);  // plane zo has landed
                 if (emit && own) {
+                    const k2::OwnSlot& sl = s_own[zo & (k2::OWN_SLOTS - 1)];
                     double Sm[3];
 #pragma unroll
                     for (int c = 0; c < 3; ++c) {
@@ -932,23 +970,18 @@ __global__ void __launch_bounds__(k2::NT, 2) k_lncc_bwd(Batch b, LmParams p, int
                         for (int d = 0; d < W; ++d) s += ring[(rs + 1 + d) % W][c];
                         Sm[c] = s;
                     }
-                    const double mw = o0.mw;
-                    const double* gm = o0.gm;
-                    const double f = (double)o0.f - shf;
+                    const double mw = sl.mw[t];
+                    const double f = (double)sl.f[t] - shf;
                     const double dm = -invN * (fma(f, Sm[0], (mw - shm) * Sm[1]) - Sm[2]);
                     const int o = (zo - g.zlo) * nxy + ooff;
-                    G[o] = (float)(dm * gm[0]);
-                    G[n + o] = (float)(dm * gm[1]);
-                    G[2 * n + o] = (float)(dm * gm[2]);
-                }
-                if (emit) {
-                    o0 = o1;
-                    o1 = o2;
-                    o2 = o3;
+                    G[o] = (float)(dm * sl.gm[0][t]);
+                    G[n + o] = (float)(dm * sl.gm[1][t]);
+                    G[2 * n + o] = (float)(dm * sl.gm[2][t]);
                 }
                 x_pass(in_b, x_b);
                 store_halo(in_a);
-                load_halo(zi + 3);
+                shift_halo();
+                load_halo(zi + 2 + HD, HD - 1);
                 double* t = in_a; in_a = in_b; in_b = t;
                 t = x_a; x_a = x_b; x_b = t;
                 __syncthreads();
@@ -1631,7 +1664,13 @@ void launch_lncc_bwd(const Batch& b, const LmParams& p, cudaStream_t s) {
     const LaunchShape sh = shape_for(b.g, b.pairs, k2::TY);
     dim3 grid = sh.grid();
     grid.z = b.pairs;
-    k_lncc_bwd<2><<<grid, k2::NT, 0, s>>>(b, p, sh.chunk_len);
+    static std::atomic<unsigned long long> attr{0ull};  // per device
+    const unsigned long long bit = device_bit();
+    if (!(attr.load() & bit)) {
+        cudaFuncSetAttribute(k_lncc_bwd<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k2::OWN_BYTES);
+        attr.fetch_or(bit);
+    }
+    k_lncc_bwd<2><<<grid, k2::NT, k2::OWN_BYTES, s>>>(b, p, sh.chunk_len);
     ++g_kernel_launches;
 }
 
