@@ -224,8 +224,9 @@ def _fmt(v):
     return v
 
 
-def _suite_pair(dims, seed, warp_max, ctx, cache={}):
-    key = (tuple(dims), seed, warp_max, id(ctx))
+def _suite_pair(dims, seed, warp_max, ctx, cache):
+    """Synthetic pair + inverse ground truth, generated once per sweep."""
+    key = (tuple(dims), seed, warp_max)
     if key not in cache:
         nx, ny, nz = dims
         F, M, U = synth_pair((nz, ny, nx), seed, 12, warp_max, 0.01, 0.0, ctx=ctx)
@@ -249,12 +250,12 @@ def cmd_sweep(param, values, repeats=1, cfg_kw=None, dims=(32, 32, 32), seed=0, 
     if not values:
         raise ConfigError("sweep: empty value list")
     ctx = ctx or default_context()
-    rows = []
+    rows, pairs = [], {}
     for v in values:
         for rep in range(repeats):
             row = dict(param=param, value=v, repeat=rep)
             try:
-                F, M, ugt = _suite_pair(dims, seed + rep, warp_max, ctx)
+                F, M, ugt = _suite_pair(dims, seed + rep, warp_max, ctx, pairs)
                 kw = dict(cfg_kw or {})
                 kw[_SWEEP_PARAMS[param]] = int(v) if param == "tile_size" else float(v)
                 res = register(F, M, _reg_config(kw), ctx=ctx)

@@ -1,6 +1,6 @@
 """Per-CUDA-source-line instruction and stall totals of one kernel in an ncu
 report (needs -lineinfo and --import-source on).  Usage:
-  python tools/ncu_lines.py REPORT.ncu-rep [top_n]"""
+  python tools/ncu_lines.py REPORT.ncu-rep [top_n] [--smem] [--kernel REGEX]"""
 import csv
 import io
 import subprocess
@@ -8,7 +8,10 @@ import sys
 
 rep = sys.argv[1]
 top = int(sys.argv[2]) if len(sys.argv) > 2 and sys.argv[2].isdigit() else 30
-out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
+kfilter = []
+if "--kernel" in sys.argv:
+    kfilter = ["-k", "regex:" + sys.argv[sys.argv.index("--kernel") + 1]]
+out = subprocess.run(["ncu", "-i", rep, *kfilter, "--page", "source", "--csv", "--print-source", "cuda,sass"],
                      capture_output=True, text=True).stdout
 agg = {}
 fname = None
@@ -35,7 +38,11 @@ for row in csv.reader(io.StringIO(out)):
     # rows carry the CUDA line in col 0/1 and a SASS instruction in col 3
     key = (fname, line, row[1].strip()[:90])
     a = agg.setdefault(key, [0.0, 0.0, 0.0, 0.0])
-    num = lambda v: float(v) if v not in ("", "-") else 0.0  # noqa: E731
+    def num(v):
+        try:
+            return float(v)
+        except ValueError:
+            return 0.0
     a[0] += num(row[ie])
     a[1] += num(row[st])
     if wf is not None:
