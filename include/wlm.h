@@ -219,9 +219,16 @@ wlm_status wlm_engine_begin_level(wlm_engine* e, int level);
 /* Launch `iters` lm_iterate steps for every active pair (asynchronous; with
  * rejection enabled the retries run inside a device-side WHILE graph). */
 wlm_status wlm_engine_iterate(wlm_engine* e, int iters);
-/* Launch exactly one attempt (K2..K4 + evaluation) per pair; the unit the
- * benchmark times (rejection must be disabled). */
+/* Launch exactly one attempt (K2..K4 + evaluation) per pair (rejection must
+ * be disabled). */
 wlm_status wlm_engine_step(wlm_engine* e);
+/* Pair groups (1 or 2, default 2): with rejection off and pairs > 1, iterate
+ * runs the batch as two independent streams of attempt graphs (pairs
+ * [0, ceil(P/2)) and the rest) that join only when the call's iterations
+ * are done, so the groups' kernels overlap.  Results are identical either
+ * way (each pair's arithmetic does not depend on the grouping).  The
+ * environment variable WLM_PAIR_GROUPS=1 sets the default to 1. */
+wlm_status wlm_engine_set_pair_groups(wlm_engine* e, int groups);
 /* Copy out per-pair state / trace rows written since begin_level (syncs). */
 wlm_status wlm_engine_state(wlm_engine* e, int pair, wlm_lm_state* st, double* r,
                             double* lncc, int* iters_done);

@@ -9,6 +9,7 @@
 #include <climits>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -25,6 +26,12 @@ wlm_status engine_init(wlm_engine* e, wlm_ctx* ctx, wlm_dims d, int pairs, const
     e->g = make_geo(d);
     e->pairs = pairs;
     e->cfg = *c;
+    // pair groups of the attempt graph; WLM_PAIR_GROUPS=1
+    // captures the whole batch as one chain
+    {
+        const char* v = std::getenv("WLM_PAIR_GROUPS");
+        e->pair_groups = (v && std::atoi(v) == 1) ? 1 : 2;
+    }
     if (c->lm.tile_size < 1) {
         set_err(ctx, "lm.tile_size must be >= 1 (SPEC.md:259)");
         return WLM_INVALID_ARG;
@@ -339,7 +346,10 @@ wlm_status wlm_engine_iterate(wlm_engine* e, int iters) {
     return run(ctx, [&] {
         launch_set_targets(e->B, iters, ctx->stream);
         if (iters == 0) return;
-        if (!e->P.rejection) {
+        if (!e->P.rejection && e->grouped()) {
+            e->launch_grouped(iters, ctx->stream);
+            g_kernel_launches += (uint64_t)iters * e->group_kernels;
+        } else if (!e->P.rejection) {
             e->build_step_graph();
             for (int i = 0; i < iters; ++i) CK(cudaGraphLaunch(e->step_exec, ctx->stream));
             g_kernel_launches += (uint64_t)iters * e->body_kernels;
@@ -356,10 +366,27 @@ wlm_status wlm_engine_step(wlm_engine* e) {
     if (e->P.rejection) return WLM_UNSUPPORTED;
     wlm_ctx* ctx = e->ctx;
     return run(ctx, [&] {
-        e->build_step_graph();
-        CK(cudaGraphLaunch(e->step_exec, ctx->stream));
-        g_kernel_launches += e->body_kernels;
+        if (e->grouped()) {
+            e->launch_grouped(1, ctx->stream);
+            g_kernel_launches += e->group_kernels;
+        } else {
+            e->build_step_graph();
+            CK(cudaGraphLaunch(e->step_exec, ctx->stream));
+            g_kernel_launches += e->body_kernels;
+        }
     });
+}
+
+wlm_status wlm_engine_set_pair_groups(wlm_engine* e, int groups) {
+    if (!e || groups < 1 || groups > 2) return WLM_INVALID_ARG;
+    if (e->pair_groups != groups) {
+        wlm_ctx* ctx = e->ctx;
+        wlm_status s = run(ctx, [&] { CK(cudaStreamSynchronize(ctx->stream)); });
+        if (s != WLM_OK) return s;
+        e->invalidate_graphs();
+        e->pair_groups = groups;
+    }
+    return WLM_OK;
 }
 
 wlm_status wlm_engine_stage(wlm_engine* e, int stage) {

@@ -262,7 +262,7 @@ constexpr double kNaN64 = __builtin_nan("");
 constexpr int kZP = 4;
 template <bool GRAD>
 __global__ void __launch_bounds__(256) k_warp_moving(Batch b, int mode, int z_first, int z_last) {
-    const int pair = blockIdx.z;
+    const int pair = b.pair0 + blockIdx.z;
     const PairState* st = b.st + pair;
     if (st->done) return;
     const Geo g = b.g;
@@ -333,7 +333,7 @@ __device__ void reduce_plane_partials(const Batch& b, PairState* st, const doubl
 // reduction; K5 turns it into r = loss_raw = MSE.
 __global__ void __launch_bounds__(256) k_mse_fwd(Batch b, int chunk_len) {
     __shared__ int s_last;
-    const int pair = blockIdx.z;
+    const int pair = b.pair0 + blockIdx.z;
     PairState* st = b.st + pair;
     if (st->done) return;
     const Geo g = b.g;
@@ -366,7 +366,7 @@ __global__ void __launch_bounds__(256) k_mse_fwd(Batch b, int chunk_len) {
 // per-voxel residual r_x = f - Mw and n_x = grad M(x+u) give the Eq. 9 step
 // instead, which K3 then smooths like an Adam step.
 __global__ void __launch_bounds__(256) k_mse_grad(Batch b, int demons, double alpha) {
-    const int pair = blockIdx.z;
+    const int pair = b.pair0 + blockIdx.z;
     const PairState* st = b.st + pair;
     if (st->done || st->last_rejected) return;
     const Geo g = b.g;
@@ -432,7 +432,7 @@ __device__ __forceinline__ double mi_scale(double lo, double hi, int B) {
 // chunking and slab split), merged into HIST.
 __global__ void __launch_bounds__(256) k_mi_hist(Batch b, LmParams p, int chunk_len) {
     extern __shared__ unsigned long long sh_hist[];
-    const int pair = blockIdx.z;
+    const int pair = b.pair0 + blockIdx.z;
     const PairState* st = b.st + pair;
     if (st->done) return;
     const Geo g = b.g;
@@ -468,7 +468,7 @@ __global__ void __launch_bounds__(256) k_mi_hist(Batch b, LmParams p, int chunk_
 __global__ void k_mi_finalize(Batch b, LmParams p, int mode) {
     __shared__ double red[32];
     __shared__ double s_pm[64];
-    const int pair = blockIdx.x;
+    const int pair = b.pair0 + blockIdx.x;
     PairState* st = b.st + pair;
     if (st->done) return;
     const int B = p.mi_bins;
@@ -507,7 +507,7 @@ __global__ void k_mi_finalize(Batch b, LmParams p, int mode) {
 // g = dr/dMw grad M(x+u), dr/dMw = -(1/N) s_m sum_i a_i(t_f) sum_j b'_j(t_m) T_ij
 // at the accepted warp; skipped after a rejection (gradient unchanged).
 __global__ void __launch_bounds__(256) k_mi_grad(Batch b, LmParams p) {
-    const int pair = blockIdx.z;
+    const int pair = b.pair0 + blockIdx.z;
     const PairState* st = b.st + pair;
     if (st->done || st->last_rejected) return;
     const Geo g = b.g;
@@ -573,7 +573,7 @@ __global__ void __launch_bounds__(k1::NT, 2) k_lncc_fwd(Batch b, int chunk_len) 
     __shared__ __align__(16) double s_x[2][5][IH * TX];
     __shared__ int s_last;
 
-    const int pair = blockIdx.z;
+    const int pair = b.pair0 + blockIdx.z;
     PairState* st = b.st + pair;
     if (st->done) return;
     const Geo g = b.g;
@@ -751,7 +751,7 @@ __global__ void __launch_bounds__(k1::NT, 2) k_lncc_fwd(Batch b, int chunk_len) 
 // slab split), then the loss / damping / rejection state machine.
 __global__ void k_finalize(Batch b, LmParams p, int mode) {
     __shared__ double red[32];
-    const int pair = blockIdx.x;
+    const int pair = b.pair0 + blockIdx.x;
     PairState* st = b.st + pair;
     if (st->done) return;
     const double* psum = b.plane_sum + (long long)pair * b.g.nz;
@@ -815,7 +815,7 @@ __global__ void __launch_bounds__(k2::NT, WLM_K2_MIN_BLOCKS) k_lncc_bwd(Batch b,
     k2::OwnSlot* const s_own = reinterpret_cast<k2::OwnSlot*>(k2_smem);
     (void)p;
 
-    const int pair = blockIdx.z;
+    const int pair = b.pair0 + blockIdx.z;
     const PairState* st = b.st + pair;
     if (st->done || st->last_rejected) return;
     const Geo g = b.g;
@@ -1061,7 +1061,7 @@ __global__ void __launch_bounds__(k3::NT, 2) k_step_smooth(Batch b, LmParams p, 
     __shared__ float s_max[NT / 32];
     __shared__ double s_binv[2 * (R > 0 ? R : 1)];
 
-    const int pair = blockIdx.z;
+    const int pair = b.pair0 + blockIdx.z;
     PairState* st = b.st + pair;
     if (st->done) return;
     const Geo g = b.g;
@@ -1329,7 +1329,7 @@ __global__ void __launch_bounds__(k4::NT, 1) k_compose_smooth(Batch b, LmParams 
     double* s_binv = k4_smem + S::TOTAL; // [2R]
     uint64_t* s_bar = reinterpret_cast<uint64_t*>(k4_smem + S::OFF_BAR);  // [4] TMA ring slots
 
-    const int pair = blockIdx.z;
+    const int pair = b.pair0 + blockIdx.z;
     const PairState* st = b.st + pair;
     if (st->done) return;
     const Geo g = b.g;

@@ -157,51 +157,124 @@ struct wlm_engine {
     Batch B{};
     cudaGraphExec_t step_exec = nullptr, loop_exec = nullptr;
     cudaGraph_t step_graph = nullptr, loop_graph = nullptr;
-    int body_kernels = 0;
+    int body_kernels = 0;   // kernels per attempt graph (whole batch)
+    int group_kernels = 0;  // kernels per attempt of both pair-group graphs
+    // Pair groups: without rejection, iterate() runs the batch as two
+    // independent streams of attempt graphs (pairs [0, h) and [h, pairs))
+    // that only join at the end, so the two groups drift to different
+    // stages and their kernels overlap (a bandwidth-bound stage of one group
+    // beside a compute-bound stage of the other, and each other's tails).
+    int pair_groups = 1;
+    cudaStream_t side = nullptr;
+    cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
+    cudaGraphExec_t group_exec[2] = {nullptr, nullptr};
+    cudaGraph_t group_graph[2] = {nullptr, nullptr};
     bool shared_fm = false;         // F, M owned by a slab group (Batch set by the group)
     bool shared_plane_sum = false;  // per-plane sum(rho) owned by a slab group
 
     ~wlm_engine() {
+        for (int i = 0; i < 2; ++i) {
+            if (group_exec[i]) cudaGraphExecDestroy(group_exec[i]);
+            if (group_graph[i]) cudaGraphDestroy(group_graph[i]);
+        }
+        if (side) cudaStreamDestroy(side);
+        if (fork_ev) cudaEventDestroy(fork_ev);
+        if (join_ev) cudaEventDestroy(join_ev);
         if (step_exec) cudaGraphExecDestroy(step_exec);
         if (loop_exec) cudaGraphExecDestroy(loop_exec);
         if (step_graph) cudaGraphDestroy(step_graph);
         if (loop_graph) cudaGraphDestroy(loop_graph);
     }
 
-    // Stages of one attempt (a slab group interleaves them with exchanges).
-    void stage_grad(cudaStream_t s) {
-        if (P.metric == WLM_METRIC_MSE) launch_mse_grad(B, P, s);
-        else if (P.metric == WLM_METRIC_MI) launch_mi_grad(B, P, s);
-        else launch_lncc_bwd(B, P, s);
-        if (P.optimizer == WLM_OPT_ADAM) launch_adam(B, P, s);
+    // Stages of one attempt (a slab group interleaves them with exchanges),
+    // on the whole batch or on one pair group b.
+    void stage_grad(const Batch& b, cudaStream_t s) {
+        if (P.metric == WLM_METRIC_MSE) launch_mse_grad(b, P, s);
+        else if (P.metric == WLM_METRIC_MI) launch_mi_grad(b, P, s);
+        else launch_lncc_bwd(b, P, s);
+        if (P.optimizer == WLM_OPT_ADAM) launch_adam(b, P, s);
     }
-    void stage_step(cudaStream_t s) {
-        if (P.optimizer == WLM_OPT_LM && P.tile_k > 1) launch_tile_matrix(B, P, s);
-        launch_step_smooth(B, P, s);
+    void stage_step(const Batch& b, cudaStream_t s) {
+        if (P.optimizer == WLM_OPT_LM && P.tile_k > 1) launch_tile_matrix(b, P, s);
+        launch_step_smooth(b, P, s);
     }
-    void stage_compose(cudaStream_t s) {
-        launch_compose_smooth(B, P, s);
-        if (P.log_jacobian) launch_jacobian_diag(B, P, s);
+    void stage_compose(const Batch& b, cudaStream_t s) {
+        launch_compose_smooth(b, P, s);
+        if (P.log_jacobian) launch_jacobian_diag(b, P, s);
     }
-    void stage_eval(int mode, cudaStream_t s) {
-        if (P.metric == WLM_METRIC_MSE) launch_mse_fwd(B, P, mode, s);
-        else if (P.metric == WLM_METRIC_MI) launch_mi_fwd(B, P, mode, s);
-        else launch_lncc_fwd(B, P, mode, s);
+    void stage_eval(const Batch& b, int mode, cudaStream_t s) {
+        if (P.metric == WLM_METRIC_MSE) launch_mse_fwd(b, P, mode, s);
+        else if (P.metric == WLM_METRIC_MI) launch_mi_fwd(b, P, mode, s);
+        else launch_lncc_fwd(b, P, mode, s);
     }
-    void stage_finalize(int mode, cudaStream_t s) {
-        if (P.metric == WLM_METRIC_MI) launch_mi_finalize(B, P, mode, s);
-        else launch_finalize(B, P, mode, s);
+    void stage_finalize(const Batch& b, int mode, cudaStream_t s) {
+        if (P.metric == WLM_METRIC_MI) launch_mi_finalize(b, P, mode, s);
+        else launch_finalize(b, P, mode, s);
+    }
+    void stage_grad(cudaStream_t s) { stage_grad(B, s); }
+    void stage_step(cudaStream_t s) { stage_step(B, s); }
+    void stage_compose(cudaStream_t s) { stage_compose(B, s); }
+    void stage_eval(int mode, cudaStream_t s) { stage_eval(B, mode, s); }
+    void stage_finalize(int mode, cudaStream_t s) { stage_finalize(B, mode, s); }
+
+    void attempt(const Batch& b, cudaStream_t s) {
+        stage_grad(b, s);
+        stage_step(b, s);
+        stage_compose(b, s);
+        stage_eval(b, 1, s);
+        stage_finalize(b, 1, s);
     }
 
-    void body(cudaStream_t s) {
-        stage_grad(s);
-        stage_step(s);
-        stage_compose(s);
-        stage_eval(1, s);
-        stage_finalize(1, s);
+    // One attempt for every pair.
+    void body(cudaStream_t s) { attempt(B, s); }
+
+    // Pair group g of the batch: pairs [0, h) and [h, pairs), h = ceil(pairs/2).
+    Batch group(int gi) const {
+        Batch b = B;
+        const int h = (pairs + 1) / 2;
+        b.pair0 = gi == 0 ? 0 : h;
+        b.pairs = gi == 0 ? h : pairs - h;
+        return b;
+    }
+    bool grouped() const { return pair_groups > 1 && pairs > 1; }
+
+    void build_group_graphs() {
+        if (group_exec[0]) return;
+        if (!side) {
+            CK(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
+            CK(cudaEventCreateWithFlags(&fork_ev, cudaEventDisableTiming));
+            CK(cudaEventCreateWithFlags(&join_ev, cudaEventDisableTiming));
+        }
+        const uint64_t saved = g_kernel_launches;
+        for (int gi = 0; gi < 2; ++gi) {
+            CK(cudaStreamBeginCapture(ctx->capture, cudaStreamCaptureModeThreadLocal));
+            attempt(group(gi), ctx->capture);
+            CK(cudaStreamEndCapture(ctx->capture, &group_graph[gi]));
+            CK(cudaGraphInstantiate(&group_exec[gi], group_graph[gi], 0));
+        }
+        group_kernels = (int)(g_kernel_launches - saved);
+        g_kernel_launches = saved;
+    }
+
+    // iters attempts of every pair as two independent graph streams joined
+    // at the end (rejection off: an attempt is an iteration).
+    void launch_grouped(int iters, cudaStream_t s) {
+        build_group_graphs();
+        CK(cudaEventRecord(fork_ev, s));
+        CK(cudaStreamWaitEvent(side, fork_ev, 0));
+        for (int i = 0; i < iters; ++i) {
+            CK(cudaGraphLaunch(group_exec[0], s));
+            CK(cudaGraphLaunch(group_exec[1], side));
+        }
+        CK(cudaEventRecord(join_ev, side));
+        CK(cudaStreamWaitEvent(s, join_ev, 0));
     }
 
     void invalidate_graphs() {
+        for (int i = 0; i < 2; ++i) {
+            if (group_exec[i]) { cudaGraphExecDestroy(group_exec[i]); group_exec[i] = nullptr; }
+            if (group_graph[i]) { cudaGraphDestroy(group_graph[i]); group_graph[i] = nullptr; }
+        }
         if (step_exec) { cudaGraphExecDestroy(step_exec); step_exec = nullptr; }
         if (loop_exec) { cudaGraphExecDestroy(loop_exec); loop_exec = nullptr; }
         if (step_graph) { cudaGraphDestroy(step_graph); step_graph = nullptr; }
@@ -239,6 +312,7 @@ struct wlm_engine {
         CK(cudaStreamBeginCaptureToGraph(ctx->capture, bodyg, nullptr, nullptr, 0,
                                          cudaStreamCaptureModeThreadLocal));
         body(ctx->capture);
+        body_kernels = (int)(g_kernel_launches - saved);
         launch_loop_cond(B, h, ctx->capture);
         cudaGraph_t out = nullptr;
         CK(cudaStreamEndCapture(ctx->capture, &out));

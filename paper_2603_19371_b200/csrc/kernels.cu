@@ -65,7 +65,7 @@ __device__ double block_sum(double v, double* red) {
 
 // Adam, pointwise; t = accepted iterations + 1 at this level.
 __global__ void k_adam(Batch b, LmParams p) {
-    const int pair = blockIdx.y;
+    const int pair = b.pair0 + blockIdx.y;
     const PairState* st = b.st + pair;
     if (st->done) return;
     const long long n = b.g.n, n3 = 3 * n;
@@ -121,7 +121,7 @@ __device__ __forceinline__ void interior(int n, int& lo, int& hi) {
 
 __global__ void k_jacobian_diag(Batch b, LmParams p) {
     __shared__ float s_min[32];
-    const int pair = blockIdx.y;
+    const int pair = b.pair0 + blockIdx.y;
     PairState* st = b.st + pair;
     if (st->done) return;
     const Geo g = b.g;
@@ -468,7 +468,7 @@ __device__ __forceinline__ void add_outer(double H[6], double g0, double g1, dou
 // Engine: one thread per (pair, tile); g is the stored fp32 gradient (SoA).
 __global__ void k_tile_matrix(Batch b, LmParams p) {
     const long long ntiles = (long long)b.tkx * b.tky * b.tkz;
-    const int pair = blockIdx.y;
+    const int pair = b.pair0 + blockIdx.y;
     const PairState* st = b.st + pair;
     if (st->done) return;
     const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;

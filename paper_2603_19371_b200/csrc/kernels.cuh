@@ -61,7 +61,8 @@ struct LmParams {
 // Buffers of a batch of `pairs` registrations of identical geometry.
 struct Batch {
     Geo g;
-    int pairs;
+    int pairs;        // pairs in this launch: pair0 .. pair0 + pairs - 1
+    int pair0;        // first pair (a pair group of the engine's batch; 0 otherwise)
     const float* F;   // [pair][n]
     const float* M;   // [pair][n]
     float* U;         // [pair][2][3][n] ping-pong warps

@@ -82,6 +82,10 @@ class Engine:
     def iterate(self, iters):
         self._chk(self.lib.wlm_engine_iterate(self.h, int(iters)))
 
+    def set_pair_groups(self, groups):
+        """1 or 2 independent streams of attempt graphs in iterate() (wlm.h)."""
+        self._chk(self.lib.wlm_engine_set_pair_groups(self.h, int(groups)))
+
     def step(self):
         self._chk(self.lib.wlm_engine_step(self.h))
 

@@ -310,6 +310,30 @@ def test_degenerate_and_ragged_dims_match_oracle(P, ctx, shape):
     compare_runs(tr, tr_o, aos(warp[0]), u_o, 1e-6, 1e-5)
 
 
+def test_pair_groups_do_not_change_results(P, ctx):
+    """Two pair-group streams (the default) vs one chain: bit-identical warps
+    and traces, with an odd pair count (groups of 2 and 1)."""
+    shape = (20, 24, 28)
+    Fs, Ms = zip(*[O.synth_pair(shape, 300 + s, num_blobs=6, warp_max=2.0)[:2] for s in range(3)])
+    F, M = np.stack(Fs), np.stack(Ms)
+    cfg = P.reg_config(nlevels=1, factors=[1], iters=[12])
+    out = {}
+    for groups in (1, 2):
+        eng = P.Engine(shape, pairs=3, cfg=cfg, ctx=ctx)
+        eng.set_pair_groups(groups)
+        eng.load(F, M)
+        eng.set_warp(None)
+        eng.begin_level(0)
+        eng.iterate(7)
+        eng.iterate(5)
+        out[groups] = (eng.get_warp(), [eng.trace(p) for p in range(3)])
+        eng.close()
+    assert np.array_equal(out[1][0], out[2][0])
+    assert same_trace(out[1][1], out[2][1]) and len(out[2][1][2]) == 12
+    with pytest.raises(P.InvalidArgument):
+        P.Engine(shape, pairs=1, cfg=cfg, ctx=ctx).set_pair_groups(3)
+
+
 def test_batch_pairs_are_independent_and_deterministic(P, ctx):
     shape = (24, 28, 32)
     Fs, Ms = [], []
@@ -597,4 +621,6 @@ def test_bench_json_contract():
     assert rf["bound"] == "hbm" and 0 < rf["frac"] < 1 and rf["peak"] > 0 and rf["unit"] == "GB/s"
     e2e = line["e2e"]
     assert e2e["h2d_bytes_per_step"] > 0 and e2e["d2h_bytes_per_step"] > 0 and e2e["value"] > 0
-    assert line["gpu_launches"] == 6 * 3  # K2, K3, K4, K1a, K1b, K5 per step
+    # K2, K3, K4, K1a, K1b, K5 per attempt and pair group (2 groups of 1 pair
+    # here), plus the iteration-target kernel of the one iterate() call
+    assert line["gpu_launches"] == 6 * 2 * 3 + 1
