@@ -222,12 +222,12 @@ wlm_status wlm_engine_iterate(wlm_engine* e, int iters);
 /* Launch exactly one attempt (K2..K4 + evaluation) per pair (rejection must
  * be disabled). */
 wlm_status wlm_engine_step(wlm_engine* e);
-/* Pair groups (1 or 2, default 2): with rejection off and pairs > 1, iterate
- * runs the batch as two independent streams of attempt graphs (pairs
- * [0, ceil(P/2)) and the rest) that join only when the call's iterations
- * are done, so the groups' kernels overlap.  Results are identical either
- * way (each pair's arithmetic does not depend on the grouping).  The
- * environment variable WLM_PAIR_GROUPS=1 sets the default to 1. */
+/* Pair groups (1..4, default 2): with rejection off and pairs > 1, iterate
+ * runs the batch as that many independent streams of attempt graphs
+ * (contiguous pair ranges) that join only when the call's iterations are
+ * done, so the groups' kernels overlap.  Results are identical for any
+ * grouping (each pair's arithmetic does not depend on it).  The environment
+ * variable WLM_PAIR_GROUPS sets the default. */
 wlm_status wlm_engine_set_pair_groups(wlm_engine* e, int groups);
 /* Copy out per-pair state / trace rows written since begin_level (syncs). */
 wlm_status wlm_engine_state(wlm_engine* e, int pair, wlm_lm_state* st, double* r,

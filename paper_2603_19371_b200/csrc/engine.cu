@@ -30,7 +30,8 @@ wlm_status engine_init(wlm_engine* e, wlm_ctx* ctx, wlm_dims d, int pairs, const
     // captures the whole batch as one chain
     {
         const char* v = std::getenv("WLM_PAIR_GROUPS");
-        e->pair_groups = (v && std::atoi(v) == 1) ? 1 : 2;
+        const int n = v ? std::atoi(v) : 0;
+        e->pair_groups = (n >= 1 && n <= wlm_engine::kMaxGroups) ? n : 2;
     }
     if (c->lm.tile_size < 1) {
         set_err(ctx, "lm.tile_size must be >= 1 (SPEC.md:259)");
@@ -378,7 +379,7 @@ wlm_status wlm_engine_step(wlm_engine* e) {
 }
 
 wlm_status wlm_engine_set_pair_groups(wlm_engine* e, int groups) {
-    if (!e || groups < 1 || groups > 2) return WLM_INVALID_ARG;
+    if (!e || groups < 1 || groups > wlm_engine::kMaxGroups) return WLM_INVALID_ARG;
     if (e->pair_groups != groups) {
         wlm_ctx* ctx = e->ctx;
         wlm_status s = run(ctx, [&] { CK(cudaStreamSynchronize(ctx->stream)); });

@@ -164,22 +164,23 @@ struct wlm_engine {
     // that only join at the end, so the two groups drift to different
     // stages and their kernels overlap (a bandwidth-bound stage of one group
     // beside a compute-bound stage of the other, and each other's tails).
+    static constexpr int kMaxGroups = 4;
     int pair_groups = 1;
-    cudaStream_t side = nullptr;
-    cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
-    cudaGraphExec_t group_exec[2] = {nullptr, nullptr};
-    cudaGraph_t group_graph[2] = {nullptr, nullptr};
+    cudaStream_t side[kMaxGroups] = {};  // side[0] unused (group 0 runs on the ctx stream)
+    cudaEvent_t fork_ev = nullptr, join_ev[kMaxGroups] = {};
+    cudaGraphExec_t group_exec[kMaxGroups] = {};
+    cudaGraph_t group_graph[kMaxGroups] = {};
     bool shared_fm = false;         // F, M owned by a slab group (Batch set by the group)
     bool shared_plane_sum = false;  // per-plane sum(rho) owned by a slab group
 
     ~wlm_engine() {
-        for (int i = 0; i < 2; ++i) {
+        for (int i = 0; i < kMaxGroups; ++i) {
             if (group_exec[i]) cudaGraphExecDestroy(group_exec[i]);
             if (group_graph[i]) cudaGraphDestroy(group_graph[i]);
+            if (side[i]) cudaStreamDestroy(side[i]);
+            if (join_ev[i]) cudaEventDestroy(join_ev[i]);
         }
-        if (side) cudaStreamDestroy(side);
         if (fork_ev) cudaEventDestroy(fork_ev);
-        if (join_ev) cudaEventDestroy(join_ev);
         if (step_exec) cudaGraphExecDestroy(step_exec);
         if (loop_exec) cudaGraphExecDestroy(loop_exec);
         if (step_graph) cudaGraphDestroy(step_graph);
@@ -228,25 +229,27 @@ struct wlm_engine {
     // One attempt for every pair.
     void body(cudaStream_t s) { attempt(B, s); }
 
-    // Pair group g of the batch: pairs [0, h) and [h, pairs), h = ceil(pairs/2).
+    // Pair groups: contiguous, sizes differing by at most one.
+    int ngroups() const { return std::min(pair_groups, pairs); }
     Batch group(int gi) const {
         Batch b = B;
-        const int h = (pairs + 1) / 2;
-        b.pair0 = gi == 0 ? 0 : h;
-        b.pairs = gi == 0 ? h : pairs - h;
+        const int G = ngroups(), q = pairs / G, r = pairs % G;
+        b.pair0 = gi * q + std::min(gi, r);
+        b.pairs = q + (gi < r ? 1 : 0);
         return b;
     }
-    bool grouped() const { return pair_groups > 1 && pairs > 1; }
+    bool grouped() const { return ngroups() > 1; }
 
     void build_group_graphs() {
         if (group_exec[0]) return;
-        if (!side) {
-            CK(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
-            CK(cudaEventCreateWithFlags(&fork_ev, cudaEventDisableTiming));
-            CK(cudaEventCreateWithFlags(&join_ev, cudaEventDisableTiming));
+        const int G = ngroups();
+        if (!fork_ev) CK(cudaEventCreateWithFlags(&fork_ev, cudaEventDisableTiming));
+        for (int gi = 1; gi < G; ++gi) {
+            if (!side[gi]) CK(cudaStreamCreateWithFlags(&side[gi], cudaStreamNonBlocking));
+            if (!join_ev[gi]) CK(cudaEventCreateWithFlags(&join_ev[gi], cudaEventDisableTiming));
         }
         const uint64_t saved = g_kernel_launches;
-        for (int gi = 0; gi < 2; ++gi) {
+        for (int gi = 0; gi < G; ++gi) {
             CK(cudaStreamBeginCapture(ctx->capture, cudaStreamCaptureModeThreadLocal));
             attempt(group(gi), ctx->capture);
             CK(cudaStreamEndCapture(ctx->capture, &group_graph[gi]));
@@ -256,22 +259,23 @@ struct wlm_engine {
         g_kernel_launches = saved;
     }
 
-    // iters attempts of every pair as two independent graph streams joined
-    // at the end (rejection off: an attempt is an iteration).
+    // iters attempts of every pair as independent graph streams, one per
+    // group, joined at the end (rejection off: an attempt is an iteration).
     void launch_grouped(int iters, cudaStream_t s) {
         build_group_graphs();
+        const int G = ngroups();
         CK(cudaEventRecord(fork_ev, s));
-        CK(cudaStreamWaitEvent(side, fork_ev, 0));
-        for (int i = 0; i < iters; ++i) {
-            CK(cudaGraphLaunch(group_exec[0], s));
-            CK(cudaGraphLaunch(group_exec[1], side));
+        for (int gi = 1; gi < G; ++gi) CK(cudaStreamWaitEvent(side[gi], fork_ev, 0));
+        for (int i = 0; i < iters; ++i)
+            for (int gi = 0; gi < G; ++gi) CK(cudaGraphLaunch(group_exec[gi], gi == 0 ? s : side[gi]));
+        for (int gi = 1; gi < G; ++gi) {
+            CK(cudaEventRecord(join_ev[gi], side[gi]));
+            CK(cudaStreamWaitEvent(s, join_ev[gi], 0));
         }
-        CK(cudaEventRecord(join_ev, side));
-        CK(cudaStreamWaitEvent(s, join_ev, 0));
     }
 
     void invalidate_graphs() {
-        for (int i = 0; i < 2; ++i) {
+        for (int i = 0; i < kMaxGroups; ++i) {
             if (group_exec[i]) { cudaGraphExecDestroy(group_exec[i]); group_exec[i] = nullptr; }
             if (group_graph[i]) { cudaGraphDestroy(group_graph[i]); group_graph[i] = nullptr; }
         }

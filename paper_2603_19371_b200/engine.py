@@ -83,7 +83,7 @@ class Engine:
         self._chk(self.lib.wlm_engine_iterate(self.h, int(iters)))
 
     def set_pair_groups(self, groups):
-        """1 or 2 independent streams of attempt graphs in iterate() (wlm.h)."""
+        """1..4 independent streams of attempt graphs in iterate() (wlm.h)."""
         self._chk(self.lib.wlm_engine_set_pair_groups(self.h, int(groups)))
 
     def step(self):

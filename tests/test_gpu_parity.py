@@ -331,7 +331,7 @@ def test_pair_groups_do_not_change_results(P, ctx):
     assert np.array_equal(out[1][0], out[2][0])
     assert same_trace(out[1][1], out[2][1]) and len(out[2][1][2]) == 12
     with pytest.raises(P.InvalidArgument):
-        P.Engine(shape, pairs=1, cfg=cfg, ctx=ctx).set_pair_groups(3)
+        P.Engine(shape, pairs=1, cfg=cfg, ctx=ctx).set_pair_groups(5)
 
 
 def test_batch_pairs_are_independent_and_deterministic(P, ctx):
