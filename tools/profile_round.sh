@@ -10,7 +10,9 @@ SHORT="python bench.py --steps 3 --warmup 3 --no-cpu-baseline --e2e-iters 1"
 $SHORT > gpurun_out/plain.log 2>&1 && \
   ncu --metrics gpu__time_duration.sum --clock-control none -s 130 -c 42 --csv \
       --log-file gpurun_out/launches_final.csv $SHORT > gpurun_out/ncu_launch.log 2>&1; echo "launches rc=$?"
-$SHORT > gpurun_out/plain2.log 2>&1 && \
+# the full capture profiles whole-batch launches (one pair group), the unit
+# bench.py's per-stage CUDA-event times and roofline.traffic refer to
+$SHORT > gpurun_out/plain2.log 2>&1 && WLM_PAIR_GROUPS=1 \
   ncu --set full --clock-control none --import-source on \
       -k regex:'k_warp_moving|k_lncc_fwd|k_finalize|k_lncc_bwd|k_step_smooth|k_compose_smooth' -s 12 -c 6 \
       -o gpurun_out/prof_final $SHORT > gpurun_out/ncu_full.log 2>&1; echo "full rc=$?"
