@@ -300,41 +300,42 @@ __global__ void __launch_bounds__(256) k_warp_moving(Batch b, int mode, int z_fi
     }
 }
 
-// The pair's last CTA (of a 2D grid of 256-thread CTAs) reduces the owned
-// planes' per-(tile, warp) partials in a fixed order into plane_sum[z];
-// foreign planes are zeroed for the NCCL slab all-reduce.
-__device__ void reduce_plane_partials(const Batch& b, PairState* st, const double* part, int tiles,
-                                      int* s_last) {
-    const Geo& g = b.g;
-    const int nblk = gridDim.x * gridDim.y;
-    if (threadIdx.x == 0) {
-        __threadfence();
-        const unsigned prev = atomicAdd(&st->counter, 1u);
-        *s_last = prev == (unsigned)(nblk - 1);
+// Per-plane sum(rho) (or sum e^2) from the (plane, tile, warp) partials: one
+// CTA per (plane, pair), strided coalesced loads, then a fixed tree, so the
+// sum depends on neither the chunking nor the slab split (and not on which
+// CTA finished last).  Planes outside [zs, ze) are zeroed for the NCCL
+// all-reduce of a distributed slab group.
+__global__ void __launch_bounds__(256) k_plane_sums(Batch b) {
+    __shared__ double red[32];
+    const int z = blockIdx.x;
+    const int pair = b.pair0 + blockIdx.y;
+    const PairState* st = b.st + pair;
+    if (st->done) return;
+    const Geo g = b.g;
+    double* __restrict__ psum = b.plane_sum + (long long)pair * g.nz;
+    if (z < g.zs || z >= g.ze) {
+        if (b.zero_foreign_planes && threadIdx.x == 0) psum[z] = 0.0;
+        return;
     }
-    __syncthreads();
-    if (!*s_last) return;
-    __threadfence();
-    double* __restrict__ psum = b.plane_sum + (long long)(st - b.st) * g.nz;
-    for (int z = threadIdx.x; z < g.nz; z += blockDim.x) {
-        double s = 0.0;
-        if (z >= g.zs && z < g.ze) {
-            const double* pz = part + (long long)z * tiles * 8;
-            for (int i = 0; i < tiles * 8; ++i) s += __ldcg(pz + i);
-        }
-        if (z >= g.zs && z < g.ze) psum[z] = s;
-        else if (b.zero_foreign_planes) psum[z] = 0.0;
-    }
-    if (threadIdx.x == 0) st->counter = 0u;
+    const long long m = (long long)cdiv(g.nx, 32) * cdiv(g.ny, 8) * 8;
+    const double* __restrict__ pz = b.partials + ((long long)pair * g.nz + z) * m;
+    double s = 0.0;
+    for (long long i = threadIdx.x; i < m; i += blockDim.x) s += __ldcg(pz + i);
+    s = block_sum(s, red);
+    if (threadIdx.x == 0) psum[z] = s;
+}
+
+void launch_plane_sums(const Batch& b, cudaStream_t s) {
+    k_plane_sums<<<dim3(b.g.nz, b.pairs), 256, 0, s>>>(b);
+    ++g_kernel_launches;
 }
 
 // MSE forward: one fp64 partial of sum (f - Mw)^2 per
 // (plane, tile, warp) in the K1b layout, then the same fixed-order plane
 // reduction; K5 turns it into r = loss_raw = MSE.
 __global__ void __launch_bounds__(256) k_mse_fwd(Batch b, int chunk_len) {
-    __shared__ int s_last;
     const int pair = b.pair0 + blockIdx.z;
-    PairState* st = b.st + pair;
+    const PairState* st = b.st + pair;
     if (st->done) return;
     const Geo g = b.g;
     const int nxy = g.nx * g.ny;
@@ -357,7 +358,6 @@ __global__ void __launch_bounds__(256) k_mse_fwd(Batch b, int chunk_len) {
         e2 = warp_sum(e2);
         if (ox == 0) part[((long long)z * tiles + blockIdx.x) * 8 + oy] = e2;
     }
-    reduce_plane_partials(b, st, part, tiles, &s_last);
 }
 
 // MSE gradient: g = -2 (f - Mw) / N * grad M(x+u) at the accepted warp
@@ -548,8 +548,8 @@ __global__ void __launch_bounds__(256) k_mi_grad(Batch b, LmParams p) {
 //   rho = c / sqrt(vf vm); A = 1/(n sqrt(vf vm)); B = -rho/(n vm)  -> fp32
 //   E = A' mu_f' + B' mu_m'  (fp64, from the rounded A', B', so K2's
 //   f' S_A + m' S_B - S_E cancels exactly).
-//   sum(rho): one partial per (plane, tile, warp); the last CTA of the pair
-//   reduces them per owned plane in a fixed order into plane_sum[z].
+//   sum(rho): one partial per (plane, tile, warp); k_plane_sums (one CTA per
+//   plane) reduces them in a fixed order into plane_sum[z].
 // Schedule (as K3): one barrier per plane; phase p runs the y-pass of plane p
 // (z ring, plane p - R out), the x-pass of plane p+1 (two outputs per thread
 // from 16-byte shared loads), the halo tile of plane p+2 and the loads of
@@ -571,7 +571,6 @@ __global__ void __launch_bounds__(k1::NT, 2) k_lncc_fwd(Batch b, int chunk_len) 
     constexpr int IWP = S::IWP, IH = S::IH, NI = S::NI, SL = S::SL, NV = S::NV;
     __shared__ __align__(16) double s_in[2][2][NI];  // [buffer][f', m'][tile]
     __shared__ __align__(16) double s_x[2][5][IH * TX];
-    __shared__ int s_last;
 
     const int pair = b.pair0 + blockIdx.z;
     PairState* st = b.st + pair;
@@ -744,7 +743,6 @@ __global__ void __launch_bounds__(k1::NT, 2) k_lncc_fwd(Batch b, int chunk_len) 
         }
     }
 
-    reduce_plane_partials(b, st, part, tiles, &s_last);
 }
 
 // K5: r from the per-plane sums in z order (identical on every rank for any
@@ -1613,6 +1611,7 @@ void launch_mse_fwd(const Batch& b, const LmParams& p, int mode, cudaStream_t s)
     grid.z = b.pairs;
     k_mse_fwd<<<grid, 256, 0, s>>>(b, sh.chunk_len);
     g_kernel_launches += 2;
+    launch_plane_sums(b, s);
 }
 
 void launch_mi_fwd(const Batch& b, const LmParams& p, int mode, cudaStream_t s) {
@@ -1653,6 +1652,7 @@ void launch_lncc_fwd(const Batch& b, const LmParams& p, int mode, cudaStream_t s
     grid.z = b.pairs;
     k_lncc_fwd<2><<<grid, k1::NT, 0, s>>>(b, sh.chunk_len);
     g_kernel_launches += 2;
+    launch_plane_sums(b, s);
 }
 
 void launch_finalize(const Batch& b, const LmParams& p, int mode, cudaStream_t s) {

@@ -8,8 +8,8 @@
 // register ring of 2R+1 planes that is filtered along z.  Every global
 // read/write is a unit-stride row of one SoA plane (coalesced), the halo
 // overlap between neighbouring CTAs is served by L2, and there are no float
-// atomics: sums are per-CTA fp64 partials reduced in a fixed order by the
-// last CTA of each pair (deterministic), maxima use exact
+// atomics: sums are per-CTA fp64 partials reduced in a fixed order, one CTA
+// per plane (deterministic), maxima use exact
 // ordered-integer atomics.
 #include <algorithm>
 #include <cfloat>

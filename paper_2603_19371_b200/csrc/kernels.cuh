@@ -10,8 +10,8 @@
 
 namespace wlm {
 
-// Per-pair device-resident optimizer state.  Mutated only by the evaluation
-// kernel's last block (one writer), read by the other kernels, so an
+// Per-pair device-resident optimizer state.  Mutated only by the finalize
+// kernel (one CTA per pair, one writer), read by the other kernels, so an
 // iteration needs no host round trip.
 struct PairState {
     double lambda, L1, L2;   // LmState
@@ -105,9 +105,10 @@ void launch_mse_grad(const Batch& b, const LmParams& p, cudaStream_t s);
 // K4's TMA descriptor for the engine's U buffer (box = one warp-ring slot);
 // leaves tma_u_ok = 0 when the layout does not allow it (nx % 4 != 0).
 void make_tma_u(Batch& b, int R_warp);
-// K1: warp + LNCC window moments + coefficients + sum(rho); last block runs
-// the loss/damping/rejection state machine.  mode 0 evaluates the accepted
-// warp (level start), mode 1 the attempt in the other buffer.
+// K1: warp + LNCC window moments + coefficients + per-plane sum(rho) (K1a,
+// K1b, k_plane_sums); K5 then runs the loss/damping/rejection state machine.
+// mode 0 evaluates the accepted warp (level start), mode 1 the attempt in
+// the other buffer.
 void launch_lncc_fwd(const Batch& b, const LmParams& p, int mode, cudaStream_t s);
 // K5: r = 1 - mean(rho) from the per-plane sums (z order), then the state
 // machine.  Runs after the plane sums of every slab are in place.

@@ -621,6 +621,6 @@ def test_bench_json_contract():
     assert rf["bound"] == "hbm" and 0 < rf["frac"] < 1 and rf["peak"] > 0 and rf["unit"] == "GB/s"
     e2e = line["e2e"]
     assert e2e["h2d_bytes_per_step"] > 0 and e2e["d2h_bytes_per_step"] > 0 and e2e["value"] > 0
-    # K2, K3, K4, K1a, K1b, K5 per attempt and pair group (2 groups of 1 pair
+    # K2, K3, K4, K1a, K1b, plane sums, K5 per attempt and pair group (2 groups of 1 pair
     # here), plus the iteration-target kernel of the one iterate() call
-    assert line["gpu_launches"] == 6 * 2 * 3 + 1
+    assert line["gpu_launches"] == 7 * 2 * 3 + 1
