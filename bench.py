@@ -252,8 +252,8 @@ def run_ours(args, rank, world, local):
     ctx2 = P.Context(local)
     eng2 = P.Engine(shape, pairs=pairs, cfg=cfg, ctx=ctx2)
     engines = ((eng, ctx), (eng2, ctx2))
-    for e, _ in engines:  # the two engines already overlap: one stream each
-        e.set_pair_groups(1)
+    for e, _ in engines:  # the two engines already overlap each other
+        e.set_pair_groups(args.e2e_groups)
 
     def e2e_launch(e):
         e.load(F_h, M_h)
@@ -328,8 +328,8 @@ def run_ours(args, rank, world, local):
                 "d2h_bytes_per_step": 3 * pairs * nvox * 4,
                 "iters_per_step": e2e_iters, "steps": pipe_steps,
                 "path": "wlm_engine_load(host) + wlm_engine_iterate + wlm_engine_get_warp(host)",
-                "overlap": "two engines on two streams alternate steps: step k+1's input copy and "
-                           "step k's warp copy overlap the other engine's iterations",
+                "overlap": "two engines alternate steps: step k+1's input copy and step k's warp "
+                           "copy overlap the other engine's iterations",
                 "serial_value": round(serial_val, 4),
                 "serial": "one engine, one step after the other (copies not overlapped)"},
         "gpu_launches": int(launches_timed),
@@ -607,6 +607,7 @@ def main():
     ap.add_argument("--size", type=int, default=192)
     ap.add_argument("--pairs-per-gpu", type=int, default=8)
     ap.add_argument("--e2e-iters", type=int, default=100)
+    ap.add_argument("--e2e-groups", type=int, default=2, help="pair groups of each pipelined e2e engine")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extra", action="store_true", help="skip the config 2/3 pyramid runs")
     ap.add_argument("--ref-budget-s", type=float, default=200.0)

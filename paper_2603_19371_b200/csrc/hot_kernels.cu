@@ -1606,7 +1606,7 @@ void launch_mse_fwd(const Batch& b, const LmParams& p, int mode, cudaStream_t s)
     (void)p;
     const dim3 wgrid(cdiv(b.g.nx, 32) * cdiv(b.g.ny, 8), cdiv(b.g.ze - b.g.zs, kZP), b.pairs);
     k_warp_moving<false><<<wgrid, 256, 0, s>>>(b, mode, b.g.zs, b.g.ze);
-    const LaunchShape sh = shape_for(b.g, b.pairs, 8);
+    const LaunchShape sh = shape_for(b.g, b.pairs, 8, b.ctas_per_sm);
     dim3 grid = sh.grid();
     grid.z = b.pairs;
     k_mse_fwd<<<grid, 256, 0, s>>>(b, sh.chunk_len);
@@ -1617,7 +1617,7 @@ void launch_mse_fwd(const Batch& b, const LmParams& p, int mode, cudaStream_t s)
 void launch_mi_fwd(const Batch& b, const LmParams& p, int mode, cudaStream_t s) {
     const dim3 wgrid(cdiv(b.g.nx, 32) * cdiv(b.g.ny, 8), cdiv(b.g.ze - b.g.zs, kZP), b.pairs);
     k_warp_moving<false><<<wgrid, 256, 0, s>>>(b, mode, b.g.zs, b.g.ze);
-    const LaunchShape sh = shape_for(b.g, b.pairs, 8);
+    const LaunchShape sh = shape_for(b.g, b.pairs, 8, b.ctas_per_sm);
     dim3 grid = sh.grid();
     grid.z = b.pairs;
     k_mi_hist<<<grid, 256, sizeof(unsigned long long) * p.mi_bins * p.mi_bins, s>>>(b, p, sh.chunk_len);
@@ -1647,7 +1647,7 @@ void launch_lncc_fwd(const Batch& b, const LmParams& p, int mode, cudaStream_t s
     const int zf = std::max(0, b.g.zs - 2), zl = std::min(b.g.nz, b.g.ze + 2);
     const dim3 wgrid(cdiv(b.g.nx, 32) * cdiv(b.g.ny, 8), cdiv(zl - zf, kZP), b.pairs);
     k_warp_moving<true><<<wgrid, 256, 0, s>>>(b, mode, zf, zl);
-    const LaunchShape sh = shape_for(b.g, b.pairs, k1::TY);
+    const LaunchShape sh = shape_for(b.g, b.pairs, k1::TY, b.ctas_per_sm);
     dim3 grid = sh.grid();
     grid.z = b.pairs;
     k_lncc_fwd<2><<<grid, k1::NT, 0, s>>>(b, sh.chunk_len);
@@ -1661,7 +1661,7 @@ void launch_finalize(const Batch& b, const LmParams& p, int mode, cudaStream_t s
 }
 
 void launch_lncc_bwd(const Batch& b, const LmParams& p, cudaStream_t s) {
-    const LaunchShape sh = shape_for(b.g, b.pairs, k2::TY);
+    const LaunchShape sh = shape_for(b.g, b.pairs, k2::TY, b.ctas_per_sm);
     dim3 grid = sh.grid();
     grid.z = b.pairs;
     static std::atomic<unsigned long long> attr{0ull};  // per device
@@ -1675,7 +1675,7 @@ void launch_lncc_bwd(const Batch& b, const LmParams& p, cudaStream_t s) {
 }
 
 void launch_step_smooth(const Batch& b, const LmParams& p, cudaStream_t s) {
-    const LaunchShape sh = shape_for(b.g, b.pairs, k3::TY);
+    const LaunchShape sh = shape_for(b.g, b.pairs, k3::TY, b.ctas_per_sm);
     dim3 grid = sh.grid();
     grid.z = b.pairs;
     if (p.optimizer == WLM_OPT_LM && p.tile_k > 1) {
@@ -1717,7 +1717,7 @@ void make_tma_u(Batch& b, int Rw) {
 }
 
 void launch_compose_smooth(const Batch& b, const LmParams& p, cudaStream_t s) {
-    const LaunchShape sh = shape_for(b.g, b.pairs, k4::TY);
+    const LaunchShape sh = shape_for(b.g, b.pairs, k4::TY, b.ctas_per_sm);
     dim3 grid = sh.grid();
     grid.z = b.pairs;
     WLM_DISPATCH_R(p.Rw, ({

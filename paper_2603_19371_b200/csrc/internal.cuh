@@ -236,6 +236,7 @@ struct wlm_engine {
         const int G = ngroups(), q = pairs / G, r = pairs % G;
         b.pair0 = gi * q + std::min(gi, r);
         b.pairs = q + (gi < r ? 1 : 0);
+        b.ctas_per_sm = 1;  // measured: 10.90 -> 11.28 Gvoxel/s at 8 x 192^3 against 4
         return b;
     }
     bool grouped() const { return ngroups() > 1; }

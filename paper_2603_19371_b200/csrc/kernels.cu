@@ -33,15 +33,16 @@ __host__ __device__ inline int cdiv(int a, int b) { return (a + b - 1) / b; }
 
 dim3 LaunchShape::grid() const { return dim3(tiles_x * tiles_y, chunks, 1); }
 
-LaunchShape shape_for(const Geo& g, int pairs, int ty) {
+LaunchShape shape_for(const Geo& g, int pairs, int ty, int ctas_per_sm) {
     LaunchShape s;
     s.tiles_x = cdiv(g.nx, TX);
     s.tiles_y = cdiv(g.ny, ty);
     const long long tiles = (long long)s.tiles_x * s.tiles_y * pairs;
-    // chunks of the owned planes: aim for >= 4 resident CTAs per SM worth of
-    // work; keep >= 8 planes a chunk
+    // chunks of the owned planes: aim for ~4 CTAs per SM worth of work (a
+    // pair group, whose tails the other group fills, aims for 1: every
+    // chunk re-reads 2R halo planes); keep >= 8 planes a chunk
     const int nzo = g.ze - g.zs;
-    const long long want = (long long)kNumSMs * 4;
+    const long long want = (long long)kNumSMs * (ctas_per_sm > 0 ? ctas_per_sm : 4);
     int chunks = (int)std::max<long long>(1, std::min<long long>(nzo, (want + tiles - 1) / tiles));
     int len = cdiv(nzo, chunks);
     len = std::max(len, std::min(nzo, 8));

@@ -85,13 +85,16 @@ struct Batch {
     int tma_u_ok;       // K4 stages the accepted warp by TMA (tma_u valid)
     CUtensorMap tma_u;  // 5D map over U: (x, y, local z, buffer*3 + component, pair)
     int max_blocks;
+    int ctas_per_sm;    // z-chunking target of this launch (0 -> 4; pair groups use 1)
 };
 
 struct LaunchShape {
     int tiles_x, tiles_y, chunks, chunk_len;
     dim3 grid() const;
 };
-LaunchShape shape_for(const Geo& g, int pairs, int ty);
+// z-chunking of a stencil launch: enough chunks that the launch has about
+// ctas_per_sm x SMs CTAs (0 -> 4), each chunk >= 8 planes.
+LaunchShape shape_for(const Geo& g, int pairs, int ty, int ctas_per_sm = 0);
 
 // MSE: K1a warp + per-plane sum (f - Mw)^2; gradient
 // g = -2 (f - Mw)/N grad M(x+u) (pointwise, analytic interpolant gradient).
