@@ -222,8 +222,9 @@ wlm_status wlm_engine_iterate(wlm_engine* e, int iters);
 /* Launch exactly one attempt (K2..K4 + evaluation) per pair (rejection must
  * be disabled). */
 wlm_status wlm_engine_step(wlm_engine* e);
-/* Pair groups (1..4, default 2): with rejection off and pairs > 1, iterate
- * runs the batch as that many independent streams of attempt graphs
+/* Pair groups (1..4, default 2): with pairs > 1, iterate
+ * runs the batch as that many independent streams of attempt graphs (with
+ * rejection on: of device-side WHILE graphs, one per group)
  * (contiguous pair ranges) that join only when the call's iterations are
  * done, so the groups' kernels overlap.  Results are identical for any
  * grouping (each pair's arithmetic does not depend on it).  The environment

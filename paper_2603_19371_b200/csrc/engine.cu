@@ -354,6 +354,9 @@ wlm_status wlm_engine_iterate(wlm_engine* e, int iters) {
             e->build_step_graph();
             for (int i = 0; i < iters; ++i) CK(cudaGraphLaunch(e->step_exec, ctx->stream));
             g_kernel_launches += (uint64_t)iters * e->body_kernels;
+        } else if (e->grouped()) {
+            e->launch_grouped_loop(ctx->stream);
+            g_kernel_launches += (uint64_t)e->group_kernels + e->ngroups();  // at least one trip
         } else {
             e->build_loop_graph();
             CK(cudaGraphLaunch(e->loop_exec, ctx->stream));

@@ -168,8 +168,8 @@ struct wlm_engine {
     int pair_groups = 1;
     cudaStream_t side[kMaxGroups] = {};  // side[0] unused (group 0 runs on the ctx stream)
     cudaEvent_t fork_ev = nullptr, join_ev[kMaxGroups] = {};
-    cudaGraphExec_t group_exec[kMaxGroups] = {};
-    cudaGraph_t group_graph[kMaxGroups] = {};
+    cudaGraphExec_t group_exec[kMaxGroups] = {}, group_loop_exec[kMaxGroups] = {};
+    cudaGraph_t group_graph[kMaxGroups] = {}, group_loop_graph[kMaxGroups] = {};
     bool shared_fm = false;         // F, M owned by a slab group (Batch set by the group)
     bool shared_plane_sum = false;  // per-plane sum(rho) owned by a slab group
 
@@ -177,6 +177,8 @@ struct wlm_engine {
         for (int i = 0; i < kMaxGroups; ++i) {
             if (group_exec[i]) cudaGraphExecDestroy(group_exec[i]);
             if (group_graph[i]) cudaGraphDestroy(group_graph[i]);
+            if (group_loop_exec[i]) cudaGraphExecDestroy(group_loop_exec[i]);
+            if (group_loop_graph[i]) cudaGraphDestroy(group_loop_graph[i]);
             if (side[i]) cudaStreamDestroy(side[i]);
             if (join_ev[i]) cudaEventDestroy(join_ev[i]);
         }
@@ -279,6 +281,8 @@ struct wlm_engine {
         for (int i = 0; i < kMaxGroups; ++i) {
             if (group_exec[i]) { cudaGraphExecDestroy(group_exec[i]); group_exec[i] = nullptr; }
             if (group_graph[i]) { cudaGraphDestroy(group_graph[i]); group_graph[i] = nullptr; }
+            if (group_loop_exec[i]) { cudaGraphExecDestroy(group_loop_exec[i]); group_loop_exec[i] = nullptr; }
+            if (group_loop_graph[i]) { cudaGraphDestroy(group_loop_graph[i]); group_loop_graph[i] = nullptr; }
         }
         if (step_exec) { cudaGraphExecDestroy(step_exec); step_exec = nullptr; }
         if (loop_exec) { cudaGraphExecDestroy(loop_exec); loop_exec = nullptr; }
@@ -299,11 +303,12 @@ struct wlm_engine {
 
     // WHILE(any pair not done) { body; cond } -- rejection retries and the
     // iteration count live entirely on the device.
-    void build_loop_graph() {
-        if (loop_exec) return;
-        CK(cudaGraphCreate(&loop_graph, 0));
+    // WHILE(any pair of b not done) { attempt(b); cond } -- rejection retries
+    // and the iteration count live entirely on the device.
+    void make_loop_graph(const Batch& b, cudaGraph_t& graph, cudaGraphExec_t& exec, int* kernels) {
+        CK(cudaGraphCreate(&graph, 0));
         cudaGraphConditionalHandle h;
-        CK(cudaGraphConditionalHandleCreate(&h, loop_graph, 1, cudaGraphCondAssignDefault));
+        CK(cudaGraphConditionalHandleCreate(&h, graph, 1, cudaGraphCondAssignDefault));
         alignas(cudaGraphNodeParams) unsigned char raw[sizeof(cudaGraphNodeParams)] = {};
         cudaGraphNodeParams& cp = *reinterpret_cast<cudaGraphNodeParams*>(raw);
         cp.type = cudaGraphNodeTypeConditional;
@@ -311,18 +316,47 @@ struct wlm_engine {
         cp.conditional.type = cudaGraphCondTypeWhile;
         cp.conditional.size = 1;
         cudaGraphNode_t node;
-        CK(cudaGraphAddNode(&node, loop_graph, nullptr, 0, &cp));
+        CK(cudaGraphAddNode(&node, graph, nullptr, 0, &cp));
         cudaGraph_t bodyg = cp.conditional.phGraph_out[0];
         const uint64_t saved = g_kernel_launches;
         CK(cudaStreamBeginCaptureToGraph(ctx->capture, bodyg, nullptr, nullptr, 0,
                                          cudaStreamCaptureModeThreadLocal));
-        body(ctx->capture);
-        body_kernels = (int)(g_kernel_launches - saved);
-        launch_loop_cond(B, h, ctx->capture);
+        attempt(b, ctx->capture);
+        *kernels = (int)(g_kernel_launches - saved);
+        launch_loop_cond(b, h, ctx->capture);
         cudaGraph_t out = nullptr;
         CK(cudaStreamEndCapture(ctx->capture, &out));
         g_kernel_launches = saved;
-        CK(cudaGraphInstantiate(&loop_exec, loop_graph, 0));
+        CK(cudaGraphInstantiate(&exec, graph, 0));
+    }
+    void build_loop_graph() {
+        if (loop_exec) return;
+        make_loop_graph(B, loop_graph, loop_exec, &body_kernels);
+    }
+    // With rejection on, each pair group loops in its own WHILE graph on its
+    // own stream; the groups join when all their pairs are done.
+    void launch_grouped_loop(cudaStream_t s) {
+        const int G = ngroups();
+        if (!group_loop_exec[0]) {
+            if (!fork_ev) CK(cudaEventCreateWithFlags(&fork_ev, cudaEventDisableTiming));
+            for (int gi = 1; gi < G; ++gi) {
+                if (!side[gi]) CK(cudaStreamCreateWithFlags(&side[gi], cudaStreamNonBlocking));
+                if (!join_ev[gi]) CK(cudaEventCreateWithFlags(&join_ev[gi], cudaEventDisableTiming));
+            }
+            int k = 0, total = 0;
+            for (int gi = 0; gi < G; ++gi) {
+                make_loop_graph(group(gi), group_loop_graph[gi], group_loop_exec[gi], &k);
+                total += k;
+            }
+            group_kernels = total;
+        }
+        CK(cudaEventRecord(fork_ev, s));
+        for (int gi = 1; gi < G; ++gi) CK(cudaStreamWaitEvent(side[gi], fork_ev, 0));
+        for (int gi = 0; gi < G; ++gi) CK(cudaGraphLaunch(group_loop_exec[gi], gi == 0 ? s : side[gi]));
+        for (int gi = 1; gi < G; ++gi) {
+            CK(cudaEventRecord(join_ev[gi], side[gi]));
+            CK(cudaStreamWaitEvent(s, join_ev[gi], 0));
+        }
     }
 };
 

@@ -244,7 +244,7 @@ void launch_jacobian_diag(const Batch& b, const LmParams& p, cudaStream_t s) {
 }
 
 void launch_loop_cond(const Batch& b, cudaGraphConditionalHandle h, cudaStream_t s) {
-    k_loop_cond<<<1, 1, 0, s>>>(b.st, b.pairs, h);
+    k_loop_cond<<<1, 1, 0, s>>>(b.st + b.pair0, b.pairs, h);
     ++g_kernel_launches;
 }
 

@@ -310,26 +310,31 @@ def test_degenerate_and_ragged_dims_match_oracle(P, ctx, shape):
     compare_runs(tr, tr_o, aos(warp[0]), u_o, 1e-6, 1e-5)
 
 
-def test_pair_groups_do_not_change_results(P, ctx):
-    """Two pair-group streams (the default) vs one chain: bit-identical warps
-    and traces, with an odd pair count (groups of 2 and 1)."""
-    shape = (20, 24, 28)
-    Fs, Ms = zip(*[O.synth_pair(shape, 300 + s, num_blobs=6, warp_max=2.0)[:2] for s in range(3)])
+@pytest.mark.parametrize("rejection", [0, 1])
+def test_pair_groups_do_not_change_results(P, ctx, rejection):
+    """Pair-group streams (the default: 2) vs one chain: bit-identical warps
+    and traces, with an odd pair count (groups of 2 and 1, or 1, 1, 1), with
+    rejection off (graph streams) and on (one WHILE graph per group)."""
+    shape = (24, 28, 32)
+    Fs, Ms = zip(*[O.synth_pair(shape, 300 + s, num_blobs=10, warp_max=3.0)[:2] for s in range(3)])
     F, M = np.stack(Fs), np.stack(Ms)
-    cfg = P.reg_config(nlevels=1, factors=[1], iters=[12])
+    cfg = P.reg_config(nlevels=1, factors=[1], iters=[40], **{"lm.rejection": rejection, "lm.tau": 0.2})
     out = {}
-    for groups in (1, 2):
+    for groups in (1, 2, 3):
         eng = P.Engine(shape, pairs=3, cfg=cfg, ctx=ctx)
         eng.set_pair_groups(groups)
         eng.load(F, M)
         eng.set_warp(None)
         eng.begin_level(0)
-        eng.iterate(7)
-        eng.iterate(5)
+        eng.iterate(25)
+        eng.iterate(15)
         out[groups] = (eng.get_warp(), [eng.trace(p) for p in range(3)])
         eng.close()
-    assert np.array_equal(out[1][0], out[2][0])
-    assert same_trace(out[1][1], out[2][1]) and len(out[2][1][2]) == 12
+    for groups in (2, 3):
+        assert np.array_equal(out[1][0], out[groups][0])
+        assert same_trace(out[1][1], out[groups][1]) and len(out[groups][1][2]) == 40
+    if rejection:
+        assert sum(t["retries"] for tr in out[2][1] for t in tr) > 0, "should exercise rejections"
     with pytest.raises(P.InvalidArgument):
         P.Engine(shape, pairs=1, cfg=cfg, ctx=ctx).set_pair_groups(5)
 
