@@ -164,7 +164,7 @@ __global__ void k_begin_level(PairState* st, int pairs, int level, int reset_lam
     s.hist_n = 0; s.L1 = 0.0; s.L2 = 0.0;
     s.iter = 0; s.retries = 0; s.done = 0; s.status = 0; s.trace_len = 0; s.attempt = 0;
     s.last_rejected = 0; s.iters_target = INT_MAX; s.level = level;
-    s.max_bits = 0u; s.counter = 0u; s.jac_bits = 0x7f800000;
+    s.max_bits = 0u; s.jac_bits = 0x7f800000;
 }
 
 __global__ void k_set_targets(PairState* st, int pairs, int iters) {

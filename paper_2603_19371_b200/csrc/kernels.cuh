@@ -29,7 +29,6 @@ struct PairState {
     int iters_target;
     int level;
     unsigned max_bits;       // max |dU_s| as ordered bits (K3 -> K4)
-    unsigned counter;        // last-block election counter (K1)
     int jac_bits;            // min det(I + grad eps dU_s), ordered int
     float shift_f, shift_m;  // per-pair intensity shift for the fp32 moments
     double lo_f, hi_f, lo_m, hi_m;  // min / max of F and M (MI normalisation)
