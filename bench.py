@@ -510,6 +510,20 @@ def load_traffic(kernel):
     return None
 
 
+def host_cpu():
+    """nproc and the CPU model of the box (SURVEY §8(d) CPU-baseline note)."""
+    model = "unknown"
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"nproc": os.cpu_count() or 1, "model": model}
+
+
 def cpu_baseline_sample(F, M):
     """Reference CPU path (reference field.cpp primitives + restated LNCC/LM),
     single thread, one LM iteration of one 192^3 pair of the same workload."""
@@ -529,7 +543,8 @@ def cpu_baseline_sample(F, M):
     # count it as 1 iteration (conservative for the CPU)
     return {"value": round(n / dt / 1e9, 6), "unit": "Gvoxel/s", "cores": 1, "kind": kind,
             "sample": f"1 LM iteration (incl. initial residual) of pair 0 at {F.shape[0]}^3, "
-                      f"{dt:.1f} s, single thread (the reference is serial)"}
+                      f"{dt:.1f} s, single thread (the reference is serial)",
+            "host": host_cpu()}
 
 
 # ------------------------------------------------------------- reference ----
@@ -592,7 +607,8 @@ def run_reference(args, rank, world):
         "cpu_baseline": {"value": round(value, 6), "unit": "Gvoxel/s", "cores": pairs * per_pair, "kind": kind,
                          "sample": f"{done} steps x 1 LM iteration (incl. initial residual) on {pairs} "
                                    f"pairs of {n}^3, one registration thread per pair x {per_pair} "
-                                   f"threads inside"},
+                                   f"threads inside",
+                         "host": host_cpu()},
         "e2e": {"value": round(value, 6), "unit": "Gvoxel/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
