@@ -1037,8 +1037,12 @@ __device__ __forceinline__ double border_inv(const double* t, int p, int n, int 
     return p < R ? t[p] : t[R + (n - 1 - p)];
 }
 
+#ifndef WLM_K3_COLUMN_Y
+#define WLM_K3_COLUMN_Y 1
+#endif
 namespace k3 {
 constexpr int TX = 32, TY = 8, NT = 256;
+constexpr bool COLY = WLM_K3_COLUMN_Y;
 template <int R>
 struct Shape {
     static constexpr int IWP = TX + 2 * R;  // halo row (even: 16-byte aligned rows of doubles)
@@ -1046,6 +1050,10 @@ struct Shape {
     static constexpr int NI = IWP * IH;
     static constexpr int SLOTS = (NI + NT - 1) / NT;
     static constexpr int NV = (2 + 2 * R + 1) / 2;  // 16-byte loads per x pair
+    // dynamic shared memory (doubles): s_in[2][3][NI], s_x[2][3][IH*TX],
+    // s_y[2][3][TY*TX] (column y-pass only)
+    static constexpr int IN_D = 2 * 3 * NI, X_D = 2 * 3 * IH * TX, Y_D = COLY ? 2 * 3 * TY * TX : 0;
+    static constexpr size_t BYTES = sizeof(double) * (IN_D + X_D + Y_D);
 };
 }  // namespace k3
 
@@ -1054,8 +1062,10 @@ __global__ void __launch_bounds__(k3::NT, 2) k_step_smooth(Batch b, LmParams p, 
     using S = k3::Shape<R>;
     constexpr int TX = k3::TX, NT = k3::NT, W = 2 * R + 1;
     constexpr int IWP = S::IWP, IH = S::IH, NI = S::NI, SL = S::SLOTS, NV = S::NV;
-    __shared__ __align__(16) double s_in[2][3][NI];
-    __shared__ __align__(16) double s_x[2][3][IH * TX];
+    extern __shared__ __align__(16) double k3_smem[];
+    double* const s_in0 = k3_smem;                 // [buffer][channel][NI]
+    double* const s_x0 = k3_smem + S::IN_D;        // [buffer][channel][IH][TX]
+    double* const s_y0 = s_x0 + S::X_D;            // [buffer][channel][TY][TX]
     __shared__ float s_max[NT / 32];
     __shared__ double s_binv[2 * (R > 0 ? R : 1)];
 
@@ -1173,10 +1183,30 @@ __global__ void __launch_bounds__(k3::NT, 2) k_step_smooth(Batch b, LmParams p, 
     float mx = 0.f;
 
     const int z0 = zb - R, z1 = ze + R;
-    double* in_a = &s_in[0][0][0];  // halo tile of plane p + 2 (written)
-    double* in_b = &s_in[1][0][0];  // halo tile of plane p + 1 (x-passed)
-    double* x_a = &s_x[0][0][0];    // x-passed plane p (y-passed)
-    double* x_b = &s_x[1][0][0];
+    double* in_a = s_in0;              // halo tile of plane p + 2 (written)
+    double* in_b = s_in0 + 3 * NI;     // halo tile of plane p + 1 (x-passed)
+    double* x_a = s_x0;                // x-passed plane p (y-passed)
+    double* x_b = s_x0 + 3 * IH * TX;
+    double* y_a = s_y0;                // column pass: y-passed plane p (read by the ring)
+    double* y_b = s_y0 + 3 * k3::TY * TX;
+    // column y-pass: thread (channel yc, column ox, half yh) of the first 6
+    // warps forms 4 outputs from its column's 4 + 2R x-sums held in
+    // registers, in the same fma order as the per-output 7-tap sum
+    constexpr int YH = k3::TY / 2;
+    const int yc = threadIdx.x >> 6, yh = (threadIdx.x >> 5) & 1;
+    auto y_pass = [&](const double* in, double* out) {
+        if (yc >= 3) return;
+        double v[YH + 2 * R];
+#pragma unroll
+        for (int r = 0; r < YH + 2 * R; ++r) v[r] = in[yc * IH * TX + (yh * YH + r) * TX + ox];
+#pragma unroll
+        for (int o = 0; o < YH; ++o) {
+            double acc = 0.0;
+#pragma unroll
+            for (int d = 0; d < W; ++d) acc = fma(w[d], v[o + d], acc);
+            out[yc * k3::TY * TX + (yh * YH + o) * TX + ox] = acc;
+        }
+    };
     auto ztile = [&](int z) { return tiled && z >= 0 && z < g.nz ? z / tk : 0; };
     load_halo(z0);
     hz = ztile(z0);
@@ -1186,19 +1216,36 @@ __global__ void __launch_bounds__(k3::NT, 2) k_step_smooth(Batch b, LmParams p, 
     store_halo(in_b);
     __syncthreads();
     x_pass(in_a, x_a);
-    load_halo(z0 + 2);
-    __syncthreads();
+    if (k3::COLY) {
+        // deeper prologue: y_a = plane z0, x_b = plane z0+1, in_a = plane z0+2
+        x_pass(in_b, x_b);
+        load_halo(z0 + 2);
+        __syncthreads();
+        y_pass(x_a, y_a);
+        hz = ztile(z0 + 2);
+        store_halo(in_a);
+        load_halo(z0 + 3);
+        __syncthreads();
+    } else {
+        load_halo(z0 + 2);
+        __syncthreads();
+    }
     for (int zbase = z0; zbase < z1; zbase += W) {
 #pragma unroll
         for (int rs = 0; rs < W; ++rs) {
             const int zi = zbase + rs;
             if (zi < z1) {
+                if (k3::COLY) {
 #pragma unroll
-                for (int c = 0; c < 3; ++c) {
-                    double s = 0.0;
+                    for (int c = 0; c < 3; ++c) ring[rs][c] = y_a[c * k3::TY * TX + oy * TX + ox];
+                } else {
 #pragma unroll
-                    for (int d = 0; d < W; ++d) s = fma(w[d], x_a[c * IH * TX + (oy + d) * TX + ox], s);
-                    ring[rs][c] = s;
+                    for (int c = 0; c < 3; ++c) {
+                        double s = 0.0;
+#pragma unroll
+                        for (int d = 0; d < W; ++d) s = fma(w[d], x_a[c * IH * TX + (oy + d) * TX + ox], s);
+                        ring[rs][c] = s;
+                    }
                 }
                 const int zo = zi - R;
                 if (zo >= zb && own) {
@@ -1215,10 +1262,19 @@ __global__ void __launch_bounds__(k3::NT, 2) k_step_smooth(Batch b, LmParams p, 
                         mx = fmaxf(mx, fabsf(v));
                     }
                 }
-                x_pass(in_b, x_b);
-                hz = ztile(zi + 2);
-                store_halo(in_a);
-                load_halo(zi + 3);
+                if (k3::COLY) {
+                    y_pass(x_b, y_b);
+                    x_pass(in_a, x_a);
+                    hz = ztile(zi + 3);
+                    store_halo(in_b);
+                    load_halo(zi + 4);
+                    double* t = y_a; y_a = y_b; y_b = t;
+                } else {
+                    x_pass(in_b, x_b);
+                    hz = ztile(zi + 2);
+                    store_halo(in_a);
+                    load_halo(zi + 3);
+                }
                 double* t = in_a; in_a = in_b; in_b = t;
                 t = x_a; x_a = x_b; x_b = t;
                 __syncthreads();
@@ -1678,11 +1734,21 @@ void launch_step_smooth(const Batch& b, const LmParams& p, cudaStream_t s) {
     const LaunchShape sh = shape_for(b.g, b.pairs, k3::TY, b.ctas_per_sm);
     dim3 grid = sh.grid();
     grid.z = b.pairs;
-    if (p.optimizer == WLM_OPT_LM && p.tile_k > 1) {
-        WLM_DISPATCH_R(p.Ru, (k_step_smooth<RR, true><<<grid, k3::NT, 0, s>>>(b, p, sh.chunk_len)));
-    } else {
-        WLM_DISPATCH_R(p.Ru, (k_step_smooth<RR, false><<<grid, k3::NT, 0, s>>>(b, p, sh.chunk_len)));
-    }
+    WLM_DISPATCH_R(p.Ru, ({
+        static std::atomic<unsigned long long> attr{0ull};  // per device
+        const unsigned long long bit = device_bit();
+        if (!(attr.load() & bit)) {
+            cudaFuncSetAttribute(k_step_smooth<RR, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)k3::Shape<RR>::BYTES);
+            cudaFuncSetAttribute(k_step_smooth<RR, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)k3::Shape<RR>::BYTES);
+            attr.fetch_or(bit);
+        }
+        if (p.optimizer == WLM_OPT_LM && p.tile_k > 1)
+            k_step_smooth<RR, true><<<grid, k3::NT, k3::Shape<RR>::BYTES, s>>>(b, p, sh.chunk_len);
+        else
+            k_step_smooth<RR, false><<<grid, k3::NT, k3::Shape<RR>::BYTES, s>>>(b, p, sh.chunk_len);
+    }));
     ++g_kernel_launches;
 }
 
