@@ -114,8 +114,16 @@ def dist_init(n_gpus):
     if world > 1:
         import torch
         import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # WLM_BENCH_BACKEND=gloo exercises the multi-rank path on fewer GPUs
+        # than ranks (host barrier and max; ranks share devices round-robin,
+        # so the timings are not scaling numbers)
+        if os.environ.get("WLM_BENCH_BACKEND", "nccl") == "gloo":
+            local = local % max(1, torch.cuda.device_count())
+            torch.cuda.set_device(local)
+            dist.init_process_group("gloo")
+        else:
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     return rank, world, local
 
 

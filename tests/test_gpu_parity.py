@@ -629,3 +629,27 @@ def test_bench_json_contract():
     # K2, K3, K4, K1a, K1b, plane sums, K5 per attempt and pair group (2 groups of 1 pair
     # here), plus the iteration-target kernel of the one iterate() call
     assert line["gpu_launches"] == 7 * 2 * 3 + 1
+
+
+def test_bench_two_ranks_under_torchrun():
+    """The driver's N > 1 launch (torchrun, one process per rank) end to end:
+    one JSON line from rank 0 with the aggregate over ranks.  This box has
+    one GPU, so the two ranks share it over a gloo group
+    (WLM_BENCH_BACKEND=gloo); the value is not a scaling number."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, WLM_BENCH_BACKEND="gloo")
+    out = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                          "--master-addr", "127.0.0.1", "--master-port", "29533",
+                          os.path.join(root, "bench.py"), "--gpus", "2", "--steps", "3", "--warmup", "3",
+                          "--size", "64", "--pairs-per-gpu", "2", "--no-cpu-baseline", "--no-extra",
+                          "--e2e-iters", "2"], capture_output=True, text=True, timeout=900, env=env)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [ln for ln in out.stdout.strip().splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    line = json.loads(lines[0])
+    assert line["n_gpus"] == 2 and line["config"]["global_batch"] == 4 and line["value"] > 0
+    assert line["e2e"]["value"] > 0 and line["gpu_launches"] == 7 * 2 * 3 + 1
