@@ -94,8 +94,8 @@ wlm_status engine_init(wlm_engine* e, wlm_ctx* ctx, wlm_dims d, int pairs, const
     P.mi_sigma = c->mi_sigma;
     P.Ru = smooth_radius(c->sigma_update);
     P.Rw = smooth_radius(c->sigma_warp);
-    if (P.Ru > 3 || P.Rw > 3) {
-        set_err(ctx, "fused smoothing supports sigma <= 1 (radius <= 3)");
+    if (P.Ru > 6 || P.Rw > 6) {
+        set_err(ctx, "fused smoothing supports sigma <= 2 (radius <= 6)");
         return WLM_UNSUPPORTED;
     }
     fill_half_kernel(c->sigma_update, P.Ru, P.wu, &P.wu_full);

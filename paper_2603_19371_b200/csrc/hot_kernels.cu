@@ -1143,10 +1143,10 @@ __global__ void __launch_bounds__(k3::NT, 2) k_step_smooth(Batch b, LmParams p, 
 #pragma unroll
     for (int d = 0; d < W; ++d) w[d] = p.wud[d < R ? R - d : d - R];
 
-    // x-pass item: row xr, pair xj (outputs x = 2xj, 2xj + 1)
-    const int xr = threadIdx.x >> 4, xj = threadIdx.x & 15;
-    auto x_pass = [&](const double* in, double* out) {
-        if (xr >= IH) return;
+    // x-pass item: row xr, pair xj (outputs x = 2xj, 2xj + 1); NT / 16 rows
+    // per sweep, so radii with IH > 16 rows (R > 4) take a second sweep
+    const int xr0 = threadIdx.x >> 4, xj = threadIdx.x & 15;
+    auto x_row = [&](const double* in, double* out, int xr) {
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
             double v[2 * NV];
@@ -1163,6 +1163,13 @@ __global__ void __launch_bounds__(k3::NT, 2) k_step_smooth(Batch b, LmParams p, 
                 o1 = fma(w[d], v[d + 1], o1);
             }
             *reinterpret_cast<double2*>(out + c * IH * TX + xr * TX + 2 * xj) = make_double2(o0, o1);
+        }
+    };
+    auto x_pass = [&](const double* in, double* out) {
+        if (IH <= NT / 16) {
+            if (xr0 < IH) x_row(in, out, xr0);
+        } else {
+            for (int xr = xr0; xr < IH; xr += NT / 16) x_row(in, out, xr);
         }
     };
 
@@ -1653,6 +1660,9 @@ __global__ void __launch_bounds__(k4::NT, 1) k_compose_smooth(Batch b, LmParams 
         case 1: { constexpr int RR = 1; CALL; } break; \
         case 2: { constexpr int RR = 2; CALL; } break; \
         case 3: { constexpr int RR = 3; CALL; } break; \
+        case 4: { constexpr int RR = 4; CALL; } break; \
+        case 5: { constexpr int RR = 5; CALL; } break; \
+        case 6: { constexpr int RR = 6; CALL; } break; \
         default: break;                                \
     }
 

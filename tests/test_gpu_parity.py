@@ -653,3 +653,52 @@ def test_bench_two_ranks_under_torchrun():
     line = json.loads(lines[0])
     assert line["n_gpus"] == 2 and line["config"]["global_batch"] == 4 and line["value"] > 0
     assert line["e2e"]["value"] > 0 and line["gpu_launches"] == 7 * 2 * 3 + 1
+
+
+def _fuzz_case(i):
+    """Seeded random (shape, config) for the engine-vs-oracle sweep."""
+    rng = np.random.default_rng(1000 + i)
+    shape = tuple(int(v) for v in rng.integers(6, 26, size=3))
+    metric = int(rng.choice([0, 0, 1, 2])) if min(shape) > 4 else int(rng.choice([1, 2]))
+    optimizer = int(rng.choice([0, 0, 0, 1, 2, 3] if metric == 1 else [0, 0, 0, 1, 2]))
+    kw = dict(nlevels=1, factors=[1], iters=[8], metric=metric, optimizer=optimizer,
+              sigma_update=float(rng.choice([0.0, 0.7, 1.0, 1.0, 1.3, 1.5, 2.0])),
+              sigma_warp=float(rng.choice([0.0, 0.5, 0.5, 0.8, 1.6])))
+    if optimizer == 0:
+        kw["lm.rejection"] = int(rng.integers(0, 2))
+        kw["lm.tau"] = float(rng.choice([0.0, 0.2, 1.0]))
+        kw["lm.lambda0"] = float(rng.choice([1e-4, 0.006, 0.5]))
+        kw["lm.tile_size"] = int(rng.choice([1, 1, 2, 3]))
+    if metric == 2:
+        kw["mi_bins"] = int(rng.choice([8, 16, 32]))
+    warp_max = float(rng.uniform(0.5, min(shape) / 4 - 0.1))
+    return shape, kw, warp_max, int(rng.integers(0, 1 << 30))
+
+
+@pytest.mark.parametrize("case", range(24))
+def test_random_configs_match_storage_oracle(P, ctx, case):
+    """Seeded sweep over shapes (ragged, thin), losses, optimizers, rejection,
+    damping, tile sizes and smoothing sigmas: the engine against the
+    fp32-storage oracle at the storage bar (loss 1e-6, decisions and lambda
+    identical, warp 1e-5)."""
+    shape, kw, warp_max, seed = _fuzz_case(case)
+    for attempt in range(6):  # thin volumes: halve warp_max until a diffeomorphic draw
+        try:
+            F, M, _ = O.synth_pair(shape, seed, num_blobs=6, warp_max=warp_max / 2 ** attempt)
+            break
+        except ValueError:
+            continue
+    else:
+        raise AssertionError("synth: no positive-Jacobian draw")
+    warp, (tr,), _ = run_engine(P, ctx, F, M, P.reg_config(**kw), 8)
+    rc, u_o, _, tr_o = oracle_level(F, M, O.default_config(**kw), 8, "fp32")
+    assert rc == 0
+    compare_runs(tr, tr_o, aos(warp[0]), u_o, 1e-6, 1e-5)
+
+
+def test_smoothing_radius_limit(P, ctx):
+    """The fused smoothing kernels are instantiated for radius <= 6
+    (sigma <= 2); larger sigmas are refused, not silently skipped."""
+    P.Engine((8, 8, 8), 1, P.reg_config(sigma_update=2.0, sigma_warp=2.0), ctx=ctx).close()
+    with pytest.raises(P.WlmError):
+        P.Engine((8, 8, 8), 1, P.reg_config(sigma_update=2.1), ctx=ctx)
