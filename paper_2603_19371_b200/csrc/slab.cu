@@ -103,7 +103,14 @@ namespace {
 
 int cdiv_host(int a, int b) { return (a + b - 1) / b; }
 
-constexpr int kHalo = 4;  // >= max(R_u, R_w + 1, 2) for sigma <= 1
+constexpr int kHalo = 4;  // minimum halo depth: >= max(R_u, R_w + 1, 2) for sigma <= 1
+
+// Halo planes a slab keeps: K3 reads g R_u planes out, K4 composes R_w
+// planes out from a warp ring one plane wider, K1 reads Mw 2 planes out.
+int slab_halo(int Ru, int Rw) { return std::max(kHalo, std::max(Ru, Rw + 1)); }
+int slab_halo(const wlm_reg_config* cfg) {
+    return slab_halo(smooth_radius(cfg->sigma_update), smooth_radius(cfg->sigma_warp));
+}
 
 enum Buffer { BUF_G = 0, BUF_V = 1, BUF_U = 2, BUF_ABE = 3, BUF_TM = 4 };
 
@@ -511,7 +518,7 @@ wlm_status make_group(wlm_ctx* ctx, wlm_dims d, int nslabs, int first, int count
             int zs, ze;
             const int tk = std::max(1, cfg->lm.tile_size);
             partition(d.nz, nslabs, k, &zs, &ze, tk);
-            e->g = make_slab_geo(d, zs, ze, kHalo);
+            e->g = make_slab_geo(d, zs, ze, slab_halo(e->P.Ru, e->P.Rw));
             grp->attach(e);
             grp->plan.push_back(slab_plan(d, nslabs, k, e->P.Ru, e->P.Rw, tk));
             hst.push_back(e->st.p);
@@ -541,7 +548,8 @@ wlm_status check_split(wlm_ctx* ctx, wlm_dims d, int nslabs, const wlm_reg_confi
     // every slab (tile-aligned when tiled) holds at least the halo depth and,
     // with tiles, the R_u + k planes its halo tiles can reach into
     const int tk = std::max(1, cfg->lm.tile_size);
-    const int need = tk > 1 ? std::max(kHalo, smooth_radius(cfg->sigma_update) + tk) : kHalo;
+    const int halo = slab_halo(cfg);
+    const int need = tk > 1 ? std::max(halo, smooth_radius(cfg->sigma_update) + tk) : halo;
     for (int k = 0; k < nslabs; ++k) {
         int zs, ze;
         partition(d.nz, nslabs, k, &zs, &ze, tk);
@@ -567,7 +575,7 @@ wlm_status wlm_slab_partition(int nz, int nslabs, int slab, int* zs, int* ze) {
 wlm_status wlm_slab_halo_plan(wlm_dims d, int nslabs, int slab, const wlm_reg_config* cfg, wlm_halo_xfer* rows,
                               size_t cap, size_t* len) {
     if (!cfg || !len || nslabs < 1 || slab < 0 || slab >= nslabs || !valid_dims(d)) return WLM_INVALID_ARG;
-    if (d.nz / nslabs < kHalo) return WLM_INVALID_ARG;
+    if (d.nz / nslabs < slab_halo(cfg)) return WLM_INVALID_ARG;
     const auto p = slab_plan(d, nslabs, slab, smooth_radius(cfg->sigma_update), smooth_radius(cfg->sigma_warp),
                              std::max(1, cfg->lm.tile_size));
     *len = p.size();

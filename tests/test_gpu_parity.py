@@ -432,14 +432,15 @@ def run_slabs(P, ctx, F, M, cfg, iters, nslabs):
 
 
 @pytest.mark.parametrize("extra", [{}, {"lm.rejection": 1, "lm.tau": 0.2, "log_jacobian": 1},
-                                   {"optimizer": 1}])
+                                   {"optimizer": 1}, {"sigma_update": 2.0, "sigma_warp": 1.6}])
 def test_slab_group_is_bit_identical_to_single_domain(P, ctx, extra):
     """Config 5 decomposition: 1, 2, 3 and 5 z-slabs (uneven splits) give the
     single-domain engine's losses, decisions, lambda and warp bit for bit."""
     F, M, _ = O.synth_pair((20, 24, 28), 21, num_blobs=8, warp_max=2.5)
     cfg = P.reg_config(nlevels=1, factors=[1], iters=[12], **extra)
     w1, (t1,), (s1,) = run_engine(P, ctx, F, M, cfg, 12)
-    for ns in (1, 2, 3, 5):
+    # wide kernels (radius 6 / 5) need 6 halo planes: at most 3 slabs of 20
+    for ns in ((1, 2, 3) if "sigma_warp" in extra else (1, 2, 3, 5)):
         w, t, s = run_slabs(P, ctx, F, M, cfg, 12, ns)
         assert same_trace(t, t1), ns
         assert np.array_equal(w, w1[0]), (ns, float(np.abs(w - w1[0]).max()))
