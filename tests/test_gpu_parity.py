@@ -703,3 +703,31 @@ def test_smoothing_radius_limit(P, ctx):
     P.Engine((8, 8, 8), 1, P.reg_config(sigma_update=2.0, sigma_warp=2.0), ctx=ctx).close()
     with pytest.raises(P.WlmError):
         P.Engine((8, 8, 8), 1, P.reg_config(sigma_update=2.1), ctx=ctx)
+
+
+@pytest.mark.parametrize("case", range(12))
+def test_random_configs_slab_invariance(P, ctx, case):
+    """The same seeded sweep through z-slab groups: any feasible slab count
+    reproduces the single-domain engine bit for bit."""
+    shape, kw, warp_max, seed = _fuzz_case(100 + case)
+    shape = (max(shape[0], 24),) + shape[1:]  # room for >= 2 slabs of the widest halo + tile
+    for attempt in range(6):
+        try:
+            F, M, _ = O.synth_pair(shape, seed, num_blobs=6, warp_max=warp_max / 2 ** attempt)
+            break
+        except ValueError:
+            continue
+    else:
+        raise AssertionError("synth: no positive-Jacobian draw")
+    cfg = P.reg_config(**kw)
+    w1, (t1,), _ = run_engine(P, ctx, F, M, cfg, 8)
+    tested = 0
+    for ns in (2, 3, 4):
+        try:
+            w, t, _ = run_slabs(P, ctx, F, M, cfg, 8, ns)
+        except P.InvalidArgument:
+            continue  # slabs thinner than the halo / tile: refused by design
+        assert same_trace(t, t1), (ns, kw)
+        assert np.array_equal(w, w1[0]), (ns, kw)
+        tested += 1
+    assert tested > 0
