@@ -731,3 +731,34 @@ def test_random_configs_slab_invariance(P, ctx, case):
         assert np.array_equal(w, w1[0]), (ns, kw)
         tested += 1
     assert tested > 0
+
+
+@pytest.mark.parametrize("case", range(10))
+def test_random_pyramids_match_storage_oracle(P, ctx, case):
+    """Seeded random pyramids through wlm_register (levels, warp inheritance,
+    lambda carry, every loss / optimizer of the sweep) against the
+    fp32-storage oracle's register, whole trace at the storage bar."""
+    shape, kw, warp_max, seed = _fuzz_case(200 + case)
+    rng = np.random.default_rng(300 + case)
+    shape = tuple(max(s, 12) for s in shape)
+    sched = [[2, 1], [3, 1], [4, 2, 1]][int(rng.integers(0, 3))]
+    kw = dict(kw, nlevels=len(sched), factors=sched, iters=[int(rng.integers(3, 9)) for _ in sched])
+    if kw["metric"] == 0 and any(-(-s // sched[0]) <= 4 for s in shape):
+        kw["metric"] = 1  # the coarsest level must fit an LNCC window
+        if kw["optimizer"] == 3:
+            kw["optimizer"] = 0
+    for attempt in range(6):
+        try:
+            F, M, _ = O.synth_pair(shape, seed, num_blobs=6, warp_max=warp_max / 2 ** attempt)
+            break
+        except ValueError:
+            continue
+    else:
+        raise AssertionError("synth: no positive-Jacobian draw")
+    res = P.register(F, M, P.reg_config(**kw), ctx=ctx)
+    with O.fp32_storage():
+        rc, w_s, tr_s, _ = O.register(F, M, O.default_config(**kw))
+    assert rc == 0 and len(res.loss_trace) == len(tr_s) == sum(kw["iters"])
+    for a, b in zip(res.loss_trace, tr_s):
+        assert (a.level, a.iter) == (b.level, b.iter)
+    compare_runs(res.loss_trace, tr_s, res.final_warp, w_s, 1e-6, 1e-5)
