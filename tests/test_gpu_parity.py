@@ -762,3 +762,34 @@ def test_random_pyramids_match_storage_oracle(P, ctx, case):
     for a, b in zip(res.loss_trace, tr_s):
         assert (a.level, a.iter) == (b.level, b.iter)
     compare_runs(res.loss_trace, tr_s, res.final_warp, w_s, 1e-6, 1e-5)
+
+
+@pytest.mark.parametrize("case", range(12))
+def test_random_field_ops_match_oracle(P, ctx, case):
+    """Seeded random shapes, fields and sigmas through the host-buffer
+    mirrors of field.hpp and the SPEC residuals, against the oracle."""
+    rng = np.random.default_rng(500 + case)
+    shape = tuple(int(v) for v in rng.integers(5, 20, size=3))
+    u = smooth_field(shape, 600 + case, sigma=1.5, amp=float(rng.uniform(0.3, 3.0)))
+    v = smooth_field(shape, 700 + case, sigma=1.0, amp=1.0)
+    u = u.astype(np.float32).astype(np.float64)
+    v = v.astype(np.float32).astype(np.float64)
+    eps = float(rng.uniform(0.05, 0.4))
+    scale = max(np.abs(u).max(), np.abs(v).max())
+    assert np.abs(P.compose_warp(u, v, eps, ctx=ctx) - O.compose_warp(u, v, eps)).max() < 2e-5 * scale
+    sig = float(rng.choice([0.3, 0.5, 1.0, 1.7, 2.5]))
+    assert np.abs(P.gaussian_smooth(u, sig, ctx=ctx) - O.gaussian_smooth(u, sig)).max() < 2e-6 * scale
+    assert P.max_abs_component(u, ctx=ctx) == pytest.approx(O.max_abs_component(u), rel=1e-7)
+    assert P.jacobian_det_min(u, ctx=ctx) == pytest.approx(O.jacobian_det_min(u), abs=2e-5)
+    F = O.gaussian_smooth(rng.normal(size=shape), 1.0).astype(np.float32).astype(np.float64)
+    M = O.gaussian_smooth(rng.normal(size=shape), 1.0).astype(np.float32).astype(np.float64)
+    r_o, g_o = O.residual_mse(F, M, u)
+    rep = P.residual_mse(F, M, u, ctx=ctx)
+    assert abs(rep.r - r_o) <= 1e-5 * abs(r_o) and rel(rep.g, g_o) < 1e-4
+    r_o, g_o = O.residual_mi(F, M, u, bins=16, sigma=1.0)[:2]
+    rep = P.residual_mi(F, M, u, bins=16, sigma=1.0, ctx=ctx)
+    assert abs(rep.r - r_o) <= 1e-5 * abs(r_o) and rel(rep.g, g_o) < 1e-4
+    if min(shape) > 4:
+        r_o, g_o, _ = O.residual_lncc(F, M, u)
+        rep = P.residual_lncc(F, M, u, ctx=ctx)
+        assert abs(rep.r - r_o) <= 1e-5 * abs(r_o) and rel(rep.g, g_o) < 1e-4
