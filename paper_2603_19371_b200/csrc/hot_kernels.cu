@@ -1,11 +1,16 @@
 // hot_kernels.cu -- the kernels of one LM attempt.
 //
-//   K1a k_warp_moving    Mw = M(x + u) in fp64 (flat gather kernel)
-//   K1b k_lncc_fwd       LNCC window moments -> rho, A, B, E; per-plane sum(rho)
+//   K1a k_warp_moving    Mw = M(x + u) and grad M(x + u) in fp64 (flat gather kernel)
+//   K1b k_lncc_fwd       LNCC window moments -> rho, A, B, E; sum(rho) per (plane, tile, warp)
+//       k_plane_sums     per-plane sum(rho), one CTA per plane, fixed order
 //   K5  k_finalize       sum(rho) in z order -> r; loss/damping/rejection state
-//   K2  k_lncc_bwd       adjoint window sums -> g
-//   K3  k_step_smooth    LM step + Gaussian(sigma_update) + max|.|
-//   K4  k_compose_smooth compositive resample + Gaussian(sigma_warp)
+//   K2  k_lncc_bwd       adjoint window sums -> g (F, Mw, grad M staged by cp.async)
+//   K3  k_step_smooth    LM step + Gaussian(sigma_update) + max|.| (column y-pass)
+//   K4  k_compose_smooth compositive resample (TMA-staged warp ring) + Gaussian(sigma_warp)
+//   MSE / MI: k_mse_fwd, k_mse_grad, k_mi_hist, k_mi_finalize, k_mi_grad
+//
+// The engine launches these per pair group (internal.cuh): a Batch view with
+// pair0 / pairs, one stream of attempt graphs per group.
 //
 // Schedule of the stencil kernels (hot.cuh): a CTA owns a 32 x 8 column of
 // output voxels and a chunk of the rank's owned z planes.  Per input plane it
