@@ -793,3 +793,32 @@ def test_random_field_ops_match_oracle(P, ctx, case):
         r_o, g_o, _ = O.residual_lncc(F, M, u)
         rep = P.residual_lncc(F, M, u, ctx=ctx)
         assert abs(rep.r - r_o) <= 1e-5 * abs(r_o) and rel(rep.g, g_o) < 1e-4
+
+
+@pytest.mark.parametrize("groups", [1, 2])
+def test_nonfinite_pair_does_not_disturb_the_batch(P, ctx, groups):
+    """A pair whose moving image holds a NaN aborts alone (its
+    state reports the non-finite loss) while the other pairs of the batch run
+    to the end bit-identically to a batch without it."""
+    shape = (20, 24, 28)
+    Fs, Ms = zip(*[O.synth_pair(shape, 800 + s, num_blobs=6, warp_max=2.0)[:2] for s in range(3)])
+    F, M = np.stack(Fs), np.stack(Ms).copy()
+    cfg = P.reg_config(nlevels=1, factors=[1], iters=[10])
+    ref, ref_tr = {}, {}
+    for p in (0, 2):
+        w, (tr,), _ = run_engine(P, ctx, F[p], M[p], cfg, 10)
+        ref[p], ref_tr[p] = w[0], tr
+    M[1, 5, 6, 7] = np.nan
+    eng = P.Engine(shape, pairs=3, cfg=cfg, ctx=ctx)
+    eng.set_pair_groups(groups)
+    eng.load(F, M)
+    eng.set_warp(None)
+    eng.begin_level(0)
+    eng.iterate(10)
+    warps = eng.get_warp()
+    for p in (0, 2):
+        assert np.array_equal(warps[p], ref[p]) and same_trace(eng.trace(p), ref_tr[p])
+    with pytest.raises(P.NonFiniteLoss):
+        eng.state(1)
+    assert len(eng.trace(1)) < 10
+    eng.close()
