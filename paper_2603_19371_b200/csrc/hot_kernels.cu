@@ -1330,7 +1330,11 @@ struct Shape {
     static constexpr int XO = 4;
     static constexpr int UW = (TX + R + 1 + XO + 3) / 4 * 4, UH = TY + 2 * R + 2, UN = UW * UH;
     static constexpr int IWP = UW, NI = IWP * IH;
-    static constexpr int SL = (NI + NT - 1) / NT, USL = (UN + NT - 1) / NT;
+    // composed items enumerated compactly (IW per row); the last, partial
+    // slot goes to the highest threads, away from the x-pass threads (the
+    // lowest 16 * IH), so few warps carry both
+    static constexpr int NIV = IW * IH;
+    static constexpr int SL = (NIV + NT - 1) / NT, USL = (UN + NT - 1) / NT;
     static constexpr int NV = (2 + 2 * R + 1) / 2;
     // ring slot: [3][UH][UW] fp32 (one TMA box), 128-byte aligned
     static constexpr int SLOT = (3 * UN + 31) / 32 * 32;
@@ -1419,16 +1423,19 @@ __global__ void __launch_bounds__(k4::NT, 1) k_compose_smooth(Batch b, LmParams 
         const int gx = x0 - S::XO + idx % UW, gy = y0 - R - 1 + idx / UW;
         uoff[s] = (idx < UN && gx >= 0 && gx < g.nx && gy >= 0 && gy < g.ny) ? gx + g.nx * gy : -1;
     }
-    // composed items (tile origin x0 - R, y0 - R)
-    int voff[SL], vx[SL], vy[SL];
+    // composed items (tile origin x0 - R, y0 - R): slot s of this thread is
+    // item j (row j / IW, column j % IW) at tile index iidx[s] (-1: none)
+    int voff[SL], vx[SL], vy[SL], iidx[SL];
 #pragma unroll
     for (int s = 0; s < SL; ++s) {
-        const int idx = threadIdx.x + s * NT;
-        vx[s] = x0 - R + idx % IWP;
-        vy[s] = y0 - R + idx / IWP;
-        voff[s] = (idx < NI && idx % IWP < S::IW && vx[s] >= 0 && vx[s] < g.nx && vy[s] >= 0 && vy[s] < g.ny)
-                      ? vx[s] + g.nx * vy[s]
-                      : -1;
+        constexpr int REM = S::NIV - (SL - 1) * NT;  // items of the last slot
+        const int j = s < SL - 1 ? threadIdx.x + s * NT
+                                 : ((int)threadIdx.x >= NT - REM ? (SL - 1) * NT + threadIdx.x - (NT - REM) : -1);
+        const int row = j / S::IW, col = j % S::IW;
+        iidx[s] = j >= 0 ? row * IWP + col : -1;
+        vx[s] = x0 - R + col;
+        vy[s] = y0 - R + row;
+        voff[s] = (j >= 0 && vx[s] >= 0 && vx[s] < g.nx && vy[s] >= 0 && vy[s] < g.ny) ? vx[s] + g.nx * vy[s] : -1;
     }
     float pu[USL][3], pv[SL][3];
     auto load_u = [&](int z) {
@@ -1483,8 +1490,8 @@ __global__ void __launch_bounds__(k4::NT, 1) k_compose_smooth(Batch b, LmParams 
         const bool zin = z >= 0 && z < g.nz;
 #pragma unroll
         for (int s = 0; s < SL; ++s) {
-            const int idx = threadIdx.x + s * NT;
-            if (idx >= NI || idx % IWP >= S::IW) continue;
+            const int idx = iidx[s];
+            if (idx < 0) continue;
             double o3[3] = {0.0, 0.0, 0.0};
             if (zin && voff[s] >= 0) {
                 const double dx = eps * pv[s][0], dy = eps * pv[s][1], dz = eps * pv[s][2];
