@@ -159,6 +159,16 @@ __device__ void finalize_pair(PairState* st, const LmParams& p, int mode, double
     st->jac_bits = 0x7f800000;
 }
 
+// Item of slot s of this thread when NI halo items are dealt over NT
+// threads in SL = ceil(NI / NT) slots: full slots in thread order, the
+// partial last slot on the highest threads (the x-passes run on the lowest
+// threads), -1 for none.  Constant arguments fold at compile time.
+__device__ __forceinline__ int halo_item(int s, int SL, int NI, int NT) {
+    if (s < SL - 1) return (int)threadIdx.x + s * NT;
+    const int rem = NI - (SL - 1) * NT;
+    return (int)threadIdx.x >= NT - rem ? (SL - 1) * NT + (int)threadIdx.x - (NT - rem) : -1;
+}
+
 // Block-wide fixed-order double sum (result valid in thread 0).
 static __device__ double block_sum(double v, double* red) {
     v = warp_sum(v);
@@ -838,9 +848,9 @@ __global__ void __launch_bounds__(k2::NT, WLM_K2_MIN_BLOCKS) k_lncc_bwd(Batch b,
     int hoff[SL];
 #pragma unroll
     for (int s = 0; s < SL; ++s) {
-        const int idx = threadIdx.x + s * NT;
+        const int idx = halo_item(s, SL, NI, NT);
         const int gx = x0 - R + idx % IWP, gy = y0 - R + idx / IWP;
-        hoff[s] = (idx < NI && gx >= 0 && gx < g.nx && gy >= 0 && gy < g.ny) ? gx + g.nx * gy : -1;
+        hoff[s] = (idx >= 0 && gx >= 0 && gx < g.nx && gy >= 0 && gy < g.ny) ? gx + g.nx * gy : -1;
     }
     // halo registers, HALO_DEPTH planes in flight: h[0] is stored this
     // phase, the rest were loaded in earlier phases and move down after it
@@ -865,8 +875,8 @@ __global__ void __launch_bounds__(k2::NT, WLM_K2_MIN_BLOCKS) k_lncc_bwd(Batch b,
     auto store_halo = [&](double* dst) {
 #pragma unroll
         for (int s = 0; s < SL; ++s) {
-            const int idx = threadIdx.x + s * NT;
-            if (idx >= NI) continue;
+            const int idx = halo_item(s, SL, NI, NT);
+            if (idx < 0) continue;
             dst[idx] = (double)ha[0][s];
             dst[NI + idx] = (double)hb[0][s];
             dst[2 * NI + idx] = he[0][s];
@@ -1093,10 +1103,10 @@ __global__ void __launch_bounds__(k3::NT, 2) k_step_smooth(Batch b, LmParams p, 
     int hoff[SL];
 #pragma unroll
     for (int s = 0; s < SL; ++s) {
-        const int idx = threadIdx.x + s * NT;
+        const int idx = halo_item(s, SL, NI, NT);
         const int ix = idx % IWP, iy = idx / IWP;
         const int gx = x0 - R + ix, gy = y0 - R + iy;
-        hoff[s] = (idx < NI && gx >= 0 && gx < g.nx && gy >= 0 && gy < g.ny) ? gx + g.nx * gy : -1;
+        hoff[s] = (idx >= 0 && gx >= 0 && gx < g.nx && gy >= 0 && gy < g.ny) ? gx + g.nx * gy : -1;
     }
     float hg[SL][3];
     auto load_halo = [&](int z) {
@@ -1119,7 +1129,7 @@ __global__ void __launch_bounds__(k3::NT, 2) k_step_smooth(Batch b, LmParams p, 
     int htile[SL];  // (y tile) * tkx + x tile of each halo item
 #pragma unroll
     for (int s = 0; s < SL; ++s) {
-        const int idx = threadIdx.x + s * NT;
+        const int idx = halo_item(s, SL, NI, NT);
         const int gx = x0 - R + idx % IWP, gy = y0 - R + idx / IWP;
         htile[s] = (tiled && hoff[s] >= 0) ? (gy / tk) * b.tkx + gx / tk : 0;
     }
@@ -1127,8 +1137,8 @@ __global__ void __launch_bounds__(k3::NT, 2) k_step_smooth(Batch b, LmParams p, 
     auto store_halo = [&](double* dst) {
 #pragma unroll
         for (int s = 0; s < SL; ++s) {
-            const int idx = threadIdx.x + s * NT;
-            if (idx >= NI) continue;
+            const int idx = halo_item(s, SL, NI, NT);
+            if (idx < 0) continue;
             const double a = hg[s][0], bb = hg[s][1], c = hg[s][2];
             if (tiled) {
                 const double* M6 = TM + ((long long)hz * b.tkx * b.tky + htile[s]) * 6;
@@ -1430,7 +1440,7 @@ __global__ void __launch_bounds__(k4::NT, 1) k_compose_smooth(Batch b, LmParams 
     for (int s = 0; s < SL; ++s) {
         constexpr int REM = S::NIV - (SL - 1) * NT;  // items of the last slot
         const int j = s < SL - 1 ? threadIdx.x + s * NT
-                                 : ((int)threadIdx.x >= NT - REM ? (SL - 1) * NT + threadIdx.x - (NT - REM) : -1);
+                                 : ((int)threadIdx.x >= NT - REM ? (SL - 1) * NT + (int)threadIdx.x - (NT - REM) : -1);
         const int row = j / S::IW, col = j % S::IW;
         iidx[s] = j >= 0 ? row * IWP + col : -1;
         vx[s] = x0 - R + col;
