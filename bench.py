@@ -329,6 +329,10 @@ def run_ours(args, rank, world, local):
                      "algorithmic_bytes_per_voxel": KERNEL_BYTES[dom],
                      "design_bytes_per_voxel": DESIGN_BYTES[dom],
                      "per_kernel_ms": {k: round(v, 4) for k, v in per_kernel.items()},
+                     # every stage against the same peak: canonical bytes / time
+                     "per_kernel_frac": {k: round(KERNEL_BYTES[k] * launch_vox / (v * 1e-3) / 1e9 / hbm, 4)
+                                         for k, v in per_kernel.items()},
+                     "per_kernel_traffic": {k: load_traffic(k) for k in per_kernel},
                      "iteration_frac": round(it_frac, 4),
                      "iteration_bytes_per_voxel": BYTES_PER_VOXEL_ITER},
         "e2e": {"value": round(e2e_val, 4), "unit": "Gvoxel/s",
