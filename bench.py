@@ -238,6 +238,7 @@ def run_ours(args, rank, world, local):
     def e2e_once():
         eng.load(F_h, M_h)
         eng.set_warp(None)
+        eng.reset()
         eng.begin_level(0)
         eng.iterate(e2e_iters)
         ctx.check(lib.wlm_engine_get_warp(eng.h, U_h.data_ptr(), 1))
@@ -266,6 +267,7 @@ def run_ours(args, rank, world, local):
     def e2e_launch(e):
         e.load(F_h, M_h)
         e.set_warp(None)
+        e.reset()  # each step registers its pairs afresh
         e.begin_level(0)
         e.iterate(e2e_iters)
 

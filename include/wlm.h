@@ -214,6 +214,10 @@ wlm_status wlm_engine_load(wlm_engine* e, const float* F, const float* M, int is
 /* Set the current warps (fp32 SoA, device or host); NULL -> zero warps. */
 wlm_status wlm_engine_set_warp(wlm_engine* e, const float* u, int is_host);
 wlm_status wlm_engine_get_warp(wlm_engine* e, float* u, int is_host);
+/* New registrations on the loaded pairs: lambda back to lambda0, loss
+ * history and counters cleared (begin_level keeps lambda, which is the
+ * SPEC.md:389 carry between pyramid levels of one registration). */
+wlm_status wlm_engine_reset(wlm_engine* e);
 /* Start a level: reset loss history, evaluate r(u) (lambda kept). */
 wlm_status wlm_engine_begin_level(wlm_engine* e, int level);
 /* Launch `iters` lm_iterate steps for every active pair (asynchronous; with

@@ -10,6 +10,6 @@ there is no CPU fallback.
 from ._lib import LIB_PATH, load  # noqa: F401
 from .warplm import *  # noqa: F401,F403
 from .warplm import Context, default_context, reg_config  # noqa: F401
-from .engine import Engine, SlabGroup  # noqa: F401
+from .engine import BatchPipeline, Engine, SlabGroup  # noqa: F401
 
 __version__ = "0.1.0"

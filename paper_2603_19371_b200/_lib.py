@@ -114,6 +114,7 @@ SIGNATURES = {
     "wlm_engine_begin_level": (C.c_int, [_ENG, C.c_int]),
     "wlm_engine_iterate": (C.c_int, [_ENG, C.c_int]),
     "wlm_engine_set_pair_groups": (C.c_int, [_ENG, C.c_int]),
+    "wlm_engine_reset": (C.c_int, [_ENG]),
     "wlm_engine_step": (C.c_int, [_ENG]),
     "wlm_engine_state": (C.c_int, [_ENG, C.c_int, C.POINTER(LmState), _D, _D,
                                    C.POINTER(C.c_int)]),

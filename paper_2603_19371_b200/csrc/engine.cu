@@ -331,6 +331,12 @@ wlm_status wlm_engine_get_warp(wlm_engine* e, float* u, int is_host) {
     });
 }
 
+wlm_status wlm_engine_reset(wlm_engine* e) {
+    if (!e) return WLM_INVALID_ARG;
+    wlm_ctx* ctx = e->ctx;
+    return run(ctx, [&] { launch_begin_level(e->B, e->P, 0, 1, e->cfg.lm.lambda0, ctx->stream); });
+}
+
 wlm_status wlm_engine_begin_level(wlm_engine* e, int level) {
     if (!e) return WLM_INVALID_ARG;
     wlm_ctx* ctx = e->ctx;

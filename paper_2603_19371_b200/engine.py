@@ -76,6 +76,11 @@ class Engine:
     def get_warp_device(self, tensor):
         self._chk(self.lib.wlm_engine_get_warp(self.h, tensor.data_ptr(), 0))
 
+    def reset(self):
+        """New registrations on the loaded pairs: lambda back to lambda0
+        (begin_level alone carries lambda, as between pyramid levels)."""
+        self._chk(self.lib.wlm_engine_reset(self.h))
+
     def begin_level(self, level=0):
         self._chk(self.lib.wlm_engine_begin_level(self.h, int(level)))
 
@@ -192,6 +197,11 @@ class SlabGroup:
         self._chk(self.lib.wlm_slab_group_get_warp(self.h, p, host))
         return out
 
+    def reset(self):
+        """New registrations on the loaded pairs: lambda back to lambda0
+        (begin_level alone carries lambda, as between pyramid levels)."""
+        self._chk(self.lib.wlm_engine_reset(self.h))
+
     def begin_level(self, level=0):
         self._chk(self.lib.wlm_slab_group_begin_level(self.h, int(level)))
 
@@ -223,3 +233,49 @@ class SlabGroup:
             self.close()
         except Exception:
             pass
+
+
+class BatchPipeline:
+    """Serving loop for a stream of batches of identical geometry: two engines
+    (two contexts, two streams) alternate, so batch k+1's input copy and
+    batch k's warp copy run under the other engine's iterations.  Each batch
+    is one registration level of ``iters`` iterations from the identity warp
+    (the bench's pipelined e2e measurement is this loop).
+
+        pipe = BatchPipeline((192, 192, 192), pairs=8, cfg=cfg, iters=100)
+        for warps in pipe.run(batches):   # batches: iterable of (F, M)
+            ...                            # (pairs, 3, nz, ny, nx) float32
+
+    Results are those of running every batch alone on one engine.  Inputs
+    may be host arrays (pinned memory overlaps best) or CUDA tensors."""
+
+    def __init__(self, shape, pairs, cfg: RegConfig | None = None, iters=100, device=0):
+        self.shape = tuple(int(s) for s in shape)
+        self.pairs = int(pairs)
+        self.iters = int(iters)
+        self.ctxs = [Context(device), Context(device)]
+        self.engines = [Engine(self.shape, self.pairs, cfg, ctx=c) for c in self.ctxs]
+
+    def _launch(self, eng, F, M):
+        eng.load(F, M)
+        eng.set_warp(None)
+        eng.reset()  # a new batch is a new registration: lambda0, not the last batch's lambda
+        eng.begin_level(0)
+        eng.iterate(self.iters)
+
+    def run(self, batches):
+        pending = None
+        for k, (F, M) in enumerate(batches):
+            eng = self.engines[k % 2]
+            self._launch(eng, F, M)      # queued behind nothing on this engine's stream
+            if pending is not None:
+                yield pending.get_warp()  # the other engine: waits for its iterations, copies out
+            pending = eng
+        if pending is not None:
+            yield pending.get_warp()
+
+    def close(self):
+        for e in self.engines:
+            e.close()
+        for c in self.ctxs:
+            c.close()

@@ -822,3 +822,21 @@ def test_nonfinite_pair_does_not_disturb_the_batch(P, ctx, groups):
         eng.state(1)
     assert len(eng.trace(1)) < 10
     eng.close()
+
+
+def test_batch_pipeline_matches_sequential_runs(P, ctx):
+    """BatchPipeline (two engines alternating, copies overlapped) returns
+    exactly the warps of running each batch alone."""
+    shape = (20, 24, 28)
+    batches = []
+    for b in range(3):
+        pr = [O.synth_pair(shape, 900 + 2 * b + i, num_blobs=6, warp_max=2.0)[:2] for i in range(2)]
+        batches.append((np.stack([p[0] for p in pr]), np.stack([p[1] for p in pr])))
+    cfg = P.reg_config(nlevels=1, factors=[1], iters=[9])
+    pipe = P.BatchPipeline(shape, 2, cfg, iters=9)
+    got = list(pipe.run(batches))
+    pipe.close()
+    assert len(got) == 3
+    for (F, M), w in zip(batches, got):
+        ref, _, _ = run_engine(P, ctx, F, M, cfg, 9, pairs=2)
+        assert np.array_equal(w, ref)
