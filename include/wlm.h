@@ -298,6 +298,8 @@ void wlm_slab_group_destroy(wlm_slab_group* g);
 wlm_status wlm_slab_group_load(wlm_slab_group* g, const float* F, const float* M, int is_host);
 wlm_status wlm_slab_group_set_warp(wlm_slab_group* g, const float* u, int is_host);
 wlm_status wlm_slab_group_get_warp(wlm_slab_group* g, float* u, int is_host);
+/* New registration (lambda back to lambda0, as wlm_engine_reset). */
+wlm_status wlm_slab_group_reset(wlm_slab_group* g);
 wlm_status wlm_slab_group_begin_level(wlm_slab_group* g, int level);
 wlm_status wlm_slab_group_iterate(wlm_slab_group* g, int iters);
 /* Trace of the registration; fails if the slabs' state machines disagree. */

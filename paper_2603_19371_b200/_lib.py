@@ -139,6 +139,7 @@ SIGNATURES = {
     "wlm_slab_group_set_warp": (C.c_int, [_ENG, _VP, C.c_int]),
     "wlm_slab_group_get_warp": (C.c_int, [_ENG, _VP, C.c_int]),
     "wlm_slab_group_begin_level": (C.c_int, [_ENG, C.c_int]),
+    "wlm_slab_group_reset": (C.c_int, [_ENG]),
     "wlm_slab_group_iterate": (C.c_int, [_ENG, C.c_int]),
     "wlm_slab_group_trace": (C.c_int, [_ENG, C.POINTER(StepLog), C.c_size_t, C.POINTER(C.c_size_t)]),
     "wlm_slab_group_state": (C.c_int, [_ENG, C.POINTER(LmState), _D, _D, C.POINTER(C.c_int)]),

@@ -689,6 +689,14 @@ wlm_status wlm_slab_group_owned(const wlm_slab_group* g, int* zs, int* ze) {
     return WLM_OK;
 }
 
+wlm_status wlm_slab_group_reset(wlm_slab_group* g) {
+    if (!g) return WLM_INVALID_ARG;
+    wlm_ctx* ctx = g->ctx;
+    return run(ctx, [&] {
+        for (auto* e : g->eng) launch_begin_level(e->B, e->P, 0, 1, e->cfg.lm.lambda0, ctx->stream);
+    });
+}
+
 wlm_status wlm_slab_group_begin_level(wlm_slab_group* g, int level) {
     if (!g) return WLM_INVALID_ARG;
     wlm_ctx* ctx = g->ctx;

@@ -205,6 +205,10 @@ class SlabGroup:
     def begin_level(self, level=0):
         self._chk(self.lib.wlm_slab_group_begin_level(self.h, int(level)))
 
+    def reset(self):
+        """New registration: lambda back to lambda0 (begin_level carries it)."""
+        self._chk(self.lib.wlm_slab_group_reset(self.h))
+
     def iterate(self, iters):
         self._chk(self.lib.wlm_slab_group_iterate(self.h, int(iters)))
 

@@ -840,3 +840,25 @@ def test_batch_pipeline_matches_sequential_runs(P, ctx):
     for (F, M), w in zip(batches, got):
         ref, _, _ = run_engine(P, ctx, F, M, cfg, 9, pairs=2)
         assert np.array_equal(w, ref)
+
+
+def test_reused_engine_and_slab_group_reset(P, ctx):
+    """A second registration on a reused engine or slab group equals a fresh
+    one after reset(); without it lambda carries over (SPEC.md:389 carry)."""
+    shape = (20, 24, 28)
+    A = O.synth_pair(shape, 950, num_blobs=6, warp_max=2.0)[:2]
+    Bp = O.synth_pair(shape, 951, num_blobs=6, warp_max=2.0)[:2]
+    cfg = P.reg_config(nlevels=1, factors=[1], iters=[8])
+    fresh, (tr_f,), _ = run_engine(P, ctx, Bp[0], Bp[1], cfg, 8)
+    for make in (lambda: P.Engine(shape, 1, cfg, ctx=ctx), lambda: P.SlabGroup(shape, 2, cfg=cfg, ctx=ctx)):
+        g = make()
+        for F, M in (A, Bp):
+            g.load(F[None] if isinstance(g, P.Engine) else F, M[None] if isinstance(g, P.Engine) else M)
+            g.set_warp(None)
+            g.reset()
+            g.begin_level(0)
+            g.iterate(8)
+        w = g.get_warp()
+        w = w[0] if isinstance(g, P.Engine) else w
+        assert np.array_equal(w, fresh[0])
+        g.close()
