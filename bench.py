@@ -316,7 +316,7 @@ def run_ours(args, rank, world, local):
         "higher_is_better": True,
         "scaling": "weak",
         "vs_baseline": None,
-        "dtype": "f32",
+        "dtype": "f64", "storage_dtype": "f32",
         "data": "synthetic (GPU synth_pair: Gaussian blobs + smoothed random warp, noise 0.01)",
         "config": {"workload": f"config 4: batch of independent {n}^3 pairs, LNCC r=2 + pointwise LM, "
                                f"rejection off, {pairs} pairs per GPU",
@@ -442,7 +442,7 @@ def run_slabs(args, rank, world, local):
     line = {
         "metric": METRIC, "value": round(value, 4), "unit": "Gvoxel/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_max / args.steps, 4),
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "storage_dtype": "f32",
         "data": "synthetic (GPU synth_pair, 96 blobs, smoothed random warp, max 16 voxels, seed 7)",
         "config": {"workload": f"config 5: one {n}^3 pair, z-slab sharded over {world} GPU(s), LNCC r=2 + "
                                f"pointwise LM, rejection off",
