@@ -862,3 +862,53 @@ def test_reused_engine_and_slab_group_reset(P, ctx):
         w = w[0] if isinstance(g, P.Engine) else w
         assert np.array_equal(w, fresh[0])
         g.close()
+
+
+# ------------------------------------------------- BASELINE's full size ----
+@pytest.fixture(scope="module")
+def full_pairs():
+    """Config 4's volume size (192^3, BASELINE.json configs[3]), seeds 1000
+    and 1001 as in bench.py's reference arm."""
+    return [O.synth_pair((192, 192, 192), 1000 + s, num_blobs=12, warp_max=6.0)[:2] for s in range(2)]
+
+
+def test_config4_full_size_vs_oracle(P, ctx, full_pairs):
+    """The parity bar at the bench's own size: 4 LM iterations of one 192^3
+    pair against the fp32-storage oracle (the tight bar: loss 1e-6, warp
+    rel-L2 1e-5; measured 1e-15 / 1.9e-10) and the pure fp64 oracle (loss
+    1e-5, same decisions and lambda).  Against fp64 the warp bar is the
+    storage floor itself: at 192^3 with 6-voxel displacements, fp32 storage
+    of u moves a few hundred sample points across a trilinear knot, where
+    grad M jumps, so the fp32-storage oracle is already 4.3e-4 (rel-L2) from
+    the fp64 one after 4 iterations (1 iteration: 4.4e-8); the device must
+    sit on that floor, not beyond it."""
+    F, M = full_pairs[0]
+    it = 4
+    cfg_p = P.reg_config(nlevels=1, factors=[1], iters=[it])
+    cfg_o = O.default_config(nlevels=1, factors=[1], iters=[it])
+    warp, (tr,), _ = run_engine(P, ctx, F, M, cfg_p, it)
+    w = aos(warp[0])
+    rc, u32, _, tr32 = oracle_level(F, M, cfg_o, it, "fp32")
+    assert rc == 0
+    compare_runs(tr, tr32, w, u32, 1e-6, 1e-5)
+    rc, u64, _, tr64 = oracle_level(F, M, cfg_o, it, "fp64")
+    assert rc == 0
+    compare_runs(tr, tr64, w, u64, 1e-5, None)
+    floor = rel(u32, u64)
+    assert rel(w, u64) <= floor * (1 + 1e-3) + 1e-6, (rel(w, u64), floor)
+
+
+def test_config4_full_size_batch_and_slab_invariance(P, ctx, full_pairs):
+    """Size-independent properties at 192^3: a pair's result does not depend
+    on its batch (bit-identical to the single-pair run) nor on a 4-slab z
+    split (config 5's decomposition), over 10 iterations."""
+    Fs = np.stack([p[0] for p in full_pairs])
+    Ms = np.stack([p[1] for p in full_pairs])
+    it = 10
+    cfg = P.reg_config(nlevels=1, factors=[1], iters=[it])
+    wb, trb, _ = run_engine(P, ctx, Fs, Ms, cfg, it, pairs=2)
+    for s in range(2):
+        w1, (t1,), _ = run_engine(P, ctx, Fs[s], Ms[s], cfg, it)
+        assert np.array_equal(w1[0], wb[s]) and same_trace(t1, trb[s]), s
+    w, t, _ = run_slabs(P, ctx, Fs[0], Ms[0], cfg, it, 4)
+    assert same_trace(t, trb[0]) and np.array_equal(w, wb[0])
