@@ -912,3 +912,38 @@ def test_config4_full_size_batch_and_slab_invariance(P, ctx, full_pairs):
         assert np.array_equal(w1[0], wb[s]) and same_trace(t1, trb[s]), s
     w, t, _ = run_slabs(P, ctx, Fs[0], Ms[0], cfg, it, 4)
     assert same_trace(t, trb[0]) and np.array_equal(w, wb[0])
+
+
+@pytest.mark.parametrize("n,nslabs", [(512, 4), (1024, 2)])
+def test_config5_large_slab_split_bit_identical(P, ctx, n, nslabs):
+    """Config 5's decomposition at the north star's sizes (512^3 and the
+    config's own 1024^3): the GPU synth_pair (seed 7, 96 blobs, max
+    displacement 16, as bench.py --config 5), one slab against a z-slab
+    split over 3 LM iterations: losses, decisions, lambda and the whole warp
+    bit-identical, compared on the device (1024^3 peaks near 120 GB)."""
+    import ctypes as C
+
+    import torch
+    from paper_2603_19371_b200._lib import Dims, SynthSpec
+    shape = (n, n, n)
+    F = torch.empty(shape, dtype=torch.float32, device="cuda:0")
+    M = torch.empty(shape, dtype=torch.float32, device="cuda:0")
+    spec = SynthSpec(Dims(n, n, n), 96, 0.0, 16.0, 0.01, 7)
+    ctx.check(P.load().wlm_synth_pair(ctx.h, C.byref(spec), F.data_ptr(), M.data_ptr(), None, 1))
+    cfg = P.reg_config(nlevels=1, factors=[1], iters=[3])
+    out = {}
+    for ns in (1, nslabs):
+        grp = P.SlabGroup(shape, ns, cfg=cfg, ctx=ctx)
+        grp.load(F, M)
+        grp.set_warp(None)
+        grp.begin_level(0)
+        grp.iterate(3)
+        w = torch.zeros((3,) + shape, dtype=torch.float32, device="cuda:0")
+        grp.get_warp(w)
+        out[ns] = (w, grp.trace(), grp.state())
+        grp.close()
+        del grp
+    (w1, t1, s1), (w4, t4, s4) = out[1], out[nslabs]
+    assert len(t1) >= 3 and all(math.isfinite(r["r"]) for r in t1)
+    assert same_trace(t4, t1) and s4["lam"] == s1["lam"] and s4["r"] == s1["r"]
+    assert bool(torch.equal(w1, w4)) and float(w1.abs().max()) > 0.0
