@@ -17,8 +17,15 @@ build/%.o: $(CSRC)/%.cu $(HDRS)
 	@mkdir -p build
 	$(NVCC) $(ARCH) $(NVFLAGS) -Iinclude -c $< -o $@
 
+# the sources' hash is linked in (wlm_source_hash), so a library left stale
+# by edited sources is refused at load time (_lib.load)
+SRC_HASH = $(shell cat $(sort $(SRCS) $(HDRS)) | sha256sum | cut -c1-16)
+
 $(LIB): $(OBJS)
-	$(NVCC) $(ARCH) -shared -o $@ $(OBJS)
+	@mkdir -p build
+	printf 'const char* wlm_source_hash(void) { return "%s"; }\n' $(SRC_HASH) > build/src_hash.c
+	gcc -O2 -fPIC -c build/src_hash.c -o build/src_hash.o
+	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) build/src_hash.o
 
 oracle:
 	$(MAKE) -C oracle

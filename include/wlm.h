@@ -141,6 +141,9 @@ uint64_t wlm_ctx_launch_count(const wlm_ctx* ctx);
 void wlm_default_reg_config(wlm_reg_config* cfg);
 /* Library build id string (arch, version). */
 const char* wlm_version(void);
+/* First 16 hex digits of sha256 over the library's sources (Makefile
+ * SRC_HASH); the Python layer refuses a library built from other sources. */
+const char* wlm_source_hash(void);
 
 /* ---- host-buffer mirror of the reference field module (fp64, AoS) ---- */
 wlm_status wlm_warp_volume(wlm_ctx* ctx, const double* M, const double* u, wlm_dims d,

@@ -83,6 +83,7 @@ SIGNATURES = {
     "wlm_ctx_launch_count": (C.c_uint64, [_CTX]),
     "wlm_default_reg_config": (None, [C.POINTER(RegConfig)]),
     "wlm_version": (C.c_char_p, []),
+    "wlm_source_hash": (C.c_char_p, []),
     "wlm_warp_volume": (C.c_int, [_CTX, _D, _D, Dims, _D, _D]),
     "wlm_sample_field_points": (C.c_int, [_CTX, _D, Dims, _D, C.c_size_t, _D]),
     "wlm_compose_warp": (C.c_int, [_CTX, _D, Dims, _D, Dims, C.c_double, _D]),
@@ -155,6 +156,24 @@ SIGNATURES = {
 _lib = None
 
 
+def source_hash():
+    """sha256 (16 hex digits) of the sources the Makefile hashes into the
+    library, in the same (sorted path) order; None if they are absent."""
+    import glob
+    import hashlib
+    root = os.path.dirname(HERE)
+    rels = [os.path.relpath(p, root) for p in glob.glob(os.path.join(HERE, "csrc", "*.cu"))
+            + glob.glob(os.path.join(HERE, "csrc", "*.cuh"))] + [os.path.join("include", "wlm.h")]
+    paths = [os.path.join(root, r) for r in sorted(rels)]
+    if not all(os.path.exists(p) for p in paths):
+        return None
+    h = hashlib.sha256()
+    for p in paths:
+        with open(p, "rb") as f:
+            h.update(f.read())
+    return h.hexdigest()[:16]
+
+
 def load():
     """Load libwarplm_b200.so (raises if it was not built)."""
     global _lib
@@ -166,6 +185,11 @@ def load():
             fn = getattr(lib, name)
             fn.restype = res
             fn.argtypes = args
+        want = source_hash()
+        got = lib.wlm_source_hash().decode()
+        if want is not None and got != want and not os.environ.get("WLM_LIB_PATH"):
+            raise ImportError(f"{LIB_PATH} was built from other sources (hash {got}, sources {want}): "
+                              "run `make` (or __graft_entry__.build())")
         _lib = lib
     return _lib
 

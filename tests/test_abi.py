@@ -37,6 +37,19 @@ def test_library_is_sm100a():
     assert "sm_100a" in out, out
 
 
+def test_library_built_from_these_sources(monkeypatch):
+    """The library carries the hash of the sources it was built from; a stale
+    library (sources edited, not rebuilt) is refused at load, not used."""
+    from paper_2603_19371_b200 import _lib
+    assert C.CDLL(_lib.LIB_PATH).wlm_source_hash  # exported
+    lib = _lib.load()
+    assert lib.wlm_source_hash().decode() == _lib.source_hash()
+    monkeypatch.setattr(_lib, "_lib", None)
+    monkeypatch.setattr(_lib, "source_hash", lambda: "0" * 16)
+    with pytest.raises(ImportError, match="other sources"):
+        _lib.load()
+
+
 def test_no_gpu_means_loud_failure():
     import paper_2603_19371_b200 as P
     import torch
