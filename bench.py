@@ -1,13 +1,14 @@
 """Benchmark of the factored-LM iteration (BASELINE.json config 4).
 
-Workload: a batch of independent 192^3 synthetic pairs per GPU (config 4:
-64 pairs over 8 B200 -> 8 pairs per GPU; weak scaling: per-GPU work fixed),
-LNCC + LM, rejection off.  One step = one lm_iterate attempt for every pair
-on the GPU (K2 gradient, K3 LM step + smoothing + max, K4 compositive
-resample + smoothing, K1 warp + LNCC + device-side damping).  Inputs
-(~3.9 GB per GPU) are larger than L2, so no flush is needed.
+Workload: config 4, a batch of 64 independent 192^3 synthetic pairs split
+64/N per GPU (strong scaling: the global batch is fixed), LNCC + LM,
+rejection off.  One step = one lm_iterate attempt for every pair on the GPU
+(K2 gradient, K3 LM step + smoothing + max, K4 compositive resample +
+smoothing, K1 warp + LNCC + device-side damping).  Inputs (~31 GB per GPU at
+N=1) are far larger than L2, so no flush is needed.
 
   python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+  python bench.py --cpu-tables     # + config-1 and 192^3 primitive CPU tables
 
 Multi-GPU: launched by torchrun, one rank per GPU; no data-path collective
 (pairs are independent); timing = max over ranks (NCCL all-reduce of the
@@ -44,6 +45,23 @@ KERNEL_BYTES = {"K1_lncc_fwd": 32, "K2_lncc_bwd": 44, "K3_step_smooth": 24, "K4_
 DESIGN_BYTES = {"K1_lncc_fwd": 76, "K2_lncc_bwd": 64, "K3_step_smooth": 24, "K4_compose_smooth": 36}
 STAGE_ID = {"K1_lncc_fwd": 0, "K2_lncc_bwd": 1, "K3_step_smooth": 2, "K4_compose_smooth": 3}
 BYTES_PER_VOXEL_ITER = sum(KERNEL_BYTES.values())  # 136 (SURVEY 8(d) canonical)
+
+
+def config4(n, global_batch, world):
+    """The `config` object of both arms (identical, so the driver's arms
+    compare like with like); per-arm details live outside it."""
+    return {"workload": f"config 4: batch of {global_batch} independent {n}^3 pairs, LNCC r=2 + "
+                        f"pointwise LM, rejection off",
+            "global_batch": global_batch, "volume": [n, n, n],
+            "parallelism": f"dp{world} (independent pairs split {global_batch}/{world} per GPU, "
+                           f"no collective)",
+            "l2": f"inputs > L2 (68 B/voxel x {n ** 3} voxels per pair)"}
+
+
+def warp_max(n):
+    """Config 4's maximum displacement (6 voxels at 192^3), scaled down for
+    the small sizes the tests use (a 6-voxel warp folds a 24^3 volume)."""
+    return 6.0 if n >= 96 else n / 16.0
 
 
 def peaks():
@@ -162,7 +180,7 @@ def run_ours(args, rank, world, local):
     n = args.size
     shape = (n, n, n)
     nvox = n ** 3
-    pairs = args.pairs_per_gpu
+    pairs = args.pairs_per_gpu or max(1, args.global_batch // world)
     ctx = P.Context(local)
     lib = P.load()
     cfg = P.reg_config(nlevels=1, factors=[1], iters=[100])
@@ -174,7 +192,7 @@ def run_ours(args, rank, world, local):
     M_h = torch.empty((pairs,) + shape, dtype=torch.float32, pin_memory=True)
     for p in range(pairs):
         seed = 1000 + rank * pairs + p
-        spec = SynthSpec(Dims(n, n, n), 12, 0.0, 6.0, 0.01, seed)
+        spec = SynthSpec(Dims(n, n, n), 12, 0.0, warp_max(n), 0.01, seed)
         ctx.check(lib.wlm_synth_pair(ctx.h, C.byref(spec), F_h[p].data_ptr(), M_h[p].data_ptr(),
                                      None, 0))
     stream = torch.cuda.ExternalStream(ctx.stream(), device=f"cuda:{local}")
@@ -244,7 +262,7 @@ def run_ours(args, rank, world, local):
         ctx.check(lib.wlm_engine_get_warp(eng.h, U_h.data_ptr(), 1))
 
     e2e_once()  # warm (graph already built)
-    e2e_steps = max(1, min(3, args.steps))
+    e2e_steps = max(1, min(2, args.steps))
     barrier(world, local)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
@@ -299,7 +317,9 @@ def run_ours(args, rank, world, local):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline_sample(F_h[0].numpy(), M_h[0].numpy())
+        cpu = cpu_baseline_sample([(F_h[p].numpy(), M_h[p].numpy()) for p in range(pairs)])
+        if args.cpu_tables:
+            cpu["tables"] = cpu_tables()
     extra = None
     if rank == 0 and world == 1 and not args.no_extra:
         eng.close()  # free the batch engine before the pyramid runs
@@ -314,15 +334,13 @@ def run_ours(args, rank, world, local):
         "warmup": args.warmup,
         "ms_per_step": round(ms_max / args.steps, 5),
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": "strong" if not args.pairs_per_gpu else "weak",
         "vs_baseline": None,
         "dtype": "f64", "storage_dtype": "f32",
-        "data": "synthetic (GPU synth_pair: Gaussian blobs + smoothed random warp, noise 0.01)",
-        "config": {"workload": f"config 4: batch of independent {n}^3 pairs, LNCC r=2 + pointwise LM, "
-                               f"rejection off, {pairs} pairs per GPU",
-                   "global_batch": world * pairs, "volume": list(shape), "pairs_per_gpu": pairs,
-                   "parallelism": f"dp{world} (independent pairs, no collective)",
-                   "l2": "inputs > L2 (68 B/voxel x %d voxels per GPU)" % (pairs * nvox)},
+        "data": "synthetic (GPU synth_pair: Gaussian blobs + smoothed random warp max 6, noise 0.01, "
+                "seeds 1000+)",
+        "config": config4(n, world * pairs, world),
+        "pairs_per_gpu": pairs,
         "iters_per_s": round(iters_per_s, 2),
         "iters_per_s_per_pair": round(args.steps / (ms_max * 1e-3), 2),
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1),
@@ -426,6 +444,7 @@ def run_slabs(args, rank, world, local):
         t0 = time.perf_counter()
         grp.load(F_h, M_h)
         grp.set_warp(None)
+        grp.reset()  # a fresh registration: lambda0, empty loss history
         grp.begin_level(0)
         grp.iterate(args.e2e_iters)
         grp.get_warp(U_h)
@@ -538,91 +557,166 @@ def host_cpu():
     return {"nproc": os.cpu_count() or 1, "model": model}
 
 
-def cpu_baseline_sample(F, M):
-    """Reference CPU path (reference field.cpp primitives + restated LNCC/LM),
-    single thread, one LM iteration of one 192^3 pair of the same workload."""
+def _cpu_kind():
+    import oracle as O
+    return "reference" if O.have_ref() else "port"
+
+
+def cpu_registrations(data, iters):
+    """One single-threaded registration per (F, M) pair, all pairs in parallel
+    (one per host core): each runs its level's initial residual, then `iters`
+    LM attempts.  The reference code is serial, so the host cores are used by
+    running independent registrations side by side.
+    Returns the per-pair arrays of attempt wall times (initial residual
+    excluded: a steady-state iteration evaluates one residual)."""
     import numpy as np
 
     import oracle as O
-    kind = "reference" if O.have_ref() else "port"
+    kind = _cpu_kind()
     L = O.lib(kind)
     L.orc_set_threads(1)
-    cfg = O.default_config(nlevels=1, factors=[1], iters=[1])
-    n = F.size
-    t0 = time.perf_counter()
-    rc, _, _, _ = O.lm_run_level(F, M, np.zeros(F.shape + (3,)), cfg, 1, kind=kind)
-    dt = time.perf_counter() - t0
+    cfg = O.default_config(nlevels=1, factors=[1], iters=[iters])
+    out = [None] * len(data)
+
+    def one(i):
+        F, M = data[i]
+        F = np.ascontiguousarray(F, np.float64)
+        M = np.ascontiguousarray(M, np.float64)
+        rc, _, _, ts = O.lm_run_level_timed(F, M, np.zeros(F.shape + (3,)), cfg, iters, kind=kind)
+        out[i] = ts
+
+    th = [threading.Thread(target=one, args=(i,)) for i in range(len(data))]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
     L.orc_set_threads(min(8, os.cpu_count() or 1))
-    # lm_run_level(1) = initial residual + 1 attempt (2 residual evaluations);
-    # count it as 1 iteration (conservative for the CPU)
-    return {"value": round(n / dt / 1e9, 6), "unit": "Gvoxel/s", "cores": 1, "kind": kind,
-            "sample": f"1 LM iteration (incl. initial residual) of pair 0 at {F.shape[0]}^3, "
-                      f"{dt:.1f} s, single thread (the reference is serial)",
+    return out, kind
+
+
+def cpu_baseline_sample(pairs_data, warm=2, timed=5):
+    """Reference CPU path (oracle/_ref: the reference's own field.cpp
+    primitives + the restated LNCC/LM modules) on the box's host cores, on
+    the same workload's first pairs (the GPU-generated inputs): one
+    single-threaded registration per core, each 2 warm-up + 5 timed LM
+    attempts; per-iteration time = the median of the 5, step
+    time = the slowest core's."""
+    import numpy as np
+    cores = os.cpu_count() or 1
+    data = pairs_data[:min(cores, len(pairs_data))]
+    t0 = time.perf_counter()
+    times, kind = cpu_registrations(data, warm + timed)
+    wall = time.perf_counter() - t0
+    per_pair = [float(np.median(t[warm:warm + timed])) for t in times]
+    step_s = max(per_pair)
+    nvox = data[0][0].size
+    value = len(data) * nvox / step_s / 1e9
+    return {"value": round(value, 6), "unit": "Gvoxel/s", "cores": len(data), "kind": kind,
+            "sample": f"{len(data)} pairs of the workload ({data[0][0].shape[0]}^3), one single-threaded "
+                      f"registration per core in parallel; per pair {warm} warm-up + {timed} timed LM "
+                      f"attempts after the initial residual, median attempt (SPEC.md:467); "
+                      f"{wall:.0f} s wall",
+            "s_per_iteration_single_thread": round(float(np.median(per_pair)), 3),
             "host": host_cpu()}
+
+
+def cpu_tables():
+    """SURVEY 8(d) CPU tables on the box's host: the full config-1 oracle run
+    (64^3 x 100 iterations, single thread) and the reference primitives at
+    192^3 (single thread, the reference's own field.cpp functions)."""
+    import ctypes as C
+
+    import numpy as np
+
+    import oracle as O
+    out = {}
+    kind = _cpu_kind()
+    L = O.lib(kind)
+    L.orc_set_threads(1)
+    F, M, _ = O.synth_pair((64, 64, 64), 0, num_blobs=12, warp_max=3.0)
+    cfg = O.default_config(nlevels=1, factors=[1], iters=[100])
+    t0 = time.perf_counter()
+    rc, _, tr, ts = O.lm_run_level_timed(F, M, np.zeros(F.shape + (3,)), cfg, 100, kind=kind)
+    out["config1_64cubed_100_iters"] = {"wall_s": round(time.perf_counter() - t0, 3), "threads": 1,
+                                        "median_iter_s": round(float(np.median(ts)), 5),
+                                        "final_r": tr[-1].r, "kind": kind}
+    if O.have_ref():
+        R = O.ref_lib()
+        n = 192
+        rng = np.random.default_rng(0)
+        vol = rng.random((n, n, n))
+        u = np.ascontiguousarray(rng.normal(size=(n, n, n, 3)) * 2.0)
+        v = np.ascontiguousarray(rng.normal(size=(n, n, n, 3)) * 0.3)
+        Mw = np.empty((n, n, n))
+        gM = np.empty((n, n, n, 3))
+        out_f = np.empty_like(u)
+        P = lambda a: a.ctypes.data_as(C.POINTER(C.c_double))  # noqa: E731
+        rows = {}
+
+        def tm(name, fn):
+            t = time.perf_counter()
+            fn()
+            rows[name] = round(time.perf_counter() - t, 4)
+
+        tm("warp+grad", lambda: R.ref_warp_volume(P(vol), P(u), n, n, n, P(Mw), P(gM)))
+        tm("normalize (max)", lambda: R.ref_normalize_step(P(v), n, n, n, 0.4, 1e-12))
+        tm("compose_warp", lambda: R.ref_compose_warp(P(u), n, n, n, P(v), n, n, n, 0.2, P(out_f)))
+        tm("smooth 3ch sigma=1", lambda: R.ref_gaussian_smooth(P(u), n, n, n, 3, 1.0))
+        tm("smooth 3ch sigma=0.5", lambda: R.ref_gaussian_smooth(P(u), n, n, n, 3, 0.5))
+        tm("smooth 1ch sigma=1", lambda: R.ref_gaussian_smooth(P(vol), n, n, n, 1, 1.0))
+        tm("jacobian_det_min", lambda: R.ref_jacobian_det_min(P(u), n, n, n))
+        rows["sum"] = round(sum(rows.values()), 4)
+        out["reference_primitives_192_s"] = rows
+    L.orc_set_threads(min(8, os.cpu_count() or 1))
+    out["host"] = host_cpu()
+    return out
 
 
 # ------------------------------------------------------------- reference ----
 def run_reference(args, rank, world):
     """The reference CPU implementation on the box's host cores: reference
     field.cpp primitives (oracle/_ref) + the restated spec-only modules, one
-    single-threaded registration per core, pairs in parallel."""
+    single-threaded registration per core, pairs in parallel.  A step is one
+    LM attempt of every sampled pair (the slowest core's attempt time); the
+    levels' initial residuals are excluded, as in the GPU arm, whose timed
+    steps are attempts only."""
     import numpy as np
 
     import oracle as O
-    kind = "reference" if O.have_ref() else "port"
-    L = O.lib(kind)
     n = args.size
     shape = (n, n, n)
     nvox = n ** 3
     cores = os.cpu_count() or 1
-    pairs = min(args.pairs_per_gpu, cores)
-    # all host threads: one registration per pair, the rest inside each
-    # (the oracle's plane-parallel loops; reference field.cpp calls are serial)
-    per_pair = max(1, cores // pairs)
-    L.orc_set_threads(per_pair)
-    data = []
-    for p in range(pairs):
-        F, M, _ = O.synth_pair(shape, 1000 + p, num_blobs=12, warp_max=6.0)
-        data.append((F, M))
-    cfg = O.default_config(nlevels=1, factors=[1], iters=[1])
-    u0 = np.zeros(shape + (3,))
-
-    def one_step():
-        th = []
-        for F, M in data:
-            t = threading.Thread(target=O.lm_run_level, args=(F, M, u0, cfg, 1), kwargs={"kind": kind})
-            t.start()
-            th.append(t)
-        for t in th:
-            t.join()
-
-    budget = args.ref_budget_s
-    t_start = time.perf_counter()
-    for _ in range(min(args.warmup, 1)):
-        one_step()
-    done = 0
+    gb = args.global_batch if not args.pairs_per_gpu else args.pairs_per_gpu * world
+    npairs = min(gb, cores)
     t0 = time.perf_counter()
-    for _ in range(args.steps):
-        one_step()
-        done += 1
-        if time.perf_counter() - t_start > budget:
-            break
-    dt = time.perf_counter() - t0
-    value = pairs * nvox * done / dt / 1e9
+    data = [O.synth_pair(shape, 1000 + p, num_blobs=12, warp_max=warp_max(n))[:2] for p in range(npairs)]
+    t_synth = time.perf_counter() - t0
+    # bound the sample: as many steps as fit the budget at the measured rate
+    # (one probe attempt per pair first)
+    warm = max(1, min(args.warmup, 2))
+    probe, kind = cpu_registrations(data, 1)
+    per_attempt = max(max(t) for t in probe)
+    steps = max(1, min(args.steps, int(args.ref_budget_s / max(per_attempt, 1e-9)) - warm))
+    times, kind = cpu_registrations(data, warm + steps)
+    step_s = [max(t[k] for t in times) for k in range(warm, warm + steps)]
+    dt = float(sum(step_s))
+    value = npairs * nvox * steps / dt / 1e9
+    sample = (f"{steps} steps x 1 LM attempt of {npairs} pairs of {n}^3 (oracle synth_pair seeds 1000+), "
+              f"one single-threaded registration per host core; step = the slowest pair's attempt; "
+              f"{warm} warm-up attempts and the initial residual excluded; inputs made in {t_synth:.0f} s")
     return {
         "metric": METRIC, "value": round(value, 6), "unit": "Gvoxel/s", "n_gpus": world,
-        "steps": args.steps, "steps_timed": done, "warmup": args.warmup,
-        "ms_per_step": round(dt * 1e3 / max(done, 1), 1), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "impl": "reference",
-        "data": "synthetic (oracle synth_pair, seeds 1000+)",
-        "config": {"workload": f"config 4: batch of independent {n}^3 pairs, LNCC r=2 + pointwise LM, "
-                               f"rejection off; CPU sample {pairs} pairs in parallel",
-                   "global_batch": pairs, "volume": list(shape)},
-        "cpu_baseline": {"value": round(value, 6), "unit": "Gvoxel/s", "cores": pairs * per_pair, "kind": kind,
-                         "sample": f"{done} steps x 1 LM iteration (incl. initial residual) on {pairs} "
-                                   f"pairs of {n}^3, one registration thread per pair x {per_pair} "
-                                   f"threads inside",
-                         "host": host_cpu()},
+        "steps": args.steps, "steps_timed": steps, "warmup": args.warmup,
+        "ms_per_step": round(dt * 1e3 / steps, 1), "higher_is_better": True,
+        "scaling": "strong" if not args.pairs_per_gpu else "weak", "vs_baseline": None,
+        "dtype": "f64", "impl": "reference",
+        "data": "synthetic (oracle synth_pair: Gaussian blobs + smoothed random warp max 6, noise 0.01, "
+                "seeds 1000+)",
+        "config": config4(n, gb, world),
+        "cpu_baseline": {"value": round(value, 6), "unit": "Gvoxel/s", "cores": npairs, "kind": kind,
+                         "sample": sample, "s_per_iteration_single_thread":
+                             round(float(np.median(step_s)), 3), "host": host_cpu()},
         "e2e": {"value": round(value, 6), "unit": "Gvoxel/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -635,7 +729,11 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--size", type=int, default=192)
-    ap.add_argument("--pairs-per-gpu", type=int, default=8)
+    ap.add_argument("--global-batch", type=int, default=64, help="config 4: pairs split over the GPUs")
+    ap.add_argument("--pairs-per-gpu", type=int, default=0,
+                    help="fixed pairs per GPU instead (weak scaling); 0 = global batch / N")
+    ap.add_argument("--cpu-tables", action="store_true",
+                    help="add the config-1 run and the 192^3 primitive table to cpu_baseline")
     ap.add_argument("--e2e-iters", type=int, default=100)
     ap.add_argument("--e2e-groups", type=int, default=2, help="pair groups of each pipelined e2e engine")
     ap.add_argument("--no-cpu-baseline", action="store_true")

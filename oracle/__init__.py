@@ -109,6 +109,8 @@ def _declare(lib):
         "orc_upsample_warp": (None, [_D, Dims, Dims, C.c_double, _D]),
         "orc_lm_run_level": (C.c_int, [_D, _D, Dims, _D, C.POINTER(RegConfig), C.POINTER(LmState),
                                        C.c_int, C.c_int, C.POINTER(StepLog), _I]),
+        "orc_lm_run_level_timed": (C.c_int, [_D, _D, Dims, _D, C.POINTER(RegConfig), C.POINTER(LmState),
+                                             C.c_int, C.c_int, C.POINTER(StepLog), _I, _D, C.c_int, _I]),
         "orc_register": (C.c_int, [_F, _F, Dims, C.POINTER(RegConfig), _D, C.POINTER(StepLog),
                                    C.c_size_t, C.POINTER(C.c_size_t), _D]),
         "orc_synth_pair": (C.c_int, [C.POINTER(SynthSpec), _F, _F, _F]),
@@ -396,6 +398,22 @@ def lm_run_level(F, M, u, cfg: RegConfig, iters, state: LmState | None = None, l
     rc = lib(kind).orc_lm_run_level(_p(F), _p(M), dims_of(F), _p(u), C.byref(cfg), C.byref(st),
                                     level, iters, trace, C.byref(nt))
     return rc, u, st, [trace[i] for i in range(nt.value)]
+
+
+def lm_run_level_timed(F, M, u, cfg: RegConfig, iters, kind="port"):
+    """lm_run_level plus the wall time of every attempt (LM step through the
+    residual at the trial warp; the level's initial residual excluded)."""
+    F, M = _c64(F), _c64(M)
+    u = _c64(u).copy()
+    st = LmState(cfg.lm.lambda0, 0, 0.0, 0.0)
+    trace = (StepLog * max(iters, 1))()
+    nt = C.c_int(0)
+    cap = max(1, iters * (cfg.lm.max_retries + 1))
+    times = np.zeros(cap)
+    na = C.c_int(0)
+    rc = lib(kind).orc_lm_run_level_timed(_p(F), _p(M), dims_of(F), _p(u), C.byref(cfg), C.byref(st),
+                                          0, iters, trace, C.byref(nt), _p(times), cap, C.byref(na))
+    return rc, u, [trace[i] for i in range(nt.value)], times[:na.value]
 
 
 def register(F, M, cfg: RegConfig, kind="port"):

@@ -12,6 +12,7 @@
 #include "oracle.h"
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstring>
 #include <limits>
@@ -939,6 +940,12 @@ void orc_upsample_warp(const double* u, orc_dims d, orc_dims nd, double scale, d
 //   u' = smooth(u', sigma_warp); r' = residual(u'); reject? }  ->
 //   update_damping(r'); u <- u'.
 // Adam / GD share the smooth-normalize-compose path (A10).
+// Wall time of every attempt (LM step .. residual at the trial warp) of the
+// calling thread's orc_lm_run_level_timed call: the CPU baseline's
+// per-iteration cost without the level's initial residual (bench.py).
+static thread_local double* t_attempt_s = nullptr;
+static thread_local int t_attempt_cap = 0, t_attempt_n = 0;
+
 int orc_lm_run_level(const double* F, const double* M, orc_dims d, double* u,
                      const orc_reg_config* c, orc_lm_state* state, int level, int iters,
                      orc_step_log* trace, int* ntrace) {
@@ -966,6 +973,7 @@ int orc_lm_run_level(const double* F, const double* M, orc_dims d, double* u,
         double rn = 0.0, ln = 0.0, eps = 0.0, jac = kNaN;
         bool forced = false;
         for (;;) {
+            const auto t_att0 = std::chrono::steady_clock::now();
             const bool dev = g_fp32_storage == 2 && (g_dev_flags & 1);
             const bool dev4 = g_fp32_storage == 2 && (g_dev_flags & 2);
             if (c->optimizer == ORC_OPT_LM && c->lm.tile_size > 1) {
@@ -1009,6 +1017,9 @@ int orc_lm_run_level(const double* F, const double* M, orc_dims d, double* u,
                 jac = jac_min(inc.data(), d);
             }
             rn = residual(unew.data(), gnew.data(), &ln);
+            if (t_attempt_s && t_attempt_n < t_attempt_cap)
+                t_attempt_s[t_attempt_n++] =
+                    std::chrono::duration<double>(std::chrono::steady_clock::now() - t_att0).count();
             if (!std::isfinite(rn)) {
                 if (trace && ntrace) *ntrace = nt;
                 return ORC_NONFINITE;
@@ -1036,6 +1047,19 @@ int orc_lm_run_level(const double* F, const double* M, orc_dims d, double* u,
     }
     if (ntrace) *ntrace = nt;
     return ORC_OK;
+}
+
+int orc_lm_run_level_timed(const double* F, const double* M, orc_dims d, double* u,
+                           const orc_reg_config* c, orc_lm_state* state, int level, int iters,
+                           orc_step_log* trace, int* ntrace, double* attempt_s, int cap, int* nattempts) {
+    t_attempt_s = attempt_s;
+    t_attempt_cap = cap;
+    t_attempt_n = 0;
+    const int rc = orc_lm_run_level(F, M, d, u, c, state, level, iters, trace, ntrace);
+    if (nattempts) *nattempts = t_attempt_n;
+    t_attempt_s = nullptr;
+    t_attempt_cap = t_attempt_n = 0;
+    return rc;
 }
 
 // register(F, M, cfg): coarse -> fine, warp inherited with

@@ -164,6 +164,11 @@ void orc_upsample_warp(const double* u, orc_dims d, orc_dims nd, double scale,
 int orc_lm_run_level(const double* F, const double* M, orc_dims d, double* u,
                      const orc_reg_config* c, orc_lm_state* state, int level, int iters,
                      orc_step_log* trace, int* ntrace);
+// orc_lm_run_level plus the wall time of each attempt (step -> residual at
+// the trial warp) in attempt_s[0 .. *nattempts), at most cap entries.
+int orc_lm_run_level_timed(const double* F, const double* M, orc_dims d, double* u,
+                           const orc_reg_config* c, orc_lm_state* state, int level, int iters,
+                           orc_step_log* trace, int* ntrace, double* attempt_s, int cap, int* nattempts);
 int orc_register(const float* F, const float* M, orc_dims d, const orc_reg_config* c,
                  double* warp_out, orc_step_log* trace, size_t cap, size_t* len,
                  double* jac_final);

@@ -108,6 +108,17 @@ wlm_status engine_init(wlm_engine* e, wlm_ctx* ctx, wlm_dims d, int pairs, const
     return WLM_OK;
 }
 
+// A new registration starts from zero Adam moments: k_adam's bias correction
+// restarts at t = 1 with the iteration counter, and stale m, v would be
+// amplified by it.
+void clear_adam_moments(wlm_engine* e, cudaStream_t s) {
+    if (e->P.optimizer != WLM_OPT_ADAM) return;
+    wlm_ctx* ctx = e->ctx;
+    const size_t bytes = sizeof(float) * (size_t)e->pairs * 3 * (size_t)e->g.n;
+    CK(cudaMemsetAsync(e->AM.p, 0, bytes, s));
+    CK(cudaMemsetAsync(e->AV.p, 0, bytes, s));
+}
+
 void engine_alloc(wlm_engine* e) {
     wlm_ctx* ctx = e->ctx;
     const size_t n = (size_t)e->g.n, B = (size_t)e->pairs;
@@ -334,7 +345,10 @@ wlm_status wlm_engine_get_warp(wlm_engine* e, float* u, int is_host) {
 wlm_status wlm_engine_reset(wlm_engine* e) {
     if (!e) return WLM_INVALID_ARG;
     wlm_ctx* ctx = e->ctx;
-    return run(ctx, [&] { launch_begin_level(e->B, e->P, 0, 1, e->cfg.lm.lambda0, ctx->stream); });
+    return run(ctx, [&] {
+        launch_begin_level(e->B, e->P, 0, 1, e->cfg.lm.lambda0, ctx->stream);
+        clear_adam_moments(e, ctx->stream);
+    });
 }
 
 wlm_status wlm_engine_begin_level(wlm_engine* e, int level) {

@@ -364,6 +364,7 @@ struct wlm_engine {
 namespace wlm {
 wlm_status engine_init(wlm_engine* e, wlm_ctx* ctx, wlm_dims d, int pairs, const wlm_reg_config* c);
 void engine_alloc(wlm_engine* e);
+void clear_adam_moments(wlm_engine* e, cudaStream_t s);
 std::vector<PairState> read_states(wlm_engine* e);
 void copy_warps_in(wlm_engine* e, const float* u, int is_host);
 }  // namespace wlm

@@ -544,7 +544,7 @@ wlm_status make_group(wlm_ctx* ctx, wlm_dims d, int nslabs, int first, int count
 }
 
 wlm_status check_split(wlm_ctx* ctx, wlm_dims d, int nslabs, const wlm_reg_config* cfg) {
-    if (!ctx || nslabs < 1 || !valid_dims(d)) return WLM_INVALID_ARG;
+    if (nslabs < 1 || !valid_dims(d)) return WLM_INVALID_ARG;  // ctx may be null (host-only helpers)
     // every slab (tile-aligned when tiled) holds at least the halo depth and,
     // with tiles, the R_u + k planes its halo tiles can reach into
     const int tk = std::max(1, cfg->lm.tile_size);
@@ -575,7 +575,10 @@ wlm_status wlm_slab_partition(int nz, int nslabs, int slab, int* zs, int* ze) {
 wlm_status wlm_slab_halo_plan(wlm_dims d, int nslabs, int slab, const wlm_reg_config* cfg, wlm_halo_xfer* rows,
                               size_t cap, size_t* len) {
     if (!cfg || !len || nslabs < 1 || slab < 0 || slab >= nslabs || !valid_dims(d)) return WLM_INVALID_ARG;
-    if (d.nz / nslabs < slab_halo(cfg)) return WLM_INVALID_ARG;
+    // the same per-slab test as wlm_slab_group_create (tile-aligned splits,
+    // R_u + k planes with tiles): no plan for a split a group would refuse
+    const wlm_status ok = check_split(nullptr, d, nslabs, cfg);
+    if (ok != WLM_OK) return ok;
     const auto p = slab_plan(d, nslabs, slab, smooth_radius(cfg->sigma_update), smooth_radius(cfg->sigma_warp),
                              std::max(1, cfg->lm.tile_size));
     *len = p.size();
@@ -587,6 +590,7 @@ wlm_status wlm_slab_group_create(wlm_ctx* ctx, wlm_dims d, int nslabs, const wlm
                                  wlm_slab_group** out) {
     if (!out || !cfg) return WLM_INVALID_ARG;
     *out = nullptr;
+    if (!ctx) return WLM_INVALID_ARG;
     const wlm_status s = check_split(ctx, d, nslabs, cfg);
     if (s != WLM_OK) return s;
     return make_group(ctx, d, nslabs, 0, nslabs, cfg, nullptr, out);
@@ -604,7 +608,7 @@ wlm_status wlm_nccl_unique_id(const char* nccl_lib, unsigned char id[128]) {
 
 wlm_status wlm_slab_group_create_nccl(wlm_ctx* ctx, wlm_dims d, int rank, int nranks, const unsigned char id[128],
                                       const char* nccl_lib, const wlm_reg_config* cfg, wlm_slab_group** out) {
-    if (!out || !cfg || !id || rank < 0 || rank >= nranks) return WLM_INVALID_ARG;
+    if (!ctx || !out || !cfg || !id || rank < 0 || rank >= nranks) return WLM_INVALID_ARG;
     *out = nullptr;
     wlm_status s = check_split(ctx, d, nranks, cfg);
     if (s != WLM_OK) return s;
@@ -693,7 +697,10 @@ wlm_status wlm_slab_group_reset(wlm_slab_group* g) {
     if (!g) return WLM_INVALID_ARG;
     wlm_ctx* ctx = g->ctx;
     return run(ctx, [&] {
-        for (auto* e : g->eng) launch_begin_level(e->B, e->P, 0, 1, e->cfg.lm.lambda0, ctx->stream);
+        for (auto* e : g->eng) {
+            launch_begin_level(e->B, e->P, 0, 1, e->cfg.lm.lambda0, ctx->stream);
+            clear_adam_moments(e, ctx->stream);
+        }
     });
 }
 

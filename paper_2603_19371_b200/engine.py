@@ -197,11 +197,6 @@ class SlabGroup:
         self._chk(self.lib.wlm_slab_group_get_warp(self.h, p, host))
         return out
 
-    def reset(self):
-        """New registrations on the loaded pairs: lambda back to lambda0
-        (begin_level alone carries lambda, as between pyramid levels)."""
-        self._chk(self.lib.wlm_engine_reset(self.h))
-
     def begin_level(self, level=0):
         self._chk(self.lib.wlm_slab_group_begin_level(self.h, int(level)))
 

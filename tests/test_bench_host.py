@@ -55,3 +55,35 @@ def test_reference_arm_other_ranks_exit_silently():
     out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--steps", "1",
                           "--warmup", "1"], env=env, capture_output=True, text=True, timeout=120)
     assert out.returncode == 0 and out.stdout.strip() == ""
+
+
+def test_reference_arm_line_and_config_match_ours():
+    """The reference arm (CPU) prints the contract's line with the same
+    `config` object our arm uses (bench.config4), attempts only in its
+    timed steps, and a cpu_baseline describing the sample."""
+    import json
+    import subprocess
+    import sys
+    sys.path.insert(0, ROOT)
+    import bench
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--steps", "2",
+                          "--warmup", "1", "--size", "24", "--global-batch", "2"],
+                         capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = json.loads(out.stdout.strip().splitlines()[-1])
+    assert line["impl"] == "reference" and line["value"] > 0 and line["unit"] == "Gvoxel/s"
+    assert line["config"] == bench.config4(24, 2, 1)
+    assert line["steps_timed"] == 2 and line["cpu_baseline"]["cores"] == min(2, os.cpu_count())
+    assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["e2e"]["value"] == line["value"]
+
+
+def test_cpu_registrations_time_attempts_only():
+    """Attempt timings exclude the level's initial residual: k attempts give
+    k timings, each positive."""
+    import sys
+    sys.path.insert(0, ROOT)
+    import bench
+    import oracle as O
+    F, M, _ = O.synth_pair((16, 16, 16), 3, num_blobs=4, warp_max=1.0)
+    times, kind = bench.cpu_registrations([(F, M), (F, M)], 3)
+    assert len(times) == 2 and all(len(t) == 3 and (t > 0).all() for t in times)

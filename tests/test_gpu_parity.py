@@ -842,13 +842,17 @@ def test_batch_pipeline_matches_sequential_runs(P, ctx):
         assert np.array_equal(w, ref)
 
 
-def test_reused_engine_and_slab_group_reset(P, ctx):
+@pytest.mark.parametrize("opt", ["lm", "adam"])
+def test_reused_engine_and_slab_group_reset(P, ctx, opt):
     """A second registration on a reused engine or slab group equals a fresh
-    one after reset(); without it lambda carries over (SPEC.md:389 carry)."""
+    one after reset(); without it lambda carries over (SPEC.md:389 carry).
+    With Adam, reset() also zeroes the moments (k_adam's bias correction
+    restarts at t = 1; stale m, v would be amplified)."""
     shape = (20, 24, 28)
     A = O.synth_pair(shape, 950, num_blobs=6, warp_max=2.0)[:2]
     Bp = O.synth_pair(shape, 951, num_blobs=6, warp_max=2.0)[:2]
-    cfg = P.reg_config(nlevels=1, factors=[1], iters=[8])
+    extra = {"optimizer": P.OPT_ADAM} if opt == "adam" else {}
+    cfg = P.reg_config(nlevels=1, factors=[1], iters=[8], **extra)
     fresh, (tr_f,), _ = run_engine(P, ctx, Bp[0], Bp[1], cfg, 8)
     for make in (lambda: P.Engine(shape, 1, cfg, ctx=ctx), lambda: P.SlabGroup(shape, 2, cfg=cfg, ctx=ctx)):
         g = make()

@@ -127,3 +127,13 @@ def test_tiled_plans_have_twin_sends():
                 twin = [q for q in plans[r["peer"]] if q["peer"] == s and q["buffer"] == "tm"
                         and q["send"] != r["send"] and (q["z0"], q["z1"]) == (r["z0"], r["z1"])]
                 assert len(twin) == 1, (k, ns, s, r)
+
+
+def test_halo_plan_refuses_what_a_group_refuses():
+    """wlm_slab_halo_plan applies the slab group's own per-slab test: with
+    tiles (k = 4) a split whose tile-aligned slabs are thinner than R_u + k
+    is refused by both, though nz / nslabs alone would pass."""
+    cfg = P.reg_config(nlevels=1, factors=[1], iters=[1], **{"lm.tile_size": 4})
+    with pytest.raises(ValueError):
+        slabs.halo_plan((24, 8, 8), 4, 0, cfg)   # 6 planes per slab < R_u (3) + k (4)
+    slabs.halo_plan((24, 8, 8), 3, 0, cfg)       # 8 planes per slab: fine
