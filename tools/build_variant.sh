@@ -14,5 +14,7 @@ for f in kernels hot_kernels engine ops synth slab io; do
   objs="$objs $out/$f.o"
 done
 wait
-nvcc -gencode arch=compute_100a,code=sm_100a -shared -o $out/libwarplm_b200.so $objs
+printf 'const char* wlm_source_hash(void) { return "variant-%s"; }\n' "$name" > $out/src_hash.c
+gcc -O2 -fPIC -c $out/src_hash.c -o $out/src_hash.o
+nvcc -gencode arch=compute_100a,code=sm_100a -shared -o $out/libwarplm_b200.so $objs $out/src_hash.o
 echo "built $out/libwarplm_b200.so"
