@@ -1055,9 +1055,17 @@ __device__ __forceinline__ double border_inv(const double* t, int p, int n, int 
 #ifndef WLM_K3_COLUMN_Y
 #define WLM_K3_COLUMN_Y 1
 #endif
+#ifndef WLM_K3_TY
+#define WLM_K3_TY 16
+#endif
 namespace k3 {
-constexpr int TX = 32, TY = 8, NT = 256;
+// 32 x TY tiles of 32 TY threads; TY = 16 (one CTA of 512 per SM) halves
+// the halo share of the LM-step producer against 32 x 8 (2.08 -> 1.63 halo
+// items and 1.75 -> 1.375 x-pass rows per output)
+constexpr int TX = 32, TY = WLM_K3_TY, NT = 32 * TY;
+constexpr int MINB = NT <= 256 ? 2 : 1;
 constexpr bool COLY = WLM_K3_COLUMN_Y;
+constexpr int NQ = TY / 4;  // column y-pass: 4 outputs per thread, NQ per column
 template <int R>
 struct Shape {
     static constexpr int IWP = TX + 2 * R;  // halo row (even: 16-byte aligned rows of doubles)
@@ -1073,7 +1081,7 @@ struct Shape {
 }  // namespace k3
 
 template <int R, bool TILED>
-__global__ void __launch_bounds__(k3::NT, 2) k_step_smooth(Batch b, LmParams p, int chunk_len) {
+__global__ void __launch_bounds__(k3::NT, k3::MINB) k_step_smooth(Batch b, LmParams p, int chunk_len) {
     using S = k3::Shape<R>;
     constexpr int TX = k3::TX, NT = k3::NT, W = 2 * R + 1;
     constexpr int IWP = S::IWP, IH = S::IH, NI = S::NI, SL = S::SLOTS, NV = S::NV;
@@ -1211,14 +1219,14 @@ __global__ void __launch_bounds__(k3::NT, 2) k_step_smooth(Batch b, LmParams p, 
     double* x_b = s_x0 + 3 * IH * TX;
     double* y_a = s_y0;                // column pass: y-passed plane p (read by the ring)
     double* y_b = s_y0 + 3 * k3::TY * TX;
-    // column y-pass: thread (channel yc, column ox, half yh) of the last 6
-    // warps forms 4 outputs from its column's 4 + 2R x-sums held in
+    // column y-pass: thread (channel yc, column ox, quarter yh) of the last
+    // 3 NQ warps forms 4 outputs from its column's 4 + 2R x-sums held in
     // registers, in the same fma order as the per-output 7-tap sum
-    constexpr int YH = k3::TY / 2;
-    // the column pass runs on the highest 6 warps and the x-pass on the
-    // lowest 7, so fewer warps carry both (K3 0.970 -> 0.966 ms)
-    const int yt = (int)threadIdx.x - (NT - 192);
-    const int yc = yt >= 0 ? yt >> 6 : 3, yh = (yt >> 5) & 1;
+    constexpr int YH = 4, NQ = k3::NQ;
+    // the column pass runs on the highest warps and the x-pass on the
+    // lowest, so fewer warps carry both (K3 0.970 -> 0.966 ms at TY = 8)
+    const int yt = (int)threadIdx.x - (NT - 3 * NQ * 32);
+    const int yc = yt >= 0 ? yt / (NQ * 32) : 3, yh = (yt >> 5) % NQ;
     auto y_pass = [&](const double* in, double* out) {
         if (yc >= 3) return;
         double v[YH + 2 * R];
