@@ -139,6 +139,17 @@ void engine_alloc(wlm_engine* e) {
         e->AV = DevBuf<float>(ctx, B * 3 * n);
         CK(cudaMemsetAsync(e->AM.p, 0, sizeof(float) * B * 3 * n, ctx->stream));
         CK(cudaMemsetAsync(e->AV.p, 0, sizeof(float) * B * 3 * n, ctx->stream));
+        // bias corrections 1 - beta^t with the host's std::pow (the oracle's)
+        const int nt = e->P.trace_cap + 1;
+        std::vector<double> bc(2 * (size_t)nt);
+        for (int t = 1; t <= nt; ++t) {
+            bc[t - 1] = 1.0 - std::pow(e->P.adam_b1, t);
+            bc[nt + t - 1] = 1.0 - std::pow(e->P.adam_b2, t);
+        }
+        e->ABC = DevBuf<double>(ctx, bc.size());
+        CK(cudaMemcpy(e->ABC.p, bc.data(), sizeof(double) * bc.size(), cudaMemcpyHostToDevice));
+        e->P.adam_bc = e->ABC.p;
+        e->P.adam_bc_n = nt;
     }
     e->st = DevBuf<PairState>(ctx, B);
     CK(cudaMemsetAsync(e->st.p, 0, sizeof(PairState) * B, ctx->stream));

@@ -65,6 +65,10 @@ __device__ double block_sum(double v, double* red) {
 }
 
 // Adam, pointwise; t = accepted iterations + 1 at this level.
+// fp64 arithmetic with fp32 storage of m, v and the step, in the oracle's
+// operation order (orc_adam_step: no fused multiply-adds, IEEE division and
+// square root, bias corrections from the host's std::pow), so the stored
+// values are the fp32-storage oracle's bit for bit.
 __global__ void k_adam(Batch b, LmParams p) {
     const int pair = b.pair0 + blockIdx.y;
     const PairState* st = b.st + pair;
@@ -73,22 +77,24 @@ __global__ void k_adam(Batch b, LmParams p) {
     float* G = b.G + (long long)pair * n3;
     float* Mm = b.AM + (long long)pair * n3;
     float* Vv = b.AV + (long long)pair * n3;
-    const int t = st->iter + 1;
-    const float b1 = (float)p.adam_b1, b2 = (float)p.adam_b2;
-    const float bc1 = (float)(1.0 - pow(p.adam_b1, t)), bc2 = (float)(1.0 - pow(p.adam_b2, t));
-    const float lr = (float)p.adam_lr, ep = (float)p.adam_eps;
+    const int t = min(st->iter + 1, p.adam_bc_n);
+    const double b1 = p.adam_b1, b2 = p.adam_b2;
+    const double c1 = __dadd_rn(1.0, -b1), c2 = __dadd_rn(1.0, -b2);
+    const double bc1 = p.adam_bc[t - 1], bc2 = p.adam_bc[p.adam_bc_n + t - 1];
+    const double lr = p.adam_lr, ep = p.adam_eps;
     // owned planes of each component (slab halos are refreshed by exchange)
     const long long nxy = (long long)b.g.nx * b.g.ny;
     const long long lo = (b.g.zs - b.g.zlo) * nxy, cnt = (b.g.ze - b.g.zs) * nxy;
     for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < 3 * cnt;
          j += (long long)gridDim.x * blockDim.x) {
         const long long i = (j / cnt) * n + lo + j % cnt;
-        const float gi = G[i];
-        const float m = fmaf(b1, Mm[i], (1.f - b1) * gi);
-        const float v = fmaf(b2, Vv[i], (1.f - b2) * gi * gi);
+        const double gi = G[i];
+        const float m = (float)__dadd_rn(__dmul_rn(b1, (double)Mm[i]), __dmul_rn(c1, gi));
+        const float v = (float)__dadd_rn(__dmul_rn(b2, (double)Vv[i]), __dmul_rn(__dmul_rn(c2, gi), gi));
         Mm[i] = m;
         Vv[i] = v;
-        G[i] = -lr * (m / bc1) / (sqrtf(v / bc2) + ep);
+        const double mh = __ddiv_rn((double)m, bc1), vh = __ddiv_rn((double)v, bc2);
+        G[i] = (float)__ddiv_rn(__dmul_rn(-lr, mh), __dadd_rn(__dsqrt_rn(vh), ep));
     }
 }
 

@@ -43,6 +43,10 @@ struct LmParams {
     double mu_plus, mu_minus, lambda_max, tau;
     double target, step_floor;
     double adam_b1, adam_b2, adam_eps, adam_lr, gd_lr;
+    // Adam bias corrections 1 - beta^t for t = 1 .. adam_bc_n (host
+    // std::pow, the oracle's own values): [0][t-1] beta1, [1][t-1] beta2
+    const double* adam_bc;
+    int adam_bc_n;
     int rejection, max_retries, optimizer, log_jacobian;
     int trace_cap;
     int script_n;

@@ -10,7 +10,8 @@ tests/golden/fullsize_<name>.npz with
                with the same oracle synth_pair and checks the hash)
   <var>_trace  per accepted iteration: level, iter, r, lambda, accepted,
                retries  (var = fp64 | fp32)
-  <var>_warp_s the final warp at a fixed sample of voxels (fp64; AoS x, y, z)
+  <var>_warp_s the final warp at a fixed sample of voxels (rounded to fp32,
+               the device's storage precision; AoS x, y, z)
   <var>_warp_norm  the whole final warp's L2 norm
   sample_idx   the sampled flat voxel indices (seeded, sorted)
 
@@ -80,7 +81,7 @@ def run(name):
         assert rc == 0, (name, var, rc)
         flat = w.reshape(-1, 3)
         out[f"{var}_trace"] = trace_array(tr)
-        out[f"{var}_warp_s"] = flat[out["sample_idx"]].copy()
+        out[f"{var}_warp_s"] = flat[out["sample_idx"]].astype(np.float32)  # the device stores fp32
         out[f"{var}_warp_norm"] = np.array(np.linalg.norm(w))
         out[f"{var}_jac"] = np.array(jac)
         print(f"{name} {var}: {len(tr)} iterations, {sum(int(t.retries) for t in tr)} retries, "
