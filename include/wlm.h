@@ -6,8 +6,10 @@
  *
  *   reference interface (file:line)                      replaced by
  *   --------------------------------------------------   ------------------------------
- *   field.hpp:82   sample_trilinear                      wlm_warp_volume (whole volume)
- *   field.hpp:90   sample_trilinear_grad                 wlm_warp_volume (+ gradient)
+ *   field.hpp:82   sample_trilinear                      wlm_sample_trilinear_grad_points,
+ *                                                        wlm_warp_volume (whole volume)
+ *   field.hpp:90   sample_trilinear_grad                 wlm_sample_trilinear_grad_points,
+ *                                                        wlm_warp_volume (+ gradient)
  *   field.hpp:93   sample_field                          wlm_sample_field_points
  *   field.hpp:96   compose_warp                          wlm_compose_warp
  *   field.hpp:99   max_abs_component                     wlm_max_abs_component
@@ -36,7 +38,9 @@
  * Host-buffer entry points take the reference's own layout: fp64, x-fastest
  * (field.hpp:25-30), displacement fields component-innermost AoS
  * (field.hpp:50-58).  They upload, run on the GPU and download, like a
- * by-value reference call.  Device entry points (wlm_dev_*) take fp32
+ * by-value reference call; the field-module mirrors keep the data fp64 and
+ * evaluate the reference's expressions in its operation order, so they
+ * return the reference function's bits.  Device entry points (wlm_dev_*) take fp32
  * structure-of-arrays device pointers (one plane per component) and run on
  * the context's stream with no host synchronisation.
  *
@@ -148,6 +152,11 @@ const char* wlm_source_hash(void);
 /* ---- host-buffer mirror of the reference field module (fp64, AoS) ---- */
 wlm_status wlm_warp_volume(wlm_ctx* ctx, const double* M, const double* u, wlm_dims d,
                            double* Mw, double* gradM /* nullable */);
+/* sample_trilinear(_grad) at npts points p = pts[3i..3i+2] (x, y, z): value
+ * and analytic gradient (field.cpp:43-90, NaN value for a non-finite p). */
+wlm_status wlm_sample_trilinear_grad_points(wlm_ctx* ctx, const double* vol, wlm_dims d,
+                                            const double* pts /* 3*npts */, size_t npts,
+                                            double* val /* npts */, double* grad /* 3*npts, nullable */);
 wlm_status wlm_sample_field_points(wlm_ctx* ctx, const double* u, wlm_dims d,
                                    const double* pts /* 3*npts */, size_t npts,
                                    double* out /* 3*npts */);

@@ -23,6 +23,7 @@
 //   register                  SPEC.md:362      register_pair -> RegResult   runtime_error (non-finite)
 #pragma once
 
+#include <array>
 #include <cstddef>
 #include <memory>
 #include <stdexcept>
@@ -69,6 +70,38 @@ inline void check(wlm_status s, const Context& c) {
 template <class D>
 wlm_dims dims_of(const D& d) {
     return wlm_dims{d.nx, d.ny, d.nz};
+}
+
+// sample_trilinear / sample_trilinear_grad (field.hpp:82-90) at one point;
+// Vec3 is std::array<double, 3> (field.hpp:10), SampleGrad {value, grad}.
+struct SampleGrad {
+    double value = 0.0;
+    std::array<double, 3> grad{0.0, 0.0, 0.0};
+};
+
+template <class Volume>
+SampleGrad sample_trilinear_grad(const Volume& vol, double px, double py, double pz,
+                                 Context& c = default_context()) {
+    const double p[3] = {px, py, pz};
+    SampleGrad s;
+    check(wlm_sample_trilinear_grad_points(c.get(), vol.data.data(), dims_of(vol.dims), p, 1, &s.value,
+                                           s.grad.data()),
+          c);
+    return s;
+}
+
+template <class Volume>
+double sample_trilinear(const Volume& vol, double px, double py, double pz, Context& c = default_context()) {
+    return sample_trilinear_grad(vol, px, py, pz, c).value;
+}
+
+// sample_field (field.hpp:93): the three components at one point.
+template <class Field>
+std::array<double, 3> sample_field(const Field& u, double px, double py, double pz, Context& c = default_context()) {
+    const double p[3] = {px, py, pz};
+    std::array<double, 3> out{};
+    check(wlm_sample_field_points(c.get(), u.data.data(), dims_of(u.dims), p, 1, out.data()), c);
+    return out;
 }
 
 template <class Field>
@@ -160,6 +193,48 @@ ResidualReport<Field> residual_mi(const Volume& F, const Volume& M, const Field&
                           &rep.r, &rep.loss_raw, rep.g.data.data()),
           c);
     return rep;
+}
+
+// lm_step_pointwise: -r g / (|g|^2 + lambda) per voxel.
+template <class Field>
+Field lm_step_pointwise(double r, const Field& g, double lambda, Context& c = default_context()) {
+    Field out(g.dims);
+    check(wlm_lm_step_pointwise(c.get(), r, g.data.data(), dims_of(g.dims), lambda, out.data.data()), c);
+    return out;
+}
+
+// update_damping / rejection_test: host scalar state, the
+// arithmetic the device state machine runs.
+inline void update_damping(wlm_lm_state& s, double loss_new, const wlm_lm_config& cfg) {
+    wlm_update_damping(&s, loss_new, &cfg);
+}
+inline bool rejection_test(double loss_new, double loss_prev, double loss_prev2, double tau) {
+    return wlm_rejection_test(loss_new, loss_prev, loss_prev2, tau) != 0;
+}
+
+// downsample: Gaussian sigma 0.5 f, stride f, dims ceil(n / f).
+template <class Volume>
+Volume downsample(const Volume& vol, int factor, Context& c = default_context()) {
+    wlm_dims nd{};
+    const int f = factor < 1 ? 1 : factor;
+    std::vector<double> tmp(((std::size_t)(vol.dims.nx + f - 1) / f) * ((vol.dims.ny + f - 1) / f) *
+                            ((vol.dims.nz + f - 1) / f));
+    check(wlm_downsample(c.get(), vol.data.data(), dims_of(vol.dims), factor, tmp.data(), &nd), c);
+    decltype(vol.dims) od = vol.dims;
+    od.nx = nd.nx;
+    od.ny = nd.ny;
+    od.nz = nd.nz;
+    Volume out(od);
+    out.data = std::move(tmp);
+    return out;
+}
+
+// upsample_warp: trilinear at x / scale, values * scale.
+template <class Field, class Dims>
+Field upsample_warp(const Field& u, const Dims& new_dims, double scale, Context& c = default_context()) {
+    Field out(new_dims);
+    check(wlm_upsample_warp(c.get(), u.data.data(), dims_of(u.dims), dims_of(new_dims), scale, out.data.data()), c);
+    return out;
 }
 
 template <class Field>

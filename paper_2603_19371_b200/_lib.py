@@ -86,6 +86,7 @@ SIGNATURES = {
     "wlm_source_hash": (C.c_char_p, []),
     "wlm_warp_volume": (C.c_int, [_CTX, _D, _D, Dims, _D, _D]),
     "wlm_sample_field_points": (C.c_int, [_CTX, _D, Dims, _D, C.c_size_t, _D]),
+    "wlm_sample_trilinear_grad_points": (C.c_int, [_CTX, _D, Dims, _D, C.c_size_t, _D, _D]),
     "wlm_compose_warp": (C.c_int, [_CTX, _D, Dims, _D, Dims, C.c_double, _D]),
     "wlm_max_abs_component": (C.c_int, [_CTX, _D, Dims, _D]),
     "wlm_normalize_step": (C.c_int, [_CTX, _D, Dims, C.c_double, C.c_double, _D]),

@@ -365,6 +365,23 @@ namespace wlm {
 wlm_status engine_init(wlm_engine* e, wlm_ctx* ctx, wlm_dims d, int pairs, const wlm_reg_config* c);
 void engine_alloc(wlm_engine* e);
 void clear_adam_moments(wlm_engine* e, cudaStream_t s);
+// fp64 reference-order field kernels (field64.cu)
+std::vector<double> gaussian_taps64(double sigma, int* R);
+void launch_warp_volume64(const double* M, const double* u, wlm_dims d, double* Mw, double* gM, cudaStream_t s);
+void launch_compose64(const double* u, const double* v, double eps, wlm_dims d, double* out, cudaStream_t s);
+void launch_sample_points64(const double* u, wlm_dims d, const double* pts, long long npts, double* out,
+                            cudaStream_t s);
+void launch_sample_grad_points64(const double* v, wlm_dims d, const double* pts, long long npts, double* val,
+                                 double* grad, cudaStream_t s);
+void launch_max_abs64(const double* v, long long count, unsigned long long* out, cudaStream_t s);
+void launch_jacobian_min64(const double* u, wlm_dims d, unsigned long long* out, cudaStream_t s);
+double jacobian_key_to_double(unsigned long long k);
+unsigned long long jacobian_key_init();
+void smooth64(double* data, double* tmp, const double* dw, int R, wlm_dims d, int nchan, long long cstride,
+              long long estride, cudaStream_t s);
+void launch_lm_step64(double r, const double* g, long long n, double lambda, double* out, cudaStream_t s);
+void launch_stride64(const double* in, wlm_dims d, int f, double* out, wlm_dims nd, cudaStream_t s);
+void launch_upsample64(const double* u, wlm_dims d, wlm_dims nd, double scale, double* out, cudaStream_t s);
 std::vector<PairState> read_states(wlm_engine* e);
 void copy_warps_in(wlm_engine* e, const float* u, int is_host);
 }  // namespace wlm

@@ -309,24 +309,6 @@ inline int grid_for(long long n, int threads) {
 }
 }  // namespace
 
-__global__ void k_compose(const float* __restrict__ u, const float* __restrict__ v, float eps,
-                          float* __restrict__ out, Geo g) {
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < g.n;
-         i += (long long)gridDim.x * blockDim.x) {
-        const int x = (int)(i % g.nx), y = (int)((i / g.nx) % g.ny), z = (int)(i / ((long long)g.nx * g.ny));
-        const float dx = eps * v[i], dy = eps * v[g.n + i], dz = eps * v[2 * g.n + i];
-        const Cell c = make_cell(g, x, y, z, dx, dy, dz);
-        out[i] = dx + cell_sample(u, c);
-        out[g.n + i] = dy + cell_sample(u + g.n, c);
-        out[2 * g.n + i] = dz + cell_sample(u + 2 * g.n, c);
-    }
-}
-
-void launch_compose(const float* u, const float* v, float eps, float* out, const Geo& g, cudaStream_t s) {
-    k_compose<<<grid_for(g.n, 256), 256, 0, s>>>(u, v, eps, out, g);
-    ++g_kernel_launches;
-}
-
 // One separable Gaussian pass along `axis` for all channels (generic radius,
 // truncated at max(1, ceil(3 sigma)) and renormalised, field.cpp:205-269).
 struct Taps {
@@ -372,21 +354,6 @@ void launch_smooth_generic(const float* in, float* out, float* tmp, int nchan, c
     k_smooth_axis<<<blocks, 256, 0, s>>>(out, tmp, nchan, g, 1, t);
     k_smooth_axis<<<blocks, 256, 0, s>>>(tmp, out, nchan, g, 2, t);
     g_kernel_launches += 3;
-}
-
-__global__ void k_warp(const float* __restrict__ M, const float* __restrict__ u, float* Mw, float* gM, Geo g) {
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < g.n;
-         i += (long long)gridDim.x * blockDim.x) {
-        const int x = (int)(i % g.nx), y = (int)((i / g.nx) % g.ny), z = (int)(i / ((long long)g.nx * g.ny));
-        float a, b, c;
-        Mw[i] = sample_grad(M, g, x, y, z, u[i], u[g.n + i], u[2 * g.n + i], a, b, c);
-        if (gM) { gM[i] = a; gM[g.n + i] = b; gM[2 * g.n + i] = c; }
-    }
-}
-
-void launch_warp(const float* M, const float* u, float* Mw, float* gM, const Geo& g, cudaStream_t s) {
-    k_warp<<<grid_for(g.n, 256), 256, 0, s>>>(M, u, Mw, gM, g);
-    ++g_kernel_launches;
 }
 
 __global__ void k_max_abs(const float* __restrict__ v, long long count, unsigned* out) {
@@ -436,19 +403,6 @@ void launch_jacdet(const float* u, const Geo& g, int* out_ordered, cudaStream_t 
     ++g_kernel_launches;
 }
 
-__global__ void k_lm_pointwise(float r, const float* __restrict__ g, float lam, float* out, long long n) {
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
-         i += (long long)gridDim.x * blockDim.x) {
-        const float a = g[i], b = g[n + i], c = g[2 * n + i];
-        const float s = -r / (fmaf(a, a, fmaf(b, b, c * c)) + lam);
-        out[i] = s * a; out[n + i] = s * b; out[2 * n + i] = s * c;
-    }
-}
-
-void launch_lm_pointwise(double r, const float* g, double lambda, float* out, long long n, cudaStream_t s) {
-    k_lm_pointwise<<<grid_for(n, 256), 256, 0, s>>>((float)r, g, (float)lambda, out, n);
-    ++g_kernel_launches;
-}
 
 // -r (H + lambda I)^{-1} by the adjugate, rounding steps as the oracle's
 // tile_step_matrix (no contraction).
@@ -634,19 +588,6 @@ void launch_upsample(const float* u, const Geo& g, const Geo& gd, float scale, f
     ++g_kernel_launches;
 }
 
-__global__ void k_sample_points(const float* __restrict__ u, Geo g, const double* pts, long long npts, double* out) {
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < npts;
-         i += (long long)gridDim.x * blockDim.x) {
-        const Cell c = cell_at_point(g, pts[3 * i], pts[3 * i + 1], pts[3 * i + 2]);
-        for (int ch = 0; ch < 3; ++ch) out[3 * i + ch] = (double)cell_sample(u + ch * g.n, c);
-    }
-}
-
-void launch_sample_points(const float* u, const Geo& g, const double* pts, long long npts, double* out,
-                          cudaStream_t s) {
-    k_sample_points<<<grid_for(npts, 256), 256, 0, s>>>(u, g, pts, npts, out);
-    ++g_kernel_launches;
-}
 
 __global__ void k_aos_to_soa(const double* __restrict__ in, float* __restrict__ out, long long n, int nchan) {
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n * nchan;

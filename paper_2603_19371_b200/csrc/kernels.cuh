@@ -146,13 +146,11 @@ void launch_shifts(const Batch& b, cudaStream_t s);
 // Device constants (window-count reciprocals); idempotent.
 void init_constants();
 
-// ---- standalone field ops (fp32 SoA device buffers) ----
-void launch_compose(const float* u, const float* v, float eps, float* out, const Geo& g,
-                    cudaStream_t s);
+// ---- generator helpers (synth_pair; fp32 SoA device buffers) ----
+
 void launch_smooth_generic(const float* in, float* out, float* tmp, int nchan, const Geo& g,
                            double sigma, cudaStream_t s);
-void launch_warp(const float* M, const float* u, float* Mw, float* gM, const Geo& g,
-                 cudaStream_t s);
+
 void launch_max_abs(const float* v, long long count, unsigned* out_bits, cudaStream_t s);
 void launch_jacdet(const float* u, const Geo& g, int* out_ordered, cudaStream_t s);
 // Tiled LM (Eq. 5): per-tile -r (H + lambda I)^{-1}, H = sum g g^T.
@@ -170,16 +168,14 @@ __device__ __forceinline__ void demons_step(double rx, double a, double b, doubl
 }
 void launch_demons_pointwise(const double* r, const double* n, long long N, double alpha, double* out,
                              cudaStream_t s);
-void launch_lm_pointwise(double r, const float* g, double lambda, float* out, long long n,
-                         cudaStream_t s);
+
 void launch_nonfinite(const float* v, long long count, int* flag, cudaStream_t s);
 // Gaussian(sigma = 0.5 f) + stride f in one fp64 pass (pyramid levels).
 void launch_downsample_gauss(const float* in, const Geo& g, int f, float* out, const Geo& gd,
                              cudaStream_t s);
 void launch_upsample(const float* u, const Geo& g, const Geo& gd, float scale, float* out,
                      cudaStream_t s);
-void launch_sample_points(const float* u, const Geo& g, const double* pts, long long npts,
-                          double* out, cudaStream_t s);
+
 // AoS fp64 <-> SoA fp32 conversions.
 void launch_aos_to_soa(const double* in, float* out, long long n, int nchan, cudaStream_t s);
 void launch_soa_to_aos(const float* in, double* out, long long n, int nchan, cudaStream_t s);

@@ -1,7 +1,11 @@
 // ops.cu -- host-buffer mirror of the reference API (fp64 AoS in/out, like a
-// by-value warplm:: call) and the register() pyramid driver.  Each entry
-// point uploads, converts to the device layout (fp32 SoA), runs sm_100a
-// kernels, and converts back.  No CPU compute path exists.
+// by-value warplm:: call) and the register() pyramid driver.  The `field`
+// mirrors (warp_volume, sample_field, compose_warp, max_abs_component,
+// normalize_step, jacobian_det_min, gaussian_smooth, lm_step_pointwise,
+// downsample, upsample_warp) keep the caller's fp64 AoS data and run the
+// reference's arithmetic in its operation order on the device (field64.cu),
+// so they return the reference's bits.  The residual mirrors run the
+// engine's own hot kernels.  No CPU compute path exists.
 #include <cmath>
 #include <limits>
 #include <vector>
@@ -29,27 +33,51 @@ void download_aos(wlm_ctx* ctx, const float* dev, size_t n, int nchan, double* h
     CK(cudaStreamSynchronize(ctx->stream));
 }
 
-float read_max(wlm_ctx* ctx, const float* v, long long count) {
-    DevBuf<unsigned> bits(ctx, 1);
-    CK(cudaMemsetAsync(bits.p, 0, sizeof(unsigned), ctx->stream));
-    launch_max_abs(v, count, bits.p, ctx->stream);
-    unsigned h = 0;
-    CK(cudaMemcpyAsync(&h, bits.p, sizeof(unsigned), cudaMemcpyDeviceToHost, ctx->stream));
-    CK(cudaStreamSynchronize(ctx->stream));
-    float f;
-    std::memcpy(&f, &h, 4);
-    return f;
+
+
+DevBuf<double> upload64(wlm_ctx* ctx, const double* host, size_t count) {
+    DevBuf<double> d(ctx, count);
+    CK(cudaMemcpyAsync(d.p, host, sizeof(double) * count, cudaMemcpyHostToDevice, ctx->stream));
+    return d;
 }
 
-double read_jacdet(wlm_ctx* ctx, const float* u, const Geo& g) {
-    DevBuf<int> o(ctx, 1);
-    const int inf_bits = 0x7f800000;
-    CK(cudaMemcpyAsync(o.p, &inf_bits, sizeof(int), cudaMemcpyHostToDevice, ctx->stream));
-    launch_jacdet(u, g, o.p, ctx->stream);
-    int h = 0;
-    CK(cudaMemcpyAsync(&h, o.p, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+void download64(wlm_ctx* ctx, const double* dev, size_t count, double* host) {
+    CK(cudaMemcpyAsync(host, dev, sizeof(double) * count, cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
-    return (double)ordered_to_float(h);
+}
+
+double read_max64(wlm_ctx* ctx, const double* v, long long count) {
+    DevBuf<unsigned long long> bits(ctx, 1);
+    CK(cudaMemsetAsync(bits.p, 0, sizeof(unsigned long long), ctx->stream));
+    launch_max_abs64(v, count, bits.p, ctx->stream);
+    unsigned long long h = 0;
+    CK(cudaMemcpyAsync(&h, bits.p, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    double m;
+    std::memcpy(&m, &h, 8);
+    return m;
+}
+
+// jacobian_det_min of an fp64 AoS device field (field.cpp:172-201)
+double read_jacdet64(wlm_ctx* ctx, const double* u, wlm_dims d) {
+    DevBuf<unsigned long long> o(ctx, 1);
+    const unsigned long long init = jacobian_key_init();
+    CK(cudaMemcpyAsync(o.p, &init, sizeof(init), cudaMemcpyHostToDevice, ctx->stream));
+    launch_jacobian_min64(u, d, o.p, ctx->stream);
+    unsigned long long h = 0;
+    CK(cudaMemcpyAsync(&h, o.p, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    return jacobian_key_to_double(h);
+}
+
+// gaussian_smooth of an fp64 AoS device array in place (field.cpp:253-269)
+void smooth_aos64(wlm_ctx* ctx, double* data, wlm_dims d, int nchan, double sigma) {
+    if (sigma <= 0.0) return;  // field.cpp:254, :263
+    int R = 0;
+    const std::vector<double> w = gaussian_taps64(sigma, &R);
+    DevBuf<double> dw = upload64(ctx, w.data(), w.size()), tmp(ctx, nvox(d) * nchan);
+    smooth64(data, tmp.p, dw.p, R, d, nchan, 1, nchan, ctx->stream);
+    CK(cudaStreamSynchronize(ctx->stream));
 }
 
 wlm_status bad(wlm_ctx* ctx, wlm_status s, const char* msg) {
@@ -66,12 +94,25 @@ wlm_status wlm_warp_volume(wlm_ctx* ctx, const double* M, const double* u, wlm_d
     if (!M || !u || !Mw || !valid_dims(d)) return bad(ctx, WLM_INVALID_ARG, "warp_volume: bad args");
     return run(ctx, [&] {
         const size_t n = nvox(d);
-        const Geo g = make_geo(d);
-        DevBuf<float> dM = upload_soa(ctx, M, n, 1), du = upload_soa(ctx, u, n, 3);
-        DevBuf<float> dw(ctx, n), dg(ctx, gradM ? 3 * n : 0);
-        launch_warp(dM.p, du.p, dw.p, gradM ? dg.p : nullptr, g, ctx->stream);
-        download_aos(ctx, dw.p, n, 1, Mw);
-        if (gradM) download_aos(ctx, dg.p, n, 3, gradM);
+        DevBuf<double> dM = upload64(ctx, M, n), du = upload64(ctx, u, 3 * n);
+        DevBuf<double> dw(ctx, n), dg(ctx, gradM ? 3 * n : 0);
+        launch_warp_volume64(dM.p, du.p, d, dw.p, gradM ? dg.p : nullptr, ctx->stream);
+        download64(ctx, dw.p, n, Mw);
+        if (gradM) download64(ctx, dg.p, 3 * n, gradM);
+    });
+}
+
+// sample_trilinear / sample_trilinear_grad at arbitrary points
+// (field.cpp:43-90): value and analytic interpolant gradient, fp64.
+wlm_status wlm_sample_trilinear_grad_points(wlm_ctx* ctx, const double* vol, wlm_dims d, const double* pts,
+                                            size_t npts, double* val, double* grad) {
+    if (!vol || !pts || !val || !valid_dims(d)) return bad(ctx, WLM_INVALID_ARG, "sample_trilinear: bad args");
+    return run(ctx, [&] {
+        DevBuf<double> dv = upload64(ctx, vol, nvox(d)), dp = upload64(ctx, pts, 3 * npts);
+        DevBuf<double> dval(ctx, npts), dg(ctx, grad ? 3 * npts : 0);
+        launch_sample_grad_points64(dv.p, d, dp.p, (long long)npts, dval.p, grad ? dg.p : nullptr, ctx->stream);
+        download64(ctx, dval.p, npts, val);
+        if (grad) download64(ctx, dg.p, 3 * npts, grad);
     });
 }
 
@@ -80,12 +121,9 @@ wlm_status wlm_sample_field_points(wlm_ctx* ctx, const double* u, wlm_dims d, co
     if (!u || !pts || !out || !valid_dims(d)) return bad(ctx, WLM_INVALID_ARG, "sample_field: bad args");
     return run(ctx, [&] {
         const size_t n = nvox(d);
-        DevBuf<float> du = upload_soa(ctx, u, n, 3);
-        DevBuf<double> dp(ctx, 3 * npts), dout(ctx, 3 * npts);
-        CK(cudaMemcpyAsync(dp.p, pts, sizeof(double) * 3 * npts, cudaMemcpyHostToDevice, ctx->stream));
-        launch_sample_points(du.p, make_geo(d), dp.p, (long long)npts, dout.p, ctx->stream);
-        CK(cudaMemcpyAsync(out, dout.p, sizeof(double) * 3 * npts, cudaMemcpyDeviceToHost, ctx->stream));
-        CK(cudaStreamSynchronize(ctx->stream));
+        DevBuf<double> du = upload64(ctx, u, 3 * n), dp = upload64(ctx, pts, 3 * npts), dout(ctx, 3 * npts);
+        launch_sample_points64(du.p, d, dp.p, (long long)npts, dout.p, ctx->stream);
+        download64(ctx, dout.p, 3 * npts, out);
     });
 }
 
@@ -98,9 +136,9 @@ wlm_status wlm_compose_warp(wlm_ctx* ctx, const double* u, wlm_dims du, const do
     if (!same_dims(du, dv)) return bad(ctx, WLM_DIM_MISMATCH, "compose_warp: dimension mismatch");
     return run(ctx, [&] {
         const size_t n = nvox(du);
-        DevBuf<float> a = upload_soa(ctx, u, n, 3), b = upload_soa(ctx, v, n, 3), o(ctx, 3 * n);
-        launch_compose(a.p, b.p, (float)eps, o.p, make_geo(du), ctx->stream);
-        download_aos(ctx, o.p, n, 3, out);
+        DevBuf<double> a = upload64(ctx, u, 3 * n), b = upload64(ctx, v, 3 * n), o(ctx, 3 * n);
+        launch_compose64(a.p, b.p, eps, du, o.p, ctx->stream);
+        download64(ctx, o.p, 3 * n, out);
     });
 }
 
@@ -108,8 +146,8 @@ wlm_status wlm_max_abs_component(wlm_ctx* ctx, const double* v, wlm_dims d, doub
     if (!v || !out || !valid_dims(d)) return bad(ctx, WLM_INVALID_ARG, "max_abs_component: bad args");
     return run(ctx, [&] {
         const size_t n = nvox(d);
-        DevBuf<float> a = upload_soa(ctx, v, n, 3);
-        *out = (double)read_max(ctx, a.p, (long long)(3 * n));
+        DevBuf<double> a = upload64(ctx, v, 3 * n);
+        *out = read_max64(ctx, a.p, (long long)(3 * n));
     });
 }
 
@@ -130,20 +168,19 @@ wlm_status wlm_jacobian_det_min(wlm_ctx* ctx, const double* u, wlm_dims d, doubl
     if (d.nx < 2 || d.ny < 2 || d.nz < 2)
         return bad(ctx, WLM_INVALID_ARG, "jacobian_det_min: dims must be >= 2 per axis");
     return run(ctx, [&] {
-        DevBuf<float> a = upload_soa(ctx, u, nvox(d), 3);
-        *out = read_jacdet(ctx, a.p, make_geo(d));
+        DevBuf<double> a = upload64(ctx, u, 3 * nvox(d));
+        *out = read_jacdet64(ctx, a.p, d);
     });
 }
 
 static wlm_status smooth_common(wlm_ctx* ctx, const double* in, wlm_dims d, double sigma, double* out,
                                 int nchan) {
     if (!in || !out || !valid_dims(d)) return bad(ctx, WLM_INVALID_ARG, "gaussian_smooth: bad args");
-    if (sigma > 21.0) return bad(ctx, WLM_UNSUPPORTED, "gaussian_smooth: sigma > 21 (radius > 64)");
     return run(ctx, [&] {
-        const size_t n = nvox(d);
-        DevBuf<float> a = upload_soa(ctx, in, n, nchan), o(ctx, nchan * n), t(ctx, nchan * n);
-        launch_smooth_generic(a.p, o.p, t.p, nchan, make_geo(d), sigma, ctx->stream);
-        download_aos(ctx, o.p, n, nchan, out);
+        const size_t n = nvox(d) * nchan;
+        DevBuf<double> a = upload64(ctx, in, n);
+        smooth_aos64(ctx, a.p, d, nchan, sigma);  // any sigma (radius ceil(3 sigma), field.cpp:206)
+        download64(ctx, a.p, n, out);
     });
 }
 
@@ -324,9 +361,9 @@ wlm_status wlm_lm_step_pointwise(wlm_ctx* ctx, double r, const double* g, wlm_di
         return bad(ctx, WLM_INVALID_ARG, "lm_step_pointwise: bad args (lambda > 0)");
     return run(ctx, [&] {
         const size_t n = nvox(d);
-        DevBuf<float> a = upload_soa(ctx, g, n, 3), o(ctx, 3 * n);
-        launch_lm_pointwise(r, a.p, lambda, o.p, (long long)n, ctx->stream);
-        download_aos(ctx, o.p, n, 3, out);
+        DevBuf<double> a = upload64(ctx, g, 3 * n), o(ctx, 3 * n);
+        launch_lm_step64(r, a.p, (long long)n, lambda, o.p, ctx->stream);
+        download64(ctx, o.p, 3 * n, out);
     });
 }
 
@@ -359,11 +396,12 @@ wlm_status wlm_downsample(wlm_ctx* ctx, const double* vol, wlm_dims d, int facto
     if (out_dims) *out_dims = nd;
     return run(ctx, [&] {
         const size_t n = nvox(d);
-        DevBuf<float> a = upload_soa(ctx, vol, n, 1);
-        if (factor == 1) { download_aos(ctx, a.p, n, 1, out); return; }
-        DevBuf<float> o(ctx, nvox(nd));
-        launch_downsample_gauss(a.p, make_geo(d), factor, o.p, make_geo(nd), ctx->stream);
-        download_aos(ctx, o.p, nvox(nd), 1, out);
+        DevBuf<double> a = upload64(ctx, vol, n);
+        if (factor == 1) { download64(ctx, a.p, n, out); return; }
+        smooth_aos64(ctx, a.p, d, 1, 0.5 * factor);  // Gaussian sigma = 0.5 f
+        DevBuf<double> o(ctx, nvox(nd));
+        launch_stride64(a.p, d, factor, o.p, nd, ctx->stream);
+        download64(ctx, o.p, nvox(nd), out);
     });
 }
 
@@ -373,9 +411,9 @@ wlm_status wlm_upsample_warp(wlm_ctx* ctx, const double* u, wlm_dims d, wlm_dims
     if (!u || !out || !valid_dims(d) || !valid_dims(nd) || !(scale > 0.0))
         return bad(ctx, WLM_INVALID_ARG, "upsample_warp: invalid dims");
     return run(ctx, [&] {
-        DevBuf<float> a = upload_soa(ctx, u, nvox(d), 3), o(ctx, 3 * nvox(nd));
-        launch_upsample(a.p, make_geo(d), make_geo(nd), (float)scale, o.p, ctx->stream);
-        download_aos(ctx, o.p, nvox(nd), 3, out);
+        DevBuf<double> a = upload64(ctx, u, 3 * nvox(d)), o(ctx, 3 * nvox(nd));
+        launch_upsample64(a.p, d, nd, scale, o.p, ctx->stream);
+        download64(ctx, o.p, 3 * nvox(nd), out);
     });
 }
 
@@ -466,8 +504,16 @@ wlm_status wlm_register(wlm_ctx* ctx, const float* F, const float* M, wlm_dims d
         const std::vector<PairState> ps = read_states(prev);
         const float* uf = prev->U.p + (size_t)ps[0].cur * 3 * n;
         download_aos(ctx, uf, n, 3, warp_out);
-        if (jac_final) *jac_final = d.nx >= 2 && d.ny >= 2 && d.nz >= 2 ? read_jacdet(ctx, uf, g0)
-                                                                        : std::numeric_limits<double>::quiet_NaN();
+        if (jac_final) {
+            if (d.nx >= 2 && d.ny >= 2 && d.nz >= 2) {
+                // the reference's fp64 jacobian_det_min of the (fp32) final warp
+                DevBuf<double> w64(ctx, 3 * n);
+                launch_soa_to_aos(uf, w64.p, (long long)n, 3, ctx->stream);
+                *jac_final = read_jacdet64(ctx, w64.p, d);
+            } else {
+                *jac_final = std::numeric_limits<double>::quiet_NaN();
+            }
+        }
         wlm_engine_destroy(prev);
     });
     if (s != WLM_OK) return s;

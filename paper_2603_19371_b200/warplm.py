@@ -41,6 +41,7 @@ from ._lib import (AdamConfig, Dims, DimensionMismatch, InvalidArgument, LmConfi
 __all__ = [
     "Context", "StepScale", "ResidualReport", "RegResult", "compose_warp", "max_abs_component",
     "normalize_step", "jacobian_det_min", "gaussian_smooth", "all_finite", "sample_field",
+    "sample_trilinear", "sample_trilinear_grad",
     "warp_volume", "residual_lncc", "lm_step_pointwise", "update_damping", "rejection_test",
     "downsample", "upsample_warp", "state_bytes", "register", "reg_config", "lm_config",
     "DimensionMismatch", "InvalidArgument", "NonFiniteLoss", "WlmError", "OPT_LM", "OPT_ADAM",
@@ -218,6 +219,24 @@ def all_finite(a, ctx=None) -> bool:
     out = C.c_int()
     c.check(c.lib.wlm_all_finite(c.h, _p(a), a.size, C.byref(out)))
     return bool(out.value)
+
+
+def sample_trilinear_grad(vol, points, ctx=None):
+    """sample_trilinear_grad (field.cpp:47-90) at N points (x, y, z): values
+    (N,) and analytic gradients (N, 3); NaN value for a non-finite point."""
+    vol = _vol(vol)
+    pts = np.ascontiguousarray(np.atleast_2d(points), dtype=np.float64)
+    c = _ctx(ctx)
+    val = np.empty(pts.shape[0])
+    grad = np.empty_like(pts)
+    c.check(c.lib.wlm_sample_trilinear_grad_points(c.h, _p(vol), _dims(vol.shape), _p(pts), pts.shape[0],
+                                                   _p(val), _p(grad)))
+    return val, grad
+
+
+def sample_trilinear(vol, points, ctx=None):
+    """sample_trilinear (field.cpp:43-45) at N points."""
+    return sample_trilinear_grad(vol, points, ctx=ctx)[0]
 
 
 def sample_field(u, points, ctx=None):
