@@ -6,7 +6,7 @@ ARCH    := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS ?= -O3 -std=c++17 -lineinfo -Xcompiler -fPIC -Xptxas -warn-spills
 PKG     := paper_2603_19371_b200
 CSRC    := $(PKG)/csrc
-SRCS    := $(CSRC)/kernels.cu $(CSRC)/hot_kernels.cu $(CSRC)/engine.cu $(CSRC)/ops.cu $(CSRC)/synth.cu $(CSRC)/slab.cu $(CSRC)/io.cu $(CSRC)/field64.cu
+SRCS    := $(CSRC)/kernels.cu $(CSRC)/hot_kernels.cu $(CSRC)/engine.cu $(CSRC)/ops.cu $(CSRC)/synth.cu $(CSRC)/slab.cu $(CSRC)/io.cu $(CSRC)/field64.cu $(CSRC)/generic.cu
 HDRS    := include/wlm.h $(CSRC)/common.cuh $(CSRC)/hot.cuh $(CSRC)/kernels.cuh $(CSRC)/internal.cuh
 OBJS    := $(patsubst $(CSRC)/%.cu,build/%.o,$(SRCS))
 LIB     := $(PKG)/libwarplm_b200.so

@@ -54,9 +54,9 @@ wlm_status engine_init(wlm_engine* e, wlm_ctx* ctx, wlm_dims d, int pairs, const
         set_err(ctx, "DEMONS needs metric = MSE (per-voxel residual, SPEC.md:166) and alpha > 0 (SPEC.md:243)");
         return WLM_INVALID_ARG;
     }
-    if (c->metric == WLM_METRIC_LNCC && c->lncc_radius != 2) {
-        set_err(ctx, "lncc_radius != 2 is not instantiated");
-        return WLM_UNSUPPORTED;
+    if (c->metric == WLM_METRIC_LNCC && c->lncc_radius < 1) {
+        set_err(ctx, "lncc_radius must be >= 1 (SPEC.md:123)");
+        return WLM_INVALID_ARG;
     }
     if ((long long)d.nx * d.ny * d.nz >= (1ll << 31)) {
         set_err(ctx, "volumes of 2^31 voxels or more are not supported (io.cpp:13 cap)");
@@ -94,14 +94,16 @@ wlm_status engine_init(wlm_engine* e, wlm_ctx* ctx, wlm_dims d, int pairs, const
     P.mi_sigma = c->mi_sigma;
     P.Ru = smooth_radius(c->sigma_update);
     P.Rw = smooth_radius(c->sigma_warp);
-    if (P.Ru > 6 || P.Rw > 6) {
-        set_err(ctx, "fused smoothing supports sigma <= 2 (radius <= 6)");
-        return WLM_UNSUPPORTED;
+    // radius <= 6 (sigma <= 2): the fused K3 / K4; larger: generic.cu
+    // half-kernels of the fused K3 / K4 (radius <= 6; LmParams holds 8 taps)
+    if (P.Ru <= 6) {
+        fill_half_kernel(c->sigma_update, P.Ru, P.wu, &P.wu_full);
+        fill_half_kernel(c->sigma_update, P.Ru, P.wud, &P.wud_full);
     }
-    fill_half_kernel(c->sigma_update, P.Ru, P.wu, &P.wu_full);
-    fill_half_kernel(c->sigma_update, P.Ru, P.wud, &P.wud_full);
-    fill_half_kernel(c->sigma_warp, P.Rw, P.wwd, &P.wwd_full);
-    fill_half_kernel(c->sigma_warp, P.Rw, P.ww, &P.ww_full);
+    if (P.Rw <= 6) {
+        fill_half_kernel(c->sigma_warp, P.Rw, P.wwd, &P.wwd_full);
+        fill_half_kernel(c->sigma_warp, P.Rw, P.ww, &P.ww_full);
+    }
     int maxit = 0;
     for (int i = 0; i < c->nlevels && i < WLM_MAX_LEVELS; ++i) maxit = std::max(maxit, c->iters[i]);
     P.trace_cap = std::max(1024, maxit + 1);
@@ -151,6 +153,19 @@ void engine_alloc(wlm_engine* e) {
         e->P.adam_bc = e->ABC.p;
         e->P.adam_bc_n = nt;
     }
+    // generic paths (generic.cu): fp64 scratch and device Gaussian taps
+    const bool gen_lncc = e->P.metric == WLM_METRIC_LNCC && e->P.radius != 2;
+    if (gen_lncc || e->P.Ru > 6 || e->P.Rw > 6) e->X64 = DevBuf<double>(ctx, B * generic_scratch_doubles(e->g));
+    auto taps = [&](double sigma, int R, DevBuf<double>& buf) -> const double* {
+        if (R <= 6) return nullptr;
+        int r = 0;
+        const std::vector<double> w = gaussian_taps64(sigma, &r);
+        buf = DevBuf<double>(ctx, w.size());
+        CK(cudaMemcpy(buf.p, w.data(), sizeof(double) * w.size(), cudaMemcpyHostToDevice));
+        return buf.p;
+    };
+    e->P.taps_u = taps(e->cfg.sigma_update, e->P.Ru, e->TAPU);
+    e->P.taps_w = taps(e->cfg.sigma_warp, e->P.Rw, e->TAPW);
     e->st = DevBuf<PairState>(ctx, B);
     CK(cudaMemsetAsync(e->st.p, 0, sizeof(PairState) * B, ctx->stream));
     const int tiles = plane_tiles(e->g);
@@ -187,6 +202,7 @@ void engine_alloc(wlm_engine* e) {
     b.TM = e->TM.p;
     b.HIST = e->HIST.p;
     b.MIT = e->MIT.p;
+    b.X64 = e->X64.p;
     b.max_blocks = tiles;
     make_tma_u(b, e->P.Rw);
     CK(cudaMemsetAsync(e->U.p, 0, sizeof(float) * B * 6 * n, ctx->stream));

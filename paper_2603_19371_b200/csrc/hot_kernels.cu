@@ -1817,8 +1817,17 @@ void launch_mse_grad(const Batch& b, const LmParams& p, cudaStream_t s) {
     ++g_kernel_launches;
 }
 
+void launch_warp_moving_grad(const Batch& b, int mode, int zf, int zl, cudaStream_t s) {
+    const dim3 wgrid(cdiv(b.g.nx, 32) * cdiv(b.g.ny, 8), cdiv(zl - zf, kZP), b.pairs);
+    k_warp_moving<true><<<wgrid, 256, 0, s>>>(b, mode, zf, zl);
+    ++g_kernel_launches;
+}
+
 void launch_lncc_fwd(const Batch& b, const LmParams& p, int mode, cudaStream_t s) {
-    (void)p;
+    if (p.radius != 2) {
+        launch_lncc_fwd_generic(b, p, mode, s);
+        return;
+    }
     // Mw for the owned planes plus the window pass's 2-plane halo
     const int zf = std::max(0, b.g.zs - 2), zl = std::min(b.g.nz, b.g.ze + 2);
     const dim3 wgrid(cdiv(b.g.nx, 32) * cdiv(b.g.ny, 8), cdiv(zl - zf, kZP), b.pairs);
@@ -1837,6 +1846,10 @@ void launch_finalize(const Batch& b, const LmParams& p, int mode, cudaStream_t s
 }
 
 void launch_lncc_bwd(const Batch& b, const LmParams& p, cudaStream_t s) {
+    if (p.radius != 2) {
+        launch_lncc_bwd_generic(b, p, s);
+        return;
+    }
     const LaunchShape sh = shape_for(b.g, b.pairs, k2::TY, b.ctas_per_sm);
     dim3 grid = sh.grid();
     grid.z = b.pairs;
@@ -1851,6 +1864,10 @@ void launch_lncc_bwd(const Batch& b, const LmParams& p, cudaStream_t s) {
 }
 
 void launch_step_smooth(const Batch& b, const LmParams& p, cudaStream_t s) {
+    if (p.Ru > 6) {
+        launch_step_smooth_generic(b, p, p.taps_u, p.Ru, s);
+        return;
+    }
     const LaunchShape sh = shape_for(b.g, b.pairs, k3::TY, b.ctas_per_sm);
     dim3 grid = sh.grid();
     grid.z = b.pairs;
@@ -1903,6 +1920,10 @@ void make_tma_u(Batch& b, int Rw) {
 }
 
 void launch_compose_smooth(const Batch& b, const LmParams& p, cudaStream_t s) {
+    if (p.Rw > 6) {
+        launch_compose_smooth_generic(b, p, p.taps_w, p.Rw, s);
+        return;
+    }
     const LaunchShape sh = shape_for(b.g, b.pairs, k4::TY, b.ctas_per_sm);
     dim3 grid = sh.grid();
     grid.z = b.pairs;

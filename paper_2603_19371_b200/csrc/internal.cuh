@@ -151,7 +151,7 @@ struct wlm_engine {
     DevBuf<float> F, M, U, ABE, G, VS, AM, AV;
     DevBuf<double> MW, GM;
     DevBuf<PairState> st;
-    DevBuf<double> partials, script, shift_part, plane_sum, TM, MIT, ABC;
+    DevBuf<double> partials, script, shift_part, plane_sum, TM, MIT, ABC, X64, TAPU, TAPW;
     DevBuf<unsigned long long> HIST;
     DevBuf<wlm_step_log> trace;
     Batch B{};

@@ -47,6 +47,10 @@ struct LmParams {
     // std::pow, the oracle's own values): [0][t-1] beta1, [1][t-1] beta2
     const double* adam_bc;
     int adam_bc_n;
+    // fp64 Gaussian taps w[0 .. 2R] of sigma_update / sigma_warp for the
+    // generic smoothing paths (radius > 6), device pointers or null
+    const double* taps_u;
+    const double* taps_w;
     int rejection, max_retries, optimizer, log_jacobian;
     int trace_cap;
     int script_n;
@@ -57,7 +61,7 @@ struct LmParams {
     float wu_full, ww_full;
     double wud[8], wud_full;  // fp64 copies of the kernels (K3/K4 sum in fp64)
     double wwd[8], wwd_full;
-    int radius;            // LNCC window radius (template-dispatched: 2 only in v1)
+    int radius;            // LNCC window radius (2: fused K1b/K2; others: generic.cu)
     int metric;            // WLM_METRIC_LNCC | WLM_METRIC_MSE
     double demons_alpha;   // DemonsConfig.alpha (optimizer DEMONS)
     int tile_k;            // LmConfig.tile_size (Eq. 5); 1 = pointwise Eq. 4
@@ -88,6 +92,7 @@ struct Batch {
     double* TM;       // [pair][tiles][6] tiled LM: -r (H + lambda I)^{-1} (symmetric), or null
     unsigned long long* HIST;  // [pair][B*B] MI joint histogram, fixed point 2^-32 (exact sums)
     double* MIT;      // [pair][B*B] MI gradient table dMI/dp_ij - dMI/dp_m(j)
+    double* X64;      // [pair][10][n] fp64 scratch of the generic paths (generic.cu), or null
     int tkx, tky, tkz;  // tile counts (tile_k > 1)
     int tma_u_ok;       // K4 stages the accepted warp by TMA (tma_u valid)
     CUtensorMap tma_u;  // 5D map over U: (x, y, local z, buffer*3 + component, pair)
@@ -170,6 +175,15 @@ void launch_demons_pointwise(const double* r, const double* n, long long N, doub
                              cudaStream_t s);
 
 void launch_nonfinite(const float* v, long long count, int* flag, cudaStream_t s);
+// K1a alone over planes [zf, zl) (the generic LNCC path's warp + gradient).
+void launch_warp_moving_grad(const Batch& b, int mode, int zf, int zl, cudaStream_t s);
+void launch_plane_sums(const Batch& b, cudaStream_t s);
+// generic.cu: LNCC radius != 2, smoothing radius > 6
+size_t generic_scratch_doubles(const Geo& g);
+void launch_lncc_fwd_generic(const Batch& b, const LmParams& p, int mode, cudaStream_t s);
+void launch_lncc_bwd_generic(const Batch& b, const LmParams& p, cudaStream_t s);
+void launch_step_smooth_generic(const Batch& b, const LmParams& p, const double* w, int R, cudaStream_t s);
+void launch_compose_smooth_generic(const Batch& b, const LmParams& p, const double* w, int R, cudaStream_t s);
 // Gaussian(sigma = 0.5 f) + stride f in one fp64 pass (pyramid levels).
 void launch_downsample_gauss(const float* in, const Geo& g, int f, float* out, const Geo& gd,
                              cudaStream_t s);

@@ -545,6 +545,13 @@ wlm_status make_group(wlm_ctx* ctx, wlm_dims d, int nslabs, int first, int count
 
 wlm_status check_split(wlm_ctx* ctx, wlm_dims d, int nslabs, const wlm_reg_config* cfg) {
     if (nslabs < 1 || !valid_dims(d)) return WLM_INVALID_ARG;  // ctx may be null (host-only helpers)
+    // slabs run the fused kernels only (LNCC radius 2, smoothing radius <= 6);
+    // the generic paths (generic.cu) are single-domain
+    if ((cfg->metric == WLM_METRIC_LNCC && cfg->lncc_radius != 2) || smooth_radius(cfg->sigma_update) > 6 ||
+        smooth_radius(cfg->sigma_warp) > 6) {
+        set_err(ctx, "slab_group: LNCC radius 2 and sigma <= 2 only (the generic paths are single-domain)");
+        return WLM_UNSUPPORTED;
+    }
     // every slab (tile-aligned when tiled) holds at least the halo depth and,
     // with tiles, the R_u + k planes its halo tiles can reach into
     const int tk = std::max(1, cfg->lm.tile_size);

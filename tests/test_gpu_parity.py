@@ -721,12 +721,44 @@ def test_random_configs_match_storage_oracle(P, ctx, case):
     compare_runs(tr, tr_o, aos(warp[0]), u_o, 1e-6, 1e-5)
 
 
-def test_smoothing_radius_limit(P, ctx):
-    """The fused smoothing kernels are instantiated for radius <= 6
-    (sigma <= 2); larger sigmas are refused, not silently skipped."""
-    P.Engine((8, 8, 8), 1, P.reg_config(sigma_update=2.0, sigma_warp=2.0), ctx=ctx).close()
+@pytest.mark.parametrize("su,sw", [(3.0, 0.5), (1.0, 2.5), (2.6, 3.1)])
+def test_large_sigma_engine_vs_oracle(P, ctx, su, sw):
+    """sigma_update / sigma_warp > 2 (radius > 6: generic.cu's Gaussian passes,
+    the reference's gaussian_smooth takes any sigma > 0, field.cpp:205-213)
+    against the fp32-storage oracle (loss 1e-6, identical decisions and
+    lambda, warp 1e-5) and the fp64 oracle (loss 1e-5).  Slab groups refuse
+    these radii (single-domain paths)."""
+    F, M, _ = O.synth_pair((26, 30, 34), 41, num_blobs=8, warp_max=2.5)
+    kw = dict(nlevels=1, factors=[1], iters=[15], sigma_update=su, sigma_warp=sw,
+              **{"lm.rejection": 1, "lm.tau": 0.3})
+    warp, (tr,), _ = run_engine(P, ctx, F, M, P.reg_config(**kw), 15)
+    for storage, lt, wt in (("fp32", 1e-6, 1e-5), ("fp64", 1e-5, 1e-4)):
+        rc, u_o, _, tr_o = oracle_level(F, M, O.default_config(**kw), 15, storage)
+        assert rc == 0
+        compare_runs(tr, tr_o, aos(warp[0]), u_o, lt, wt)
     with pytest.raises(P.WlmError):
-        P.Engine((8, 8, 8), 1, P.reg_config(sigma_update=2.1), ctx=ctx)
+        P.SlabGroup((26, 30, 34), 2, cfg=P.reg_config(**kw), ctx=ctx)
+
+
+@pytest.mark.parametrize("radius", [1, 3, 4])
+def test_lncc_any_radius_vs_oracle(P, ctx, radius):
+    """lncc_radius >= 1: the residual mirror and a
+    rejection-on LM run (generic.cu's window passes for radius != 2)
+    against the oracle."""
+    F, M, _ = O.synth_pair((24, 28, 22), 50 + radius, num_blobs=8, warp_max=2.0)
+    F64, M64 = F.astype(np.float64), M.astype(np.float64)
+    u = smooth_field(F.shape, 9, sigma=1.5, amp=1.5).astype(np.float32).astype(np.float64)
+    rep = P.residual_lncc(F64, M64, u, radius=radius, ctx=ctx)
+    r_o, g_o, lncc_o = O.residual_lncc(F64, M64, u, radius=radius)
+    assert abs(rep.r - r_o) <= 1e-9 * abs(r_o) and rel(rep.g, g_o) < 1e-6
+    kw = dict(nlevels=1, factors=[1], iters=[12], lncc_radius=radius, **{"lm.rejection": 1, "lm.tau": 0.3})
+    warp, (tr,), _ = run_engine(P, ctx, F, M, P.reg_config(**kw), 12)
+    for storage, lt, wt in (("fp32", 1e-6, 1e-5), ("fp64", 1e-5, 1e-4)):
+        rc, u_o, _, tr_o = oracle_level(F, M, O.default_config(**kw), 12, storage)
+        assert rc == 0
+        compare_runs(tr, tr_o, aos(warp[0]), u_o, lt, wt)
+    with pytest.raises(P.InvalidArgument):
+        P.Engine(F.shape, 1, P.reg_config(lncc_radius=0), ctx=ctx)
 
 
 @pytest.mark.parametrize("case", range(12))

@@ -8,7 +8,7 @@ out=build/var_$name
 mkdir -p $out
 C=paper_2603_19371_b200/csrc
 objs=""
-for f in kernels hot_kernels engine ops synth slab io field64; do
+for f in kernels hot_kernels engine ops synth slab io field64 generic; do
   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -lineinfo -Xcompiler -fPIC -Iinclude "$@" \
        -c $C/$f.cu -o $out/$f.o &
   objs="$objs $out/$f.o"
