@@ -11,7 +11,13 @@ HDRS    := include/wlm.h $(CSRC)/common.cuh $(CSRC)/hot.cuh $(CSRC)/kernels.cuh 
 OBJS    := $(patsubst $(CSRC)/%.cu,build/%.o,$(SRCS))
 LIB     := $(PKG)/libwarplm_b200.so
 
-all: $(LIB) oracle
+SHIM    := tests/nccl_shim/libnccl_shim.so
+
+all: $(LIB) oracle $(SHIM)
+
+# test infrastructure: two-rank NCCL stand-in over CUDA IPC (tests/test_slab_ranks.py)
+$(SHIM): tests/nccl_shim/nccl_shim.cu
+	$(NVCC) $(ARCH) -O2 -std=c++17 -Xcompiler -fPIC -shared -o $@ $< -lrt
 
 build/%.o: $(CSRC)/%.cu $(HDRS)
 	@mkdir -p build
@@ -31,7 +37,7 @@ oracle:
 	$(MAKE) -C oracle
 
 clean:
-	rm -rf build $(LIB)
+	rm -rf build $(LIB) $(SHIM)
 	$(MAKE) -C oracle clean
 
 .PHONY: all oracle clean

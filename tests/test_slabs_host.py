@@ -137,3 +137,19 @@ def test_halo_plan_refuses_what_a_group_refuses():
     with pytest.raises(ValueError):
         slabs.halo_plan((24, 8, 8), 4, 0, cfg)   # 6 planes per slab < R_u (3) + k (4)
     slabs.halo_plan((24, 8, 8), 3, 0, cfg)       # 8 planes per slab: fine
+
+
+def test_nccl_shim_exports_what_the_transport_binds():
+    """tests/nccl_shim/libnccl_shim.so (the two-rank stand-in of
+    tests/test_slab_ranks.py) exports every symbol slab.cu's NCCL loader
+    resolves, and hands out distinct unique ids (no GPU needed)."""
+    import ctypes as C
+    import re
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    src = open(os.path.join(root, "paper_2603_19371_b200", "csrc", "slab.cu")).read()
+    wanted = re.findall(r'SYM\(\w+, "(nccl\w+)"\)', src)
+    assert len(wanted) >= 9
+    lib = C.CDLL(os.path.join(root, "tests", "nccl_shim", "libnccl_shim.so"))
+    assert all(hasattr(lib, w) for w in wanted), [w for w in wanted if not hasattr(lib, w)]
+    a, b = C.create_string_buffer(128), C.create_string_buffer(128)
+    assert lib.ncclGetUniqueId(a) == 0 and lib.ncclGetUniqueId(b) == 0 and a.raw != b.raw
