@@ -603,6 +603,8 @@ __global__ void __launch_bounds__(k1::NT, 2) k_lncc_fwd(Batch b, int chunk_len) 
     const double shf = st->shift_f, shm = st->shift_m;
     const int tiles = cdiv(g.nx, TX) * cdiv(g.ny, k1::TY);
     double* __restrict__ part = b.partials + (long long)pair * g.nz * tiles * (NT / 32);
+    double* __restrict__ part_cta = part + blockIdx.x * (NT / 32) + (threadIdx.x >> 5);  // + plane * part_plane
+    const int part_plane = tiles * (NT / 32);
 
     int hoff[SL];
 #pragma unroll
@@ -746,7 +748,7 @@ __global__ void __launch_bounds__(k1::NT, 2) k_lncc_fwd(Batch b, int chunk_len) 
                         Eout[o] = Ee;
                     }
                     rho = warp_sum(rho);
-                    if (ox == 0) part[((long long)zo * tiles + blockIdx.x) * (NT / 32) + oy] = rho;
+                    if (ox == 0) part_cta[(long long)zo * part_plane] = rho;
                 }
                 x_pass(in_b, x_b);
                 complete(zi + 2, in_a);
@@ -1344,6 +1346,9 @@ __global__ void __launch_bounds__(k3::NT, k3::MINB) k_step_smooth(Batch b, LmPar
 #ifndef WLM_K4_ROWS
 #define WLM_K4_ROWS 1
 #endif
+#ifndef WLM_K4_FLOATTEST
+#define WLM_K4_FLOATTEST 1
+#endif
 namespace k4 {
 constexpr int TX = 32, TY = 16, NT = 512;
 template <int R>
@@ -1551,8 +1556,15 @@ __global__ void __launch_bounds__(k4::NT, 1) k_compose_smooth(Batch b, LmParams 
             if (idx < 0) continue;
             double o3[3];
             const double dx = eps * pv[s][0], dy = eps * pv[s][1], dz = eps * pv[s][2];
+            // d = eps dU_s is finite iff the stored fp32 step is (eps <= target
+            // / max |dU_s| keeps |d| <= target), and its sign is the step's
+#if WLM_K4_FLOATTEST
+            if (fmaxf(fabsf(pv[s][0]), fmaxf(fabsf(pv[s][1]), fabsf(pv[s][2]))) <= FLT_MAX) {
+                const int fx = pv[s][0] < 0.f ? -1 : 0, fy = pv[s][1] < 0.f ? -1 : 0, fz = pv[s][2] < 0.f ? -1 : 0;
+#else
             if (isfinite(dx + dy + dz)) {
                 const int fx = dx < 0.0 ? -1 : 0, fy = dy < 0.0 ? -1 : 0, fz = dz < 0.0 ? -1 : 0;
+#endif
                 const double tx = dx - (double)fx, ty = dy - (double)fy, tz = dz - (double)fz;
                 const int a = (vy[s] + fy - (y0 - R - 1)) * UW + vx[s] + fx - (x0 - S::XO);
                 const float* p0 = s_u + ((z + fz + 4) & 3) * S::SLOT + a;
