@@ -47,7 +47,7 @@ class RegConfig(C.Structure):
                 ("target_max_disp", C.c_double), ("step_floor", C.c_double),
                 ("sigma_update", C.c_double), ("sigma_warp", C.c_double),
                 ("log_jacobian", C.c_int), ("metric", C.c_int), ("demons_alpha", C.c_double),
-                ("mi_bins", C.c_int), ("mi_sigma", C.c_double)]
+                ("mi_bins", C.c_int), ("mi_sigma", C.c_double), ("low_memory", C.c_int)]
 
 
 class SynthSpec(C.Structure):

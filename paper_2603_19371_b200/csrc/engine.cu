@@ -92,6 +92,8 @@ wlm_status engine_init(wlm_engine* e, wlm_ctx* ctx, wlm_dims d, int pairs, const
     P.tile_k = c->lm.tile_size;
     P.mi_bins = c->mi_bins;
     P.mi_sigma = c->mi_sigma;
+    // memory layout: K2 re-gathers grad M(x+u) (fused LNCC path only)
+    P.lean = c->low_memory && c->metric == WLM_METRIC_LNCC && c->lncc_radius == 2 ? 1 : 0;
     P.Ru = smooth_radius(c->sigma_update);
     P.Rw = smooth_radius(c->sigma_warp);
     // radius <= 6 (sigma <= 2): the fused K3 / K4; larger: generic.cu
@@ -131,7 +133,7 @@ void engine_alloc(wlm_engine* e) {
     e->U = DevBuf<float>(ctx, B * 6 * n);
     e->ABE = DevBuf<float>(ctx, B * 4 * n);  // A, B fp32 + E fp64
     e->MW = DevBuf<double>(ctx, B * n);
-    if (e->P.metric == WLM_METRIC_LNCC) e->GM = DevBuf<double>(ctx, B * 3 * n);  // K1a -> K2
+    if (e->P.metric == WLM_METRIC_LNCC && !e->P.lean) e->GM = DevBuf<double>(ctx, B * 3 * n);  // K1a -> K2
     e->shift_part = DevBuf<double>(ctx, B * 2 * 256 * 3);  // sums + (min, max)
     init_constants();
     e->G = DevBuf<float>(ctx, B * 3 * n);
@@ -267,6 +269,7 @@ void wlm_default_reg_config(wlm_reg_config* c) {
     c->demons_alpha = 1.0;
     c->mi_bins = 32;
     c->mi_sigma = 1.0;
+    c->low_memory = 0;
 }
 
 wlm_status wlm_ctx_create(int device, wlm_ctx** out) {

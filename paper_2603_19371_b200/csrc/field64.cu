@@ -191,20 +191,33 @@ __host__ __device__ inline double dkey_inv(unsigned long long k) {
 
 // field.cpp:157-201: det(I + grad u), central differences, min over the
 // interior (the whole axis where n == 2).
-__device__ __forceinline__ double axis_derivative64(const double* __restrict__ u, wlm_dims d, int x, int y, int z,
-                                                    int c, int axis) {
+// element (voxel i, component c) of an fp64 AoS field or of an fp32 SoA
+// field (the engine's warp, widened exactly)
+struct Aos64 {
+    const double* u;
+    __device__ double operator()(long long i, int c, long long) const { return u[3 * i + c]; }
+};
+struct Soa32 {
+    const float* u;
+    __device__ double operator()(long long i, int c, long long n) const { return (double)u[c * n + i]; }
+};
+
+template <class Acc>
+__device__ __forceinline__ double axis_derivative64(const Acc& u, wlm_dims d, int x, int y, int z, int c, int axis) {
     const int n = axis == 0 ? d.nx : axis == 1 ? d.ny : d.nz;
     const int p = axis == 0 ? x : axis == 1 ? y : z;
+    const long long nv = (long long)d.nx * d.ny * d.nz;
     auto value = [&](int q) {
         const int xx = axis == 0 ? q : x, yy = axis == 1 ? q : y, zz = axis == 2 ? q : z;
-        return u[3 * ((long long)xx + (long long)d.nx * ((long long)yy + (long long)d.ny * zz)) + c];
+        return u((long long)xx + (long long)d.nx * ((long long)yy + (long long)d.ny * zz), c, nv);
     };
     if (p >= 1 && p + 1 <= n - 1) return __dmul_rn(0.5, __dsub_rn(value(p + 1), value(p - 1)));
     if (p == 0) return __dsub_rn(value(1), value(0));
     return __dsub_rn(value(p), value(p - 1));
 }
 
-__global__ void k_jacobian_min64(const double* __restrict__ u, wlm_dims d, unsigned long long* out) {
+template <class Acc>
+__global__ void k_jacobian_min64(Acc u, wlm_dims d, unsigned long long* out) {
     const int x0 = d.nx >= 3 ? 1 : 0, x1 = d.nx >= 3 ? d.nx - 2 : d.nx - 1;
     const int y0 = d.ny >= 3 ? 1 : 0, y1 = d.ny >= 3 ? d.ny - 2 : d.ny - 1;
     const int z0 = d.nz >= 3 ? 1 : 0, z1 = d.nz >= 3 ? d.nz - 2 : d.nz - 1;
@@ -338,7 +351,12 @@ void launch_max_abs64(const double* v, long long count, unsigned long long* out,
 }
 
 void launch_jacobian_min64(const double* u, wlm_dims d, unsigned long long* out, cudaStream_t s) {
-    k_jacobian_min64<<<grid_1d((long long)nvox(d)), 256, 0, s>>>(u, d, out);
+    k_jacobian_min64<<<grid_1d((long long)nvox(d)), 256, 0, s>>>(Aos64{u}, d, out);
+    ++g_kernel_launches;
+}
+
+void launch_jacobian_min64_soa32(const float* u, wlm_dims d, unsigned long long* out, cudaStream_t s) {
+    k_jacobian_min64<<<grid_1d((long long)nvox(d)), 256, 0, s>>>(Soa32{u}, d, out);
     ++g_kernel_launches;
 }
 

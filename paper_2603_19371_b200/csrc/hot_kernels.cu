@@ -813,10 +813,17 @@ struct OwnSlot {
     double gm[3][NT];
     float f[NT];
 };
+// low-memory layout: the accepted warp of the output voxel instead of K1a's
+// Mw and grad M; K2 gathers M(x + u) itself (sample_vol, K1a's arithmetic)
+struct OwnSlotLean {
+    float u[3][NT];
+    float f[NT];
+};
 constexpr size_t OWN_BYTES = sizeof(OwnSlot) * OWN_SLOTS;
+constexpr size_t OWN_BYTES_LEAN = sizeof(OwnSlotLean) * OWN_SLOTS;
 }  // namespace k2
 
-template <int R>
+template <int R, bool LEAN>
 #ifndef WLM_K2_MIN_BLOCKS
 #define WLM_K2_MIN_BLOCKS 2
 #endif
@@ -828,6 +835,7 @@ __global__ void __launch_bounds__(k2::NT, WLM_K2_MIN_BLOCKS) k_lncc_bwd(Batch b,
     __shared__ __align__(16) double s_x[2][3][IH * TX];
     extern __shared__ __align__(16) unsigned char k2_smem[];
     k2::OwnSlot* const s_own = reinterpret_cast<k2::OwnSlot*>(k2_smem);
+    k2::OwnSlotLean* const s_lean = reinterpret_cast<k2::OwnSlotLean*>(k2_smem);
     (void)p;
 
     const int pair = b.pair0 + blockIdx.z;
@@ -925,7 +933,20 @@ __global__ void __launch_bounds__(k2::NT, WLM_K2_MIN_BLOCKS) k_lncc_bwd(Batch b,
     const double* __restrict__ MWp = b.MW + (long long)pair * n;
     const double* __restrict__ GMp = b.GM + (long long)pair * 3 * n;
     const int t = threadIdx.x;
+    const float* __restrict__ Uacc = b.U + ((long long)pair * 2 + st->cur) * 3 * n;
     auto issue_own = [&](int zo) {
+        if (LEAN) {
+            if (own && zo >= zb && zo < ze) {
+                k2::OwnSlotLean& sl = s_lean[zo & (k2::OWN_SLOTS - 1)];
+                const int o = (zo - g.zlo) * nxy + ooff;
+                __pipeline_memcpy_async(&sl.f[t], F + zo * nxy + ooff, sizeof(float));
+                __pipeline_memcpy_async(&sl.u[0][t], Uacc + o, sizeof(float));
+                __pipeline_memcpy_async(&sl.u[1][t], Uacc + n + o, sizeof(float));
+                __pipeline_memcpy_async(&sl.u[2][t], Uacc + 2 * n + o, sizeof(float));
+            }
+            __pipeline_commit();
+            return;
+        }
         if (own && zo >= zb && zo < ze) {
             k2::OwnSlot& sl = s_own[zo & (k2::OWN_SLOTS - 1)];
             const int o = (zo - g.zlo) * nxy + ooff;
@@ -976,7 +997,6 @@ __global__ void __launch_bounds__(k2::NT, WLM_K2_MIN_BLOCKS) k_lncc_bwd(Batch b,
                 }
                 if (emit) __pipeline_wait_prior(k2::OWN_AHEAD);  // plane zo has landed
                 if (emit && own) {
-                    const k2::OwnSlot& sl = s_own[zo & (k2::OWN_SLOTS - 1)];
                     double Sm[3];
 #pragma unroll
                     for (int c = 0; c < 3; ++c) {
@@ -985,13 +1005,24 @@ __global__ void __launch_bounds__(k2::NT, WLM_K2_MIN_BLOCKS) k_lncc_bwd(Batch b,
                         for (int d = 0; d < W; ++d) s += ring[(rs + 1 + d) % W][c];
                         Sm[c] = s;
                     }
-                    const double mw = sl.mw[t];
-                    const double f = (double)sl.f[t] - shf;
+                    double mw, gm[3], fv;
+                    if (LEAN) {
+                        const k2::OwnSlotLean& sl = s_lean[zo & (k2::OWN_SLOTS - 1)];
+                        mw = sample_vol<true>(b.M + (long long)pair * g.nfull, g, x, y, zo, sl.u[0][t], sl.u[1][t],
+                                              sl.u[2][t], gm);
+                        fv = sl.f[t];
+                    } else {
+                        const k2::OwnSlot& sl = s_own[zo & (k2::OWN_SLOTS - 1)];
+                        mw = sl.mw[t];
+                        gm[0] = sl.gm[0][t]; gm[1] = sl.gm[1][t]; gm[2] = sl.gm[2][t];
+                        fv = sl.f[t];
+                    }
+                    const double f = fv - shf;
                     const double dm = -invN * (fma(f, Sm[0], (mw - shm) * Sm[1]) - Sm[2]);
                     const int o = (zo - g.zlo) * nxy + ooff;
-                    G[o] = (float)(dm * sl.gm[0][t]);
-                    G[n + o] = (float)(dm * sl.gm[1][t]);
-                    G[2 * n + o] = (float)(dm * sl.gm[2][t]);
+                    G[o] = (float)(dm * gm[0]);
+                    G[n + o] = (float)(dm * gm[1]);
+                    G[2 * n + o] = (float)(dm * gm[2]);
                 }
                 x_pass(in_b, x_b);
                 store_halo(in_a);
@@ -1843,7 +1874,10 @@ void launch_lncc_fwd(const Batch& b, const LmParams& p, int mode, cudaStream_t s
     // Mw for the owned planes plus the window pass's 2-plane halo
     const int zf = std::max(0, b.g.zs - 2), zl = std::min(b.g.nz, b.g.ze + 2);
     const dim3 wgrid(cdiv(b.g.nx, 32) * cdiv(b.g.ny, 8), cdiv(zl - zf, kZP), b.pairs);
-    k_warp_moving<true><<<wgrid, 256, 0, s>>>(b, mode, zf, zl);
+    if (p.lean)
+        k_warp_moving<false><<<wgrid, 256, 0, s>>>(b, mode, zf, zl);  // K2 gathers grad M itself
+    else
+        k_warp_moving<true><<<wgrid, 256, 0, s>>>(b, mode, zf, zl);
     const LaunchShape sh = shape_for(b.g, b.pairs, k1::TY, b.ctas_per_sm);
     dim3 grid = sh.grid();
     grid.z = b.pairs;
@@ -1868,10 +1902,15 @@ void launch_lncc_bwd(const Batch& b, const LmParams& p, cudaStream_t s) {
     static std::atomic<unsigned long long> attr{0ull};  // per device
     const unsigned long long bit = device_bit();
     if (!(attr.load() & bit)) {
-        cudaFuncSetAttribute(k_lncc_bwd<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k2::OWN_BYTES);
+        cudaFuncSetAttribute(k_lncc_bwd<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k2::OWN_BYTES);
+        cudaFuncSetAttribute(k_lncc_bwd<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)k2::OWN_BYTES_LEAN);
         attr.fetch_or(bit);
     }
-    k_lncc_bwd<2><<<grid, k2::NT, k2::OWN_BYTES, s>>>(b, p, sh.chunk_len);
+    if (p.lean)
+        k_lncc_bwd<2, true><<<grid, k2::NT, k2::OWN_BYTES_LEAN, s>>>(b, p, sh.chunk_len);
+    else
+        k_lncc_bwd<2, false><<<grid, k2::NT, k2::OWN_BYTES, s>>>(b, p, sh.chunk_len);
     ++g_kernel_launches;
 }
 

@@ -375,6 +375,7 @@ void launch_sample_grad_points64(const double* v, wlm_dims d, const double* pts,
                                  double* grad, cudaStream_t s);
 void launch_max_abs64(const double* v, long long count, unsigned long long* out, cudaStream_t s);
 void launch_jacobian_min64(const double* u, wlm_dims d, unsigned long long* out, cudaStream_t s);
+void launch_jacobian_min64_soa32(const float* u, wlm_dims d, unsigned long long* out, cudaStream_t s);
 double jacobian_key_to_double(unsigned long long k);
 unsigned long long jacobian_key_init();
 void smooth64(double* data, double* tmp, const double* dw, int R, wlm_dims d, int nchan, long long cstride,

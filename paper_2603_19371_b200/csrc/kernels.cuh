@@ -65,6 +65,7 @@ struct LmParams {
     int metric;            // WLM_METRIC_LNCC | WLM_METRIC_MSE
     double demons_alpha;   // DemonsConfig.alpha (optimizer DEMONS)
     int tile_k;            // LmConfig.tile_size (Eq. 5); 1 = pointwise Eq. 4
+    int lean;              // LNCC low-memory layout: no grad M buffer, K2 gathers (wlm_reg_config.low_memory)
     int mi_bins;           // MI: B x B Parzen grid
     double mi_sigma;       // MI: Parzen sigma in bin widths
 };

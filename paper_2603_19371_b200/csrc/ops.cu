@@ -26,11 +26,29 @@ DevBuf<float> upload_soa(wlm_ctx* ctx, const double* host, size_t n, int nchan) 
     return out;
 }
 
+__global__ void k_soa_to_aos_range(const float* __restrict__ in, long long n, long long off, long long cnt, int nchan,
+                                   double* __restrict__ out) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < cnt * nchan;
+         i += (long long)gridDim.x * blockDim.x)
+        out[i] = (double)in[(i % nchan) * n + off + i / nchan];
+}
+
+// fp32 SoA device -> fp64 AoS host through a bounded device staging buffer
+// (at most 2^20 voxels at a time), so the result download does not raise the
+// peak device memory by 8 B per voxel and channel.
 void download_aos(wlm_ctx* ctx, const float* dev, size_t n, int nchan, double* host) {
-    DevBuf<double> tmp(ctx, n * nchan);
-    launch_soa_to_aos(dev, tmp.p, (long long)n, nchan, ctx->stream);
-    CK(cudaMemcpyAsync(host, tmp.p, sizeof(double) * n * nchan, cudaMemcpyDeviceToHost, ctx->stream));
-    CK(cudaStreamSynchronize(ctx->stream));
+    const size_t chunk = std::min<size_t>(n, (size_t)1 << 20);
+    DevBuf<double> tmp(ctx, chunk * nchan);
+    for (size_t off = 0; off < n; off += chunk) {
+        const size_t cnt = std::min(chunk, n - off);
+        const int grid = (int)std::min<size_t>(148 * 8, (cnt * nchan + 255) / 256);
+        k_soa_to_aos_range<<<grid, 256, 0, ctx->stream>>>(dev, (long long)n, (long long)off, (long long)cnt, nchan,
+                                                          tmp.p);
+        ++g_kernel_launches;
+        CK(cudaMemcpyAsync(host + off * nchan, tmp.p, sizeof(double) * cnt * nchan, cudaMemcpyDeviceToHost,
+                           ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+    }
 }
 
 
@@ -59,11 +77,12 @@ double read_max64(wlm_ctx* ctx, const double* v, long long count) {
 }
 
 // jacobian_det_min of an fp64 AoS device field (field.cpp:172-201)
-double read_jacdet64(wlm_ctx* ctx, const double* u, wlm_dims d) {
+double read_jacdet64(wlm_ctx* ctx, const double* u, wlm_dims d, const float* u_soa32 = nullptr) {
     DevBuf<unsigned long long> o(ctx, 1);
     const unsigned long long init = jacobian_key_init();
     CK(cudaMemcpyAsync(o.p, &init, sizeof(init), cudaMemcpyHostToDevice, ctx->stream));
-    launch_jacobian_min64(u, d, o.p, ctx->stream);
+    if (u_soa32) launch_jacobian_min64_soa32(u_soa32, d, o.p, ctx->stream);
+    else launch_jacobian_min64(u, d, o.p, ctx->stream);
     unsigned long long h = 0;
     CK(cudaMemcpyAsync(&h, o.p, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
@@ -507,9 +526,7 @@ wlm_status wlm_register(wlm_ctx* ctx, const float* F, const float* M, wlm_dims d
         if (jac_final) {
             if (d.nx >= 2 && d.ny >= 2 && d.nz >= 2) {
                 // the reference's fp64 jacobian_det_min of the (fp32) final warp
-                DevBuf<double> w64(ctx, 3 * n);
-                launch_soa_to_aos(uf, w64.p, (long long)n, 3, ctx->stream);
-                *jac_final = read_jacdet64(ctx, w64.p, d);
+                *jac_final = read_jacdet64(ctx, nullptr, d, uf);
             } else {
                 *jac_final = std::numeric_limits<double>::quiet_NaN();
             }

@@ -1006,3 +1006,26 @@ def test_config5_large_slab_split_bit_identical(P, ctx, n, nslabs):
     assert len(t1) >= 3 and all(math.isfinite(r["r"]) for r in t1)
     assert same_trace(t4, t1) and s4["lam"] == s1["lam"] and s4["r"] == s1["r"]
     assert bool(torch.equal(w1, w4)) and float(w1.abs().max()) > 0.0
+
+
+@pytest.mark.parametrize("rejection", [0, 1])
+def test_low_memory_layout_is_bit_identical(P, ctx, rejection):
+    """low_memory = 1 (no fp64 grad M buffer; K2 re-gathers M at x + u with
+    K1a's arithmetic) gives the default layout's warps and traces bit for
+    bit, through the batch engine and the pyramid driver, and holds 24 B
+    per voxel less device memory (the grad M buffer)."""
+    shape = (26, 30, 34)
+    F, M, _ = O.synth_pair(shape, 61, num_blobs=8, warp_max=2.5)
+    kw = dict(nlevels=1, factors=[1], iters=[20], **{"lm.rejection": rejection, "lm.tau": 0.05})
+    out = {}
+    for lean in (0, 1):
+        w, (t,), _ = run_engine(P, ctx, F, M, P.reg_config(low_memory=lean, **kw), 20)
+        out[lean] = (w, t)
+    assert np.array_equal(out[0][0], out[1][0]) and same_trace(out[0][1], out[1][1])
+    if rejection:
+        assert sum(r["retries"] for r in out[0][1]) > 0
+    kw = dict(nlevels=2, factors=[2, 1], iters=[15, 10])
+    res = {lean: P.register(F, M, P.reg_config(low_memory=lean, **kw), ctx=ctx) for lean in (0, 1)}
+    assert np.array_equal(res[0].final_warp, res[1].final_warp)
+    assert [(a.r, a.lam) for a in res[0].loss_trace] == [(a.r, a.lam) for a in res[1].loss_trace]
+    assert res[0].peak_device_bytes - res[1].peak_device_bytes == 24 * int(np.prod(shape))
