@@ -1380,6 +1380,9 @@ __global__ void __launch_bounds__(k3::NT, k3::MINB) k_step_smooth(Batch b, LmPar
 #ifndef WLM_K4_FLOATTEST
 #define WLM_K4_FLOATTEST 1
 #endif
+#ifndef WLM_K4_UW32
+#define WLM_K4_UW32 0
+#endif
 namespace k4 {
 constexpr int TX = 32, TY = 16, NT = 512;
 template <int R>
@@ -1391,7 +1394,15 @@ struct Shape {
     // padded to 16 bytes (the box's inner extent), covering x0 - R - 1 ..
     // x0 + TX + R
     static constexpr int XO = 4;
-    static constexpr int UW = (TX + R + 1 + XO + 3) / 4 * 4, UH = TY + 2 * R + 2, UN = UW * UH;
+    // WLM_K4_UW32 pads the rows to a multiple of 32 floats: the resample
+    // reads of a warp come from two ring rows wherever the sign of d_y
+    // changes along it, and a 40-float row stride (8 banks) makes lanes 24
+    // apart collide (ncu: ~50% excess wavefronts on the corner reads).  The
+    // 64-float rows remove that but cost more (TMA box and tile 60% wider):
+    // K4 1.522 -> 1.600 ms, so the default keeps 40.
+    static constexpr int UW0 = (TX + R + 1 + XO + 3) / 4 * 4;
+    static constexpr int UW = WLM_K4_UW32 && R == 2 ? (UW0 + 31) / 32 * 32 : UW0;
+    static constexpr int UH = TY + 2 * R + 2, UN = UW * UH;
     static constexpr int IWP = UW, NI = IWP * IH;
     // composed items enumerated compactly (IW per row); the last, partial
     // slot goes to the highest threads, away from the x-pass threads (the
@@ -1866,23 +1877,34 @@ void launch_warp_moving_grad(const Batch& b, int mode, int zf, int zl, cudaStrea
     ++g_kernel_launches;
 }
 
-void launch_lncc_fwd(const Batch& b, const LmParams& p, int mode, cudaStream_t s) {
-    if (p.radius != 2) {
-        launch_lncc_fwd_generic(b, p, mode, s);
-        return;
-    }
-    // Mw for the owned planes plus the window pass's 2-plane halo
+// K1a over the owned planes plus the window pass's 2-plane halo
+void launch_lncc_warp(const Batch& b, const LmParams& p, int mode, cudaStream_t s) {
     const int zf = std::max(0, b.g.zs - 2), zl = std::min(b.g.nz, b.g.ze + 2);
     const dim3 wgrid(cdiv(b.g.nx, 32) * cdiv(b.g.ny, 8), cdiv(zl - zf, kZP), b.pairs);
     if (p.lean)
         k_warp_moving<false><<<wgrid, 256, 0, s>>>(b, mode, zf, zl);  // K2 gathers grad M itself
     else
         k_warp_moving<true><<<wgrid, 256, 0, s>>>(b, mode, zf, zl);
+    ++g_kernel_launches;
+}
+
+// K1b over the owned planes [b.g.zs, b.g.ze) (a slab's boundary or interior
+// view: every voxel's arithmetic is independent of the range)
+void launch_lncc_window(const Batch& b, cudaStream_t s) {
     const LaunchShape sh = shape_for(b.g, b.pairs, k1::TY, b.ctas_per_sm);
     dim3 grid = sh.grid();
     grid.z = b.pairs;
     k_lncc_fwd<2><<<grid, k1::NT, 0, s>>>(b, sh.chunk_len);
-    g_kernel_launches += 2;
+    ++g_kernel_launches;
+}
+
+void launch_lncc_fwd(const Batch& b, const LmParams& p, int mode, cudaStream_t s) {
+    if (p.radius != 2) {
+        launch_lncc_fwd_generic(b, p, mode, s);
+        return;
+    }
+    launch_lncc_warp(b, p, mode, s);
+    launch_lncc_window(b, s);
     launch_plane_sums(b, s);
 }
 

@@ -179,6 +179,9 @@ void launch_nonfinite(const float* v, long long count, int* flag, cudaStream_t s
 // K1a alone over planes [zf, zl) (the generic LNCC path's warp + gradient).
 void launch_warp_moving_grad(const Batch& b, int mode, int zf, int zl, cudaStream_t s);
 void launch_plane_sums(const Batch& b, cudaStream_t s);
+// K1's pieces (the fused radius-2 path): K1a, K1b (range = b.g.zs .. b.g.ze)
+void launch_lncc_warp(const Batch& b, const LmParams& p, int mode, cudaStream_t s);
+void launch_lncc_window(const Batch& b, cudaStream_t s);
 // generic.cu: LNCC radius != 2, smoothing radius > 6
 size_t generic_scratch_doubles(const Geo& g);
 void launch_lncc_fwd_generic(const Batch& b, const LmParams& p, int mode, cudaStream_t s);

@@ -34,6 +34,8 @@
 #include <string>
 #include <vector>
 
+#include <cstdlib>
+
 #include "internal.cuh"
 
 using namespace wlm;
@@ -236,7 +238,14 @@ struct wlm_slab_group {
     cudaGraph_t step_graph = nullptr, loop_graph = nullptr;
     int body_kernels = 0;
 
+    // interior / boundary overlap (see body_overlap)
+    cudaStream_t side = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+
     ~wlm_slab_group() {
+        if (side) cudaStreamDestroy(side);
+        if (ev_fork) cudaEventDestroy(ev_fork);
+        if (ev_join) cudaEventDestroy(ev_join);
         if (step_exec) cudaGraphExecDestroy(step_exec);
         if (loop_exec) cudaGraphExecDestroy(loop_exec);
         if (step_graph) cudaGraphDestroy(step_graph);
@@ -400,7 +409,90 @@ struct wlm_slab_group {
         exchange(BUF_ABE, s);
     }
 
+    // Interior / boundary split: every stage whose output a
+    // neighbour needs runs first on the planes it sends (the plan's send
+    // rows), the exchange is queued behind those, and the remaining interior
+    // planes run on a side stream meanwhile; the streams join before the
+    // next stage.  Every voxel's arithmetic is independent of the launch
+    // range (z sums are direct sums over the ring), so the split is bit-
+    // identical to one launch.  Fused LNCC (radius 2) path with pointwise
+    // steps; WLM_SLAB_OVERLAP=0 keeps the serial body.
+    bool overlap_enabled() const {
+        const LmParams& P = eng[0]->P;
+        const char* v = std::getenv("WLM_SLAB_OVERLAP");
+        if (v && std::atoi(v) == 0) return false;
+        return P.metric == WLM_METRIC_LNCC && P.radius == 2 && P.tile_k <= 1 && P.Ru <= 6 && P.Rw <= 6;
+    }
+
+    // Boundary views (the planes engine li sends of buffer b) and the
+    // interior view of its owned planes.
+    void views(size_t li, int b, std::vector<std::pair<wlm_engine*, Batch>>& bnd,
+               std::vector<std::pair<wlm_engine*, Batch>>& inner) const {
+        wlm_engine* e = eng[li];
+        const int zs = e->g.zs, ze = e->g.ze;
+        int lo = zs, hi = ze;  // interior [lo, hi)
+        for (const wlm_halo_xfer& r : plan[li]) {
+            if (r.buffer != b || !r.send) continue;
+            if (r.z0 == zs) lo = std::max(lo, r.z1);
+            if (r.z1 == ze) hi = std::min(hi, r.z0);
+        }
+        auto view = [&](int z0, int z1) {
+            Batch v = e->B;
+            v.g.zs = z0;
+            v.g.ze = z1;
+            return v;
+        };
+        if (lo >= hi) {  // thin slab: everything is boundary
+            bnd.push_back({e, e->B});
+            return;
+        }
+        if (lo > zs) bnd.push_back({e, view(zs, lo)});
+        if (hi < ze) bnd.push_back({e, view(hi, ze)});
+        inner.push_back({e, view(lo, hi)});
+    }
+
+    template <class Fn>
+    void staged(int b, Fn fn, cudaStream_t s) {
+        std::vector<std::pair<wlm_engine*, Batch>> bnd, inner;
+        for (size_t li = 0; li < eng.size(); ++li) views(li, b, bnd, inner);
+        CK(cudaEventRecord(ev_fork, s));
+        CK(cudaStreamWaitEvent(side, ev_fork, 0));
+        for (auto& v : bnd) fn(v.first, v.second, s);
+        exchange(b, s);
+        for (auto& v : inner) fn(v.first, v.second, side);
+        CK(cudaEventRecord(ev_join, side));
+        CK(cudaStreamWaitEvent(s, ev_join, 0));
+    }
+
+    void body_overlap(cudaStream_t s) {
+        if (!side) {
+            CK(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
+            CK(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
+            CK(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
+        }
+        staged(BUF_G, [](wlm_engine* e, const Batch& v, cudaStream_t st) { e->stage_grad(v, st); }, s);
+        staged(BUF_V, [](wlm_engine* e, const Batch& v, cudaStream_t st) { launch_step_smooth(v, e->P, st); }, s);
+        reduce_max(0, s);
+        staged(BUF_U, [](wlm_engine* e, const Batch& v, cudaStream_t st) { launch_compose_smooth(v, e->P, st); },
+               s);
+        if (eng[0]->P.log_jacobian) {
+            for (auto* e : eng) launch_jacobian_diag(e->B, e->P, s);
+            reduce_max(1, s);
+        }
+        // evaluate(1): K1a on the owned planes + halo, K1b split, then the
+        // per-plane sums and the loss on the whole slab
+        for (auto* e : eng) launch_lncc_warp(e->B, e->P, 1, s);
+        staged(BUF_ABE, [](wlm_engine*, const Batch& v, cudaStream_t st) { launch_lncc_window(v, st); }, s);
+        for (auto* e : eng) launch_plane_sums(e->B, s);
+        reduce_planes(s);
+        for (auto* e : eng) e->stage_finalize(1, s);
+    }
+
     void body(cudaStream_t s) {
+        if (overlap_enabled()) {
+            body_overlap(s);
+            return;
+        }
         for (auto* e : eng) e->stage_grad(s);
         exchange(BUF_G, s);
         if (eng[0]->P.optimizer == WLM_OPT_LM && eng[0]->P.tile_k > 1) {
@@ -456,10 +548,45 @@ struct wlm_slab_group {
         CK(cudaGraphInstantiate(&loop_exec, loop_graph, 0));
     }
 
-    // nccl transport: attempts are launched eagerly (collectives inside
-    // conditional graph bodies are not relied on).  Attempts of a finished
-    // registration are no-ops on the device, so with rejection the host
-    // launches the lower bound of remaining attempts, then re-reads the state.
+    // nccl transport without rejection: the attempt (kernels, halo
+    // send/recv groups and all-reduces) is captured once as a CUDA graph
+    // (NCCL supports stream capture) and launched per iteration.  A transport
+    // that cannot be captured (a capture error, e.g. a host-synchronising
+    // NCCL stand-in) leaves the group on eager launches.
+    int graph_state = 0;  // 0 untried, 1 captured, -1 not capturable
+    bool try_step_graph() {
+        if (graph_state != 0) return graph_state > 0;
+        const uint64_t saved = g_kernel_launches;
+        cudaGraph_t gr = nullptr;
+        bool ok = cudaStreamBeginCapture(ctx->capture, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
+        if (ok) {
+            try {
+                body(ctx->capture);
+            } catch (const Fail&) {
+                ok = false;
+            }
+            const cudaError_t e = cudaStreamEndCapture(ctx->capture, &gr);
+            ok = ok && e == cudaSuccess && gr != nullptr;
+        }
+        body_kernels = (int)(g_kernel_launches - saved);
+        g_kernel_launches = saved;
+        if (ok && cudaGraphInstantiate(&step_exec, gr, 0) == cudaSuccess) {
+            step_graph = gr;
+            graph_state = 1;
+        } else {
+            if (gr) cudaGraphDestroy(gr);
+            step_exec = nullptr;
+            graph_state = -1;
+        }
+        cudaGetLastError();  // clear a failed capture's sticky-free error state
+        return graph_state > 0;
+    }
+
+    // nccl transport with rejection (or when capture failed): attempts are
+    // launched eagerly (collectives inside conditional graph bodies are not
+    // relied on).  Attempts of a finished registration are no-ops on the
+    // device, so with rejection the host launches the lower bound of
+    // remaining attempts, then re-reads the state.
     void iterate_eager(int iters) {
         cudaStream_t s = ctx->stream;
         if (!eng[0]->P.rejection) {
@@ -727,7 +854,12 @@ wlm_status wlm_slab_group_iterate(wlm_slab_group* g, int iters) {
         for (auto* e : g->eng) launch_set_targets(e->B, iters, ctx->stream);
         if (iters == 0) return;
         if (g->distributed()) {
-            g->iterate_eager(iters);
+            if (!g->eng[0]->P.rejection && g->try_step_graph()) {
+                for (int i = 0; i < iters; ++i) CK(cudaGraphLaunch(g->step_exec, ctx->stream));
+                g_kernel_launches += (uint64_t)iters * g->body_kernels;
+            } else {
+                g->iterate_eager(iters);
+            }
         } else if (!g->eng[0]->P.rejection) {
             g->build_step_graph();
             for (int i = 0; i < iters; ++i) CK(cudaGraphLaunch(g->step_exec, ctx->stream));
