@@ -111,7 +111,12 @@ def test_cpp_adapter_accepts_reference_types(tmp_path):
                    "double f(const warplm::DispField3& u, const warplm::DispField3& v) {\n"
                    "  warplm::DispField3 w = wlm_warplm::compose_warp(u, v, 0.3);\n"
                    "  warplm::Volume3 s = wlm_warplm::gaussian_smooth(warplm::Volume3(u.dims), 1.0);\n"
-                   "  return wlm_warplm::normalize_step(w, warplm::StepScale{}) + s.data[0]\n"
+                   "  warplm::Volume3 h = wlm_warplm::downsample(s, 2);\n"
+                   "  warplm::DispField3 up = wlm_warplm::upsample_warp(w, u.dims, 1.0);\n"
+                   "  warplm::DispField3 st = wlm_warplm::lm_step_pointwise(0.5, w, 0.1);\n"
+                   "  warplm::Vec3 sf = wlm_warplm::sample_field(up, 0.5, 0.5, 0.5);\n"
+                   "  return wlm_warplm::normalize_step(w, warplm::StepScale{}) + s.data[0] + h.data[0]\n"
+                   "       + wlm_warplm::sample_trilinear(s, 0.5, 0.5, 0.5) + sf[0] + st.data[0]\n"
                    "       + wlm_warplm::jacobian_det_min(w);\n}\n")
     subprocess.run(["g++", "-std=c++20", "-fsyntax-only", "-I", "/root/reference/proj/include",
                     "-I", os.path.join(ROOT, "include"), str(src)], check=True)
