@@ -134,3 +134,44 @@ def test_full_size_trajectory_vs_both_oracles(P, ctx, name):
     assert dec_k >= int(0.9 * floor_dec), (name, "decisions vs fp64", dec_k, floor_dec)
     floor_w = np.linalg.norm(fx["fp32_warp_s"] - fx["fp64_warp_s"]) / np.linalg.norm(fx["fp64_warp_s"])
     assert wrel(fx["fp64_warp_s"]) <= 1.02 * floor_w, (name, wrel(fx["fp64_warp_s"]), floor_w)
+
+
+def test_config5_decomposition_at_512_vs_oracle(P, ctx):
+    """Config 5's path (GPU synth_pair of the config's kind: 96 blobs,
+    displacement up to 8 at 512^3, z-slab group of 2 slabs with the
+    interior / boundary overlap) against the fp32-storage oracle on the host
+    for the first evaluation and 2 LM iterations: loss 1e-6, identical
+    lambda, warp rel-L2 1e-6.  (The oracle cannot hold 1024^3 in host
+    memory; 1024^3 itself is covered by P-invariance, test_gpu_parity.py.)"""
+    import ctypes as C
+
+    import oracle as O
+    from paper_2603_19371_b200._lib import Dims, SynthSpec
+    n, it = 512, 2
+    shape = (n, n, n)
+    F = np.empty(shape, np.float32)
+    M = np.empty(shape, np.float32)
+    spec = SynthSpec(Dims(n, n, n), 96, 0.0, 8.0, 0.01, 7)
+    ctx.check(P.load().wlm_synth_pair(ctx.h, C.byref(spec), F.ctypes.data, M.ctypes.data, None, 0))
+    cfg = P.reg_config(nlevels=1, factors=[1], iters=[it])
+    grp = P.SlabGroup(shape, 2, cfg=cfg, ctx=ctx)
+    grp.load(F, M)
+    grp.set_warp(None)
+    grp.begin_level(0)
+    grp.iterate(it)
+    w, tr = grp.get_warp(), grp.trace()
+    grp.close()
+    L = O.lib()
+    L.orc_set_threads(os.cpu_count() or 1)
+    try:
+        with O.fp32_storage():
+            rc, u_o, _, tr_o = O.lm_run_level(F, M, np.zeros(shape + (3,)), O.default_config(
+                nlevels=1, factors=[1], iters=[it]), it)
+    finally:
+        L.orc_set_threads(min(8, os.cpu_count() or 1))
+    assert rc == 0 and len(tr) == len(tr_o) == it
+    for a, b in zip(tr, tr_o):
+        assert abs(a["r"] - b.r) <= 1e-6 * abs(b.r), (a["r"], b.r)
+        assert a["lam"] == b.lam
+    u_d = np.moveaxis(w.astype(np.float64), 0, -1)
+    assert np.linalg.norm(u_d - u_o) / np.linalg.norm(u_o) <= 1e-6
