@@ -1357,278 +1357,6 @@ __global__ void __launch_bounds__(k3::NT, k3::MINB) k_step_smooth(Batch b, LmPar
     }
 }
 
-// K3 in compensated fp32 (experiment, WLM_K3_F32; not the default): the LM
-// step in fp32 and the Gaussian with hi/lo-split fp32 weights (two fmaf per
-// tap), fp64 normalisation by the exact weight sums -- the oracle's
-// precision mode "K3hilo" (tools/precision_modes.py), which stays inside
-// both north-star bars on config 1.  Half the shared-memory bytes and ring
-// registers of K3, no fp32 -> fp64 conversions.
-#ifndef WLM_K3_F32
-#define WLM_K3_F32 0
-#endif
-template <int R>
-__global__ void __launch_bounds__(k3::NT, k3::MINB) k_step_smooth_f32(Batch b, LmParams p, int chunk_len) {
-    constexpr bool TILED = false;
-    using S = k3::Shape<R>;
-    constexpr int TX = k3::TX, NT = k3::NT, W = 2 * R + 1;
-    constexpr int IWP = S::IWP, IH = S::IH, NI = S::NI, SL = S::SLOTS, NV = S::NV;
-    extern __shared__ __align__(16) float k3f_smem[];
-    float* const s_in0 = k3f_smem;
-    float* const s_x0 = k3f_smem + S::IN_D;
-    float* const s_y0 = s_x0 + S::X_D;
-    __shared__ float s_max[NT / 32];
-    __shared__ double s_binv[2 * (R > 0 ? R : 1)];
-
-    const int pair = b.pair0 + blockIdx.z;
-    PairState* st = b.st + pair;
-    if (st->done) return;
-    const Geo g = b.g;
-    const long long n = g.n;
-    const int nxy = g.nx * g.ny;
-    const int tiles_x = cdiv(g.nx, TX);
-    const int x0 = (blockIdx.x % tiles_x) * TX, y0 = (blockIdx.x / tiles_x) * k3::TY;
-    fill_border_inv(s_binv, g.nz, R, p.wud, p.wud_full);
-    const int zb = g.zs + blockIdx.y * chunk_len, ze = min(zb + chunk_len, g.ze);
-    const float* __restrict__ Gin = b.G + (long long)pair * 3 * n;
-    float* __restrict__ V = b.VS + (long long)pair * 3 * n;
-    const int opt = p.optimizer;
-    const double r = st->r_cur, lam = st->lambda;
-    const double kc = opt == WLM_OPT_GD ? -p.gd_lr : 1.0;
-    const float rf = (float)r, lf = (float)lam;
-
-    int hoff[SL];
-#pragma unroll
-    for (int s = 0; s < SL; ++s) {
-        const int idx = halo_item(s, SL, NI, NT);
-        const int ix = idx % IWP, iy = idx / IWP;
-        const int gx = x0 - R + ix, gy = y0 - R + iy;
-        hoff[s] = (idx >= 0 && gx >= 0 && gx < g.nx && gy >= 0 && gy < g.ny) ? gx + g.nx * gy : -1;
-    }
-    float hg[SL][3];
-    auto load_halo = [&](int z) {
-        const bool zin = z >= 0 && z < g.nz && z < ze + R;
-        const int base = (z - g.zlo) * nxy;
-#pragma unroll
-        for (int s = 0; s < SL; ++s) {
-            if (zin && hoff[s] >= 0) {
-                const int o = base + hoff[s];
-                hg[s][0] = __ldg(Gin + o); hg[s][1] = __ldg(Gin + n + o); hg[s][2] = __ldg(Gin + 2 * n + o);
-            } else {
-                hg[s][0] = hg[s][1] = hg[s][2] = 0.f;
-            }
-        }
-    };
-    // tiled LM (Eq. 5): the item's k^3 tile matrix -r (H + lambda I)^{-1}
-    const int tk = p.tile_k;
-    constexpr bool tiled = TILED;  // launched only for LM with tile_size > 1
-    const double* __restrict__ TM = tiled ? b.TM + (long long)pair * 6 * b.tkx * b.tky * b.tkz : nullptr;
-    int htile[SL];  // (y tile) * tkx + x tile of each halo item
-#pragma unroll
-    for (int s = 0; s < SL; ++s) {
-        const int idx = halo_item(s, SL, NI, NT);
-        const int gx = x0 - R + idx % IWP, gy = y0 - R + idx / IWP;
-        htile[s] = (tiled && hoff[s] >= 0) ? (gy / tk) * b.tkx + gx / tk : 0;
-    }
-    int hz = 0;  // z tile of the plane being stored
-    auto store_halo = [&](float* dst) {
-#pragma unroll
-        for (int s = 0; s < SL; ++s) {
-            const int idx = halo_item(s, SL, NI, NT);
-            if (idx < 0) continue;
-            const float a = hg[s][0], bb = hg[s][1], c = hg[s][2];
-            if (tiled) {
-                const double* M6 = TM + ((long long)hz * b.tkx * b.tky + htile[s]) * 6;
-                dst[idx] = M6[0] * a + M6[1] * bb + M6[2] * c;
-                dst[NI + idx] = M6[1] * a + M6[3] * bb + M6[4] * c;
-                dst[2 * NI + idx] = M6[2] * a + M6[4] * bb + M6[5] * c;
-                continue;
-            }
-            // fp32 step (the oracle's dev_step32)
-            float k = (float)kc;
-            if (opt == WLM_OPT_LM) k = -rf * (1.f / (fmaf(a, a, fmaf(bb, bb, c * c)) + lf));
-            dst[idx] = k * a;
-            dst[NI + idx] = k * bb;
-            dst[2 * NI + idx] = k * c;
-        }
-    };
-    // hi / lo split fp32 weights: w_hi + w_lo = the fp64 weight to ~2^-48
-    float wh[W], wl[W];
-#pragma unroll
-    for (int d = 0; d < W; ++d) {
-        const double wd = p.wud[d < R ? R - d : d - R];
-        wh[d] = (float)wd;
-        wl[d] = (float)(wd - (double)wh[d]);
-    }
-
-    // x-pass item: row xr, pair xj (outputs x = 2xj, 2xj + 1); NT / 16 rows
-    // per sweep, so radii with IH > 16 rows (R > 4) take a second sweep
-    const int xr0 = threadIdx.x >> 4, xj = threadIdx.x & 15;
-    auto x_row = [&](const float* in, float* out, int xr) {
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-            float v[2 * NV];
-            const float2* src = reinterpret_cast<const float2*>(in + c * NI + xr * IWP + 2 * xj);
-#pragma unroll
-            for (int q = 0; q < NV; ++q) {
-                const float2 t = src[q];
-                v[2 * q] = t.x; v[2 * q + 1] = t.y;
-            }
-            float o0 = 0.f, o1 = 0.f;
-#pragma unroll
-            for (int d = 0; d < W; ++d) {
-                o0 = fmaf(wh[d], v[d], o0);
-                o0 = fmaf(wl[d], v[d], o0);
-                o1 = fmaf(wh[d], v[d + 1], o1);
-                o1 = fmaf(wl[d], v[d + 1], o1);
-            }
-            *reinterpret_cast<float2*>(out + c * IH * TX + xr * TX + 2 * xj) = make_float2(o0, o1);
-        }
-    };
-    auto x_pass = [&](const float* in, float* out) {
-        if (IH <= NT / 16) {
-            if (xr0 < IH) x_row(in, out, xr0);
-        } else {
-            for (int xr = xr0; xr < IH; xr += NT / 16) x_row(in, out, xr);
-        }
-    };
-
-    const int ox = threadIdx.x & 31, oy = threadIdx.x >> 5;
-    const int x = x0 + ox, y = y0 + oy;
-    const bool own = x < g.nx && y < g.ny;
-    const double inv_xy = own ? 1.0 / (axis_wsum_t<double>(x, g.nx, R, p.wud, p.wud_full) *
-                                       axis_wsum_t<double>(y, g.ny, R, p.wud, p.wud_full))
-                              : 0.0;
-    const double inv_full = inv_xy / p.wud_full;
-    const int ooff = x + g.nx * y;
-
-    float ring[W][3];
-#pragma unroll
-    for (int d = 0; d < W; ++d)
-#pragma unroll
-        for (int c = 0; c < 3; ++c) ring[d][c] = 0.f;
-    float mx = 0.f;
-
-    const int z0 = zb - R, z1 = ze + R;
-    float* in_a = s_in0;
-    float* in_b = s_in0 + 3 * NI;
-    float* x_a = s_x0;
-    float* x_b = s_x0 + 3 * IH * TX;
-    float* y_a = s_y0;
-    float* y_b = s_y0 + 3 * k3::TY * TX;
-    // column y-pass: thread (channel yc, column ox, quarter yh) of the last
-    // 3 NQ warps forms 4 outputs from its column's 4 + 2R x-sums held in
-    // registers, in the same fma order as the per-output 7-tap sum
-    constexpr int YH = 4, NQ = k3::NQ;
-    // the column pass runs on the highest warps and the x-pass on the
-    // lowest, so fewer warps carry both (K3 0.970 -> 0.966 ms at TY = 8)
-    const int yt = (int)threadIdx.x - (NT - 3 * NQ * 32);
-    const int yc = yt >= 0 ? yt / (NQ * 32) : 3, yh = (yt >> 5) % NQ;
-    auto y_pass = [&](const float* in, float* out) {
-        if (yc >= 3) return;
-        float v[YH + 2 * R];
-#pragma unroll
-        for (int r = 0; r < YH + 2 * R; ++r) v[r] = in[yc * IH * TX + (yh * YH + r) * TX + ox];
-#pragma unroll
-        for (int o = 0; o < YH; ++o) {
-            float acc = 0.f;
-#pragma unroll
-            for (int d = 0; d < W; ++d) {
-                acc = fmaf(wh[d], v[o + d], acc);
-                acc = fmaf(wl[d], v[o + d], acc);
-            }
-            out[yc * k3::TY * TX + (yh * YH + o) * TX + ox] = acc;
-        }
-    };
-    auto ztile = [&](int z) { return tiled && z >= 0 && z < g.nz ? z / tk : 0; };
-    load_halo(z0);
-    hz = ztile(z0);
-    store_halo(in_a);
-    load_halo(z0 + 1);
-    hz = ztile(z0 + 1);
-    store_halo(in_b);
-    __syncthreads();
-    x_pass(in_a, x_a);
-    if (k3::COLY) {
-        // deeper prologue: y_a = plane z0, x_b = plane z0+1, in_a = plane z0+2
-        x_pass(in_b, x_b);
-        load_halo(z0 + 2);
-        __syncthreads();
-        y_pass(x_a, y_a);
-        hz = ztile(z0 + 2);
-        store_halo(in_a);
-        load_halo(z0 + 3);
-        __syncthreads();
-    } else {
-        load_halo(z0 + 2);
-        __syncthreads();
-    }
-    for (int zbase = z0; zbase < z1; zbase += W) {
-#pragma unroll
-        for (int rs = 0; rs < W; ++rs) {
-            const int zi = zbase + rs;
-            if (zi < z1) {
-                if (k3::COLY) {
-#pragma unroll
-                    for (int c = 0; c < 3; ++c) ring[rs][c] = y_a[c * k3::TY * TX + oy * TX + ox];
-                } else {
-#pragma unroll
-                    for (int c = 0; c < 3; ++c) {
-                        float s = 0.f;
-#pragma unroll
-                        for (int d = 0; d < W; ++d) {
-                            s = fmaf(wh[d], x_a[c * IH * TX + (oy + d) * TX + ox], s);
-                            s = fmaf(wl[d], x_a[c * IH * TX + (oy + d) * TX + ox], s);
-                        }
-                        ring[rs][c] = s;
-                    }
-                }
-                const int zo = zi - R;
-                if (zo >= zb && own) {
-                    double inv = inv_full;
-                    if (zo < R || zo + R > g.nz - 1) inv = inv_xy * border_inv(s_binv, zo, g.nz, R);
-                    const int o = (zo - g.zlo) * nxy + ooff;
-#pragma unroll
-                    for (int c = 0; c < 3; ++c) {
-                        float s = 0.f;
-#pragma unroll
-                        for (int d = 0; d < W; ++d) {
-                            s = fmaf(wh[d], ring[(rs + 1 + d) % W][c], s);
-                            s = fmaf(wl[d], ring[(rs + 1 + d) % W][c], s);
-                        }
-                        const float v = (float)((double)s * inv);  // fp64 normalisation (exact weight sums)
-                        V[c * n + o] = v;
-                        mx = fmaxf(mx, fabsf(v));
-                    }
-                }
-                if (k3::COLY) {
-                    y_pass(x_b, y_b);
-                    x_pass(in_a, x_a);
-                    hz = ztile(zi + 3);
-                    store_halo(in_b);
-                    load_halo(zi + 4);
-                    float* t = y_a; y_a = y_b; y_b = t;
-                } else {
-                    x_pass(in_b, x_b);
-                    hz = ztile(zi + 2);
-                    store_halo(in_a);
-                    load_halo(zi + 3);
-                }
-                float* t = in_a; in_a = in_b; in_b = t;
-                t = x_a; x_a = x_b; x_b = t;
-                __syncthreads();
-            }
-        }
-    }
-    mx = warp_max(mx);
-    if ((threadIdx.x & 31) == 0) s_max[threadIdx.x >> 5] = mx;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        float m = 0.f;
-        for (int i = 0; i < NT / 32; ++i) m = fmaxf(m, s_max[i]);
-        atomic_max_nonneg(&st->max_bits, m);
-    }
-}
-
 // K4: u'(x) = d(x) + u(x + d(x)), d = eps dU_s, eps = target / max(max|dU_s|,
 // floor) (Eq. 2, field.cpp:123-155), then Gaussian(sigma_warp); fp64
 // arithmetic, fp32 storage.  The normalised step bounds |d| <= target < 0.5
@@ -2228,14 +1956,6 @@ void launch_step_smooth(const Batch& b, const LmParams& p, cudaStream_t s) {
         }
         if (p.optimizer == WLM_OPT_LM && p.tile_k > 1) {
             k_step_smooth<RR, true><<<grid, k3::NT, k3::Shape<RR>::BYTES, s>>>(b, p, sh.chunk_len);
-        } else if (WLM_K3_F32 && RR == 3) {
-            static std::atomic<unsigned long long> attr32{0ull};
-            if (!(attr32.load() & bit)) {
-                cudaFuncSetAttribute(k_step_smooth_f32<RR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)(k3::Shape<RR>::BYTES / 2));
-                attr32.fetch_or(bit);
-            }
-            k_step_smooth_f32<RR><<<grid, k3::NT, k3::Shape<RR>::BYTES / 2, s>>>(b, p, sh.chunk_len);
         } else {
             k_step_smooth<RR, false><<<grid, k3::NT, k3::Shape<RR>::BYTES, s>>>(b, p, sh.chunk_len);
         }
