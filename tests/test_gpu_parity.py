@@ -456,7 +456,8 @@ def run_slabs(P, ctx, F, M, cfg, iters, nslabs):
 
 
 @pytest.mark.parametrize("extra", [{}, {"lm.rejection": 1, "lm.tau": 0.2, "log_jacobian": 1},
-                                   {"optimizer": 1}, {"sigma_update": 2.0, "sigma_warp": 1.6}])
+                                   {"optimizer": 1}, {"sigma_update": 2.0, "sigma_warp": 1.6},
+                                   {"low_memory": 1, "lm.rejection": 1, "lm.tau": 0.2}])
 def test_slab_group_is_bit_identical_to_single_domain(P, ctx, extra):
     """Config 5 decomposition: 1, 2, 3 and 5 z-slabs (uneven splits) give the
     single-domain engine's losses, decisions, lambda and warp bit for bit."""

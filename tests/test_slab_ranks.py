@@ -26,7 +26,8 @@ SHIM = os.path.join(HERE, "nccl_shim", "libnccl_shim.so")
 pytestmark = pytest.mark.gpu
 
 SHAPE = (24, 20, 28)  # (nz, ny, nx): two slabs of 12 planes
-CASES = [{}, {"lm.rejection": 1, "lm.tau": 0.05, "log_jacobian": 1}, {"optimizer": 1}, {"metric": 2}]
+CASES = [{}, {"lm.rejection": 1, "lm.tau": 0.05, "log_jacobian": 1}, {"optimizer": 1}, {"metric": 2},
+         {"low_memory": 1}]
 
 
 def _pair():
