@@ -516,6 +516,7 @@ def pyramid_configs(ctx, lib):
     res, dt, att = run(F, M, cfg)
     out["config2"] = {"dims": [160, 192, 224], "schedule": "[4,2,1] x [100,75,50]", "rejection": True,
                       "wall_s": round(dt, 4), "attempts": att, "accepted_iters": len(res.loss_trace),
+                      "attempts_per_s": round(att / dt, 1), "accepted_iters_per_s": round(len(res.loss_trace) / dt, 1),
                       "final_r": res.loss_trace[-1].r, "peak_device_bytes": res.peak_device_bytes}
     F, M = synth(224, 192, 224, 2, 8.0)
     kw = dict(nlevels=4, factors=[8, 4, 2, 1], iters=[100, 100, 75, 50])
@@ -651,6 +652,19 @@ def cpu_tables():
     out["config1_64cubed_100_iters"] = {"wall_s": round(time.perf_counter() - t0, 3), "threads": 1,
                                         "median_iter_s": round(float(np.median(ts)), 5),
                                         "final_r": tr[-1].r, "kind": kind}
+    # one 192^3 registration on all host cores: the oracle port's plane-
+    # parallel loops (deterministic reductions), 2 warm-up + 5
+    # timed attempts, median (SURVEY 8(d) CPU baseline 3)
+    cores = os.cpu_count() or 1
+    Lp = O.lib("port")
+    Lp.orc_set_threads(cores)
+    F2, M2, _ = O.synth_pair((192, 192, 192), 1000, num_blobs=12, warp_max=6.0)
+    cfg7 = O.default_config(nlevels=1, factors=[1], iters=[7])
+    rc, _, _, ts = O.lm_run_level_timed(F2, M2, np.zeros(F2.shape + (3,)), cfg7, 7, kind="port")
+    Lp.orc_set_threads(min(8, cores))
+    out["one_192cubed_registration_all_cores"] = {"threads": cores, "kind": "port",
+                                                   "median_attempt_s": round(float(np.median(ts[2:7])), 4),
+                                                   "gvoxel_per_s": round(192 ** 3 / float(np.median(ts[2:7])) / 1e9, 6)}
     if O.have_ref():
         R = O.ref_lib()
         n = 192
