@@ -183,7 +183,7 @@ def run_ours(args, rank, world, local):
     pairs = args.pairs_per_gpu or max(1, args.global_batch // world)
     ctx = P.Context(local)
     lib = P.load()
-    cfg = P.reg_config(nlevels=1, factors=[1], iters=[100])
+    cfg = P.reg_config(nlevels=1, factors=[1], iters=[100], low_memory=args.low_memory)
     eng = P.Engine(shape, pairs=pairs, cfg=cfg, ctx=ctx)
 
     # synthetic pairs (config 4 seeds 1000..1063), generated on the GPU by the
@@ -757,6 +757,8 @@ def main():
     ap.add_argument("--global-batch", type=int, default=64, help="config 4: pairs split over the GPUs")
     ap.add_argument("--pairs-per-gpu", type=int, default=0,
                     help="fixed pairs per GPU instead (weak scaling); 0 = global batch / N")
+    ap.add_argument("--low-memory", type=int, default=0,
+                    help="wlm_reg_config.low_memory: 1 = no grad M buffer, K2 re-gathers (identical results)")
     ap.add_argument("--cpu-tables", action="store_true",
                     help="add the config-1 run and the 192^3 primitive table to cpu_baseline")
     ap.add_argument("--e2e-iters", type=int, default=100)
