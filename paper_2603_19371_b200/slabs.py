@@ -51,7 +51,11 @@ def halo_plan(shape, nslabs, slab, cfg: RegConfig | None = None):
 
 
 def nccl_library():
-    """Path of the libnccl.so.2 torch uses (the one to dlopen), or None."""
+    """Path of the libnccl.so.2 to dlopen: $WLM_NCCL_LIB when set (e.g. the
+    two-rank test stand-in), else the one torch uses, or None."""
+    env = os.environ.get("WLM_NCCL_LIB")
+    if env:
+        return env
     try:
         import nvidia.nccl  # noqa: F401
         for d in nvidia.nccl.__path__:

@@ -109,3 +109,25 @@ def test_two_rank_slabs_bit_identical_to_single_domain(ctx, extra):
     assert owned == [(0, 12), (12, 24)]
     if extra.get("lm.rejection"):
         assert sum(row["retries"] for row in t1) > 0, "the case should exercise the retry loop"
+
+
+def test_bench_config5_two_ranks_under_torchrun():
+    """bench.py --config 5 under the driver's torchrun launch with two ranks
+    (one GPU: gloo for torch.distributed, the NCCL stand-in for the slab
+    transport via WLM_NCCL_LIB): one JSON line from rank 0, strong scaling,
+    the slab group's multi-rank path (unique-id broadcast, RankSlab, owned
+    planes, e2e with host buffers) end to end."""
+    import json
+    import subprocess
+    env = dict(os.environ, WLM_BENCH_BACKEND="gloo", WLM_NCCL_LIB=SHIM)
+    out = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                          "--master-addr", "127.0.0.1", "--master-port", "29541",
+                          os.path.join(ROOT, "bench.py"), "--config", "5", "--size", "96", "--gpus", "2",
+                          "--steps", "3", "--warmup", "3", "--e2e-iters", "2"],
+                         capture_output=True, text=True, timeout=900, env=env)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [ln for ln in out.stdout.strip().splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    line = json.loads(lines[0])
+    assert line["n_gpus"] == 2 and line["scaling"] == "strong" and line["value"] > 0
+    assert "z-slab x2" in line["config"]["parallelism"] and line["e2e"]["value"] > 0
