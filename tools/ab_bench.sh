@@ -6,7 +6,7 @@ set -u
 mkdir -p gpurun_out
 run() {
   local tag=$1 lib=$2
-  WLM_LIB_PATH=$lib python bench.py --steps 20 --warmup 5 --no-extra --no-cpu-baseline --e2e-iters 1 --pairs-per-gpu 8 \
+  WLM_LIB_PATH=$lib python bench.py --steps 20 --warmup 5 --no-extra --no-cpu-baseline --e2e-iters 1 --pairs-per-gpu ${PAIRS:-8} \
     > gpurun_out/ab_$tag.json 2> gpurun_out/ab_$tag.err
   python - "$tag" <<'PY'
 import json, sys
