@@ -371,6 +371,8 @@ def run_ours(args, rank, world, local):
         line["cpu_baseline"] = cpu
     if extra:
         line["pyramid_configs"] = extra
+    if rank == 0 and world == 1 and args.table6:
+        line["table6"] = table6(ctx)
     traffic = load_traffic(dom)
     if traffic:
         line["roofline"]["traffic"] = traffic
@@ -543,6 +545,55 @@ def pyramid_configs(ctx, lib):
                       "state_bytes": {"lm": P.state_bytes(P.OPT_LM, (224, 192, 224)),
                                       "adam": P.state_bytes(P.OPT_ADAM, (224, 192, 224))}}
     return out
+
+
+def table6(ctx, sizes=(64, 128, 192, 256, 320, 384, 448, 512), steps=20):
+    """PAPER.md:585-610 (Table 6, FireANTs on an A6000: Adam vs LM peak memory
+    and time per step on N^3) on this engine: one pair per size, peak device
+    memory of the engine (arena high-water mark) and CUDA-event time per LM
+    attempt, for LM and Adam, in the default and the low-memory layouts."""
+    import ctypes as C
+
+    import numpy as np
+    import torch
+
+    import paper_2603_19371_b200 as P
+    from paper_2603_19371_b200._lib import Dims, SynthSpec
+    lib = P.load()
+    rows = []
+    for n in sizes:
+        F = np.empty((n, n, n), np.float32)
+        M = np.empty((n, n, n), np.float32)
+        spec = SynthSpec(Dims(n, n, n), 12, 0.0, min(6.0, n / 32.0), 0.01, 5)
+        ctx.check(lib.wlm_synth_pair(ctx.h, C.byref(spec), F.ctypes.data, M.ctypes.data, None, 0))
+        row = {"n": n}
+        for lean in (0, 1):
+            for name, opt in (("lm", P.OPT_LM), ("adam", P.OPT_ADAM)):
+                c = P.Context(0)
+                cfg = P.reg_config(nlevels=1, factors=[1], iters=[steps + 3], optimizer=opt, low_memory=lean)
+                eng = P.Engine((n, n, n), pairs=1, cfg=cfg, ctx=c)
+                eng.load(F[None], M[None])
+                eng.set_warp(None)
+                eng.begin_level(0)
+                eng.iterate(3)
+                c.synchronize()
+                stream = torch.cuda.ExternalStream(c.stream(), device="cuda:0")
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                eng.iterate(steps)
+                e1.record(stream)
+                e1.synchronize()
+                key = name + ("_lowmem" if lean else "")
+                row[key + "_peak_bytes"] = c.peak_bytes
+                row[key + "_ms_per_step"] = round(e0.elapsed_time(e1) / steps, 4)
+                eng.close()
+                c.close()
+        for sfx in ("", "_lowmem"):
+            row["lm_saving" + sfx] = round(1 - row["lm" + sfx + "_peak_bytes"] / row["adam" + sfx + "_peak_bytes"], 4)
+            row["adam_over_lm_time" + sfx] = round(row["adam" + sfx + "_ms_per_step"] /
+                                                   row["lm" + sfx + "_ms_per_step"], 3)
+        rows.append(row)
+    return rows
 
 
 def load_traffic(kernel):
@@ -760,6 +811,8 @@ def main():
                     help="fixed pairs per GPU instead (weak scaling); 0 = global batch / N")
     ap.add_argument("--low-memory", type=int, default=0,
                     help="wlm_reg_config.low_memory: 1 = no grad M buffer, K2 re-gathers (identical results)")
+    ap.add_argument("--table6", action="store_true",
+                    help="add PAPER.md Table 6's memory / time comparison (LM vs Adam, 64^3 .. 512^3)")
     ap.add_argument("--cpu-tables", action="store_true",
                     help="add the config-1 run and the 192^3 primitive table to cpu_baseline")
     ap.add_argument("--e2e-iters", type=int, default=100)
