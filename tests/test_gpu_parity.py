@@ -722,6 +722,45 @@ def test_random_configs_match_storage_oracle(P, ctx, case):
     compare_runs(tr, tr_o, aos(warp[0]), u_o, 1e-6, 1e-5)
 
 
+def _fuzz_generic_case(i):
+    """Seeded random configs for the generic device paths (LNCC radius != 2,
+    sigma > 2) and the low-memory layout, with the optimizers, rejection and
+    tiled LM."""
+    rng = np.random.default_rng(5000 + i)
+    radius = int(rng.choice([1, 2, 3]))
+    shape = tuple(int(v) for v in rng.integers(2 * radius + 3, 24, size=3))
+    optimizer = int(rng.choice([0, 0, 1, 2]))
+    kw = dict(nlevels=1, factors=[1], iters=[8], optimizer=optimizer, lncc_radius=radius,
+              sigma_update=float(rng.choice([1.0, 2.4, 3.0])), sigma_warp=float(rng.choice([0.5, 0.8, 2.2])),
+              low_memory=int(rng.integers(0, 2)))
+    if optimizer == 0:
+        kw["lm.rejection"] = int(rng.integers(0, 2))
+        kw["lm.tau"] = float(rng.choice([0.05, 0.3]))
+        kw["lm.tile_size"] = int(rng.choice([1, 1, 2]))
+    return shape, kw, float(rng.uniform(0.5, min(shape) / 4 - 0.1)), int(rng.integers(0, 1 << 30))
+
+
+@pytest.mark.parametrize("case", range(12))
+def test_random_generic_configs_match_storage_oracle(P, ctx, case):
+    """Seeded sweep over the generic paths and the low-memory layout against
+    the fp32-storage oracle at the storage bar (loss 1e-6, decisions and
+    lambda identical, warp 1e-5)."""
+    shape, kw, warp_max, seed = _fuzz_generic_case(case)
+    for attempt in range(6):
+        try:
+            F, M, _ = O.synth_pair(shape, seed, num_blobs=6, warp_max=warp_max / 2 ** attempt)
+            break
+        except ValueError:
+            continue
+    else:
+        raise AssertionError("synth: no positive-Jacobian draw")
+    warp, (tr,), _ = run_engine(P, ctx, F, M, P.reg_config(**kw), 8)
+    okw = {k: v for k, v in kw.items() if k != "low_memory"}
+    rc, u_o, _, tr_o = oracle_level(F, M, O.default_config(**okw), 8, "fp32")
+    assert rc == 0
+    compare_runs(tr, tr_o, aos(warp[0]), u_o, 1e-6, 1e-5)
+
+
 @pytest.mark.parametrize("su,sw", [(3.0, 0.5), (1.0, 2.5), (2.6, 3.1)])
 def test_large_sigma_engine_vs_oracle(P, ctx, su, sw):
     """sigma_update / sigma_warp > 2 (radius > 6: generic.cu's Gaussian passes,
