@@ -1,5 +1,9 @@
-// kernels.cu -- sm_100a kernels of the factored-LM iteration (SURVEY §2.2
-// K1-K5) and the standalone field operations.
+// kernels.cu -- the per-iteration support kernels of the factored-LM
+// iteration (Adam step, Jacobian diagnostic, level / iteration state, the
+// intensity shifts, tiled-LM matrices, Demons), the pyramid kernels, the
+// synth_pair helpers (fp32 smoothing, max, Jacobian) and the layout
+// conversions.  The stencil kernels K1-K4 are in hot_kernels.cu, the fp64
+// field mirrors in field64.cu, the generic-radius paths in generic.cu.
 //
 // All hot-path kernels share one z-marching separable-stencil schedule: a
 // CTA owns a 32 x TY column of output voxels and a chunk of z planes; each
