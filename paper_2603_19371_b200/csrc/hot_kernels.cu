@@ -655,19 +655,29 @@ __global__ void __launch_bounds__(k1::NT, 2) k_lncc_fwd(Batch b, int chunk_len) 
             m[2 * q] = c.x; m[2 * q + 1] = c.y;
         }
         double a[2][5];
+        // the two windows share taps 1..W-1: sum them once, then add the
+        // outer tap of each side (a fixed order per output: chunk- and
+        // slab-invariant like the direct sums)
+        {
+            double c0 = f[1], c1 = m[1], c2 = f[1] * f[1], c3 = m[1] * m[1], c4 = f[1] * m[1];
 #pragma unroll
-        for (int j = 0; j < 2; ++j) {
-            double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0, a4 = 0.0;
-#pragma unroll
-            for (int d = 0; d < W; ++d) {
-                const double fv = f[j + d], mv = m[j + d];
-                a0 += fv;
-                a1 += mv;
-                a2 = fma(fv, fv, a2);
-                a3 = fma(mv, mv, a3);
-                a4 = fma(fv, mv, a4);
+            for (int d = 2; d < W; ++d) {
+                const double fv = f[d], mv = m[d];
+                c0 += fv;
+                c1 += mv;
+                c2 = fma(fv, fv, c2);
+                c3 = fma(mv, mv, c3);
+                c4 = fma(fv, mv, c4);
             }
-            a[j][0] = a0; a[j][1] = a1; a[j][2] = a2; a[j][3] = a3; a[j][4] = a4;
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+                const double fv = f[j * W], mv = m[j * W];
+                a[j][0] = c0 + fv;
+                a[j][1] = c1 + mv;
+                a[j][2] = fma(fv, fv, c2);
+                a[j][3] = fma(mv, mv, c3);
+                a[j][4] = fma(fv, mv, c4);
+            }
         }
         // the two outputs of a moment are adjacent: one 16-byte store each
 #pragma unroll
@@ -707,9 +717,9 @@ __global__ void __launch_bounds__(k1::NT, 2) k_lncc_fwd(Batch b, int chunk_len) 
                 // y pass into the static ring; z sum taken directly over the ring
 #pragma unroll
                 for (int c = 0; c < 5; ++c) {
-                    double s = 0.0;
+                    double s = x_a[c * IH * TX + oy * TX + ox];
 #pragma unroll
-                    for (int d = 0; d < W; ++d) s += x_a[c * IH * TX + (oy + d) * TX + ox];
+                    for (int d = 1; d < W; ++d) s += x_a[c * IH * TX + (oy + d) * TX + ox];
                     ring[rs][c] = s;
                 }
                 const int zo = zi - R;
@@ -719,9 +729,9 @@ __global__ void __launch_bounds__(k1::NT, 2) k_lncc_fwd(Batch b, int chunk_len) 
                         double Sm[5];
 #pragma unroll
                         for (int c = 0; c < 5; ++c) {
-                            double s = 0.0;
+                            double s = ring[(rs + 1) % W][c];
 #pragma unroll
-                            for (int d = 0; d < W; ++d) s += ring[(rs + 1 + d) % W][c];
+                            for (int d = 1; d < W; ++d) s += ring[(rs + 1 + d) % W][c];
                             Sm[c] = s;
                         }
                         const double inv = c_inv_count[cxy * axis_count(zo, g.nz, R)];
@@ -914,13 +924,11 @@ __global__ void __launch_bounds__(k2::NT, WLM_K2_MIN_BLOCKS) k_lncc_bwd(Batch b,
                 const double2 t = src[q];
                 v[2 * q] = t.x; v[2 * q + 1] = t.y;
             }
-            double o0 = 0.0, o1 = 0.0;
+            // taps 1..W-1 are shared by the two windows (as K1b)
+            double core = v[1];
 #pragma unroll
-            for (int d = 0; d < W; ++d) {
-                o0 += v[d];
-                o1 += v[d + 1];
-            }
-            *reinterpret_cast<double2*>(out + c * IH * TX + xr * TX + 2 * xj) = make_double2(o0, o1);
+            for (int d = 2; d < W; ++d) core += v[d];
+            *reinterpret_cast<double2*>(out + c * IH * TX + xr * TX + 2 * xj) = make_double2(v[0] + core, core + v[W]);
         }
     };
 
@@ -990,9 +998,9 @@ __global__ void __launch_bounds__(k2::NT, WLM_K2_MIN_BLOCKS) k_lncc_bwd(Batch b,
                 if (emit) issue_own(zo + k2::OWN_AHEAD);
 #pragma unroll
                 for (int c = 0; c < 3; ++c) {
-                    double s = 0.0;
+                    double s = x_a[c * IH * TX + oy * TX + ox];
 #pragma unroll
-                    for (int d = 0; d < W; ++d) s += x_a[c * IH * TX + (oy + d) * TX + ox];
+                    for (int d = 1; d < W; ++d) s += x_a[c * IH * TX + (oy + d) * TX + ox];
                     ring[rs][c] = s;
                 }
                 if (emit) __pipeline_wait_prior(k2::OWN_AHEAD);  // plane zo has landed
@@ -1000,9 +1008,9 @@ __global__ void __launch_bounds__(k2::NT, WLM_K2_MIN_BLOCKS) k_lncc_bwd(Batch b,
                     double Sm[3];
 #pragma unroll
                     for (int c = 0; c < 3; ++c) {
-                        double s = 0.0;
+                        double s = ring[(rs + 1) % W][c];
 #pragma unroll
-                        for (int d = 0; d < W; ++d) s += ring[(rs + 1 + d) % W][c];
+                        for (int d = 1; d < W; ++d) s += ring[(rs + 1 + d) % W][c];
                         Sm[c] = s;
                     }
                     double mw, gm[3], fv;
