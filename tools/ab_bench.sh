@@ -19,6 +19,6 @@ except Exception as e:
 PY
 }
 for rep in 1 2; do
-  run base "" 
+  [ "${SKIPBASE:-0}" = 1 ] || run base ""
   for v in "$@"; do run $v build/var_$v/libwarplm_b200.so; done
 done
