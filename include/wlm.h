@@ -310,6 +310,12 @@ wlm_status wlm_slab_group_create_nccl(wlm_ctx* ctx, wlm_dims d, int rank, int nr
                                       const wlm_reg_config* cfg, wlm_slab_group** out);
 /* Planes [zs, ze) owned by this group's slabs (get_warp fills only these). */
 wlm_status wlm_slab_group_owned(const wlm_slab_group* g, int* zs, int* ze);
+/* Which halo exchanges the producing kernels fuse (bit k: buffer kind k of
+ * wlm_halo_xfer -- 0 g, 1 dU_s, 2 warp, 3 A/B/E): the kernel stores the
+ * neighbour's halo planes into its buffer itself (peer memory through CUDA
+ * IPC across processes) and the exchange only orders.  0 with one slab or
+ * WLM_SLAB_FUSED=0 (every exchange copies). */
+wlm_status wlm_slab_group_fused_halos(const wlm_slab_group* g, int* mask);
 void wlm_slab_group_destroy(wlm_slab_group* g);
 wlm_status wlm_slab_group_load(wlm_slab_group* g, const float* F, const float* M, int is_host);
 wlm_status wlm_slab_group_set_warp(wlm_slab_group* g, const float* u, int is_host);

@@ -136,6 +136,7 @@ SIGNATURES = {
     "wlm_slab_group_create_nccl": (C.c_int, [_CTX, Dims, C.c_int, C.c_int, C.c_char_p, C.c_char_p,
                                              C.POINTER(RegConfig), C.POINTER(_ENG)]),
     "wlm_slab_group_owned": (C.c_int, [_ENG, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
+    "wlm_slab_group_fused_halos": (C.c_int, [_ENG, C.POINTER(C.c_int)]),
     "wlm_slab_group_destroy": (None, [_ENG]),
     "wlm_slab_group_load": (C.c_int, [_ENG, _VP, _VP, C.c_int]),
     "wlm_slab_group_set_warp": (C.c_int, [_ENG, _VP, C.c_int]),

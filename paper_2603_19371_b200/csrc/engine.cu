@@ -200,6 +200,8 @@ void engine_alloc(wlm_engine* e) {
     b.partials = e->partials.p;
     if (!e->shared_plane_sum) b.plane_sum = e->plane_sum.p;
     b.zero_foreign_planes = 0;
+    b.peer_on = 0;  // a slab group turns on its fused halo stores after allocation
+    std::memset(&b.peer, 0, sizeof(b.peer));
     b.shift_part = e->shift_part.p;
     b.TM = e->TM.p;
     b.HIST = e->HIST.p;

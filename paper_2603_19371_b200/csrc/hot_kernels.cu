@@ -263,6 +263,17 @@ __device__ __forceinline__ double sample_vol(const float* __restrict__ M, const 
 constexpr double kNaN64 = __builtin_nan("");
 
 // ---------------------------------------------------------------------------
+// Fused halo stores (Batch::peer): plane z of kind k goes to neighbour side sd
+// when it lies in that side's send range; the remote voxel index follows the
+// neighbour's buffer origin.
+__device__ __forceinline__ bool peer_sends(const Batch& b, int sd, int k, int z) {
+    return sd == 0 ? z < b.peer.lo_end[k] : z >= b.peer.hi_begin[k];
+}
+__device__ __forceinline__ long long peer_index(const Batch& b, int sd, int z, int nxy, int ooff) {
+    return (long long)(z - b.peer.zlo[sd]) * nxy + ooff;
+}
+
+// ---------------------------------------------------------------------------
 // K1a: warp of the moving image, Mw(x) = M(x + u(x)) in fp64, for the owned
 // planes plus the 2 halo planes the window pass reads.  Block (32 x 8) = a
 // 32 x 8 (x, y) tile of one plane; one voxel per thread, few registers (high
@@ -579,7 +590,7 @@ struct Shape {
 };
 }  // namespace k1
 
-template <int R>
+template <int R, bool PEER = false>
 __global__ void __launch_bounds__(k1::NT, 2) k_lncc_fwd(Batch b, int chunk_len) {
     using S = k1::Shape<R>;
     constexpr int TX = k1::TX, NT = k1::NT, W = 2 * R + 1;
@@ -756,6 +767,17 @@ __global__ void __launch_bounds__(k1::NT, 2) k_lncc_fwd(Batch b, int chunk_len) 
                         Aout[o] = Aa;
                         Bout[o] = Bb;
                         Eout[o] = Ee;
+                        if (PEER) {
+#pragma unroll
+                            for (int sd = 0; sd < 2; ++sd)
+                                if (peer_sends(b, sd, 3, zo)) {
+                                    float* Rm = b.peer.abe[sd];
+                                    const long long rn = b.peer.n[sd], ri = peer_index(b, sd, zo, nxy, ooff);
+                                    Rm[ri] = Aa;
+                                    Rm[rn + ri] = Bb;
+                                    reinterpret_cast<double*>(Rm + 2 * rn)[ri] = Ee;
+                                }
+                        }
                     }
                     rho = warp_sum(rho);
                     if (ox == 0) part_cta[(long long)zo * part_plane] = rho;
@@ -833,7 +855,7 @@ constexpr size_t OWN_BYTES = sizeof(OwnSlot) * OWN_SLOTS;
 constexpr size_t OWN_BYTES_LEAN = sizeof(OwnSlotLean) * OWN_SLOTS;
 }  // namespace k2
 
-template <int R, bool LEAN>
+template <int R, bool LEAN, bool PEER = false>
 #ifndef WLM_K2_MIN_BLOCKS
 #define WLM_K2_MIN_BLOCKS 2
 #endif
@@ -1031,6 +1053,17 @@ __global__ void __launch_bounds__(k2::NT, WLM_K2_MIN_BLOCKS) k_lncc_bwd(Batch b,
                     G[o] = (float)(dm * gm[0]);
                     G[n + o] = (float)(dm * gm[1]);
                     G[2 * n + o] = (float)(dm * gm[2]);
+                    if (PEER) {
+#pragma unroll
+                        for (int sd = 0; sd < 2; ++sd)
+                            if (peer_sends(b, sd, 0, zo)) {
+                                float* Rm = b.peer.g[sd] + peer_index(b, sd, zo, nxy, ooff);
+                                const long long rn = b.peer.n[sd];
+                                Rm[0] = (float)(dm * gm[0]);
+                                Rm[rn] = (float)(dm * gm[1]);
+                                Rm[2 * rn] = (float)(dm * gm[2]);
+                            }
+                    }
                 }
                 x_pass(in_b, x_b);
                 store_halo(in_a);
@@ -1121,7 +1154,7 @@ struct Shape {
 };
 }  // namespace k3
 
-template <int R, bool TILED>
+template <int R, bool TILED, bool PEER = false>
 __global__ void __launch_bounds__(k3::NT, k3::MINB) k_step_smooth(Batch b, LmParams p, int chunk_len) {
     using S = k3::Shape<R>;
     constexpr int TX = k3::TX, NT = k3::NT, W = 2 * R + 1;
@@ -1326,6 +1359,7 @@ __global__ void __launch_bounds__(k3::NT, k3::MINB) k_step_smooth(Batch b, LmPar
                     double inv = inv_full;
                     if (zo < R || zo + R > g.nz - 1) inv = inv_xy * border_inv(s_binv, zo, g.nz, R);
                     const int o = (zo - g.zlo) * nxy + ooff;
+                    float vv[3];
 #pragma unroll
                     for (int c = 0; c < 3; ++c) {
                         double s = 0.0;
@@ -1333,7 +1367,19 @@ __global__ void __launch_bounds__(k3::NT, k3::MINB) k_step_smooth(Batch b, LmPar
                         for (int d = 0; d < W; ++d) s = fma(w[d], ring[(rs + 1 + d) % W][c], s);
                         const float v = (float)(s * inv);
                         V[c * n + o] = v;
+                        vv[c] = v;
                         mx = fmaxf(mx, fabsf(v));
+                    }
+                    if (PEER) {
+#pragma unroll
+                        for (int sd = 0; sd < 2; ++sd)
+                            if (peer_sends(b, sd, 1, zo)) {
+                                float* Rm = b.peer.v[sd] + peer_index(b, sd, zo, nxy, ooff);
+                                const long long rn = b.peer.n[sd];
+                                Rm[0] = vv[0];
+                                Rm[rn] = vv[1];
+                                Rm[2 * rn] = vv[2];
+                            }
                     }
                 }
                 if (k3::COLY) {
@@ -1464,7 +1510,7 @@ __device__ __forceinline__ void tma_load_5d(void* dst, const CUtensorMap* map, i
 // path) arrives in its ring slot by one bulk tensor copy issued by thread 0;
 // consumers wait on the slot's mbarrier.  Used when the U rows are 16-byte
 // multiples (nx % 4 == 0), else the register-staged path.
-template <int R, bool TMA>
+template <int R, bool TMA, bool PEER = false>
 __global__ void __launch_bounds__(k4::NT, 1) k_compose_smooth(Batch b, LmParams p, int chunk_len,
                                                               const __grid_constant__ CUtensorMap tmap_u) {
     using S = k4::Shape<R>;
@@ -1799,12 +1845,25 @@ __global__ void __launch_bounds__(k4::NT, 1) k_compose_smooth(Batch b, LmParams 
                     double inv = inv_full;
                     if (zo < R || zo + R > g.nz - 1) inv = inv_xy * border_inv(s_binv, zo, g.nz, R);
                     const int o = (zo - g.zlo) * nxy + ooff;
+                    float uu[3];
 #pragma unroll
                     for (int c = 0; c < 3; ++c) {
                         double s = 0.0;
 #pragma unroll
                         for (int d = 0; d < W; ++d) s = fma(w[d], ring[(rs + 1 + d) % W][c], s);
-                        UN_[c * n + o] = (float)(s * inv);
+                        uu[c] = (float)(s * inv);
+                        UN_[c * n + o] = uu[c];
+                    }
+                    if (PEER) {
+#pragma unroll
+                        for (int sd = 0; sd < 2; ++sd)
+                            if (peer_sends(b, sd, 2, zo)) {
+                                const long long rn = b.peer.n[sd];
+                                float* Rm = b.peer.u[sd] + (1 - cur) * 3 * rn + peer_index(b, sd, zo, nxy, ooff);
+                                Rm[0] = uu[0];
+                                Rm[rn] = uu[1];
+                                Rm[2 * rn] = uu[2];
+                            }
                     }
                 }
                 // plane zi was last read by compose(zi + 1) before the barrier
@@ -1902,7 +1961,10 @@ void launch_lncc_window(const Batch& b, cudaStream_t s) {
     const LaunchShape sh = shape_for(b.g, b.pairs, k1::TY, b.ctas_per_sm);
     dim3 grid = sh.grid();
     grid.z = b.pairs;
-    k_lncc_fwd<2><<<grid, k1::NT, 0, s>>>(b, sh.chunk_len);
+    if (b.peer_on)
+        k_lncc_fwd<2, true><<<grid, k1::NT, 0, s>>>(b, sh.chunk_len);
+    else
+        k_lncc_fwd<2><<<grid, k1::NT, 0, s>>>(b, sh.chunk_len);
     ++g_kernel_launches;
 }
 
@@ -1935,10 +1997,18 @@ void launch_lncc_bwd(const Batch& b, const LmParams& p, cudaStream_t s) {
         cudaFuncSetAttribute(k_lncc_bwd<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k2::OWN_BYTES);
         cudaFuncSetAttribute(k_lncc_bwd<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)k2::OWN_BYTES_LEAN);
+        cudaFuncSetAttribute(k_lncc_bwd<2, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)k2::OWN_BYTES);
+        cudaFuncSetAttribute(k_lncc_bwd<2, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)k2::OWN_BYTES_LEAN);
         attr.fetch_or(bit);
     }
-    if (p.lean)
+    if (p.lean && b.peer_on)
+        k_lncc_bwd<2, true, true><<<grid, k2::NT, k2::OWN_BYTES_LEAN, s>>>(b, p, sh.chunk_len);
+    else if (p.lean)
         k_lncc_bwd<2, true><<<grid, k2::NT, k2::OWN_BYTES_LEAN, s>>>(b, p, sh.chunk_len);
+    else if (b.peer_on)
+        k_lncc_bwd<2, false, true><<<grid, k2::NT, k2::OWN_BYTES, s>>>(b, p, sh.chunk_len);
     else
         k_lncc_bwd<2, false><<<grid, k2::NT, k2::OWN_BYTES, s>>>(b, p, sh.chunk_len);
     ++g_kernel_launches;
@@ -1960,10 +2030,14 @@ void launch_step_smooth(const Batch& b, const LmParams& p, cudaStream_t s) {
                                  (int)k3::Shape<RR>::BYTES);
             cudaFuncSetAttribute(k_step_smooth<RR, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)k3::Shape<RR>::BYTES);
+            cudaFuncSetAttribute(k_step_smooth<RR, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)k3::Shape<RR>::BYTES);
             attr.fetch_or(bit);
         }
         if (p.optimizer == WLM_OPT_LM && p.tile_k > 1) {
             k_step_smooth<RR, true><<<grid, k3::NT, k3::Shape<RR>::BYTES, s>>>(b, p, sh.chunk_len);
+        } else if (b.peer_on) {  // fused halo stores (slab groups; never tiled)
+            k_step_smooth<RR, false, true><<<grid, k3::NT, k3::Shape<RR>::BYTES, s>>>(b, p, sh.chunk_len);
         } else {
             k_step_smooth<RR, false><<<grid, k3::NT, k3::Shape<RR>::BYTES, s>>>(b, p, sh.chunk_len);
         }
@@ -2017,9 +2091,17 @@ void launch_compose_smooth(const Batch& b, const LmParams& p, cudaStream_t s) {
                                  (int)k4::Shape<RR>::BYTES);
             cudaFuncSetAttribute(k_compose_smooth<RR, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)k4::Shape<RR>::BYTES);
+            cudaFuncSetAttribute(k_compose_smooth<RR, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)k4::Shape<RR>::BYTES);
+            cudaFuncSetAttribute(k_compose_smooth<RR, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)k4::Shape<RR>::BYTES);
             attr.fetch_or(bit);
         }
-        if (b.tma_u_ok)
+        if (b.peer_on && b.tma_u_ok)
+            k_compose_smooth<RR, true, true><<<grid, k4::NT, k4::Shape<RR>::BYTES, s>>>(b, p, sh.chunk_len, b.tma_u);
+        else if (b.peer_on)
+            k_compose_smooth<RR, false, true><<<grid, k4::NT, k4::Shape<RR>::BYTES, s>>>(b, p, sh.chunk_len, b.tma_u);
+        else if (b.tma_u_ok)
             k_compose_smooth<RR, true><<<grid, k4::NT, k4::Shape<RR>::BYTES, s>>>(b, p, sh.chunk_len, b.tma_u);
         else
             k_compose_smooth<RR, false><<<grid, k4::NT, k4::Shape<RR>::BYTES, s>>>(b, p, sh.chunk_len, b.tma_u);

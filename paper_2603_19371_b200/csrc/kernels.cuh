@@ -71,6 +71,24 @@ struct LmParams {
 };
 
 // Buffers of a batch of `pairs` registrations of identical geometry.
+// Fused halo stores of a slab group (slab.cu): an output plane
+// that a neighbouring slab keeps as halo is stored by the producing kernel
+// straight into that slab's buffer as well -- peer memory (CUDA IPC over
+// NVLink) with one process per GPU, the same device in-process -- so no
+// separate exchange moves it.  Buffer kinds: 0 g (K2), 1 dU_s (K3), 2 the
+// attempt warp (K4), 3 A, B, E (K1b).  Side 0 is the lower neighbour, 1 the
+// upper; slab engines hold one pair.
+struct HaloPeer {
+    float* g[2];
+    float* v[2];
+    float* u[2];      // the neighbour's U (both ping-pong buffers)
+    float* abe[2];
+    long long n[2];   // the neighbour's channel stride (voxels incl. its halo)
+    int zlo[2];       // the neighbour's first buffer plane
+    int lo_end[4];    // planes [g.zs, lo_end[k]) of kind k go to the lower neighbour
+    int hi_begin[4];  // planes [hi_begin[k], g.ze) go to the upper one
+};
+
 struct Batch {
     Geo g;
     int pairs;        // pairs in this launch: pair0 .. pair0 + pairs - 1
@@ -99,6 +117,8 @@ struct Batch {
     CUtensorMap tma_u;  // 5D map over U: (x, y, local z, buffer*3 + component, pair)
     int max_blocks;
     int ctas_per_sm;    // z-chunking target of this launch (0 -> 4; pair groups use 1)
+    int peer_on;        // fused halo stores (peer valid)
+    HaloPeer peer;
 };
 
 struct LaunchShape {

@@ -32,6 +32,7 @@
 #include <algorithm>
 #include <cstring>
 #include <string>
+#include <array>
 #include <vector>
 
 #include <cstdlib>
@@ -46,7 +47,7 @@ typedef struct ncclComm* Comm;
 struct UniqueId {
     char internal[128];
 };
-enum { Int32 = 2, Uint32 = 3, Uint64 = 5, Float32 = 7, Float64 = 8 };
+enum { Uint8 = 1, Int32 = 2, Uint32 = 3, Uint64 = 5, Float32 = 7, Float64 = 8 };
 enum { Sum = 0, Max = 2, Min = 3 };
 typedef int (*GetUniqueId_t)(UniqueId*);
 typedef int (*CommInitRank_t)(Comm*, int, UniqueId, int);
@@ -242,7 +243,14 @@ struct wlm_slab_group {
     cudaStream_t side = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
 
+    // fused halo stores (see setup_fused): per buffer kind, whether the
+    // producing kernel stores the neighbours' halo planes itself
+    bool fused[4] = {false, false, false, false};
+    std::vector<void*> ipc_open;  // neighbour buffers mapped by CUDA IPC (nccl)
+    DevBuf<int> token;            // [send, recv lower, recv upper] ordering tokens (nccl)
+
     ~wlm_slab_group() {
+        for (void* q : ipc_open) cudaIpcCloseMemHandle(q);
         if (side) cudaStreamDestroy(side);
         if (ev_fork) cudaEventDestroy(ev_fork);
         if (ev_join) cudaEventDestroy(ev_join);
@@ -368,6 +376,138 @@ struct wlm_slab_group {
         nccl_check(nccl::g_api.group_end(), "ncclGroupEnd");
     }
 
+    // Fused halo stores.  K2 (g), K3 (dU_s),
+    // K4 (the attempt warp) and K1b (A, B, E) store each output plane that a
+    // neighbour keeps as halo straight into the neighbour's buffer as well:
+    // the same device in-process; peer memory mapped by CUDA IPC (NVLink on
+    // a multi-GPU node) with one process per GPU.  The exchange after such a
+    // stage then moves no data: in-process the single stream already orders
+    // the neighbour's consumer after every producer; across processes a
+    // 4-byte ncclSend/ncclRecv with each neighbour, queued behind the
+    // producer, orders it (the neighbour's consumer waits for the token,
+    // which is sent after the producer kernel completed).  Each producer
+    // writes only planes the receiver does not itself write, into the buffer
+    // the receiver reads next, and every write happens after the receiver's
+    // last read of the previous contents (its previous stage chain precedes
+    // the token the producer waited for), so the result is bit-identical to
+    // the copy exchange.  Kinds whose producer is not a fused kernel (Adam's
+    // g, MSE/MI, tiled LM's step, the generic paths) keep the exchange.
+    // WLM_SLAB_FUSED=0 keeps every exchange.
+    void setup_fused() {
+        const char* v = std::getenv("WLM_SLAB_FUSED");
+        if ((v && std::atoi(v) == 0) || nslabs < 2) return;
+        const LmParams& P = eng[0]->P;
+        const bool lncc2 = P.metric == WLM_METRIC_LNCC && P.radius == 2;
+        fused[BUF_G] = lncc2 && P.optimizer != WLM_OPT_ADAM && P.tile_k <= 1;
+        fused[BUF_V] = P.Ru <= 6 && P.tile_k <= 1;
+        fused[BUF_U] = P.Rw <= 6;
+        fused[BUF_ABE] = lncc2;
+        struct Info {
+            cudaIpcMemHandle_t h[4];
+            long long n;
+            int zlo, pad;
+        };
+        // this process's (or engine's) buffers as a neighbour sees them
+        auto bases = [](wlm_engine* e, void* out[4]) {
+            out[0] = e->G.p; out[1] = e->VS.p; out[2] = e->U.p; out[3] = e->ABE.p;
+        };
+        std::vector<std::array<void*, 4>> nb_base(2 * eng.size(), {nullptr, nullptr, nullptr, nullptr});
+        std::vector<long long> nb_n(2 * eng.size(), 0);
+        std::vector<int> nb_zlo(2 * eng.size(), 0);
+        if (!distributed()) {
+            for (size_t li = 0; li < eng.size(); ++li)
+                for (int sd = 0; sd < 2; ++sd) {
+                    const int k = first + (int)li + (sd == 0 ? -1 : 1);
+                    if (k < first || k >= first + (int)eng.size()) continue;
+                    wlm_engine* o = local(k);
+                    void* b4[4];
+                    bases(o, b4);
+                    for (int q = 0; q < 4; ++q) nb_base[2 * li + sd][q] = b4[q];
+                    nb_n[2 * li + sd] = o->g.n;
+                    nb_zlo[2 * li + sd] = o->g.zlo;
+                }
+        } else {
+            wlm_engine* e = eng[0];
+            Info mine{};
+            void* b4[4];
+            bases(e, b4);
+            for (int q = 0; q < 4; ++q) CK(cudaIpcGetMemHandle(&mine.h[q], b4[q]));
+            mine.n = e->g.n;
+            mine.zlo = e->g.zlo;
+            DevBuf<unsigned char> buf(ctx, 3 * sizeof(Info));
+            cudaStream_t st = ctx->stream;
+            CK(cudaMemcpyAsync(buf.p, &mine, sizeof(Info), cudaMemcpyHostToDevice, st));
+            nccl_check(nccl::g_api.group_start(), "ncclGroupStart");
+            for (int sd = 0; sd < 2; ++sd) {
+                const int k = first + (sd == 0 ? -1 : 1);
+                if (k < 0 || k >= nslabs) continue;
+                nccl_check(nccl::g_api.send(buf.p, sizeof(Info), nccl::Uint8, k, comm, st), "ncclSend");
+                nccl_check(nccl::g_api.recv(buf.p + (1 + sd) * sizeof(Info), sizeof(Info), nccl::Uint8, k, comm, st),
+                           "ncclRecv");
+            }
+            nccl_check(nccl::g_api.group_end(), "ncclGroupEnd");
+            Info theirs[2];
+            CK(cudaMemcpyAsync(theirs, buf.p + sizeof(Info), 2 * sizeof(Info), cudaMemcpyDeviceToHost, st));
+            CK(cudaStreamSynchronize(st));
+            for (int sd = 0; sd < 2; ++sd) {
+                const int k = first + (sd == 0 ? -1 : 1);
+                if (k < 0 || k >= nslabs) continue;
+                for (int q = 0; q < 4; ++q) {
+                    void* ptr = nullptr;
+                    CK(cudaIpcOpenMemHandle(&ptr, theirs[sd].h[q], cudaIpcMemLazyEnablePeerAccess));
+                    ipc_open.push_back(ptr);
+                    nb_base[sd][q] = ptr;
+                }
+                nb_n[sd] = theirs[sd].n;
+                nb_zlo[sd] = theirs[sd].zlo;
+            }
+            token = DevBuf<int>(ctx, 3);
+            CK(cudaMemsetAsync(token.p, 0, sizeof(int) * 3, st));
+        }
+        for (size_t li = 0; li < eng.size(); ++li) {
+            wlm_engine* e = eng[li];
+            HaloPeer hp{};
+            for (int sd = 0; sd < 2; ++sd) {
+                hp.g[sd] = static_cast<float*>(nb_base[2 * li + sd][0]);
+                hp.v[sd] = static_cast<float*>(nb_base[2 * li + sd][1]);
+                hp.u[sd] = static_cast<float*>(nb_base[2 * li + sd][2]);
+                hp.abe[sd] = static_cast<float*>(nb_base[2 * li + sd][3]);
+                hp.n[sd] = nb_n[2 * li + sd];
+                hp.zlo[sd] = nb_zlo[2 * li + sd];
+            }
+            for (int k = 0; k < 4; ++k) {
+                hp.lo_end[k] = e->g.zs;  // empty unless a fused send row says otherwise
+                hp.hi_begin[k] = e->g.ze;
+            }
+            for (const wlm_halo_xfer& r : plan[li]) {
+                if (!r.send || r.buffer > BUF_ABE || !fused[r.buffer]) continue;
+                if (r.peer < first + (int)li) hp.lo_end[r.buffer] = r.z1;  // [zs, z1) to the lower neighbour
+                else hp.hi_begin[r.buffer] = r.z0;                        // [z0, ze) to the upper one
+            }
+            e->B.peer = hp;
+            e->B.peer_on = 1;
+        }
+    }
+    bool any_fused() const { return fused[0] || fused[1] || fused[2] || fused[3]; }
+
+    // The halo step after a producer stage of buffer kind b: the copy
+    // exchange, or (fused) only the ordering token across processes.
+    void halo(int b, cudaStream_t s) {
+        if (b > BUF_ABE || !fused[b]) {
+            exchange(b, s);
+            return;
+        }
+        if (!distributed()) return;
+        nccl_check(nccl::g_api.group_start(), "ncclGroupStart");
+        for (int sd = 0; sd < 2; ++sd) {
+            const int k = first + (sd == 0 ? -1 : 1);
+            if (k < 0 || k >= nslabs) continue;
+            nccl_check(nccl::g_api.send(token.p, 1, nccl::Int32, k, comm, s), "ncclSend(token)");
+            nccl_check(nccl::g_api.recv(token.p + 1 + sd, 1, nccl::Int32, k, comm, s), "ncclRecv(token)");
+        }
+        nccl_check(nccl::g_api.group_end(), "ncclGroupEnd");
+    }
+
     void reduce_max(int jac, cudaStream_t s) {
         if (!distributed()) {
             k_group_combine<<<1, 1, 0, s>>>(sts.p, (int)eng.size(), jac);
@@ -406,7 +546,7 @@ struct wlm_slab_group {
         for (auto* e : eng) e->stage_eval(mode, s);
         reduce_planes(s);
         for (auto* e : eng) e->stage_finalize(mode, s);
-        exchange(BUF_ABE, s);
+        halo(BUF_ABE, s);
     }
 
     // Interior / boundary split: every stage whose output a
@@ -420,7 +560,7 @@ struct wlm_slab_group {
     bool overlap_enabled() const {
         const LmParams& P = eng[0]->P;
         const char* v = std::getenv("WLM_SLAB_OVERLAP");
-        if (v && std::atoi(v) == 0) return false;
+        if ((v && std::atoi(v) == 0) || any_fused()) return false;  // fused stores need no split
         return P.metric == WLM_METRIC_LNCC && P.radius == 2 && P.tile_k <= 1 && P.Ru <= 6 && P.Rw <= 6;
     }
 
@@ -494,7 +634,7 @@ struct wlm_slab_group {
             return;
         }
         for (auto* e : eng) e->stage_grad(s);
-        exchange(BUF_G, s);
+        halo(BUF_G, s);
         if (eng[0]->P.optimizer == WLM_OPT_LM && eng[0]->P.tile_k > 1) {
             for (auto* e : eng) launch_tile_matrix(e->B, e->P, s);  // owned tiles
             exchange(BUF_TM, s);                                   // halo tiles
@@ -503,9 +643,9 @@ struct wlm_slab_group {
             for (auto* e : eng) e->stage_step(s);
         }
         reduce_max(0, s);
-        exchange(BUF_V, s);
+        halo(BUF_V, s);
         for (auto* e : eng) launch_compose_smooth(e->B, e->P, s);
-        exchange(BUF_U, s);
+        halo(BUF_U, s);
         if (eng[0]->P.log_jacobian) {
             for (auto* e : eng) launch_jacobian_diag(e->B, e->P, s);
             reduce_max(1, s);
@@ -650,6 +790,7 @@ wlm_status make_group(wlm_ctx* ctx, wlm_dims d, int nslabs, int first, int count
             grp->plan.push_back(slab_plan(d, nslabs, k, e->P.Ru, e->P.Rw, tk));
             hst.push_back(e->st.p);
         }
+        grp->setup_fused();
         grp->sts = DevBuf<PairState*>(ctx, hst.size());
         CK(cudaMemcpyAsync(grp->sts.p, hst.data(), sizeof(PairState*) * hst.size(), cudaMemcpyHostToDevice,
                            ctx->stream));
@@ -818,6 +959,14 @@ wlm_status wlm_slab_group_get_warp(wlm_slab_group* g, float* u, int is_host) {
         }
         CK(cudaStreamSynchronize(ctx->stream));
     });
+}
+
+wlm_status wlm_slab_group_fused_halos(const wlm_slab_group* g, int* mask) {
+    if (!g || !mask) return WLM_INVALID_ARG;
+    *mask = 0;
+    for (int k = 0; k < 4; ++k)
+        if (g->fused[k]) *mask |= 1 << k;
+    return WLM_OK;
 }
 
 wlm_status wlm_slab_group_owned(const wlm_slab_group* g, int* zs, int* ze) {

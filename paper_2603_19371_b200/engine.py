@@ -204,6 +204,13 @@ class SlabGroup:
         """New registration: lambda back to lambda0 (begin_level carries it)."""
         self._chk(self.lib.wlm_slab_group_reset(self.h))
 
+    def fused_halos(self):
+        """Bit mask of the halo exchanges fused into their producing kernels
+        (bit 0 g, 1 dU_s, 2 warp, 3 A/B/E; include/wlm.h)."""
+        m = C.c_int()
+        self._chk(self.lib.wlm_slab_group_fused_halos(self.h, C.byref(m)))
+        return m.value
+
     def iterate(self, iters):
         self._chk(self.lib.wlm_slab_group_iterate(self.h, int(iters)))
 

@@ -444,8 +444,10 @@ def test_cpp_adapter_runs_on_gpu(tmp_path):
 
 
 # ------------------------------------------------------- z-slab groups ----
-def run_slabs(P, ctx, F, M, cfg, iters, nslabs):
+def run_slabs(P, ctx, F, M, cfg, iters, nslabs, want_fused=None):
     grp = P.SlabGroup(F.shape, nslabs, cfg=cfg, ctx=ctx)
+    if want_fused is not None:
+        assert grp.fused_halos() == want_fused, (nslabs, grp.fused_halos(), want_fused)
     grp.load(F, M)
     grp.set_warp(None)
     grp.begin_level(0)
@@ -458,15 +460,22 @@ def run_slabs(P, ctx, F, M, cfg, iters, nslabs):
 @pytest.mark.parametrize("extra", [{}, {"lm.rejection": 1, "lm.tau": 0.2, "log_jacobian": 1},
                                    {"optimizer": 1}, {"sigma_update": 2.0, "sigma_warp": 1.6},
                                    {"low_memory": 1, "lm.rejection": 1, "lm.tau": 0.2}])
-def test_slab_group_is_bit_identical_to_single_domain(P, ctx, extra):
+@pytest.mark.parametrize("fused", ["1", "0"])
+def test_slab_group_is_bit_identical_to_single_domain(P, ctx, extra, fused, monkeypatch):
     """Config 5 decomposition: 1, 2, 3 and 5 z-slabs (uneven splits) give the
-    single-domain engine's losses, decisions, lambda and warp bit for bit."""
+    single-domain engine's losses, decisions, lambda and warp bit for bit,
+    with the producers' fused halo stores (default) and with the copy
+    exchange (WLM_SLAB_FUSED=0)."""
+    monkeypatch.setenv("WLM_SLAB_FUSED", fused)
     F, M, _ = O.synth_pair((20, 24, 28), 21, num_blobs=8, warp_max=2.5)
     cfg = P.reg_config(nlevels=1, factors=[1], iters=[12], **extra)
     w1, (t1,), (s1,) = run_engine(P, ctx, F, M, cfg, 12)
     # wide kernels (radius 6 / 5) need 6 halo planes: at most 3 slabs of 20
+    # fused kinds: g unless Adam (its step is produced by k_adam), dU_s, the
+    # warp and A/B/E; none with one slab or with WLM_SLAB_FUSED=0
+    mask = 0b1111 if extra.get("optimizer", 0) != 1 else 0b1110
     for ns in ((1, 2, 3) if "sigma_warp" in extra else (1, 2, 3, 5)):
-        w, t, s = run_slabs(P, ctx, F, M, cfg, 12, ns)
+        w, t, s = run_slabs(P, ctx, F, M, cfg, 12, ns, want_fused=mask if fused == "1" and ns > 1 else 0)
         assert same_trace(t, t1), ns
         assert np.array_equal(w, w1[0]), (ns, float(np.abs(w - w1[0]).max()))
         assert s["lam"] == s1["lam"] and s["r"] == s1["r"]

@@ -8,9 +8,12 @@ ranks share it and the NCCL library the transport dlopens is the test
 stand-in tests/nccl_shim/libnccl_shim.so (the same ABI over CUDA IPC with
 host-side synchronisation: no kernel of one rank waits on the other's).
 
-Bar: both ranks' traces and the owned planes of their warps are bit-identical
+Bar: every rank's trace and the owned planes of its warp are bit-identical
 to the single-domain engine's, with and without rejection (whose retry loop
-re-reads the device state on the host), with Adam, and with MI.
+re-reads the device state on the host), with Adam, and with MI; with the
+fused halo stores (K2, K3, K4 and K1b store the neighbour's halo planes
+into its buffer, mapped by CUDA IPC, and the exchange is a 4-byte ordering
+token) and with the copy exchange.
 """
 import multiprocessing as mp
 import os
@@ -45,12 +48,13 @@ def _rank(rank, uid, extra, iters, q, nranks=2):
         ctx = P.Context(0)
         cfg = P.reg_config(nlevels=1, factors=[1], iters=[iters], **extra)
         grp = slabs.RankSlab(SHAPE, rank, nranks, uid, cfg=cfg, ctx=ctx, nccl_lib=SHIM)
+        fused = grp.fused_halos()
         grp.load(F, M)
         grp.set_warp(None)
         grp.begin_level(0)
         grp.iterate(iters)
         zs, ze = grp.owned()
-        q.put((rank, zs, ze, grp.get_local_warp(), grp.trace(), grp.state()))
+        q.put((rank, zs, ze, grp.get_local_warp(), grp.trace(), grp.state(), fused))
         grp.close()
         ctx.close()
     except Exception as e:  # report, never hang the parent
@@ -113,7 +117,8 @@ def test_three_and_four_rank_slabs_bit_identical(ctx, nranks, extra):
     got = _run_ranks(nranks, extra, iters)
     z = 0
     for r in range(nranks):
-        _, zs, ze, w, t, s = got[r]
+        _, zs, ze, w, t, s, fm = got[r]
+        assert fm == (0b1111 if extra.get("optimizer", 0) != 1 else 0b1110), fm
         assert zs == z and ze > zs
         z = ze
         assert same_trace(t, t1), (r, extra)
@@ -123,15 +128,24 @@ def test_three_and_four_rank_slabs_bit_identical(ctx, nranks, extra):
 
 
 @pytest.mark.parametrize("extra", CASES)
-def test_two_rank_slabs_bit_identical_to_single_domain(ctx, extra):
+@pytest.mark.parametrize("fused", ["1", "0"])
+def test_two_rank_slabs_bit_identical_to_single_domain(ctx, extra, fused, monkeypatch):
+    """Two ranks, with the producers' fused halo stores into the
+    neighbour's buffer mapped by CUDA IPC (default) and with the NCCL
+    send/recv copy exchange (WLM_SLAB_FUSED=0); the spawned ranks inherit
+    the setting."""
+    monkeypatch.setenv("WLM_SLAB_FUSED", fused)
     import paper_2603_19371_b200 as P
     assert os.path.exists(SHIM), "build the shim: make (tests/nccl_shim/libnccl_shim.so)"
     iters = 20  # with rejection (tau 0.05) the oracle retries 20 times on this pair
     w1, t1, s1 = _single_domain(P, ctx, extra, iters)
     got = _run_ranks(2, extra, iters)
     owned = []
+    want = 0 if fused == "0" else (0b1110 if extra.get("optimizer", 0) == 1 else
+                                   0b0110 if extra.get("metric", 0) != 0 else 0b1111)
     for r in range(2):
-        _, zs, ze, w, t, s = got[r]
+        _, zs, ze, w, t, s, fm = got[r]
+        assert fm == want, (fm, want)
         owned.append((zs, ze))
         assert same_trace(t, t1), (r, extra)
         assert s["lam"] == s1["lam"] and s["r"] == s1["r"]
