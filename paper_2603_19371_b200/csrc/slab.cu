@@ -449,20 +449,38 @@ struct wlm_slab_group {
             Info theirs[2];
             CK(cudaMemcpyAsync(theirs, buf.p + sizeof(Info), 2 * sizeof(Info), cudaMemcpyDeviceToHost, st));
             CK(cudaStreamSynchronize(st));
-            for (int sd = 0; sd < 2; ++sd) {
+            int ok = 1;
+            for (int sd = 0; sd < 2 && ok; ++sd) {
                 const int k = first + (sd == 0 ? -1 : 1);
                 if (k < 0 || k >= nslabs) continue;
-                for (int q = 0; q < 4; ++q) {
+                for (int q = 0; q < 4 && ok; ++q) {
                     void* ptr = nullptr;
-                    CK(cudaIpcOpenMemHandle(&ptr, theirs[sd].h[q], cudaIpcMemLazyEnablePeerAccess));
+                    if (cudaIpcOpenMemHandle(&ptr, theirs[sd].h[q], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+                        cudaGetLastError();
+                        ok = 0;  // no peer mapping (GPUs without P2P): every rank keeps the copy exchange
+                        break;
+                    }
                     ipc_open.push_back(ptr);
                     nb_base[sd][q] = ptr;
                 }
                 nb_n[sd] = theirs[sd].n;
                 nb_zlo[sd] = theirs[sd].zlo;
             }
+            // the decision must be the same on every rank (tokens and copies
+            // do not match each other): min over the communicator
             token = DevBuf<int>(ctx, 3);
+            CK(cudaMemcpyAsync(token.p, &ok, sizeof(int), cudaMemcpyHostToDevice, st));
+            nccl_check(nccl::g_api.all_reduce(token.p, token.p, 1, nccl::Int32, nccl::Min, comm, st),
+                       "ncclAllReduce(min)");
+            CK(cudaMemcpyAsync(&ok, token.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+            CK(cudaStreamSynchronize(st));
             CK(cudaMemsetAsync(token.p, 0, sizeof(int) * 3, st));
+            if (!ok) {
+                for (void* q : ipc_open) cudaIpcCloseMemHandle(q);
+                ipc_open.clear();
+                for (bool& f : fused) f = false;
+                return;
+            }
         }
         for (size_t li = 0; li < eng.size(); ++li) {
             wlm_engine* e = eng[li];
