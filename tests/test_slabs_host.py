@@ -60,6 +60,37 @@ def test_halo_plans_match_pairwise(ns):
     check_plans(shape, ns, plans, cfg)
 
 
+@pytest.mark.parametrize("ns", [2, 3, 5, 8])
+@pytest.mark.parametrize("sig", [(1.0, 0.5), (0.5, 1.0), (2.0, 1.6)])
+def test_fused_store_ranges_are_one_face_run_per_neighbour(ns, sig):
+    """What the fused halo stores rely on (slab.cu setup_fused): per buffer
+    kind a slab sends at most one row to each neighbour, the lower one's
+    starting at its first owned plane and the upper one's ending at its
+    last, so a producer's store test is 'plane < lo_end' / 'plane >=
+    hi_begin'; and every send row's planes are exactly the receiver's halo
+    rows of that kind (no plane the receiver itself writes)."""
+    cfg = P.reg_config(nlevels=1, factors=[1], iters=[1], sigma_update=sig[0], sigma_warp=sig[1])
+    shape = (8 * ns + 16, 8, 8)
+    parts = slabs.partition(shape[0], ns)
+    plans = [slabs.halo_plan(shape, ns, k, cfg) for k in range(ns)]
+    for k, rows in enumerate(plans):
+        zs, ze = parts[k]
+        for buf in ("g", "dU_s", "warp", "abe"):
+            sends = [r for r in rows if r["buffer"] == buf and r["send"]]
+            lo = [r for r in sends if r["peer"] == k - 1]
+            hi = [r for r in sends if r["peer"] == k + 1]
+            assert len(lo) == (1 if k > 0 else 0) and len(hi) == (1 if k + 1 < ns else 0)
+            assert len(lo) + len(hi) == len(sends)
+            if lo:
+                assert lo[0]["z0"] == zs
+                pz0, pz1 = parts[k - 1]
+                assert not (pz0 <= lo[0]["z0"] < pz1)  # the receiver's halo, not its own planes
+            if hi:
+                assert hi[0]["z1"] == ze
+                pz0, pz1 = parts[k + 1]
+                assert not (pz0 <= hi[0]["z1"] - 1 < pz1)
+
+
 def test_halo_plan_follows_sigma():
     cfg = P.reg_config(nlevels=1, factors=[1], iters=[1], sigma_update=0.5, sigma_warp=1.0)
     shape = (40, 8, 8)
