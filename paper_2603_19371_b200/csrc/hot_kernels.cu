@@ -1579,7 +1579,8 @@ __global__ void __launch_bounds__(k4::NT, 1) k_compose_smooth(Batch b, LmParams 
                 row = NW + (w - (NW - EXTRA)); col = R + lane;
             } else if (w >= NW - EXTRA - EW) {
                 const int e = (w - (NW - EXTRA - EW)) * 32 + lane;
-                if (e < EDGE) { row = e / (2 * R); const int k = e % (2 * R); col = k < R ? k : TX + k; }
+                constexpr int R2 = 2 * R > 0 ? 2 * R : 1;  // (the branch runs for R == 2 only)
+                if (e < EDGE) { row = e / R2; const int k = e % R2; col = k < R ? k : TX + k; }
             }
             j = row >= 0 ? row * S::IW + col : -1;
         }
