@@ -10,7 +10,7 @@
 set -u
 mkdir -p gpurun_out
 nvidia-smi --query-gpu=name,clocks.max.sm,driver_version --format=csv > gpurun_out/r02_gpu.txt
-python bench.py --cpu-tables > gpurun_out/r02_bench.json 2> gpurun_out/r02_bench.err; echo "bench rc=$?"
+python bench.py --cpu-tables --table6 > gpurun_out/r02_bench.json 2> gpurun_out/r02_bench.err; echo "bench rc=$?"
 SHORT="python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-extra --e2e-iters 1"
 $SHORT > gpurun_out/r02_plain.log 2>&1 && \
   ncu --metrics gpu__time_duration.sum --clock-control none -s 100 -c 60 --csv \
