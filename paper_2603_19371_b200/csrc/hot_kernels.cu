@@ -776,6 +776,7 @@ __global__ void __launch_bounds__(k1::NT, 2) k_lncc_fwd(Batch b, int chunk_len) 
                                     Rm[ri] = Aa;
                                     Rm[rn + ri] = Bb;
                                     reinterpret_cast<double*>(Rm + 2 * rn)[ri] = Ee;
+                                    __threadfence_system();  // visible to the peer GPU before the token
                                 }
                         }
                     }
@@ -1062,6 +1063,7 @@ __global__ void __launch_bounds__(k2::NT, WLM_K2_MIN_BLOCKS) k_lncc_bwd(Batch b,
                                 Rm[0] = (float)(dm * gm[0]);
                                 Rm[rn] = (float)(dm * gm[1]);
                                 Rm[2 * rn] = (float)(dm * gm[2]);
+                                __threadfence_system();
                             }
                     }
                 }
@@ -1379,6 +1381,7 @@ __global__ void __launch_bounds__(k3::NT, k3::MINB) k_step_smooth(Batch b, LmPar
                                 Rm[0] = vv[0];
                                 Rm[rn] = vv[1];
                                 Rm[2 * rn] = vv[2];
+                                __threadfence_system();
                             }
                     }
                 }
@@ -1864,6 +1867,7 @@ __global__ void __launch_bounds__(k4::NT, 1) k_compose_smooth(Batch b, LmParams 
                                 Rm[0] = uu[0];
                                 Rm[rn] = uu[1];
                                 Rm[2 * rn] = uu[2];
+                                __threadfence_system();
                             }
                     }
                 }
