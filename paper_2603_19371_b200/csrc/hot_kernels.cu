@@ -285,7 +285,10 @@ __device__ __forceinline__ long long peer_index(const Batch& b, int sd, int z, i
 // evaluated warp becomes the accepted one exactly when K2 runs next (K2 is
 // skipped after a rejection), so K2 reads Mw and grad M instead of
 // re-gathering M at the same points.
-constexpr int kZP = 4;
+#ifndef WLM_K1A_ZP
+#define WLM_K1A_ZP 4
+#endif
+constexpr int kZP = WLM_K1A_ZP;
 template <bool GRAD>
 __global__ void __launch_bounds__(256) k_warp_moving(Batch b, int mode, int z_first, int z_last) {
     const int pair = b.pair0 + blockIdx.z;
