@@ -402,6 +402,7 @@ struct wlm_slab_group {
         fused[BUF_V] = P.Ru <= 6 && P.tile_k <= 1;
         fused[BUF_U] = P.Rw <= 6;
         fused[BUF_ABE] = lncc2;
+        if (!any_fused()) return;  // the same decision on every rank (same config)
         struct Info {
             cudaIpcMemHandle_t h[4];
             long long n;
