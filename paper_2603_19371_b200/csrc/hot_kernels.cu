@@ -38,6 +38,12 @@
 #include "hot.cuh"
 #include "kernels.cuh"
 
+// K4's Gaussian taps as constant-bank DFMA operands instead of registers
+// (WLM_CW_K4: K4 11.60 -> 11.43 ms; the same in K3 costs 7.45 -> 7.78, so K3
+// keeps its taps in registers)
+#ifndef WLM_CW_K4
+#define WLM_CW_K4 1
+#endif
 namespace wlm {
 
 using hot::NT;
@@ -1241,9 +1247,10 @@ __global__ void __launch_bounds__(k3::NT, k3::MINB) k_step_smooth(Batch b, LmPar
             dst[2 * NI + idx] = k * c;
         }
     };
-    double w[W];
+    double w_[W];
 #pragma unroll
-    for (int d = 0; d < W; ++d) w[d] = p.wud[d < R ? R - d : d - R];
+    for (int d = 0; d < W; ++d) w_[d] = p.wud[d < R ? R - d : d - R];
+#define w(d) w_[d]
 
     // x-pass item: row xr, pair xj (outputs x = 2xj, 2xj + 1); NT / 16 rows
     // per sweep, so radii with IH > 16 rows (R > 4) take a second sweep
@@ -1261,8 +1268,8 @@ __global__ void __launch_bounds__(k3::NT, k3::MINB) k_step_smooth(Batch b, LmPar
             double o0 = 0.0, o1 = 0.0;
 #pragma unroll
             for (int d = 0; d < W; ++d) {
-                o0 = fma(w[d], v[d], o0);
-                o1 = fma(w[d], v[d + 1], o1);
+                o0 = fma(w(d), v[d], o0);
+                o1 = fma(w(d), v[d + 1], o1);
             }
             *reinterpret_cast<double2*>(out + c * IH * TX + xr * TX + 2 * xj) = make_double2(o0, o1);
         }
@@ -1315,7 +1322,7 @@ __global__ void __launch_bounds__(k3::NT, k3::MINB) k_step_smooth(Batch b, LmPar
         for (int o = 0; o < YH; ++o) {
             double acc = 0.0;
 #pragma unroll
-            for (int d = 0; d < W; ++d) acc = fma(w[d], v[o + d], acc);
+            for (int d = 0; d < W; ++d) acc = fma(w(d), v[o + d], acc);
             out[yc * k3::TY * TX + (yh * YH + o) * TX + ox] = acc;
         }
     };
@@ -1355,7 +1362,7 @@ __global__ void __launch_bounds__(k3::NT, k3::MINB) k_step_smooth(Batch b, LmPar
                     for (int c = 0; c < 3; ++c) {
                         double s = 0.0;
 #pragma unroll
-                        for (int d = 0; d < W; ++d) s = fma(w[d], x_a[c * IH * TX + (oy + d) * TX + ox], s);
+                        for (int d = 0; d < W; ++d) s = fma(w(d), x_a[c * IH * TX + (oy + d) * TX + ox], s);
                         ring[rs][c] = s;
                     }
                 }
@@ -1369,7 +1376,7 @@ __global__ void __launch_bounds__(k3::NT, k3::MINB) k_step_smooth(Batch b, LmPar
                     for (int c = 0; c < 3; ++c) {
                         double s = 0.0;
 #pragma unroll
-                        for (int d = 0; d < W; ++d) s = fma(w[d], ring[(rs + 1 + d) % W][c], s);
+                        for (int d = 0; d < W; ++d) s = fma(w(d), ring[(rs + 1 + d) % W][c], s);
                         const float v = (float)(s * inv);
                         V[c * n + o] = v;
                         vv[c] = v;
@@ -1416,6 +1423,8 @@ __global__ void __launch_bounds__(k3::NT, k3::MINB) k_step_smooth(Batch b, LmPar
         atomic_max_nonneg(&st->max_bits, m);
     }
 }
+
+#undef w
 
 // K4: u'(x) = d(x) + u(x + d(x)), d = eps dU_s, eps = target / max(max|dU_s|,
 // floor) (Eq. 2, field.cpp:123-155), then Gaussian(sigma_warp); fp64
@@ -1754,9 +1763,14 @@ __global__ void __launch_bounds__(k4::NT, 1) k_compose_smooth(Batch b, LmParams 
     auto tma_wait = [&](int z) {
         if (TMA) mbar_wait(&s_bar[(z + 4) & 3], (uint32_t)(((z - zfirst) >> 2) & 1));
     };
-    double w[W];
+#if WLM_CW_K4
+#define wk(d) p.wwd[(d) < R ? R - (d) : (d) - R]
+#else
+    double wk_[W];
 #pragma unroll
-    for (int d = 0; d < W; ++d) w[d] = p.wwd[d < R ? R - d : d - R];
+    for (int d = 0; d < W; ++d) wk_[d] = p.wwd[d < R ? R - d : d - R];
+#define wk(d) wk_[d]
+#endif
     const int xr = threadIdx.x >> 4, xj = threadIdx.x & 15;
     auto x_pass = [&](const double* in, double* out) {
         if (xr >= IH) return;
@@ -1772,8 +1786,8 @@ __global__ void __launch_bounds__(k4::NT, 1) k_compose_smooth(Batch b, LmParams 
             double o0 = 0.0, o1 = 0.0;
 #pragma unroll
             for (int d = 0; d < W; ++d) {
-                o0 = fma(w[d], v[d], o0);
-                o1 = fma(w[d], v[d + 1], o1);
+                o0 = fma(wk(d), v[d], o0);
+                o1 = fma(wk(d), v[d + 1], o1);
             }
             *reinterpret_cast<double2*>(out + c * IH * TX + xr * TX + 2 * xj) = make_double2(o0, o1);
         }
@@ -1844,7 +1858,7 @@ __global__ void __launch_bounds__(k4::NT, 1) k_compose_smooth(Batch b, LmParams 
                 for (int c = 0; c < 3; ++c) {
                     double s = 0.0;
 #pragma unroll
-                    for (int d = 0; d < W; ++d) s = fma(w[d], x_a[c * IH * TX + (oy + d) * TX + ox], s);
+                    for (int d = 0; d < W; ++d) s = fma(wk(d), x_a[c * IH * TX + (oy + d) * TX + ox], s);
                     ring[rs][c] = s;
                 }
                 const int zo = zi - R;
@@ -1857,7 +1871,7 @@ __global__ void __launch_bounds__(k4::NT, 1) k_compose_smooth(Batch b, LmParams 
                     for (int c = 0; c < 3; ++c) {
                         double s = 0.0;
 #pragma unroll
-                        for (int d = 0; d < W; ++d) s = fma(w[d], ring[(rs + 1 + d) % W][c], s);
+                        for (int d = 0; d < W; ++d) s = fma(wk(d), ring[(rs + 1 + d) % W][c], s);
                         uu[c] = (float)(s * inv);
                         UN_[c * n + o] = uu[c];
                     }
@@ -1893,6 +1907,7 @@ __global__ void __launch_bounds__(k4::NT, 1) k_compose_smooth(Batch b, LmParams 
 }
 
 // ---------------------------------------------------------------------------
+#undef wk
 #define WLM_DISPATCH_R(R_, CALL)                       \
     switch (R_) {                                      \
         case 0: { constexpr int RR = 0; CALL; } break; \
