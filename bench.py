@@ -411,6 +411,7 @@ def run_slabs(args, rank, world, local):
         grp = slabs.RankSlab(shape, rank, world, uid, cfg=cfg, ctx=ctx)
     else:
         grp = P.SlabGroup(shape, 1, cfg=cfg, ctx=ctx)
+    grp_fused = grp.fused_halos()
     grp.load(F_d, M_d)
     F_h = F_d.cpu().pin_memory() if args.e2e_iters > 0 else None
     M_h = M_d.cpu().pin_memory() if args.e2e_iters > 0 else None
@@ -469,7 +470,10 @@ def run_slabs(args, rank, world, local):
         "config": {"workload": f"config 5: one {n}^3 pair, z-slab sharded over {world} GPU(s), LNCC r=2 + "
                                f"pointwise LM, rejection off",
                    "volume": list(shape), "parallelism": f"z-slab x{world} (halo exchange + NCCL all-reduce)"
-                   if world > 1 else "single slab", "l2": "inputs > L2"},
+                   if world > 1 else "single slab", "l2": "inputs > L2",
+                   # exchanges fused into the producing kernels (bit 0 g, 1 dU_s, 2 warp, 3 A/B/E:
+                   # peer-memory stores + an ordering token; include/wlm.h)
+                   "fused_halos": f"{grp_fused:04b}"},
         "iters_per_s": round(args.steps / (ms_max * 1e-3), 3),
         "roofline": {"bound": "hbm", "kernel": "iteration (K1..K4 + exchanges)",
                      "achieved": round(value * BYTES_PER_VOXEL_ITER / max(world, 1), 1), "peak": hbm,

@@ -155,23 +155,26 @@ def test_two_rank_slabs_bit_identical_to_single_domain(ctx, extra, fused, monkey
         assert sum(row["retries"] for row in t1) > 0, "the case should exercise the retry loop"
 
 
-def test_bench_config5_two_ranks_under_torchrun():
-    """bench.py --config 5 under the driver's torchrun launch with two ranks
-    (one GPU: gloo for torch.distributed, the NCCL stand-in for the slab
-    transport via WLM_NCCL_LIB): one JSON line from rank 0, strong scaling,
-    the slab group's multi-rank path (unique-id broadcast, RankSlab, owned
-    planes, e2e with host buffers) end to end."""
+@pytest.mark.parametrize("nproc,size", [(2, 96), (4, 128)])
+def test_bench_config5_ranks_under_torchrun(nproc, size):
+    """bench.py --config 5 under the driver's torchrun launch with two and
+    four ranks (one GPU: gloo for torch.distributed, the NCCL stand-in for
+    the slab transport via WLM_NCCL_LIB; four ranks have middle slabs with
+    two neighbours): one JSON line from rank 0, strong scaling, the slab
+    group's multi-rank path (unique-id broadcast, RankSlab, owned planes,
+    fused halo stores, e2e with host buffers) end to end."""
     import json
     import subprocess
     env = dict(os.environ, WLM_BENCH_BACKEND="gloo", WLM_NCCL_LIB=SHIM)
-    out = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
-                          "--master-addr", "127.0.0.1", "--master-port", "29541",
-                          os.path.join(ROOT, "bench.py"), "--config", "5", "--size", "96", "--gpus", "2",
+    out = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", str(nproc),
+                          "--master-addr", "127.0.0.1", "--master-port", str(29541 + nproc),
+                          os.path.join(ROOT, "bench.py"), "--config", "5", "--size", str(size), "--gpus", str(nproc),
                           "--steps", "3", "--warmup", "3", "--e2e-iters", "2"],
                          capture_output=True, text=True, timeout=900, env=env)
     assert out.returncode == 0, out.stderr[-3000:]
     lines = [ln for ln in out.stdout.strip().splitlines() if ln.startswith("{")]
     assert len(lines) == 1
     line = json.loads(lines[0])
-    assert line["n_gpus"] == 2 and line["scaling"] == "strong" and line["value"] > 0
-    assert "z-slab x2" in line["config"]["parallelism"] and line["e2e"]["value"] > 0
+    assert line["n_gpus"] == nproc and line["scaling"] == "strong" and line["value"] > 0
+    assert f"z-slab x{nproc}" in line["config"]["parallelism"] and line["e2e"]["value"] > 0
+    assert line["config"]["fused_halos"] == "1111"  # every exchange fused into its producer
