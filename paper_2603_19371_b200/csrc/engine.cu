@@ -137,7 +137,9 @@ void engine_alloc(wlm_engine* e) {
     e->shift_part = DevBuf<double>(ctx, B * 2 * 256 * 3);  // sums + (min, max)
     init_constants();
     e->G = DevBuf<float>(ctx, B * 3 * n);
-    e->VS = DevBuf<float>(ctx, B * 3 * n);
+    // dU_s (K3 -> K4, the Jacobian) shares ABE's memory: A, B, E are written by
+    // K1b and last read by K2, so they are dead exactly while dU_s lives
+    // (12 B/voxel less)
     if (e->P.optimizer == WLM_OPT_ADAM) {
         e->AM = DevBuf<float>(ctx, B * 3 * n);
         e->AV = DevBuf<float>(ctx, B * 3 * n);
@@ -192,7 +194,9 @@ void engine_alloc(wlm_engine* e) {
     b.g = e->g;
     b.pairs = e->pairs;
     if (!e->shared_fm) { b.F = e->F.p; b.M = e->M.p; }
-    b.U = e->U.p; b.ABE = e->ABE.p; b.G = e->G.p; b.VS = e->VS.p;
+    b.U = e->U.p; b.ABE = e->ABE.p; b.G = e->G.p;
+    b.VS = e->ABE.p;
+    b.vs_ps = 4 * (long long)n;
     b.AM = e->AM.p; b.AV = e->AV.p;
     b.MW = e->MW.p;
     b.GM = e->GM.p;
@@ -499,7 +503,7 @@ wlm_status wlm_engine_buffers(wlm_engine* e, const float** F, const float** M, f
         if (F) *F = e->F.p;
         if (M) *M = e->M.p;
         if (g) *g = e->G.p;
-        if (vs) *vs = e->VS.p;
+        if (vs) *vs = e->B.VS;  // pair stride 4 n (inside ABE)
         if (abe) *abe = e->ABE.p;
         if (u_cur) {
             const std::vector<PairState> v = read_states(e);
@@ -525,7 +529,7 @@ wlm_status wlm_engine_read_buffer(wlm_engine* e, int which, int pair, float* hos
                 break;
             }
             case 3: src = e->G.p + pair * 3 * n; break;
-            case 4: src = e->VS.p + pair * 3 * n; break;
+            case 4: src = e->B.VS + (size_t)pair * e->B.vs_ps; break;
             default: src = e->ABE.p + pair * 4 * n; break;
         }
         CK(cudaMemcpyAsync(host, src, sizeof(float) * count, cudaMemcpyDeviceToHost, ctx->stream));

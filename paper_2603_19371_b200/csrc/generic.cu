@@ -229,7 +229,7 @@ __global__ void k_gen_store_vs(Batch b, int c0) {
     PairState* st = b.st + pair;
     if (st->done) return;
     const long long n = b.g.n;
-    float* V = b.VS + (long long)pair * 3 * n;
+    float* V = b.VS + (long long)pair * b.vs_ps;
     float mx = 0.f;
     GEN_LOOP(j, 3 * n) {
         const float v = (float)scratch(b, pair, c0 + (int)(j / n))[j % n];
@@ -259,7 +259,7 @@ __global__ void k_gen_compose(Batch b, LmParams p) {
     if (st->done) return;
     const Geo g = b.g;
     const long long n = g.n;
-    const float* V = b.VS + (long long)pair * 3 * n;
+    const float* V = b.VS + (long long)pair * b.vs_ps;
     const float* U = b.U + ((long long)pair * 2 + st->cur) * 3 * n;
     const double eps = p.target / fmax((double)__uint_as_float(st->max_bits), p.step_floor);
     GEN_LOOP(i, n) {

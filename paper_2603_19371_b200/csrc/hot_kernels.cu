@@ -1188,7 +1188,7 @@ __global__ void __launch_bounds__(k3::NT, k3::MINB) k_step_smooth(Batch b, LmPar
     fill_border_inv(s_binv, g.nz, R, p.wud, p.wud_full);
     const int zb = g.zs + blockIdx.y * chunk_len, ze = min(zb + chunk_len, g.ze);
     const float* __restrict__ Gin = b.G + (long long)pair * 3 * n;
-    float* __restrict__ V = b.VS + (long long)pair * 3 * n;
+    float* __restrict__ V = b.VS + (long long)pair * b.vs_ps;
     const int opt = p.optimizer;
     const double r = st->r_cur, lam = st->lambda;
     const double kc = opt == WLM_OPT_GD ? -p.gd_lr : 1.0;
@@ -1552,7 +1552,7 @@ __global__ void __launch_bounds__(k4::NT, 1) k_compose_smooth(Batch b, LmParams 
     const int x0 = (blockIdx.x % tiles_x) * TX, y0 = (blockIdx.x / tiles_x) * k4::TY;
     const int zb = g.zs + blockIdx.y * chunk_len, ze = min(zb + chunk_len, g.ze);
     const int cur = st->cur;
-    const float* __restrict__ Vin = b.VS + (long long)pair * 3 * n;
+    const float* __restrict__ Vin = b.VS + (long long)pair * b.vs_ps;
     const float* __restrict__ U = b.U + ((long long)pair * 2 + cur) * 3 * n;
     float* __restrict__ UN_ = b.U + ((long long)pair * 2 + (1 - cur)) * 3 * n;
     const double eps = p.target / fmax((double)__uint_as_float(st->max_bits), p.step_floor);

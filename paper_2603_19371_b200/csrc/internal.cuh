@@ -148,7 +148,7 @@ struct wlm_engine {
     int pairs = 0;
     wlm_reg_config cfg{};
     LmParams P{};
-    DevBuf<float> F, M, U, ABE, G, VS, AM, AV;
+    DevBuf<float> F, M, U, ABE, G, AM, AV;  // dU_s lives inside ABE (Batch::VS)
     DevBuf<double> MW, GM;
     DevBuf<PairState> st;
     DevBuf<double> partials, script, shift_part, plane_sum, TM, MIT, ABC, X64, TAPU, TAPW;

@@ -136,7 +136,7 @@ __global__ void k_jacobian_diag(Batch b, LmParams p) {
     PairState* st = b.st + pair;
     if (st->done) return;
     const Geo g = b.g;
-    const float* V = b.VS + (long long)pair * 3 * g.n;
+    const float* V = b.VS + (long long)pair * b.vs_ps;
     const double eps = p.target / fmax((double)__uint_as_float(st->max_bits), p.step_floor);
     int xl, xh, yl, yh, zl, zh;
     interior(g.nx, xl, xh); interior(g.ny, yl, yh); interior(g.nz, zl, zh);

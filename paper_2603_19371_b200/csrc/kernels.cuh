@@ -100,7 +100,9 @@ struct Batch {
     double* MW;       // [pair][n]     warped moving image M(x + u) (fp64, K1a -> K1b, K2)
     double* GM;       // [pair][3][n]  grad M(x + u) of the evaluated warp (LNCC: K1a -> K2), or null
     float* G;         // [pair][3][n]  gradient g, Adam step in place
-    float* VS;        // [pair][3][n]  smoothed step dU_s
+    float* VS;        // [pair][3][n]  smoothed step dU_s, pair stride vs_ps: it lives in the
+                      // ABE buffer (A, B, E are dead from K2 to the next K1b, while dU_s lives)
+    long long vs_ps;  // VS pair stride in floats (4 n)
     float* AM;        // [pair][3][n]  Adam first moment (or null)
     float* AV;        // [pair][3][n]  Adam second moment (or null)
     PairState* st;    // [pair]

@@ -285,7 +285,7 @@ struct wlm_slab_group {
         const long long n = e->g.n;
         switch (b) {
             case BUF_G: return {{(char*)e->G.p, 4, n, 3}};
-            case BUF_V: return {{(char*)e->VS.p, 4, n, 3}};
+            case BUF_V: return {{(char*)e->B.VS, 4, n, 3}};  // inside ABE (one pair)
             case BUF_U: return {{(char*)e->U.p, 4, n, 6}};  // both ping-pong buffers (nccl)
             default: return {{(char*)e->ABE.p, 4, n, 2}, {(char*)(e->ABE.p + 2 * n), 8, n, 1}};
         }
@@ -409,8 +409,9 @@ struct wlm_slab_group {
             int zlo, pad;
         };
         // this process's (or engine's) buffers as a neighbour sees them
+        // (dU_s lives inside ABE: one allocation, one mapping for both)
         auto bases = [](wlm_engine* e, void* out[4]) {
-            out[0] = e->G.p; out[1] = e->VS.p; out[2] = e->U.p; out[3] = e->ABE.p;
+            out[0] = e->G.p; out[1] = e->B.VS; out[2] = e->U.p; out[3] = e->ABE.p;
         };
         std::vector<std::array<void*, 4>> nb_base(2 * eng.size(), {nullptr, nullptr, nullptr, nullptr});
         std::vector<long long> nb_n(2 * eng.size(), 0);
@@ -432,7 +433,8 @@ struct wlm_slab_group {
             Info mine{};
             void* b4[4];
             bases(e, b4);
-            for (int q = 0; q < 4; ++q) CK(cudaIpcGetMemHandle(&mine.h[q], b4[q]));
+            for (int q = 0; q < 4; ++q)
+                if (q != 1) CK(cudaIpcGetMemHandle(&mine.h[q], b4[q]));
             mine.n = e->g.n;
             mine.zlo = e->g.zlo;
             DevBuf<unsigned char> buf(ctx, 3 * sizeof(Info));
@@ -455,6 +457,7 @@ struct wlm_slab_group {
                 const int k = first + (sd == 0 ? -1 : 1);
                 if (k < 0 || k >= nslabs) continue;
                 for (int q = 0; q < 4 && ok; ++q) {
+                    if (q == 1) continue;  // dU_s: the ABE mapping (set below)
                     void* ptr = nullptr;
                     if (cudaIpcOpenMemHandle(&ptr, theirs[sd].h[q], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
                         cudaGetLastError();
@@ -464,6 +467,7 @@ struct wlm_slab_group {
                     ipc_open.push_back(ptr);
                     nb_base[sd][q] = ptr;
                 }
+                nb_base[sd][1] = nb_base[sd][3];
                 nb_n[sd] = theirs[sd].n;
                 nb_zlo[sd] = theirs[sd].zlo;
             }
