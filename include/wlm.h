@@ -119,8 +119,8 @@ typedef struct {
     int mi_bins;         /* MetricConfig.mi_bins B, 2..64 (default 32) */
     double mi_sigma;     /* MetricConfig.mi_parzen_sigma in bin widths, (0, 2] (default 1) */
     /* Device layout (not a reference parameter): 0 = speed (K1a hands the
-     * fp64 grad M(x+u) to K2, 104 B/voxel for LNCC); 1 = memory (K2
-     * re-gathers M at x+u itself, 80 B/voxel).  Results are identical. */
+     * fp64 grad M(x+u) to K2, 92 B/voxel for LNCC); 1 = memory (K2
+     * re-gathers M at x+u itself, 68 B/voxel).  Results are identical. */
     int low_memory;
 } wlm_reg_config;
 
